@@ -1,0 +1,563 @@
+// qfso.cpp — CPU ORACLE for QFactor-Sample instantiation (arXiv 2405.12866).
+//
+// TEST INFRASTRUCTURE ONLY (see qfso.h).  Plain, slow, obviously correct:
+// dense loops in double, long double accumulation, its own Jacobi SVD, no BLAS,
+// no SIMD, no blocking or fusion beyond what the paper's algorithm states.
+// OpenMP (if enabled) only runs independent multistarts side by side.
+//
+// Citations: P:<line> = /root/reference/PAPER.md line; DESIGN.md §2 lists the
+// readings taken where the paper is silent (numbered R1..R21 there and below).
+#include "qfso.h"
+
+#include <chrono>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <limits>
+#include <vector>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+namespace {
+
+typedef std::complex<double> cd;
+typedef std::complex<long double> cld;
+
+// ---------------------------------------------------------------- indexing --
+// R1: little-endian amplitudes; the quadruple r of a gate on (p0, p1) is the
+// r-th assignment of the other n-2 qubits, obtained by inserting zero bits at
+// the two gate positions (ascending); member l sits at base | b0<<p0 | b1<<p1
+// with l = b0 + 2 b1.
+inline long insert_zero_bit(long v, int pos) {
+  long low = v & ((1L << pos) - 1);
+  long high = v >> pos;
+  return (high << (pos + 1)) | low;
+}
+inline long quad_base(long r, int p0, int p1) {
+  int lo = p0 < p1 ? p0 : p1, hi = p0 < p1 ? p1 : p0;
+  return insert_zero_bit(insert_zero_bit(r, lo), hi);
+}
+inline long quad_index(long base, int l, int p0, int p1) {
+  return base | (long)(l & 1) << p0 | (long)((l >> 1) & 1) << p1;
+}
+
+inline cd ld(const double *p, long i) { return cd(p[2 * i], p[2 * i + 1]); }
+inline void st(double *p, long i, cd v) { p[2 * i] = v.real(); p[2 * i + 1] = v.imag(); }
+
+bool valid_pair(int n, int p0, int p1) {
+  return n >= 2 && p0 >= 0 && p1 >= 0 && p0 < n && p1 < n && p0 != p1;
+}
+
+// ------------------------------------------------------------- gate apply --
+// P:59 ("QFactor utilizes tensor network contractions"), P:127 (B tensors):
+// psi[idx(l_out)] <- sum_l G[l_out][l] psi[idx(l)] for every quadruple.
+void apply_gate(int n, int p0, int p1, const cd G[16], int m, double *psi) {
+  const long N = 1L << n;
+  for (int s = 0; s < m; ++s) {
+    double *row = psi + 2 * (long)s * N;
+    for (long r = 0; r < N / 4; ++r) {
+      long base = quad_base(r, p0, p1);
+      cd v[4];
+      for (int l = 0; l < 4; ++l) v[l] = ld(row, quad_index(base, l, p0, p1));
+      for (int lo = 0; lo < 4; ++lo) {
+        cd acc = 0;
+        for (int l = 0; l < 4; ++l) acc += G[4 * lo + l] * v[l];
+        st(row, quad_index(base, lo, p0, p1), acc);
+      }
+    }
+  }
+}
+
+void load_gate(const double *g, cd G[16]) {
+  for (int i = 0; i < 16; ++i) G[i] = cd(g[2 * i], g[2 * i + 1]);
+}
+void adjoint(const cd A[16], cd Ad[16]) {
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) Ad[4 * i + j] = std::conj(A[4 * j + i]);
+}
+
+// ------------------------------------------------------------ environment --
+// P:121-125 ("for any specific gate u_i ... can be written as Re(Tr(E u_i))"),
+// P:172 (Fig. env_calc: trace all legs except the gate's): R4 orientation
+// E[l_in][l_out] = sum_m sum_r phi_m[idx_r(l_in)] conj(chi_m[idx_r(l_out)]),
+// so that Tr(E G) = sum_m <chi_m | G phi_m>.  Accumulated in long double in the
+// order m ascending, then r ascending.
+void environment(int n, int p0, int p1, int m0, int m1, int mstride, const double *phi,
+                 const double *chi, cld E[16]) {
+  const long N = 1L << n;
+  for (int m = m0; m < m1; m += mstride) {
+    const double *f = phi + 2 * (long)m * N;
+    const double *c = chi + 2 * (long)m * N;
+    for (long r = 0; r < N / 4; ++r) {
+      long base = quad_base(r, p0, p1);
+      cd fv[4], cv[4];
+      for (int l = 0; l < 4; ++l) {
+        fv[l] = ld(f, quad_index(base, l, p0, p1));
+        cv[l] = ld(c, quad_index(base, l, p0, p1));
+      }
+      for (int a = 0; a < 4; ++a)
+        for (int b = 0; b < 4; ++b) {
+          cd t = fv[a] * std::conj(cv[b]);
+          E[4 * a + b] += cld(t.real(), t.imag());
+        }
+    }
+  }
+}
+
+// ------------------------------------------------------------------- SVD --
+// E = X D Y^dag, u_new = Y X^dag.  The paper does not name its SVD
+// routine (R5); the oracle uses Hestenes one-sided Jacobi: complex rotations on
+// column pairs (j, k) from the right, chosen so the new a_j^dag a_k = 0, and
+// accumulated into V.  Converged when every pair has
+// |a_j^dag a_k| <= 1e-15 ||a_j|| ||a_k|| (cap 30 sweeps).  Then
+// sigma_j = ||a_j||, X_j = a_j / sigma_j, Y = V.  Columns with
+// sigma_j <= 1e-14 sigma_max are numerically null: X_j is completed by
+// Gram-Schmidt on e_0..e_3 against the other columns (R5).
+int svd4(const cd A_in[16], cd X[16], double sigma[4], cd Y[16]) {
+  cd A[16], V[16];
+  for (int i = 0; i < 16; ++i) { A[i] = A_in[i]; V[i] = (i % 5 == 0) ? cd(1, 0) : cd(0, 0); }
+  int sweep = 0;
+  for (; sweep < 30; ++sweep) {
+    bool rotated = false;
+    for (int j = 0; j < 3; ++j)
+      for (int k = j + 1; k < 4; ++k) {
+        double alpha = 0, beta = 0;
+        cd gamma = 0;
+        for (int r = 0; r < 4; ++r) {
+          alpha += std::norm(A[4 * r + j]);
+          beta += std::norm(A[4 * r + k]);
+          gamma += std::conj(A[4 * r + j]) * A[4 * r + k];
+        }
+        double ag = std::abs(gamma);
+        if (ag == 0.0 || ag <= 1e-15 * std::sqrt(alpha) * std::sqrt(beta)) continue;
+        rotated = true;
+        cd ph = gamma / ag;                       // e^{i phi}
+        double zeta = (beta - alpha) / (2.0 * ag);
+        double t = (zeta >= 0 ? 1.0 : -1.0) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
+        double c = 1.0 / std::sqrt(1.0 + t * t);
+        double s = c * t;
+        // [a_j' a_k'] = [a_j a_k] J,  J = [[c, s e^{i phi}], [-s e^{-i phi}, c]]
+        for (int r = 0; r < 4; ++r) {
+          cd aj = A[4 * r + j], ak = A[4 * r + k];
+          A[4 * r + j] = c * aj - s * std::conj(ph) * ak;
+          A[4 * r + k] = s * ph * aj + c * ak;
+          cd vj = V[4 * r + j], vk = V[4 * r + k];
+          V[4 * r + j] = c * vj - s * std::conj(ph) * vk;
+          V[4 * r + k] = s * ph * vj + c * vk;
+        }
+      }
+    if (!rotated) break;
+  }
+  double smax = 0;
+  for (int j = 0; j < 4; ++j) {
+    double nn = 0;
+    for (int r = 0; r < 4; ++r) nn += std::norm(A[4 * r + j]);
+    sigma[j] = std::sqrt(nn);
+    if (sigma[j] > smax) smax = sigma[j];
+  }
+  bool null_col[4];
+  for (int j = 0; j < 4; ++j) {
+    null_col[j] = !(sigma[j] > 1e-14 * smax) || smax == 0.0;
+    for (int r = 0; r < 4; ++r) X[4 * r + j] = null_col[j] ? cd(0, 0) : A[4 * r + j] / sigma[j];
+  }
+  // complete null columns: Gram-Schmidt of e_0..e_3 against the filled columns
+  for (int j = 0; j < 4; ++j) {
+    if (!null_col[j]) continue;
+    for (int e = 0; e < 4; ++e) {
+      cd v[4];
+      for (int r = 0; r < 4; ++r) v[r] = (r == e) ? cd(1, 0) : cd(0, 0);
+      for (int pass = 0; pass < 2; ++pass)
+        for (int q = 0; q < 4; ++q) {
+          if (q == j || (null_col[q] && q > j)) continue;
+          cd d = 0;
+          for (int r = 0; r < 4; ++r) d += std::conj(X[4 * r + q]) * v[r];
+          for (int r = 0; r < 4; ++r) v[r] -= d * X[4 * r + q];
+        }
+      double nv = 0;
+      for (int r = 0; r < 4; ++r) nv += std::norm(v[r]);
+      nv = std::sqrt(nv);
+      if (nv > 0.5) {
+        for (int r = 0; r < 4; ++r) X[4 * r + j] = v[r] / nv;
+        break;
+      }
+    }
+  }
+  for (int i = 0; i < 16; ++i) Y[i] = V[i];
+  return sweep;
+}
+
+// P:59-62 with the beta term of P:380-386 (R15: u = the current, old gate):
+// E' = (1 - beta) E + beta u^dag;  E' = X D Y^dag;  u_new = Y X^dag.
+void polar_update(const cd E[16], const cd Gold[16], double beta, cd Gnew[16], double *sig_sum) {
+  cd Ep[16], Gd[16], X[16], Y[16];
+  double sg[4];
+  adjoint(Gold, Gd);
+  for (int i = 0; i < 16; ++i) Ep[i] = (1.0 - beta) * E[i] + beta * Gd[i];
+  svd4(Ep, X, sg, Y);
+  for (int a = 0; a < 4; ++a)
+    for (int b = 0; b < 4; ++b) {
+      cd acc = 0;
+      for (int j = 0; j < 4; ++j) acc += Y[4 * a + j] * std::conj(X[4 * b + j]);
+      Gnew[4 * a + b] = acc;
+    }
+  if (sig_sum) *sig_sum = sg[0] + sg[1] + sg[2] + sg[3];
+}
+
+// ------------------------------------------------------------------ cost --
+// P:116-120 (eq:qfactor_sample_cost_function), direct form (R6):
+// (1/M) sum_j ||a_j - b_j||^2, accumulated in long double.
+long double sq_distance_sum(int n, int m0, int m1, int mstride, const double *a,
+                            const double *b) {
+  const long N = 1L << n;
+  long double acc = 0;
+  for (int m = m0; m < m1; m += mstride)
+    for (long i = 0; i < N; ++i) {
+      long double dr = (long double)a[2 * ((long)m * N + i)] - b[2 * ((long)m * N + i)];
+      long double di = (long double)a[2 * ((long)m * N + i) + 1] - b[2 * ((long)m * N + i) + 1];
+      acc += dr * dr + di * di;
+    }
+  return acc;
+}
+
+// ----------------------------------------------------------------- sweep --
+// One sweep for one start ("sweeps the circuit from right to left";
+// P:127/P:165 A and B tensors; P:172 Fig. env_calc; R2, R3):
+//  (a) B_0 = x, B_{i} = G_{i-1} B_{i-1} (previous sweep's gates, gate 0 first)
+//  (b) chi = y  (the A tensor, conjugated)
+//  (c) for i = K-1 .. 0: E_i = env(B_i, chi); G_i <- polar(E_i); chi <- G_i^dag chi
+//  (d) c_train = (1/M) sum ||chi - x||^2   (chi = C_new^dag y)
+// g > 1: sample-shard emulation — E_i and the cost sum are formed per shard
+// r (rows m = r mod g) and summed in rank order.
+struct SweepOut {
+  std::vector<cd> env;     // [K][16] (as seen, before the update)
+  std::vector<double> sig; // [K]
+  double c_train;
+};
+
+void sweep_one(int n, int K, const int32_t *pairs, cd *G /*[K][16] in/out*/, int M,
+               const double *x, const double *y, double beta, int g, SweepOut *out,
+               std::vector<double> &Bbuf, std::vector<double> &chi) {
+  const long N = 1L << n;
+  const long rowlen = 2 * (long)M * N;
+  Bbuf.resize((size_t)K * rowlen);
+  chi.resize(rowlen);
+  std::memcpy(Bbuf.data(), x, sizeof(double) * rowlen);
+  for (int i = 1; i < K; ++i) {
+    double *Bi = Bbuf.data() + (size_t)i * rowlen;
+    std::memcpy(Bi, Bbuf.data() + (size_t)(i - 1) * rowlen, sizeof(double) * rowlen);
+    apply_gate(n, pairs[2 * (i - 1)], pairs[2 * (i - 1) + 1], G + 16 * (i - 1), M, Bi);
+  }
+  std::memcpy(chi.data(), y, sizeof(double) * rowlen);
+  if (out) { out->env.assign((size_t)K * 16, cd(0, 0)); out->sig.assign(K, 0.0); }
+  for (int i = K - 1; i >= 0; --i) {
+    int p0 = pairs[2 * i], p1 = pairs[2 * i + 1];
+    cld Etot[16];
+    for (int q = 0; q < 16; ++q) Etot[q] = 0;
+    for (int r = 0; r < g; ++r) {
+      cld Er[16];
+      for (int q = 0; q < 16; ++q) Er[q] = 0;
+      environment(n, p0, p1, r, M, g, Bbuf.data() + (size_t)i * rowlen, chi.data(), Er);
+      for (int q = 0; q < 16; ++q) Etot[q] += cd((double)Er[q].real(), (double)Er[q].imag());
+    }
+    cd E[16];
+    for (int q = 0; q < 16; ++q) E[q] = cd((double)Etot[q].real(), (double)Etot[q].imag());
+    cd Gn[16], Gd[16];
+    double ss = 0;
+    polar_update(E, G + 16 * i, beta, Gn, &ss);
+    for (int q = 0; q < 16; ++q) G[16 * i + q] = Gn[q];
+    if (out) {
+      for (int q = 0; q < 16; ++q) out->env[16 * i + q] = E[q];
+      out->sig[i] = ss;
+    }
+    adjoint(Gn, Gd);
+    apply_gate(n, p0, p1, Gd, M, chi.data());
+  }
+  long double tot = 0;
+  for (int r = 0; r < g; ++r) tot += (double)sq_distance_sum(n, r, M, g, chi.data(), x);
+  if (out) out->c_train = (double)(tot / (long double)M);
+}
+
+double validation_cost(int n, int K, const int32_t *pairs, const cd *G, int V, const double *xv,
+                       const double *yv) {
+  const long N = 1L << n;
+  std::vector<double> psi(xv, xv + 2 * (long)V * N);
+  for (int i = 0; i < K; ++i) apply_gate(n, pairs[2 * i], pairs[2 * i + 1], G + 16 * i, V, psi.data());
+  return (double)(sq_distance_sum(n, 0, V, 1, psi.data(), yv) / (long double)V);
+}
+
+int check_structure(int n, int k, const int32_t *pairs) {
+  if (n < 2 || n > 30 || k < 1 || !pairs) return 1;
+  for (int i = 0; i < k; ++i)
+    if (!valid_pair(n, pairs[2 * i], pairs[2 * i + 1])) return 1;
+  return 0;
+}
+
+}  // namespace
+
+// ===================================================================== ABI ==
+extern "C" {
+
+int qfso_apply_gate(int n, int p0, int p1, const double *g, int dagger, int m, double *psi) {
+  if (!valid_pair(n, p0, p1) || !g || !psi || m < 0) return 1;
+  cd G[16], Gd[16];
+  load_gate(g, G);
+  if (dagger) { adjoint(G, Gd); apply_gate(n, p0, p1, Gd, m, psi); }
+  else apply_gate(n, p0, p1, G, m, psi);
+  return 0;
+}
+
+int qfso_circuit_forward(int n, int k, const int32_t *pairs, const double *gates, int m,
+                         double *psi) {
+  if (check_structure(n, k, pairs) || !gates || !psi) return 1;
+  for (int i = 0; i < k; ++i) {
+    cd G[16];
+    load_gate(gates + 32 * i, G);
+    apply_gate(n, pairs[2 * i], pairs[2 * i + 1], G, m, psi);
+  }
+  return 0;
+}
+
+int qfso_environment(int n, int p0, int p1, int m, const double *phi, const double *chi,
+                     double *env) {
+  if (!valid_pair(n, p0, p1) || !phi || !chi || !env || m < 0) return 1;
+  cld E[16];
+  for (int q = 0; q < 16; ++q) E[q] = 0;
+  environment(n, p0, p1, 0, m, 1, phi, chi, E);
+  for (int q = 0; q < 16; ++q) { env[2 * q] = (double)E[q].real(); env[2 * q + 1] = (double)E[q].imag(); }
+  return 0;
+}
+
+int qfso_svd4(const double *a, double *x, double *sigma, double *y, int *sweeps) {
+  if (!a || !x || !sigma || !y) return 1;
+  cd A[16], X[16], Y[16];
+  load_gate(a, A);
+  int sw = svd4(A, X, sigma, Y);
+  for (int i = 0; i < 16; ++i) {
+    x[2 * i] = X[i].real(); x[2 * i + 1] = X[i].imag();
+    y[2 * i] = Y[i].real(); y[2 * i + 1] = Y[i].imag();
+  }
+  if (sweeps) *sweeps = sw;
+  return 0;
+}
+
+int qfso_polar_update(const double *env, const double *g_old, double beta, double *g_new,
+                      double *sigma_sum) {
+  if (!env || !g_old || !g_new) return 1;
+  cd E[16], Go[16], Gn[16];
+  load_gate(env, E);
+  load_gate(g_old, Go);
+  polar_update(E, Go, beta, Gn, sigma_sum);
+  for (int i = 0; i < 16; ++i) { g_new[2 * i] = Gn[i].real(); g_new[2 * i + 1] = Gn[i].imag(); }
+  return 0;
+}
+
+// Scaled Newton iteration for the unitary polar factor (self-check of svd4):
+// W <- (zeta W + (zeta W)^{-dag}) / 2, zeta = sqrt(||W^{-1}||_F / ||W||_F).
+int qfso_newton_polar(const double *a, double *w, int *iters) {
+  if (!a || !w) return 1;
+  cd W[16];
+  load_gate(a, W);
+  int it = 0;
+  for (; it < 100; ++it) {
+    // inverse by Gauss-Jordan with partial pivoting
+    cd M[4][8];
+    for (int r = 0; r < 4; ++r)
+      for (int c = 0; c < 8; ++c) M[r][c] = c < 4 ? W[4 * r + c] : (c - 4 == r ? cd(1, 0) : cd(0, 0));
+    for (int c = 0; c < 4; ++c) {
+      int piv = c;
+      for (int r = c + 1; r < 4; ++r) if (std::abs(M[r][c]) > std::abs(M[piv][c])) piv = r;
+      if (std::abs(M[piv][c]) == 0.0) return 2;
+      for (int q = 0; q < 8; ++q) std::swap(M[c][q], M[piv][q]);
+      cd inv = 1.0 / M[c][c];
+      for (int q = 0; q < 8; ++q) M[c][q] *= inv;
+      for (int r = 0; r < 4; ++r) {
+        if (r == c) continue;
+        cd f = M[r][c];
+        for (int q = 0; q < 8; ++q) M[r][q] -= f * M[c][q];
+      }
+    }
+    double nw = 0, ni = 0;
+    for (int r = 0; r < 4; ++r)
+      for (int c = 0; c < 4; ++c) { nw += std::norm(W[4 * r + c]); ni += std::norm(M[r][c + 4]); }
+    double zeta = std::sqrt(std::sqrt(ni) / std::sqrt(nw));
+    cd Wn[16];
+    double diff = 0, nn = 0;
+    for (int r = 0; r < 4; ++r)
+      for (int c = 0; c < 4; ++c) {
+        // (W^{-1})^dag [r][c] = conj(Winv[c][r])
+        Wn[4 * r + c] = 0.5 * (zeta * W[4 * r + c] + std::conj(M[c][r + 4]) / zeta);
+        diff += std::norm(Wn[4 * r + c] - W[4 * r + c]);
+        nn += std::norm(Wn[4 * r + c]);
+      }
+    for (int i = 0; i < 16; ++i) W[i] = Wn[i];
+    if (std::sqrt(diff) <= 1e-15 * std::sqrt(nn)) { ++it; break; }
+  }
+  for (int i = 0; i < 16; ++i) { w[2 * i] = W[i].real(); w[2 * i + 1] = W[i].imag(); }
+  if (iters) *iters = it;
+  return 0;
+}
+
+double qfso_distance(int n, int m, const double *a, const double *b) {
+  if (m <= 0) return 0.0;
+  return (double)(sq_distance_sum(n, 0, m, 1, a, b) / (long double)m);
+}
+
+int qfso_trace_sweeps(int n, int k, const int32_t *pairs, int s, const double *init_gates, int m,
+                      const double *x, const double *y, double beta, int n_sweeps, int g,
+                      double *env_trace, double *gate_trace, double *cost_trace,
+                      double *sigma_trace, int n_threads) {
+  if (check_structure(n, k, pairs) || s < 1 || m < 1 || m > (1 << n) || !init_gates || !x ||
+      !y || n_sweeps < 0 || g < 1)
+    return 1;
+#ifdef _OPENMP
+  if (n_threads > 0) omp_set_num_threads(n_threads);
+#pragma omp parallel for schedule(dynamic, 1)
+#endif
+  for (int st = 0; st < s; ++st) {
+    std::vector<cd> G((size_t)k * 16);
+    for (int i = 0; i < 16 * k; ++i)
+      G[i] = cd(init_gates[2 * ((size_t)st * k * 16 + i)], init_gates[2 * ((size_t)st * k * 16 + i) + 1]);
+    std::vector<double> B, chi;
+    SweepOut so;
+    for (int t = 0; t < n_sweeps; ++t) {
+      sweep_one(n, k, pairs, G.data(), m, x, y, beta, g, &so, B, chi);
+      if (env_trace)
+        for (int i = 0; i < k; ++i)
+          for (int q = 0; q < 16; ++q) {
+            size_t o = ((((size_t)t * k + i) * s + st) * 16 + q) * 2;
+            env_trace[o] = so.env[16 * i + q].real();
+            env_trace[o + 1] = so.env[16 * i + q].imag();
+          }
+      if (gate_trace)
+        for (int i = 0; i < 16 * k; ++i) {
+          size_t o = (((size_t)t * s + st) * k * 16 + i) * 2;
+          gate_trace[o] = G[i].real();
+          gate_trace[o + 1] = G[i].imag();
+        }
+      if (cost_trace) cost_trace[(size_t)t * s + st] = so.c_train;
+      if (sigma_trace)
+        for (int i = 0; i < k; ++i) sigma_trace[((size_t)t * k + i) * s + st] = so.sig[i];
+    }
+  }
+  return 0;
+}
+
+// Controller (P:114 double-and-restart, P:176 plateau
+// window, P:182-192 generalisation check, P:354 keep gates on restart,
+// P:360-378 hyperparameters; readings R7-R14, R16).
+int qfso_instantiate(int n, int k, const int32_t *pairs, int m_pool, const double *x,
+                     const double *y, int v, const double *xv, const double *yv, int s,
+                     const double *init_gates, const qfso_params *p, double *out_gates,
+                     qfso_result *out, int *winner, int n_threads) {
+  const long N = 1L << n;
+  if (check_structure(n, k, pairs) || s < 1 || !p || !init_gates || !x || !y || !out_gates ||
+      !out || m_pool < 1 || m_pool > N || p->m_init < 1 || p->m_init > m_pool || v < 0 ||
+      (v > 0 && (!xv || !yv)) || p->max_iter < 1)
+    return 1;
+  struct St {
+    std::vector<cd> G;
+    int M, it, total, fails, restarts, term, conv_sweep;
+    bool has_prev, active;
+    double c_prev, c_train, c_val;
+    std::vector<double> B, chi;
+  };
+  std::vector<St> S(s);
+  for (int st = 0; st < s; ++st) {
+    S[st].G.resize((size_t)k * 16);
+    for (int i = 0; i < 16 * k; ++i)
+      S[st].G[i] = cd(init_gates[2 * ((size_t)st * k * 16 + i)], init_gates[2 * ((size_t)st * k * 16 + i) + 1]);
+    S[st].M = p->m_init; S[st].it = 0; S[st].total = 0; S[st].fails = 0; S[st].restarts = 0;
+    S[st].term = -1; S[st].conv_sweep = -1; S[st].has_prev = false; S[st].active = true;
+    S[st].c_prev = 0; S[st].c_train = NAN; S[st].c_val = NAN;
+  }
+  const double otr = p->overtrain_ratio;
+#ifdef _OPENMP
+  if (n_threads > 0) omp_set_num_threads(n_threads);
+#endif
+  for (int t = 1;; ++t) {
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic, 1)
+#endif
+    for (int st = 0; st < s; ++st) {
+      St &A = S[st];
+      if (!A.active) continue;
+      SweepOut so;
+      sweep_one(n, k, pairs, A.G.data(), A.M, x, y, p->beta, 1, &so, A.B, A.chi);  // step 1
+      A.c_train = so.c_train;
+      A.c_val = v > 0 ? validation_cost(n, k, pairs, A.G.data(), v, xv, yv) : NAN;
+    }
+    bool any_conv = false;
+    for (int st = 0; st < s; ++st) {
+      St &A = S[st];
+      if (!A.active) continue;
+      A.it += 1; A.total += 1;
+      const double c = A.c_train;
+      const bool gen_check = v > 0 && std::isfinite(otr) && A.M < N;           // step 2
+      bool conv = false;                                                       // step 3
+      if (c <= p->dist_tol) {
+        if (!gen_check) conv = true;
+        else if (c < 1e-14) conv = A.c_val <= (1.0 + otr) * p->dist_tol;
+        else conv = A.c_val / c - 1.0 <= otr;
+      }
+      if (conv) {
+        A.term = 0; A.active = false; A.conv_sweep = t; any_conv = true;
+        continue;
+      }
+      if (gen_check && A.it >= p->min_iter && A.c_val / c - 1.0 > otr) {       // step 4
+        if (2 * A.M > m_pool && A.M < N) { A.term = 3; A.active = false; continue; }
+        A.M = (int)std::min<long>(2L * A.M, N);
+        A.it = 0; A.fails = 0; A.has_prev = false; A.restarts += 1;
+      } else if (p->plateau_window > 0) {                                      // step 5
+        if (A.has_prev)
+          A.fails = (std::fabs(A.c_prev) - std::fabs(c) > p->diff_tol_r * std::fabs(c)) ? 0 : A.fails + 1;
+        A.c_prev = c; A.has_prev = true;
+        if (A.it >= p->min_iter && A.fails >= p->plateau_window) { A.term = 1; A.active = false; continue; }
+      }
+      if (A.total >= p->max_iter) { A.term = 2; A.active = false; }            // step 6
+    }
+    bool any_active = false;
+    for (int st = 0; st < s; ++st) any_active |= S[st].active;
+    if (any_conv && p->stop_on_first) {
+      for (int st = 0; st < s; ++st)
+        if (S[st].active) { S[st].active = false; S[st].term = 4; }
+      any_active = false;
+    }
+    if (!any_active) break;
+  }
+  // winner: lowest index among the earliest converged;
+  // else min c_train, ties to the lower index.
+  int win = -1, best_sweep = 1 << 30;
+  for (int st = 0; st < s; ++st)
+    if (S[st].term == 0 && S[st].conv_sweep < best_sweep) { best_sweep = S[st].conv_sweep; win = st; }
+  if (win < 0) {
+    double best = INFINITY;
+    for (int st = 0; st < s; ++st)
+      if (S[st].c_train < best) { best = S[st].c_train; win = st; }
+    if (win < 0) win = 0;
+  }
+  for (int st = 0; st < s; ++st) {
+    for (int i = 0; i < 16 * k; ++i) {
+      out_gates[2 * ((size_t)st * k * 16 + i)] = S[st].G[i].real();
+      out_gates[2 * ((size_t)st * k * 16 + i) + 1] = S[st].G[i].imag();
+    }
+    out[st].c_train = S[st].c_train; out[st].c_val = S[st].c_val;
+    out[st].sweeps = S[st].total; out[st].restarts = S[st].restarts;
+    out[st].final_m = S[st].M; out[st].term = S[st].term;
+  }
+  if (winner) *winner = win;
+  return 0;
+}
+
+int qfso_bench_sweeps(int n, int k, const int32_t *pairs, int s, const double *init_gates, int m,
+                      const double *x, const double *y, int n_sweeps, int n_threads,
+                      double *sec) {
+  auto t0 = std::chrono::steady_clock::now();
+  int rc = qfso_trace_sweeps(n, k, pairs, s, init_gates, m, x, y, 0.0, n_sweeps, 1, nullptr,
+                             nullptr, nullptr, nullptr, n_threads);
+  auto t1 = std::chrono::steady_clock::now();
+  if (sec) *sec = std::chrono::duration<double>(t1 - t0).count();
+  return rc;
+}
+
+}  // extern "C"

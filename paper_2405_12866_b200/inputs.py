@@ -1,0 +1,240 @@
+"""Seeded synthetic inputs for QFactor-Sample instantiation (harness side).
+
+This module is the ONLY code shared by the CUDA path's tests/bench and the CPU
+oracle's tests.  It draws random numbers and builds the problem the method is
+asked to solve; it holds none of the method's arithmetic (no environment, no
+SVD/polar update, no sweep, no cost).  Everything here is numpy.
+
+What it builds (SURVEY.md §8(d) "Concrete inputs"; DESIGN.md §3 "Input recipe"):
+
+* Haar-random 4x4 blocks: QR of a complex Gaussian, columns times the phases
+  of diag(R) ("columns of a random unitary matrix"; SPEC.md
+  S:82 construction).
+* Training / validation states: the columns of a thin QR of an N x M complex
+  Gaussian with the same phase fix, stored as rows ``[M][N]``
+  ("randomly selecting M mutually orthogonal states", P:112
+  "sampled from the Haar random distribution").
+* Circuit structures of the BASELINE.json configs (C1..C5, C5b, C5c).
+* Targets ``y = U x`` with U the product of the target blocks on the same
+  structure (PAPER.md P:198 re-instantiate flow: "calculate its unitary, and
+  ask QFactor-Sample to instantiate that unitary using the original partition
+  circuit structure").  The harness applies U with a tensor-leg contraction
+  (numpy tensordot over the reshaped ``(M, 2, ..., 2)`` state), a formulation
+  independent of both the oracle's bit-insertion loops and the CUDA kernels;
+  the method receives y as data (the A tensor of P:127), it never computes it.
+* Initial gates: R = Haar blocks per start ("various initial gate
+  unitaries"); W = warm start exp(i*eps*H) T_k.
+
+Conventions (DESIGN.md §2 readings 1-4): little-endian amplitude index (bit q
+of the index is qubit q); a gate on the ordered pair (p0, p1) acts on the local
+index l = b(p0) + 2*b(p1); gate matrices are row-major ``[l_out][l_in]``.
+
+Seeds: ``numpy.random.default_rng(SeedSequence([cfg, stream, idx]))`` with
+stream 0 target blocks (idx = gate), 1 training pool, 2 validation set,
+3 initial gates (idx = start), 4 random pairs.
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import numpy as np
+
+__all__ = [
+    "rng_for", "haar_unitary", "haar_states", "brick_pairs", "c4_pairs",
+    "apply_circuit_tensor", "warm_gate", "Problem", "make_problem", "CONFIGS",
+]
+
+
+def rng_for(cfg: int, stream: int, idx: int = 0) -> np.random.Generator:
+    return np.random.default_rng(np.random.SeedSequence([int(cfg), int(stream), int(idx)]))
+
+
+def _complex_gaussian(rng: np.random.Generator, shape) -> np.ndarray:
+    return (rng.standard_normal(shape) + 1j * rng.standard_normal(shape)) / math.sqrt(2.0)
+
+
+def haar_unitary(rng: np.random.Generator, d: int = 4) -> np.ndarray:
+    """Haar-random d x d unitary: QR of a complex Gaussian with phase-fixed R."""
+    z = _complex_gaussian(rng, (d, d))
+    q, r = np.linalg.qr(z)
+    ph = np.diagonal(r) / np.abs(np.diagonal(r))
+    return np.ascontiguousarray(q * ph[None, :])
+
+
+def haar_states(rng: np.random.Generator, n: int, m: int) -> np.ndarray:
+    """m mutually orthonormal Haar states on n qubits, as rows ``[m][2^n]``.
+
+    The first m columns of a Haar unitary: thin QR of a 2^n x m complex
+    Gaussian with the columns multiplied by the phases of diag(R).
+    """
+    N = 1 << n
+    if m > N or m < 1:
+        raise ValueError(f"need 1 <= m <= 2^n, got m={m}, n={n}")
+    z = _complex_gaussian(rng, (N, m))
+    q, r = np.linalg.qr(z, mode="reduced")
+    ph = np.diagonal(r) / np.abs(np.diagonal(r))
+    return np.ascontiguousarray((q * ph[None, :]).T)
+
+
+def basis_states(rng: np.random.Generator, n: int, m: int) -> np.ndarray:
+    """m distinct computational basis states (App. D)."""
+    N = 1 << n
+    idx = rng.choice(N, size=m, replace=False)
+    out = np.zeros((m, N), dtype=np.complex128)
+    out[np.arange(m), idx] = 1.0
+    return out
+
+
+def brick_pairs(n: int, k: int) -> np.ndarray:
+    """Brick-wall layout of adjacent pairs (SURVEY.md §8(c) reading 20).
+
+    Layer l has the pairs (q, q+1) for q = l mod 2, l mod 2 + 2, ... < n-1;
+    layers are concatenated and the stream is truncated to k gates.
+    """
+    out = []
+    layer = 0
+    while len(out) < k:
+        for q in range(layer % 2, n - 1, 2):
+            out.append((q, q + 1))
+        layer += 1
+    return np.asarray(out[:k], dtype=np.int32)
+
+
+def c4_pairs(n: int, k: int, rng: np.random.Generator) -> np.ndarray:
+    """Brick wall plus seeded random non-adjacent pairs (reading 20).
+
+    Slot j with j mod 5 == 4 takes a random pair (a, b), a < b, b - a >= 2;
+    the other slots take the brick stream in order.
+    """
+    n_rand = sum(1 for j in range(k) if j % 5 == 4)
+    brick = list(map(tuple, brick_pairs(n, k - n_rand)))
+    out = []
+    bi = 0
+    for j in range(k):
+        if j % 5 == 4:
+            while True:
+                a, b = sorted(int(v) for v in rng.choice(n, size=2, replace=False))
+                if b - a >= 2:
+                    break
+            out.append((a, b))
+        else:
+            out.append(brick[bi])
+            bi += 1
+    return np.asarray(out, dtype=np.int32)
+
+
+def apply_circuit_tensor(n: int, pairs: np.ndarray, gates: np.ndarray, states: np.ndarray) -> np.ndarray:
+    """Harness simulator: returns C states (rows), C = G_{K-1} ... G_0.
+
+    States are reshaped to ``(M, 2, ..., 2)``; with little-endian indices the
+    C-order axis of qubit q is ``1 + (n - 1 - q)``.  A gate matrix G[l_out][l_in]
+    with l = b(p0) + 2 b(p1) is the tensor ``G4[o1, o0, i1, i0]``.
+    """
+    m = states.shape[0]
+    psi = np.asarray(states, dtype=np.complex128).reshape((m,) + (2,) * n)
+    for (p0, p1), g in zip(np.asarray(pairs), np.asarray(gates)):
+        a0, a1 = 1 + (n - 1 - int(p0)), 1 + (n - 1 - int(p1))
+        g4 = np.asarray(g, dtype=np.complex128).reshape(2, 2, 2, 2)
+        res = np.tensordot(psi, g4, axes=([a1, a0], [2, 3]))
+        psi = np.moveaxis(res, [-2, -1], [a1, a0])
+    return np.ascontiguousarray(psi.reshape(m, 1 << n))
+
+
+def warm_gate(rng: np.random.Generator, target: np.ndarray, eps: float) -> np.ndarray:
+    """exp(i*eps*H) @ target with H = (A + A^dag)/2 scaled to spectral norm 1."""
+    a = _complex_gaussian(rng, (4, 4))
+    h = 0.5 * (a + a.conj().T)
+    w, v = np.linalg.eigh(h)
+    w = w / np.max(np.abs(w))
+    ex = (v * np.exp(1j * eps * w)[None, :]) @ v.conj().T
+    return ex @ target
+
+
+@dataclasses.dataclass
+class Problem:
+    """One synthetic instantiation problem (all arrays complex128, C-contiguous)."""
+    name: str
+    n: int
+    pairs: np.ndarray          # int32 [K][2]
+    target: np.ndarray         # [K][4][4] target blocks (harness only)
+    x: np.ndarray              # [m_pool][N] training pool
+    y: np.ndarray              # [m_pool][N] = U x
+    xv: np.ndarray             # [V][N] validation inputs
+    yv: np.ndarray             # [V][N] = U xv
+    init: np.ndarray           # [S][K][4][4] initial gates
+    m_init: int
+    params: dict
+
+    @property
+    def k(self) -> int:
+        return int(self.pairs.shape[0])
+
+    @property
+    def s(self) -> int:
+        return int(self.init.shape[0])
+
+
+# BASELINE.json configs, concretised in SURVEY.md §8(d).  Fields:
+# n, K, structure, m_init, m_pool, V, S, otr, window, max_iter.
+CONFIGS = {
+    "c1": dict(cfg=1, n=3, k=4, structure="c1", m_init=4, m_pool=4, v=0, s=1,
+               otr=math.inf, window=0, max_iter=500),
+    "c2": dict(cfg=2, n=6, k=20, structure="brick", m_init=8, m_pool=64, v=16, s=32,
+               otr=0.1, window=5, max_iter=2000),
+    "c3": dict(cfg=3, n=9, k=60, structure="brick", m_init=16, m_pool=512, v=16, s=64,
+               otr=0.1, window=5, max_iter=2000),
+    "c4": dict(cfg=4, n=12, k=150, structure="c4", m_init=32, m_pool=256, v=16, s=16,
+               otr=0.1, window=5, max_iter=2000),
+    "c5": dict(cfg=5, n=14, k=300, structure="brick", m_init=64, m_pool=64, v=16, s=1,
+               otr=math.inf, window=5, max_iter=2000),
+    "c5b": dict(cfg=6, n=10, k=100, structure="brick", m_init=16, m_pool=128, v=16, s=1,
+                otr=0.1, window=5, max_iter=2000),
+    "c5c": dict(cfg=7, n=10, k=100, structure="brick", m_init=16, m_pool=128, v=16, s=64,
+                otr=0.1, window=5, max_iter=2000),
+}
+
+
+def make_problem(name: str, init: str = "R", s: int | None = None, m_pool: int | None = None,
+                 v: int | None = None, k: int | None = None, eps: float = 0.3,
+                 m_init: int | None = None) -> Problem:
+    """Build config ``name`` (optionally reduced: fewer starts / gates / pool rows)."""
+    c = dict(CONFIGS[name])
+    cfg, n = c["cfg"], c["n"]
+    kk = c["k"] if k is None else int(k)
+    if c["structure"] == "c1":
+        pairs = np.asarray([(0, 1), (1, 2), (0, 1), (1, 2)], dtype=np.int32)[:kk]
+    elif c["structure"] == "brick":
+        pairs = brick_pairs(n, kk)
+    else:
+        pairs = c4_pairs(n, kk, rng_for(cfg, 4, 0))
+    target = np.stack([haar_unitary(rng_for(cfg, 0, j)) for j in range(kk)])
+    mp = c["m_pool"] if m_pool is None else int(m_pool)
+    vv = c["v"] if v is None else int(v)
+    x = haar_states(rng_for(cfg, 1, 0), n, mp)
+    y = apply_circuit_tensor(n, pairs, target, x)
+    if vv > 0:
+        xv = haar_states(rng_for(cfg, 2, 0), n, vv)
+        yv = apply_circuit_tensor(n, pairs, target, xv)
+    else:
+        xv = np.zeros((0, 1 << n), dtype=np.complex128)
+        yv = np.zeros((0, 1 << n), dtype=np.complex128)
+    ss = c["s"] if s is None else int(s)
+    gates = np.empty((ss, kk, 4, 4), dtype=np.complex128)
+    for st in range(ss):
+        rng = rng_for(cfg, 3, st)
+        for j in range(kk):
+            if init == "R":
+                gates[st, j] = haar_unitary(rng)
+            elif init == "W":
+                gates[st, j] = warm_gate(rng, target[j], eps)
+            elif init == "T":        # exact initialisation (fixed-point tests)
+                gates[st, j] = target[j]
+            else:
+                raise ValueError(init)
+    mi = min(c["m_init"], mp) if m_init is None else int(m_init)
+    params = dict(dist_tol=1e-8, diff_tol_r=1e-3, plateau_window=c["window"], min_iter=6,
+                  max_iter=c["max_iter"], m_init=mi, overtrain_ratio=c["otr"], beta=0.0,
+                  stop_on_first=1)
+    return Problem(name=name, n=n, pairs=pairs, target=target, x=x, y=y, xv=xv, yv=yv,
+                   init=gates, m_init=mi, params=params)

@@ -1,0 +1,454 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix.
+
+Each test names the passage it pins (P:<line> = PAPER.md line).  None of the
+expected values comes from the oracle itself or from the CUDA path: they are
+brute-force dense products (tests/qfs_dense.py), closed forms, textbook special
+cases (tests/golden/), LAPACK (numpy.linalg, test-only library cross-check),
+or invariants of the method.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2405_12866_b200 import inputs as I
+import qfs_dense as D
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+# ------------------------------------------------------------------ apply ---
+@pytest.mark.parametrize("fixture", ["cnot_apply.json", "x_on_qubit0.json"])
+def test_golden_gate_on_basis(fixture):
+    """Textbook gates on basis states (reading 1)."""
+    g = gold(fixture)
+    G = np.asarray(g["gate_rows_l_out"], dtype=np.complex128)
+    for i, j in g["basis_map"].items():
+        e = np.zeros((1, 4), np.complex128)
+        e[0, int(i)] = 1
+        out = oracle.apply_gate(2, 0, 1, G, e)
+        want = np.zeros(4)
+        want[j] = 1
+        assert np.array_equal(out[0], want)
+
+
+@pytest.mark.parametrize("n", [2, 3, 4])
+def test_apply_matches_dense_embedding(n):
+    """apply == dense 2^n x 2^n embedding times vector, every ordered pair (brute force)."""
+    rng = np.random.default_rng(100 + n)
+    psi = D.random_complex(rng, (3, 1 << n))
+    for p0 in range(n):
+        for p1 in range(n):
+            if p0 == p1:
+                continue
+            G = D.random_complex(rng, (4, 4))          # any matrix, not only unitaries
+            got = oracle.apply_gate(n, p0, p1, G, psi)
+            want = (D.embed(n, p0, p1, G) @ psi.T).T
+            assert np.abs(got - want).max() <= 1e-13 * np.abs(want).max()
+            gotd = oracle.apply_gate(n, p0, p1, G, psi, dagger=True)
+            wantd = (D.embed(n, p0, p1, G.conj().T) @ psi.T).T
+            assert np.abs(gotd - wantd).max() <= 1e-13 * np.abs(wantd).max()
+
+
+def test_apply_reversed_pair_is_swap_conjugate():
+    """(p1, p0) with G == (p0, p1) with SWAP G SWAP (SURVEY pin table)."""
+    rng = np.random.default_rng(7)
+    n = 4
+    psi = D.random_complex(rng, (2, 1 << n))
+    SW = np.eye(4)[[0, 2, 1, 3]]
+    for p0, p1 in [(0, 1), (1, 3), (0, 3), (2, 3)]:
+        G = D.random_unitary(rng)
+        a = oracle.apply_gate(n, p1, p0, G, psi)
+        b = oracle.apply_gate(n, p0, p1, SW @ G @ SW, psi)
+        assert np.abs(a - b).max() < 1e-14
+
+
+def test_apply_norm_and_inverse():
+    """Unitary gates preserve the norm; G then G^dag is the identity."""
+    rng = np.random.default_rng(8)
+    n = 6
+    psi = I.haar_states(rng, n, 4)
+    for p0, p1 in [(0, 1), (5, 2), (3, 4)]:
+        G = D.random_unitary(rng)
+        out = oracle.apply_gate(n, p0, p1, G, psi)
+        assert np.abs(np.linalg.norm(out, axis=1) - 1).max() < 1e-13
+        back = oracle.apply_gate(n, p0, p1, G, out, dagger=True)
+        assert np.abs(back - psi).max() < 1e-14
+
+
+def test_forward_matches_dense_and_harness():
+    """circuit_forward == dense product == harness tensordot simulator (P:127 B tensors)."""
+    rng = np.random.default_rng(9)
+    n = 4
+    pairs = np.array([(0, 1), (2, 3), (1, 2), (3, 0), (0, 2), (3, 1), (1, 0)], np.int32)
+    gates = np.stack([D.random_unitary(rng) for _ in pairs])
+    x = I.haar_states(rng, n, 5)
+    got = oracle.circuit_forward(n, pairs, gates, x)
+    want = (D.circuit_matrix(n, pairs, gates) @ x.T).T
+    harness = I.apply_circuit_tensor(n, pairs, gates, x)
+    assert np.abs(got - want).max() < 1e-14
+    assert np.abs(harness - want).max() < 1e-14
+
+
+# ------------------------------------------------------------ environment ---
+@pytest.mark.parametrize("n", [3, 4])
+def test_environment_matches_d2_probes(n):
+    """E[l_in][l_out] = sum_m <y_m| C_{gate i -> |l_out><l_in|} |x_m>.
+
+    Brute force: replace gate i by each of the 16 matrix units and evaluate the
+    overlap with dense matrices (SURVEY §8(c) pin 'E d^2 probe')."""
+    rng = np.random.default_rng(20 + n)
+    pairs = np.array([(0, 1), (n - 1, 1), (2, 0), (1, 2), (0, n - 1)], np.int32)
+    gates = np.stack([D.random_unitary(rng) for _ in pairs])
+    m = 3
+    x = I.haar_states(rng, n, m)
+    y = D.random_complex(rng, (m, 1 << n))
+    for i in range(len(pairs)):
+        pre = D.circuit_matrix(n, pairs[:i], gates[:i])
+        suf = D.circuit_matrix(n, pairs[i + 1:], gates[i + 1:])
+        phi = (pre @ x.T).T
+        chi = (suf.conj().T @ y.T).T
+        E = oracle.environment(n, int(pairs[i, 0]), int(pairs[i, 1]), phi, chi)
+        probe = np.zeros((4, 4), np.complex128)
+        for a in range(4):          # l_out
+            for b in range(4):      # l_in
+                unit = np.zeros((4, 4))
+                unit[a, b] = 1
+                Cab = suf @ D.embed(n, int(pairs[i, 0]), int(pairs[i, 1]), unit) @ pre
+                probe[b, a] = sum(y[j].conj() @ Cab @ x[j] for j in range(m))
+        assert np.abs(E - probe).max() <= 1e-13 * np.abs(probe).max()
+        # Tr(E G_i) = sum_m <y_m|C|x_m>  (the sample overlap)
+        C = D.circuit_matrix(n, pairs, gates)
+        ov = sum(y[j].conj() @ C @ x[j] for j in range(m))
+        assert abs(np.trace(E @ gates[i]) - ov) < 1e-13 * max(1, abs(ov))
+
+
+def test_environment_k1_full_basis_is_target_adjoint():
+    """K=1, n=2, M=4 computational basis: E = U^dag exactly; the update gives U; cost 0."""
+    rng = np.random.default_rng(31)
+    U = D.random_unitary(rng)
+    x = np.eye(4, dtype=np.complex128)
+    y = (U @ x.T).T
+    E = oracle.environment(2, 0, 1, x, y)
+    assert np.abs(E - U.conj().T).max() == 0.0
+    G, ss = oracle.polar_update(E, np.eye(4))
+    assert np.abs(G - U).max() < 1e-14
+    tr = oracle.trace_sweeps(2, np.array([[0, 1]], np.int32), np.eye(4)[None, None], x, y, 4, 1)
+    assert tr["cost"][0, 0] < 1e-28
+
+
+def test_identity_environment_perfect_match():
+    """Perfect match with the identity gate: Tr(E I) = M (north_star pin list)."""
+    rng = np.random.default_rng(32)
+    n, m = 4, 5
+    x = I.haar_states(rng, n, m)
+    E = oracle.environment(n, 1, 3, x, x)
+    assert abs(np.trace(E) - m) < 1e-13
+
+
+# ---------------------------------------------------------------- SVD/polar --
+def test_svd_golden_known_singular_values():
+    """Hand-built A = P D Q with D = diag(4,3,2,1)."""
+    g = gold("svd_known.json")
+    phP = np.array([1, 1j, -1, -1j])
+    phQ = np.array([np.exp(1j * np.pi / 3), 1, -1, 1j])
+    d = [4.0, 3.0, 2.0, 1.0]
+    A = np.zeros((4, 4), np.complex128)
+    for c in range(4):
+        A[(c + 1) % 4, c] = phP[(c + 1) % 4] * d[c] * phQ[c]
+    x, s, y, _ = oracle.svd4(A)
+    assert np.allclose(np.sort(s)[::-1], g["sigma_sorted_desc"], atol=1e-14, rtol=0)
+    G, ss = oracle.polar_update(A, np.eye(4))
+    assert abs(ss - g["sum_sigma"]) < 1e-13
+    assert abs(np.trace(A @ G).real - g["sum_sigma"]) < 1e-13
+
+
+def _hard_matrices(rng, count):
+    out = []
+    for t in range(count):
+        kind = t % 5
+        A = D.random_complex(rng, (4, 4))
+        if kind == 1:      # ill-conditioned, cond 1e8
+            u, v = D.random_unitary(rng), D.random_unitary(rng)
+            A = u @ np.diag([1, 1e-3, 1e-5, 1e-8]) @ v
+        elif kind == 2:    # rank 2
+            A = D.random_complex(rng, (4, 2)) @ D.random_complex(rng, (2, 4))
+        elif kind == 3:    # degenerate singular values
+            u, v = D.random_unitary(rng), D.random_unitary(rng)
+            A = u @ np.diag([2, 2, 1, 1]) @ v
+        elif kind == 4:    # scaled tiny / huge
+            A = A * (1e-150 if t % 2 else 1e150)
+        out.append(A)
+    return out
+
+
+def test_svd_reconstruction_unitarity_and_lapack():
+    """A = X diag(s) Y^dag, X, Y unitary; singular values == LAPACK (test-only)."""
+    rng = np.random.default_rng(40)
+    for A in _hard_matrices(rng, 500):
+        x, s, y, sweeps = oracle.svd4(A)
+        nA = np.linalg.norm(A)
+        assert np.linalg.norm(x @ np.diag(s) @ y.conj().T - A) <= 1e-13 * nA
+        assert np.abs(x.conj().T @ x - np.eye(4)).max() < 1e-13
+        assert np.abs(y.conj().T @ y - np.eye(4)).max() < 1e-13
+        ref = np.linalg.svd(A, compute_uv=False)
+        assert np.abs(np.sort(s)[::-1] - ref).max() <= 1e-13 * ref[0]
+        assert sweeps < 30
+
+
+def test_polar_von_neumann_optimality():
+    """Re Tr(E G_new) = sum sigma >= Re Tr(E V) for random unitaries V."""
+    rng = np.random.default_rng(41)
+    Vs = [D.random_unitary(rng) for _ in range(1000)]
+    for t in range(60):
+        E = D.random_complex(rng, (4, 4))
+        G, ss = oracle.polar_update(E, np.eye(4))
+        assert abs(np.trace(E @ G).real - ss) < 1e-13 * ss
+        assert abs(np.trace(E @ G).imag) < 1e-13 * ss
+        best = max(np.trace(E @ V).real for V in Vs)
+        assert best <= ss + 1e-12
+        assert abs(ss - np.linalg.svd(E, compute_uv=False).sum()) < 1e-13 * ss
+
+
+def test_polar_special_cases():
+    """E = V^dag gives V; beta = 1 gives u_old (P:386 'no update'); zero E gives a unitary."""
+    rng = np.random.default_rng(42)
+    for _ in range(50):
+        V = D.random_unitary(rng)
+        G, _ = oracle.polar_update(V.conj().T, np.eye(4))
+        assert np.abs(G - V).max() < 1e-13
+        E = D.random_complex(rng, (4, 4))
+        G1, _ = oracle.polar_update(E, V, beta=1.0)
+        assert np.abs(G1 - V).max() < 1e-13
+    G0, ss = oracle.polar_update(np.zeros((4, 4)), np.eye(4))
+    assert ss == 0 and np.abs(G0.conj().T @ G0 - np.eye(4)).max() < 1e-14
+
+
+def test_polar_matches_newton_and_handles_rank_deficiency():
+    """Jacobi polar == scaled-Newton polar (self-check) when sigma_4/sigma_1 >= 1e-6;
+    rank-deficient E still yields a unitary maximiser (reading 5)."""
+    rng = np.random.default_rng(43)
+    for A in _hard_matrices(rng, 300):
+        G, ss = oracle.polar_update(A, np.eye(4))
+        assert np.abs(G.conj().T @ G - np.eye(4)).max() < 1e-13
+        sv = np.linalg.svd(A, compute_uv=False)
+        assert abs(np.trace(A @ G).real - sv.sum()) <= 1e-13 * sv[0]
+        if sv[-1] / sv[0] >= 1e-6:
+            W, it = oracle.newton_polar(A)
+            assert np.abs(G - W.conj().T).max() < 1e-12
+
+
+# ------------------------------------------------------------------- cost ---
+def test_cost_golden_cnot_vs_identity():
+    """Full-basis sample cost == ||U - C||_F^2 / 2^n (P:48-51 vs P:116-120), hand value."""
+    g = gold("cost_cnot_vs_identity.json")
+    U = np.asarray(gold("cnot_apply.json")["gate_rows_l_out"], dtype=np.complex128)
+    x = np.eye(4, dtype=np.complex128)
+    y = (U @ x.T).T
+    assert oracle.distance(x, y) == g["sample_cost"]
+    assert np.linalg.norm(U - np.eye(4)) ** 2 == g["frobenius_sq"]
+
+
+def test_cost_range_examples():
+    """C = U gives 0; C = -U gives 4 (range [0, 4]; SURVEY pin table 'Cost')."""
+    rng = np.random.default_rng(50)
+    y = I.haar_states(rng, 5, 7)
+    assert oracle.distance(y, y) == 0.0
+    assert abs(oracle.distance(-y, y) - 4.0) < 1e-14
+
+
+def test_sample_cost_equals_full_qfactor_cost_with_full_basis():
+    """M = 2^n orthonormal (Haar): c = ||U - C||_F^2/2^n = 2(1 - Re Tr(U^dag C)/2^n)
+    (eq:qfactor_cost_func P:48-51 <-> eq:qfactor_sample_cost_function P:116-120)."""
+    n = 3
+    rng = np.random.default_rng(51)
+    pairs = np.array([(0, 1), (1, 2), (0, 2), (2, 1)], np.int32)
+    target = np.stack([D.random_unitary(rng) for _ in pairs])
+    init = np.stack([D.random_unitary(rng) for _ in pairs])[None]
+    x = I.haar_states(rng, n, 8)
+    U = D.circuit_matrix(n, pairs, target)
+    y = (U @ x.T).T
+    tr = oracle.trace_sweeps(n, pairs, init, x, y, 8, 3)
+    for t in range(3):
+        C = D.circuit_matrix(n, pairs, tr["gates"][t, 0])
+        full = np.linalg.norm(U - C) ** 2 / 8
+        alt = 2 * (1 - np.trace(U.conj().T @ C).real / 8)
+        assert abs(tr["cost"][t, 0] - full) < 1e-14
+        assert abs(full - alt) < 1e-13
+
+
+# ------------------------------------------------------------------ sweep ---
+def _small_problem(seed=60, n=4, m=6, s=2):
+    rng = np.random.default_rng(seed)
+    pairs = np.array([(0, 1), (2, 3), (1, 2), (0, 3), (1, 3), (0, 2)], np.int32)
+    target = np.stack([D.random_unitary(rng) for _ in pairs])
+    init = np.stack([np.stack([D.random_unitary(rng) for _ in pairs]) for _ in range(s)])
+    x = I.haar_states(rng, n, m)
+    U = D.circuit_matrix(n, pairs, target)
+    y = (U @ x.T).T
+    return n, pairs, target, init, x, y, U
+
+
+def test_sweep_first_update_env_matches_dense_and_chain_invariant():
+    """First sweep: E_{K-1} from the old circuit (dense); chain invariant
+    Tr(E_{i-1} G_{i-1}^old) = sum sigma(E_i) (reading 3)."""
+    n, pairs, target, init, x, y, U = _small_problem()
+    K, M = len(pairs), x.shape[0]
+    tr = oracle.trace_sweeps(n, pairs, init, x, y, M, 1)
+    for s in range(init.shape[0]):
+        C = D.circuit_matrix(n, pairs, init[s])
+        ov = sum(y[j].conj() @ C @ x[j] for j in range(M))
+        E = tr["env"][0, K - 1, s]
+        assert abs(np.trace(E @ init[s, K - 1]) - ov) < 1e-13
+        for i in range(K - 1, 0, -1):
+            lhs = np.trace(tr["env"][0, i - 1, s] @ init[s, i - 1])
+            assert abs(lhs - tr["sigma"][0, i, s]) < 1e-12
+        # E_i dense: prefix with old gates, suffix with the new ones (Fig. env_calc)
+        newg = tr["gates"][0, s]
+        for i in range(K):
+            pre = D.circuit_matrix(n, pairs[:i], init[s, :i])
+            suf = D.circuit_matrix(n, pairs[i + 1:], newg[i + 1:])
+            phi = (pre @ x.T).T
+            chi = (suf.conj().T @ y.T).T
+            Ed = oracle.environment(n, int(pairs[i, 0]), int(pairs[i, 1]), phi, chi)
+            assert np.abs(Ed - tr["env"][0, i, s]).max() < 1e-13
+
+
+def test_sweep_cost_monotone_and_monitor():
+    """beta=0: 2 - (2/M) sum sigma(E_k) is non-increasing along the sweep (K-1 -> 0)
+    and across sweeps, each value <= 2, and at gate 0 it equals c_train."""
+    n, pairs, target, init, x, y, U = _small_problem(61)
+    M = x.shape[0]
+    tr = oracle.trace_sweeps(n, pairs, init, x, y, M, 20)
+    mon = 2 - 2 / M * tr["sigma"]                  # [t][k][s]
+    K = len(pairs)
+    seq = np.concatenate([mon[t, ::-1, :] for t in range(20)], axis=0)   # visit order
+    assert (np.diff(seq, axis=0) <= 1e-13).all()
+    assert (mon <= 2 + 1e-13).all()
+    assert np.abs(mon[:, 0, :] - tr["cost"]).max() < 1e-12
+    assert (np.diff(tr["cost"], axis=0) <= 1e-13).all()
+    # gates stay unitary
+    G = tr["gates"][-1]
+    eye = np.eye(4)
+    assert max(np.abs(g.conj().T @ g - eye).max() for g in G.reshape(-1, 4, 4)) < 1e-13
+
+
+def test_exact_initialisation_fixed_point():
+    """G_init = target: cost ~0 and gates unchanged (SURVEY pin 'Sweep')."""
+    p = I.make_problem("c2", init="T", s=1)
+    tr = oracle.trace_sweeps(p.n, p.pairs, p.init, p.x, p.y, 8, 2)
+    assert tr["cost"].max() < 1e-26
+    assert np.abs(tr["gates"][-1, 0] - p.target).max() < 1e-13
+
+
+def test_k1_full_basis_solves_in_one_sweep():
+    """Single gate, full basis: the linear-form optimum is exact."""
+    rng = np.random.default_rng(62)
+    for n, (p0, p1) in [(2, (0, 1)), (3, (2, 0))]:
+        U1 = D.random_unitary(rng)
+        pairs = np.array([(p0, p1)], np.int32)
+        x = I.haar_states(rng, n, 1 << n)
+        y = I.apply_circuit_tensor(n, pairs, U1[None], x)
+        tr = oracle.trace_sweeps(n, pairs, D.random_unitary(rng)[None, None], x, y, 1 << n, 1)
+        assert tr["cost"][0, 0] < 1e-28
+        assert np.abs(tr["gates"][0, 0, 0] - U1).max() < 1e-13
+
+
+def test_two_gates_same_pair_full_basis():
+    """n=2, two gates on the same pair: after updating gate 1, E_1 = G_0 U^dag is unitary,
+    G_1 <- U G_0^dag and the cost is exactly 0 after one sweep."""
+    rng = np.random.default_rng(63)
+    U = D.random_unitary(rng)
+    G0 = D.random_unitary(rng)
+    pairs = np.array([(0, 1), (0, 1)], np.int32)
+    x = np.eye(4, dtype=np.complex128)
+    y = (U @ x.T).T
+    init = np.stack([G0, D.random_unitary(rng)])[None]
+    tr = oracle.trace_sweeps(2, pairs, init, x, y, 4, 1)
+    assert np.abs(tr["env"][0, 1, 0] - G0 @ U.conj().T).max() < 1e-14
+    assert tr["cost"][0, 0] < 1e-28
+
+
+def test_sample_shard_emulation_matches_unsharded():
+    """g-shard emulation (partials per shard summed in rank order) == g = 1."""
+    n, pairs, target, init, x, y, U = _small_problem(64, m=8)
+    a = oracle.trace_sweeps(n, pairs, init, x, y, 8, 3, g=1)
+    for g in (2, 4, 8):
+        b = oracle.trace_sweeps(n, pairs, init, x, y, 8, 3, g=g)
+        assert np.abs(a["env"] - b["env"]).max() <= 1e-13 * np.abs(a["env"]).max()
+        assert np.abs(a["gates"] - b["gates"]).max() <= 1e-13
+        assert np.abs(a["cost"] - b["cost"]).max() <= 1e-13 * a["cost"].max()
+
+
+# ------------------------------------------------------------- controller ---
+BASE = dict(dist_tol=1e-8, diff_tol_r=1e-3, plateau_window=5, min_iter=6, max_iter=200,
+            m_init=4, overtrain_ratio=0.1, beta=0.0, stop_on_first=1)
+
+
+def test_controller_beta1_plateau_at_sweep_6():
+    """beta = 1: no update -> constant cost -> PLATEAU at sweep
+    max(min_iter, window+1) = 6 with the defaults (step 5 worked consequence)."""
+    n, pairs, target, init, x, y, U = _small_problem(70, m=6, s=3)
+    p = dict(BASE, beta=1.0, overtrain_ratio=math.inf)
+    g, res, win = oracle.instantiate(n, pairs, x, y, None, None, init, p)
+    for r in res:
+        assert r["term"] == "PLATEAU" and r["sweeps"] == 6 and r["restarts"] == 0
+    assert np.abs(g - init).max() < 1e-13
+    assert win == int(np.argmin([r["c_train"] for r in res]))
+
+
+def test_controller_restart_geometry_and_min_iter():
+    """Overtrain -> double-and-restart keeping gates; M_final =
+    m_init 2^restarts; no plateau/overtrain stop before min_iter."""
+    p = I.make_problem("c2", init="R", s=3)
+    prm = dict(p.params, max_iter=60, stop_on_first=0)
+    g, res, win = oracle.instantiate(p.n, p.pairs, p.x, p.y, p.xv, p.yv, p.init, prm)
+    assert any(r["restarts"] >= 1 for r in res)
+    for r in res:
+        assert r["final_m"] == min(p.m_init * 2 ** r["restarts"], 1 << p.n)
+        assert r["sweeps"] >= prm["min_iter"] or r["term"] == "CONVERGED"
+        # total states ever used < 2 * final M ("2+4+...+m < 2m")
+        used = sum(p.m_init * 2 ** j for j in range(r["restarts"] + 1))
+        assert used < 2 * r["final_m"] or r["final_m"] == 1 << p.n
+
+
+def test_controller_pool_exhausted_and_max_iter():
+    """2M beyond the pool (M < 2^n) -> POOL_EXHAUSTED; max_iter counts all sweeps."""
+    p = I.make_problem("c2", init="R", s=2, m_pool=16)
+    prm = dict(p.params, max_iter=200, stop_on_first=0, m_init=8, plateau_window=0)
+    g, res, win = oracle.instantiate(p.n, p.pairs, p.x, p.y, p.xv, p.yv, p.init, prm)
+    for r in res:
+        assert r["term"] in ("POOL_EXHAUSTED", "CONVERGED")
+    assert any(r["term"] == "POOL_EXHAUSTED" for r in res)
+    prm2 = dict(p.params, max_iter=7, stop_on_first=0, overtrain_ratio=math.inf,
+                plateau_window=0)
+    g, res, win = oracle.instantiate(p.n, p.pairs, p.x, p.y, p.xv, p.yv, p.init, prm2)
+    for r in res:
+        assert r["term"] == "MAX_ITER" and r["sweeps"] == 7
+
+
+def test_controller_converges_warm_and_generalises():
+    """Solvable-by-construction target reaches c_train <= 1e-8 (north_star) and the
+    P:188-191 bound holds w.h.p.: >= 90% of 50 fresh Haar states have
+    ||U psi - C psi||^2 < d_tol (1 + otr)."""
+    p = I.make_problem("c2", init="W", s=4, eps=0.3)
+    prm = dict(p.params, max_iter=400)
+    g, res, win = oracle.instantiate(p.n, p.pairs, p.x, p.y, p.xv, p.yv, p.init, prm, threads=4)
+    r = res[win]
+    assert r["term"] == "CONVERGED" and r["c_train"] <= 1e-8
+    assert r["c_val"] / r["c_train"] - 1 <= 0.1 or r["final_m"] == 64 or r["c_train"] < 1e-14
+    others = [res[s]["term"] for s in range(4) if s != win]
+    assert all(t in ("STOPPED", "CONVERGED") for t in others)
+    fresh = I.haar_states(np.random.default_rng(999), p.n, 50)
+    yt = I.apply_circuit_tensor(p.n, p.pairs, p.target, fresh)
+    yc = oracle.circuit_forward(p.n, p.pairs, g[win], fresh)
+    d = np.sum(np.abs(yt - yc) ** 2, axis=1)
+    assert np.mean(d < prm["dist_tol"] * (1 + prm["overtrain_ratio"])) >= 0.9
