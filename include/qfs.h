@@ -1,0 +1,157 @@
+/* qfs.h — C ABI of the B200-native QFactor-Sample instantiation library
+ * (libqfs.so, arXiv 2405.12866).
+ *
+ * The library fits the 4x4 unitaries of a circuit of two-qubit blocks to a
+ * target U from sampled input/output states (§3): each
+ * sweep runs right to left over the gates, forms each gate's 4x4
+ * environment E over all 2^n amplitudes and M samples,
+ * replaces the gate by the unitary polar factor u = Y X^dag of E = X D Y^dag
+ * (eq:opt_u), and a host controller grows M ("double-and-restart",
+ * P:114) when the validation cost exceeds the training cost by
+ * more than overtrain_ratio.  Every step of a sweep runs in
+ * hand-written sm_100a CUDA kernels; there is no CPU fallback.
+ *
+ * Conventions (DESIGN.md §2 readings R1-R4):
+ *  - complex numbers are double[2] interleaved (re, im) (std::complex<double>,
+ *    cuDoubleComplex, numpy complex128 layout);
+ *  - amplitude index is little-endian: bit q of the index is qubit q;
+ *  - a gate on the ordered pair (p0, p1) acts on the local index
+ *    l = b(p0) + 2*b(p1); gate matrices are row-major G[l_out][l_in];
+ *  - gate 0 is applied first (nearest the input); C = G_{K-1} ... G_0;
+ *  - states are row-major [row][2^n]; gates [start][gate][4][4].
+ *
+ * Ownership: the caller owns every host buffer; qfs_set_samples COPIES its
+ * inputs (the caller may free them on return); the context owns all device
+ * memory until qfs_destroy.  A context is not thread-safe; distinct contexts
+ * are independent.  Errors are status codes only (no exceptions or exit cross
+ * the ABI); qfs_last_error(ctx) returns the message of the last failure.
+ */
+#ifndef QFS_H
+#define QFS_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct qfs_ctx qfs_ctx; /* opaque; owns all device memory */
+
+typedef enum {
+  QFS_OK = 0,
+  QFS_ERR_ARG = 1,      /* n < 2, p0 == p1, p >= n, k < 1, null pointer, bad count */
+  QFS_ERR_CAPACITY = 2, /* m_init > m_pool, m_pool > 2^n, memory plan exceeds the device,
+                           M not divisible by world in sample mode */
+  QFS_ERR_NUMERIC = 3,  /* non-finite input, or initial gate not unitary (||G^dag G - I||_max > 1e-10) */
+  QFS_ERR_DEVICE = 4,   /* CUDA / NCCL failure (message in qfs_last_error) */
+  QFS_ERR_STATE = 5     /* instantiate / trace before set_samples */
+} qfs_status;
+
+typedef enum {
+  QFS_CONVERGED = 0,      /* c_train <= dist_tol and generalisation check passed  */
+  QFS_PLATEAU = 1,        /* plateau_window consecutive non-improving sweeps */
+  QFS_MAX_ITER = 2,       /* total sweeps reached max_iter                      */
+  QFS_POOL_EXHAUSTED = 3, /* overtrain needed 2M rows but the pool is smaller (M < 2^n)  */
+  QFS_STOPPED = 4         /* stop_on_first: another start converged first                */
+} qfs_term;
+
+/* Hyperparameters of PAPER.md App. A. */
+typedef struct {
+  double dist_tol;        /* converged when c_train <= dist_tol (R8)             */
+  double diff_tol_r;      /* plateau: |c_prev| - |c| > diff_tol_r |c| is progress */
+  int plateau_window;     /* consecutive failures before PLATEAU; <= 0 disables */
+  int min_iter;           /* no PLATEAU / overtrain stop before it (R9)          */
+  int max_iter;           /* total sweeps across restarts                       */
+  int m_init;             /* number_of_training_states                          */
+  double overtrain_ratio; /* restart with 2M when c_val/c_train - 1 > otr;
+                             +INFINITY disables the generalisation check                */
+  double beta;            /* SVD of (1-beta) E + beta u^dag                 */
+  int stop_on_first;      /* 1: stop all starts at the first sweep where one converged  */
+} qfs_params;
+
+typedef struct {
+  double c_train, c_val; /* last training cost (direct form; R6) and validation cost */
+  int sweeps, restarts, final_m;
+  qfs_term term;
+} qfs_result;
+
+/* Create a context for an n-qubit circuit of k two-qubit blocks.
+ * pairs: host int32 [k][2] (ordered qubit pairs; p0 != p1, both < n).
+ * device: CUDA ordinal.  Structure only; no target. */
+qfs_status qfs_create(int n, int k, const int32_t *pairs, int device, qfs_ctx **out);
+
+/* Distributed context.  nccl_comm: an ncclComm_t whose rank
+ * and size equal (rank, world) (e.g. ProcessGroupNCCL._comm_ptr()), or NULL
+ * when world == 1.  shard_mode 0 = multistart (each rank runs its own starts,
+ * no data-path collective); 1 = sample (each rank holds rows m = rank mod world
+ * of the pool, passed LOCALLY to set_samples; partial environments and cost
+ * sums are all-reduced per gate / per sweep over NCCL). */
+qfs_status qfs_create_dist(int n, int k, const int32_t *pairs, int device, void *nccl_comm,
+                           int rank, int world, int shard_mode, qfs_ctx **out);
+
+/* Training pool x, targets y = U x (the A tensor) [m_pool][2^n][2], and
+ * validation states xv, yv = U xv [v][2^n][2] (v may be 0).  Host
+ * pointers; copied.  Training set = the first M rows of the pool; doubling
+ * takes the first 2M rows (prefix-nested, R13).  Rows should be orthonormal
+ * Haar states; this is documented, not checked. */
+qfs_status qfs_set_samples(qfs_ctx *c, int m_pool, const double *x, const double *y, int v,
+                           const double *xv, const double *yv);
+
+/* Same, from DEVICE pointers (e.g. torch CUDA tensors) on cuda_stream
+ * (cudaStream_t, NULL = legacy default stream).  Copies device-to-device. */
+qfs_status qfs_set_samples_device(qfs_ctx *c, int m_pool, const void *dx, const void *dy, int v,
+                                  const void *dxv, const void *dyv, void *cuda_stream);
+
+/* Instantiate from s starts in lockstep (P:378 multistarts): init_gates host
+ * [s][k][4][4][2]; out_gates host [s][k][4][4][2]; out host [s]; *winner = the
+ * lowest-index start converged at the earliest converging sweep, else the
+ * minimum c_train start (ties: lower index). */
+qfs_status qfs_instantiate(qfs_ctx *c, int s, const double *init_gates, const qfs_params *p,
+                           double *out_gates, qfs_result *out, int *winner);
+
+/* Parity / debug: n_sweeps sweeps at fixed M for s starts, no controller.
+ * Any trace pointer may be NULL.  Layouts (host):
+ *   env_trace   [n_sweeps][k][s][4][4][2]  environment E_i of gate i in sweep t
+ *   gate_trace  [n_sweeps][s][k][4][4][2]  gates after sweep t
+ *   cost_trace  [n_sweeps][s]              c_train after sweep t
+ *   sigma_trace [n_sweeps][k][s]           sum of singular values of E'_i */
+qfs_status qfs_trace_sweeps(qfs_ctx *c, int s, const double *init_gates, int m, double beta,
+                            int n_sweeps, double *env_trace, double *gate_trace,
+                            double *cost_trace, double *sigma_trace);
+
+/* Throughput: exactly n_sweeps sweeps at fixed M for all s starts (no
+ * controller, no validation); *sec = elapsed seconds from CUDA events. */
+qfs_status qfs_bench_sweeps(qfs_ctx *c, int s, const double *init_gates, int m, int n_sweeps,
+                            double *sec);
+
+/* Kernel-level entry points (unit tests of each kernel against the oracle).
+ * All host pointers; each call copies in, runs ONE kernel launch, copies out. */
+/* psi [m][2^n][2] in place: psi <- G psi (dagger: G^dag psi) on (p0, p1). */
+qfs_status qfs_op_apply(qfs_ctx *c, int p0, int p1, const double *g, int dagger, int m,
+                        double *psi);
+/* env [4][4][2] = sum_m sum_r phi[idx(l_in)] conj(chi[idx(l_out)]). */
+qfs_status qfs_op_environment(qfs_ctx *c, int p0, int p1, int m, const double *phi,
+                              const double *chi, double *env);
+/* batch polar update: g_new[i] = Y X^dag of SVD((1-beta) env[i] + beta g_old[i]^dag),
+ * sigma_sum[i] = sum of singular values; env, g_old, g_new [count][4][4][2]. */
+qfs_status qfs_op_polar(qfs_ctx *c, int count, const double *env, const double *g_old,
+                        double beta, double *g_new, double *sigma_sum);
+
+/* Profiling: when enabled, every kernel launch is bracketed by CUDA events on
+ * the library's stream and accumulated per kernel class.  qfs_profile_read
+ * fills up to cap entries: names (static strings), launches, total ms,
+ * algorithmic bytes and flops; returns the number of classes in *count. */
+qfs_status qfs_profile_enable(qfs_ctx *c, int on);
+qfs_status qfs_profile_read(qfs_ctx *c, int cap, const char **names, long long *launches,
+                            double *ms, double *bytes, double *flops, int *count);
+
+/* Number of kernel launches issued since the context was created. */
+long long qfs_launch_count(const qfs_ctx *c);
+/* The library's CUDA stream (cudaStream_t) — for callers that order work. */
+void *qfs_stream(const qfs_ctx *c);
+
+const char *qfs_last_error(const qfs_ctx *c);
+void qfs_destroy(qfs_ctx *c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

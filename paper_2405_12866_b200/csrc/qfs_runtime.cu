@@ -1,0 +1,898 @@
+// qfs_runtime.cu — context, device memory plan, sweep driver, host controller
+// and the C ABI of libqfs.so (include/qfs.h).
+//
+// The sweep driver issues, per sweep:
+//   forward (B cache)  -> K fused backward launches (chi update + E_i + polar)
+//   -> final cost launch -> validation forward (when requested)
+// on one CUDA stream, captured once into a CUDA graph per launch shape.  The
+// host controller reads the S
+// costs per sweep (a few bytes) and decides convergence, plateau, overtrain
+// double-and-restart, max_iter, stop_on_first.  No CPU fallback exists: every
+// arithmetic step of the sweep runs in qfs_kernels.cu.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/qfs.h"
+#include "qfs_internal.h"
+
+using namespace qfs;
+
+namespace {
+
+enum KClass { K_FWD_ROW = 0, K_FWD_GATE, K_BWD, K_POLAR, K_FINAL, K_VAL_ROW, K_DIST, K_REDUCE,
+              K_NCCL, K_OP, K_NCLASS };
+const char *kClassName[K_NCLASS] = {"fwd_row", "fwd_gate", "bwd", "polar", "final",
+                                    "val_row", "dist", "row_reduce", "nccl_allreduce", "unit_op"};
+
+struct ProfRec {
+  int cls;
+  cudaEvent_t e0, e1;
+  double bytes, flops;
+};
+
+}  // namespace
+
+struct qfs_ctx {
+  int n = 0, K = 0, device = 0;
+  long long N = 0;
+  std::vector<int32_t> pairs;
+  int2 *d_pairs = nullptr;
+  cudaStream_t st = nullptr;
+  // distribution
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1, mode = 0;
+  int *d_flag = nullptr;
+  // samples
+  int m_pool = 0, V = 0;
+  bool have_samples = false;
+  double2 *d_x = nullptr, *d_y = nullptr, *d_xv = nullptr, *d_yv = nullptr;
+  // work buffers
+  int G_cap = 0, S_cap = 0, M_cap = 0, V_cap = 0, nb_cap = 0;
+  double2 *d_gates = nullptr, *d_chi = nullptr, *d_B = nullptr, *d_vb0 = nullptr, *d_vb1 = nullptr;
+  double *d_partials = nullptr, *d_ered = nullptr, *d_sig = nullptr, *d_csum = nullptr,
+         *d_rowout = nullptr, *d_cval = nullptr;
+  unsigned *d_counters = nullptr;
+  Slot *d_slots = nullptr;
+  double *h_csum = nullptr, *h_cval = nullptr;  // pinned
+  double2 *d_env_trace = nullptr;
+  size_t env_trace_cap = 0;
+  // graph cache
+  cudaGraphExec_t gexec = nullptr;
+  long long gkey[8] = {0};
+  long long glaunches = 0;
+  // profiling
+  bool prof = false;
+  std::vector<ProfRec> prec;
+  std::vector<cudaEvent_t> ev_pool;
+  double p_ms[K_NCLASS] = {0}, p_bytes[K_NCLASS] = {0}, p_flops[K_NCLASS] = {0};
+  long long p_cnt[K_NCLASS] = {0};
+  long long launches = 0;
+  std::string err;
+};
+
+namespace {
+
+qfs_status fail(qfs_ctx *c, qfs_status s, const std::string &msg) {
+  if (c) c->err = msg;
+  return s;
+}
+
+#define CUDA_TRY(c, expr)                                                                   \
+  do {                                                                                      \
+    cudaError_t e_ = (expr);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail(c, QFS_ERR_DEVICE, std::string(#expr " failed: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define NCCL_TRY(c, expr)                                                                   \
+  do {                                                                                      \
+    ncclResult_t r_ = (expr);                                                               \
+    if (r_ != ncclSuccess)                                                                  \
+      return fail(c, QFS_ERR_DEVICE, std::string(#expr " failed: ") + ncclGetErrorString(r_)); \
+  } while (0)
+
+template <typename T>
+void dfree(T *&p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+// ---- profiling helpers: bracket a launch with events on the library stream
+cudaEvent_t take_event(qfs_ctx *c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+struct LaunchScope {
+  qfs_ctx *c;
+  int cls;
+  double bytes, flops;
+  cudaEvent_t e0 = nullptr;
+  LaunchScope(qfs_ctx *c_, int cls_, double b, double f) : c(c_), cls(cls_), bytes(b), flops(f) {
+    c->launches++;
+    if (c->prof) {
+      e0 = take_event(c);
+      cudaEventRecord(e0, c->st);
+    }
+  }
+  ~LaunchScope() {
+    if (c->prof) {
+      cudaEvent_t e1 = take_event(c);
+      cudaEventRecord(e1, c->st);
+      c->prec.push_back({cls, e0, e1, bytes, flops});
+    }
+  }
+};
+
+void prof_collect(qfs_ctx *c) {
+  if (c->prec.empty()) return;
+  cudaStreamSynchronize(c->st);
+  for (auto &r : c->prec) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, r.e0, r.e1);
+    c->p_ms[r.cls] += ms;
+    c->p_cnt[r.cls] += 1;
+    c->p_bytes[r.cls] += r.bytes;
+    c->p_flops[r.cls] += r.flops;
+    c->ev_pool.push_back(r.e0);
+    c->ev_pool.push_back(r.e1);
+  }
+  c->prec.clear();
+}
+
+bool finite_all(const double *p, size_t cnt) {
+  for (size_t i = 0; i < cnt; ++i)
+    if (!std::isfinite(p[i])) return false;
+  return true;
+}
+
+// initial gates must be unitary (||G^dag G - I||_max <= 1e-10)
+bool unitary_all(const double *g, size_t count) {
+  for (size_t q = 0; q < count; ++q) {
+    const double *G = g + q * 32;
+    for (int a = 0; a < 4; ++a)
+      for (int b = 0; b < 4; ++b) {
+        double re = 0, im = 0;
+        for (int r = 0; r < 4; ++r) {
+          double ar = G[2 * (4 * r + a)], ai = -G[2 * (4 * r + a) + 1];  // conj(G[r][a])
+          double br = G[2 * (4 * r + b)], bi = G[2 * (4 * r + b) + 1];
+          re += ar * br - ai * bi;
+          im += ar * bi + ai * br;
+        }
+        if (std::fabs(re - (a == b ? 1.0 : 0.0)) > 1e-10 || std::fabs(im) > 1e-10) return false;
+      }
+  }
+  return true;
+}
+
+int blocks_per_start(long long items, int n_slots) {
+  const int target = 148 * 4;
+  long long nb = (target + n_slots - 1) / n_slots;
+  long long maxnb = (items + 255) / 256;
+  if (nb > maxnb) nb = maxnb;
+  if (nb < 1) nb = 1;
+  return (int)nb;
+}
+
+// memory plan (bytes) for S starts, M_cap rows per start, V validation rows
+size_t plan_bytes(const qfs_ctx *c, int S, int M, int V, int nb) {
+  size_t N = (size_t)c->N;
+  size_t b = 0;
+  b += (size_t)S * M * N * 16;                             // chi
+  if (c->K > 1) b += (size_t)(c->K - 1) * S * M * N * 16;  // B cache
+  if (c->n > fwd_row_max_n() && V > 0) b += 2 * (size_t)S * V * N * 16;
+  b += (size_t)S * nb * 32 * 8 + (size_t)S * 64 * 8 + (size_t)S * c->K * 8 + (size_t)S * (V + 4) * 8;
+  return b;
+}
+
+qfs_status ensure_gates(qfs_ctx *c, int S) {
+  if (S <= c->G_cap) return QFS_OK;
+  dfree(c->d_gates);
+  c->G_cap = 0;
+  CUDA_TRY(c, cudaMalloc(&c->d_gates, (size_t)S * c->K * 16 * sizeof(double2)));
+  c->G_cap = S;
+  if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+  return QFS_OK;
+}
+
+// Per-sweep state (chi, B cache, validation buffers, reduction scratch) for S
+// starts of up to M local rows.  Contents are rebuilt every sweep, so growing
+// (on a double-and-restart) may discard them; the gates live elsewhere.
+qfs_status ensure_state(qfs_ctx *c, int S, int M, int V) {
+  const int nb = blocks_per_start(((long long)M * c->N) >> 2, 1);
+  if (S <= c->S_cap && M <= c->M_cap && V <= c->V_cap && nb <= c->nb_cap) return QFS_OK;
+  S = std::max(S, c->S_cap);
+  M = std::max(M, c->M_cap);
+  V = std::max(V, c->V_cap);
+  const int nbc = std::max(nb, c->nb_cap);
+  CUDA_TRY(c, cudaStreamSynchronize(c->st));
+  dfree(c->d_chi); dfree(c->d_B); dfree(c->d_vb0); dfree(c->d_vb1);
+  dfree(c->d_partials); dfree(c->d_ered); dfree(c->d_sig); dfree(c->d_csum); dfree(c->d_rowout);
+  dfree(c->d_cval); dfree(c->d_counters); dfree(c->d_slots);
+  if (c->h_csum) cudaFreeHost(c->h_csum);
+  if (c->h_cval) cudaFreeHost(c->h_cval);
+  c->h_csum = c->h_cval = nullptr;
+  c->S_cap = c->M_cap = c->V_cap = c->nb_cap = 0;
+  if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+  size_t need = plan_bytes(c, S, M, V, nbc);
+  size_t fr = 0, tot = 0;
+  CUDA_TRY(c, cudaMemGetInfo(&fr, &tot));
+  if (need + (256ull << 20) > fr) {
+    char buf[256];
+    snprintf(buf, sizeof buf, "memory plan %.2f GB exceeds free device memory %.2f GB (S=%d M=%d)",
+             need / 1e9, fr / 1e9, S, M);
+    return fail(c, QFS_ERR_CAPACITY, buf);
+  }
+  const size_t N = (size_t)c->N;
+  CUDA_TRY(c, cudaMalloc(&c->d_chi, (size_t)S * M * N * sizeof(double2)));
+  if (c->K > 1) CUDA_TRY(c, cudaMalloc(&c->d_B, (size_t)(c->K - 1) * S * M * N * sizeof(double2)));
+  if (c->n > fwd_row_max_n() && V > 0) {
+    CUDA_TRY(c, cudaMalloc(&c->d_vb0, (size_t)S * V * N * sizeof(double2)));
+    CUDA_TRY(c, cudaMalloc(&c->d_vb1, (size_t)S * V * N * sizeof(double2)));
+  }
+  CUDA_TRY(c, cudaMalloc(&c->d_partials, (size_t)S * nbc * 32 * sizeof(double)));
+  CUDA_TRY(c, cudaMalloc(&c->d_ered, (size_t)S * 32 * sizeof(double)));
+  CUDA_TRY(c, cudaMalloc(&c->d_sig, (size_t)S * c->K * sizeof(double)));
+  CUDA_TRY(c, cudaMalloc(&c->d_csum, (size_t)S * sizeof(double)));
+  CUDA_TRY(c, cudaMalloc(&c->d_cval, (size_t)S * sizeof(double)));
+  CUDA_TRY(c, cudaMalloc(&c->d_rowout, (size_t)S * std::max(V, 1) * sizeof(double)));
+  CUDA_TRY(c, cudaMalloc(&c->d_counters, (size_t)S * 2 * sizeof(unsigned)));
+  CUDA_TRY(c, cudaMemset(c->d_counters, 0, (size_t)S * 2 * sizeof(unsigned)));
+  CUDA_TRY(c, cudaMalloc(&c->d_slots, (size_t)S * sizeof(Slot)));
+  CUDA_TRY(c, cudaMallocHost(&c->h_csum, (size_t)S * sizeof(double)));
+  CUDA_TRY(c, cudaMallocHost(&c->h_cval, (size_t)S * sizeof(double)));
+  c->S_cap = S; c->M_cap = M; c->V_cap = V; c->nb_cap = nbc;
+  return QFS_OK;
+}
+
+// ---------------------------------------------------------------- sweep ----
+struct SweepSpec {
+  std::vector<Slot> slots;   // active starts (local rows per start)
+  int M_max = 0;
+  bool want_val = false;
+  double beta = 0.0;
+  double2 *env_trace = nullptr;  // device [K][S][16] or nullptr
+  int S = 0;                     // total starts (trace layout / strides)
+};
+
+// Issue one sweep's launches on c->st (no host synchronisation).
+qfs_status issue_sweep(qfs_ctx *c, const SweepSpec &sp) {
+  const int ns = (int)sp.slots.size();
+  const int K = c->K, n = c->n;
+  const long long N = c->N;
+  const long long Mc = c->M_cap;
+  const Rows xpool{c->d_x, 0}, ypool{c->d_y, 0};
+  double units = 0;  // amplitudes of all active training rows
+  for (auto &s : sp.slots) units += (double)s.m * (double)N;
+  // (a) forward: B_1 .. B_{K-1}
+  if (K > 1) {
+    if (n <= fwd_row_max_n()) {
+      FwdRowParams f{};
+      f.n = n; f.K = K; f.mode = 0; f.rows = 0; f.slots = c->d_slots; f.pairs = c->d_pairs;
+      f.gates = c->d_gates; f.src = xpool; f.B = c->d_B;
+      f.b_gate_stride = (long long)c->S_cap * Mc * N; f.b_stride_s = Mc;
+      LaunchScope ls(c, K_FWD_ROW, units * (16.0 + 16.0 * (K - 1)), units * 32.0 * (K - 1));
+      CUDA_TRY(c, launch_fwd_row(f, ns, sp.M_max, c->st));
+    } else {
+      for (int k = 0; k + 1 < K; ++k) {
+        FwdGateParams f{};
+        f.n = n; f.k = k; f.K = K; f.rows_fixed = 0; f.slots = c->d_slots;
+        f.p0 = c->pairs[2 * k]; f.p1 = c->pairs[2 * k + 1]; f.gates = c->d_gates;
+        f.nb = blocks_per_start(((long long)sp.M_max * N) >> 2, ns);
+        f.src = k == 0 ? xpool : Rows{c->d_B + (long long)(k - 1) * c->S_cap * Mc * N, Mc};
+        f.dst = RowsW{c->d_B + (long long)k * c->S_cap * Mc * N, Mc};
+        LaunchScope ls(c, K_FWD_GATE, units * 32.0, units * 32.0);
+        CUDA_TRY(c, launch_fwd_gate(f, ns, c->st));
+      }
+    }
+  }
+  // (b, c) backward: gate i = K-1 .. 0 (P:112 right to left; Fig. env_calc)
+  for (int i = K - 1; i >= 0; --i) {
+    BwdParams b{};
+    b.n = n; b.K = K; b.slots = c->d_slots; b.gates = c->d_gates; b.gates_w = c->d_gates;
+    b.partials = c->d_partials; b.counters = c->d_counters; b.e_red = c->d_ered;
+    b.fuse_polar = (c->mode == 1 && c->world > 1) ? 0 : 1;
+    b.beta = sp.beta; b.sig = c->d_sig; b.env_trace = sp.env_trace; b.S = sp.S;
+    const bool upd = i < K - 1;
+    b.upd_gate = upd ? i + 1 : -1;
+    b.env_gate = i;
+    const int p0 = c->pairs[2 * i], p1 = c->pairs[2 * i + 1];
+    int loc[4], nu;
+    if (!upd) {
+      loc[0] = p0; loc[1] = p1; nu = 2;
+    } else {
+      loc[0] = c->pairs[2 * (i + 1)]; loc[1] = c->pairs[2 * (i + 1) + 1]; nu = 2;
+      int ex[2], ne = 0;
+      for (int q : {p0, p1})
+        if (q != loc[0] && q != loc[1]) ex[ne++] = q;
+      if (ne == 2 && ex[0] > ex[1]) std::swap(ex[0], ex[1]);
+      for (int t = 0; t < ne; ++t) loc[nu++] = ex[t];
+    }
+    int tp0 = -1, tp1 = -1;
+    for (int t = 0; t < nu; ++t) {
+      if (loc[t] == p0) tp0 = t;
+      if (loc[t] == p1) tp1 = t;
+    }
+    b.nu = nu;
+    int srt[4];
+    for (int t = 0; t < nu; ++t) srt[t] = loc[t];
+    std::sort(srt, srt + nu);
+    for (int t = 0; t < 4; ++t) b.ins[t] = t < nu ? srt[t] : 0;
+    for (int v = 0; v < 16; ++v) {
+      long long o = 0;
+      for (int t = 0; t < nu; ++t)
+        if ((v >> t) & 1) o |= 1LL << loc[t];
+      b.off[v] = v < (1 << nu) ? o : 0;
+    }
+    b.chi_src = (i >= K - 2) ? ypool : Rows{c->d_chi, Mc};
+    b.chi_dst = upd ? RowsW{c->d_chi, Mc} : RowsW{nullptr, 0};
+    b.phi = i == 0 ? xpool : Rows{c->d_B + (long long)(i - 1) * c->S_cap * Mc * N, Mc};
+    b.nb = blocks_per_start(((long long)sp.M_max * N) >> nu, ns);
+    {
+      LaunchScope ls(c, K_BWD, units * (upd ? 48.0 : 32.0), units * (upd ? 64.0 : 32.0));
+      CUDA_TRY(c, launch_bwd(b, ns, tp0, tp1, upd, c->st));
+    }
+    if (!b.fuse_polar) {
+      {
+        LaunchScope ls(c, K_NCCL, 0, 0);
+        NCCL_TRY(c, ncclAllReduce(c->d_ered, c->d_ered, (size_t)ns * 32, ncclFloat64, ncclSum,
+                                  c->comm, c->st));
+      }
+      PolarParams pp{};
+      pp.K = K; pp.gate = i; pp.S = sp.S; pp.n_slots = ns; pp.slots = c->d_slots;
+      pp.e_red = c->d_ered; pp.gates = c->d_gates; pp.beta = sp.beta; pp.sig = c->d_sig;
+      pp.env_trace = sp.env_trace;
+      LaunchScope ls(c, K_POLAR, 0, 0);
+      CUDA_TRY(c, launch_polar(pp, ns, c->st));
+    }
+  }
+  // (d) c_train = (1/M) sum ||G_0^dag chi - x||^2   (direct form R6)
+  {
+    FinalParams fp{};
+    fp.n = n; fp.slots = c->d_slots;
+    fp.chi = K == 1 ? ypool : Rows{c->d_chi, Mc};
+    fp.x = xpool; fp.p0 = c->pairs[0]; fp.p1 = c->pairs[1]; fp.gates = c->d_gates; fp.K = K;
+    fp.partials = c->d_partials; fp.counters = c->d_counters + c->S_cap; fp.out_sum = c->d_csum;
+    fp.nb = blocks_per_start(((long long)sp.M_max * N) >> 2, ns);
+    LaunchScope ls(c, K_FINAL, units * 32.0, units * 35.0);
+    CUDA_TRY(c, launch_final(fp, ns, c->st));
+  }
+  if (c->mode == 1 && c->world > 1) {
+    LaunchScope ls(c, K_NCCL, 0, 0);
+    NCCL_TRY(c, ncclAllReduce(c->d_csum, c->d_csum, ns, ncclFloat64, ncclSum, c->comm, c->st));
+  }
+  // validation cost with the post-sweep gates
+  if (sp.want_val && c->V > 0) {
+    const double vunits = (double)ns * c->V * (double)N;
+    if (n <= fwd_row_max_n()) {
+      FwdRowParams f{};
+      f.n = n; f.K = K; f.mode = 1; f.rows = c->V; f.slots = c->d_slots; f.pairs = c->d_pairs;
+      f.gates = c->d_gates; f.src = Rows{c->d_xv, 0}; f.ref = Rows{c->d_yv, 0};
+      f.row_out = c->d_rowout;
+      LaunchScope ls(c, K_VAL_ROW, vunits * 32.0, vunits * 32.0 * K);
+      CUDA_TRY(c, launch_fwd_row(f, ns, c->V, c->st));
+    } else {
+      for (int k = 0; k < K; ++k) {
+        FwdGateParams f{};
+        f.n = n; f.k = k; f.K = K; f.rows_fixed = c->V; f.slots = c->d_slots;
+        f.p0 = c->pairs[2 * k]; f.p1 = c->pairs[2 * k + 1]; f.gates = c->d_gates;
+        f.nb = blocks_per_start(((long long)c->V * N) >> 2, ns);
+        double2 *dst = (k & 1) ? c->d_vb1 : c->d_vb0;
+        const double2 *src = k == 0 ? c->d_xv : ((k & 1) ? c->d_vb0 : c->d_vb1);
+        f.src = Rows{src, k == 0 ? 0 : (long long)c->V};
+        f.dst = RowsW{dst, (long long)c->V};
+        LaunchScope ls(c, K_FWD_GATE, vunits * 32.0, vunits * 32.0);
+        CUDA_TRY(c, launch_fwd_gate(f, ns, c->st));
+      }
+      DistParams d{};
+      d.n = n; d.rows = c->V; d.slots = c->d_slots;
+      d.a = Rows{((K - 1) & 1) ? c->d_vb1 : c->d_vb0, (long long)c->V};
+      d.b = Rows{c->d_yv, 0}; d.row_out = c->d_rowout;
+      LaunchScope ls(c, K_DIST, vunits * 32.0, vunits * 3.0);
+      CUDA_TRY(c, launch_dist(d, ns, c->st));
+    }
+    LaunchScope ls(c, K_REDUCE, 0, 0);
+    CUDA_TRY(c, launch_row_reduce(c->d_rowout, c->V, c->d_cval, ns, c->st));
+  }
+  return QFS_OK;
+}
+
+// Run one sweep: upload the slot table, issue (graph-captured when not
+// profiling and not tracing), and copy the per-start cost sums back.
+qfs_status run_sweep(qfs_ctx *c, const SweepSpec &sp, std::vector<double> &csum,
+                     std::vector<double> &cval) {
+  const int ns = (int)sp.slots.size();
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_slots, sp.slots.data(), ns * sizeof(Slot),
+                              cudaMemcpyHostToDevice, c->st));
+  const bool use_graph = !c->prof && sp.env_trace == nullptr;
+  if (use_graph) {
+    long long key[8] = {ns, sp.M_max, sp.want_val, (long long)(sp.beta * 1e15), sp.S, c->S_cap,
+                        c->M_cap, 1};
+    if (!c->gexec || std::memcmp(key, c->gkey, sizeof key) != 0) {
+      if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+      cudaGraph_t g;
+      CUDA_TRY(c, cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+      long long before = c->launches;
+      qfs_status s = issue_sweep(c, sp);
+      cudaError_t e = cudaStreamEndCapture(c->st, &g);
+      if (s != QFS_OK) return s;
+      if (e != cudaSuccess) return fail(c, QFS_ERR_DEVICE, std::string("graph capture: ") + cudaGetErrorString(e));
+      CUDA_TRY(c, cudaGraphInstantiate(&c->gexec, g, 0));
+      cudaGraphDestroy(g);
+      std::memcpy(c->gkey, key, sizeof key);
+      c->glaunches = c->launches - before;
+      c->launches = before;
+    }
+    CUDA_TRY(c, cudaGraphLaunch(c->gexec, c->st));
+    c->launches += c->glaunches;
+  } else {
+    qfs_status s = issue_sweep(c, sp);
+    if (s != QFS_OK) return s;
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(c->h_csum, c->d_csum, ns * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  if (sp.want_val && c->V > 0)
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_cval, c->d_cval, ns * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(c, cudaStreamSynchronize(c->st));
+  csum.assign(c->h_csum, c->h_csum + ns);
+  if (sp.want_val && c->V > 0) cval.assign(c->h_cval, c->h_cval + ns);
+  else cval.assign(ns, NAN);
+  if (c->prof) prof_collect(c);
+  return QFS_OK;
+}
+
+qfs_status upload_gates(qfs_ctx *c, int s, const double *init) {
+  if (!finite_all(init, (size_t)s * c->K * 32)) return fail(c, QFS_ERR_NUMERIC, "non-finite initial gate");
+  if (!unitary_all(init, (size_t)s * c->K)) return fail(c, QFS_ERR_NUMERIC, "initial gate not unitary (tol 1e-10)");
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_gates, init, (size_t)s * c->K * 16 * sizeof(double2),
+                              cudaMemcpyHostToDevice, c->st));
+  return QFS_OK;
+}
+
+qfs_status check_ready(qfs_ctx *c, int s) {
+  if (!c) return QFS_ERR_ARG;
+  if (!c->have_samples) return fail(c, QFS_ERR_STATE, "set_samples has not been called");
+  if (s < 1) return fail(c, QFS_ERR_ARG, "s must be >= 1");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  return QFS_OK;
+}
+
+qfs_status create_common(int n, int k, const int32_t *pairs, int device, qfs_ctx **out) {
+  if (!out) return QFS_ERR_ARG;
+  *out = nullptr;
+  if (n < 2 || n > 26 || k < 1 || !pairs) return QFS_ERR_ARG;
+  for (int i = 0; i < k; ++i) {
+    int a = pairs[2 * i], b = pairs[2 * i + 1];
+    if (a < 0 || b < 0 || a >= n || b >= n || a == b) return QFS_ERR_ARG;
+  }
+  qfs_ctx *c = new qfs_ctx();
+  c->n = n; c->K = k; c->N = 1LL << n; c->device = device;
+  c->pairs.assign(pairs, pairs + 2 * k);
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_pairs, k * sizeof(int2));
+  if (e == cudaSuccess) e = cudaMemcpy(c->d_pairs, pairs, k * sizeof(int2), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_flag, 4 * sizeof(int));
+  if (e != cudaSuccess) {
+    c->err = std::string("device init: ") + cudaGetErrorString(e);
+    *out = c;  // caller can read the error, then destroy
+    return QFS_ERR_DEVICE;
+  }
+  *out = c;
+  return QFS_OK;
+}
+
+}  // namespace
+
+// ======================================================================= ABI ==
+extern "C" {
+
+qfs_status qfs_create(int n, int k, const int32_t *pairs, int device, qfs_ctx **out) {
+  return create_common(n, k, pairs, device, out);
+}
+
+qfs_status qfs_create_dist(int n, int k, const int32_t *pairs, int device, void *nccl_comm,
+                           int rank, int world, int shard_mode, qfs_ctx **out) {
+  if (world < 1 || rank < 0 || rank >= world || (shard_mode != 0 && shard_mode != 1) ||
+      (world > 1 && !nccl_comm))
+    return QFS_ERR_ARG;
+  qfs_status s = create_common(n, k, pairs, device, out);
+  if (s != QFS_OK) return s;
+  qfs_ctx *c = *out;
+  c->comm = (ncclComm_t)nccl_comm;
+  c->rank = rank; c->world = world; c->mode = shard_mode;
+  if (c->comm) {
+    int cr = -1, cn = -1;
+    if (ncclCommUserRank(c->comm, &cr) != ncclSuccess || ncclCommCount(c->comm, &cn) != ncclSuccess ||
+        cr != rank || cn != world)
+      return fail(c, QFS_ERR_ARG, "nccl communicator rank/size mismatch");
+  }
+  return QFS_OK;
+}
+
+static qfs_status set_samples_impl(qfs_ctx *c, int m_pool, const void *x, const void *y, int v,
+                                   const void *xv, const void *yv, cudaMemcpyKind kind,
+                                   cudaStream_t ust) {
+  if (!c) return QFS_ERR_ARG;
+  if (m_pool < 1 || !x || !y || v < 0 || (v > 0 && (!xv || !yv)))
+    return fail(c, QFS_ERR_ARG, "bad sample arguments");
+  if ((long long)m_pool * (c->mode == 1 ? c->world : 1) > c->N)
+    return fail(c, QFS_ERR_CAPACITY, "m_pool > 2^n");
+  if (kind == cudaMemcpyHostToDevice) {
+    if (!finite_all((const double *)x, (size_t)m_pool * c->N * 2) ||
+        !finite_all((const double *)y, (size_t)m_pool * c->N * 2) ||
+        (v > 0 && (!finite_all((const double *)xv, (size_t)v * c->N * 2) ||
+                   !finite_all((const double *)yv, (size_t)v * c->N * 2))))
+      return fail(c, QFS_ERR_NUMERIC, "non-finite sample");
+  }
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  if (m_pool != c->m_pool) {
+    dfree(c->d_x); dfree(c->d_y);
+    CUDA_TRY(c, cudaMalloc(&c->d_x, (size_t)m_pool * c->N * sizeof(double2)));
+    CUDA_TRY(c, cudaMalloc(&c->d_y, (size_t)m_pool * c->N * sizeof(double2)));
+  }
+  if (v != c->V) {
+    dfree(c->d_xv); dfree(c->d_yv);
+    if (v > 0) {
+      CUDA_TRY(c, cudaMalloc(&c->d_xv, (size_t)v * c->N * sizeof(double2)));
+      CUDA_TRY(c, cudaMalloc(&c->d_yv, (size_t)v * c->N * sizeof(double2)));
+    }
+  }
+  cudaStream_t st = kind == cudaMemcpyHostToDevice ? c->st : ust;
+  const size_t rb = (size_t)c->N * sizeof(double2);
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_x, x, m_pool * rb, kind, st));
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_y, y, m_pool * rb, kind, st));
+  if (v > 0) {
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_xv, xv, v * rb, kind, st));
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_yv, yv, v * rb, kind, st));
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(st));
+  c->m_pool = m_pool; c->V = v; c->have_samples = true;
+  if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+  return QFS_OK;
+}
+
+qfs_status qfs_set_samples(qfs_ctx *c, int m_pool, const double *x, const double *y, int v,
+                           const double *xv, const double *yv) {
+  return set_samples_impl(c, m_pool, x, y, v, xv, yv, cudaMemcpyHostToDevice, nullptr);
+}
+
+qfs_status qfs_set_samples_device(qfs_ctx *c, int m_pool, const void *dx, const void *dy, int v,
+                                  const void *dxv, const void *dyv, void *cuda_stream) {
+  return set_samples_impl(c, m_pool, dx, dy, v, dxv, dyv, cudaMemcpyDeviceToDevice,
+                          (cudaStream_t)cuda_stream);
+}
+
+qfs_status qfs_trace_sweeps(qfs_ctx *c, int s, const double *init_gates, int m, double beta,
+                            int n_sweeps, double *env_trace, double *gate_trace,
+                            double *cost_trace, double *sigma_trace) {
+  qfs_status st = check_ready(c, s);
+  if (st != QFS_OK) return st;
+  if (!init_gates || n_sweeps < 0) return fail(c, QFS_ERR_ARG, "bad trace arguments");
+  const int wm = c->mode == 1 ? c->world : 1;
+  if (m < 1 || m % wm != 0) return fail(c, QFS_ERR_CAPACITY, "M must be >= 1 and divisible by world");
+  const int ml = m / wm;
+  if (ml > c->m_pool) return fail(c, QFS_ERR_CAPACITY, "M exceeds the pool");
+  if ((st = ensure_gates(c, s)) != QFS_OK) return st;
+  if ((st = ensure_state(c, s, ml, c->V)) != QFS_OK) return st;
+  if ((st = upload_gates(c, s, init_gates)) != QFS_OK) return st;
+  const size_t tr = (size_t)c->K * s * 16;
+  if (env_trace && tr > c->env_trace_cap) {
+    dfree(c->d_env_trace);
+    CUDA_TRY(c, cudaMalloc(&c->d_env_trace, tr * sizeof(double2)));
+    c->env_trace_cap = tr;
+  }
+  SweepSpec sp;
+  for (int q = 0; q < s; ++q) sp.slots.push_back({q, ml});
+  sp.M_max = ml; sp.want_val = false; sp.beta = beta; sp.S = s;
+  sp.env_trace = env_trace ? c->d_env_trace : nullptr;
+  std::vector<double> csum, cval;
+  for (int t = 0; t < n_sweeps; ++t) {
+    if ((st = run_sweep(c, sp, csum, cval)) != QFS_OK) return st;
+    if (env_trace)
+      CUDA_TRY(c, cudaMemcpy(env_trace + (size_t)t * tr * 2, c->d_env_trace, tr * sizeof(double2),
+                             cudaMemcpyDeviceToHost));
+    if (gate_trace)
+      CUDA_TRY(c, cudaMemcpy(gate_trace + (size_t)t * s * c->K * 32, c->d_gates,
+                             (size_t)s * c->K * sizeof(double2) * 16, cudaMemcpyDeviceToHost));
+    if (cost_trace)
+      for (int q = 0; q < s; ++q) cost_trace[(size_t)t * s + q] = csum[q] / m;
+    if (sigma_trace) {
+      std::vector<double> sg((size_t)s * c->K);
+      CUDA_TRY(c, cudaMemcpy(sg.data(), c->d_sig, sg.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      for (int i = 0; i < c->K; ++i)
+        for (int q = 0; q < s; ++q) sigma_trace[((size_t)t * c->K + i) * s + q] = sg[(size_t)q * c->K + i];
+    }
+  }
+  return QFS_OK;
+}
+
+qfs_status qfs_bench_sweeps(qfs_ctx *c, int s, const double *init_gates, int m, int n_sweeps,
+                            double *sec) {
+  qfs_status st = check_ready(c, s);
+  if (st != QFS_OK) return st;
+  const int wm = c->mode == 1 ? c->world : 1;
+  if (!init_gates || n_sweeps < 1 || m < 1 || m % wm || m / wm > c->m_pool)
+    return fail(c, QFS_ERR_ARG, "bad bench arguments");
+  const int ml = m / wm;
+  if ((st = ensure_gates(c, s)) != QFS_OK) return st;
+  if ((st = ensure_state(c, s, ml, c->V)) != QFS_OK) return st;
+  if ((st = upload_gates(c, s, init_gates)) != QFS_OK) return st;
+  SweepSpec sp;
+  for (int q = 0; q < s; ++q) sp.slots.push_back({q, ml});
+  sp.M_max = ml; sp.S = s;
+  std::vector<double> csum, cval;
+  cudaEvent_t e0, e1;
+  CUDA_TRY(c, cudaEventCreate(&e0));
+  CUDA_TRY(c, cudaEventCreate(&e1));
+  CUDA_TRY(c, cudaEventRecord(e0, c->st));
+  for (int t = 0; t < n_sweeps; ++t)
+    if ((st = run_sweep(c, sp, csum, cval)) != QFS_OK) return st;
+  CUDA_TRY(c, cudaEventRecord(e1, c->st));
+  CUDA_TRY(c, cudaEventSynchronize(e1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (sec) *sec = ms * 1e-3;
+  return QFS_OK;
+}
+
+// Controller (readings R7-R14, R16).
+qfs_status qfs_instantiate(qfs_ctx *c, int s, const double *init_gates, const qfs_params *p,
+                           double *out_gates, qfs_result *out, int *winner) {
+  qfs_status st = check_ready(c, s);
+  if (st != QFS_OK) return st;
+  if (!init_gates || !p || !out_gates || !out) return fail(c, QFS_ERR_ARG, "null argument");
+  const int wm = c->mode == 1 ? c->world : 1;
+  const long long Nfull = c->N;
+  const int pool_g = c->m_pool * wm;  // global pool rows
+  if (p->m_init < 1 || p->m_init > pool_g) return fail(c, QFS_ERR_CAPACITY, "m_init > m_pool");
+  if (p->m_init % wm) return fail(c, QFS_ERR_CAPACITY, "m_init not divisible by world");
+  if (p->max_iter < 1) return fail(c, QFS_ERR_ARG, "max_iter < 1");
+  if ((st = ensure_gates(c, s)) != QFS_OK) return st;
+  if ((st = upload_gates(c, s, init_gates)) != QFS_OK) return st;
+  struct S_ {
+    int M, it, total, fails, restarts, term, conv_sweep;
+    bool has_prev, active;
+    double c_prev, c_train, c_val;
+  };
+  std::vector<S_> A(s);
+  for (auto &a : A) {
+    a.M = p->m_init; a.it = a.total = a.fails = a.restarts = 0; a.term = -1; a.conv_sweep = -1;
+    a.has_prev = false; a.active = true; a.c_prev = 0; a.c_train = NAN; a.c_val = NAN;
+  }
+  const double otr = p->overtrain_ratio;
+  const bool multi_rank = c->world > 1 && c->comm && c->mode == 0;
+  std::vector<double> csum, cval;
+  for (int t = 1;; ++t) {
+    SweepSpec sp;
+    sp.S = s; sp.beta = p->beta;
+    for (int q = 0; q < s; ++q)
+      if (A[q].active) {
+        sp.slots.push_back({q, A[q].M / wm});
+        sp.M_max = std::max(sp.M_max, A[q].M / wm);
+      }
+    sp.want_val = c->V > 0;
+    bool any_conv = false, any_active = false;
+    if (!sp.slots.empty()) {
+      if ((st = ensure_state(c, s, sp.M_max, c->V)) != QFS_OK) return st;
+      if ((st = run_sweep(c, sp, csum, cval)) != QFS_OK) return st;
+      for (size_t j = 0; j < sp.slots.size(); ++j) {
+        S_ &a = A[sp.slots[j].s];
+        a.c_train = csum[j] / a.M;
+        a.c_val = c->V > 0 ? cval[j] / c->V : NAN;
+        a.it += 1; a.total += 1;                                               // step 1
+        const double cc = a.c_train;
+        const bool gen_check = c->V > 0 && std::isfinite(otr) && a.M < Nfull;  // step 2
+        bool conv = false;                                                     // step 3
+        if (cc <= p->dist_tol) {
+          if (!gen_check) conv = true;
+          else if (cc < 1e-14) conv = a.c_val <= (1.0 + otr) * p->dist_tol;
+          else conv = a.c_val / cc - 1.0 <= otr;
+        }
+        if (conv) { a.term = QFS_CONVERGED; a.active = false; a.conv_sweep = t; any_conv = true; continue; }
+        if (gen_check && a.it >= p->min_iter && a.c_val / cc - 1.0 > otr) {    // step 4
+          if (2LL * a.M > pool_g && a.M < Nfull) { a.term = QFS_POOL_EXHAUSTED; a.active = false; continue; }
+          a.M = (int)std::min<long long>(2LL * a.M, Nfull);
+          a.it = 0; a.fails = 0; a.has_prev = false; a.restarts += 1;
+        } else if (p->plateau_window > 0) {                                    // step 5
+          if (a.has_prev)
+            a.fails = (std::fabs(a.c_prev) - std::fabs(cc) > p->diff_tol_r * std::fabs(cc)) ? 0 : a.fails + 1;
+          a.c_prev = cc; a.has_prev = true;
+          if (a.it >= p->min_iter && a.fails >= p->plateau_window) { a.term = QFS_PLATEAU; a.active = false; continue; }
+        }
+        if (a.total >= p->max_iter) { a.term = QFS_MAX_ITER; a.active = false; }  // step 6
+      }
+    }
+    for (auto &a : A) any_active |= a.active;
+    if (multi_rank) {  // "any converged" / "any active" across ranks
+      int h[2] = {any_conv ? 1 : 0, any_active ? 1 : 0};
+      CUDA_TRY(c, cudaMemcpyAsync(c->d_flag, h, sizeof h, cudaMemcpyHostToDevice, c->st));
+      NCCL_TRY(c, ncclAllReduce(c->d_flag, c->d_flag, 2, ncclInt32, ncclMax, c->comm, c->st));
+      CUDA_TRY(c, cudaMemcpyAsync(h, c->d_flag, sizeof h, cudaMemcpyDeviceToHost, c->st));
+      CUDA_TRY(c, cudaStreamSynchronize(c->st));
+      any_conv = h[0] != 0;
+      any_active = h[1] != 0;
+    }
+    if (any_conv && p->stop_on_first) {
+      for (auto &a : A)
+        if (a.active) { a.active = false; a.term = QFS_STOPPED; }
+      break;
+    }
+    if (!any_active) break;
+  }
+  int win = -1, best = 1 << 30;
+  for (int q = 0; q < s; ++q)
+    if (A[q].term == QFS_CONVERGED && A[q].conv_sweep < best) { best = A[q].conv_sweep; win = q; }
+  if (win < 0) {
+    double bc = INFINITY;
+    for (int q = 0; q < s; ++q)
+      if (A[q].c_train < bc) { bc = A[q].c_train; win = q; }
+    if (win < 0) win = 0;
+  }
+  CUDA_TRY(c, cudaMemcpy(out_gates, c->d_gates, (size_t)s * c->K * 16 * sizeof(double2),
+                         cudaMemcpyDeviceToHost));
+  for (int q = 0; q < s; ++q) {
+    out[q].c_train = A[q].c_train; out[q].c_val = A[q].c_val; out[q].sweeps = A[q].total;
+    out[q].restarts = A[q].restarts; out[q].final_m = A[q].M; out[q].term = (qfs_term)A[q].term;
+  }
+  if (winner) *winner = win;
+  return QFS_OK;
+}
+
+qfs_status qfs_op_apply(qfs_ctx *c, int p0, int p1, const double *g, int dagger, int m,
+                        double *psi) {
+  if (!c || !g || !psi || m < 1 || p0 < 0 || p1 < 0 || p0 >= c->n || p1 >= c->n || p0 == p1)
+    return fail(c, QFS_ERR_ARG, "bad apply arguments");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  ApplyParams a{};
+  a.n = c->n; a.p0 = p0; a.p1 = p1; a.m = m;
+  for (int r = 0; r < 4; ++r)
+    for (int q = 0; q < 4; ++q) {
+      const double *e = dagger ? g + 2 * (4 * q + r) : g + 2 * (4 * r + q);
+      a.g[4 * r + q] = make_double2(e[0], dagger ? -e[1] : e[1]);
+    }
+  double2 *d = nullptr;
+  const size_t bytes = (size_t)m * c->N * sizeof(double2);
+  CUDA_TRY(c, cudaMalloc(&d, bytes));
+  a.psi = d;
+  cudaError_t e = cudaMemcpy(d, psi, bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    LaunchScope ls(c, K_OP, 2.0 * bytes, 32.0 * m * c->N);
+    e = launch_apply(a, c->st);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->st);
+  if (e == cudaSuccess) e = cudaMemcpy(psi, d, bytes, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(c, QFS_ERR_DEVICE, cudaGetErrorString(e));
+  return QFS_OK;
+}
+
+qfs_status qfs_op_environment(qfs_ctx *c, int p0, int p1, int m, const double *phi,
+                              const double *chi, double *env) {
+  if (!c || !phi || !chi || !env || m < 1 || p0 < 0 || p1 < 0 || p0 >= c->n || p1 >= c->n || p0 == p1)
+    return fail(c, QFS_ERR_ARG, "bad environment arguments");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  const size_t bytes = (size_t)m * c->N * sizeof(double2);
+  double2 *dphi = nullptr, *dchi = nullptr;
+  double *dpart = nullptr, *dred = nullptr;
+  unsigned *dcnt = nullptr;
+  Slot *dsl = nullptr;
+  BwdParams b{};
+  b.n = c->n; b.K = 1; b.nu = 2;
+  b.nb = blocks_per_start(((long long)m * c->N) >> 2, 1);
+  cudaError_t e = cudaMalloc(&dphi, bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&dchi, bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&dpart, (size_t)b.nb * 32 * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&dred, 32 * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&dcnt, sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaMalloc(&dsl, sizeof(Slot));
+  Slot sl{0, m};
+  if (e == cudaSuccess) e = cudaMemcpy(dphi, phi, bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(dchi, chi, bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(dcnt, 0, sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaMemcpy(dsl, &sl, sizeof sl, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    b.slots = dsl; b.chi_src = Rows{dchi, 0}; b.chi_dst = RowsW{nullptr, 0}; b.phi = Rows{dphi, 0};
+    int lo = std::min(p0, p1), hi = std::max(p0, p1);
+    b.ins[0] = lo; b.ins[1] = hi;
+    for (int v = 0; v < 16; ++v)
+      b.off[v] = v < 4 ? (((long long)(v & 1) << p0) | ((long long)((v >> 1) & 1) << p1)) : 0;
+    b.partials = dpart; b.counters = dcnt; b.e_red = dred; b.fuse_polar = 0; b.env_gate = 0;
+    b.upd_gate = -1; b.S = 1;
+    LaunchScope ls(c, K_OP, 2.0 * bytes, 32.0 * m * c->N);
+    e = launch_bwd(b, 1, 0, 1, false, c->st);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->st);
+  if (e == cudaSuccess) e = cudaMemcpy(env, dred, 32 * sizeof(double), cudaMemcpyDeviceToHost);
+  cudaFree(dphi); cudaFree(dchi); cudaFree(dpart); cudaFree(dred); cudaFree(dcnt); cudaFree(dsl);
+  if (e != cudaSuccess) return fail(c, QFS_ERR_DEVICE, cudaGetErrorString(e));
+  return QFS_OK;
+}
+
+qfs_status qfs_op_polar(qfs_ctx *c, int count, const double *env, const double *g_old,
+                        double beta, double *g_new, double *sigma_sum) {
+  if (!c || count < 1 || !env || !g_old || !g_new || !sigma_sum)
+    return fail(c, QFS_ERR_ARG, "bad polar arguments");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  const size_t mb = (size_t)count * 16 * sizeof(double2);
+  double2 *de = nullptr, *dg = nullptr, *dn = nullptr;
+  double *ds = nullptr;
+  cudaError_t e = cudaMalloc(&de, mb);
+  if (e == cudaSuccess) e = cudaMalloc(&dg, mb);
+  if (e == cudaSuccess) e = cudaMalloc(&dn, mb);
+  if (e == cudaSuccess) e = cudaMalloc(&ds, count * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemcpy(de, env, mb, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(dg, g_old, mb, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    LaunchScope ls(c, K_OP, 3.0 * mb, 0);
+    e = launch_polar_batch(de, dg, beta, dn, ds, count, c->st);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->st);
+  if (e == cudaSuccess) e = cudaMemcpy(g_new, dn, mb, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(sigma_sum, ds, count * sizeof(double), cudaMemcpyDeviceToHost);
+  cudaFree(de); cudaFree(dg); cudaFree(dn); cudaFree(ds);
+  if (e != cudaSuccess) return fail(c, QFS_ERR_DEVICE, cudaGetErrorString(e));
+  return QFS_OK;
+}
+
+qfs_status qfs_profile_enable(qfs_ctx *c, int on) {
+  if (!c) return QFS_ERR_ARG;
+  prof_collect(c);
+  c->prof = on != 0;
+  if (on) {
+    for (int q = 0; q < K_NCLASS; ++q) { c->p_ms[q] = c->p_bytes[q] = c->p_flops[q] = 0; c->p_cnt[q] = 0; }
+  }
+  return QFS_OK;
+}
+
+qfs_status qfs_profile_read(qfs_ctx *c, int cap, const char **names, long long *launches,
+                            double *ms, double *bytes, double *flops, int *count) {
+  if (!c) return QFS_ERR_ARG;
+  prof_collect(c);
+  for (int q = 0; q < K_NCLASS && q < cap; ++q) {
+    if (names) names[q] = kClassName[q];
+    if (launches) launches[q] = c->p_cnt[q];
+    if (ms) ms[q] = c->p_ms[q];
+    if (bytes) bytes[q] = c->p_bytes[q];
+    if (flops) flops[q] = c->p_flops[q];
+  }
+  if (count) *count = K_NCLASS;
+  return QFS_OK;
+}
+
+long long qfs_launch_count(const qfs_ctx *c) { return c ? c->launches : 0; }
+void *qfs_stream(const qfs_ctx *c) { return c ? (void *)c->st : nullptr; }
+const char *qfs_last_error(const qfs_ctx *c) { return c ? c->err.c_str() : "null context"; }
+
+void qfs_destroy(qfs_ctx *c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->st) cudaStreamSynchronize(c->st);
+  prof_collect(c);
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  dfree(c->d_pairs); dfree(c->d_flag); dfree(c->d_x); dfree(c->d_y); dfree(c->d_xv); dfree(c->d_yv);
+  dfree(c->d_gates); dfree(c->d_chi); dfree(c->d_B); dfree(c->d_vb0); dfree(c->d_vb1);
+  dfree(c->d_partials); dfree(c->d_ered); dfree(c->d_sig); dfree(c->d_csum); dfree(c->d_rowout);
+  dfree(c->d_cval); dfree(c->d_counters); dfree(c->d_slots); dfree(c->d_env_trace);
+  if (c->h_csum) cudaFreeHost(c->h_csum);
+  if (c->h_cval) cudaFreeHost(c->h_cval);
+  if (c->st) cudaStreamDestroy(c->st);
+  delete c;
+}
+
+}  // extern "C"

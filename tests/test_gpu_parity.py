@@ -1,0 +1,294 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerances (SURVEY.md §8(c) "Parity tolerances"; north_star: 1e-10 relative
+in complex128 over the first 5 sweeps):
+  E:     ||E_gpu - E_orc||_F <= 1e-10 ||E_orc||_F
+  gates: ||G_gpu - G_orc||_F <= 2e-10, only where sigma_4/sigma_1 >= 1e-8 (the
+         polar factor is unique there; reading R5) — otherwise costs only
+  cost:  |dc| <= 1e-10 c + 1e-15
+Inputs are the seeded synthetic configs of paper_2405_12866_b200.inputs.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2405_12866_b200 import inputs as I
+
+pytestmark = pytest.mark.gpu
+
+ENV_TOL, GATE_TOL, COST_TOL = 1e-10, 2e-10, 1e-10
+
+
+@pytest.fixture(scope="module")
+def qfs():
+    from paper_2405_12866_b200 import build, qfs as Q
+    build.build()
+    return Q
+
+
+def _ctx(Q, n, pairs, **kw):
+    return Q.Context(n, pairs, **kw)
+
+
+def rand_c(rng, shape):
+    return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+
+
+def unitary(rng):
+    return I.haar_unitary(rng)
+
+
+# ------------------------------------------------------------ kernel ops ----
+@pytest.mark.parametrize("n", [2, 3, 5, 8])
+def test_op_apply_all_pairs(qfs, n):
+    rng = np.random.default_rng(n)
+    m = 3
+    psi = rand_c(rng, (m, 1 << n))
+    ctx = _ctx(qfs, n, [[0, 1]])
+    for p0 in range(n):
+        for p1 in range(n):
+            if p0 == p1:
+                continue
+            g = rand_c(rng, (4, 4))
+            for dag in (False, True):
+                got = ctx.op_apply(p0, p1, g, psi, dagger=dag)
+                want = oracle.apply_gate(n, p0, p1, g, psi, dagger=dag)
+                assert np.abs(got - want).max() <= 1e-14 * np.abs(want).max()
+
+
+@pytest.mark.parametrize("n,m", [(2, 1), (4, 3), (7, 5), (11, 2)])
+def test_op_environment(qfs, n, m):
+    rng = np.random.default_rng(10 + n)
+    phi, chi = rand_c(rng, (m, 1 << n)), rand_c(rng, (m, 1 << n))
+    ctx = _ctx(qfs, n, [[0, 1]])
+    for p0, p1 in [(0, 1), (1, 0), (0, n - 1), (n - 1, n - 2)] if n > 2 else [(0, 1), (1, 0)]:
+        got = ctx.op_environment(p0, p1, phi, chi)
+        want = oracle.environment(n, p0, p1, phi, chi)
+        assert np.linalg.norm(got - want) <= 1e-13 * np.linalg.norm(want)
+
+
+def _matrices(rng, count):
+    out = []
+    for t in range(count):
+        kind = t % 6
+        if kind == 0:
+            a = rand_c(rng, (4, 4))
+        elif kind == 1:
+            a = unitary(rng) @ np.diag([1, 1e-3, 1e-5, 1e-8]) @ unitary(rng)
+        elif kind == 2:
+            a = rand_c(rng, (4, 2)) @ rand_c(rng, (2, 4))
+        elif kind == 3:
+            a = unitary(rng) @ np.diag([2, 2, 1, 1]) @ unitary(rng)
+        elif kind == 4:
+            a = unitary(rng).conj().T * (1 + 1e-3 * rng.standard_normal())
+        else:
+            a = rand_c(rng, (4, 4)) * 10.0 ** rng.integers(-6, 6)
+        out.append(a)
+    return np.stack(out)
+
+
+def test_op_polar_against_oracle(qfs):
+    """K3 on 20k seeded random, ill-conditioned, rank-deficient and degenerate 4x4s."""
+    rng = np.random.default_rng(123)
+    E = _matrices(rng, 20000)
+    G0 = np.stack([unitary(rng) for _ in range(len(E))])
+    ctx = _ctx(qfs, 2, [[0, 1]])
+    for beta in (0.0, 0.3):
+        gn, ss = ctx.op_polar(E, G0, beta)
+        for i in range(0, len(E), 7):
+            go, so = oracle.polar_update(E[i], G0[i], beta)
+            ep = (1 - beta) * E[i] + beta * G0[i].conj().T
+            sv = np.linalg.svd(ep, compute_uv=False)
+            assert abs(ss[i] - so) <= 1e-12 * so
+            assert np.abs(gn[i].conj().T @ gn[i] - np.eye(4)).max() < 1e-13
+            assert abs(np.trace(ep @ gn[i]).real - sv.sum()) <= 1e-12 * sv[0]
+            if sv[-1] / sv[0] >= 1e-8:
+                # polar-factor perturbation bound ~ eps * cond (both sides round)
+                tol = max(GATE_TOL, 50 * 2.2e-16 * sv[0] / sv[-1])
+                assert np.linalg.norm(gn[i] - go) <= tol
+
+
+# ------------------------------------------------------------- sweep parity --
+def _compare_traces(gt, ot, label):
+    env_g, env_o = gt["env"], ot["env"]
+    T, K, S = env_o.shape[:3]
+    worst = dict(env=0.0, gate=0.0, cost=0.0)
+    for t in range(T):
+        for s in range(S):
+            for i in range(K):
+                eo = env_o[t, i, s]
+                r = np.linalg.norm(env_g[t, i, s] - eo) / np.linalg.norm(eo)
+                worst["env"] = max(worst["env"], r)
+                assert r <= ENV_TOL, (label, "env", t, i, s, r)
+                sv = np.linalg.svd(eo, compute_uv=False)
+                if sv[-1] / sv[0] >= 1e-8:
+                    d = np.linalg.norm(gt["gates"][t, s, i] - ot["gates"][t, s, i])
+                    worst["gate"] = max(worst["gate"], d)
+                    assert d <= GATE_TOL, (label, "gate", t, s, i, d)
+            co, cg = ot["cost"][t, s], gt["cost"][t, s]
+            worst["cost"] = max(worst["cost"], abs(co - cg) / max(co, 1e-300))
+            assert abs(co - cg) <= COST_TOL * co + 1e-15, (label, "cost", t, s, co, cg)
+    assert np.abs(gt["sigma"] - ot["sigma"]).max() <= 1e-10 * np.abs(ot["sigma"]).max()
+    return worst
+
+
+CASES = [
+    # name, init, S, m (None = config m_init), sweeps, K override
+    ("c1", "R", 1, None, 5, None),
+    ("c2", "R", 32, None, 5, None),
+    ("c2", "W", 8, 64, 5, None),
+    ("c3", "R", 8, None, 5, None),
+    ("c3", "W", 4, 32, 5, None),
+    ("c4", "W", 2, None, 3, 40),
+    ("c5b", "W", 1, 16, 3, 30),
+]
+
+
+@pytest.mark.parametrize("name,init,s,m,sweeps,k", CASES)
+def test_trace_parity(qfs, name, init, s, m, sweeps, k):
+    p = I.make_problem(name, init=init, s=s, k=k)
+    m = m or p.m_init
+    ctx = _ctx(qfs, p.n, p.pairs)
+    ctx.set_samples(p.x, p.y, p.xv, p.yv)
+    gt = ctx.trace_sweeps(p.init, m, sweeps)
+    ot = oracle.trace_sweeps(p.n, p.pairs, p.init, p.x, p.y, m, sweeps)
+    _compare_traces(gt, ot, f"{name}-{init}")
+
+
+def test_trace_parity_ragged_and_degenerate(qfs):
+    """Ragged M (odd row counts), reversed / non-adjacent / repeated pairs, K=1, n=2."""
+    rng = np.random.default_rng(5)
+    for n, pairs, m in [(2, [[0, 1]], 3), (2, [[1, 0], [0, 1], [1, 0]], 4),
+                        (5, [[4, 0], [0, 4], [2, 3], [3, 1], [1, 3], [0, 2]], 7),
+                        (9, [[8, 0], [1, 2], [2, 1], [5, 7]], 5)]:
+        pairs = np.asarray(pairs, np.int32)
+        target = np.stack([unitary(rng) for _ in pairs])
+        x = I.haar_states(rng, n, m)
+        y = I.apply_circuit_tensor(n, pairs, target, x)
+        init = np.stack([np.stack([unitary(rng) for _ in pairs]) for _ in range(3)])
+        ctx = _ctx(qfs, n, pairs)
+        ctx.set_samples(x, y)
+        gt = ctx.trace_sweeps(init, m, 4)
+        ot = oracle.trace_sweeps(n, pairs, init, x, y, m, 4)
+        _compare_traces(gt, ot, f"ragged n={n}")
+
+
+def test_trace_parity_streamed_forward_n14(qfs):
+    """n = 14 takes the per-gate streamed forward (no whole row in SMEM)."""
+    rng = np.random.default_rng(14)
+    n = 14
+    pairs = I.brick_pairs(n, 10)
+    pairs[3] = [13, 0]
+    target = np.stack([unitary(rng) for _ in pairs])
+    x = I.haar_states(rng, n, 2)
+    y = I.apply_circuit_tensor(n, pairs, target, x)
+    xv = I.haar_states(rng, n, 2)
+    yv = I.apply_circuit_tensor(n, pairs, target, xv)
+    init = np.stack([unitary(rng) for _ in pairs])[None]
+    ctx = _ctx(qfs, n, pairs)
+    ctx.set_samples(x, y, xv, yv)
+    gt = ctx.trace_sweeps(init, 2, 2)
+    ot = oracle.trace_sweeps(n, pairs, init, x, y, 2, 2)
+    _compare_traces(gt, ot, "n14")
+    # controller with validation on the streamed path
+    prm = dict(dist_tol=1e-8, diff_tol_r=1e-3, plateau_window=5, min_iter=6, max_iter=3, m_init=2,
+               overtrain_ratio=1e300, beta=0.0, stop_on_first=1)
+    g1, r1, w1 = ctx.instantiate(init, prm)
+    g2, r2, w2 = oracle.instantiate(n, pairs, x, y, xv, yv, init, prm)
+    assert abs(r1[0]["c_val"] - r2[0]["c_val"]) <= 1e-10 * r2[0]["c_val"]
+    assert abs(r1[0]["c_train"] - r2[0]["c_train"]) <= 1e-10 * r2[0]["c_train"]
+
+
+def test_full_size_c4_sampled_starts(qfs):
+    """C4 at full size (S=16, M=32, K=150, n=12) in the bench's launch shape;
+    the oracle recomputes two of the 16 starts (starts are independent)."""
+    p = I.make_problem("c4", init="R")
+    ctx = _ctx(qfs, p.n, p.pairs)
+    ctx.set_samples(p.x, p.y, p.xv, p.yv)
+    gt = ctx.trace_sweeps(p.init, p.m_init, 2)
+    pick = [0, 11]
+    ot = oracle.trace_sweeps(p.n, p.pairs, p.init[pick], p.x, p.y, p.m_init, 2)
+    sub = dict(env=gt["env"][:, :, pick], gates=gt["gates"][:, pick], cost=gt["cost"][:, pick],
+               sigma=gt["sigma"][:, :, pick])
+    _compare_traces(sub, ot, "c4-full")
+
+
+# ----------------------------------------------------------- instantiation --
+def _inst_both(qfs, p, prm):
+    ctx = _ctx(qfs, p.n, p.pairs)
+    ctx.set_samples(p.x, p.y, p.xv, p.yv)
+    g1, r1, w1 = ctx.instantiate(p.init, prm)
+    g2, r2, w2 = oracle.instantiate(p.n, p.pairs, p.x, p.y, p.xv, p.yv, p.init, prm, threads=8)
+    return (g1, r1, w1), (g2, r2, w2)
+
+
+def test_instantiate_c1_parity(qfs):
+    """C1 as configured (500 sweeps, plateau off): same termination, sweeps, final cost."""
+    p = I.make_problem("c1", init="R")
+    (g1, r1, w1), (g2, r2, w2) = _inst_both(qfs, p, dict(p.params))
+    assert r1[0]["term"] == r2[0]["term"] and r1[0]["sweeps"] == r2[0]["sweeps"]
+    assert abs(r1[0]["c_train"] - r2[0]["c_train"]) <= 1e-7 * r2[0]["c_train"] + 1e-14
+
+
+@pytest.mark.parametrize("name,s", [("c2", 4), ("c3", 2)])
+def test_instantiate_warm_converges_and_matches(qfs, name, s):
+    """Solvable-by-construction targets reach c_train <= 1e-8 on the GPU and the
+    controller takes the same decisions as the oracle (termination, restarts,
+    final M, sweep count within +-2; SURVEY §8(c) 'parity unpinned' rule)."""
+    p = I.make_problem(name, init="W", s=s)
+    prm = dict(p.params, max_iter=300)
+    (g1, r1, w1), (g2, r2, w2) = _inst_both(qfs, p, prm)
+    assert r1[w1]["term"] == "CONVERGED" and r1[w1]["c_train"] <= 1e-8
+    assert w1 == w2
+    for a, b in zip(r1, r2):
+        assert a["term"] == b["term"] and a["restarts"] == b["restarts"] and a["final_m"] == b["final_m"]
+        assert abs(a["sweeps"] - b["sweeps"]) <= 2
+
+
+def test_instantiate_restart_geometry_gpu(qfs):
+    """Double-and-restart on the GPU path (C2 random init, per-start ragged M)."""
+    p = I.make_problem("c2", init="R", s=6)
+    prm = dict(p.params, max_iter=40, stop_on_first=0)
+    (g1, r1, w1), (g2, r2, w2) = _inst_both(qfs, p, prm)
+    assert any(r["restarts"] > 0 for r in r1)
+    for a, b in zip(r1, r2):
+        assert a["final_m"] == min(p.m_init * 2 ** a["restarts"], 64)
+        assert a["term"] == b["term"] and a["restarts"] == b["restarts"]
+
+
+def test_deterministic_bitwise(qfs):
+    p = I.make_problem("c3", init="R", s=8)
+    ctx = _ctx(qfs, p.n, p.pairs)
+    ctx.set_samples(p.x, p.y, p.xv, p.yv)
+    a = ctx.trace_sweeps(p.init, 16, 2)
+    b = ctx.trace_sweeps(p.init, 16, 2)
+    assert np.array_equal(a["gates"], b["gates"]) and np.array_equal(a["cost"], b["cost"])
+
+
+def test_errors(qfs):
+    from paper_2405_12866_b200.qfs import QfsError
+    p = I.make_problem("c1")
+    with pytest.raises(QfsError) as ei:
+        qfs.Context(3, [[0, 0]])
+    assert ei.value.status == 1
+    ctx = _ctx(qfs, p.n, p.pairs)
+    prm = dict(p.params)
+    with pytest.raises(QfsError) as ei:
+        ctx.instantiate(p.init, prm)
+    assert ei.value.status == 5           # ERR_STATE before set_samples
+    ctx.set_samples(p.x, p.y)
+    bad = p.init.copy()
+    bad[0, 0] *= 1.5
+    with pytest.raises(QfsError) as ei:
+        ctx.instantiate(bad, prm)
+    assert ei.value.status == 3           # ERR_NUMERIC non-unitary gate
+    with pytest.raises(QfsError) as ei:
+        ctx.instantiate(p.init, dict(prm, m_init=8))
+    assert ei.value.status == 2           # ERR_CAPACITY m_init > m_pool
+    nanx = p.x.copy()
+    nanx[0, 0] = np.nan
+    with pytest.raises(QfsError) as ei:
+        ctx.set_samples(nanx, p.y)
+    assert ei.value.status == 3
