@@ -1,0 +1,337 @@
+#!/usr/bin/env python
+"""QFactor-Sample instantiation benchmark on B200 (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl reference]
+
+Workload: BASELINE.json config C4 — n = 12 qubits, K = 150
+two-qubit blocks (brick wall + seeded random non-adjacent pairs), M = 32
+training states, 16 validation states, S = 16 multistarts per GPU, complex128,
+seeded synthetic Haar data (the paper's Table-1 partitions are not available).
+A "step" is one pass of the whole hot path: one sweep of every start (B-cache
+forward, K fused backward/environment/polar launches, sweep-end cost), the
+validation forward, and the host controller's decision — i.e. one iteration
+of qfs_instantiate with its stopping rules unable to fire.
+
+value  = start-sweeps per second, whole job (sum over ranks / max-over-ranks
+         device time).  Multi-GPU: multistarts sharded across ranks (weak
+         scaling, no data-path collective).
+e2e    = the same metric through the public API from host buffers: every step
+         qfs_set_samples (pinned host -> device) + qfs_instantiate(max_iter=1)
+         with host init gates in and host gates/results out.
+roofline = the dominant kernel (by device time in the timed region): algorithmic
+         bytes / CUDA-event duration vs measured HBM copy bandwidth.
+cpu_baseline = the CPU oracle (oracle/) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "QFactor-Sample sweeps/sec + time-to-solution per instantiation; % HBM/FP64 peak"
+UNIT = "start-sweeps/s"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def bench_params(max_iter, m_init):
+    # stopping rules that cannot fire: every call runs exactly max_iter sweeps
+    # (validation still computed every sweep: finite overtrain ratio, M < 2^n)
+    return dict(dist_tol=-1.0, diff_tol_r=1e-3, plateau_window=0, min_iter=6, max_iter=int(max_iter),
+                m_init=int(m_init), overtrain_ratio=1e300, beta=0.0, stop_on_first=0)
+
+
+def cpu_oracle_run(prob, m, starts, threads, steps=1):
+    """The oracle as it stands: `steps` controller steps (sweep + validation) of
+    `starts` starts at fixed M.  Returns (start-sweeps/s, seconds)."""
+    import oracle
+    oracle.build()
+    init = prob.init[:starts]
+    prm = bench_params(1, m)
+    t0 = time.perf_counter()
+    g = init
+    for _ in range(steps):
+        g, _, _ = oracle.instantiate(prob.n, prob.pairs, prob.x, prob.y, prob.xv, prob.yv, g, prm,
+                                     threads=threads)
+    dt = time.perf_counter() - t0
+    return starts * steps / dt, dt
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--starts", type=int, default=None, help="multistarts per GPU (default: config S)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-tts", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    from paper_2405_12866_b200 import inputs as I
+    cfgd = I.CONFIGS[args.config]
+    s_per = args.starts or cfgd["s"]
+    config = {"workload": f"{args.config.upper()}: n={cfgd['n']} K={cfgd['k']} M={cfgd['m_init']} "
+                          f"V={cfgd['v']} S={s_per}/GPU complex128 (BASELINE.json configs[{cfgd['cfg'] - 1}])",
+              "n": cfgd["n"], "k": cfgd["k"], "m": cfgd["m_init"], "v": cfgd["v"],
+              "starts_per_gpu": s_per, "starts_total": s_per * world,
+              "parallelism": f"multistart x{world}",
+              "l2": "inputs larger than L2 (B cache %.1f GB/GPU > 126 MB)" % (
+                  (cfgd["k"] - 1) * s_per * cfgd["m_init"] * (16 << cfgd["n"]) / 1e9)}
+
+    if args.impl == "reference":
+        # the reference arm is the CPU oracle (no reference code exists for this paper)
+        if rank != 0:
+            return
+        cores = host_cores()
+        prob = I.make_problem(args.config, init="R", s=max(cores, 1))
+        starts = min(cores, s_per)
+        cpu_oracle_run(prob, cfgd["m_init"], starts, cores, steps=1)  # warm (one step)
+        v, dt = cpu_oracle_run(prob, cfgd["m_init"], starts, cores, steps=args.steps)
+        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0,
+                "steps": args.steps, "warmup": 1, "ms_per_step": dt / args.steps * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": config,
+                "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                                 "sample": f"{starts} starts x {args.steps} controller steps of {args.config.upper()}"},
+                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2405_12866_b200 import build, qfs
+    build.build()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    # seeded synthetic problem; starts of rank r are [r*S, (r+1)*S) of the seeded stream
+    prob = I.make_problem(args.config, init="R", s=s_per * world)
+    init = np.ascontiguousarray(prob.init[rank * s_per:(rank + 1) * s_per])
+    m = cfgd["m_init"]
+    ctx = qfs.Context(prob.n, prob.pairs, device=local)
+    ctx.set_samples(prob.x, prob.y, prob.xv, prob.yv)
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=local)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- warm-up (also captures the CUDA graph of the sweep)
+    gates, _, _ = ctx.instantiate(init, bench_params(args.warmup, m))
+
+    # ---- timed region: K steps, device time from CUDA events on the library stream
+    l0 = ctx.launch_count()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        gates, res, _ = ctx.instantiate(gates, bench_params(args.steps, m))
+        ev1.record(stream)
+        ev1.synchronize()
+    barrier()
+    launches = ctx.launch_count() - l0
+    dt = max_over_ranks(ev0.elapsed_time(ev1) / 1e3)
+    value = s_per * world * args.steps / dt
+    assert all(r["sweeps"] == args.steps for r in res), res
+
+    # ---- per-kernel CUDA-event durations: the same K steps again with one event
+    # pair around each phase of the sweep (the run of forward launches, the run
+    # of backward launches, ...), recorded as event nodes inside the sweep graph
+    # on the library stream; avg launch duration = phase time / launches.
+    ctx.profile_enable(True)
+    ctx.instantiate(gates, bench_params(2, m))     # capture the instrumented graph
+    ctx.profile_enable(True)                       # reset counters, keep the graph
+    barrier()
+    pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    pe0.record(stream)
+    gates, _, _ = ctx.instantiate(gates, bench_params(args.steps, m))
+    pe1.record(stream)
+    pe1.synchronize()
+    prof = ctx.profile_read()
+    ctx.profile_enable(False)
+    prof_step_ms = pe0.elapsed_time(pe1) / args.steps
+
+    # ---- roofline of the dominant kernel (by device time)
+    peak, peak_src = load_peaks()
+    dom = max((k for k in prof if prof[k]["launches"] > 0), key=lambda k: prof[k]["ms"])
+    pd = prof[dom]
+    tot_ms = sum(v["ms"] for v in prof.values())
+    achieved = pd["bytes"] / (pd["ms"] * 1e-3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        try:
+            with open(tf) as f:
+                tj = json.load(f)
+            traffic = tj.get(args.config, {}).get(dom)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                "avg_launch_us": round(pd["ms"] / pd["launches"] * 1e3, 3),
+                "bytes_per_launch": pd["bytes"] / pd["launches"],
+                "share_of_kernel_time": round(pd["ms"] / tot_ms, 4),
+                "profiled_ms_per_step": round(prof_step_ms, 4),
+                "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
+                                "gbs": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1) if v["ms"] > 0 else 0,
+                                "tflops": round(v["flops"] / (v["ms"] * 1e-3) / 1e12, 3) if v["ms"] > 0 else 0}
+                            for k, v in prof.items() if v["launches"] > 0}}
+
+    # ---- e2e: through the public API from pinned host buffers, copies in the timed region
+    N = 1 << prob.n
+    hx = torch.from_numpy(prob.x).pin_memory()
+    hy = torch.from_numpy(prob.y).pin_memory()
+    hxv = torch.from_numpy(prob.xv).pin_memory()
+    hyv = torch.from_numpy(prob.yv).pin_memory()
+    h2d = (hx.numel() + hy.numel() + hxv.numel() + hyv.numel()) * 16 + init.nbytes
+    d2h = init.nbytes + s_per * 32
+    g = gates
+    e2e_steps = max(3, min(args.steps, 10))
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        ctx.set_samples_host_ptr(hx.shape[0], hx.data_ptr(), hy.data_ptr(), hxv.shape[0], hxv.data_ptr(),
+                                 hyv.data_ptr())
+        g, _, _ = ctx.instantiate(g, bench_params(1, m))
+    barrier()
+    e2e_dt = max_over_ranks(time.perf_counter() - t0)
+    e2e = {"value": s_per * world * e2e_steps / e2e_dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": int(d2h), "steps": e2e_steps}
+
+    # ---- time to solution (rank 0): warm-start instance of the same config, real stopping rules
+    tts = None
+    if rank == 0 and not args.no_tts:
+        pw = I.make_problem(args.config, init="W", s=s_per)
+        prm = dict(pw.params, max_iter=300)
+        ctx.set_samples(pw.x, pw.y, pw.xv, pw.yv)
+        ctx.instantiate(pw.init, dict(prm, max_iter=2))  # warm graph shapes
+        t0 = time.perf_counter()
+        gw, rw, ww = ctx.instantiate(pw.init, prm)
+        tsec = time.perf_counter() - t0
+        tts = {"seconds": round(tsec, 4), "sweeps": rw[ww]["sweeps"], "term": rw[ww]["term"],
+               "c_train": rw[ww]["c_train"], "final_m": rw[ww]["final_m"], "init": "W (eps=0.3)",
+               "success_fraction": sum(r["term"] == "CONVERGED" for r in rw) / len(rw)}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cores = host_cores()
+        starts = min(cores, s_per)
+        v, cdt = cpu_oracle_run(prob, m, starts, cores, steps=1)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{starts} starts x 1 controller step (sweep + validation) of {args.config.upper()}, "
+                         f"{cdt:.1f} s wall"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": config, "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline,
+                "cpu_baseline": cpu, "clocks": clk.summary(), "time_to_solution": tts,
+                "amp_gate_updates_per_s": value * m * N * prob.k}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

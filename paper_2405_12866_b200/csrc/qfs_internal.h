@@ -13,41 +13,45 @@ struct Slot {
   int m;
 };
 
-// Row addressing: row (s, m) of a state array starts at
-//   base + (s * stride_s + m) * 2^n     (double2 elements)
-// stride_s = 0 for the shared pools (x, y, xv, yv), M_cap for per-start buffers.
-struct Rows {
+// Strided view of a state array: element (start s, amplitude a, sample m) is
+//   base[s * ss + a * sa + m * sm]          (double2 = one complex128)
+// Work buffers (chi, B cache) are sample-minor: sa = M_cap, sm = 1, so the
+// 32 lanes of a warp (consecutive m) touch one contiguous 512-byte run for any
+// gate qubit pair.  The transposed pools use ss = 0, sa = m_pool, sm = 1;
+// row-major arrays (validation, unit ops) use sa = 1, sm = 2^n.
+struct View {
   const double2 *base;
-  long long stride_s;
+  long long ss, sa, sm;
 };
-struct RowsW {
+struct ViewW {
   double2 *base;
-  long long stride_s;
+  long long ss, sa, sm;
 };
 
 // Fused backward step for gate i (bwd_kernel):
 //   chi <- G_{i+1}^dag chi (if update) and E_i += phi_i (x) conj(chi)
 // over the 2^nu-amplitude groups spanned by the union of both gates' bits.
 struct BwdParams {
-  int n, nu, nb;              // qubits, union bits, blocks per start
+  int n, nu, nb;              // qubits, union bits, CTAs per start
   int upd_gate, env_gate;     // i+1 (or -1), i
-  int K;
+  int K, S;                   // gates, total starts (trace layout)
   const Slot *slots;
-  Rows chi_src;
-  RowsW chi_dst;              // base == nullptr: do not write chi back
-  Rows phi;
+  View chi_src;
+  ViewW chi_dst;              // base == nullptr: do not write chi back
+  View phi;
   uint32_t ins[4];            // union bit positions, ascending (for zero insertion)
   long long off[16];          // amplitude offset of local index v (local bit t <-> loc[t])
   const double2 *gates;       // [S][K][16]
   double2 *gates_w;           // same array (written by the polar step)
+  double2 *vprev;             // [S][K][16] right singular vectors (warm start) or nullptr
   double *partials;           // [S_act][nb][32]
   unsigned *counters;         // [S_act]
   double *e_red;              // [S_act][32]: reduced E (sample mode: before all-reduce)
-  int fuse_polar;             // 1: the last block of each start runs the polar update
+  int fuse_polar;             // 1: the last CTA of each start runs the polar update
   double beta;
   double *sig;                // [S][K] sum sigma, or nullptr
   double2 *env_trace;         // [K][S][16] for this sweep, or nullptr
-  int S;                      // total starts (trace layout)
+  unsigned long long *dbg;    // diagnostics: [K][4] globaltimer stamps, or nullptr
 };
 
 // Polar update of E (already reduced / all-reduced) for each active start.
@@ -56,6 +60,7 @@ struct PolarParams {
   const Slot *slots;
   const double *e_red;        // [S_act][32]
   double2 *gates;             // [S][K][16]
+  double2 *vprev;             // [S][K][16] or nullptr
   double beta;
   double *sig;                // [S][K] or nullptr
   double2 *env_trace;         // [K][S][16] or nullptr
@@ -63,49 +68,42 @@ struct PolarParams {
 
 // Sweep-end cost: chi' = G_0^dag chi ; sum_m ||chi'_m - x_m||^2 (direct form)
 struct FinalParams {
-  int n, nb;
+  int n, nb, K;
   const Slot *slots;
-  Rows chi;
-  Rows x;
+  View chi, x;
   int p0, p1;
-  const double2 *gates;       // gate 0 of each start: gates + s*K*16
-  int K;
+  const double2 *gates;       // gate 0 of start s: gates + s*K*16
   double *partials;           // [S_act][nb]
   unsigned *counters;         // [S_act]
   double *out_sum;            // [S_act] raw sum (host divides by M)
 };
 
-// Whole-row forward in shared memory (n <= 13): one CTA per (start, row).
-//   mode 0 (train): writes B_1..B_{K-1} (B_{k+1} = G_k B_k, B_0 = x)
-//   mode 1 (valid): applies all K gates, then sum ||row - yv_row||^2
-struct FwdRowParams {
-  int n, K, mode, rows;       // rows: number of validation rows (mode 1)
-  const Slot *slots;
-  const int2 *pairs;          // [K]
-  const double2 *gates;       // [S][K][16]
-  Rows src;                   // x pool / xv pool
-  double2 *B;                 // mode 0: [K-1][S][M_cap][N]
-  long long b_gate_stride;    // S * M_cap * N
-  long long b_stride_s;       // M_cap
-  Rows ref;                   // mode 1: yv pool
-  double *row_out;            // mode 1: [S_act][rows] per-row sums
-};
-
-// Per-gate streamed forward (n >= 14): dst = G_k src for every row of every slot.
+// Per-gate forward: dst = G_k src for every (quadruple, sample) of every slot.
 struct FwdGateParams {
   int n, nb, k, K, rows_fixed; // rows_fixed > 0: that many rows per start (validation)
   const Slot *slots;
   int p0, p1;
   const double2 *gates;
-  Rows src;
-  RowsW dst;
+  View src;
+  ViewW dst;
+};
+
+// Whole-row validation forward in shared memory (n <= 13): one CTA per
+// (start, validation row); all K gates, then sum ||row - yv_row||^2.
+struct ValRowParams {
+  int n, K, rows;
+  const Slot *slots;
+  const int2 *pairs;          // [K]
+  const double2 *gates;       // [S][K][16]
+  const double2 *xv, *yv;     // row-major [rows][2^n]
+  double *row_out;            // [S_act][rows]
 };
 
 // Row distance sums (streamed validation end): out[j*rows + r] = ||a - b||^2
 struct DistParams {
   int n, rows;
   const Slot *slots;
-  Rows a, b;
+  View a, b;
   double *row_out;
 };
 
@@ -121,15 +119,19 @@ cudaError_t launch_bwd(const BwdParams &p, int n_slots, int tp0, int tp1, bool u
                        cudaStream_t st);
 cudaError_t launch_polar(const PolarParams &p, int n_slots, cudaStream_t st);
 cudaError_t launch_final(const FinalParams &p, int n_slots, cudaStream_t st);
-cudaError_t launch_fwd_row(const FwdRowParams &p, int n_slots, int max_rows, cudaStream_t st);
 cudaError_t launch_fwd_gate(const FwdGateParams &p, int n_slots, cudaStream_t st);
+cudaError_t launch_val_row(const ValRowParams &p, int n_slots, cudaStream_t st);
 cudaError_t launch_dist(const DistParams &p, int n_slots, cudaStream_t st);
 cudaError_t launch_row_reduce(const double *row_in, int rows, double *out, int n_slots,
                               cudaStream_t st);
 cudaError_t launch_apply(const ApplyParams &p, cudaStream_t st);
 cudaError_t launch_polar_batch(const double2 *env, const double2 *g_old, double beta,
                                double2 *g_new, double *sig, int count, cudaStream_t st);
-int fwd_row_max_n();   // largest n the shared-memory row forward supports
-int bwd_threads();
+cudaError_t launch_transpose(const double2 *src, double2 *dst, int rows, long long cols,
+                             cudaStream_t st);
+cudaError_t launch_finite_check(const double *p, long long n, int *flag, cudaStream_t st);
+cudaError_t launch_identity_fill(double2 *v, long long count16, cudaStream_t st);
+int val_row_max_n();        // largest n the shared-memory validation forward supports
+int blocks_per_sm(int nu);  // resident CTAs per SM of the backward kernel
 
 }  // namespace qfs

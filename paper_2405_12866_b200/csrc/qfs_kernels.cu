@@ -1,18 +1,24 @@
 // qfs_kernels.cu — sm_100a kernels of the QFactor-Sample sweep (arXiv 2405.12866).
 //
 // Hot path of one sweep (§3):
-//   fwd_row_kernel / fwd_gate_kernel : B_{k+1} = G_k B_k (the B tensors)
-//   bwd_kernel                       : chi <- G_{i+1}^dag chi fused with the
-//                                      environment E_i = sum phi (x) conj(chi)
-//                                      and, in its last CTA per start, the one-warp
-//                                      Jacobi polar update u = Y X^dag (eq:opt_u P:59-62)
-//   final_kernel                     : chi <- G_0^dag chi, c_train = (1/M) sum ||chi - x||^2
-//   fwd_row_kernel (mode 1)          : validation cost
+//   fwd_gate_kernel : B_{k+1} = G_k B_k, the B tensors
+//   bwd_kernel      : chi <- G_{i+1}^dag chi fused with the environment
+//                     E_i = sum phi (x) conj(chi) (Fig. env_calc);
+//                     its last CTA per start reduces the CTA partials in order
+//                     and runs the half-warp Jacobi polar update u = Y X^dag
+//                     (eq:opt_u)
+//   final_kernel    : chi <- G_0^dag chi, c_train = (1/M) sum ||chi - x||^2
+//   val_row_kernel  : validation cost with the post-sweep gates
 // All arithmetic is FP64 (complex128).  Every reduction runs in a fixed order
 // (per-thread -> warp shuffle -> CTA -> CTA partials summed in index order by
 // the last CTA), so results are deterministic for a given launch shape.
 //
-// No code here is shared with the CPU oracle (oracle/qfso.cpp).
+// State arrays are sample-minor ([start][amplitude][sample], View in
+// qfs_internal.h): a warp's lanes take consecutive samples of the same
+// amplitude, so each of a thread's 2^nu amplitude loads is one fully coalesced
+// 512-byte warp access whatever qubits the gate acts on.
+//
+// No code here is shared with the CPU oracle.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -24,8 +30,12 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int BWD_THREADS = 256;
-constexpr int FWD_THREADS = 512;
+constexpr int BWD_STAGES = 3;  // LDGSTS pipeline depth of the backward kernel
+constexpr int FWD_THREADS = 256;
+constexpr int FWD_STAGES = 4;   // LDGSTS pipeline depth of the forward kernel
+constexpr int VAL_THREADS = 512;
 constexpr int RED_THREADS = 256;
+constexpr int JACOBI_MAX_SWEEPS = 20;
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
@@ -43,173 +53,204 @@ __device__ __forceinline__ long long insert_zero(long long v, int pos) {
   long long low = v & ((1LL << pos) - 1);
   return ((v >> pos) << (pos + 1)) | low;
 }
+__device__ __forceinline__ unsigned insert_zero32(unsigned v, int pos) {
+  return ((v >> pos) << (pos + 1)) | (v & ((1u << pos) - 1u));
+}
 
-// ------------------------------------------------------------ warp polar --
-// One-warp one-sided (Hestenes) Jacobi SVD of the 4x4 complex A (shared
-// memory, overwritten), followed by G = V X^dag (eq:opt_u: E = X D Y^dag,
-// u = Y X^dag with Y = V).  Rounds rotate two disjoint column pairs at once
-// ((0,1)(2,3) / (0,2)(1,3) / (0,3)(1,2)); 8 lanes hold one matrix row of the
-// pair each (A and V rows); the 2x2 rotation follows the classical formulas
-//   zeta = (beta - alpha) / (2|gamma|), t = sgn(zeta) / (|zeta| + sqrt(1 + zeta^2)),
-//   c = 1/sqrt(1 + t^2), s = c t,  [a_j a_k] <- [a_j a_k] [[c, s e^{i phi}], [-s e^{-i phi}, c]]
-// with gamma = a_j^dag a_k = |gamma| e^{i phi}.  Converged when no pair has
-// |gamma| > 1e-15 ||a_j|| ||a_k||.  Columns with sigma <= 1e-14 sigma_max are
-// null; X is completed there by Gram-Schmidt on e_0..e_3 (R5).
-__device__ void warp_polar(double2 *sA, double2 *sV, double2 *sX, double2 *sG, double *sig_sum,
-                           int lane) {
-  if (lane < 16) sV[lane] = make_double2((lane % 5 == 0) ? 1.0 : 0.0, 0.0);
-  __syncwarp();
-  const int p = (lane >> 2) & 1, r = lane & 3;
-  const bool act = lane < 8;
-  for (int sweep = 0; sweep < 24; ++sweep) {
-    bool any = false;
-#pragma unroll 1
-    for (int rho = 0; rho < 3; ++rho) {
-      int j, k;
-      if (rho == 0) { j = 2 * p; k = 2 * p + 1; }
-      else if (rho == 1) { j = p; k = p + 2; }
-      else { j = p; k = 3 - p; }
-      double2 aj = sA[4 * r + j], ak = sA[4 * r + k];
-      double2 vj = sV[4 * r + j], vk = sV[4 * r + k];
+// Division by an invariant d (1 <= d < 2^31) for numerators < 2^31:
+// q = (umulhi(n, mul) + n) >> l with l = ceil(log2 d), mul = 2^32 (2^l - d) / d + 1.
+struct FastDiv {
+  unsigned d, mul;
+  int l;
+  __device__ explicit FastDiv(unsigned dd) : d(dd) {
+    l = 0;
+    while ((1u << l) < d) ++l;
+    mul = (unsigned)((((unsigned long long)1 << 32) * ((1ull << l) - d)) / d + 1);
+  }
+  __device__ __forceinline__ unsigned div(unsigned n) const { return (__umulhi(n, mul) + n) >> l; }
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// LDGSTS: 16-byte global -> shared copy without a register round trip
+// (zero-filled when !valid); .cg = cached in L2 only.
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ double2 shfl_c(double2 v, int src) {
+  return make_double2(__shfl_sync(FULL, v.x, src), __shfl_sync(FULL, v.y, src));
+}
+__device__ __forceinline__ double2 shfl_xor_c(double2 v, int m) {
+  return make_double2(__shfl_xor_sync(FULL, v.x, m), __shfl_xor_sync(FULL, v.y, m));
+}
+
+// ------------------------------------------------------------ polar update --
+// Half-warp one-sided (Hestenes) Jacobi SVD and polar factor of a 4x4 complex
+// matrix; lane l = 4r + j of each 16-lane half holds A[r][j] and V[r][j] in
+// registers (both halves of a warp may work on different matrices).
+//
+//   A_0 = E' V_0 (V_0 = warm-start right singular vectors, any unitary),
+//   rounds rotate the disjoint column pairs (j, j ^ x), x = 1, 2, 3:
+//     gamma = a_j^dag a_k = |gamma| e^{i phi},  zeta = (||a_k||^2 - ||a_j||^2) / (2|gamma|),
+//     t = sgn(zeta) / (|zeta| + sqrt(1 + zeta^2)),  c = 1/sqrt(1 + t^2),  s = c t,
+//     [a_j a_k] <- [a_j a_k] [[c, s e^{i phi}], [-s e^{-i phi}, c]]   (same on V)
+//   until no pair has |gamma| > 1e-15 ||a_j|| ||a_k||; then sigma_j = ||a_j||,
+//   X_j = a_j / sigma_j (null columns, sigma_j <= 1e-14 sigma_max, completed by
+//   Gram-Schmidt on e_0..e_3; R5) and G = V X^dag (eq:opt_u:
+//   E = X D Y^dag, u = Y X^dag with Y = V).  Square roots and divisions are
+//   rsqrt-based (MUFU.RSQ64H + Newton) to keep the serial chain short.
+// E' is scaled by an exact power of two first (the polar factor is scale-free).
+// scratch: 16 double2 of shared memory per half (null-column path only).
+__device__ void hw_polar(double2 e, double2 v0, double2 &g_out, double2 &v_out, double &sig_sum,
+                         double2 *scratch) {
+  const int lane = threadIdx.x & 31;
+  const int hb = lane & 16;         // half-warp base lane
+  const int l = lane & 15;
+  const int r = l >> 2, j = l & 3;
+  // exact power-of-two scaling of E'
+  double mx = fmax(fabs(e.x), fabs(e.y));
+#pragma unroll
+  for (int o = 1; o < 16; o <<= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+  const int ex = mx > 0.0 ? ilogb(mx) : 0;
+  e.x = scalbn(e.x, -ex);
+  e.y = scalbn(e.y, -ex);
+  // A_0 = E' V_0
+  double2 a = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) cfma(a, shfl_c(e, hb | (4 * r + q)), shfl_c(v0, hb | (4 * q + j)));
+  double2 v = v0;
+  for (int sweep = 0; sweep < JACOBI_MAX_SWEEPS; ++sweep) {
+    bool rotated = false;
+#pragma unroll
+    for (int x = 1; x <= 3; ++x) {
+      const double2 ap = shfl_xor_c(a, x);
+      const double2 vp = shfl_xor_c(v, x);
+      const bool lo = (j & (x == 1 ? 1 : 2)) == 0;
+      const double2 aj = lo ? a : ap, ak = lo ? ap : a;
+      const double2 vj = lo ? v : vp, vk = lo ? vp : v;
       double al = aj.x * aj.x + aj.y * aj.y;
       double be = ak.x * ak.x + ak.y * ak.y;
       double gr = aj.x * ak.x + aj.y * ak.y;
       double gi = aj.x * ak.y - aj.y * ak.x;
 #pragma unroll
-      for (int o = 1; o <= 2; o <<= 1) {
+      for (int o = 4; o <= 8; o <<= 1) {
         al += __shfl_xor_sync(FULL, al, o);
         be += __shfl_xor_sync(FULL, be, o);
         gr += __shfl_xor_sync(FULL, gr, o);
         gi += __shfl_xor_sync(FULL, gi, o);
       }
-      const double ag = sqrt(gr * gr + gi * gi);
-      const bool rot = act && ag > 0.0 && ag > 1e-15 * sqrt(al) * sqrt(be);
-      __syncwarp();
-      if (rot) {
-        const double rag = 1.0 / ag;
+      const double ag2 = gr * gr + gi * gi;
+      if (ag2 > 0.0 && ag2 > 1e-30 * al * be) {
+        rotated = true;
+        const double rag = rsqrt(ag2);
         const double zeta = (be - al) * 0.5 * rag;
-        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double c = 1.0 / sqrt(1.0 + t * t);
+        const double w = fma(zeta, zeta, 1.0);
+        const double den = fabs(zeta) + w * rsqrt(w);
+        const double rd = rsqrt(den);
+        const double t = (zeta >= 0.0 ? rd : -rd) * rd;
+        const double c = rsqrt(fma(t, t, 1.0));
         const double s = c * t;
         const double pr = gr * rag, pi = gi * rag;
-        // conj(ph) * a_k and ph * a_j
-        double2 ca = make_double2(pr * ak.x + pi * ak.y, pr * ak.y - pi * ak.x);
-        double2 pa = make_double2(pr * aj.x - pi * aj.y, pr * aj.y + pi * aj.x);
-        sA[4 * r + j] = make_double2(c * aj.x - s * ca.x, c * aj.y - s * ca.y);
-        sA[4 * r + k] = make_double2(s * pa.x + c * ak.x, s * pa.y + c * ak.y);
-        double2 cv = make_double2(pr * vk.x + pi * vk.y, pr * vk.y - pi * vk.x);
-        double2 pv = make_double2(pr * vj.x - pi * vj.y, pr * vj.y + pi * vj.x);
-        sV[4 * r + j] = make_double2(c * vj.x - s * cv.x, c * vj.y - s * cv.y);
-        sV[4 * r + k] = make_double2(s * pv.x + c * vk.x, s * pv.y + c * vk.y);
-      }
-      any |= (__any_sync(FULL, rot) != 0);
-      __syncwarp();
-    }
-    if (!any) break;
-  }
-  // singular values = column norms
-  double nn = 0.0;
-  if (lane < 4) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      double2 a = sA[4 * q + lane];
-      nn += a.x * a.x + a.y * a.y;
-    }
-  }
-  const double sig = sqrt(nn);
-  double sg[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) sg[q] = __shfl_sync(FULL, sig, q);
-  const double smax = fmax(fmax(sg[0], sg[1]), fmax(sg[2], sg[3]));
-  bool nul[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) nul[q] = !(sg[q] > 1e-14 * smax) || smax == 0.0;
-  if (lane < 16) {
-    const int jj = lane & 3;
-    double2 a = sA[lane];
-    sX[lane] = nul[jj] ? make_double2(0.0, 0.0) : make_double2(a.x / sg[jj], a.y / sg[jj]);
-  }
-  __syncwarp();
-  if (lane == 0 && (nul[0] || nul[1] || nul[2] || nul[3])) {
-    for (int j = 0; j < 4; ++j) {
-      if (!nul[j]) continue;
-      for (int e = 0; e < 4; ++e) {
-        double2 v[4];
-        for (int q = 0; q < 4; ++q) v[q] = make_double2(q == e ? 1.0 : 0.0, 0.0);
-        for (int pass = 0; pass < 2; ++pass)
-          for (int q = 0; q < 4; ++q) {
-            if (q == j || (nul[q] && q > j)) continue;
-            double2 d = make_double2(0.0, 0.0);
-            for (int rr = 0; rr < 4; ++rr) cfma(d, cconj(sX[4 * rr + q]), v[rr]);
-            for (int rr = 0; rr < 4; ++rr) {
-              double2 t = cmul(d, sX[4 * rr + q]);
-              v[rr].x -= t.x;
-              v[rr].y -= t.y;
-            }
-          }
-        double nv = 0.0;
-        for (int rr = 0; rr < 4; ++rr) nv += v[rr].x * v[rr].x + v[rr].y * v[rr].y;
-        nv = sqrt(nv);
-        if (nv > 0.5) {
-          for (int rr = 0; rr < 4; ++rr) sX[4 * rr + j] = make_double2(v[rr].x / nv, v[rr].y / nv);
-          break;
+        if (lo) {  // a_j' = c a_j - s conj(ph) a_k
+          a = make_double2(c * aj.x - s * (pr * ak.x + pi * ak.y), c * aj.y - s * (pr * ak.y - pi * ak.x));
+          v = make_double2(c * vj.x - s * (pr * vk.x + pi * vk.y), c * vj.y - s * (pr * vk.y - pi * vk.x));
+        } else {   // a_k' = s ph a_j + c a_k
+          a = make_double2(s * (pr * aj.x - pi * aj.y) + c * ak.x, s * (pr * aj.y + pi * aj.x) + c * ak.y);
+          v = make_double2(s * (pr * vj.x - pi * vj.y) + c * vk.x, s * (pr * vj.y + pi * vj.x) + c * vk.y);
         }
       }
     }
+    if (!__any_sync(FULL, rotated)) break;
   }
-  __syncwarp();
-  if (lane < 16) {
-    const int a = lane >> 2, b = lane & 3;
-    double2 acc = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) cfma(acc, sV[4 * a + q], cconj(sX[4 * b + q]));
-    sG[lane] = acc;
-  }
-  if (lane == 0) *sig_sum = sg[0] + sg[1] + sg[2] + sg[3];
-  __syncwarp();
-}
-
-// E' = (1 - beta) E + beta G_old^dag into sA, then polar; result written to
-// gate slot gout (global) and the optional monitors.
-__device__ void polar_from_reduced(const double *e32 /*smem or global, 32 doubles*/,
-                                   double2 *gout, double beta, double *sig_out,
-                                   double2 *env_out, double2 *sA, double2 *sV, double2 *sX,
-                                   double2 *sG, double *sSig, int lane) {
-  if (lane < 16) {
-    double2 e = make_double2(e32[2 * lane], e32[2 * lane + 1]);
-    if (env_out) env_out[lane] = e;
-    if (beta != 0.0) {
-      const int a = lane >> 2, b = lane & 3;
-      double2 go = gout[4 * b + a];  // (G^dag)[a][b] = conj(G[b][a])
-      e = make_double2((1.0 - beta) * e.x + beta * go.x, (1.0 - beta) * e.y - beta * go.y);
+  // sigma_j = ||a_j|| (reduce over rows), sigma_max over columns
+  double nn = a.x * a.x + a.y * a.y;
+  nn += __shfl_xor_sync(FULL, nn, 4);
+  nn += __shfl_xor_sync(FULL, nn, 8);
+  const double sig = sqrt(nn);
+  double smax = sig;
+  smax = fmax(smax, __shfl_xor_sync(FULL, smax, 1));
+  smax = fmax(smax, __shfl_xor_sync(FULL, smax, 2));
+  const bool nul = !(sig > 1e-14 * smax) || smax == 0.0;
+  double2 xx = nul ? make_double2(0.0, 0.0) : make_double2(a.x / sig, a.y / sig);
+  if (__any_sync(FULL, nul)) {  // rare: complete the null columns of X
+    scratch[l] = xx;
+    __syncwarp();
+    const unsigned nm = __ballot_sync(FULL, nul && r == 0);  // bit (hb + j): column j null
+    const unsigned cols = (nm >> hb) & 0xFu;
+    if (l == 0 && cols) {
+      for (int jj = 0; jj < 4; ++jj) {
+        if (!((cols >> jj) & 1)) continue;
+        for (int e0 = 0; e0 < 4; ++e0) {
+          double2 u[4];
+          for (int q = 0; q < 4; ++q) u[q] = make_double2(q == e0 ? 1.0 : 0.0, 0.0);
+          for (int pass = 0; pass < 2; ++pass)
+            for (int q = 0; q < 4; ++q) {
+              if (q == jj || (((cols >> q) & 1) && q > jj)) continue;
+              double2 d = make_double2(0.0, 0.0);
+              for (int rr = 0; rr < 4; ++rr) cfma(d, cconj(scratch[4 * rr + q]), u[rr]);
+              for (int rr = 0; rr < 4; ++rr) {
+                const double2 tq = cmul(d, scratch[4 * rr + q]);
+                u[rr].x -= tq.x;
+                u[rr].y -= tq.y;
+              }
+            }
+          double nv = 0.0;
+          for (int rr = 0; rr < 4; ++rr) nv += u[rr].x * u[rr].x + u[rr].y * u[rr].y;
+          nv = sqrt(nv);
+          if (nv > 0.5) {
+            for (int rr = 0; rr < 4; ++rr) scratch[4 * rr + jj] = make_double2(u[rr].x / nv, u[rr].y / nv);
+            break;
+          }
+        }
+      }
     }
-    sA[lane] = e;
+    __syncwarp();
+    xx = scratch[l];
+    __syncwarp();
   }
-  __syncwarp();
-  warp_polar(sA, sV, sX, sG, sSig, lane);
-  if (lane < 16) gout[lane] = sG[lane];
-  if (lane == 0 && sig_out) *sig_out = *sSig;
+  // G[r][j] = sum_q V[r][q] conj(X[j][q])
+  double2 g = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) cfma(g, shfl_c(v, hb | (4 * r + q)), cconj(shfl_c(xx, hb | (4 * j + q))));
+  double ss = sig;                       // each column's lanes hold sigma_j
+  ss += __shfl_xor_sync(FULL, ss, 1);
+  ss += __shfl_xor_sync(FULL, ss, 2);
+  g_out = g;
+  v_out = v;
+  sig_sum = scalbn(ss, ex);
 }
 
-// Sum NV per-thread values over the CTA: warp shuffles, then warps in order.
-// Result in out[0..NV) (shared), valid after the trailing __syncthreads.
-template <int NV>
-__device__ void block_sum(double (&acc)[NV], double *red /*[nwarps][NV]*/, double *out) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-  for (int q = 0; q < NV; ++q) {
-    double v = acc[q];
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-    if (lane == 0) red[warp * NV + q] = v;
+// Polar step of one start by one warp (lanes 16-31 mirror lanes 0-15):
+// E' = (1 - beta) E + beta G_old^dag; writes G_i, V_i, sum sigma, E trace.
+__device__ void polar_write(const double *e32, double2 *gout, double2 *vslot, double beta,
+                            double *sig_out, double2 *env_out, double2 *scratch) {
+  const int lane = threadIdx.x & 31, l = lane & 15;
+  double2 e = make_double2(e32[2 * l], e32[2 * l + 1]);
+  if (env_out && lane < 16) env_out[l] = e;
+  if (beta != 0.0) {
+    const double2 go = gout[4 * (l & 3) + (l >> 2)];  // (G^dag)[r][j] = conj(G[j][r])
+    e = make_double2((1.0 - beta) * e.x + beta * go.x, (1.0 - beta) * e.y - beta * go.y);
   }
-  __syncthreads();
-  for (int q = threadIdx.x; q < NV; q += blockDim.x) {
-    double v = 0.0;
-    for (int w = 0; w < nw; ++w) v += red[w * NV + q];
-    out[q] = v;
+  const double2 v0 = vslot ? vslot[l] : make_double2((l % 5 == 0) ? 1.0 : 0.0, 0.0);
+  double2 g, v;
+  double ss;
+  hw_polar(e, v0, g, v, ss, scratch + (lane & 16));
+  __syncwarp();
+  if (lane < 16) {
+    gout[l] = g;
+    if (vslot) vslot[l] = v;
   }
-  __syncthreads();
+  if (lane == 0 && sig_out) *sig_out = ss;
 }
 
 // Last-CTA election for the per-start reduction of CTA partials.
@@ -218,7 +259,7 @@ __device__ bool elect_last(unsigned *counter, unsigned nb) {
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned t = atomicAdd(counter, 1u);
+    const unsigned t = atomicAdd(counter, 1u);
     last = (t == nb - 1);
     if (last) *counter = 0u;
   }
@@ -227,187 +268,280 @@ __device__ bool elect_last(unsigned *counter, unsigned nb) {
   return last;
 }
 
-// local index v of member l of the P-quadruple w (compile-time)
-template <int NU, int TP0, int TP1>
-__device__ constexpr int pv(int w, int l) {
-  int v = ((l & 1) << TP0) | (((l >> 1) & 1) << TP1);
-  int bit = 0;
-  for (int t = 0; t < NU; ++t) {
-    if (t == TP0 || t == TP1) continue;
-    v |= ((w >> bit) & 1) << t;
-    ++bit;
-  }
-  return v;
+// P-index (0..3) of local amplitude index v for the pair at local bits (TP0, TP1)
+template <int TP0, int TP1>
+__device__ __forceinline__ int pidx(int v) {
+  return ((v >> TP0) & 1) | (((v >> TP1) & 1) << 1);
 }
 
 // ---------------------------------------------------------------- backward --
-// Gate i of the right-to-left sweep (Fig. env_calc):
-//   if UPD: chi <- G_{i+1}^dag chi on the Q pair (local bits 0,1)
-//   E_i[a][b] += phi[idx_P(a)] conj(chi[idx_P(b)]) on the P pair (local TP0,TP1)
-// Each thread owns whole 2^NU-amplitude groups, so the chi update is in place
-// and race-free.  CTA partials -> last CTA per start reduces in CTA order and
-// (fuse_polar) runs the one-warp polar update of gate i.
+// Gate i of the right-to-left sweep (Fig. env_calc).  Work item =
+// (2^NU-amplitude group g, sample m), m fastest.  T = 2^(NU-2) threads share an
+// item: thread t owns the Q-quadruple whose local bits >= 2 equal t (local bits
+// 0,1 are the Q pair = gate i+1).  Per item:
+//   if UPD: chi <- G_{i+1}^dag chi on the thread's own Q-quadruple, written back;
+//   all-gather of the updated chi among the T threads (shfl_xor);
+//   E_i[a][b] += phi[v_a] conj(chi[v_b]) for each pair of members (v_a owned,
+//   v_b any) of one P-quadruple (the P pair = gate i sits at local TP0, TP1).
+// Accumulators are keyed by compile-time (la & PLO, lb & PLO, x); the target
+// entry (a, b) is fixed by the key and t, so each warp lane-group writes each
+// E entry exactly once in the CTA reduction (deterministic order).
 template <int NU, int TP0, int TP1, bool UPD>
-__global__ void __launch_bounds__(BWD_THREADS) bwd_kernel(const BwdParams P) {
-  constexpr int NV = 1 << NU;
-  constexpr int NQ = NV / 4;
+__global__ void __launch_bounds__(BWD_THREADS, 2) bwd_kernel(const BwdParams P) {
+  constexpr int T = 1 << (NU - 2);
+  constexpr int LPT = 32 / T;
+  constexpr int NWARP = BWD_THREADS / 32;
+  constexpr int PLO = ((TP0 < 2) ? (1 << TP0) : 0) | ((TP1 < 2) ? (1 << TP1) : 0);
+  constexpr int NPT_T = (((1 << NU) - 1) & ~((1 << TP0) | (1 << TP1))) >> 2;
   __shared__ double2 sQ[16];
-  __shared__ double red[(BWD_THREADS / 32) * 32];
+  __shared__ double2 red[NWARP][16];
   __shared__ double sum32[32];
-  __shared__ double2 sA[16], sV[16], sX[16], sG[16];
-  __shared__ double sSig;
+  __shared__ double2 scratch[32];
 
-  const int j = blockIdx.y;
-  const Slot sl = P.slots[j];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = lane / LPT, ml = lane % LPT;
+  const int jslot = blockIdx.y;
+  const Slot sl = P.slots[jslot];
   const int s = sl.s;
-  const int lgG = P.n - NU;
-  const long long N = 1LL << P.n;
-  const long long items = (long long)sl.m << lgG;
-  const long long chunk = (items + P.nb - 1) / P.nb;
-  const long long beg = (long long)blockIdx.x * chunk;
-  const long long end = min(items, beg + chunk);
+  const unsigned Ms = (unsigned)sl.m;
+  // work units = (group g, block of LPT consecutive samples); a warp takes one
+  // unit at a time, lane (t, ml) handling sample mb*LPT + ml, Q-quadruple t.
+  const unsigned nmb = (Ms + LPT - 1) / LPT;
+  const unsigned units = (1u << (P.n - NU)) * nmb;
+  const unsigned chunk = (units + P.nb - 1) / P.nb;
+  const unsigned beg = blockIdx.x * chunk;
+  const unsigned end = min(units, beg + chunk);
+  const FastDiv fdu(nmb);
 
   if (UPD && threadIdx.x < 16) {
     const int a = threadIdx.x >> 2, b = threadIdx.x & 3;
     const double2 g = P.gates[((long long)s * P.K + P.upd_gate) * 16 + 4 * b + a];
     sQ[threadIdx.x] = cconj(g);  // (G^dag)[a][b]
   }
+  if (P.dbg && threadIdx.x == 0) atomicMin(P.dbg + 4 * P.env_gate, gtimer());
   __syncthreads();
 
-  double acc[32];
+  double2 acc[4][4][T];
 #pragma unroll
-  for (int q = 0; q < 32; ++q) acc[q] = 0.0;
+  for (int p = 0; p < 4; ++p)
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int x = 0; x < T; ++x) acc[p][q][x] = make_double2(0.0, 0.0);
 
-  const double2 *csrc = P.chi_src.base + (long long)s * P.chi_src.stride_s * N;
-  double2 *cdst = P.chi_dst.base ? P.chi_dst.base + (long long)s * P.chi_dst.stride_s * N : nullptr;
-  const double2 *fsrc = P.phi.base + (long long)s * P.phi.stride_s * N;
+  const double2 *csrc = P.chi_src.base + (long long)s * P.chi_src.ss;
+  double2 *cdst = P.chi_dst.base ? P.chi_dst.base + (long long)s * P.chi_dst.ss : nullptr;
+  const double2 *fsrc = P.phi.base + (long long)s * P.phi.ss;
+  const long long csa = P.chi_src.sa, csm = P.chi_src.sm;
+  const long long dsa = P.chi_dst.sa, dsm = P.chi_dst.sm;
+  const long long fsa = P.phi.sa, fsm = P.phi.sm;
+  long long offc[4], offd[4], offf[4];  // own Q-quadruple amplitude offsets per view
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    const long long o = P.off[4 * t + l];
+    offc[l] = o * csa;
+    offd[l] = o * dsa;
+    offf[l] = o * fsa;
+  }
 
-  for (long long w = beg + threadIdx.x; w < end; w += blockDim.x) {
-    const long long m = w >> lgG;
-    long long g = w & ((1LL << lgG) - 1);
+  // Items of this thread: w_k = beg + warp*LPT + k*NWARP*LPT + ml.  Their 8
+  // amplitudes (own Q-quadruple of chi and phi) are staged into shared memory
+  // with LDGSTS, BWD_STAGES-1 items ahead, so the bytes in flight are bounded
+  // by shared memory rather than registers.  Each thread reads back only its
+  // own slots: cp.async.wait_group suffices, no CTA barrier in the loop.
+  extern __shared__ double2 stage_buf[];  // [BWD_STAGES][8][BWD_THREADS]
+  const unsigned ustart = beg + warp;
+  const int iters = ustart < end ? (int)((end - ustart + NWARP - 1) / NWARP) : 0;
+  auto locate = [&](int k, unsigned &g, unsigned &m) -> bool {
+    const unsigned u = ustart + (unsigned)k * NWARP;
+    if (k >= iters) return false;
+    g = fdu.div(u);
+    m = (u - g * nmb) * LPT + ml;
 #pragma unroll
-    for (int t = 0; t < NU; ++t) g = insert_zero(g, P.ins[t]);
-    const long long rowoff = m * N + g;
-    double2 c[NV];
+    for (int q = 0; q < NU; ++q) g = insert_zero32(g, P.ins[q]);
+    return m < Ms;
+  };
+  auto issue = [&](int k) {
+    unsigned g = 0, m = 0;
+    const bool ok = locate(k, g, m);
+    double2 *st = stage_buf + (k % BWD_STAGES) * 8 * BWD_THREADS + threadIdx.x;
+    const double2 *cp = csrc + (long long)g * csa + (long long)m * csm;
+    const double2 *fp = fsrc + (long long)g * fsa + (long long)m * fsm;
 #pragma unroll
-    for (int v = 0; v < NV; ++v) c[v] = csrc[rowoff + P.off[v]];
+    for (int l = 0; l < 4; ++l) cp_async16(st + l * BWD_THREADS, ok ? cp + offc[l] : csrc, ok);
+#pragma unroll
+    for (int l = 0; l < 4; ++l) cp_async16(st + (4 + l) * BWD_THREADS, ok ? fp + offf[l] : fsrc, ok);
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int k = 0; k < BWD_STAGES - 1; ++k) issue(k);
+
+  for (int k = 0; k < iters; ++k) {
+    issue(k + BWD_STAGES - 1);
+    cp_async_wait<BWD_STAGES - 1>();
+    unsigned g = 0, m = 0;
+    const bool valid = locate(k, g, m);
+    const double2 *st = stage_buf + (k % BWD_STAGES) * 8 * BWD_THREADS + threadIdx.x;
+    double2 c[4], f[4];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) c[l] = st[l * BWD_THREADS];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) f[l] = st[(4 + l) * BWD_THREADS];
     if (UPD) {
+      double2 o[4];
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        double2 o[4];
+      for (int a = 0; a < 4; ++a) {
+        o[a] = make_double2(0.0, 0.0);
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          o[a] = make_double2(0.0, 0.0);
-#pragma unroll
-          for (int b = 0; b < 4; ++b) cfma(o[a], sQ[4 * a + b], c[4 * q + b]);
-        }
-#pragma unroll
-        for (int a = 0; a < 4; ++a) c[4 * q + a] = o[a];
+        for (int b = 0; b < 4; ++b) cfma(o[a], sQ[4 * a + b], c[b]);
       }
-      if (cdst) {
 #pragma unroll
-        for (int v = 0; v < NV; ++v) cdst[rowoff + P.off[v]] = c[v];
+      for (int a = 0; a < 4; ++a) c[a] = o[a];
+      if (cdst && valid) {
+        double2 *dp = cdst + (long long)g * dsa + (long long)m * dsm;
+#pragma unroll
+        for (int l = 0; l < 4; ++l) dp[offd[l]] = c[l];
       }
     }
+    // all-gather of chi among the T threads of the item, then the environment terms
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      double2 f[4];
+    for (int x = 0; x < T; ++x) {
+      if ((x & NPT_T) != 0) continue;  // partner differs in a non-P bit: no shared P-quadruple
+      double2 cx[4];
 #pragma unroll
-      for (int l = 0; l < 4; ++l) f[l] = fsrc[rowoff + P.off[pv<NU, TP0, TP1>(q, l)]];
+      for (int l = 0; l < 4; ++l) cx[l] = x == 0 ? c[l] : shfl_xor_c(c[l], x * LPT);
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+      for (int la = 0; la < 4; ++la)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const double2 cb = c[pv<NU, TP0, TP1>(q, b)];
-          // f[a] * conj(cb)
-          acc[8 * a + 2 * b] = fma(f[a].x, cb.x, acc[8 * a + 2 * b]);
-          acc[8 * a + 2 * b] = fma(f[a].y, cb.y, acc[8 * a + 2 * b]);
-          acc[8 * a + 2 * b + 1] = fma(f[a].y, cb.x, acc[8 * a + 2 * b + 1]);
-          acc[8 * a + 2 * b + 1] = fma(-f[a].x, cb.y, acc[8 * a + 2 * b + 1]);
+        for (int lb = 0; lb < 4; ++lb) {
+          if (((la ^ lb) & ~PLO & 3) != 0) continue;
+          double2 &e = acc[la & PLO][lb & PLO][x];
+          // f[la] * conj(cx[lb])
+          e.x = fma(f[la].x, cx[lb].x, e.x);
+          e.x = fma(f[la].y, cx[lb].y, e.x);
+          e.y = fma(f[la].y, cx[lb].x, e.y);
+          e.y = fma(-f[la].x, cx[lb].y, e.y);
         }
     }
   }
+  cp_async_wait<0>();
 
-  block_sum<32>(acc, red, sum32);
-  if (threadIdx.x < 32)
-    P.partials[((long long)j * P.nb + blockIdx.x) * 32 + threadIdx.x] = sum32[threadIdx.x];
-  if (!elect_last(&P.counters[j], (unsigned)P.nb)) return;
-  if (threadIdx.x < 32) {
-    double e = 0.0;
-    const double *pp = P.partials + (long long)j * P.nb * 32 + threadIdx.x;
-    for (int b = 0; b < P.nb; ++b) e += __ldcg(pp + (long long)b * 32);
-    sum32[threadIdx.x] = e;
-    if (!P.fuse_polar) P.e_red[(long long)j * 32 + threadIdx.x] = e;
-  }
+  // CTA reduction: over the sample lanes of each lane-group, then warps in order
+#pragma unroll
+  for (int pa = 0; pa < 4; ++pa)
+#pragma unroll
+    for (int pb = 0; pb < 4; ++pb)
+#pragma unroll
+      for (int x = 0; x < T; ++x) {
+        if ((pa & ~PLO) || (pb & ~PLO) || (x & NPT_T)) continue;
+        double2 v = acc[pa][pb][x];
+#pragma unroll
+        for (int o = LPT / 2; o >= 1; o >>= 1) {
+          v.x += __shfl_xor_sync(FULL, v.x, o);
+          v.y += __shfl_xor_sync(FULL, v.y, o);
+        }
+        if (ml == 0) {
+          const int a = pidx<TP0, TP1>(pa | (t << 2));
+          const int b = pidx<TP0, TP1>(pb | ((t ^ x) << 2));
+          red[warp][4 * a + b] = v;
+        }
+      }
   __syncthreads();
-  if (!P.fuse_polar || threadIdx.x >= 32) return;
-  double2 *gout = P.gates_w + ((long long)s * P.K + P.env_gate) * 16;
-  polar_from_reduced(sum32, gout, P.beta, P.sig ? P.sig + (long long)s * P.K + P.env_gate : nullptr,
-                     P.env_trace ? P.env_trace + ((long long)P.env_gate * P.S + s) * 16 : nullptr,
-                     sA, sV, sX, sG, &sSig, threadIdx.x);
+  if (threadIdx.x < 32) {
+    const int e = threadIdx.x >> 1, im = threadIdx.x & 1;
+    double v = 0.0;
+#pragma unroll
+    for (int wq = 0; wq < NWARP; ++wq) v += im ? red[wq][e].y : red[wq][e].x;
+    P.partials[((long long)jslot * P.nb + blockIdx.x) * 32 + threadIdx.x] = v;
+  }
+  if (!elect_last(&P.counters[jslot], (unsigned)P.nb)) return;
+  if (threadIdx.x >= 32) return;
+  if (P.dbg && threadIdx.x == 0) atomicMax(P.dbg + 4 * P.env_gate + 1, gtimer());
+  {
+    const double *pp = P.partials + (long long)jslot * P.nb * 32 + threadIdx.x;
+    double e = 0.0;
+    int b = 0;
+    for (; b + 4 <= P.nb; b += 4) {  // loads batched, adds in CTA order
+      const double x0 = __ldcg(pp + (long long)b * 32), x1 = __ldcg(pp + (long long)(b + 1) * 32);
+      const double x2 = __ldcg(pp + (long long)(b + 2) * 32), x3 = __ldcg(pp + (long long)(b + 3) * 32);
+      e += x0; e += x1; e += x2; e += x3;
+    }
+    for (; b < P.nb; ++b) e += __ldcg(pp + (long long)b * 32);
+    sum32[threadIdx.x] = e;
+    if (!P.fuse_polar) P.e_red[(long long)jslot * 32 + threadIdx.x] = e;
+  }
+  __syncwarp();
+  if (P.dbg && threadIdx.x == 0) atomicMax(P.dbg + 4 * P.env_gate + 2, gtimer());
+  if (!P.fuse_polar) return;
+  const long long gi = (long long)s * P.K + P.env_gate;
+  polar_write(sum32, P.gates_w + gi * 16, P.vprev ? P.vprev + gi * 16 : nullptr, P.beta,
+              P.sig ? P.sig + gi : nullptr,
+              P.env_trace ? P.env_trace + ((long long)P.env_gate * P.S + s) * 16 : nullptr, scratch);
+  if (P.dbg && threadIdx.x == 0) atomicMax(P.dbg + 4 * P.env_gate + 3, gtimer());
 }
 
-// polar step alone (sample-sharded mode, after the NCCL all-reduce of E)
+// polar step alone (sample-sharded mode, after the NCCL all-reduce of E): one warp per start
 __global__ void polar_kernel(const PolarParams P) {
-  __shared__ double2 sA[4][16], sV[4][16], sX[4][16], sG[4][16];
-  __shared__ double sSig[4];
   __shared__ double e32[4][32];
+  __shared__ double2 scratch[4][32];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int j = blockIdx.x * 4 + w;
   if (j >= P.n_slots) return;
   const Slot sl = P.slots[j];
   e32[w][lane] = P.e_red[(long long)j * 32 + lane];
   __syncwarp();
-  double2 *gout = P.gates + ((long long)sl.s * P.K + P.gate) * 16;
-  polar_from_reduced(e32[w], gout, P.beta, P.sig ? P.sig + (long long)sl.s * P.K + P.gate : nullptr,
-                     P.env_trace ? P.env_trace + ((long long)P.gate * P.S + sl.s) * 16 : nullptr,
-                     sA[w], sV[w], sX[w], sG[w], &sSig[w], lane);
+  const long long gi = (long long)sl.s * P.K + P.gate;
+  polar_write(e32[w], P.gates + gi * 16, P.vprev ? P.vprev + gi * 16 : nullptr, P.beta,
+              P.sig ? P.sig + gi : nullptr,
+              P.env_trace ? P.env_trace + ((long long)P.gate * P.S + sl.s) * 16 : nullptr, scratch[w]);
 }
 
 // --------------------------------------------------------------- final cost --
-__global__ void __launch_bounds__(RED_THREADS) final_kernel(const FinalParams P) {
+__global__ void __launch_bounds__(RED_THREADS, 4) final_kernel(const FinalParams P) {
   __shared__ double2 sQ[16];
   __shared__ double red[RED_THREADS / 32];
-  __shared__ double tot;
   const int j = blockIdx.y;
   const Slot sl = P.slots[j];
   const int s = sl.s;
-  const long long N = 1LL << P.n;
-  const long long items = (long long)sl.m << (P.n - 2);
-  const long long chunk = (items + P.nb - 1) / P.nb;
-  const long long beg = (long long)blockIdx.x * chunk, end = min(items, beg + chunk);
+  const unsigned Ms = (unsigned)sl.m;
+  const unsigned items = Ms << (P.n - 2);
+  const unsigned chunk = (items + P.nb - 1) / P.nb;
+  const unsigned beg = blockIdx.x * chunk, end = min(items, beg + chunk);
+  const FastDiv fdm(Ms);
   if (threadIdx.x < 16) {
     const int a = threadIdx.x >> 2, b = threadIdx.x & 3;
     sQ[threadIdx.x] = cconj(P.gates[(long long)s * P.K * 16 + 4 * b + a]);
   }
   __syncthreads();
   const int lo = min(P.p0, P.p1), hi = max(P.p0, P.p1);
-  const long long o1 = 1LL << P.p0, o2 = 1LL << P.p1;
-  const double2 *c = P.chi.base + (long long)s * P.chi.stride_s * N;
-  const double2 *x = P.x.base + (long long)s * P.x.stride_s * N;
+  const unsigned o[4] = {0u, 1u << P.p0, 1u << P.p1, (1u << P.p0) | (1u << P.p1)};
+  const double2 *cb = P.chi.base + (long long)s * P.chi.ss;
+  const double2 *xb = P.x.base + (long long)s * P.x.ss;
   double acc = 0.0;
-  for (long long w = beg + threadIdx.x; w < end; w += blockDim.x) {
-    const long long m = w >> (P.n - 2);
-    const long long r = w & ((1LL << (P.n - 2)) - 1);
-    const long long base = m * N + insert_zero(insert_zero(r, lo), hi);
-    const long long off[4] = {0, o1, o2, o1 | o2};
-    double2 v[4];
+  for (unsigned w = beg + threadIdx.x; w < end; w += blockDim.x) {
+    const unsigned q = fdm.div(w);
+    const unsigned m = w - q * Ms;
+    const unsigned base = insert_zero32(insert_zero32(q, lo), hi);
+    const double2 *cp = cb + (long long)base * P.chi.sa + (long long)m * P.chi.sm;
+    const double2 *xp = xb + (long long)base * P.x.sa + (long long)m * P.x.sm;
+    double2 v[4], xv[4];
 #pragma unroll
-    for (int l = 0; l < 4; ++l) v[l] = __ldcg(c + base + off[l]);
+    for (int l = 0; l < 4; ++l) v[l] = cp[(long long)o[l] * P.chi.sa];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) xv[l] = __ldcs(xp + (long long)o[l] * P.x.sa);
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
-      double2 o = make_double2(0.0, 0.0);
+      double2 r = make_double2(0.0, 0.0);
 #pragma unroll
-      for (int b = 0; b < 4; ++b) cfma(o, sQ[4 * a + b], v[b]);
-      const double2 xv = __ldcs(x + base + off[a]);
-      const double dr = o.x - xv.x, di = o.y - xv.y;
+      for (int b = 0; b < 4; ++b) cfma(r, sQ[4 * a + b], v[b]);
+      const double dr = r.x - xv[a].x, di = r.y - xv[a].y;
       acc = fma(dr, dr, acc);
       acc = fma(di, di, acc);
     }
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+  for (int q = 16; q >= 1; q >>= 1) acc += __shfl_xor_sync(FULL, acc, q);
   if (lane == 0) red[warp] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -423,37 +557,95 @@ __global__ void __launch_bounds__(RED_THREADS) final_kernel(const FinalParams P)
   }
 }
 
-// -------------------------------------------------------- forward (rows) ----
-// One CTA per (start, row): the whole 2^n row lives in shared memory; the K
-// (or K-1) gates are applied in order, gate k+1 is staged while gate k runs.
-__global__ void __launch_bounds__(FWD_THREADS) fwd_row_kernel(const FwdRowParams P) {
-  extern __shared__ double2 row[];
-  __shared__ double2 sG[2][16];
-  __shared__ double red[FWD_THREADS / 32];
+// ------------------------------------------------------ forward (per gate) --
+// B_{k+1} = G_k B_k for every (quadruple, sample) of every active start.
+__global__ void __launch_bounds__(FWD_THREADS, 3) fwd_gate_kernel(const FwdGateParams P) {
+  __shared__ double2 sG[16];
   const int j = blockIdx.y;
   const Slot sl = P.slots[j];
   const int s = sl.s;
-  const int nrows = P.mode == 0 ? sl.m : P.rows;
-  const int m = blockIdx.x;
-  if (m >= nrows) return;
-  const long long N = 1LL << P.n;
-  const int ngates = P.mode == 0 ? P.K - 1 : P.K;
-  const double2 *src = P.src.base + ((long long)s * P.src.stride_s + m) * N;
-  for (long long i = threadIdx.x; i < N; i += blockDim.x) row[i] = __ldcs(src + i);
-  const double2 *gs = P.gates + (long long)s * P.K * 16;
-  if (threadIdx.x < 16 && ngates > 0) sG[0][threadIdx.x] = gs[threadIdx.x];
+  const unsigned Ms = (unsigned)(P.rows_fixed > 0 ? P.rows_fixed : sl.m);
+  const unsigned items = Ms << (P.n - 2);
+  const unsigned chunk = (items + P.nb - 1) / P.nb;
+  const unsigned beg = blockIdx.x * chunk, end = min(items, beg + chunk);
+  const FastDiv fdm(Ms);
+  if (threadIdx.x < 16) sG[threadIdx.x] = P.gates[((long long)s * P.K + P.k) * 16 + threadIdx.x];
   __syncthreads();
-  for (int k = 0; k < ngates; ++k) {
+  const int lo = min(P.p0, P.p1), hi = max(P.p0, P.p1);
+  const long long so1 = (1LL << P.p0) * P.src.sa, so2 = (1LL << P.p1) * P.src.sa;
+  const long long do1 = (1LL << P.p0) * P.dst.sa, do2 = (1LL << P.p1) * P.dst.sa;
+  const long long soff[4] = {0, so1, so2, so1 + so2}, doff[4] = {0, do1, do2, do1 + do2};
+  const double2 *src = P.src.base + (long long)s * P.src.ss;
+  double2 *dst = P.dst.base + (long long)s * P.dst.ss;
+  // LDGSTS pipeline (FWD_STAGES-1 items ahead per thread, own slots only)
+  extern __shared__ double2 fstage[];  // [FWD_STAGES][4][FWD_THREADS]
+  const unsigned stride = blockDim.x;
+  const int iters = beg + threadIdx.x < end ? (int)((end - beg - threadIdx.x + stride - 1) / stride) : 0;
+  auto locate = [&](int k, unsigned &base, unsigned &m) -> bool {
+    const unsigned w = beg + threadIdx.x + (unsigned)k * stride;
+    if (k >= iters) return false;
+    const unsigned q = fdm.div(w);
+    m = w - q * Ms;
+    base = insert_zero32(insert_zero32(q, lo), hi);
+    return true;
+  };
+  auto issue = [&](int k) {
+    unsigned base = 0, m = 0;
+    const bool ok = locate(k, base, m);
+    double2 *stp = fstage + (k % FWD_STAGES) * 4 * FWD_THREADS + threadIdx.x;
+    const double2 *sp = src + (long long)base * P.src.sa + (long long)m * P.src.sm;
+#pragma unroll
+    for (int l = 0; l < 4; ++l) cp_async16(stp + l * FWD_THREADS, ok ? sp + soff[l] : src, ok);
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int k = 0; k < FWD_STAGES - 1; ++k) issue(k);
+  for (int k = 0; k < iters; ++k) {
+    issue(k + FWD_STAGES - 1);
+    cp_async_wait<FWD_STAGES - 1>();
+    unsigned base = 0, m = 0;
+    locate(k, base, m);
+    const double2 *stp = fstage + (k % FWD_STAGES) * 4 * FWD_THREADS + threadIdx.x;
+    double2 v[4];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) v[l] = stp[l * FWD_THREADS];
+    double2 *dp = dst + (long long)base * P.dst.sa + (long long)m * P.dst.sm;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      double2 r = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) cfma(r, sG[4 * a + b], v[b]);
+      dp[doff[a]] = r;
+    }
+  }
+  cp_async_wait<0>();
+}
+
+// --------------------------------------------------- validation (row in SMEM) --
+// One CTA per (start, validation row): the whole 2^n row lives in shared
+// memory, the K gates are applied in order (gate k+1 staged while gate k runs),
+// then the row's squared distance to yv.
+__global__ void __launch_bounds__(VAL_THREADS) val_row_kernel(const ValRowParams P) {
+  extern __shared__ double2 row[];
+  __shared__ double2 sG[2][16];
+  __shared__ double red[VAL_THREADS / 32];
+  const int j = blockIdx.y;
+  const int s = P.slots[j].s;
+  const int m = blockIdx.x;
+  const long long N = 1LL << P.n;
+  const double2 *src = P.xv + (long long)m * N;
+  for (long long i = threadIdx.x; i < N; i += blockDim.x) row[i] = __ldg(src + i);
+  const double2 *gs = P.gates + (long long)s * P.K * 16;
+  if (threadIdx.x < 16) sG[0][threadIdx.x] = gs[threadIdx.x];
+  __syncthreads();
+  for (int k = 0; k < P.K; ++k) {
     const int2 pr = __ldg(P.pairs + k);
     const double2 *G = sG[k & 1];
     double2 nxt;
-    const bool stage = threadIdx.x < 16 && k + 1 < ngates;
+    const bool stage = threadIdx.x < 16 && k + 1 < P.K;
     if (stage) nxt = gs[(long long)(k + 1) * 16 + threadIdx.x];
     const int lo = min(pr.x, pr.y), hi = max(pr.x, pr.y);
     const long long o1 = 1LL << pr.x, o2 = 1LL << pr.y;
-    double2 *dst = P.mode == 0 ? P.B + (long long)k * P.b_gate_stride +
-                                     ((long long)s * P.b_stride_s + m) * N
-                               : nullptr;
     for (long long r = threadIdx.x; r < (N >> 2); r += blockDim.x) {
       const long long base = insert_zero(insert_zero(r, lo), hi);
       const long long off[4] = {base, base | o1, base | o2, base | o1 | o2};
@@ -468,68 +660,27 @@ __global__ void __launch_bounds__(FWD_THREADS) fwd_row_kernel(const FwdRowParams
       }
 #pragma unroll
       for (int a = 0; a < 4; ++a) row[off[a]] = o[a];
-      if (dst) {
-#pragma unroll
-        for (int a = 0; a < 4; ++a) dst[off[a]] = o[a];
-      }
     }
     if (stage) sG[(k + 1) & 1][threadIdx.x] = nxt;
     __syncthreads();
   }
-  if (P.mode == 1) {
-    const double2 *ref = P.ref.base + ((long long)s * P.ref.stride_s + m) * N;
-    double acc = 0.0;
-    for (long long i = threadIdx.x; i < N; i += blockDim.x) {
-      const double2 a = row[i], b = __ldcs(ref + i);
-      const double dr = a.x - b.x, di = a.y - b.y;
-      acc = fma(dr, dr, acc);
-      acc = fma(di, di, acc);
-    }
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
-    if (lane == 0) red[warp] = acc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += red[q];
-      P.row_out[(long long)j * P.rows + m] = t;
-    }
+  const double2 *ref = P.yv + (long long)m * N;
+  double acc = 0.0;
+  for (long long i = threadIdx.x; i < N; i += blockDim.x) {
+    const double2 a = row[i], b = __ldg(ref + i);
+    const double dr = a.x - b.x, di = a.y - b.y;
+    acc = fma(dr, dr, acc);
+    acc = fma(di, di, acc);
   }
-}
-
-// ------------------------------------------------------ forward (per gate) --
-__global__ void __launch_bounds__(RED_THREADS) fwd_gate_kernel(const FwdGateParams P) {
-  __shared__ double2 sG[16];
-  const int j = blockIdx.y;
-  const Slot sl = P.slots[j];
-  const int s = sl.s;
-  const int rows = P.rows_fixed > 0 ? P.rows_fixed : sl.m;
-  const long long N = 1LL << P.n;
-  const long long items = (long long)rows << (P.n - 2);
-  const long long chunk = (items + P.nb - 1) / P.nb;
-  const long long beg = (long long)blockIdx.x * chunk, end = min(items, beg + chunk);
-  if (threadIdx.x < 16) sG[threadIdx.x] = P.gates[((long long)s * P.K + P.k) * 16 + threadIdx.x];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 16; q >= 1; q >>= 1) acc += __shfl_xor_sync(FULL, acc, q);
+  if (lane == 0) red[warp] = acc;
   __syncthreads();
-  const int lo = min(P.p0, P.p1), hi = max(P.p0, P.p1);
-  const long long o1 = 1LL << P.p0, o2 = 1LL << P.p1;
-  const double2 *src = P.src.base + (long long)s * P.src.stride_s * N;
-  double2 *dst = P.dst.base + (long long)s * P.dst.stride_s * N;
-  for (long long w = beg + threadIdx.x; w < end; w += blockDim.x) {
-    const long long m = w >> (P.n - 2);
-    const long long r = w & ((1LL << (P.n - 2)) - 1);
-    const long long base = m * N + insert_zero(insert_zero(r, lo), hi);
-    const long long off[4] = {base, base | o1, base | o2, base | o1 | o2};
-    double2 v[4];
-#pragma unroll
-    for (int l = 0; l < 4; ++l) v[l] = src[off[l]];
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      double2 o = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int b = 0; b < 4; ++b) cfma(o, sG[4 * a + b], v[b]);
-      dst[off[a]] = o;
-    }
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += red[q];
+    P.row_out[(long long)j * P.rows + m] = t;
   }
 }
 
@@ -539,18 +690,18 @@ __global__ void __launch_bounds__(RED_THREADS) dist_kernel(const DistParams P) {
   const int j = blockIdx.y, m = blockIdx.x;
   const Slot sl = P.slots[j];
   const long long N = 1LL << P.n;
-  const double2 *a = P.a.base + ((long long)sl.s * P.a.stride_s + m) * N;
-  const double2 *b = P.b.base + ((long long)sl.s * P.b.stride_s + m) * N;
+  const double2 *a = P.a.base + (long long)sl.s * P.a.ss + (long long)m * P.a.sm;
+  const double2 *b = P.b.base + (long long)sl.s * P.b.ss + (long long)m * P.b.sm;
   double acc = 0.0;
   for (long long i = threadIdx.x; i < N; i += blockDim.x) {
-    const double2 u = a[i], v = b[i];
+    const double2 u = a[i * P.a.sa], v = b[i * P.b.sa];
     const double dr = u.x - v.x, di = u.y - v.y;
     acc = fma(dr, dr, acc);
     acc = fma(di, di, acc);
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+  for (int q = 16; q >= 1; q >>= 1) acc += __shfl_xor_sync(FULL, acc, q);
   if (lane == 0) red[warp] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -567,6 +718,39 @@ __global__ void row_reduce_kernel(const double *row_in, int rows, double *out, i
   double t = 0.0;
   for (int r = 0; r < rows; ++r) t += row_in[(long long)j * rows + r];
   out[j] = t;
+}
+
+// [rows][cols] -> [cols][rows] (pools to the sample-minor layout), 32x32 tiles
+__global__ void transpose_kernel(const double2 *src, double2 *dst, int rows, long long cols) {
+  __shared__ double2 tile[32][33];
+  const long long c0 = (long long)blockIdx.x * 32;
+  const int r0 = blockIdx.y * 32;
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const int r = r0 + dy;
+    const long long c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[dy][threadIdx.x] = src[(long long)r * cols + c];
+  }
+  __syncthreads();
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const long long c = c0 + dy;
+    const int r = r0 + threadIdx.x;
+    if (r < rows && c < cols) dst[c * rows + r] = tile[threadIdx.x][dy];
+  }
+}
+
+__global__ void identity_fill_kernel(double2 *v, long long count16) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count16 * 16;
+       i += (long long)gridDim.x * blockDim.x)
+    v[i] = make_double2((i % 16) % 5 == 0 ? 1.0 : 0.0, 0.0);
+}
+
+// non-finite detection over a sample array (ERR_NUMERIC check on the device)
+__global__ void finite_check_kernel(const double *p, long long n, int *flag) {
+  int bad = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    bad |= !isfinite(p[i]);
+  if (__any_sync(FULL, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
 }
 
 // ---------------------------------------------------------------- unit ops --
@@ -594,32 +778,48 @@ __global__ void apply_kernel(const ApplyParams P) {
   }
 }
 
+// two matrices per warp (one per 16-lane half), cold start (V_0 = I)
 __global__ void polar_batch_kernel(const double2 *env, const double2 *g_old, double beta,
                                    double2 *g_new, double *sig, int count) {
-  __shared__ double2 sA[4][16], sV[4][16], sX[4][16], sG[4][16];
-  __shared__ double sSig[4];
-  __shared__ double e32[4][32];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i = blockIdx.x * 4 + w;
-  if (i >= count) return;
-  const double *ep = reinterpret_cast<const double *>(env + (long long)i * 16);
-  e32[w][lane] = ep[lane];
-  if (lane < 16) g_new[(long long)i * 16 + lane] = g_old[(long long)i * 16 + lane];
-  __syncwarp();
-  polar_from_reduced(e32[w], g_new + (long long)i * 16, beta, sig + i, nullptr, sA[w], sV[w],
-                     sX[w], sG[w], &sSig[w], lane);
+  __shared__ double2 scratch[4][32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, l = lane & 15;
+  const int i = (blockIdx.x * 4 + w) * 2 + (lane >> 4);
+  const bool valid = i < count;
+  const int ii = valid ? i : count - 1;  // keep the whole warp converged
+  double2 e = env[(long long)ii * 16 + l];
+  if (beta != 0.0) {
+    const double2 go = g_old[(long long)ii * 16 + 4 * (l & 3) + (l >> 2)];
+    e = make_double2((1.0 - beta) * e.x + beta * go.x, (1.0 - beta) * e.y - beta * go.y);
+  }
+  const double2 v0 = make_double2((l % 5 == 0) ? 1.0 : 0.0, 0.0);
+  double2 g, v;
+  double ss;
+  hw_polar(e, v0, g, v, ss, scratch[w] + (lane & 16));
+  if (valid) {
+    g_new[(long long)i * 16 + l] = g;
+    if (l == 0) sig[i] = ss;
+  }
 }
 
 }  // namespace
 
 // ================================================================ launchers ==
-int bwd_threads() { return BWD_THREADS; }
-int fwd_row_max_n() { return 13; }
+int val_row_max_n() { return 13; }
+int blocks_per_sm(int nu) { (void)nu; return 2; }
 
 cudaError_t launch_bwd(const BwdParams &p, int n_slots, int tp0, int tp1, bool upd,
                        cudaStream_t st) {
   dim3 grid(p.nb, n_slots), block(BWD_THREADS);
-#define QFS_BWD(NU, A, B, U) bwd_kernel<NU, A, B, U><<<grid, block, 0, st>>>(p)
+  const int smem = BWD_STAGES * 8 * BWD_THREADS * (int)sizeof(double2);
+#define QFS_BWD(NU, A, B, U)                                                                   \
+  do {                                                                                         \
+    static bool attr = false;                                                                  \
+    if (!attr) {                                                                               \
+      cudaFuncSetAttribute(bwd_kernel<NU, A, B, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+      attr = true;                                                                             \
+    }                                                                                          \
+    bwd_kernel<NU, A, B, U><<<grid, block, smem, st>>>(p);                                     \
+  } while (0)
   if (!upd) {
     QFS_BWD(2, 0, 1, false);
   } else if (p.nu == 2) {
@@ -648,20 +848,25 @@ cudaError_t launch_final(const FinalParams &p, int n_slots, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_fwd_row(const FwdRowParams &p, int n_slots, int max_rows, cudaStream_t st) {
-  const size_t smem = sizeof(double2) << p.n;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(fwd_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         sizeof(double2) << 13);
-    attr_set = true;
+cudaError_t launch_fwd_gate(const FwdGateParams &p, int n_slots, cudaStream_t st) {
+  const int smem = FWD_STAGES * 4 * FWD_THREADS * (int)sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(fwd_gate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
   }
-  fwd_row_kernel<<<dim3(max_rows, n_slots), FWD_THREADS, smem, st>>>(p);
+  fwd_gate_kernel<<<dim3(p.nb, n_slots), FWD_THREADS, smem, st>>>(p);
   return cudaGetLastError();
 }
 
-cudaError_t launch_fwd_gate(const FwdGateParams &p, int n_slots, cudaStream_t st) {
-  fwd_gate_kernel<<<dim3(p.nb, n_slots), RED_THREADS, 0, st>>>(p);
+cudaError_t launch_val_row(const ValRowParams &p, int n_slots, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(val_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(double2) << 13));
+    attr_set = true;
+  }
+  val_row_kernel<<<dim3(p.rows, n_slots), VAL_THREADS, sizeof(double2) << p.n, st>>>(p);
   return cudaGetLastError();
 }
 
@@ -687,7 +892,30 @@ cudaError_t launch_apply(const ApplyParams &p, cudaStream_t st) {
 
 cudaError_t launch_polar_batch(const double2 *env, const double2 *g_old, double beta,
                                double2 *g_new, double *sig, int count, cudaStream_t st) {
-  polar_batch_kernel<<<(count + 3) / 4, 128, 0, st>>>(env, g_old, beta, g_new, sig, count);
+  polar_batch_kernel<<<(count + 7) / 8, 128, 0, st>>>(env, g_old, beta, g_new, sig, count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_transpose(const double2 *src, double2 *dst, int rows, long long cols,
+                             cudaStream_t st) {
+  dim3 grid((unsigned)((cols + 31) / 32), (rows + 31) / 32), block(32, 8);
+  transpose_kernel<<<grid, block, 0, st>>>(src, dst, rows, cols);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finite_check(const double *p, long long n, int *flag, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  long long blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  finite_check_kernel<<<(unsigned)blocks, 256, 0, st>>>(p, n, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_identity_fill(double2 *v, long long count16, cudaStream_t st) {
+  if (count16 <= 0) return cudaSuccess;
+  long long blocks = (count16 * 16 + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  identity_fill_kernel<<<(unsigned)blocks, 256, 0, st>>>(v, count16);
   return cudaGetLastError();
 }
 

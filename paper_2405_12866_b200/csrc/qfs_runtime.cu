@@ -16,6 +16,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -29,14 +30,18 @@ namespace {
 
 enum KClass { K_FWD_ROW = 0, K_FWD_GATE, K_BWD, K_POLAR, K_FINAL, K_VAL_ROW, K_DIST, K_REDUCE,
               K_NCCL, K_OP, K_NCLASS };
-const char *kClassName[K_NCLASS] = {"fwd_row", "fwd_gate", "bwd", "polar", "final",
-                                    "val_row", "dist", "row_reduce", "nccl_allreduce", "unit_op"};
+// profiling classes: fwd_gate / bwd / final / validation are PHASES (one event
+// pair around the whole run of launches of that step of the sweep)
+const char *kClassName[K_NCLASS] = {"unused", "fwd_gate", "bwd", "polar", "final",
+                                    "validation", "dist", "row_reduce", "nccl_allreduce", "unit_op"};
 
 struct ProfRec {
   int cls;
   cudaEvent_t e0, e1;
   double bytes, flops;
+  long long n;  // kernel launches covered by the event pair
 };
+struct PhaseScope;
 
 }  // namespace
 
@@ -46,6 +51,13 @@ struct qfs_ctx {
   std::vector<int32_t> pairs;
   int2 *d_pairs = nullptr;
   cudaStream_t st = nullptr;
+  cudaStream_t cur_st = nullptr;       // stream of the launches being issued
+  // lockstep start groups on parallel streams (one group's polar tail overlaps
+  // another group's contraction); QFS_GROUPS overrides the default
+  static constexpr int GMAX = 8;
+  int groups = 1;
+  cudaStream_t gst[GMAX] = {nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join[GMAX] = {nullptr};
   // distribution
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1, mode = 0;
@@ -53,9 +65,11 @@ struct qfs_ctx {
   // samples
   int m_pool = 0, V = 0;
   bool have_samples = false;
-  double2 *d_x = nullptr, *d_y = nullptr, *d_xv = nullptr, *d_yv = nullptr;
+  double2 *d_x = nullptr, *d_y = nullptr;    // pools, TRANSPOSED: [2^n][m_pool] (sample-minor)
+  double2 *d_xv = nullptr, *d_yv = nullptr;  // validation, row-major [V][2^n]
   // work buffers
   int G_cap = 0, S_cap = 0, M_cap = 0, V_cap = 0, nb_cap = 0;
+  double2 *d_vprev = nullptr;  // [S][K][16] right singular vectors of the last polar step (warm start)
   double2 *d_gates = nullptr, *d_chi = nullptr, *d_B = nullptr, *d_vb0 = nullptr, *d_vb1 = nullptr;
   double *d_partials = nullptr, *d_ered = nullptr, *d_sig = nullptr, *d_csum = nullptr,
          *d_rowout = nullptr, *d_cval = nullptr;
@@ -64,18 +78,26 @@ struct qfs_ctx {
   double *h_csum = nullptr, *h_cval = nullptr;  // pinned
   double2 *d_env_trace = nullptr;
   size_t env_trace_cap = 0;
+  double2 *d_stage = nullptr;  // row-major staging of the pools for the transpose
+  size_t stage_bytes = 0;
   // graph cache
   cudaGraphExec_t gexec = nullptr;
   long long gkey[8] = {0};
   long long glaunches = 0;
   // profiling
-  bool prof = false;
-  std::vector<ProfRec> prec;
+  bool prof = false, capturing = false;
+  PhaseScope *phase = nullptr;  // open profiling phase (event pair around a run of launches)
+  std::vector<ProfRec> prec;   // eager launches (events released after collection)
+  std::vector<ProfRec> gprec;  // event nodes of the cached graph (kept with the graph)
   std::vector<cudaEvent_t> ev_pool;
   double p_ms[K_NCLASS] = {0}, p_bytes[K_NCLASS] = {0}, p_flops[K_NCLASS] = {0};
   long long p_cnt[K_NCLASS] = {0};
   long long launches = 0;
   std::string err;
+  // diagnostics (env QFS_TAIL_TIMING=1): per-gate globaltimer stamps of bwd
+  unsigned long long *d_dbg = nullptr;
+  std::vector<double> dbg_acc;  // [3]: main phase, partial reduce, polar (ns, summed)
+  long long dbg_n = 0;
 };
 
 namespace {
@@ -116,6 +138,38 @@ cudaEvent_t take_event(qfs_ctx *c) {
   cudaEventCreate(&e);
   return e;
 }
+void record_event(qfs_ctx *c, cudaEvent_t e) {
+  // inside stream capture the record becomes an event node of the graph
+  if (c->capturing) cudaEventRecordWithFlags(e, c->cur_st, cudaEventRecordExternal);
+  else cudaEventRecord(e, c->cur_st);
+}
+// A run of launches of one kernel class timed by ONE event pair on the
+// launching stream (forward phase, backward phase, ...): per-launch event
+// pairs would serialise the graph and inflate every kernel's duration.
+struct PhaseScope {
+  qfs_ctx *c;
+  int cls;
+  cudaEvent_t e0 = nullptr;
+  double bytes = 0, flops = 0;
+  long long n = 0;
+  PhaseScope(qfs_ctx *c_, int cls_) : c(c_), cls(cls_) {
+    c->phase = this;
+    if (c->prof) {
+      e0 = take_event(c);
+      record_event(c, e0);
+    }
+  }
+  ~PhaseScope() {
+    c->phase = nullptr;
+    if (c->prof) {
+      cudaEvent_t e1 = take_event(c);
+      record_event(c, e1);
+      (c->capturing ? c->gprec : c->prec).push_back({cls, e0, e1, bytes, flops, n});
+    }
+  }
+};
+// One kernel launch: counted, and attributed to the open phase (or, for the
+// unit ops outside any phase, timed by its own event pair).
 struct LaunchScope {
   qfs_ctx *c;
   int cls;
@@ -123,19 +177,42 @@ struct LaunchScope {
   cudaEvent_t e0 = nullptr;
   LaunchScope(qfs_ctx *c_, int cls_, double b, double f) : c(c_), cls(cls_), bytes(b), flops(f) {
     c->launches++;
-    if (c->prof) {
+    if (c->phase) {
+      c->phase->bytes += b;
+      c->phase->flops += f;
+      c->phase->n += 1;
+    } else if (c->prof) {
       e0 = take_event(c);
-      cudaEventRecord(e0, c->st);
+      record_event(c, e0);
     }
   }
   ~LaunchScope() {
-    if (c->prof) {
+    if (!c->phase && c->prof) {
       cudaEvent_t e1 = take_event(c);
-      cudaEventRecord(e1, c->st);
-      c->prec.push_back({cls, e0, e1, bytes, flops});
+      record_event(c, e1);
+      (c->capturing ? c->gprec : c->prec).push_back({cls, e0, e1, bytes, flops, 1});
     }
   }
 };
+
+// accumulate the event pairs of one replay of the cached graph (after a sync)
+void prof_collect_graph(qfs_ctx *c) {
+  for (auto &r : c->gprec) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, r.e0, r.e1);
+    c->p_ms[r.cls] += ms;
+    c->p_cnt[r.cls] += r.n;
+    c->p_bytes[r.cls] += r.bytes;
+    c->p_flops[r.cls] += r.flops;
+  }
+}
+
+void drop_graph(qfs_ctx *c) {
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  c->gexec = nullptr;
+  for (auto &r : c->gprec) { c->ev_pool.push_back(r.e0); c->ev_pool.push_back(r.e1); }
+  c->gprec.clear();
+}
 
 void prof_collect(qfs_ctx *c) {
   if (c->prec.empty()) return;
@@ -144,7 +221,7 @@ void prof_collect(qfs_ctx *c) {
     float ms = 0;
     cudaEventElapsedTime(&ms, r.e0, r.e1);
     c->p_ms[r.cls] += ms;
-    c->p_cnt[r.cls] += 1;
+    c->p_cnt[r.cls] += r.n;
     c->p_bytes[r.cls] += r.bytes;
     c->p_flops[r.cls] += r.flops;
     c->ev_pool.push_back(r.e0);
@@ -178,9 +255,12 @@ bool unitary_all(const double *g, size_t count) {
   return true;
 }
 
-int blocks_per_start(long long items, int n_slots) {
-  const int target = 148 * 4;
-  long long nb = (target + n_slots - 1) / n_slots;
+// CTAs per start: one full wave over the 148 SMs (resident CTAs per SM = bpsm),
+// never more CTAs than 256-item chunks.
+constexpr int kMaxBlocksPerStart = 148 * 4;
+int blocks_per_start(long long items, int n_slots, int bpsm = 4) {
+  const int target = 148 * std::min(bpsm, 4);
+  long long nb = target / n_slots;
   long long maxnb = (items + 255) / 256;
   if (nb > maxnb) nb = maxnb;
   if (nb < 1) nb = 1;
@@ -193,7 +273,7 @@ size_t plan_bytes(const qfs_ctx *c, int S, int M, int V, int nb) {
   size_t b = 0;
   b += (size_t)S * M * N * 16;                             // chi
   if (c->K > 1) b += (size_t)(c->K - 1) * S * M * N * 16;  // B cache
-  if (c->n > fwd_row_max_n() && V > 0) b += 2 * (size_t)S * V * N * 16;
+  if (c->n > val_row_max_n() && V > 0) b += 2 * (size_t)S * V * N * 16;
   b += (size_t)S * nb * 32 * 8 + (size_t)S * 64 * 8 + (size_t)S * c->K * 8 + (size_t)S * (V + 4) * 8;
   return b;
 }
@@ -201,10 +281,12 @@ size_t plan_bytes(const qfs_ctx *c, int S, int M, int V, int nb) {
 qfs_status ensure_gates(qfs_ctx *c, int S) {
   if (S <= c->G_cap) return QFS_OK;
   dfree(c->d_gates);
+  dfree(c->d_vprev);
   c->G_cap = 0;
   CUDA_TRY(c, cudaMalloc(&c->d_gates, (size_t)S * c->K * 16 * sizeof(double2)));
+  CUDA_TRY(c, cudaMalloc(&c->d_vprev, (size_t)S * c->K * 16 * sizeof(double2)));
   c->G_cap = S;
-  if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+  drop_graph(c);
   return QFS_OK;
 }
 
@@ -212,7 +294,7 @@ qfs_status ensure_gates(qfs_ctx *c, int S) {
 // starts of up to M local rows.  Contents are rebuilt every sweep, so growing
 // (on a double-and-restart) may discard them; the gates live elsewhere.
 qfs_status ensure_state(qfs_ctx *c, int S, int M, int V) {
-  const int nb = blocks_per_start(((long long)M * c->N) >> 2, 1);
+  const int nb = kMaxBlocksPerStart;  // any launch: nb <= 148 * 4 (blocks_per_start)
   if (S <= c->S_cap && M <= c->M_cap && V <= c->V_cap && nb <= c->nb_cap) return QFS_OK;
   S = std::max(S, c->S_cap);
   M = std::max(M, c->M_cap);
@@ -226,7 +308,7 @@ qfs_status ensure_state(qfs_ctx *c, int S, int M, int V) {
   if (c->h_cval) cudaFreeHost(c->h_cval);
   c->h_csum = c->h_cval = nullptr;
   c->S_cap = c->M_cap = c->V_cap = c->nb_cap = 0;
-  if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+  drop_graph(c);
   size_t need = plan_bytes(c, S, M, V, nbc);
   size_t fr = 0, tot = 0;
   CUDA_TRY(c, cudaMemGetInfo(&fr, &tot));
@@ -239,7 +321,7 @@ qfs_status ensure_state(qfs_ctx *c, int S, int M, int V) {
   const size_t N = (size_t)c->N;
   CUDA_TRY(c, cudaMalloc(&c->d_chi, (size_t)S * M * N * sizeof(double2)));
   if (c->K > 1) CUDA_TRY(c, cudaMalloc(&c->d_B, (size_t)(c->K - 1) * S * M * N * sizeof(double2)));
-  if (c->n > fwd_row_max_n() && V > 0) {
+  if (c->n > val_row_max_n() && V > 0) {
     CUDA_TRY(c, cudaMalloc(&c->d_vb0, (size_t)S * V * N * sizeof(double2)));
     CUDA_TRY(c, cudaMalloc(&c->d_vb1, (size_t)S * V * N * sizeof(double2)));
   }
@@ -268,44 +350,51 @@ struct SweepSpec {
   int S = 0;                     // total starts (trace layout / strides)
 };
 
-// Issue one sweep's launches on c->st (no host synchronisation).
-qfs_status issue_sweep(qfs_ctx *c, const SweepSpec &sp) {
-  const int ns = (int)sp.slots.size();
+// Issue the launches of one sweep for the slots [j0, j1) on stream st (no host
+// synchronisation).  Scratch arrays indexed by slot are offset by j0.
+qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStream_t st) {
+  const int ns = j1 - j0;
   const int K = c->K, n = c->n;
+  c->cur_st = st;
+  int M_max = 0;
+  for (int j = j0; j < j1; ++j) M_max = std::max(M_max, sp.slots[j].m);
+  const Slot *slots = c->d_slots + j0;
+  double *partials = c->d_partials + (long long)j0 * c->nb_cap * 32;
+  unsigned *cnt_b = c->d_counters + j0, *cnt_f = c->d_counters + c->S_cap + j0;
+  double *ered = c->d_ered + (long long)j0 * 32, *csum = c->d_csum + j0, *cval = c->d_cval + j0;
+  double *rowout = c->d_rowout + (long long)j0 * std::max(c->V, 1);
   const long long N = c->N;
   const long long Mc = c->M_cap;
-  const Rows xpool{c->d_x, 0}, ypool{c->d_y, 0};
+  const View xpool{c->d_x, 0, c->m_pool, 1}, ypool{c->d_y, 0, c->m_pool, 1};
+  const long long sS = N * Mc;                      // per-start stride of chi / B
+  auto Bk = [&](int k) -> double2 * { return c->d_B + (long long)(k - 1) * c->S_cap * sS; };
   double units = 0;  // amplitudes of all active training rows
-  for (auto &s : sp.slots) units += (double)s.m * (double)N;
-  // (a) forward: B_1 .. B_{K-1}
+  for (int j = j0; j < j1; ++j) units += (double)sp.slots[j].m * (double)N;
+  // (a) forward: B_1 .. B_{K-1}, one coalesced launch per gate
   if (K > 1) {
-    if (n <= fwd_row_max_n()) {
-      FwdRowParams f{};
-      f.n = n; f.K = K; f.mode = 0; f.rows = 0; f.slots = c->d_slots; f.pairs = c->d_pairs;
-      f.gates = c->d_gates; f.src = xpool; f.B = c->d_B;
-      f.b_gate_stride = (long long)c->S_cap * Mc * N; f.b_stride_s = Mc;
-      LaunchScope ls(c, K_FWD_ROW, units * (16.0 + 16.0 * (K - 1)), units * 32.0 * (K - 1));
-      CUDA_TRY(c, launch_fwd_row(f, ns, sp.M_max, c->st));
-    } else {
-      for (int k = 0; k + 1 < K; ++k) {
-        FwdGateParams f{};
-        f.n = n; f.k = k; f.K = K; f.rows_fixed = 0; f.slots = c->d_slots;
-        f.p0 = c->pairs[2 * k]; f.p1 = c->pairs[2 * k + 1]; f.gates = c->d_gates;
-        f.nb = blocks_per_start(((long long)sp.M_max * N) >> 2, ns);
-        f.src = k == 0 ? xpool : Rows{c->d_B + (long long)(k - 1) * c->S_cap * Mc * N, Mc};
-        f.dst = RowsW{c->d_B + (long long)k * c->S_cap * Mc * N, Mc};
-        LaunchScope ls(c, K_FWD_GATE, units * 32.0, units * 32.0);
-        CUDA_TRY(c, launch_fwd_gate(f, ns, c->st));
-      }
-    }
+  PhaseScope phase_fwd(c, K_FWD_GATE);
+  for (int k = 0; k + 1 < K; ++k) {
+    FwdGateParams f{};
+    f.n = n; f.k = k; f.K = K; f.rows_fixed = 0; f.slots = slots;
+    f.p0 = c->pairs[2 * k]; f.p1 = c->pairs[2 * k + 1]; f.gates = c->d_gates;
+    f.nb = blocks_per_start(((long long)M_max * N) >> 2, ns, 3);
+    f.src = k == 0 ? xpool : View{Bk(k), sS, Mc, 1};
+    f.dst = ViewW{Bk(k + 1), sS, Mc, 1};
+    LaunchScope ls(c, K_FWD_GATE, units * 32.0, units * 32.0);
+    CUDA_TRY(c, launch_fwd_gate(f, ns, st));
+  }
   }
   // (b, c) backward: gate i = K-1 .. 0 (P:112 right to left; Fig. env_calc)
+  {
+  PhaseScope phase_bwd(c, K_BWD);
   for (int i = K - 1; i >= 0; --i) {
     BwdParams b{};
-    b.n = n; b.K = K; b.slots = c->d_slots; b.gates = c->d_gates; b.gates_w = c->d_gates;
-    b.partials = c->d_partials; b.counters = c->d_counters; b.e_red = c->d_ered;
+    b.n = n; b.K = K; b.slots = slots; b.gates = c->d_gates; b.gates_w = c->d_gates;
+    b.partials = partials; b.counters = cnt_b; b.e_red = ered;
     b.fuse_polar = (c->mode == 1 && c->world > 1) ? 0 : 1;
     b.beta = sp.beta; b.sig = c->d_sig; b.env_trace = sp.env_trace; b.S = sp.S;
+    b.vprev = c->d_vprev;
+    b.dbg = c->d_dbg;
     const bool upd = i < K - 1;
     b.upd_gate = upd ? i + 1 : -1;
     b.env_gate = i;
@@ -337,76 +426,103 @@ qfs_status issue_sweep(qfs_ctx *c, const SweepSpec &sp) {
         if ((v >> t) & 1) o |= 1LL << loc[t];
       b.off[v] = v < (1 << nu) ? o : 0;
     }
-    b.chi_src = (i >= K - 2) ? ypool : Rows{c->d_chi, Mc};
-    b.chi_dst = upd ? RowsW{c->d_chi, Mc} : RowsW{nullptr, 0};
-    b.phi = i == 0 ? xpool : Rows{c->d_B + (long long)(i - 1) * c->S_cap * Mc * N, Mc};
-    b.nb = blocks_per_start(((long long)sp.M_max * N) >> nu, ns);
+    b.chi_src = (i >= K - 2) ? ypool : View{c->d_chi, sS, Mc, 1};
+    b.chi_dst = upd ? ViewW{c->d_chi, sS, Mc, 1} : ViewW{nullptr, 0, 0, 0};
+    b.phi = i == 0 ? xpool : View{Bk(i), sS, Mc, 1};
+    {
+      const long long lpt = 32 >> (nu - 2);
+      const long long units = (N >> nu) * ((M_max + lpt - 1) / lpt);
+      b.nb = blocks_per_start(units * 32, ns, blocks_per_sm(nu));
+    }
     {
       LaunchScope ls(c, K_BWD, units * (upd ? 48.0 : 32.0), units * (upd ? 64.0 : 32.0));
-      CUDA_TRY(c, launch_bwd(b, ns, tp0, tp1, upd, c->st));
+      CUDA_TRY(c, launch_bwd(b, ns, tp0, tp1, upd, st));
     }
     if (!b.fuse_polar) {
       {
         LaunchScope ls(c, K_NCCL, 0, 0);
-        NCCL_TRY(c, ncclAllReduce(c->d_ered, c->d_ered, (size_t)ns * 32, ncclFloat64, ncclSum,
-                                  c->comm, c->st));
+        NCCL_TRY(c, ncclAllReduce(ered, ered, (size_t)ns * 32, ncclFloat64, ncclSum,
+                                  c->comm, st));
       }
       PolarParams pp{};
-      pp.K = K; pp.gate = i; pp.S = sp.S; pp.n_slots = ns; pp.slots = c->d_slots;
-      pp.e_red = c->d_ered; pp.gates = c->d_gates; pp.beta = sp.beta; pp.sig = c->d_sig;
-      pp.env_trace = sp.env_trace;
+      pp.K = K; pp.gate = i; pp.S = sp.S; pp.n_slots = ns; pp.slots = slots;
+      pp.e_red = ered; pp.gates = c->d_gates; pp.beta = sp.beta; pp.sig = c->d_sig;
+      pp.env_trace = sp.env_trace; pp.vprev = c->d_vprev;
       LaunchScope ls(c, K_POLAR, 0, 0);
-      CUDA_TRY(c, launch_polar(pp, ns, c->st));
+      CUDA_TRY(c, launch_polar(pp, ns, st));
     }
+  }
   }
   // (d) c_train = (1/M) sum ||G_0^dag chi - x||^2   (direct form R6)
   {
+    PhaseScope phase_final(c, K_FINAL);
     FinalParams fp{};
-    fp.n = n; fp.slots = c->d_slots;
-    fp.chi = K == 1 ? ypool : Rows{c->d_chi, Mc};
+    fp.n = n; fp.slots = slots;
+    fp.chi = K == 1 ? ypool : View{c->d_chi, sS, Mc, 1};
     fp.x = xpool; fp.p0 = c->pairs[0]; fp.p1 = c->pairs[1]; fp.gates = c->d_gates; fp.K = K;
-    fp.partials = c->d_partials; fp.counters = c->d_counters + c->S_cap; fp.out_sum = c->d_csum;
-    fp.nb = blocks_per_start(((long long)sp.M_max * N) >> 2, ns);
+    fp.partials = partials; fp.counters = cnt_f; fp.out_sum = csum;
+    fp.nb = blocks_per_start(((long long)M_max * N) >> 2, ns);
     LaunchScope ls(c, K_FINAL, units * 32.0, units * 35.0);
-    CUDA_TRY(c, launch_final(fp, ns, c->st));
+    CUDA_TRY(c, launch_final(fp, ns, st));
   }
   if (c->mode == 1 && c->world > 1) {
     LaunchScope ls(c, K_NCCL, 0, 0);
-    NCCL_TRY(c, ncclAllReduce(c->d_csum, c->d_csum, ns, ncclFloat64, ncclSum, c->comm, c->st));
+    NCCL_TRY(c, ncclAllReduce(csum, csum, ns, ncclFloat64, ncclSum, c->comm, st));
   }
   // validation cost with the post-sweep gates
   if (sp.want_val && c->V > 0) {
+    PhaseScope phase_val(c, K_VAL_ROW);
     const double vunits = (double)ns * c->V * (double)N;
-    if (n <= fwd_row_max_n()) {
-      FwdRowParams f{};
-      f.n = n; f.K = K; f.mode = 1; f.rows = c->V; f.slots = c->d_slots; f.pairs = c->d_pairs;
-      f.gates = c->d_gates; f.src = Rows{c->d_xv, 0}; f.ref = Rows{c->d_yv, 0};
-      f.row_out = c->d_rowout;
+    if (n <= val_row_max_n()) {
+      ValRowParams f{};
+      f.n = n; f.K = K; f.rows = c->V; f.slots = slots; f.pairs = c->d_pairs;
+      f.gates = c->d_gates; f.xv = c->d_xv; f.yv = c->d_yv; f.row_out = rowout;
       LaunchScope ls(c, K_VAL_ROW, vunits * 32.0, vunits * 32.0 * K);
-      CUDA_TRY(c, launch_fwd_row(f, ns, c->V, c->st));
+      CUDA_TRY(c, launch_val_row(f, ns, st));
     } else {
+      const long long VN = (long long)c->V * N;
       for (int k = 0; k < K; ++k) {
         FwdGateParams f{};
-        f.n = n; f.k = k; f.K = K; f.rows_fixed = c->V; f.slots = c->d_slots;
+        f.n = n; f.k = k; f.K = K; f.rows_fixed = c->V; f.slots = slots;
         f.p0 = c->pairs[2 * k]; f.p1 = c->pairs[2 * k + 1]; f.gates = c->d_gates;
         f.nb = blocks_per_start(((long long)c->V * N) >> 2, ns);
         double2 *dst = (k & 1) ? c->d_vb1 : c->d_vb0;
         const double2 *src = k == 0 ? c->d_xv : ((k & 1) ? c->d_vb0 : c->d_vb1);
-        f.src = Rows{src, k == 0 ? 0 : (long long)c->V};
-        f.dst = RowsW{dst, (long long)c->V};
+        f.src = View{src, k == 0 ? 0 : VN, 1, N};
+        f.dst = ViewW{dst, VN, 1, N};
         LaunchScope ls(c, K_FWD_GATE, vunits * 32.0, vunits * 32.0);
-        CUDA_TRY(c, launch_fwd_gate(f, ns, c->st));
+        CUDA_TRY(c, launch_fwd_gate(f, ns, st));
       }
       DistParams d{};
-      d.n = n; d.rows = c->V; d.slots = c->d_slots;
-      d.a = Rows{((K - 1) & 1) ? c->d_vb1 : c->d_vb0, (long long)c->V};
-      d.b = Rows{c->d_yv, 0}; d.row_out = c->d_rowout;
+      d.n = n; d.rows = c->V; d.slots = slots;
+      d.a = View{((K - 1) & 1) ? c->d_vb1 : c->d_vb0, VN, 1, N};
+      d.b = View{c->d_yv, 0, 1, N}; d.row_out = rowout;
       LaunchScope ls(c, K_DIST, vunits * 32.0, vunits * 3.0);
-      CUDA_TRY(c, launch_dist(d, ns, c->st));
+      CUDA_TRY(c, launch_dist(d, ns, st));
     }
     LaunchScope ls(c, K_REDUCE, 0, 0);
-    CUDA_TRY(c, launch_row_reduce(c->d_rowout, c->V, c->d_cval, ns, c->st));
+    CUDA_TRY(c, launch_row_reduce(rowout, c->V, cval, ns, st));
   }
+  return QFS_OK;
+}
+
+// Issue one sweep: the active slots are split into lockstep groups, each on
+// its own stream (parallel graph branches), joined back into c->st.
+qfs_status issue_sweep(qfs_ctx *c, const SweepSpec &sp) {
+  const int ns = (int)sp.slots.size();
+  int G = std::min(c->groups, ns);
+  if (c->mode == 1 && c->world > 1) G = 1;  // NCCL calls stay on one stream, one order
+  if (G <= 1) return issue_group(c, sp, 0, ns, c->st);
+  CUDA_TRY(c, cudaEventRecord(c->ev_fork, c->st));
+  for (int g = 0; g < G; ++g) {
+    const int j0 = (int)((long long)ns * g / G), j1 = (int)((long long)ns * (g + 1) / G);
+    CUDA_TRY(c, cudaStreamWaitEvent(c->gst[g], c->ev_fork, 0));
+    qfs_status r = issue_group(c, sp, j0, j1, c->gst[g]);
+    if (r != QFS_OK) return r;
+    CUDA_TRY(c, cudaEventRecord(c->ev_join[g], c->gst[g]));
+  }
+  for (int g = 0; g < G; ++g) CUDA_TRY(c, cudaStreamWaitEvent(c->st, c->ev_join[g], 0));
+  c->cur_st = c->st;
   return QFS_OK;
 }
 
@@ -417,16 +533,23 @@ qfs_status run_sweep(qfs_ctx *c, const SweepSpec &sp, std::vector<double> &csum,
   const int ns = (int)sp.slots.size();
   CUDA_TRY(c, cudaMemcpyAsync(c->d_slots, sp.slots.data(), ns * sizeof(Slot),
                               cudaMemcpyHostToDevice, c->st));
-  const bool use_graph = !c->prof && sp.env_trace == nullptr;
+  if (c->d_dbg) {
+    std::vector<unsigned long long> init((size_t)4 * c->K);
+    for (int i = 0; i < c->K; ++i) { init[4 * i] = ~0ull; init[4 * i + 1] = init[4 * i + 2] = init[4 * i + 3] = 0; }
+    CUDA_TRY(c, cudaMemcpy(c->d_dbg, init.data(), init.size() * 8, cudaMemcpyHostToDevice));
+  }
+  const bool use_graph = sp.env_trace == nullptr;
   if (use_graph) {
     long long key[8] = {ns, sp.M_max, sp.want_val, (long long)(sp.beta * 1e15), sp.S, c->S_cap,
-                        c->M_cap, 1};
+                        c->M_cap, (c->prof ? 2 : 1) + 4 * c->groups};
     if (!c->gexec || std::memcmp(key, c->gkey, sizeof key) != 0) {
-      if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+      drop_graph(c);
       cudaGraph_t g;
       CUDA_TRY(c, cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
       long long before = c->launches;
+      c->capturing = true;
       qfs_status s = issue_sweep(c, sp);
+      c->capturing = false;
       cudaError_t e = cudaStreamEndCapture(c->st, &g);
       if (s != QFS_OK) return s;
       if (e != cudaSuccess) return fail(c, QFS_ERR_DEVICE, std::string("graph capture: ") + cudaGetErrorString(e));
@@ -449,7 +572,21 @@ qfs_status run_sweep(qfs_ctx *c, const SweepSpec &sp, std::vector<double> &csum,
   csum.assign(c->h_csum, c->h_csum + ns);
   if (sp.want_val && c->V > 0) cval.assign(c->h_cval, c->h_cval + ns);
   else cval.assign(ns, NAN);
-  if (c->prof) prof_collect(c);
+  if (c->prof) {
+    if (use_graph) prof_collect_graph(c);
+    prof_collect(c);
+  }
+  if (c->d_dbg) {
+    std::vector<unsigned long long> h((size_t)4 * c->K);
+    CUDA_TRY(c, cudaMemcpy(h.data(), c->d_dbg, h.size() * 8, cudaMemcpyDeviceToHost));
+    if (c->dbg_acc.empty()) c->dbg_acc.assign(3, 0.0);
+    for (int i = 0; i < c->K; ++i) {
+      c->dbg_acc[0] += (double)(h[4 * i + 1] - h[4 * i]);
+      c->dbg_acc[1] += (double)(h[4 * i + 2] - h[4 * i + 1]);
+      c->dbg_acc[2] += (double)(h[4 * i + 3] - h[4 * i + 2]);
+      c->dbg_n++;
+    }
+  }
   return QFS_OK;
 }
 
@@ -458,6 +595,8 @@ qfs_status upload_gates(qfs_ctx *c, int s, const double *init) {
   if (!unitary_all(init, (size_t)s * c->K)) return fail(c, QFS_ERR_NUMERIC, "initial gate not unitary (tol 1e-10)");
   CUDA_TRY(c, cudaMemcpyAsync(c->d_gates, init, (size_t)s * c->K * 16 * sizeof(double2),
                               cudaMemcpyHostToDevice, c->st));
+  CUDA_TRY(c, launch_identity_fill(c->d_vprev, (long long)s * c->K, c->st));
+  c->launches++;
   return QFS_OK;
 }
 
@@ -485,10 +624,20 @@ qfs_status create_common(int n, int k, const int32_t *pairs, int device, qfs_ctx
   if (e == cudaSuccess) e = cudaMalloc(&c->d_pairs, k * sizeof(int2));
   if (e == cudaSuccess) e = cudaMemcpy(c->d_pairs, pairs, k * sizeof(int2), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_flag, 4 * sizeof(int));
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+  for (int g = 0; g < qfs_ctx::GMAX && e == cudaSuccess; ++g) {
+    e = cudaStreamCreateWithFlags(&c->gst[g], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join[g], cudaEventDisableTiming);
+  }
+  c->cur_st = c->st;
+  if (const char *gs = getenv("QFS_GROUPS")) c->groups = std::max(1, std::min(qfs_ctx::GMAX, atoi(gs)));
   if (e != cudaSuccess) {
     c->err = std::string("device init: ") + cudaGetErrorString(e);
     *out = c;  // caller can read the error, then destroy
     return QFS_ERR_DEVICE;
+  }
+  if (getenv("QFS_TAIL_TIMING")) {
+    cudaMalloc(&c->d_dbg, (size_t)4 * k * sizeof(unsigned long long));
   }
   *out = c;
   return QFS_OK;
@@ -530,18 +679,12 @@ static qfs_status set_samples_impl(qfs_ctx *c, int m_pool, const void *x, const 
     return fail(c, QFS_ERR_ARG, "bad sample arguments");
   if ((long long)m_pool * (c->mode == 1 ? c->world : 1) > c->N)
     return fail(c, QFS_ERR_CAPACITY, "m_pool > 2^n");
-  if (kind == cudaMemcpyHostToDevice) {
-    if (!finite_all((const double *)x, (size_t)m_pool * c->N * 2) ||
-        !finite_all((const double *)y, (size_t)m_pool * c->N * 2) ||
-        (v > 0 && (!finite_all((const double *)xv, (size_t)v * c->N * 2) ||
-                   !finite_all((const double *)yv, (size_t)v * c->N * 2))))
-      return fail(c, QFS_ERR_NUMERIC, "non-finite sample");
-  }
   CUDA_TRY(c, cudaSetDevice(c->device));
   if (m_pool != c->m_pool) {
     dfree(c->d_x); dfree(c->d_y);
     CUDA_TRY(c, cudaMalloc(&c->d_x, (size_t)m_pool * c->N * sizeof(double2)));
     CUDA_TRY(c, cudaMalloc(&c->d_y, (size_t)m_pool * c->N * sizeof(double2)));
+    c->m_pool = 0;
   }
   if (v != c->V) {
     dfree(c->d_xv); dfree(c->d_yv);
@@ -552,15 +695,34 @@ static qfs_status set_samples_impl(qfs_ctx *c, int m_pool, const void *x, const 
   }
   cudaStream_t st = kind == cudaMemcpyHostToDevice ? c->st : ust;
   const size_t rb = (size_t)c->N * sizeof(double2);
-  CUDA_TRY(c, cudaMemcpyAsync(c->d_x, x, m_pool * rb, kind, st));
-  CUDA_TRY(c, cudaMemcpyAsync(c->d_y, y, m_pool * rb, kind, st));
+  // stage the row-major pools, then transpose to the sample-minor layout
+  if ((size_t)m_pool * rb > c->stage_bytes) {
+    dfree(c->d_stage);
+    CUDA_TRY(c, cudaMalloc(&c->d_stage, (size_t)m_pool * rb));
+    c->stage_bytes = (size_t)m_pool * rb;
+  }
+  CUDA_TRY(c, cudaMemsetAsync(c->d_flag, 0, sizeof(int), st));
+  for (int q = 0; q < 2; ++q) {
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_stage, q == 0 ? x : y, m_pool * rb, kind, st));
+    CUDA_TRY(c, launch_finite_check((const double *)c->d_stage, (long long)m_pool * c->N * 2, c->d_flag, st));
+    CUDA_TRY(c, launch_transpose(c->d_stage, q == 0 ? c->d_x : c->d_y, m_pool, c->N, st));
+  }
   if (v > 0) {
     CUDA_TRY(c, cudaMemcpyAsync(c->d_xv, xv, v * rb, kind, st));
     CUDA_TRY(c, cudaMemcpyAsync(c->d_yv, yv, v * rb, kind, st));
+    CUDA_TRY(c, launch_finite_check((const double *)c->d_xv, (long long)v * c->N * 2, c->d_flag, st));
+    CUDA_TRY(c, launch_finite_check((const double *)c->d_yv, (long long)v * c->N * 2, c->d_flag, st));
   }
+  int bad = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(&bad, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(c, cudaStreamSynchronize(st));
+  c->launches += v > 0 ? 6 : 4;
   c->m_pool = m_pool; c->V = v; c->have_samples = true;
-  if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+  if (bad) {
+    c->have_samples = false;
+    return fail(c, QFS_ERR_NUMERIC, "non-finite sample");
+  }
+  drop_graph(c);
   return QFS_OK;
 }
 
@@ -771,6 +933,7 @@ qfs_status qfs_op_apply(qfs_ctx *c, int p0, int p1, const double *g, int dagger,
   a.psi = d;
   cudaError_t e = cudaMemcpy(d, psi, bytes, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) {
+    c->cur_st = c->st;
     LaunchScope ls(c, K_OP, 2.0 * bytes, 32.0 * m * c->N);
     e = launch_apply(a, c->st);
   }
@@ -793,7 +956,7 @@ qfs_status qfs_op_environment(qfs_ctx *c, int p0, int p1, int m, const double *p
   Slot *dsl = nullptr;
   BwdParams b{};
   b.n = c->n; b.K = 1; b.nu = 2;
-  b.nb = blocks_per_start(((long long)m * c->N) >> 2, 1);
+  b.nb = blocks_per_start((c->N >> 2) * ((m + 31) / 32) * 32, 1, 2);
   cudaError_t e = cudaMalloc(&dphi, bytes);
   if (e == cudaSuccess) e = cudaMalloc(&dchi, bytes);
   if (e == cudaSuccess) e = cudaMalloc(&dpart, (size_t)b.nb * 32 * sizeof(double));
@@ -806,13 +969,15 @@ qfs_status qfs_op_environment(qfs_ctx *c, int p0, int p1, int m, const double *p
   if (e == cudaSuccess) e = cudaMemset(dcnt, 0, sizeof(unsigned));
   if (e == cudaSuccess) e = cudaMemcpy(dsl, &sl, sizeof sl, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) {
-    b.slots = dsl; b.chi_src = Rows{dchi, 0}; b.chi_dst = RowsW{nullptr, 0}; b.phi = Rows{dphi, 0};
+    b.slots = dsl; b.chi_src = View{dchi, 0, 1, c->N}; b.chi_dst = ViewW{nullptr, 0, 0, 0};
+    b.phi = View{dphi, 0, 1, c->N};
     int lo = std::min(p0, p1), hi = std::max(p0, p1);
     b.ins[0] = lo; b.ins[1] = hi;
     for (int v = 0; v < 16; ++v)
       b.off[v] = v < 4 ? (((long long)(v & 1) << p0) | ((long long)((v >> 1) & 1) << p1)) : 0;
     b.partials = dpart; b.counters = dcnt; b.e_red = dred; b.fuse_polar = 0; b.env_gate = 0;
     b.upd_gate = -1; b.S = 1;
+    c->cur_st = c->st;
     LaunchScope ls(c, K_OP, 2.0 * bytes, 32.0 * m * c->N);
     e = launch_bwd(b, 1, 0, 1, false, c->st);
   }
@@ -838,6 +1003,7 @@ qfs_status qfs_op_polar(qfs_ctx *c, int count, const double *env, const double *
   if (e == cudaSuccess) e = cudaMemcpy(de, env, mb, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(dg, g_old, mb, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) {
+    c->cur_st = c->st;
     LaunchScope ls(c, K_OP, 3.0 * mb, 0);
     e = launch_polar_batch(de, dg, beta, dn, ds, count, c->st);
   }
@@ -882,15 +1048,26 @@ void qfs_destroy(qfs_ctx *c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->st) cudaStreamSynchronize(c->st);
+  if (c->d_dbg && c->dbg_n)
+    fprintf(stderr, "[qfs tail timing] per gate launch (avg over %lld): first-CTA-start -> last-CTA-elected %.2f us, "
+            "partial reduce %.2f us, polar %.2f us\n", c->dbg_n, c->dbg_acc[0] / c->dbg_n / 1e3,
+            c->dbg_acc[1] / c->dbg_n / 1e3, c->dbg_acc[2] / c->dbg_n / 1e3);
+  dfree(c->d_dbg);
   prof_collect(c);
+  drop_graph(c);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
-  if (c->gexec) cudaGraphExecDestroy(c->gexec);
   dfree(c->d_pairs); dfree(c->d_flag); dfree(c->d_x); dfree(c->d_y); dfree(c->d_xv); dfree(c->d_yv);
   dfree(c->d_gates); dfree(c->d_chi); dfree(c->d_B); dfree(c->d_vb0); dfree(c->d_vb1);
   dfree(c->d_partials); dfree(c->d_ered); dfree(c->d_sig); dfree(c->d_csum); dfree(c->d_rowout);
   dfree(c->d_cval); dfree(c->d_counters); dfree(c->d_slots); dfree(c->d_env_trace);
+  dfree(c->d_stage); dfree(c->d_vprev);
   if (c->h_csum) cudaFreeHost(c->h_csum);
   if (c->h_cval) cudaFreeHost(c->h_cval);
+  for (int g = 0; g < qfs_ctx::GMAX; ++g) {
+    if (c->gst[g]) cudaStreamDestroy(c->gst[g]);
+    if (c->ev_join[g]) cudaEventDestroy(c->ev_join[g]);
+  }
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->st) cudaStreamDestroy(c->st);
   delete c;
 }

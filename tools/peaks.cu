@@ -48,6 +48,14 @@ __global__ void read_kernel(const double2 *__restrict__ a, size_t n, double *out
   if (s == 123.456) out[0] = s;
 }
 __global__ void empty_kernel() {}
+// `passes` read-modify-write passes over an L2-resident buffer inside one launch
+__global__ void rmw_loop_kernel(double2 *__restrict__ a, size_t n, int passes) {
+  size_t st = (size_t)gridDim.x * blockDim.x;
+  for (int p = 0; p < passes; ++p)
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += st) {
+      double2 v = a[i]; v.x += 1.0; a[i] = v;
+    }
+}
 
 int main() {
   int dev = 0; CK(cudaSetDevice(dev));
@@ -95,6 +103,19 @@ int main() {
            16.0 * n / (best_rd * 1e-3) / 1e9);
     CK(cudaFree(a)); CK(cudaFree(b));
   };
+  // L2: 20 passes of read+write over 16 / 32 / 64 MiB inside one launch
+  for (size_t mib : {16, 32, 64}) {
+    size_t n = (mib << 20) / 16;
+    double2 *a; CK(cudaMalloc(&a, n * 16)); CK(cudaMemset(a, 0, n * 16));
+    float best = 1e30f;
+    for (int r = 0; r < 4; ++r) {
+      CK(cudaEventRecord(e0)); rmw_loop_kernel<<<p.multiProcessorCount * 8, 256>>>(a, n, 20);
+      CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
+      float ms; CK(cudaEventElapsedTime(&ms, e0, e1)); if (r) best = std::min(best, ms);
+    }
+    printf(", \"l2loop_%zuMiB_rmw_gbs\": %.1f", mib, 20 * 32.0 * n / (best * 1e-3) / 1e9);
+    CK(cudaFree(a));
+  }
   bw(16ull << 20, "l2_16MiB");
   bw(32ull << 20, "l2_32MiB");
   bw(4ull << 30, "hbm_4GiB");
