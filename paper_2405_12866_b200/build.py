@@ -43,6 +43,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
            f"-I{os.path.join(nd, 'include')}", f"-I{os.path.join(ROOT, 'include')}",
            f"-L{os.path.join(nd, 'lib')}", f"-l:{os.path.basename(sorted(libs)[0])}",
            "-Xlinker", f"-rpath={os.path.join(nd, 'lib')}",
+           *os.environ.get("QFS_NVCC_DEFINES", "").split(),
            "-o", LIB + ".tmp", *SOURCES]
     r = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
     if r.returncode != 0:

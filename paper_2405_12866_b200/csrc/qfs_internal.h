@@ -28,19 +28,24 @@ struct ViewW {
   long long ss, sa, sm;
 };
 
-// Fused backward step for gate i (bwd_kernel):
-//   chi <- G_{i+1}^dag chi (if update) and E_i += phi_i (x) conj(chi)
+// Per-gate description of the fused backward step for gate i:
+//   chi <- G_{i+1}^dag chi (if upd) and E_i += phi_i (x) conj(chi)
 // over the 2^nu-amplitude groups spanned by the union of both gates' bits.
-struct BwdParams {
-  int n, nu, nb;              // qubits, union bits, CTAs per start
+struct GateDesc {
+  int nu, tp0, tp1, upd;      // union bits; local positions of gate i's pair; update?
   int upd_gate, env_gate;     // i+1 (or -1), i
-  int K, S;                   // gates, total starts (trace layout)
-  const Slot *slots;
+  uint32_t ins[4];            // union bit positions, ascending (for zero insertion)
+  long long off[16];          // amplitude offset of local index v (local bit t <-> loc[t])
   View chi_src;
   ViewW chi_dst;              // base == nullptr: do not write chi back
   View phi;
-  uint32_t ins[4];            // union bit positions, ascending (for zero insertion)
-  long long off[16];          // amplitude offset of local index v (local bit t <-> loc[t])
+};
+
+struct BwdParams {
+  int n, nb, K, S;            // qubits, CTAs per start, gates, total starts (trace layout)
+  const Slot *slots;
+  GateDesc g;                 // per-gate kernel: this gate
+  const GateDesc *desc;       // persistent kernel: [K] (device)
   const double2 *gates;       // [S][K][16]
   double2 *gates_w;           // same array (written by the polar step)
   double2 *vprev;             // [S][K][16] right singular vectors (warm start) or nullptr
@@ -52,6 +57,13 @@ struct BwdParams {
   double *sig;                // [S][K] sum sigma, or nullptr
   double2 *env_trace;         // [K][S][16] for this sweep, or nullptr
   unsigned long long *dbg;    // diagnostics: [K][4] globaltimer stamps, or nullptr
+  // persistent kernel only
+  unsigned *flags;            // [S_act] gates completed this sweep (release/acquire)
+  View chi_final, x_final;    // sweep-end cost: chi' = G_0^dag chi vs x
+  int fp0, fp1;               // pair of gate 0
+  double *partials2;          // [S_act][nb]
+  unsigned *counters2;        // [S_act]
+  double *out_sum;            // [S_act] sum ||chi' - x||^2
 };
 
 // Polar update of E (already reduced / all-reduced) for each active start.
@@ -115,8 +127,9 @@ struct ApplyParams {
 };
 
 // ---- launchers (qfs_kernels.cu); all return cudaGetLastError() ----
-cudaError_t launch_bwd(const BwdParams &p, int n_slots, int tp0, int tp1, bool upd,
-                       cudaStream_t st);
+cudaError_t launch_bwd(const BwdParams &p, int n_slots, cudaStream_t st);
+cudaError_t launch_bwd_persistent(const BwdParams &p, int n_slots, cudaStream_t st);
+int bwd_persistent_ctas_per_sm();  // co-resident CTAs per SM of the persistent kernel
 cudaError_t launch_polar(const PolarParams &p, int n_slots, cudaStream_t st);
 cudaError_t launch_final(const FinalParams &p, int n_slots, cudaStream_t st);
 cudaError_t launch_fwd_gate(const FwdGateParams &p, int n_slots, cudaStream_t st);

@@ -29,8 +29,17 @@ namespace qfs {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int BWD_THREADS = 256;
-constexpr int BWD_STAGES = 3;  // LDGSTS pipeline depth of the backward kernel
+#ifndef QFS_BWD_THREADS
+#define QFS_BWD_THREADS 256
+#endif
+#ifndef QFS_BWD_STAGES
+#define QFS_BWD_STAGES 4
+#endif
+#ifndef QFS_BWD_MINB
+#define QFS_BWD_MINB 1
+#endif
+constexpr int BWD_THREADS = QFS_BWD_THREADS;
+constexpr int BWD_STAGES = QFS_BWD_STAGES;  // LDGSTS pipeline depth of the backward kernel
 constexpr int FWD_THREADS = 256;
 constexpr int FWD_STAGES = 4;   // LDGSTS pipeline depth of the forward kernel
 constexpr int VAL_THREADS = 512;
@@ -151,22 +160,26 @@ __device__ void hw_polar(double2 e, double2 v0, double2 &g_out, double2 &v_out, 
       }
       const double ag2 = gr * gr + gi * gi;
       if (ag2 > 0.0 && ag2 > 1e-30 * al * be) {
+        // The same rotation as t = sgn(zeta)/(|zeta| + sqrt(1 + zeta^2)), c = 1/sqrt(1 + t^2),
+        // zeta = D/(2|gamma|), D = beta - alpha, rewritten with two rsqrt and no division:
+        //   R = sqrt(D^2 + 4|gamma|^2), den = |D| + R, r = 1/sqrt(den^2 + 4|gamma|^2),
+        //   c = den r, s e^{i phi} = 2 sgn(D) r gamma.
         rotated = true;
-        const double rag = rsqrt(ag2);
-        const double zeta = (be - al) * 0.5 * rag;
-        const double w = fma(zeta, zeta, 1.0);
-        const double den = fabs(zeta) + w * rsqrt(w);
-        const double rd = rsqrt(den);
-        const double t = (zeta >= 0.0 ? rd : -rd) * rd;
-        const double c = rsqrt(fma(t, t, 1.0));
-        const double s = c * t;
-        const double pr = gr * rag, pi = gi * rag;
-        if (lo) {  // a_j' = c a_j - s conj(ph) a_k
-          a = make_double2(c * aj.x - s * (pr * ak.x + pi * ak.y), c * aj.y - s * (pr * ak.y - pi * ak.x));
-          v = make_double2(c * vj.x - s * (pr * vk.x + pi * vk.y), c * vj.y - s * (pr * vk.y - pi * vk.x));
-        } else {   // a_k' = s ph a_j + c a_k
-          a = make_double2(s * (pr * aj.x - pi * aj.y) + c * ak.x, s * (pr * aj.y + pi * aj.x) + c * ak.y);
-          v = make_double2(s * (pr * vj.x - pi * vj.y) + c * vk.x, s * (pr * vj.y + pi * vj.x) + c * vk.y);
+        const double D = be - al;
+        const double q4 = 4.0 * ag2;
+        const double w = fma(D, D, q4);
+        const double R = w * rsqrt(w);
+        const double den = fabs(D) + R;
+        const double r = rsqrt(fma(den, den, q4));
+        const double c = den * r;
+        const double f2 = (D >= 0.0 ? 2.0 : -2.0) * r;
+        const double spr = f2 * gr, spi = f2 * gi;  // s e^{i phi}
+        if (lo) {  // a_j' = c a_j - conj(s e^{i phi}) a_k
+          a = make_double2(c * aj.x - (spr * ak.x + spi * ak.y), c * aj.y - (spr * ak.y - spi * ak.x));
+          v = make_double2(c * vj.x - (spr * vk.x + spi * vk.y), c * vj.y - (spr * vk.y - spi * vk.x));
+        } else {   // a_k' = s e^{i phi} a_j + c a_k
+          a = make_double2((spr * aj.x - spi * aj.y) + c * ak.x, (spr * aj.y + spi * aj.x) + c * ak.y);
+          v = make_double2((spr * vj.x - spi * vj.y) + c * vk.x, (spr * vj.y + spi * vj.x) + c * vk.y);
         }
       }
     }
@@ -176,12 +189,13 @@ __device__ void hw_polar(double2 e, double2 v0, double2 &g_out, double2 &v_out, 
   double nn = a.x * a.x + a.y * a.y;
   nn += __shfl_xor_sync(FULL, nn, 4);
   nn += __shfl_xor_sync(FULL, nn, 8);
-  const double sig = sqrt(nn);
+  const double rs = nn > 0.0 ? rsqrt(nn) : 0.0;
+  const double sig = nn * rs;
   double smax = sig;
   smax = fmax(smax, __shfl_xor_sync(FULL, smax, 1));
   smax = fmax(smax, __shfl_xor_sync(FULL, smax, 2));
   const bool nul = !(sig > 1e-14 * smax) || smax == 0.0;
-  double2 xx = nul ? make_double2(0.0, 0.0) : make_double2(a.x / sig, a.y / sig);
+  double2 xx = nul ? make_double2(0.0, 0.0) : make_double2(a.x * rs, a.y * rs);
   if (__any_sync(FULL, nul)) {  // rare: complete the null columns of X
     scratch[l] = xx;
     __syncwarp();
@@ -253,19 +267,20 @@ __device__ void polar_write(const double *e32, double2 *gout, double2 *vslot, do
   if (lane == 0 && sig_out) *sig_out = ss;
 }
 
-// Last-CTA election for the per-start reduction of CTA partials.
-__device__ bool elect_last(unsigned *counter, unsigned nb) {
-  __shared__ bool last;
+// Last-CTA election for the per-start reduction of CTA partials, by warp 0
+// only (the warp that wrote this CTA's partial): release fence, ticket, and an
+// acquire fence in the last CTA.  The other warps never fence or wait.
+__device__ bool warp0_elect_last(unsigned *counter, unsigned nb) {
   __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  unsigned last = 0;
+  if ((threadIdx.x & 31) == 0) {
     const unsigned t = atomicAdd(counter, 1u);
-    last = (t == nb - 1);
+    last = (t == nb - 1) ? 1u : 0u;
     if (last) *counter = 0u;
   }
-  __syncthreads();
+  last = __shfl_sync(FULL, last, 0);
   if (last) __threadfence();
-  return last;
+  return last != 0;
 }
 
 // P-index (0..3) of local amplitude index v for the pair at local bits (TP0, TP1)
@@ -274,38 +289,43 @@ __device__ __forceinline__ int pidx(int v) {
   return ((v >> TP0) & 1) | (((v >> TP1) & 1) << 1);
 }
 
+struct BwdShared {
+  double2 sQ[16];                          // G_{i+1}^dag
+  double2 red[BWD_THREADS / 32][4][16];    // per-warp (per lane-group) E partials
+  double sum32[32];
+  double2 scratch[32];
+};
+
 // ---------------------------------------------------------------- backward --
-// Gate i of the right-to-left sweep (Fig. env_calc).  Work item =
-// (2^NU-amplitude group g, sample m), m fastest.  T = 2^(NU-2) threads share an
-// item: thread t owns the Q-quadruple whose local bits >= 2 equal t (local bits
-// 0,1 are the Q pair = gate i+1).  Per item:
-//   if UPD: chi <- G_{i+1}^dag chi on the thread's own Q-quadruple, written back;
-//   all-gather of the updated chi among the T threads (shfl_xor);
-//   E_i[a][b] += phi[v_a] conj(chi[v_b]) for each pair of members (v_a owned,
-//   v_b any) of one P-quadruple (the P pair = gate i sits at local TP0, TP1).
-// Accumulators are keyed by compile-time (la & PLO, lb & PLO, x); the target
-// entry (a, b) is fixed by the key and t, so each warp lane-group writes each
-// E entry exactly once in the CTA reduction (deterministic order).
+// One CTA's share of gate i of the right-to-left sweep (Fig. env_calc
+// P:172) for start slot j; ends with warp 0 holding the CTA partial of E_i in
+// P.partials (other warps return from here).  Work unit = (group of 2^NU
+// amplitudes spanned by both gates' qubits, block of LPT consecutive samples);
+// T = 2^(NU-2) threads share a group, thread t owning the Q-quadruple whose
+// local bits >= 2 equal t (local bits 0,1 are the Q pair = gate i+1).  Per item:
+//   if UPD: chi <- G_{i+1}^dag chi on the own Q-quadruple, written back;
+//   NU == 4: the four threads transpose through shared memory so that thread t
+//     holds P-quadruple t (members in xor order a = t ^ x), phi is loaded in
+//     that order, and all 16 entries of E are accumulated per thread;
+//   NU < 4: all-gather of chi by shuffles, accumulators keyed at compile time
+//     by (la & PLO, lb & PLO, x) with the target entry fixed by the key and t.
+// chi/phi of the next items are staged into shared memory by LDGSTS,
+// BWD_STAGES-1 items ahead.  Reductions run in a fixed order (lanes, lane
+// groups, warps), so the partial is deterministic for a given launch shape.
 template <int NU, int TP0, int TP1, bool UPD>
-__global__ void __launch_bounds__(BWD_THREADS, 2) bwd_kernel(const BwdParams P) {
+__device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslot, int s,
+                                 unsigned Ms, bool fence_chi, BwdShared &sh,
+                                 double2 *stage_buf) {
   constexpr int T = 1 << (NU - 2);
   constexpr int LPT = 32 / T;
   constexpr int NWARP = BWD_THREADS / 32;
   constexpr int PLO = ((TP0 < 2) ? (1 << TP0) : 0) | ((TP1 < 2) ? (1 << TP1) : 0);
   constexpr int NPT_T = (((1 << NU) - 1) & ~((1 << TP0) | (1 << TP1))) >> 2;
-  __shared__ double2 sQ[16];
-  __shared__ double2 red[NWARP][16];
-  __shared__ double sum32[32];
-  __shared__ double2 scratch[32];
+  constexpr bool XPOSE = (NU == 4);
+  constexpr int AZ = XPOSE ? 1 : T;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int t = lane / LPT, ml = lane % LPT;
-  const int jslot = blockIdx.y;
-  const Slot sl = P.slots[jslot];
-  const int s = sl.s;
-  const unsigned Ms = (unsigned)sl.m;
-  // work units = (group g, block of LPT consecutive samples); a warp takes one
-  // unit at a time, lane (t, ml) handling sample mb*LPT + ml, Q-quadruple t.
   const unsigned nmb = (Ms + LPT - 1) / LPT;
   const unsigned units = (1u << (P.n - NU)) * nmb;
   const unsigned chunk = (units + P.nb - 1) / P.nb;
@@ -315,62 +335,59 @@ __global__ void __launch_bounds__(BWD_THREADS, 2) bwd_kernel(const BwdParams P) 
 
   if (UPD && threadIdx.x < 16) {
     const int a = threadIdx.x >> 2, b = threadIdx.x & 3;
-    const double2 g = P.gates[((long long)s * P.K + P.upd_gate) * 16 + 4 * b + a];
-    sQ[threadIdx.x] = cconj(g);  // (G^dag)[a][b]
+    const double2 g = __ldcg(P.gates + ((long long)s * P.K + G.upd_gate) * 16 + 4 * b + a);
+    sh.sQ[threadIdx.x] = cconj(g);  // (G^dag)[a][b]
   }
-  if (P.dbg && threadIdx.x == 0) atomicMin(P.dbg + 4 * P.env_gate, gtimer());
+  if (P.dbg && threadIdx.x == 0) atomicMin(P.dbg + 4 * G.env_gate, gtimer());
   __syncthreads();
 
-  double2 acc[4][4][T];
+  double2 acc[4][4][AZ];
 #pragma unroll
   for (int p = 0; p < 4; ++p)
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
-      for (int x = 0; x < T; ++x) acc[p][q][x] = make_double2(0.0, 0.0);
+      for (int x = 0; x < AZ; ++x) acc[p][q][x] = make_double2(0.0, 0.0);
 
-  const double2 *csrc = P.chi_src.base + (long long)s * P.chi_src.ss;
-  double2 *cdst = P.chi_dst.base ? P.chi_dst.base + (long long)s * P.chi_dst.ss : nullptr;
-  const double2 *fsrc = P.phi.base + (long long)s * P.phi.ss;
-  const long long csa = P.chi_src.sa, csm = P.chi_src.sm;
-  const long long dsa = P.chi_dst.sa, dsm = P.chi_dst.sm;
-  const long long fsa = P.phi.sa, fsm = P.phi.sm;
-  long long offc[4], offd[4], offf[4];  // own Q-quadruple amplitude offsets per view
+  // element offsets inside one start's block (sample-minor views: sm == 1)
+  const double2 *csrc = G.chi_src.base + (long long)s * G.chi_src.ss;
+  double2 *cdst = G.chi_dst.base ? G.chi_dst.base + (long long)s * G.chi_dst.ss : nullptr;
+  const double2 *fsrc = G.phi.base + (long long)s * G.phi.ss;
+  const unsigned csa = (unsigned)G.chi_src.sa, dsa = (unsigned)G.chi_dst.sa, fsa = (unsigned)G.phi.sa;
+  unsigned offc[4], offd[4], offf[4];
 #pragma unroll
   for (int l = 0; l < 4; ++l) {
-    const long long o = P.off[4 * t + l];
+    const unsigned o = (unsigned)G.off[4 * t + l];
     offc[l] = o * csa;
     offd[l] = o * dsa;
-    offf[l] = o * fsa;
+    offf[l] = (unsigned)G.off[XPOSE ? (t + 4 * (t ^ l)) : (4 * t + l)] * fsa;
   }
+  uint32_t ins[NU];
+#pragma unroll
+  for (int q = 0; q < NU; ++q) ins[q] = G.ins[q];
 
-  // Items of this thread: w_k = beg + warp*LPT + k*NWARP*LPT + ml.  Their 8
-  // amplitudes (own Q-quadruple of chi and phi) are staged into shared memory
-  // with LDGSTS, BWD_STAGES-1 items ahead, so the bytes in flight are bounded
-  // by shared memory rather than registers.  Each thread reads back only its
-  // own slots: cp.async.wait_group suffices, no CTA barrier in the loop.
-  extern __shared__ double2 stage_buf[];  // [BWD_STAGES][8][BWD_THREADS]
   const unsigned ustart = beg + warp;
   const int iters = ustart < end ? (int)((end - ustart + NWARP - 1) / NWARP) : 0;
-  auto locate = [&](int k, unsigned &g, unsigned &m) -> bool {
+  auto locate = [&](int k, unsigned &ec, unsigned &ed, unsigned &ef) -> bool {
     const unsigned u = ustart + (unsigned)k * NWARP;
     if (k >= iters) return false;
-    g = fdu.div(u);
-    m = (u - g * nmb) * LPT + ml;
+    unsigned g = fdu.div(u);
+    const unsigned m = (u - g * nmb) * LPT + ml;
 #pragma unroll
-    for (int q = 0; q < NU; ++q) g = insert_zero32(g, P.ins[q]);
+    for (int q = 0; q < NU; ++q) g = insert_zero32(g, ins[q]);
+    ec = g * csa + m;
+    ed = g * dsa + m;
+    ef = g * fsa + m;
     return m < Ms;
   };
   auto issue = [&](int k) {
-    unsigned g = 0, m = 0;
-    const bool ok = locate(k, g, m);
+    unsigned ec = 0, ed = 0, ef = 0;
+    const bool ok = locate(k, ec, ed, ef);
     double2 *st = stage_buf + (k % BWD_STAGES) * 8 * BWD_THREADS + threadIdx.x;
-    const double2 *cp = csrc + (long long)g * csa + (long long)m * csm;
-    const double2 *fp = fsrc + (long long)g * fsa + (long long)m * fsm;
 #pragma unroll
-    for (int l = 0; l < 4; ++l) cp_async16(st + l * BWD_THREADS, ok ? cp + offc[l] : csrc, ok);
+    for (int l = 0; l < 4; ++l) cp_async16(st + l * BWD_THREADS, csrc + (ok ? ec + offc[l] : 0u), ok);
 #pragma unroll
-    for (int l = 0; l < 4; ++l) cp_async16(st + (4 + l) * BWD_THREADS, ok ? fp + offf[l] : fsrc, ok);
+    for (int l = 0; l < 4; ++l) cp_async16(st + (4 + l) * BWD_THREADS, fsrc + (ok ? ef + offf[l] : 0u), ok);
     cp_async_commit();
   };
 #pragma unroll
@@ -379,61 +396,97 @@ __global__ void __launch_bounds__(BWD_THREADS, 2) bwd_kernel(const BwdParams P) 
   for (int k = 0; k < iters; ++k) {
     issue(k + BWD_STAGES - 1);
     cp_async_wait<BWD_STAGES - 1>();
-    unsigned g = 0, m = 0;
-    const bool valid = locate(k, g, m);
-    const double2 *st = stage_buf + (k % BWD_STAGES) * 8 * BWD_THREADS + threadIdx.x;
+    unsigned ec = 0, ed = 0, ef = 0;
+    const bool valid = locate(k, ec, ed, ef);
+    double2 *st = stage_buf + (k % BWD_STAGES) * 8 * BWD_THREADS + threadIdx.x;
     double2 c[4], f[4];
 #pragma unroll
     for (int l = 0; l < 4; ++l) c[l] = st[l * BWD_THREADS];
 #pragma unroll
     for (int l = 0; l < 4; ++l) f[l] = st[(4 + l) * BWD_THREADS];
+#ifdef QFS_DIAG_NOCOMPUTE  // diagnostic build: memory traffic only (results invalid)
+    if (UPD && cdst && valid) {
+      double2 *dp = cdst + ed;
+#pragma unroll
+      for (int l = 0; l < 4; ++l) dp[offd[l]] = c[l];
+    }
+    acc[0][0][0].x += c[0].x + f[0].x + c[1].x + f[1].x + c[2].x + f[2].x + c[3].x + f[3].x;
+    if (false)
+#endif
     if (UPD) {
       double2 o[4];
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
         o[a] = make_double2(0.0, 0.0);
 #pragma unroll
-        for (int b = 0; b < 4; ++b) cfma(o[a], sQ[4 * a + b], c[b]);
+        for (int b = 0; b < 4; ++b) cfma(o[a], sh.sQ[4 * a + b], c[b]);
       }
 #pragma unroll
       for (int a = 0; a < 4; ++a) c[a] = o[a];
       if (cdst && valid) {
-        double2 *dp = cdst + (long long)g * dsa + (long long)m * dsm;
+        double2 *dp = cdst + ed;
 #pragma unroll
         for (int l = 0; l < 4; ++l) dp[offd[l]] = c[l];
       }
     }
-    // all-gather of chi among the T threads of the item, then the environment terms
+#ifdef QFS_DIAG_NOCOMPUTE
+    if (false)
+#endif
+    if (XPOSE) {
+      // transpose through this stage's (already consumed) chi slots
+      __syncwarp();
 #pragma unroll
-    for (int x = 0; x < T; ++x) {
-      if ((x & NPT_T) != 0) continue;  // partner differs in a non-P bit: no shared P-quadruple
-      double2 cx[4];
+      for (int l = 0; l < 4; ++l) st[l * BWD_THREADS] = c[l];
+      __syncwarp();
+      double2 r[4];
+      const int lane_base = threadIdx.x - lane;
 #pragma unroll
-      for (int l = 0; l < 4; ++l) cx[l] = x == 0 ? c[l] : shfl_xor_c(c[l], x * LPT);
+      for (int x = 0; x < 4; ++x)
+        r[x] = stage_buf[(k % BWD_STAGES) * 8 * BWD_THREADS + t * BWD_THREADS + lane_base + (lane ^ (x * LPT))];
 #pragma unroll
-      for (int la = 0; la < 4; ++la)
+      for (int x = 0; x < 4; ++x)
 #pragma unroll
-        for (int lb = 0; lb < 4; ++lb) {
-          if (((la ^ lb) & ~PLO & 3) != 0) continue;
-          double2 &e = acc[la & PLO][lb & PLO][x];
-          // f[la] * conj(cx[lb])
-          e.x = fma(f[la].x, cx[lb].x, e.x);
-          e.x = fma(f[la].y, cx[lb].y, e.x);
-          e.y = fma(f[la].y, cx[lb].x, e.y);
-          e.y = fma(-f[la].x, cx[lb].y, e.y);
+        for (int y = 0; y < 4; ++y) {
+          double2 &e = acc[x][y][0];
+          e.x = fma(f[x].x, r[y].x, e.x);
+          e.x = fma(f[x].y, r[y].y, e.x);
+          e.y = fma(f[x].y, r[y].x, e.y);
+          e.y = fma(-f[x].x, r[y].y, e.y);
         }
+    } else {
+#pragma unroll
+      for (int x = 0; x < T; ++x) {
+        if ((x & NPT_T) != 0) continue;  // partner differs in a non-P bit: no shared P-quadruple
+        double2 cx[4];
+#pragma unroll
+        for (int l = 0; l < 4; ++l) cx[l] = x == 0 ? c[l] : shfl_xor_c(c[l], x * LPT);
+#pragma unroll
+        for (int la = 0; la < 4; ++la)
+#pragma unroll
+          for (int lb = 0; lb < 4; ++lb) {
+            if (((la ^ lb) & ~PLO & 3) != 0) continue;
+            double2 &e = acc[la & PLO][lb & PLO][x < AZ ? x : 0];
+            // f[la] * conj(cx[lb])
+            e.x = fma(f[la].x, cx[lb].x, e.x);
+            e.x = fma(f[la].y, cx[lb].y, e.x);
+            e.y = fma(f[la].y, cx[lb].x, e.y);
+            e.y = fma(-f[la].x, cx[lb].y, e.y);
+          }
+      }
     }
   }
   cp_async_wait<0>();
+  if (UPD && fence_chi) __threadfence();  // chi visible to the other CTAs before the ticket
 
-  // CTA reduction: over the sample lanes of each lane-group, then warps in order
+  // CTA reduction: over the sample lanes of each lane-group, then lane groups
+  // and warps in a fixed order
 #pragma unroll
   for (int pa = 0; pa < 4; ++pa)
 #pragma unroll
     for (int pb = 0; pb < 4; ++pb)
 #pragma unroll
-      for (int x = 0; x < T; ++x) {
-        if ((pa & ~PLO) || (pb & ~PLO) || (x & NPT_T)) continue;
+      for (int x = 0; x < AZ; ++x) {
+        if (!XPOSE && ((pa & ~PLO) || (pb & ~PLO) || (x & NPT_T))) continue;
         double2 v = acc[pa][pb][x];
 #pragma unroll
         for (int o = LPT / 2; o >= 1; o >>= 1) {
@@ -441,43 +494,184 @@ __global__ void __launch_bounds__(BWD_THREADS, 2) bwd_kernel(const BwdParams P) 
           v.y += __shfl_xor_sync(FULL, v.y, o);
         }
         if (ml == 0) {
-          const int a = pidx<TP0, TP1>(pa | (t << 2));
-          const int b = pidx<TP0, TP1>(pb | ((t ^ x) << 2));
-          red[warp][4 * a + b] = v;
+          int a, b;
+          if (XPOSE) {  // acc[x][y]: members t^x, t^y of P-quadruple t
+            a = pidx<TP0, TP1>(4 * (t ^ pa));
+            b = pidx<TP0, TP1>(4 * (t ^ pb));
+          } else {
+            a = pidx<TP0, TP1>(pa | (t << 2));
+            b = pidx<TP0, TP1>(pb | ((t ^ x) << 2));
+          }
+          sh.red[warp][XPOSE ? t : 0][4 * a + b] = v;
         }
       }
   __syncthreads();
-  if (threadIdx.x < 32) {
+  if (threadIdx.x >= 32) return false;  // warp 0 finishes the CTA's work
+  {
     const int e = threadIdx.x >> 1, im = threadIdx.x & 1;
     double v = 0.0;
 #pragma unroll
-    for (int wq = 0; wq < NWARP; ++wq) v += im ? red[wq][e].y : red[wq][e].x;
+    for (int wq = 0; wq < NWARP; ++wq)
+#pragma unroll
+      for (int tq = 0; tq < (XPOSE ? T : 1); ++tq) v += im ? sh.red[wq][tq][e].y : sh.red[wq][tq][e].x;
     P.partials[((long long)jslot * P.nb + blockIdx.x) * 32 + threadIdx.x] = v;
   }
-  if (!elect_last(&P.counters[jslot], (unsigned)P.nb)) return;
-  if (threadIdx.x >= 32) return;
-  if (P.dbg && threadIdx.x == 0) atomicMax(P.dbg + 4 * P.env_gate + 1, gtimer());
-  {
-    const double *pp = P.partials + (long long)jslot * P.nb * 32 + threadIdx.x;
-    double e = 0.0;
-    int b = 0;
-    for (; b + 4 <= P.nb; b += 4) {  // loads batched, adds in CTA order
-      const double x0 = __ldcg(pp + (long long)b * 32), x1 = __ldcg(pp + (long long)(b + 1) * 32);
-      const double x2 = __ldcg(pp + (long long)(b + 2) * 32), x3 = __ldcg(pp + (long long)(b + 3) * 32);
-      e += x0; e += x1; e += x2; e += x3;
-    }
-    for (; b < P.nb; ++b) e += __ldcg(pp + (long long)b * 32);
-    sum32[threadIdx.x] = e;
-    if (!P.fuse_polar) P.e_red[(long long)jslot * 32 + threadIdx.x] = e;
+  return true;
+}
+
+// Warp 0 of the last CTA of a start: sum the CTA partials in CTA order, and
+// (fuse_polar) run the polar update of gate i.
+__device__ void bwd_finish(const BwdParams &P, const GateDesc &G, int jslot, int s, BwdShared &sh) {
+  if (P.dbg && threadIdx.x == 0) atomicMax(P.dbg + 4 * G.env_gate + 1, gtimer());
+  const double *pp = P.partials + (long long)jslot * P.nb * 32 + threadIdx.x;
+  double e = 0.0;
+  for (int b0 = 0; b0 < P.nb; b0 += 16) {  // 16 loads in flight, adds in CTA order
+    double xb[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) xb[q] = b0 + q < P.nb ? __ldcg(pp + (long long)(b0 + q) * 32) : 0.0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+      if (b0 + q < P.nb) e += xb[q];
   }
+  sh.sum32[threadIdx.x] = e;
+  if (!P.fuse_polar) P.e_red[(long long)jslot * 32 + threadIdx.x] = e;
   __syncwarp();
-  if (P.dbg && threadIdx.x == 0) atomicMax(P.dbg + 4 * P.env_gate + 2, gtimer());
+  if (P.dbg && threadIdx.x == 0) atomicMax(P.dbg + 4 * G.env_gate + 2, gtimer());
   if (!P.fuse_polar) return;
-  const long long gi = (long long)s * P.K + P.env_gate;
-  polar_write(sum32, P.gates_w + gi * 16, P.vprev ? P.vprev + gi * 16 : nullptr, P.beta,
+  const long long gi = (long long)s * P.K + G.env_gate;
+  polar_write(sh.sum32, P.gates_w + gi * 16, P.vprev ? P.vprev + gi * 16 : nullptr, P.beta,
               P.sig ? P.sig + gi : nullptr,
-              P.env_trace ? P.env_trace + ((long long)P.env_gate * P.S + s) * 16 : nullptr, scratch);
-  if (P.dbg && threadIdx.x == 0) atomicMax(P.dbg + 4 * P.env_gate + 3, gtimer());
+              P.env_trace ? P.env_trace + ((long long)G.env_gate * P.S + s) * 16 : nullptr, sh.scratch);
+  if (P.dbg && threadIdx.x == 0) atomicMax(P.dbg + 4 * G.env_gate + 3, gtimer());
+}
+
+// One launch per gate (used in sample-sharded mode and by the unit op).
+template <int NU, int TP0, int TP1, bool UPD>
+__global__ void __launch_bounds__(BWD_THREADS, QFS_BWD_MINB) bwd_kernel(const BwdParams P) {
+  __shared__ BwdShared sh;
+  extern __shared__ double2 stage_buf[];  // [BWD_STAGES][8][BWD_THREADS]
+  const int jslot = blockIdx.y;
+  const Slot sl = P.slots[jslot];
+  if (!bwd_gate_partial<NU, TP0, TP1, UPD>(P, P.g, jslot, sl.s, (unsigned)sl.m, false, sh, stage_buf))
+    return;
+  if (!warp0_elect_last(&P.counters[jslot], (unsigned)P.nb)) return;
+  bwd_finish(P, P.g, jslot, sl.s, sh);
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// all threads of the CTA wait until *flag >= target (thread 0 polls)
+__device__ void cta_wait_flag(const unsigned *flag, unsigned target) {
+  if (threadIdx.x == 0)
+    while (ld_acquire(flag) < target) __nanosleep(32);
+  __syncthreads();
+}
+
+template <int NU, int TP0, int TP1, bool UPD>
+__device__ __forceinline__ bool gate_dispatch_one(const BwdParams &P, const GateDesc &G, int j, int s,
+                                                  unsigned Ms, BwdShared &sh, double2 *buf) {
+  return bwd_gate_partial<NU, TP0, TP1, UPD>(P, G, j, s, Ms, true, sh, buf);
+}
+
+// Whole backward pass of a sweep plus the sweep-end cost in ONE cooperative
+// launch: CTAs (grid nb x slots, all co-resident) loop over the gates; per
+// start, the last CTA of a gate runs the polar update and releases a flag the
+// start's CTAs acquire before the next gate (they need G_{i+1} and the chi the
+// other CTAs wrote).  Starts progress independently; no kernel boundaries.
+__global__ void __launch_bounds__(BWD_THREADS, QFS_BWD_MINB) bwd_persistent_kernel(const BwdParams P) {
+  __shared__ BwdShared sh;
+  extern __shared__ double2 stage_buf[];
+  const int j = blockIdx.y;
+  const Slot sl = P.slots[j];
+  const unsigned Ms = (unsigned)sl.m;
+  for (int i = P.K - 1; i >= 0; --i) {
+    if (i < P.K - 1) cta_wait_flag(P.flags + j, (unsigned)(P.K - 1 - i));
+    const GateDesc &G = P.desc[i];
+    bool w0;
+    if (!G.upd) {
+      w0 = gate_dispatch_one<2, 0, 1, false>(P, G, j, sl.s, Ms, sh, stage_buf);
+    } else if (G.nu == 2) {
+      w0 = G.tp0 == 0 ? gate_dispatch_one<2, 0, 1, true>(P, G, j, sl.s, Ms, sh, stage_buf)
+                      : gate_dispatch_one<2, 1, 0, true>(P, G, j, sl.s, Ms, sh, stage_buf);
+    } else if (G.nu == 3) {
+      if (G.tp0 == 0 && G.tp1 == 2) w0 = gate_dispatch_one<3, 0, 2, true>(P, G, j, sl.s, Ms, sh, stage_buf);
+      else if (G.tp0 == 2 && G.tp1 == 0) w0 = gate_dispatch_one<3, 2, 0, true>(P, G, j, sl.s, Ms, sh, stage_buf);
+      else if (G.tp0 == 1 && G.tp1 == 2) w0 = gate_dispatch_one<3, 1, 2, true>(P, G, j, sl.s, Ms, sh, stage_buf);
+      else w0 = gate_dispatch_one<3, 2, 1, true>(P, G, j, sl.s, Ms, sh, stage_buf);
+    } else {
+      w0 = G.tp0 == 2 ? gate_dispatch_one<4, 2, 3, true>(P, G, j, sl.s, Ms, sh, stage_buf)
+                      : gate_dispatch_one<4, 3, 2, true>(P, G, j, sl.s, Ms, sh, stage_buf);
+    }
+    if (w0 && warp0_elect_last(&P.counters[j], (unsigned)P.nb)) {
+      bwd_finish(P, G, j, sl.s, sh);
+      __threadfence();
+      if (threadIdx.x == 0) st_release(P.flags + j, (unsigned)(P.K - i));
+    }
+  }
+  // sweep-end cost: chi' = G_0^dag chi, sum ||chi' - x||^2 over this
+  // CTA's units of pair 0 (one sample per lane), ordered reduction
+  cta_wait_flag(P.flags + j, (unsigned)P.K);
+  {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NWARP = BWD_THREADS / 32;
+    if (threadIdx.x < 16) {
+      const int a = threadIdx.x >> 2, b = threadIdx.x & 3;
+      sh.sQ[threadIdx.x] = cconj(__ldcg(P.gates + (long long)sl.s * P.K * 16 + 4 * b + a));
+    }
+    __syncthreads();
+    const unsigned nmb = (Ms + 31) / 32;
+    const unsigned units = (1u << (P.n - 2)) * nmb;
+    const unsigned chunk = (units + P.nb - 1) / P.nb;
+    const unsigned beg = blockIdx.x * chunk, end = min(units, beg + chunk);
+    const FastDiv fdu(nmb);
+    const int lo = min(P.fp0, P.fp1), hi = max(P.fp0, P.fp1);
+    const unsigned o[4] = {0u, 1u << P.fp0, 1u << P.fp1, (1u << P.fp0) | (1u << P.fp1)};
+    const double2 *cb = P.chi_final.base + (long long)sl.s * P.chi_final.ss;
+    const unsigned csa = (unsigned)P.chi_final.sa, xsa = (unsigned)P.x_final.sa;
+    double accd = 0.0;
+    for (unsigned u = beg + warp; u < end; u += NWARP) {
+      const unsigned q = fdu.div(u);
+      const unsigned m = (u - q * nmb) * 32 + lane;
+      if (m >= Ms) continue;
+      const unsigned base = insert_zero32(insert_zero32(q, lo), hi);
+      double2 v[4], xv[4];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) v[l] = __ldcg(cb + (base + o[l]) * csa + m);
+#pragma unroll
+      for (int l = 0; l < 4; ++l) xv[l] = __ldcs(P.x_final.base + (base + o[l]) * xsa + m);
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        double2 r = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) cfma(r, sh.sQ[4 * a + b], v[b]);
+        const double dr = r.x - xv[a].x, di = r.y - xv[a].y;
+        accd = fma(dr, dr, accd);
+        accd = fma(di, di, accd);
+      }
+    }
+#pragma unroll
+    for (int q = 16; q >= 1; q >>= 1) accd += __shfl_xor_sync(FULL, accd, q);
+    if (lane == 0) sh.sum32[warp] = accd;
+    __syncthreads();
+    if (threadIdx.x >= 32) return;
+    if (threadIdx.x == 0) {
+      double tsum = 0.0;
+      for (int q = 0; q < NWARP; ++q) tsum += sh.sum32[q];
+      P.partials2[(long long)j * P.nb + blockIdx.x] = tsum;
+    }
+    if (!warp0_elect_last(&P.counters2[j], (unsigned)P.nb)) return;
+    if (threadIdx.x == 0) {
+      double tsum = 0.0;
+      for (int b = 0; b < P.nb; ++b) tsum += __ldcg(P.partials2 + (long long)j * P.nb + b);
+      P.out_sum[j] = tsum;
+    }
+  }
 }
 
 // polar step alone (sample-sharded mode, after the NCCL all-reduce of E): one warp per start
@@ -544,12 +738,13 @@ __global__ void __launch_bounds__(RED_THREADS, 4) final_kernel(const FinalParams
   for (int q = 16; q >= 1; q >>= 1) acc += __shfl_xor_sync(FULL, acc, q);
   if (lane == 0) red[warp] = acc;
   __syncthreads();
+  if (threadIdx.x >= 32) return;
   if (threadIdx.x == 0) {
     double t = 0.0;
     for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += red[q];
     P.partials[(long long)j * P.nb + blockIdx.x] = t;
   }
-  if (!elect_last(&P.counters[j], (unsigned)P.nb)) return;
+  if (!warp0_elect_last(&P.counters[j], (unsigned)P.nb)) return;
   if (threadIdx.x == 0) {
     double t = 0.0;
     for (int b = 0; b < P.nb; ++b) t += __ldcg(P.partials + (long long)j * P.nb + b);
@@ -805,12 +1000,12 @@ __global__ void polar_batch_kernel(const double2 *env, const double2 *g_old, dou
 
 // ================================================================ launchers ==
 int val_row_max_n() { return 13; }
-int blocks_per_sm(int nu) { (void)nu; return 2; }
+int blocks_per_sm(int nu) { (void)nu; return QFS_BWD_MINB; }
 
-cudaError_t launch_bwd(const BwdParams &p, int n_slots, int tp0, int tp1, bool upd,
-                       cudaStream_t st) {
+cudaError_t launch_bwd(const BwdParams &p, int n_slots, cudaStream_t st) {
   dim3 grid(p.nb, n_slots), block(BWD_THREADS);
   const int smem = BWD_STAGES * 8 * BWD_THREADS * (int)sizeof(double2);
+  const GateDesc &g = p.g;
 #define QFS_BWD(NU, A, B, U)                                                                   \
   do {                                                                                         \
     static bool attr = false;                                                                  \
@@ -820,22 +1015,52 @@ cudaError_t launch_bwd(const BwdParams &p, int n_slots, int tp0, int tp1, bool u
     }                                                                                          \
     bwd_kernel<NU, A, B, U><<<grid, block, smem, st>>>(p);                                     \
   } while (0)
-  if (!upd) {
+  if (!g.upd) {
     QFS_BWD(2, 0, 1, false);
-  } else if (p.nu == 2) {
-    if (tp0 == 0) QFS_BWD(2, 0, 1, true);
+  } else if (g.nu == 2) {
+    if (g.tp0 == 0) QFS_BWD(2, 0, 1, true);
     else QFS_BWD(2, 1, 0, true);
-  } else if (p.nu == 3) {
-    if (tp0 == 0 && tp1 == 2) QFS_BWD(3, 0, 2, true);
-    else if (tp0 == 2 && tp1 == 0) QFS_BWD(3, 2, 0, true);
-    else if (tp0 == 1 && tp1 == 2) QFS_BWD(3, 1, 2, true);
+  } else if (g.nu == 3) {
+    if (g.tp0 == 0 && g.tp1 == 2) QFS_BWD(3, 0, 2, true);
+    else if (g.tp0 == 2 && g.tp1 == 0) QFS_BWD(3, 2, 0, true);
+    else if (g.tp0 == 1 && g.tp1 == 2) QFS_BWD(3, 1, 2, true);
     else QFS_BWD(3, 2, 1, true);
   } else {
-    if (tp0 == 2) QFS_BWD(4, 2, 3, true);
+    if (g.tp0 == 2) QFS_BWD(4, 2, 3, true);
     else QFS_BWD(4, 3, 2, true);
   }
 #undef QFS_BWD
   return cudaGetLastError();
+}
+
+int bwd_persistent_ctas_per_sm() {
+  static int cached = -1;
+  if (cached < 0) {
+    const int smem = BWD_STAGES * 8 * BWD_THREADS * (int)sizeof(double2);
+    cudaFuncSetAttribute(bwd_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, bwd_persistent_kernel, BWD_THREADS, smem) !=
+        cudaSuccess)
+      nb = 1;
+    cached = nb < 1 ? 1 : nb;
+  }
+  return cached;
+}
+
+cudaError_t launch_bwd_persistent(const BwdParams &p, int n_slots, cudaStream_t st) {
+  const int smem = BWD_STAGES * 8 * BWD_THREADS * (int)sizeof(double2);
+  bwd_persistent_ctas_per_sm();  // sets the shared-memory attribute
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.nb, n_slots);
+  cfg.blockDim = dim3(BWD_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (they wait on each other)
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, bwd_persistent_kernel, p);
 }
 
 cudaError_t launch_polar(const PolarParams &p, int n_slots, cudaStream_t st) {

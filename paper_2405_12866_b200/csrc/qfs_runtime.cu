@@ -79,6 +79,13 @@ struct qfs_ctx {
   double2 *d_env_trace = nullptr;
   size_t env_trace_cap = 0;
   double2 *d_stage = nullptr;  // row-major staging of the pools for the transpose
+  // persistent backward kernel: gate descriptors, per-start release flags,
+  // sweep-end cost reduction scratch
+  GateDesc *d_desc = nullptr;
+  std::vector<GateDesc> h_desc;
+  unsigned *d_flags = nullptr, *d_counters2 = nullptr;
+  double *d_partials2 = nullptr;
+  bool persistent = false;  // QFS_PERSISTENT=1 selects the cooperative whole-backward kernel
   size_t stage_bytes = 0;
   // graph cache
   cudaGraphExec_t gexec = nullptr;
@@ -304,6 +311,7 @@ qfs_status ensure_state(qfs_ctx *c, int S, int M, int V) {
   dfree(c->d_chi); dfree(c->d_B); dfree(c->d_vb0); dfree(c->d_vb1);
   dfree(c->d_partials); dfree(c->d_ered); dfree(c->d_sig); dfree(c->d_csum); dfree(c->d_rowout);
   dfree(c->d_cval); dfree(c->d_counters); dfree(c->d_slots);
+  dfree(c->d_flags); dfree(c->d_counters2); dfree(c->d_partials2);
   if (c->h_csum) cudaFreeHost(c->h_csum);
   if (c->h_cval) cudaFreeHost(c->h_cval);
   c->h_csum = c->h_cval = nullptr;
@@ -334,6 +342,10 @@ qfs_status ensure_state(qfs_ctx *c, int S, int M, int V) {
   CUDA_TRY(c, cudaMalloc(&c->d_counters, (size_t)S * 2 * sizeof(unsigned)));
   CUDA_TRY(c, cudaMemset(c->d_counters, 0, (size_t)S * 2 * sizeof(unsigned)));
   CUDA_TRY(c, cudaMalloc(&c->d_slots, (size_t)S * sizeof(Slot)));
+  CUDA_TRY(c, cudaMalloc(&c->d_flags, (size_t)S * sizeof(unsigned)));
+  CUDA_TRY(c, cudaMalloc(&c->d_counters2, (size_t)S * sizeof(unsigned)));
+  CUDA_TRY(c, cudaMemset(c->d_counters2, 0, (size_t)S * sizeof(unsigned)));
+  CUDA_TRY(c, cudaMalloc(&c->d_partials2, (size_t)S * nbc * sizeof(double)));
   CUDA_TRY(c, cudaMallocHost(&c->h_csum, (size_t)S * sizeof(double)));
   CUDA_TRY(c, cudaMallocHost(&c->h_cval, (size_t)S * sizeof(double)));
   c->S_cap = S; c->M_cap = M; c->V_cap = V; c->nb_cap = nbc;
@@ -349,6 +361,68 @@ struct SweepSpec {
   double2 *env_trace = nullptr;  // device [K][S][16] or nullptr
   int S = 0;                     // total starts (trace layout / strides)
 };
+
+// Descriptor of the fused backward step for gate i (union of gate i's pair
+// with gate i+1's; local order: Q pair first, then gate i's other bits).
+GateDesc make_desc(const qfs_ctx *c, int i) {
+  const int K = c->K;
+  const long long N = c->N, Mc = c->M_cap, sS = N * Mc;
+  const View xpool{c->d_x, 0, c->m_pool, 1}, ypool{c->d_y, 0, c->m_pool, 1};
+  GateDesc d{};
+  const bool upd = i < K - 1;
+  d.upd = upd ? 1 : 0;
+  d.upd_gate = upd ? i + 1 : -1;
+  d.env_gate = i;
+  const int p0 = c->pairs[2 * i], p1 = c->pairs[2 * i + 1];
+  int loc[4], nu;
+  if (!upd) {
+    loc[0] = p0; loc[1] = p1; nu = 2;
+  } else {
+    loc[0] = c->pairs[2 * (i + 1)]; loc[1] = c->pairs[2 * (i + 1) + 1]; nu = 2;
+    int ex[2], ne = 0;
+    for (int q : {p0, p1})
+      if (q != loc[0] && q != loc[1]) ex[ne++] = q;
+    if (ne == 2 && ex[0] > ex[1]) std::swap(ex[0], ex[1]);
+    for (int t = 0; t < ne; ++t) loc[nu++] = ex[t];
+  }
+  d.tp0 = d.tp1 = -1;
+  for (int t = 0; t < nu; ++t) {
+    if (loc[t] == p0) d.tp0 = t;
+    if (loc[t] == p1) d.tp1 = t;
+  }
+  d.nu = nu;
+  int srt[4];
+  for (int t = 0; t < nu; ++t) srt[t] = loc[t];
+  std::sort(srt, srt + nu);
+  for (int t = 0; t < 4; ++t) d.ins[t] = t < nu ? srt[t] : 0;
+  for (int v = 0; v < 16; ++v) {
+    long long o = 0;
+    for (int t = 0; t < nu; ++t)
+      if ((v >> t) & 1) o |= 1LL << loc[t];
+    d.off[v] = v < (1 << nu) ? o : 0;
+  }
+  auto Bk = [&](int k) -> double2 * { return c->d_B + (long long)(k - 1) * c->S_cap * sS; };
+  d.chi_src = (i >= K - 2) ? ypool : View{c->d_chi, sS, Mc, 1};
+  d.chi_dst = upd ? ViewW{c->d_chi, sS, Mc, 1} : ViewW{nullptr, 0, 0, 0};
+  d.phi = i == 0 ? xpool : View{Bk(i), sS, Mc, 1};
+  return d;
+}
+
+// Upload the gate descriptors of the persistent kernel when the buffer layout
+// changed (never during stream capture).
+qfs_status prepare_desc(qfs_ctx *c) {
+  std::vector<GateDesc> h(c->K);
+  for (int i = 0; i < c->K; ++i) h[i] = make_desc(c, i);
+  if (c->d_desc && h.size() == c->h_desc.size() &&
+      std::memcmp(h.data(), c->h_desc.data(), h.size() * sizeof(GateDesc)) == 0)
+    return QFS_OK;
+  if (!c->d_desc) CUDA_TRY(c, cudaMalloc(&c->d_desc, (size_t)c->K * sizeof(GateDesc)));
+  CUDA_TRY(c, cudaMemcpy(c->d_desc, h.data(), h.size() * sizeof(GateDesc), cudaMemcpyHostToDevice));
+  c->h_desc.swap(h);
+  return QFS_OK;
+}
+
+bool use_persistent(const qfs_ctx *c) { return c->persistent && !(c->mode == 1 && c->world > 1); }
 
 // Issue the launches of one sweep for the slots [j0, j1) on stream st (no host
 // synchronisation).  Scratch arrays indexed by slot are offset by j0.
@@ -385,58 +459,47 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
   }
   }
   // (b, c) backward: gate i = K-1 .. 0 (P:112 right to left; Fig. env_calc)
+  BwdParams b{};
+  b.n = n; b.K = K; b.S = sp.S; b.slots = slots; b.gates = c->d_gates; b.gates_w = c->d_gates;
+  b.partials = partials; b.counters = cnt_b; b.e_red = ered;
+  b.fuse_polar = (c->mode == 1 && c->world > 1) ? 0 : 1;
+  b.beta = sp.beta; b.sig = c->d_sig; b.env_trace = sp.env_trace;
+  b.vprev = c->d_vprev;
+  b.dbg = c->d_dbg;
+  double bwd_bytes = 0, bwd_flops = 0;
+  for (int i = K - 1; i >= 0; --i) {
+    bwd_bytes += units * (i < K - 1 ? 48.0 : 32.0);
+    bwd_flops += units * (i < K - 1 ? 64.0 : 32.0);
+  }
+  if (use_persistent(c)) {
+    // whole backward pass + sweep-end cost: one cooperative launch
+    PhaseScope phase_bwd(c, K_BWD);
+    b.desc = c->d_desc;
+    b.nb = std::max(1, std::min(148 * bwd_persistent_ctas_per_sm() / ns, kMaxBlocksPerStart));
+    b.flags = c->d_flags + j0;
+    b.chi_final = K == 1 ? ypool : View{c->d_chi, sS, Mc, 1};
+    b.x_final = xpool; b.fp0 = c->pairs[0]; b.fp1 = c->pairs[1];
+    b.partials2 = c->d_partials2 + (long long)j0 * c->nb_cap;
+    b.counters2 = c->d_counters2 + j0;
+    b.out_sum = csum;
+    CUDA_TRY(c, cudaMemsetAsync(c->d_flags + j0, 0, ns * sizeof(unsigned), st));
+    LaunchScope ls(c, K_BWD, bwd_bytes + units * 32.0, bwd_flops + units * 35.0);
+    CUDA_TRY(c, launch_bwd_persistent(b, ns, st));
+  } else {
   {
   PhaseScope phase_bwd(c, K_BWD);
   for (int i = K - 1; i >= 0; --i) {
-    BwdParams b{};
-    b.n = n; b.K = K; b.slots = slots; b.gates = c->d_gates; b.gates_w = c->d_gates;
-    b.partials = partials; b.counters = cnt_b; b.e_red = ered;
-    b.fuse_polar = (c->mode == 1 && c->world > 1) ? 0 : 1;
-    b.beta = sp.beta; b.sig = c->d_sig; b.env_trace = sp.env_trace; b.S = sp.S;
-    b.vprev = c->d_vprev;
-    b.dbg = c->d_dbg;
-    const bool upd = i < K - 1;
-    b.upd_gate = upd ? i + 1 : -1;
-    b.env_gate = i;
-    const int p0 = c->pairs[2 * i], p1 = c->pairs[2 * i + 1];
-    int loc[4], nu;
-    if (!upd) {
-      loc[0] = p0; loc[1] = p1; nu = 2;
-    } else {
-      loc[0] = c->pairs[2 * (i + 1)]; loc[1] = c->pairs[2 * (i + 1) + 1]; nu = 2;
-      int ex[2], ne = 0;
-      for (int q : {p0, p1})
-        if (q != loc[0] && q != loc[1]) ex[ne++] = q;
-      if (ne == 2 && ex[0] > ex[1]) std::swap(ex[0], ex[1]);
-      for (int t = 0; t < ne; ++t) loc[nu++] = ex[t];
-    }
-    int tp0 = -1, tp1 = -1;
-    for (int t = 0; t < nu; ++t) {
-      if (loc[t] == p0) tp0 = t;
-      if (loc[t] == p1) tp1 = t;
-    }
-    b.nu = nu;
-    int srt[4];
-    for (int t = 0; t < nu; ++t) srt[t] = loc[t];
-    std::sort(srt, srt + nu);
-    for (int t = 0; t < 4; ++t) b.ins[t] = t < nu ? srt[t] : 0;
-    for (int v = 0; v < 16; ++v) {
-      long long o = 0;
-      for (int t = 0; t < nu; ++t)
-        if ((v >> t) & 1) o |= 1LL << loc[t];
-      b.off[v] = v < (1 << nu) ? o : 0;
-    }
-    b.chi_src = (i >= K - 2) ? ypool : View{c->d_chi, sS, Mc, 1};
-    b.chi_dst = upd ? ViewW{c->d_chi, sS, Mc, 1} : ViewW{nullptr, 0, 0, 0};
-    b.phi = i == 0 ? xpool : View{Bk(i), sS, Mc, 1};
+    b.g = make_desc(c, i);
+    const bool upd = b.g.upd != 0;
+    const int nu = b.g.nu;
     {
       const long long lpt = 32 >> (nu - 2);
-      const long long units = (N >> nu) * ((M_max + lpt - 1) / lpt);
-      b.nb = blocks_per_start(units * 32, ns, blocks_per_sm(nu));
+      const long long un = (N >> nu) * ((M_max + lpt - 1) / lpt);
+      b.nb = blocks_per_start(un * 32, ns, blocks_per_sm(nu));
     }
     {
       LaunchScope ls(c, K_BWD, units * (upd ? 48.0 : 32.0), units * (upd ? 64.0 : 32.0));
-      CUDA_TRY(c, launch_bwd(b, ns, tp0, tp1, upd, st));
+      CUDA_TRY(c, launch_bwd(b, ns, st));
     }
     if (!b.fuse_polar) {
       {
@@ -464,6 +527,7 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
     fp.nb = blocks_per_start(((long long)M_max * N) >> 2, ns);
     LaunchScope ls(c, K_FINAL, units * 32.0, units * 35.0);
     CUDA_TRY(c, launch_final(fp, ns, st));
+  }
   }
   if (c->mode == 1 && c->world > 1) {
     LaunchScope ls(c, K_NCCL, 0, 0);
@@ -531,6 +595,10 @@ qfs_status issue_sweep(qfs_ctx *c, const SweepSpec &sp) {
 qfs_status run_sweep(qfs_ctx *c, const SweepSpec &sp, std::vector<double> &csum,
                      std::vector<double> &cval) {
   const int ns = (int)sp.slots.size();
+  if (use_persistent(c)) {
+    qfs_status r = prepare_desc(c);
+    if (r != QFS_OK) return r;
+  }
   CUDA_TRY(c, cudaMemcpyAsync(c->d_slots, sp.slots.data(), ns * sizeof(Slot),
                               cudaMemcpyHostToDevice, c->st));
   if (c->d_dbg) {
@@ -631,6 +699,7 @@ qfs_status create_common(int n, int k, const int32_t *pairs, int device, qfs_ctx
   }
   c->cur_st = c->st;
   if (const char *gs = getenv("QFS_GROUPS")) c->groups = std::max(1, std::min(qfs_ctx::GMAX, atoi(gs)));
+  if (const char *ps = getenv("QFS_PERSISTENT")) c->persistent = atoi(ps) != 0;
   if (e != cudaSuccess) {
     c->err = std::string("device init: ") + cudaGetErrorString(e);
     *out = c;  // caller can read the error, then destroy
@@ -955,7 +1024,7 @@ qfs_status qfs_op_environment(qfs_ctx *c, int p0, int p1, int m, const double *p
   unsigned *dcnt = nullptr;
   Slot *dsl = nullptr;
   BwdParams b{};
-  b.n = c->n; b.K = 1; b.nu = 2;
+  b.n = c->n; b.K = 1;
   b.nb = blocks_per_start((c->N >> 2) * ((m + 31) / 32) * 32, 1, 2);
   cudaError_t e = cudaMalloc(&dphi, bytes);
   if (e == cudaSuccess) e = cudaMalloc(&dchi, bytes);
@@ -964,22 +1033,31 @@ qfs_status qfs_op_environment(qfs_ctx *c, int p0, int p1, int m, const double *p
   if (e == cudaSuccess) e = cudaMalloc(&dcnt, sizeof(unsigned));
   if (e == cudaSuccess) e = cudaMalloc(&dsl, sizeof(Slot));
   Slot sl{0, m};
-  if (e == cudaSuccess) e = cudaMemcpy(dphi, phi, bytes, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(dchi, chi, bytes, cudaMemcpyHostToDevice);
+  // the backward kernel reads sample-minor views: transpose [m][2^n] -> [2^n][m]
+  double2 *dtmp = nullptr;
+  if (e == cudaSuccess) e = cudaMalloc(&dtmp, bytes);
+  if (e == cudaSuccess) e = cudaMemcpy(dtmp, phi, bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = launch_transpose(dtmp, dphi, m, c->N, c->st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->st);
+  if (e == cudaSuccess) e = cudaMemcpy(dtmp, chi, bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = launch_transpose(dtmp, dchi, m, c->N, c->st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->st);
+  if (dtmp) cudaFree(dtmp);
   if (e == cudaSuccess) e = cudaMemset(dcnt, 0, sizeof(unsigned));
   if (e == cudaSuccess) e = cudaMemcpy(dsl, &sl, sizeof sl, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) {
-    b.slots = dsl; b.chi_src = View{dchi, 0, 1, c->N}; b.chi_dst = ViewW{nullptr, 0, 0, 0};
-    b.phi = View{dphi, 0, 1, c->N};
+    b.slots = dsl; b.g.chi_src = View{dchi, 0, m, 1}; b.g.chi_dst = ViewW{nullptr, 0, 0, 0};
+    b.g.phi = View{dphi, 0, m, 1};
     int lo = std::min(p0, p1), hi = std::max(p0, p1);
-    b.ins[0] = lo; b.ins[1] = hi;
+    b.g.nu = 2; b.g.tp0 = 0; b.g.tp1 = 1; b.g.upd = 0;
+    b.g.ins[0] = lo; b.g.ins[1] = hi;
     for (int v = 0; v < 16; ++v)
-      b.off[v] = v < 4 ? (((long long)(v & 1) << p0) | ((long long)((v >> 1) & 1) << p1)) : 0;
-    b.partials = dpart; b.counters = dcnt; b.e_red = dred; b.fuse_polar = 0; b.env_gate = 0;
-    b.upd_gate = -1; b.S = 1;
+      b.g.off[v] = v < 4 ? (((long long)(v & 1) << p0) | ((long long)((v >> 1) & 1) << p1)) : 0;
+    b.partials = dpart; b.counters = dcnt; b.e_red = dred; b.fuse_polar = 0; b.g.env_gate = 0;
+    b.g.upd_gate = -1; b.S = 1;
     c->cur_st = c->st;
     LaunchScope ls(c, K_OP, 2.0 * bytes, 32.0 * m * c->N);
-    e = launch_bwd(b, 1, 0, 1, false, c->st);
+    e = launch_bwd(b, 1, c->st);
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->st);
   if (e == cudaSuccess) e = cudaMemcpy(env, dred, 32 * sizeof(double), cudaMemcpyDeviceToHost);
@@ -1060,7 +1138,8 @@ void qfs_destroy(qfs_ctx *c) {
   dfree(c->d_gates); dfree(c->d_chi); dfree(c->d_B); dfree(c->d_vb0); dfree(c->d_vb1);
   dfree(c->d_partials); dfree(c->d_ered); dfree(c->d_sig); dfree(c->d_csum); dfree(c->d_rowout);
   dfree(c->d_cval); dfree(c->d_counters); dfree(c->d_slots); dfree(c->d_env_trace);
-  dfree(c->d_stage); dfree(c->d_vprev);
+  dfree(c->d_stage); dfree(c->d_vprev); dfree(c->d_desc);
+  dfree(c->d_flags); dfree(c->d_counters2); dfree(c->d_partials2);
   if (c->h_csum) cudaFreeHost(c->h_csum);
   if (c->h_cval) cudaFreeHost(c->h_cval);
   for (int g = 0; g < qfs_ctx::GMAX; ++g) {
