@@ -62,13 +62,14 @@ class ClockSampler:
     def __init__(self, index):
         self.index = index
         self.proc = None
-        self.lines = []
+        self.lines = []          # (host time, csv line)
+        self.window = None
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -77,7 +78,11 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self, t0, t1):
+        """The timed region, host wall clock."""
+        self.window = (t0, t1)
 
     def __exit__(self, *a):
         if self.proc:
@@ -90,7 +95,13 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        sel = self.lines
+        if self.window and self.lines:
+            t0, t1 = self.window
+            sel = [x for x in self.lines if t0 - 0.05 <= x[0] <= t1 + 0.05]
+            if not sel:  # region shorter than the sampling period: nearest samples
+                sel = sorted(self.lines, key=lambda x: abs(x[0] - 0.5 * (t0 + t1)))[:2]
+        for _, ln in sel:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 6:
                 continue
@@ -215,6 +226,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    # ---- clocks are sampled from before the warm-up (nvidia-smi needs time to start)
+    clk = ClockSampler(local).__enter__()
     # ---- warm-up (also captures the CUDA graph of the sweep)
     gates, _, _ = ctx.instantiate(init, bench_params(args.warmup, m))
 
@@ -222,11 +235,12 @@ def main():
     l0 = ctx.launch_count()
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        ev0.record(stream)
-        gates, res, _ = ctx.instantiate(gates, bench_params(args.steps, m))
-        ev1.record(stream)
-        ev1.synchronize()
+    th0 = time.time()
+    ev0.record(stream)
+    gates, res, _ = ctx.instantiate(gates, bench_params(args.steps, m))
+    ev1.record(stream)
+    ev1.synchronize()
+    clk.mark(th0, time.time())
     barrier()
     launches = ctx.launch_count() - l0
     dt = max_over_ranks(ev0.elapsed_time(ev1) / 1e3)
@@ -248,6 +262,7 @@ def main():
     pe1.synchronize()
     prof = ctx.profile_read()
     ctx.profile_enable(False)
+    clk.__exit__(None, None, None)
     prof_step_ms = pe0.elapsed_time(pe1) / args.steps
 
     # ---- roofline of the dominant kernel (by device time)

@@ -87,6 +87,14 @@ qfs_status qfs_create(int n, int k, const int32_t *pairs, int device, qfs_ctx **
 qfs_status qfs_create_dist(int n, int k, const int32_t *pairs, int device, void *nccl_comm,
                            int rank, int world, int shard_mode, qfs_ctx **out);
 
+/* NCCL bootstrap owned by the library: rank 0 calls qfs_nccl_unique_id
+ * (128 opaque bytes), the caller broadcasts them (e.g. torch.distributed), and
+ * every rank calls qfs_create_nccl; the context creates and owns the
+ * communicator (destroyed by qfs_destroy).  Same semantics as qfs_create_dist. */
+qfs_status qfs_nccl_unique_id(void *id128);
+qfs_status qfs_create_nccl(int n, int k, const int32_t *pairs, int device, const void *id128,
+                           int rank, int world, int shard_mode, qfs_ctx **out);
+
 /* Training pool x, targets y = U x (the A tensor) [m_pool][2^n][2], and
  * validation states xv, yv = U xv [v][2^n][2] (v may be 0).  Host
  * pointers; copied.  Training set = the first M rows of the pool; doubling

@@ -59,6 +59,7 @@ struct BwdParams {
   unsigned long long *dbg;    // diagnostics: [K][4] globaltimer stamps, or nullptr
   // persistent kernel only
   unsigned *flags;            // [S_act] gates completed this sweep (release/acquire)
+  int stagger;                // slots j >= n_slots/2 start after slot j - n_slots/2 finished a gate
   View chi_final, x_final;    // sweep-end cost: chi' = G_0^dag chi vs x
   int fp0, fp1;               // pair of gate 0
   double *partials2;          // [S_act][nb]
@@ -93,11 +94,24 @@ struct FinalParams {
 // Per-gate forward: dst = G_k src for every (quadruple, sample) of every slot.
 struct FwdGateParams {
   int n, nb, k, K, rows_fixed; // rows_fixed > 0: that many rows per start (validation)
+  int cache_mode;              // bit 0: stores L2::evict_last, bit 1: loads L2::evict_first
   const Slot *slots;
   int p0, p1;
   const double2 *gates;
   View src;
   ViewW dst;
+};
+
+// Two consecutive forward gates per pass (fwd2_kernel): B_{k+1}, B_{k+2}.
+struct Fwd2Params {
+  int n, nb, k, K;
+  int nu, tp0, tp1;           // union bits; local positions of gate k+1's pair
+  const Slot *slots;
+  const double2 *gates;
+  uint32_t ins[4];            // union bit positions, ascending
+  long long off[16];          // amplitude offset of local index v
+  View src;                   // B_k (sample-minor, sm == 1)
+  ViewW dst1, dst2;           // B_{k+1}, B_{k+2}
 };
 
 // Whole-row validation forward in shared memory (n <= 13): one CTA per
@@ -133,6 +147,7 @@ int bwd_persistent_ctas_per_sm();  // co-resident CTAs per SM of the persistent 
 cudaError_t launch_polar(const PolarParams &p, int n_slots, cudaStream_t st);
 cudaError_t launch_final(const FinalParams &p, int n_slots, cudaStream_t st);
 cudaError_t launch_fwd_gate(const FwdGateParams &p, int n_slots, cudaStream_t st);
+cudaError_t launch_fwd2(const Fwd2Params &p, int n_slots, cudaStream_t st);
 cudaError_t launch_val_row(const ValRowParams &p, int n_slots, cudaStream_t st);
 cudaError_t launch_dist(const DistParams &p, int n_slots, cudaStream_t st);
 cudaError_t launch_row_reduce(const double *row_in, int rows, double *out, int n_slots,

@@ -92,6 +92,28 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool va
   const int sz = valid ? 16 : 0;
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz) : "memory");
 }
+// L2 eviction-priority policies (createpolicy) and hinted LDGSTS / stores
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void cp_async16_hint(void *smem, const void *gmem, bool valid, uint64_t pol) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;\n" ::"r"(sa), "l"(gmem), "r"(sz),
+               "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void st_hint(double2 *p, double2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
@@ -590,6 +612,10 @@ __global__ void __launch_bounds__(BWD_THREADS, QFS_BWD_MINB) bwd_persistent_kern
   const int j = blockIdx.y;
   const Slot sl = P.slots[j];
   const unsigned Ms = (unsigned)sl.m;
+  // stagger: the second half of the starts lags the first by one gate, so one
+  // half's polar tail overlaps the other half's contraction on the same SMs
+  const int half = (int)gridDim.y / 2;
+  if (P.stagger && half > 0 && j >= half && P.K > 1) cta_wait_flag(P.flags + (j - half), 1u);
   for (int i = P.K - 1; i >= 0; --i) {
     if (i < P.K - 1) cta_wait_flag(P.flags + j, (unsigned)(P.K - 1 - i));
     const GateDesc &G = P.desc[i];
@@ -752,6 +778,20 @@ __global__ void __launch_bounds__(RED_THREADS, 4) final_kernel(const FinalParams
   }
 }
 
+// local index of member l of quadruple q for the pair at local bits (TP0, TP1)
+// (the other local bits, ascending, take the bits of q)
+template <int NU, int TP0, int TP1>
+__host__ __device__ constexpr int pv_idx(int q, int l) {
+  int v = ((l & 1) << TP0) | (((l >> 1) & 1) << TP1);
+  int bit = 0;
+  for (int t = 0; t < NU; ++t) {
+    if (t == TP0 || t == TP1) continue;
+    v |= ((q >> bit) & 1) << t;
+    ++bit;
+  }
+  return v;
+}
+
 // ------------------------------------------------------ forward (per gate) --
 // B_{k+1} = G_k B_k for every (quadruple, sample) of every active start.
 __global__ void __launch_bounds__(FWD_THREADS, 3) fwd_gate_kernel(const FwdGateParams P) {
@@ -784,13 +824,20 @@ __global__ void __launch_bounds__(FWD_THREADS, 3) fwd_gate_kernel(const FwdGateP
     base = insert_zero32(insert_zero32(q, lo), hi);
     return true;
   };
+  const uint64_t pol_ld = policy_evict_first(), pol_st = policy_evict_last();
+  const int cm = P.cache_mode;
   auto issue = [&](int k) {
     unsigned base = 0, m = 0;
     const bool ok = locate(k, base, m);
     double2 *stp = fstage + (k % FWD_STAGES) * 4 * FWD_THREADS + threadIdx.x;
     const double2 *sp = src + (long long)base * P.src.sa + (long long)m * P.src.sm;
+    if (cm & 2) {
 #pragma unroll
-    for (int l = 0; l < 4; ++l) cp_async16(stp + l * FWD_THREADS, ok ? sp + soff[l] : src, ok);
+      for (int l = 0; l < 4; ++l) cp_async16_hint(stp + l * FWD_THREADS, ok ? sp + soff[l] : src, ok, pol_ld);
+    } else {
+#pragma unroll
+      for (int l = 0; l < 4; ++l) cp_async16(stp + l * FWD_THREADS, ok ? sp + soff[l] : src, ok);
+    }
     cp_async_commit();
   };
 #pragma unroll
@@ -810,10 +857,86 @@ __global__ void __launch_bounds__(FWD_THREADS, 3) fwd_gate_kernel(const FwdGateP
       double2 r = make_double2(0.0, 0.0);
 #pragma unroll
       for (int b = 0; b < 4; ++b) cfma(r, sG[4 * a + b], v[b]);
-      dp[doff[a]] = r;
+      if (cm & 1) st_hint(dp + doff[a], r, pol_st);
+      else dp[doff[a]] = r;
     }
   }
   cp_async_wait<0>();
+}
+
+// ---------------------------------------------- forward, two gates per pass --
+// B_{k+1} = G_k B_k and B_{k+2} = G_{k+1} B_{k+1} in one pass: one thread per
+// (2^NU-amplitude group spanned by both pairs, sample), sample fastest (coalesced
+// warp accesses for any pair).  Local bits 0,1 = gate k's pair; gate k+1's pair
+// sits at local (TP0, TP1).  Per amplitude: 16 B read, 32 B written, instead of
+// 32 B read and 32 B written by two single-gate passes.
+template <int NU, int TP0, int TP1>
+__global__ void __launch_bounds__(FWD_THREADS, 1) fwd2_kernel(const Fwd2Params P) {
+  constexpr int NV = 1 << NU;
+  constexpr int NQ = NV / 4;
+  __shared__ double2 sG[2][16];
+  const int j = blockIdx.y;
+  const Slot sl = P.slots[j];
+  const int s = sl.s;
+  const unsigned Ms = (unsigned)sl.m;
+  const unsigned items = Ms << (P.n - NU);
+  const unsigned chunk = (items + P.nb - 1) / P.nb;
+  const unsigned beg = blockIdx.x * chunk, end = min(items, beg + chunk);
+  const FastDiv fdm(Ms);
+  if (threadIdx.x < 32) {
+    const int q = threadIdx.x >> 4, e = threadIdx.x & 15;
+    sG[q][e] = P.gates[((long long)s * P.K + P.k + q) * 16 + e];
+  }
+  __syncthreads();
+  const double2 *src = P.src.base + (long long)s * P.src.ss;
+  double2 *d1 = P.dst1.base + (long long)s * P.dst1.ss;
+  double2 *d2 = P.dst2.base + (long long)s * P.dst2.ss;
+  const unsigned ssa = (unsigned)P.src.sa, dsa = (unsigned)P.dst1.sa;
+  uint32_t ins[NU];
+#pragma unroll
+  for (int q = 0; q < NU; ++q) ins[q] = P.ins[q];
+  for (unsigned w = beg + threadIdx.x; w < end; w += blockDim.x) {
+    unsigned g = fdm.div(w);
+    const unsigned m = w - g * Ms;
+#pragma unroll
+    for (int q = 0; q < NU; ++q) g = insert_zero32(g, ins[q]);
+    const double2 *sp = src + (g * ssa + m);
+    double2 v[NV];
+#pragma unroll
+    for (int u = 0; u < NV; ++u) v[u] = sp[(unsigned)P.off[u] * ssa];
+    // gate k on local bits (0,1)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      double2 o[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        o[a] = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) cfma(o[a], sG[0][4 * a + b], v[4 * q + b]);
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) v[4 * q + a] = o[a];
+    }
+    double2 *p1 = d1 + (g * dsa + m);
+#pragma unroll
+    for (int u = 0; u < NV; ++u) p1[(unsigned)P.off[u] * dsa] = v[u];
+    // gate k+1 on local bits (TP0, TP1)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      double2 o[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        o[a] = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) cfma(o[a], sG[1][4 * a + b], v[pv_idx<NU, TP0, TP1>(q, b)]);
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) v[pv_idx<NU, TP0, TP1>(q, a)] = o[a];
+    }
+    double2 *p2 = d2 + (g * dsa + m);
+#pragma unroll
+    for (int u = 0; u < NV; ++u) p2[(unsigned)P.off[u] * dsa] = v[u];
+  }
 }
 
 // --------------------------------------------------- validation (row in SMEM) --
@@ -1081,6 +1204,25 @@ cudaError_t launch_fwd_gate(const FwdGateParams &p, int n_slots, cudaStream_t st
     attr = true;
   }
   fwd_gate_kernel<<<dim3(p.nb, n_slots), FWD_THREADS, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fwd2(const Fwd2Params &p, int n_slots, cudaStream_t st) {
+  dim3 grid(p.nb, n_slots), block(FWD_THREADS);
+#define QFS_FWD2(NU, A, B) fwd2_kernel<NU, A, B><<<grid, block, 0, st>>>(p)
+  if (p.nu == 2) {
+    if (p.tp0 == 0) QFS_FWD2(2, 0, 1);
+    else QFS_FWD2(2, 1, 0);
+  } else if (p.nu == 3) {
+    if (p.tp0 == 0 && p.tp1 == 2) QFS_FWD2(3, 0, 2);
+    else if (p.tp0 == 2 && p.tp1 == 0) QFS_FWD2(3, 2, 0);
+    else if (p.tp0 == 1 && p.tp1 == 2) QFS_FWD2(3, 1, 2);
+    else QFS_FWD2(3, 2, 1);
+  } else {
+    if (p.tp0 == 2) QFS_FWD2(4, 2, 3);
+    else QFS_FWD2(4, 3, 2);
+  }
+#undef QFS_FWD2
   return cudaGetLastError();
 }
 

@@ -60,6 +60,7 @@ struct qfs_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join[GMAX] = {nullptr};
   // distribution
   ncclComm_t comm = nullptr;
+  bool owns_comm = false;
   int rank = 0, world = 1, mode = 0;
   int *d_flag = nullptr;
   // samples
@@ -85,6 +86,9 @@ struct qfs_ctx {
   std::vector<GateDesc> h_desc;
   unsigned *d_flags = nullptr, *d_counters2 = nullptr;
   double *d_partials2 = nullptr;
+  int fwd_cache_mode = 0;   // QFS_FWD_CACHE: L2 hints of the forward kernel (diagnostic)
+  int stagger = 1;          // QFS_STAGGER: persistent kernel half-start offset
+  bool fwd_pairs = true;    // QFS_FWD_PAIRS=0: one forward pass per gate
   bool persistent = false;  // QFS_PERSISTENT=1 selects the cooperative whole-backward kernel
   size_t stage_bytes = 0;
   // graph cache
@@ -444,18 +448,56 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
   auto Bk = [&](int k) -> double2 * { return c->d_B + (long long)(k - 1) * c->S_cap * sS; };
   double units = 0;  // amplitudes of all active training rows
   for (int j = j0; j < j1; ++j) units += (double)sp.slots[j].m * (double)N;
-  // (a) forward: B_1 .. B_{K-1}, one coalesced launch per gate
+  // (a) forward: B_1 .. B_{K-1}: two gates per coalesced pass
+  // (a single-gate pass for an odd tail)
   if (K > 1) {
   PhaseScope phase_fwd(c, K_FWD_GATE);
-  for (int k = 0; k + 1 < K; ++k) {
-    FwdGateParams f{};
-    f.n = n; f.k = k; f.K = K; f.rows_fixed = 0; f.slots = slots;
-    f.p0 = c->pairs[2 * k]; f.p1 = c->pairs[2 * k + 1]; f.gates = c->d_gates;
-    f.nb = blocks_per_start(((long long)M_max * N) >> 2, ns, 3);
-    f.src = k == 0 ? xpool : View{Bk(k), sS, Mc, 1};
-    f.dst = ViewW{Bk(k + 1), sS, Mc, 1};
-    LaunchScope ls(c, K_FWD_GATE, units * 32.0, units * 32.0);
-    CUDA_TRY(c, launch_fwd_gate(f, ns, st));
+  for (int k = 0; k + 1 < K;) {
+    const View src = k == 0 ? xpool : View{Bk(k), sS, Mc, 1};
+    if (k + 2 < K && c->fwd_pairs) {
+      Fwd2Params f{};
+      f.n = n; f.k = k; f.K = K; f.slots = slots; f.gates = c->d_gates;
+      int loc[4] = {c->pairs[2 * k], c->pairs[2 * k + 1], 0, 0}, nu = 2;
+      const int q0 = c->pairs[2 * (k + 1)], q1 = c->pairs[2 * (k + 1) + 1];
+      int ex[2], ne = 0;
+      for (int q : {q0, q1})
+        if (q != loc[0] && q != loc[1]) ex[ne++] = q;
+      if (ne == 2 && ex[0] > ex[1]) std::swap(ex[0], ex[1]);
+      for (int t = 0; t < ne; ++t) loc[nu++] = ex[t];
+      f.nu = nu;
+      for (int t = 0; t < nu; ++t) {
+        if (loc[t] == q0) f.tp0 = t;
+        if (loc[t] == q1) f.tp1 = t;
+      }
+      int srt[4];
+      for (int t = 0; t < nu; ++t) srt[t] = loc[t];
+      std::sort(srt, srt + nu);
+      for (int t = 0; t < 4; ++t) f.ins[t] = t < nu ? srt[t] : 0;
+      for (int v = 0; v < 16; ++v) {
+        long long o = 0;
+        for (int t = 0; t < nu; ++t)
+          if ((v >> t) & 1) o |= 1LL << loc[t];
+        f.off[v] = v < (1 << nu) ? o : 0;
+      }
+      f.nb = blocks_per_start(((long long)M_max * N) >> nu, ns, 1);
+      f.src = src;
+      f.dst1 = ViewW{Bk(k + 1), sS, Mc, 1};
+      f.dst2 = ViewW{Bk(k + 2), sS, Mc, 1};
+      LaunchScope ls(c, K_FWD_GATE, units * 48.0, units * 64.0);
+      CUDA_TRY(c, launch_fwd2(f, ns, st));
+      k += 2;
+    } else {
+      FwdGateParams f{};
+      f.n = n; f.k = k; f.K = K; f.rows_fixed = 0; f.slots = slots;
+      f.p0 = c->pairs[2 * k]; f.p1 = c->pairs[2 * k + 1]; f.gates = c->d_gates;
+      f.nb = blocks_per_start(((long long)M_max * N) >> 2, ns, 3);
+      f.src = src;
+      f.dst = ViewW{Bk(k + 1), sS, Mc, 1};
+      f.cache_mode = c->fwd_cache_mode;
+      LaunchScope ls(c, K_FWD_GATE, units * 32.0, units * 32.0);
+      CUDA_TRY(c, launch_fwd_gate(f, ns, st));
+      k += 1;
+    }
   }
   }
   // (b, c) backward: gate i = K-1 .. 0 (P:112 right to left; Fig. env_calc)
@@ -477,6 +519,7 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
     b.desc = c->d_desc;
     b.nb = std::max(1, std::min(148 * bwd_persistent_ctas_per_sm() / ns, kMaxBlocksPerStart));
     b.flags = c->d_flags + j0;
+    b.stagger = c->stagger;
     b.chi_final = K == 1 ? ypool : View{c->d_chi, sS, Mc, 1};
     b.x_final = xpool; b.fp0 = c->pairs[0]; b.fp1 = c->pairs[1];
     b.partials2 = c->d_partials2 + (long long)j0 * c->nb_cap;
@@ -700,6 +743,9 @@ qfs_status create_common(int n, int k, const int32_t *pairs, int device, qfs_ctx
   c->cur_st = c->st;
   if (const char *gs = getenv("QFS_GROUPS")) c->groups = std::max(1, std::min(qfs_ctx::GMAX, atoi(gs)));
   if (const char *ps = getenv("QFS_PERSISTENT")) c->persistent = atoi(ps) != 0;
+  if (const char *fc = getenv("QFS_FWD_CACHE")) c->fwd_cache_mode = atoi(fc);
+  if (const char *sg = getenv("QFS_STAGGER")) c->stagger = atoi(sg);
+  if (const char *fp = getenv("QFS_FWD_PAIRS")) c->fwd_pairs = atoi(fp) != 0;
   if (e != cudaSuccess) {
     c->err = std::string("device init: ") + cudaGetErrorString(e);
     *out = c;  // caller can read the error, then destroy
@@ -737,6 +783,33 @@ qfs_status qfs_create_dist(int n, int k, const int32_t *pairs, int device, void 
         cr != rank || cn != world)
       return fail(c, QFS_ERR_ARG, "nccl communicator rank/size mismatch");
   }
+  return QFS_OK;
+}
+
+qfs_status qfs_nccl_unique_id(void *id128) {
+  if (!id128) return QFS_ERR_ARG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return QFS_ERR_DEVICE;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  std::memcpy(id128, &id, sizeof id);
+  return QFS_OK;
+}
+
+qfs_status qfs_create_nccl(int n, int k, const int32_t *pairs, int device, const void *id128,
+                           int rank, int world, int shard_mode, qfs_ctx **out) {
+  if (!id128 || world < 1 || rank < 0 || rank >= world || (shard_mode != 0 && shard_mode != 1))
+    return QFS_ERR_ARG;
+  qfs_status s = create_common(n, k, pairs, device, out);
+  if (s != QFS_OK) return s;
+  qfs_ctx *c = *out;
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof id);
+  ncclComm_t comm = nullptr;
+  ncclResult_t r = ncclCommInitRank(&comm, world, id, rank);
+  if (r != ncclSuccess) return fail(c, QFS_ERR_DEVICE, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  c->comm = comm;
+  c->owns_comm = true;
+  c->rank = rank; c->world = world; c->mode = shard_mode;
   return QFS_OK;
 }
 
@@ -1148,6 +1221,7 @@ void qfs_destroy(qfs_ctx *c) {
   }
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->st) cudaStreamDestroy(c->st);
+  if (c->owns_comm && c->comm) ncclCommDestroy(c->comm);
   delete c;
 }
 

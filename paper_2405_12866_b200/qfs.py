@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libqfs.so")
 STATUS = {0: "QFS_OK", 1: "QFS_ERR_ARG", 2: "QFS_ERR_CAPACITY", 3: "QFS_ERR_NUMERIC",
           4: "QFS_ERR_DEVICE", 5: "QFS_ERR_STATE"}
 TERM_NAMES = {0: "CONVERGED", 1: "PLATEAU", 2: "MAX_ITER", 3: "POOL_EXHAUSTED", 4: "STOPPED"}
-SYMBOLS = ["qfs_create", "qfs_create_dist", "qfs_set_samples", "qfs_set_samples_device",
+SYMBOLS = ["qfs_create", "qfs_create_dist", "qfs_nccl_unique_id", "qfs_create_nccl", "qfs_set_samples", "qfs_set_samples_device",
            "qfs_instantiate", "qfs_trace_sweeps", "qfs_bench_sweeps", "qfs_op_apply",
            "qfs_op_environment", "qfs_op_polar", "qfs_profile_enable", "qfs_profile_read",
            "qfs_launch_count", "qfs_stream", "qfs_last_error", "qfs_destroy"]
@@ -66,6 +66,8 @@ def load(path: str = LIB_PATH):
         lib.qfs_destroy.restype = None
         lib.qfs_create.argtypes = [ip, ip, vp, ip, ctypes.POINTER(vp)]
         lib.qfs_create_dist.argtypes = [ip, ip, vp, ip, vp, ip, ip, ip, ctypes.POINTER(vp)]
+        lib.qfs_nccl_unique_id.argtypes = [vp]
+        lib.qfs_create_nccl.argtypes = [ip, ip, vp, ip, vp, ip, ip, ip, ctypes.POINTER(vp)]
         lib.qfs_set_samples.argtypes = [vp, ip, vp, vp, ip, vp, vp]
         lib.qfs_set_samples_device.argtypes = [vp, ip, vp, vp, ip, vp, vp, vp]
         lib.qfs_instantiate.argtypes = [vp, ip, vp, ctypes.POINTER(Params), vp, vp, ctypes.POINTER(ip)]
@@ -95,16 +97,31 @@ def make_params(d: dict) -> Params:
     return Params(**{f: d[f] for f, _ in Params._fields_})
 
 
-class Context:
-    """One qfs_ctx: a circuit structure on one device (qfs_create / qfs_create_dist)."""
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0), to be broadcast to the other ranks."""
+    buf = ctypes.create_string_buffer(128)
+    rc = load().qfs_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p))
+    if rc != 0:
+        raise QfsError(rc, "ncclGetUniqueId failed")
+    return buf.raw
 
-    def __init__(self, n, pairs, device=0, nccl_comm=None, rank=0, world=1, shard_mode=0):
+
+class Context:
+    """One qfs_ctx: a circuit structure on one device (qfs_create / qfs_create_dist /
+    qfs_create_nccl when ``nccl_id`` is given)."""
+
+    def __init__(self, n, pairs, device=0, nccl_comm=None, rank=0, world=1, shard_mode=0, nccl_id=None):
         self.lib = load()
         self.n = int(n)
         self.pairs = np.ascontiguousarray(pairs, dtype=np.int32)
         self.k = int(self.pairs.shape[0])
         h = ctypes.c_void_p()
-        if nccl_comm is None and world == 1:
+        if nccl_id is not None:
+            idb = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            rc = self.lib.qfs_create_nccl(self.n, self.k, _ptr(self.pairs), int(device),
+                                          ctypes.cast(idb, ctypes.c_void_p), int(rank), int(world),
+                                          int(shard_mode), ctypes.byref(h))
+        elif nccl_comm is None and world == 1:
             rc = self.lib.qfs_create(self.n, self.k, _ptr(self.pairs), int(device), ctypes.byref(h))
         else:
             rc = self.lib.qfs_create_dist(self.n, self.k, _ptr(self.pairs), int(device),

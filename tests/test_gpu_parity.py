@@ -292,3 +292,37 @@ def test_errors(qfs):
     with pytest.raises(QfsError) as ei:
         ctx.set_samples(nanx, p.y)
     assert ei.value.status == 3
+
+
+# ------------------------------------------------------------- distributed --
+def test_sample_sharded_path_single_rank(qfs):
+    """qfs_create_nccl in sample mode (per-gate NCCL all-reduce of E + polar
+    kernel) with a one-rank communicator equals the oracle and the fused path."""
+    p = I.make_problem("c3", init="W", s=4)
+    nid = qfs.nccl_unique_id()
+    ctx = qfs.Context(p.n, p.pairs, nccl_id=nid, rank=0, world=1, shard_mode=1)
+    ctx.set_samples(p.x, p.y, p.xv, p.yv)
+    gt = ctx.trace_sweeps(p.init, 32, 3)
+    ot = oracle.trace_sweeps(p.n, p.pairs, p.init, p.x, p.y, 32, 3)
+    _compare_traces(gt, ot, "sample-mode")
+    ref = _ctx(qfs, p.n, p.pairs)
+    ref.set_samples(p.x, p.y, p.xv, p.yv)
+    rt = ref.trace_sweeps(p.init, 32, 3)
+    assert np.abs(rt["gates"] - gt["gates"]).max() < 1e-13
+    g1, r1, w1 = ctx.instantiate(p.init, dict(p.params, max_iter=200))
+    g2, r2, w2 = ref.instantiate(p.init, dict(p.params, max_iter=200))
+    assert w1 == w2 and r1[w1]["term"] == "CONVERGED"
+    assert [r["sweeps"] for r in r1] == [r["sweeps"] for r in r2]
+
+
+def test_multistart_dist_path_single_rank(qfs):
+    """qfs_create_nccl in multistart mode: per-sweep (any converged, any active)
+    NCCL all-reduce in the controller; same decisions as the plain context."""
+    p = I.make_problem("c2", init="W", s=4)
+    ctx = qfs.Context(p.n, p.pairs, nccl_id=qfs.nccl_unique_id(), rank=0, world=1, shard_mode=0)
+    ctx.set_samples(p.x, p.y, p.xv, p.yv)
+    g1, r1, w1 = ctx.instantiate(p.init, dict(p.params, max_iter=300))
+    g2, r2, w2 = oracle.instantiate(p.n, p.pairs, p.x, p.y, p.xv, p.yv, p.init, dict(p.params, max_iter=300))
+    assert w1 == w2 and r1[w1]["term"] == "CONVERGED"
+    for a, b in zip(r1, r2):
+        assert a["term"] == b["term"] and abs(a["sweeps"] - b["sweeps"]) <= 2

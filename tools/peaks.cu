@@ -48,6 +48,12 @@ __global__ void read_kernel(const double2 *__restrict__ a, size_t n, double *out
   if (s == 123.456) out[0] = s;
 }
 __global__ void empty_kernel() {}
+// write only: 16 B per element
+__global__ void write_kernel(double2 *__restrict__ a, size_t n) {
+  size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  size_t st = (size_t)gridDim.x * blockDim.x;
+  for (; i < n; i += st) a[i] = make_double2((double)i, 1.0);
+}
 // `passes` read-modify-write passes over an L2-resident buffer inside one launch
 __global__ void rmw_loop_kernel(double2 *__restrict__ a, size_t n, int passes) {
   size_t st = (size_t)gridDim.x * blockDim.x;
@@ -114,6 +120,18 @@ int main() {
       float ms; CK(cudaEventElapsedTime(&ms, e0, e1)); if (r) best = std::min(best, ms);
     }
     printf(", \"l2loop_%zuMiB_rmw_gbs\": %.1f", mib, 20 * 32.0 * n / (best * 1e-3) / 1e9);
+    CK(cudaFree(a));
+  }
+  {  // HBM write-only
+    size_t n = (4ull << 30) / 16;
+    double2 *a; CK(cudaMalloc(&a, n * 16));
+    float best = 1e30f;
+    for (int r = 0; r < 6; ++r) {
+      CK(cudaEventRecord(e0)); write_kernel<<<p.multiProcessorCount * 8, 256>>>(a, n);
+      CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
+      float ms; CK(cudaEventElapsedTime(&ms, e0, e1)); if (r) best = std::min(best, ms);
+    }
+    printf(", \"hbm_4GiB_write_gbs\": %.1f", 16.0 * n / (best * 1e-3) / 1e9);
     CK(cudaFree(a));
   }
   bw(16ull << 20, "l2_16MiB");
