@@ -34,6 +34,7 @@ struct ViewW {
 struct GateDesc {
   int nu, tp0, tp1, upd;      // union bits; local positions of gate i's pair; update?
   int upd_gate, env_gate;     // i+1 (or -1), i
+  int pre;                    // 1: phi does not depend on the previous launch (PDL prefetch)
   uint32_t ins[4];            // union bit positions, ascending (for zero insertion)
   long long off[16];          // amplitude offset of local index v (local bit t <-> loc[t])
   View chi_src;
@@ -159,6 +160,8 @@ cudaError_t launch_transpose(const double2 *src, double2 *dst, int rows, long lo
                              cudaStream_t st);
 cudaError_t launch_finite_check(const double *p, long long n, int *flag, cudaStream_t st);
 cudaError_t launch_identity_fill(double2 *v, long long count16, cudaStream_t st);
+void set_pdl(bool on);     // launch with programmatic dependent launch (default on)
+bool pdl_enabled();
 int val_row_max_n();        // largest n the shared-memory validation forward supports
 int blocks_per_sm(int nu);  // resident CTAs per SM of the backward kernel
 

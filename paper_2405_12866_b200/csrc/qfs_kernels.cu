@@ -118,6 +118,14 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+// Programmatic dependent launch (PDL): a kernel launched with the
+// programmatic-stream-serialization attribute may start while the previous
+// kernel on the stream drains; everything before pdl_wait() must not depend on
+// that kernel's results.  pdl_trigger() lets the next kernel start launching.
+// Both are no-ops for a kernel launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ double2 shfl_c(double2 v, int src) {
   return make_double2(__shfl_sync(FULL, v.x, src), __shfl_sync(FULL, v.y, src));
 }
@@ -355,14 +363,6 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
   const unsigned end = min(units, beg + chunk);
   const FastDiv fdu(nmb);
 
-  if (UPD && threadIdx.x < 16) {
-    const int a = threadIdx.x >> 2, b = threadIdx.x & 3;
-    const double2 g = __ldcg(P.gates + ((long long)s * P.K + G.upd_gate) * 16 + 4 * b + a);
-    sh.sQ[threadIdx.x] = cconj(g);  // (G^dag)[a][b]
-  }
-  if (P.dbg && threadIdx.x == 0) atomicMin(P.dbg + 4 * G.env_gate, gtimer());
-  __syncthreads();
-
   double2 acc[4][4][AZ];
 #pragma unroll
   for (int p = 0; p < 4; ++p)
@@ -402,18 +402,45 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
     ef = g * fsa + m;
     return m < Ms;
   };
-  auto issue = [&](int k) {
+  auto issue_part = [&](int k, bool chi, bool phi) {
     unsigned ec = 0, ed = 0, ef = 0;
     const bool ok = locate(k, ec, ed, ef);
     double2 *st = stage_buf + (k % BWD_STAGES) * 8 * BWD_THREADS + threadIdx.x;
+    if (chi) {
 #pragma unroll
-    for (int l = 0; l < 4; ++l) cp_async16(st + l * BWD_THREADS, csrc + (ok ? ec + offc[l] : 0u), ok);
+      for (int l = 0; l < 4; ++l) cp_async16(st + l * BWD_THREADS, csrc + (ok ? ec + offc[l] : 0u), ok);
+    }
+    if (phi) {
 #pragma unroll
-    for (int l = 0; l < 4; ++l) cp_async16(st + (4 + l) * BWD_THREADS, fsrc + (ok ? ef + offf[l] : 0u), ok);
+      for (int l = 0; l < 4; ++l) cp_async16(st + (4 + l) * BWD_THREADS, fsrc + (ok ? ef + offf[l] : 0u), ok);
+    }
+  };
+  auto issue = [&](int k) {
+    issue_part(k, true, true);
     cp_async_commit();
   };
+  // Prologue.  phi (B_i, written by the forward pass or the x pool) does not
+  // depend on the previous backward launch, so with G.pre its first stages are
+  // fetched before pdl_wait(), overlapping the previous launch's polar tail.
+  // chi and G_{i+1} are written by the previous launch: read after the wait.
+  if (G.pre) {
 #pragma unroll
-  for (int k = 0; k < BWD_STAGES - 1; ++k) issue(k);
+    for (int k = 0; k < BWD_STAGES - 1; ++k) issue_part(k, false, true);
+    cp_async_commit();
+  }
+  pdl_wait();
+  if (UPD && threadIdx.x < 16) {
+    const int a = threadIdx.x >> 2, b = threadIdx.x & 3;
+    const double2 g = __ldcg(P.gates + ((long long)s * P.K + G.upd_gate) * 16 + 4 * b + a);
+    sh.sQ[threadIdx.x] = cconj(g);  // (G^dag)[a][b]
+  }
+  if (P.dbg && threadIdx.x == 0) atomicMin(P.dbg + 4 * G.env_gate, gtimer());
+#pragma unroll
+  for (int k = 0; k < BWD_STAGES - 1; ++k) {
+    issue_part(k, true, !G.pre);
+    cp_async_commit();
+  }
+  __syncthreads();
 
   for (int k = 0; k < iters; ++k) {
     issue(k + BWD_STAGES - 1);
@@ -499,6 +526,7 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
   }
   cp_async_wait<0>();
   if (UPD && fence_chi) __threadfence();  // chi visible to the other CTAs before the ticket
+  pdl_trigger();  // all of this CTA's reads of chi/phi are done
 
   // CTA reduction: over the sample lanes of each lane-group, then lane groups
   // and warps in a fixed order
@@ -706,6 +734,7 @@ __global__ void polar_kernel(const PolarParams P) {
   __shared__ double2 scratch[4][32];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int j = blockIdx.x * 4 + w;
+  pdl_wait();
   if (j >= P.n_slots) return;
   const Slot sl = P.slots[j];
   e32[w][lane] = P.e_red[(long long)j * 32 + lane];
@@ -728,6 +757,7 @@ __global__ void __launch_bounds__(RED_THREADS, 4) final_kernel(const FinalParams
   const unsigned chunk = (items + P.nb - 1) / P.nb;
   const unsigned beg = blockIdx.x * chunk, end = min(items, beg + chunk);
   const FastDiv fdm(Ms);
+  pdl_wait();
   if (threadIdx.x < 16) {
     const int a = threadIdx.x >> 2, b = threadIdx.x & 3;
     sQ[threadIdx.x] = cconj(P.gates[(long long)s * P.K * 16 + 4 * b + a]);
@@ -759,6 +789,7 @@ __global__ void __launch_bounds__(RED_THREADS, 4) final_kernel(const FinalParams
       acc = fma(di, di, acc);
     }
   }
+  pdl_trigger();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int q = 16; q >= 1; q >>= 1) acc += __shfl_xor_sync(FULL, acc, q);
@@ -804,6 +835,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 3) fwd_gate_kernel(const FwdGateP
   const unsigned chunk = (items + P.nb - 1) / P.nb;
   const unsigned beg = blockIdx.x * chunk, end = min(items, beg + chunk);
   const FastDiv fdm(Ms);
+  pdl_wait();
   if (threadIdx.x < 16) sG[threadIdx.x] = P.gates[((long long)s * P.K + P.k) * 16 + threadIdx.x];
   __syncthreads();
   const int lo = min(P.p0, P.p1), hi = max(P.p0, P.p1);
@@ -862,6 +894,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 3) fwd_gate_kernel(const FwdGateP
     }
   }
   cp_async_wait<0>();
+  pdl_trigger();
 }
 
 // ---------------------------------------------- forward, two gates per pass --
@@ -883,6 +916,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) fwd2_kernel(const Fwd2Params P
   const unsigned chunk = (items + P.nb - 1) / P.nb;
   const unsigned beg = blockIdx.x * chunk, end = min(items, beg + chunk);
   const FastDiv fdm(Ms);
+  pdl_wait();
   if (threadIdx.x < 32) {
     const int q = threadIdx.x >> 4, e = threadIdx.x & 15;
     sG[q][e] = P.gates[((long long)s * P.K + P.k + q) * 16 + e];
@@ -937,6 +971,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) fwd2_kernel(const Fwd2Params P
 #pragma unroll
     for (int u = 0; u < NV; ++u) p2[(unsigned)P.off[u] * dsa] = v[u];
   }
+  pdl_trigger();
 }
 
 // --------------------------------------------------- validation (row in SMEM) --
@@ -953,6 +988,7 @@ __global__ void __launch_bounds__(VAL_THREADS) val_row_kernel(const ValRowParams
   const long long N = 1LL << P.n;
   const double2 *src = P.xv + (long long)m * N;
   for (long long i = threadIdx.x; i < N; i += blockDim.x) row[i] = __ldg(src + i);
+  pdl_wait();  // the gates are the ones the backward pass just wrote
   const double2 *gs = P.gates + (long long)s * P.K * 16;
   if (threadIdx.x < 16) sG[0][threadIdx.x] = gs[threadIdx.x];
   __syncthreads();
@@ -1006,6 +1042,7 @@ __global__ void __launch_bounds__(VAL_THREADS) val_row_kernel(const ValRowParams
 __global__ void __launch_bounds__(RED_THREADS) dist_kernel(const DistParams P) {
   __shared__ double red[RED_THREADS / 32];
   const int j = blockIdx.y, m = blockIdx.x;
+  pdl_wait();
   const Slot sl = P.slots[j];
   const long long N = 1LL << P.n;
   const double2 *a = P.a.base + (long long)sl.s * P.a.ss + (long long)m * P.a.sm;
@@ -1032,6 +1069,7 @@ __global__ void __launch_bounds__(RED_THREADS) dist_kernel(const DistParams P) {
 // out[j] = sum_r row_in[j*rows + r], in row order
 __global__ void row_reduce_kernel(const double *row_in, int rows, double *out, int n_slots) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  pdl_wait();
   if (j >= n_slots) return;
   double t = 0.0;
   for (int r = 0; r < rows; ++r) t += row_in[(long long)j * rows + r];
@@ -1122,6 +1160,28 @@ __global__ void polar_batch_kernel(const double2 *env, const double2 *g_old, dou
 }  // namespace
 
 // ================================================================ launchers ==
+namespace {
+bool g_pdl = true;
+// Launch kernel k<<<grid, block, smem, st>>>(p), with the programmatic
+// stream serialization attribute when PDL is on (the kernel may begin while
+// the previous one on the stream drains; see pdl_wait / pdl_trigger).
+template <class Prm>
+cudaError_t launch_ex(void (*k)(Prm), dim3 grid, dim3 block, size_t smem, cudaStream_t st, const Prm &p) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, p);
+}
+}  // namespace
+void set_pdl(bool on) { g_pdl = on; }
+bool pdl_enabled() { return g_pdl; }
 int val_row_max_n() { return 13; }
 int blocks_per_sm(int nu) { (void)nu; return QFS_BWD_MINB; }
 
@@ -1136,7 +1196,7 @@ cudaError_t launch_bwd(const BwdParams &p, int n_slots, cudaStream_t st) {
       cudaFuncSetAttribute(bwd_kernel<NU, A, B, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
       attr = true;                                                                             \
     }                                                                                          \
-    bwd_kernel<NU, A, B, U><<<grid, block, smem, st>>>(p);                                     \
+    launch_ex(bwd_kernel<NU, A, B, U>, grid, block, smem, st, p);                              \
   } while (0)
   if (!g.upd) {
     QFS_BWD(2, 0, 1, false);
@@ -1187,12 +1247,12 @@ cudaError_t launch_bwd_persistent(const BwdParams &p, int n_slots, cudaStream_t 
 }
 
 cudaError_t launch_polar(const PolarParams &p, int n_slots, cudaStream_t st) {
-  polar_kernel<<<(n_slots + 3) / 4, 128, 0, st>>>(p);
+  launch_ex(polar_kernel, dim3((n_slots + 3) / 4), dim3(128), 0, st, p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_final(const FinalParams &p, int n_slots, cudaStream_t st) {
-  final_kernel<<<dim3(p.nb, n_slots), RED_THREADS, 0, st>>>(p);
+  launch_ex(final_kernel, dim3(p.nb, n_slots), dim3(RED_THREADS), 0, st, p);
   return cudaGetLastError();
 }
 
@@ -1203,13 +1263,13 @@ cudaError_t launch_fwd_gate(const FwdGateParams &p, int n_slots, cudaStream_t st
     cudaFuncSetAttribute(fwd_gate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  fwd_gate_kernel<<<dim3(p.nb, n_slots), FWD_THREADS, smem, st>>>(p);
+  launch_ex(fwd_gate_kernel, dim3(p.nb, n_slots), dim3(FWD_THREADS), smem, st, p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_fwd2(const Fwd2Params &p, int n_slots, cudaStream_t st) {
   dim3 grid(p.nb, n_slots), block(FWD_THREADS);
-#define QFS_FWD2(NU, A, B) fwd2_kernel<NU, A, B><<<grid, block, 0, st>>>(p)
+#define QFS_FWD2(NU, A, B) launch_ex(fwd2_kernel<NU, A, B>, grid, block, 0, st, p)
   if (p.nu == 2) {
     if (p.tp0 == 0) QFS_FWD2(2, 0, 1);
     else QFS_FWD2(2, 1, 0);
@@ -1233,12 +1293,12 @@ cudaError_t launch_val_row(const ValRowParams &p, int n_slots, cudaStream_t st) 
                          (int)(sizeof(double2) << 13));
     attr_set = true;
   }
-  val_row_kernel<<<dim3(p.rows, n_slots), VAL_THREADS, sizeof(double2) << p.n, st>>>(p);
+  launch_ex(val_row_kernel, dim3(p.rows, n_slots), dim3(VAL_THREADS), sizeof(double2) << p.n, st, p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_dist(const DistParams &p, int n_slots, cudaStream_t st) {
-  dist_kernel<<<dim3(p.rows, n_slots), RED_THREADS, 0, st>>>(p);
+  launch_ex(dist_kernel, dim3(p.rows, n_slots), dim3(RED_THREADS), 0, st, p);
   return cudaGetLastError();
 }
 

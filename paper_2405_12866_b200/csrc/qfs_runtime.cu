@@ -377,6 +377,7 @@ GateDesc make_desc(const qfs_ctx *c, int i) {
   d.upd = upd ? 1 : 0;
   d.upd_gate = upd ? i + 1 : -1;
   d.env_gate = i;
+  d.pre = upd ? 1 : 0;  // phi = B_i (i < K-1) was written by the forward pass, not the previous launch
   const int p0 = c->pairs[2 * i], p1 = c->pairs[2 * i + 1];
   int loc[4], nu;
   if (!upd) {
@@ -746,6 +747,7 @@ qfs_status create_common(int n, int k, const int32_t *pairs, int device, qfs_ctx
   if (const char *fc = getenv("QFS_FWD_CACHE")) c->fwd_cache_mode = atoi(fc);
   if (const char *sg = getenv("QFS_STAGGER")) c->stagger = atoi(sg);
   if (const char *fp = getenv("QFS_FWD_PAIRS")) c->fwd_pairs = atoi(fp) != 0;
+  if (const char *pd = getenv("QFS_PDL")) set_pdl(atoi(pd) != 0);
   if (e != cudaSuccess) {
     c->err = std::string("device init: ") + cudaGetErrorString(e);
     *out = c;  // caller can read the error, then destroy
