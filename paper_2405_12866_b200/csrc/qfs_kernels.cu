@@ -143,13 +143,73 @@ __device__ __forceinline__ double2 shfl_xor_c(double2 v, int m) {
 //     gamma = a_j^dag a_k = |gamma| e^{i phi},  zeta = (||a_k||^2 - ||a_j||^2) / (2|gamma|),
 //     t = sgn(zeta) / (|zeta| + sqrt(1 + zeta^2)),  c = 1/sqrt(1 + t^2),  s = c t,
 //     [a_j a_k] <- [a_j a_k] [[c, s e^{i phi}], [-s e^{-i phi}, c]]   (same on V)
-//   until no pair has |gamma| > 1e-15 ||a_j|| ||a_k||; then sigma_j = ||a_j||,
+//   rotating every pair with |gamma| > 1e-15 ||a_j|| ||a_k||, and stopping after
+//   the first sweep in which no pair had |gamma| > 1e-12 ||a_j|| ||a_k|| (the
+//   rotations of that sweep are applied; convergence is quadratic, so the
+//   residual is far below 1e-12, and no sweep is spent only to verify it, nor
+//   chasing rounding noise near 1e-15); then sigma_j = ||a_j||,
 //   X_j = a_j / sigma_j (null columns, sigma_j <= 1e-14 sigma_max, completed by
 //   Gram-Schmidt on e_0..e_3; R5) and G = V X^dag (eq:opt_u:
 //   E = X D Y^dag, u = Y X^dag with Y = V).  Square roots and divisions are
 //   rsqrt-based (MUFU.RSQ64H + Newton) to keep the serial chain short.
 // E' is scaled by an exact power of two first (the polar factor is scale-free).
 // scratch: 16 double2 of shared memory per half (null-column path only).
+//
+// Fast path first (polar_ns): when E' is far enough from singular, its
+// unitary polar factor W = X Y^dag is reached by Newton-Schulz iterations
+// instead (same result up to rounding; G = W^dag = Y X^dag).
+__device__ __forceinline__ double half_sum(double v) {
+#pragma unroll
+  for (int o = 1; o < 16; o <<= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+// Newton-Schulz polar iteration on a half-warp (lane l = 4r + c holds X[r][c]):
+//   X_0 = E' / s, s = ||E'||_F / 2 (RMS singular value),
+//   X_{k+1} = X_k (3I - X_k^dag X_k) / 2   ->  W, the unitary polar factor of E'.
+// Per singular value u = sigma^2 of X_k, f = u - 1 maps to f' = u(3-u)^2/4 - 1
+// with |f'| <= f^2 for 0 < u < 2, so e_k = ||X_k^dag X_k - I||_F <= e_0^(2^k):
+// when e_0 <= 10^(-16/2^k) (k <= 10), k iterations reach e <= 1e-16 (unitary to
+// rounding).  Returns false (nothing written) when e_0 > 0.9647 for either
+// half of the warp: the Jacobi path below handles that (ill-conditioned or
+// singular E').  The decision and the count are warp-uniform.
+__device__ bool polar_ns(double2 e, int hb, int r, int c, double2 &g_out, double &ss_out) {
+  const double fro2 = half_sum(e.x * e.x + e.y * e.y);
+  if (!__all_sync(FULL, fro2 > 0.0)) return false;
+  const double rs = 2.0 * rsqrt(fro2);
+  double2 x = make_double2(e.x * rs, e.y * rs);
+  auto xhx = [&](double2 X) {  // (X^dag X)[r][c] = sum_q conj(X[q][r]) X[q][c]
+    double2 y = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) cfma(y, cconj(shfl_c(X, hb | (4 * q + r))), shfl_c(X, hb | (4 * q + c)));
+    return y;
+  };
+  double2 y = xhx(x);
+  const double dre = y.x - (r == c ? 1.0 : 0.0);
+  const double e02 = half_sum(dre * dre + y.y * y.y);  // e_0^2
+  // iterations needed: smallest k with e_0 <= 10^(-16/2^k)
+  constexpr double th2[10] = {1e-16, 1e-8, 1e-4, 1e-2, 0.1, 0.31622776601683794, 0.5623413251903491,
+                              0.7498942093324559, 0.8659643233600653, 0.9305720409296991};
+  int k = 11;
+#pragma unroll
+  for (int q = 9; q >= 0; --q)
+    if (e02 <= th2[q]) k = q + 1;
+  k = max(k, __shfl_xor_sync(FULL, k, 16));
+  if (!__all_sync(FULL, k <= 10)) return false;
+  for (int it = 0; it < k; ++it) {
+    if (it > 0) y = xhx(x);
+    const double2 t = make_double2(0.5 * ((r == c ? 3.0 : 0.0) - y.x), -0.5 * y.y);  // (3I - Y)/2
+    double2 z = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) cfma(z, shfl_c(x, hb | (4 * r + q)), shfl_c(t, hb | (4 * q + c)));
+    x = z;
+  }
+  // G = W^dag: G[r][c] = conj(W[c][r]);  sum sigma = Re Tr(W^dag E') = Re sum conj(W) o E'
+  g_out = cconj(shfl_c(x, hb | (4 * c + r)));
+  ss_out = half_sum(x.x * e.x + x.y * e.y);
+  return true;
+}
+
 __device__ void hw_polar(double2 e, double2 v0, double2 &g_out, double2 &v_out, double &sig_sum,
                          double2 *scratch) {
   const int lane = threadIdx.x & 31;
@@ -163,13 +223,34 @@ __device__ void hw_polar(double2 e, double2 v0, double2 &g_out, double2 &v_out, 
   const int ex = mx > 0.0 ? ilogb(mx) : 0;
   e.x = scalbn(e.x, -ex);
   e.y = scalbn(e.y, -ex);
+#ifdef QFS_DIAG_POLAR
+  const long long t_ns = clock64();
+#endif
+  {
+    double ss_ns;
+    if (polar_ns(e, hb, r, j, g_out, ss_ns)) {
+      v_out = v0;  // warm start of the Jacobi path left as it was
+      sig_sum = scalbn(ss_ns, ex);
+#ifdef QFS_DIAG_POLAR
+      sig_sum = 100.0 * 1e7 + (double)(clock64() - t_ns);
+#endif
+      return;
+    }
+  }
   // A_0 = E' V_0
   double2 a = make_double2(0.0, 0.0);
 #pragma unroll
   for (int q = 0; q < 4; ++q) cfma(a, shfl_c(e, hb | (4 * r + q)), shfl_c(v0, hb | (4 * q + j)));
   double2 v = v0;
+#ifdef QFS_DIAG_POLAR
+  const long long t_start = clock64();
+  int n_sweeps = 0;
+#endif
   for (int sweep = 0; sweep < JACOBI_MAX_SWEEPS; ++sweep) {
-    bool rotated = false;
+    bool big = false;  // some pair had |gamma|^2 > 1e-24 ||a_j||^2 ||a_k||^2 this sweep
+#ifdef QFS_DIAG_POLAR
+    ++n_sweeps;
+#endif
 #pragma unroll
     for (int x = 1; x <= 3; ++x) {
       const double2 ap = shfl_xor_c(a, x);
@@ -189,12 +270,13 @@ __device__ void hw_polar(double2 e, double2 v0, double2 &g_out, double2 &v_out, 
         gi += __shfl_xor_sync(FULL, gi, o);
       }
       const double ag2 = gr * gr + gi * gi;
-      if (ag2 > 0.0 && ag2 > 1e-30 * al * be) {
+      const double ab = al * be;
+      big = big || ag2 > 1e-24 * ab;
+      if (ag2 > 0.0 && ag2 > 1e-30 * ab) {
         // The same rotation as t = sgn(zeta)/(|zeta| + sqrt(1 + zeta^2)), c = 1/sqrt(1 + t^2),
         // zeta = D/(2|gamma|), D = beta - alpha, rewritten with two rsqrt and no division:
         //   R = sqrt(D^2 + 4|gamma|^2), den = |D| + R, r = 1/sqrt(den^2 + 4|gamma|^2),
         //   c = den r, s e^{i phi} = 2 sgn(D) r gamma.
-        rotated = true;
         const double D = be - al;
         const double q4 = 4.0 * ag2;
         const double w = fma(D, D, q4);
@@ -213,7 +295,7 @@ __device__ void hw_polar(double2 e, double2 v0, double2 &g_out, double2 &v_out, 
         }
       }
     }
-    if (!__any_sync(FULL, rotated)) break;
+    if (!__any_sync(FULL, big)) break;
   }
   // sigma_j = ||a_j|| (reduce over rows), sigma_max over columns
   double nn = a.x * a.x + a.y * a.y;
@@ -272,6 +354,9 @@ __device__ void hw_polar(double2 e, double2 v0, double2 &g_out, double2 &v_out, 
   g_out = g;
   v_out = v;
   sig_sum = scalbn(ss, ex);
+#ifdef QFS_DIAG_POLAR  // diagnostic build: report sweeps * 1e7 + cycles instead of sum sigma
+  sig_sum = (double)n_sweeps * 1e7 + (double)(clock64() - t_start);
+#endif
 }
 
 // Polar step of one start by one warp (lanes 16-31 mirror lanes 0-15):
