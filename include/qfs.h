@@ -151,6 +151,16 @@ qfs_status qfs_profile_enable(qfs_ctx *c, int on);
 qfs_status qfs_profile_read(qfs_ctx *c, int cap, const char **names, long long *launches,
                             double *ms, double *bytes, double *flops, int *count);
 
+/* Sweep implementation: 0 = auto (default; cluster-resident
+ * whenever a start's states fit in the shared memory of a cluster of <= 16
+ * CTAs, else streamed), 1 = streamed (B cache in HBM, one fused launch per
+ * gate), 2 = cluster-resident only (a sweep whose states do not fit fails with
+ * QFS_ERR_CAPACITY).  Both compute the same sweep; the
+ * resident one recovers B_i = G_i^dag B_{i+1} instead of storing the B cache
+ * (P:165), which changes results only at rounding level.  QFS_ERR_ARG for
+ * another value.  Takes effect at the next sweep. */
+qfs_status qfs_set_path(qfs_ctx *c, int path);
+
 /* Number of kernel launches issued since the context was created. */
 long long qfs_launch_count(const qfs_ctx *c);
 /* The library's CUDA stream (cudaStream_t) — for callers that order work. */

@@ -134,6 +134,25 @@ struct DistParams {
   double *row_out;
 };
 
+// Cluster-resident sweep (qfs_resident.cu): one cluster of C CTAs per start,
+// states of the CTA's sample slice in shared memory, whole sweep + costs.
+struct ResParams {
+  int n, K, S, C, ld;         // qubits, gates, total starts (trace layout), cluster size, rows per CTA
+  int n_slots;
+  const Slot *slots;
+  const int2 *pairs;          // [K]
+  double2 *gates;             // [S][K][16]: old gates in, new gates out
+  const double2 *x, *y;       // pools, sample-minor [2^n][m_pool]
+  long long m_pool;
+  const double2 *xv, *yv;     // validation rows, row-major [V][2^n]
+  int V, want_val;
+  double beta;
+  double *csum, *cval;        // [n_slots] raw sums ||chi - x||^2, ||C xv - yv||^2
+  double *sig;                // [S][K] sum sigma, or nullptr
+  double2 *env_trace;         // [K][S][16], or nullptr
+  unsigned long long *dbg;    // diagnostics (QFS_TAIL_TIMING): [8] summed globaltimer phases, or nullptr
+};
+
 // kernel-level unit ops
 struct ApplyParams {
   int n, p0, p1, m;
@@ -162,7 +181,11 @@ cudaError_t launch_finite_check(const double *p, long long n, int *flag, cudaStr
 cudaError_t launch_identity_fill(double2 *v, long long count16, cudaStream_t st);
 void set_pdl(bool on);     // launch with programmatic dependent launch (default on)
 bool pdl_enabled();
-int val_row_max_n();        // largest n the shared-memory validation forward supports
+int val_row_max_n();
+size_t res_smem_bytes(int n, int K, int ld);  // dynamic shared memory of the resident kernel
+size_t res_smem_limit(int minb);  // per-CTA limit when minb CTAs share an SM
+int resident_max_clusters(int C, size_t smem); // co-resident clusters of C CTAs (0: cannot launch)
+cudaError_t launch_resident(const ResParams &p, int clusters, cudaStream_t st);        // largest n the shared-memory validation forward supports
 int blocks_per_sm(int nu);  // resident CTAs per SM of the backward kernel
 
 }  // namespace qfs

@@ -22,13 +22,13 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "qfs_device.cuh"
 #include "qfs_internal.h"
 
 namespace qfs {
 
 namespace {
 
-constexpr unsigned FULL = 0xffffffffu;
 #ifndef QFS_BWD_THREADS
 #define QFS_BWD_THREADS 256
 #endif
@@ -44,320 +44,7 @@ constexpr int FWD_THREADS = 256;
 constexpr int FWD_STAGES = 4;   // LDGSTS pipeline depth of the forward kernel
 constexpr int VAL_THREADS = 512;
 constexpr int RED_THREADS = 256;
-constexpr int JACOBI_MAX_SWEEPS = 20;
 
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
-}
-// acc += a * b
-__device__ __forceinline__ void cfma(double2 &acc, double2 a, double2 b) {
-  acc.x = fma(a.x, b.x, acc.x);
-  acc.x = fma(-a.y, b.y, acc.x);
-  acc.y = fma(a.x, b.y, acc.y);
-  acc.y = fma(a.y, b.x, acc.y);
-}
-__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
-
-__device__ __forceinline__ long long insert_zero(long long v, int pos) {
-  long long low = v & ((1LL << pos) - 1);
-  return ((v >> pos) << (pos + 1)) | low;
-}
-__device__ __forceinline__ unsigned insert_zero32(unsigned v, int pos) {
-  return ((v >> pos) << (pos + 1)) | (v & ((1u << pos) - 1u));
-}
-
-// Division by an invariant d (1 <= d < 2^31) for numerators < 2^31:
-// q = (umulhi(n, mul) + n) >> l with l = ceil(log2 d), mul = 2^32 (2^l - d) / d + 1.
-struct FastDiv {
-  unsigned d, mul;
-  int l;
-  __device__ explicit FastDiv(unsigned dd) : d(dd) {
-    l = 0;
-    while ((1u << l) < d) ++l;
-    mul = (unsigned)((((unsigned long long)1 << 32) * ((1ull << l) - d)) / d + 1);
-  }
-  __device__ __forceinline__ unsigned div(unsigned n) const { return (__umulhi(n, mul) + n) >> l; }
-};
-
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-
-// LDGSTS: 16-byte global -> shared copy without a register round trip
-// (zero-filled when !valid); .cg = cached in L2 only.
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool valid) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  const int sz = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz) : "memory");
-}
-// L2 eviction-priority policies (createpolicy) and hinted LDGSTS / stores
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ void cp_async16_hint(void *smem, const void *gmem, bool valid, uint64_t pol) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  const int sz = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;\n" ::"r"(sa), "l"(gmem), "r"(sz),
-               "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ void st_hint(double2 *p, double2 v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
-
-// Programmatic dependent launch (PDL): a kernel launched with the
-// programmatic-stream-serialization attribute may start while the previous
-// kernel on the stream drains; everything before pdl_wait() must not depend on
-// that kernel's results.  pdl_trigger() lets the next kernel start launching.
-// Both are no-ops for a kernel launched without the attribute.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-
-__device__ __forceinline__ double2 shfl_c(double2 v, int src) {
-  return make_double2(__shfl_sync(FULL, v.x, src), __shfl_sync(FULL, v.y, src));
-}
-__device__ __forceinline__ double2 shfl_xor_c(double2 v, int m) {
-  return make_double2(__shfl_xor_sync(FULL, v.x, m), __shfl_xor_sync(FULL, v.y, m));
-}
-
-// ------------------------------------------------------------ polar update --
-// Half-warp one-sided (Hestenes) Jacobi SVD and polar factor of a 4x4 complex
-// matrix; lane l = 4r + j of each 16-lane half holds A[r][j] and V[r][j] in
-// registers (both halves of a warp may work on different matrices).
-//
-//   A_0 = E' V_0 (V_0 = warm-start right singular vectors, any unitary),
-//   rounds rotate the disjoint column pairs (j, j ^ x), x = 1, 2, 3:
-//     gamma = a_j^dag a_k = |gamma| e^{i phi},  zeta = (||a_k||^2 - ||a_j||^2) / (2|gamma|),
-//     t = sgn(zeta) / (|zeta| + sqrt(1 + zeta^2)),  c = 1/sqrt(1 + t^2),  s = c t,
-//     [a_j a_k] <- [a_j a_k] [[c, s e^{i phi}], [-s e^{-i phi}, c]]   (same on V)
-//   rotating every pair with |gamma| > 1e-15 ||a_j|| ||a_k||, and stopping after
-//   the first sweep in which no pair had |gamma| > 1e-12 ||a_j|| ||a_k|| (the
-//   rotations of that sweep are applied; convergence is quadratic, so the
-//   residual is far below 1e-12, and no sweep is spent only to verify it, nor
-//   chasing rounding noise near 1e-15); then sigma_j = ||a_j||,
-//   X_j = a_j / sigma_j (null columns, sigma_j <= 1e-14 sigma_max, completed by
-//   Gram-Schmidt on e_0..e_3; R5) and G = V X^dag (eq:opt_u:
-//   E = X D Y^dag, u = Y X^dag with Y = V).  Square roots and divisions are
-//   rsqrt-based (MUFU.RSQ64H + Newton) to keep the serial chain short.
-// E' is scaled by an exact power of two first (the polar factor is scale-free).
-// scratch: 16 double2 of shared memory per half (null-column path only).
-//
-// Fast path first (polar_ns): when E' is far enough from singular, its
-// unitary polar factor W = X Y^dag is reached by Newton-Schulz iterations
-// instead (same result up to rounding; G = W^dag = Y X^dag).
-__device__ __forceinline__ double half_sum(double v) {
-#pragma unroll
-  for (int o = 1; o < 16; o <<= 1) v += __shfl_xor_sync(FULL, v, o);
-  return v;
-}
-
-// Newton-Schulz polar iteration on a half-warp (lane l = 4r + c holds X[r][c]):
-//   X_0 = E' / s, s = ||E'||_F / 2 (RMS singular value),
-//   X_{k+1} = X_k (3I - X_k^dag X_k) / 2   ->  W, the unitary polar factor of E'.
-// Per singular value u = sigma^2 of X_k, f = u - 1 maps to f' = u(3-u)^2/4 - 1
-// with |f'| <= f^2 for 0 < u < 2, so e_k = ||X_k^dag X_k - I||_F <= e_0^(2^k):
-// when e_0 <= 10^(-16/2^k) (k <= 10), k iterations reach e <= 1e-16 (unitary to
-// rounding).  Returns false (nothing written) when e_0 > 0.9647 for either
-// half of the warp: the Jacobi path below handles that (ill-conditioned or
-// singular E').  The decision and the count are warp-uniform.
-__device__ bool polar_ns(double2 e, int hb, int r, int c, double2 &g_out, double &ss_out) {
-  const double fro2 = half_sum(e.x * e.x + e.y * e.y);
-  if (!__all_sync(FULL, fro2 > 0.0)) return false;
-  const double rs = 2.0 * rsqrt(fro2);
-  double2 x = make_double2(e.x * rs, e.y * rs);
-  auto xhx = [&](double2 X) {  // (X^dag X)[r][c] = sum_q conj(X[q][r]) X[q][c]
-    double2 y = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) cfma(y, cconj(shfl_c(X, hb | (4 * q + r))), shfl_c(X, hb | (4 * q + c)));
-    return y;
-  };
-  double2 y = xhx(x);
-  const double dre = y.x - (r == c ? 1.0 : 0.0);
-  const double e02 = half_sum(dre * dre + y.y * y.y);  // e_0^2
-  // iterations needed: smallest k with e_0 <= 10^(-16/2^k)
-  constexpr double th2[10] = {1e-16, 1e-8, 1e-4, 1e-2, 0.1, 0.31622776601683794, 0.5623413251903491,
-                              0.7498942093324559, 0.8659643233600653, 0.9305720409296991};
-  int k = 11;
-#pragma unroll
-  for (int q = 9; q >= 0; --q)
-    if (e02 <= th2[q]) k = q + 1;
-  k = max(k, __shfl_xor_sync(FULL, k, 16));
-  if (!__all_sync(FULL, k <= 10)) return false;
-  for (int it = 0; it < k; ++it) {
-    if (it > 0) y = xhx(x);
-    const double2 t = make_double2(0.5 * ((r == c ? 3.0 : 0.0) - y.x), -0.5 * y.y);  // (3I - Y)/2
-    double2 z = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) cfma(z, shfl_c(x, hb | (4 * r + q)), shfl_c(t, hb | (4 * q + c)));
-    x = z;
-  }
-  // G = W^dag: G[r][c] = conj(W[c][r]);  sum sigma = Re Tr(W^dag E') = Re sum conj(W) o E'
-  g_out = cconj(shfl_c(x, hb | (4 * c + r)));
-  ss_out = half_sum(x.x * e.x + x.y * e.y);
-  return true;
-}
-
-__device__ void hw_polar(double2 e, double2 v0, double2 &g_out, double2 &v_out, double &sig_sum,
-                         double2 *scratch) {
-  const int lane = threadIdx.x & 31;
-  const int hb = lane & 16;         // half-warp base lane
-  const int l = lane & 15;
-  const int r = l >> 2, j = l & 3;
-  // exact power-of-two scaling of E'
-  double mx = fmax(fabs(e.x), fabs(e.y));
-#pragma unroll
-  for (int o = 1; o < 16; o <<= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
-  const int ex = mx > 0.0 ? ilogb(mx) : 0;
-  e.x = scalbn(e.x, -ex);
-  e.y = scalbn(e.y, -ex);
-#ifdef QFS_DIAG_POLAR
-  const long long t_ns = clock64();
-#endif
-  {
-    double ss_ns;
-    if (polar_ns(e, hb, r, j, g_out, ss_ns)) {
-      v_out = v0;  // warm start of the Jacobi path left as it was
-      sig_sum = scalbn(ss_ns, ex);
-#ifdef QFS_DIAG_POLAR
-      sig_sum = 100.0 * 1e7 + (double)(clock64() - t_ns);
-#endif
-      return;
-    }
-  }
-  // A_0 = E' V_0
-  double2 a = make_double2(0.0, 0.0);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) cfma(a, shfl_c(e, hb | (4 * r + q)), shfl_c(v0, hb | (4 * q + j)));
-  double2 v = v0;
-#ifdef QFS_DIAG_POLAR
-  const long long t_start = clock64();
-  int n_sweeps = 0;
-#endif
-  for (int sweep = 0; sweep < JACOBI_MAX_SWEEPS; ++sweep) {
-    bool big = false;  // some pair had |gamma|^2 > 1e-24 ||a_j||^2 ||a_k||^2 this sweep
-#ifdef QFS_DIAG_POLAR
-    ++n_sweeps;
-#endif
-#pragma unroll
-    for (int x = 1; x <= 3; ++x) {
-      const double2 ap = shfl_xor_c(a, x);
-      const double2 vp = shfl_xor_c(v, x);
-      const bool lo = (j & (x == 1 ? 1 : 2)) == 0;
-      const double2 aj = lo ? a : ap, ak = lo ? ap : a;
-      const double2 vj = lo ? v : vp, vk = lo ? vp : v;
-      double al = aj.x * aj.x + aj.y * aj.y;
-      double be = ak.x * ak.x + ak.y * ak.y;
-      double gr = aj.x * ak.x + aj.y * ak.y;
-      double gi = aj.x * ak.y - aj.y * ak.x;
-#pragma unroll
-      for (int o = 4; o <= 8; o <<= 1) {
-        al += __shfl_xor_sync(FULL, al, o);
-        be += __shfl_xor_sync(FULL, be, o);
-        gr += __shfl_xor_sync(FULL, gr, o);
-        gi += __shfl_xor_sync(FULL, gi, o);
-      }
-      const double ag2 = gr * gr + gi * gi;
-      const double ab = al * be;
-      big = big || ag2 > 1e-24 * ab;
-      if (ag2 > 0.0 && ag2 > 1e-30 * ab) {
-        // The same rotation as t = sgn(zeta)/(|zeta| + sqrt(1 + zeta^2)), c = 1/sqrt(1 + t^2),
-        // zeta = D/(2|gamma|), D = beta - alpha, rewritten with two rsqrt and no division:
-        //   R = sqrt(D^2 + 4|gamma|^2), den = |D| + R, r = 1/sqrt(den^2 + 4|gamma|^2),
-        //   c = den r, s e^{i phi} = 2 sgn(D) r gamma.
-        const double D = be - al;
-        const double q4 = 4.0 * ag2;
-        const double w = fma(D, D, q4);
-        const double R = w * rsqrt(w);
-        const double den = fabs(D) + R;
-        const double r = rsqrt(fma(den, den, q4));
-        const double c = den * r;
-        const double f2 = (D >= 0.0 ? 2.0 : -2.0) * r;
-        const double spr = f2 * gr, spi = f2 * gi;  // s e^{i phi}
-        if (lo) {  // a_j' = c a_j - conj(s e^{i phi}) a_k
-          a = make_double2(c * aj.x - (spr * ak.x + spi * ak.y), c * aj.y - (spr * ak.y - spi * ak.x));
-          v = make_double2(c * vj.x - (spr * vk.x + spi * vk.y), c * vj.y - (spr * vk.y - spi * vk.x));
-        } else {   // a_k' = s e^{i phi} a_j + c a_k
-          a = make_double2((spr * aj.x - spi * aj.y) + c * ak.x, (spr * aj.y + spi * aj.x) + c * ak.y);
-          v = make_double2((spr * vj.x - spi * vj.y) + c * vk.x, (spr * vj.y + spi * vj.x) + c * vk.y);
-        }
-      }
-    }
-    if (!__any_sync(FULL, big)) break;
-  }
-  // sigma_j = ||a_j|| (reduce over rows), sigma_max over columns
-  double nn = a.x * a.x + a.y * a.y;
-  nn += __shfl_xor_sync(FULL, nn, 4);
-  nn += __shfl_xor_sync(FULL, nn, 8);
-  const double rs = nn > 0.0 ? rsqrt(nn) : 0.0;
-  const double sig = nn * rs;
-  double smax = sig;
-  smax = fmax(smax, __shfl_xor_sync(FULL, smax, 1));
-  smax = fmax(smax, __shfl_xor_sync(FULL, smax, 2));
-  const bool nul = !(sig > 1e-14 * smax) || smax == 0.0;
-  double2 xx = nul ? make_double2(0.0, 0.0) : make_double2(a.x * rs, a.y * rs);
-  if (__any_sync(FULL, nul)) {  // rare: complete the null columns of X
-    scratch[l] = xx;
-    __syncwarp();
-    const unsigned nm = __ballot_sync(FULL, nul && r == 0);  // bit (hb + j): column j null
-    const unsigned cols = (nm >> hb) & 0xFu;
-    if (l == 0 && cols) {
-      for (int jj = 0; jj < 4; ++jj) {
-        if (!((cols >> jj) & 1)) continue;
-        for (int e0 = 0; e0 < 4; ++e0) {
-          double2 u[4];
-          for (int q = 0; q < 4; ++q) u[q] = make_double2(q == e0 ? 1.0 : 0.0, 0.0);
-          for (int pass = 0; pass < 2; ++pass)
-            for (int q = 0; q < 4; ++q) {
-              if (q == jj || (((cols >> q) & 1) && q > jj)) continue;
-              double2 d = make_double2(0.0, 0.0);
-              for (int rr = 0; rr < 4; ++rr) cfma(d, cconj(scratch[4 * rr + q]), u[rr]);
-              for (int rr = 0; rr < 4; ++rr) {
-                const double2 tq = cmul(d, scratch[4 * rr + q]);
-                u[rr].x -= tq.x;
-                u[rr].y -= tq.y;
-              }
-            }
-          double nv = 0.0;
-          for (int rr = 0; rr < 4; ++rr) nv += u[rr].x * u[rr].x + u[rr].y * u[rr].y;
-          nv = sqrt(nv);
-          if (nv > 0.5) {
-            for (int rr = 0; rr < 4; ++rr) scratch[4 * rr + jj] = make_double2(u[rr].x / nv, u[rr].y / nv);
-            break;
-          }
-        }
-      }
-    }
-    __syncwarp();
-    xx = scratch[l];
-    __syncwarp();
-  }
-  // G[r][j] = sum_q V[r][q] conj(X[j][q])
-  double2 g = make_double2(0.0, 0.0);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) cfma(g, shfl_c(v, hb | (4 * r + q)), cconj(shfl_c(xx, hb | (4 * j + q))));
-  double ss = sig;                       // each column's lanes hold sigma_j
-  ss += __shfl_xor_sync(FULL, ss, 1);
-  ss += __shfl_xor_sync(FULL, ss, 2);
-  g_out = g;
-  v_out = v;
-  sig_sum = scalbn(ss, ex);
-#ifdef QFS_DIAG_POLAR  // diagnostic build: report sweeps * 1e7 + cycles instead of sum sigma
-  sig_sum = (double)n_sweeps * 1e7 + (double)(clock64() - t_start);
-#endif
-}
 
 // Polar step of one start by one warp (lanes 16-31 mirror lanes 0-15):
 // E' = (1 - beta) E + beta G_old^dag; writes G_i, V_i, sum sigma, E trace.

@@ -1,0 +1,453 @@
+// qfs_resident.cu — cluster-resident QFactor-Sample sweep for sm_100a.
+//
+// One thread-block cluster of C CTAs owns one multistart at a time and runs
+// its whole sweep (SURVEY.md §8 rows
+// a2-a7) out of shared memory: the forward and backward states of the CTA's
+// slice of the training samples never leave the SM.  This is the "uncompute"
+// variant of the B cache: instead of storing B_1..B_{K-1}
+// (P:165's time-memory trade-off) the forward pass keeps only
+// phi = B_{K-1} = G_{K-2}...G_0 x, and the backward pass recovers
+// B_i = G_i^dag B_{i+1} with the gate's old value (gates are unitary).
+//
+// Per gate i = K-1 .. 0 (right to left):
+//   1. all warps:  E_i partial = sum phi (x) conj(chi) over the CTA's samples
+//                  (P:121-125), warp butterfly + warps in order
+//   2. warp 0:     cluster barrier, sums the C CTA partials in rank order over
+//                  DSMEM (identical bits in every CTA), polar update
+//                  G_i <- Y X^dag (eq:opt_u) into the CTA's gate table;
+//      warps 1-7:  meanwhile phi <- G_{i-1}^dag phi (uncompute B_{i-1})
+//   3. all warps:  chi <- G_i^dag chi (the new value), fused at i = 0 with
+//                  c_train = sum ||chi - x||^2 (direct form)
+// then the validation rows run forward through the new gates.
+// Every reduction has a fixed order, so the result is deterministic for a
+// given cluster size.  No code here is shared with the CPU oracle.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "qfs_device.cuh"
+#include "qfs_internal.h"
+
+namespace qfs {
+namespace {
+
+constexpr int RES_THREADS = 256;
+constexpr int RES_WARPS = RES_THREADS / 32;
+constexpr size_t RES_SMEM_MAX = 232448;  // 227 KB opt-in dynamic shared memory per CTA
+constexpr size_t RES_SMEM_MAX2 = 113 * 1024;  // two CTAs per SM (228 KB per SM, 1 KB reserved per CTA)
+
+__device__ __forceinline__ unsigned cl_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cl_size() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cl_id() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cl_count() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+// split cluster barrier: arrive (release this thread's prior shared-memory
+// writes to the cluster) ... wait (acquire the other CTAs' writes)
+__device__ __forceinline__ void cl_arrive() { asm volatile("barrier.cluster.arrive.release;" ::: "memory"); }
+__device__ __forceinline__ void cl_wait() { asm volatile("barrier.cluster.wait.acquire;" ::: "memory"); }
+// load a double from the same shared-memory offset in CTA `rank` of the cluster
+// (volatile without a memory clobber: kept after the cluster barrier's wait,
+// which clobbers memory, but independent loads can be in flight together)
+__device__ __forceinline__ double ld_remote(const double *p, unsigned rank) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+  unsigned ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra));
+  return v;
+}
+
+// psi <- G psi (dag: G^dag psi) on the qubit pair pq for the rows jj < cnt of
+// a [2^n][ld] shared-memory state block (sample-minor: quadruple members of
+// consecutive items are consecutive samples).  Threads t0, t0 + nt, ...
+__device__ void res_apply(double2 *psi, const double2 *G, int2 pq, bool dag, int cnt, unsigned ld, int n,
+                          int t0, int nt) {
+  if (cnt <= 0) return;
+  double2 g[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) g[e] = dag ? cconj(G[4 * (e & 3) + (e >> 2)]) : G[e];  // (G^dag)[a][b] = conj(G[b][a])
+  const int lo = min(pq.x, pq.y), hi = max(pq.x, pq.y);
+  const unsigned o1 = (1u << pq.x) * ld, o2 = (1u << pq.y) * ld;
+  const unsigned items = (1u << (n - 2)) * (unsigned)cnt;
+  const FastDiv fd((unsigned)cnt);
+  for (unsigned q = (unsigned)t0; q < items; q += (unsigned)nt) {
+    const unsigned r = fd.div(q);
+    const unsigned b = insert_zero32(insert_zero32(r, lo), hi) * ld + (q - r * (unsigned)cnt);
+    double2 v[4] = {psi[b], psi[b + o1], psi[b + o2], psi[b + o1 + o2]};
+    double2 o[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      o[a] = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) cfma(o[a], g[4 * a + k], v[k]);
+    }
+    psi[b] = o[0];
+    psi[b + o1] = o[1];
+    psi[b + o2] = o[2];
+    psi[b + o1 + o2] = o[3];
+  }
+}
+
+// Warp butterfly reduce-scatter of 32 per-lane values: lane L ends with the
+// sum over the warp of value L (fixed order; 31 shuffles per lane).
+__device__ __forceinline__ double warp_reduce_scatter32(double (&acc)[32], int lane) {
+#pragma unroll
+  for (int h = 16; h >= 1; h >>= 1) {
+    const bool up = (lane & h) != 0;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const double send = up ? acc[i] : acc[i + h];
+      const double keep = up ? acc[i + h] : acc[i];
+      acc[i] = keep + __shfl_xor_sync(FULL, send, h);
+    }
+  }
+  return acc[0];
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+// E[l_in][l_out] += sum phi[idx(l_in)] conj(chi[idx(l_out)]) over this CTA's
+// items; every warp writes its reduced 32 doubles (re/im of the 16
+// entries, row-major) to red[warp][.]
+__device__ void res_env(const double2 *phi, const double2 *chi, int2 pq, int cnt, unsigned ld, int n,
+                        double *red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double acc[32];
+#pragma unroll
+  for (int e = 0; e < 32; ++e) acc[e] = 0.0;
+  if (cnt > 0) {
+    const int lo = min(pq.x, pq.y), hi = max(pq.x, pq.y);
+    const unsigned o1 = (1u << pq.x) * ld, o2 = (1u << pq.y) * ld;
+    const unsigned items = (1u << (n - 2)) * (unsigned)cnt;
+    const FastDiv fd((unsigned)cnt);
+    for (unsigned q = threadIdx.x; q < items; q += RES_THREADS) {
+      const unsigned r = fd.div(q);
+      const unsigned b = insert_zero32(insert_zero32(r, lo), hi) * ld + (q - r * (unsigned)cnt);
+      const double2 f[4] = {phi[b], phi[b + o1], phi[b + o2], phi[b + o1 + o2]};
+      const double2 c[4] = {chi[b], chi[b + o1], chi[b + o2], chi[b + o1 + o2]};
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {  // f[a] * conj(c[k])
+          double &re = acc[2 * (4 * a + k)], &im = acc[2 * (4 * a + k) + 1];
+          re = fma(f[a].x, c[k].x, re);
+          re = fma(f[a].y, c[k].y, re);
+          im = fma(f[a].y, c[k].x, im);
+          im = fma(-f[a].x, c[k].y, im);
+        }
+    }
+  }
+  red[warp * 32 + lane] = warp_reduce_scatter32(acc, lane);
+}
+
+struct ResSmem {
+  double2 *G;     // [K][16] gate table of the current start (old -> new in place)
+  double *red;    // [RES_WARPS][32]
+  double *buf;    // [2][32] CTA partial of E (read by the cluster over DSMEM)
+  double *cbuf;   // [2] CTA partial costs (train, validation)
+  double2 *scr;   // [32] polar scratch
+  int2 *pr;       // [K] qubit pairs
+  double2 *phi;   // [2^n][ld]
+  double2 *chi;   // [2^n][ld]
+};
+
+__device__ ResSmem res_carve(unsigned char *base, int K, int n, int ld) {
+  ResSmem m;
+  m.G = (double2 *)base;
+  m.red = (double *)(m.G + K * 16);
+  m.buf = m.red + RES_WARPS * 32;
+  m.cbuf = m.buf + 64;
+  m.scr = (double2 *)(m.cbuf + 2);
+  m.pr = (int2 *)(m.scr + 32);
+  uintptr_t p = (uintptr_t)(m.pr + K);
+  p = (p + 15) & ~(uintptr_t)15;
+  m.phi = (double2 *)p;
+  m.chi = m.phi + ((size_t)ld << n);
+  return m;
+}
+
+// MINB = resident CTAs per SM the kernel is compiled for (2: <= 128 registers,
+// <= 113 KB shared memory each, so one CTA's polar tail overlaps another
+// start's contraction on the same SM).
+template <int MINB>
+__global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int K = P.K, n = P.n;
+  const unsigned N = 1u << n, ld = (unsigned)P.ld;
+  const ResSmem sm = res_carve(smem_raw, K, n, P.ld);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned rank = cl_rank(), C = cl_size();
+
+  pdl_wait();
+  for (int k = tid; k < K; k += RES_THREADS) sm.pr[k] = P.pairs[k];
+  // diagnostics: phase times of cluster 0, rank 0 (thread 0), summed over gates
+  const bool dbg = P.dbg && cl_id() == 0 && rank == 0 && tid == 0;
+  unsigned long long t_prev = 0, ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  auto stamp = [&](int k) {
+    if (dbg) {
+      const unsigned long long t = gtimer();
+      if (k >= 0) ph[k] += t - t_prev;
+      t_prev = t;
+    }
+  };
+
+  for (int j = (int)cl_id(); j < P.n_slots; j += (int)cl_count()) {
+    const Slot sl = P.slots[j];
+    const int s = sl.s, M = sl.m;
+    const int ms = (M + (int)C - 1) / (int)C;
+    const int m0 = (int)rank * ms;
+    const int cnt = max(0, min(ms, M - m0));
+    double2 *gglob = P.gates + (long long)s * K * 16;
+    for (int q = tid; q < K * 16; q += RES_THREADS) sm.G[q] = gglob[q];
+    for (unsigned q = tid; q < N * (unsigned)cnt; q += RES_THREADS) {
+      const unsigned a = q / (unsigned)cnt, jj = q - a * (unsigned)cnt;
+      const long long gi = (long long)a * P.m_pool + m0 + jj;
+      sm.phi[a * ld + jj] = __ldg(P.x + gi);
+      sm.chi[a * ld + jj] = __ldg(P.y + gi);
+    }
+    __syncthreads();
+    stamp(0);  // [0] load
+    // forward with the previous sweep's gates: phi = B_{K-1} = G_{K-2} ... G_0 x
+    for (int k = 0; k + 1 < K; ++k) {
+      res_apply(sm.phi, sm.G + 16 * k, sm.pr[k], false, cnt, ld, n, tid, RES_THREADS);
+      __syncthreads();
+    }
+    stamp(1);  // [1] forward
+    double train = 0.0;
+    for (int i = K - 1; i >= 0; --i) {
+      const int par = i & 1;
+      res_env(sm.phi, sm.chi, sm.pr[i], cnt, ld, n, sm.red);
+      __syncthreads();
+      stamp(2);  // [2] environment pass
+      if (warp == 0) {
+        double e = 0.0;
+#pragma unroll
+        for (int w = 0; w < RES_WARPS; ++w) e += sm.red[w * 32 + lane];
+        sm.buf[par * 32 + lane] = e;
+      }
+      cl_arrive();
+      if (warp == 0) {
+        cl_wait();
+        double rv[16];  // all remote loads in flight first, then summed in rank order
+#pragma unroll
+        for (unsigned c = 0; c < 16; ++c) rv[c] = c < C ? ld_remote(sm.buf + par * 32 + lane, c) : 0.0;
+        double e = 0.0;
+#pragma unroll
+        for (unsigned c = 0; c < 16; ++c)
+          if (c < C) e += rv[c];
+        stamp(3);  // [3] CTA + cluster reduction
+        const int l = lane & 15;
+        double2 ev = make_double2(__shfl_sync(FULL, e, 2 * l), __shfl_sync(FULL, e, 2 * l + 1));
+        double2 *gi = sm.G + 16 * i;
+        if (P.env_trace && rank == 0 && lane < 16) P.env_trace[((long long)i * P.S + s) * 16 + l] = ev;
+        if (P.beta != 0.0) {  // E' = (1 - beta) E + beta G_old^dag
+          const double2 go = gi[4 * (l & 3) + (l >> 2)];
+          ev = make_double2((1.0 - P.beta) * ev.x + P.beta * go.x, (1.0 - P.beta) * ev.y - P.beta * go.y);
+        }
+        double2 g, v;
+        double ss;
+        hw_polar(ev, make_double2((l % 5 == 0) ? 1.0 : 0.0, 0.0), g, v, ss, sm.scr + (lane & 16));
+        __syncwarp();
+        if (lane < 16) gi[l] = g;
+        if (rank == 0) {
+          if (lane < 16) gglob[16 * i + l] = g;
+          if (lane == 0 && P.sig) P.sig[(long long)s * K + i] = ss;
+        }
+        stamp(4);  // [4] polar
+      } else {
+        // uncompute B_{i-1} = G_{i-1}^dag B_i with the old G_{i-1}, overlapping the polar
+        if (i > 0) res_apply(sm.phi, sm.G + 16 * (i - 1), sm.pr[i - 1], true, cnt, ld, n, tid - 32, RES_THREADS - 32);
+        cl_wait();
+      }
+      __syncthreads();
+      stamp(5);  // [5] wait for the uncompute warps
+      if (i > 0) {
+        res_apply(sm.chi, sm.G + 16 * i, sm.pr[i], true, cnt, ld, n, tid, RES_THREADS);
+      } else if (cnt > 0) {
+        // chi' = G_0^dag chi and c_train = sum ||chi' - x||^2
+        const double2 *G = sm.G;
+        double2 g[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) g[e] = cconj(G[4 * (e & 3) + (e >> 2)]);
+        const int2 pq = sm.pr[0];
+        const int lo = min(pq.x, pq.y), hi = max(pq.x, pq.y);
+        const unsigned o[4] = {0u, (1u << pq.x), (1u << pq.y), (1u << pq.x) | (1u << pq.y)};
+        const unsigned items = (N >> 2) * (unsigned)cnt;
+        const FastDiv fd((unsigned)cnt);
+        for (unsigned q = tid; q < items; q += RES_THREADS) {
+          const unsigned r = fd.div(q), jj = q - r * (unsigned)cnt;
+          const unsigned base = insert_zero32(insert_zero32(r, lo), hi);
+          double2 v[4];
+#pragma unroll
+          for (int l = 0; l < 4; ++l) v[l] = sm.chi[(base | o[l]) * ld + jj];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            double2 rr = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) cfma(rr, g[4 * a + k], v[k]);
+            const double2 xv = __ldg(P.x + (long long)(base | o[a]) * P.m_pool + m0 + jj);
+            const double dr = rr.x - xv.x, di = rr.y - xv.y;
+            train = fma(dr, dr, train);
+            train = fma(di, di, train);
+          }
+        }
+      }
+      __syncthreads();
+      stamp(6);  // [6] chi update
+    }
+    // validation cost with the post-sweep gates: this CTA's rows
+    // v = rank, rank + C, ..., in batches of ld rows through the phi buffer
+    double val = 0.0;
+    if (P.want_val && P.V > 0) {
+      const int rows = (P.V - (int)rank + (int)C - 1) / (int)C;
+      for (int b0 = 0; b0 < rows; b0 += (int)ld) {
+        const int nb = min((int)ld, rows - b0);
+        for (unsigned q = tid; q < N * (unsigned)nb; q += RES_THREADS) {
+          const unsigned jj = q / N, a = q - jj * N;
+          const long long row = (long long)rank + (long long)C * (b0 + jj);
+          sm.phi[a * ld + jj] = __ldg(P.xv + row * N + a);
+        }
+        __syncthreads();
+        for (int k = 0; k < K; ++k) {
+          res_apply(sm.phi, sm.G + 16 * k, sm.pr[k], false, nb, ld, n, tid, RES_THREADS);
+          __syncthreads();
+        }
+        for (unsigned q = tid; q < N * (unsigned)nb; q += RES_THREADS) {
+          const unsigned jj = q / N, a = q - jj * N;
+          const long long row = (long long)rank + (long long)C * (b0 + jj);
+          const double2 u = sm.phi[a * ld + jj], w = __ldg(P.yv + row * N + a);
+          const double dr = u.x - w.x, di = u.y - w.y;
+          val = fma(dr, dr, val);
+          val = fma(di, di, val);
+        }
+        __syncthreads();
+      }
+    }
+    stamp(7);  // [7] validation
+    if (dbg)
+      for (int q = 0; q < 8; ++q) atomicAdd(P.dbg + q, ph[q]);
+    // costs: threads -> warps (in order) -> CTA -> cluster ranks (in order)
+    train = warp_sum(train);
+    val = warp_sum(val);
+    if (lane == 0) {
+      sm.red[warp] = train;
+      sm.red[RES_WARPS + warp] = val;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0, v = 0.0;
+      for (int w = 0; w < RES_WARPS; ++w) {
+        t += sm.red[w];
+        v += sm.red[RES_WARPS + w];
+      }
+      sm.cbuf[0] = t;
+      sm.cbuf[1] = v;
+    }
+    cl_arrive();
+    cl_wait();
+    if (rank == 0 && tid == 0) {
+      double t = 0.0, v = 0.0;
+      for (unsigned c = 0; c < C; ++c) {
+        t += ld_remote(sm.cbuf, c);
+        v += ld_remote(sm.cbuf + 1, c);
+      }
+      P.csum[j] = t;
+      if (P.want_val && P.V > 0) P.cval[j] = v;
+    }
+    // the next start rewrites the gate table and (later) cbuf: every CTA waits
+    // until rank 0 has read the remote costs
+    cl_arrive();
+    cl_wait();
+  }
+  pdl_trigger();
+}
+
+}  // namespace
+
+size_t res_smem_bytes(int n, int K, int ld) {
+  size_t b = (size_t)K * 16 * sizeof(double2) + (RES_WARPS * 32 + 64 + 2) * sizeof(double) +
+             32 * sizeof(double2) + (size_t)K * sizeof(int2);
+  b = (b + 15) & ~(size_t)15;
+  b += 2 * ((size_t)ld << n) * sizeof(double2);
+  return b;
+}
+size_t res_smem_limit(int minb) { return minb >= 2 ? RES_SMEM_MAX2 : RES_SMEM_MAX; }
+
+namespace {
+template <int MINB>
+void res_set_attrs() {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(res_sweep_kernel<MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)res_smem_limit(MINB));
+    cudaFuncSetAttribute(res_sweep_kernel<MINB>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr = true;
+  }
+}
+}  // namespace
+
+int resident_max_clusters(int C, size_t smem) {
+  const int minb = smem <= RES_SMEM_MAX2 ? 2 : 1;
+  if (minb == 2) res_set_attrs<2>();
+  else res_set_attrs<1>();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C * 148);
+  cfg.blockDim = dim3(RES_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute a[1];
+  a[0].id = cudaLaunchAttributeClusterDimension;
+  a[0].val.clusterDim.x = C;
+  a[0].val.clusterDim.y = 1;
+  a[0].val.clusterDim.z = 1;
+  cfg.attrs = a;
+  cfg.numAttrs = 1;
+  int num = 0;
+  const cudaError_t e = minb == 2 ? cudaOccupancyMaxActiveClusters(&num, res_sweep_kernel<2>, &cfg)
+                                  : cudaOccupancyMaxActiveClusters(&num, res_sweep_kernel<1>, &cfg);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return num;
+}
+
+cudaError_t launch_resident(const ResParams &p, int clusters, cudaStream_t st) {
+  const size_t smem = res_smem_bytes(p.n, p.K, p.ld);
+  resident_max_clusters(p.C, smem);  // sets the function attributes
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.C * clusters);
+  cfg.blockDim = dim3(RES_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute a[2];
+  a[0].id = cudaLaunchAttributeClusterDimension;
+  a[0].val.clusterDim.x = p.C;
+  a[0].val.clusterDim.y = 1;
+  a[0].val.clusterDim.z = 1;
+  a[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = a;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  return smem <= RES_SMEM_MAX2 ? cudaLaunchKernelEx(&cfg, res_sweep_kernel<2>, p)
+                               : cudaLaunchKernelEx(&cfg, res_sweep_kernel<1>, p);
+}
+
+}  // namespace qfs

@@ -29,11 +29,12 @@ using namespace qfs;
 namespace {
 
 enum KClass { K_FWD_ROW = 0, K_FWD_GATE, K_BWD, K_POLAR, K_FINAL, K_VAL_ROW, K_DIST, K_REDUCE,
-              K_NCCL, K_OP, K_NCLASS };
+              K_NCCL, K_OP, K_RES, K_NCLASS };
 // profiling classes: fwd_gate / bwd / final / validation are PHASES (one event
 // pair around the whole run of launches of that step of the sweep)
 const char *kClassName[K_NCLASS] = {"unused", "fwd_gate", "bwd", "polar", "final",
-                                    "validation", "dist", "row_reduce", "nccl_allreduce", "unit_op"};
+                                    "validation", "dist", "row_reduce", "nccl_allreduce", "unit_op",
+                                    "resident"};
 
 struct ProfRec {
   int cls;
@@ -90,6 +91,8 @@ struct qfs_ctx {
   int stagger = 1;          // QFS_STAGGER: persistent kernel half-start offset
   bool fwd_pairs = true;    // QFS_FWD_PAIRS=0: one forward pass per gate
   bool persistent = false;  // QFS_PERSISTENT=1 selects the cooperative whole-backward kernel
+  int res_per_sm = 1;       // QFS_RES_PER_SM: resident CTAs per SM the cluster plan targets
+  int path = 0;             // 0 auto, 1 streamed (B cache in HBM), 2 cluster-resident (qfs_set_path / QFS_PATH)
   size_t stage_bytes = 0;
   // graph cache
   cudaGraphExec_t gexec = nullptr;
@@ -108,6 +111,8 @@ struct qfs_ctx {
   // diagnostics (env QFS_TAIL_TIMING=1): per-gate globaltimer stamps of bwd
   unsigned long long *d_dbg = nullptr;
   std::vector<double> dbg_acc;  // [3]: main phase, partial reduce, polar (ns, summed)
+  unsigned long long *d_res_dbg = nullptr;  // [8] resident-kernel phase sums (ns), QFS_TAIL_TIMING
+  long long res_sweeps = 0;
   long long dbg_n = 0;
 };
 
@@ -429,6 +434,42 @@ qfs_status prepare_desc(qfs_ctx *c) {
 
 bool use_persistent(const qfs_ctx *c) { return c->persistent && !(c->mode == 1 && c->world > 1); }
 
+// Plan of the cluster-resident sweep (qfs_resident.cu) for ns starts of up to
+// M_max rows: the smallest power-of-two cluster whose CTAs hold their slice of
+// phi and chi (2 * 2^n * ceil(M/C) complex128) plus the gate table in shared
+// memory, widened while the starts still leave SMs idle and each CTA keeps >= 2
+// rows.  False when no cluster size up to 16 fits (or in sample-sharded mode:
+// the per-gate environment all-reduce crosses GPUs).
+struct ResPlan {
+  int C = 0, ld = 0, clusters = 0;
+  size_t smem = 0;
+};
+bool res_plan(const qfs_ctx *c, int M_max, int ns, ResPlan &pl) {
+  if (c->path == 1 || (c->mode == 1 && c->world > 1) || c->n > 13 || M_max < 1) return false;
+  // one CTA per SM (QFS_RES_PER_SM=2: two, <= 113 KB and <= 128 registers
+  // each — measured slower: the per-gate chain is latency-bound, not
+  // throughput-bound); then widen the cluster while the CTAs of all starts
+  // still fit on the GPU at once and each keeps >= 2 rows
+  int C = 1, per_sm = c->res_per_sm;
+  if (per_sm == 2)
+    for (; C <= 16; C *= 2)
+      if (res_smem_bytes(c->n, c->K, (M_max + C - 1) / C) <= res_smem_limit(2)) break;
+  if (per_sm != 2 || C > 16) {
+    per_sm = 1;
+    for (C = 1; C <= 16; C *= 2)
+      if (res_smem_bytes(c->n, c->K, (M_max + C - 1) / C) <= res_smem_limit(1)) break;
+    if (C > 16) return false;
+  }
+  while (C < 16 && (long long)ns * 2 * C <= 148LL * per_sm && (M_max + 2 * C - 1) / (2 * C) >= 2) C *= 2;
+  pl.C = C;
+  pl.ld = (M_max + C - 1) / C;
+  pl.smem = res_smem_bytes(c->n, c->K, pl.ld);
+  const int mx = resident_max_clusters(C, pl.smem);
+  if (mx < 1) return false;
+  pl.clusters = std::min(ns, mx);
+  return true;
+}
+
 // Issue the launches of one sweep for the slots [j0, j1) on stream st (no host
 // synchronisation).  Scratch arrays indexed by slot are offset by j0.
 qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStream_t st) {
@@ -437,6 +478,25 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
   c->cur_st = st;
   int M_max = 0;
   for (int j = j0; j < j1; ++j) M_max = std::max(M_max, sp.slots[j].m);
+  ResPlan pl;
+  if (res_plan(c, M_max, ns, pl)) {
+    // whole sweep + costs + validation in one cluster-resident launch
+    ResParams r{};
+    r.n = n; r.K = K; r.S = sp.S; r.C = pl.C; r.ld = pl.ld; r.n_slots = ns;
+    r.slots = c->d_slots + j0; r.pairs = c->d_pairs; r.gates = c->d_gates;
+    r.x = c->d_x; r.y = c->d_y; r.m_pool = c->m_pool; r.xv = c->d_xv; r.yv = c->d_yv;
+    r.V = c->V; r.want_val = sp.want_val ? 1 : 0; r.beta = sp.beta;
+    r.csum = c->d_csum + j0; r.cval = c->d_cval + j0; r.sig = c->d_sig; r.env_trace = sp.env_trace;
+    r.dbg = c->d_res_dbg;
+    double units = 0;
+    for (int j = j0; j < j1; ++j) units += (double)sp.slots[j].m * (double)c->N;
+    const double vunits = (sp.want_val && c->V > 0) ? (double)ns * c->V * (double)c->N : 0.0;
+    PhaseScope phase(c, K_RES);
+    LaunchScope ls(c, K_RES, 0.0, units * 96.0 * K + vunits * 32.0 * K);
+    CUDA_TRY(c, launch_resident(r, pl.clusters, st));
+    return QFS_OK;
+  }
+  if (c->path == 2) return fail(c, QFS_ERR_CAPACITY, "resident path requested but the state does not fit");
   const Slot *slots = c->d_slots + j0;
   double *partials = c->d_partials + (long long)j0 * c->nb_cap * 32;
   unsigned *cnt_b = c->d_counters + j0, *cnt_f = c->d_counters + c->S_cap + j0;
@@ -672,10 +732,12 @@ qfs_status run_sweep(qfs_ctx *c, const SweepSpec &sp, std::vector<double> &csum,
       c->launches = before;
     }
     CUDA_TRY(c, cudaGraphLaunch(c->gexec, c->st));
+    c->res_sweeps++;
     c->launches += c->glaunches;
   } else {
     qfs_status s = issue_sweep(c, sp);
     if (s != QFS_OK) return s;
+    c->res_sweeps++;
   }
   CUDA_TRY(c, cudaMemcpyAsync(c->h_csum, c->d_csum, ns * sizeof(double), cudaMemcpyDeviceToHost, c->st));
   if (sp.want_val && c->V > 0)
@@ -748,6 +810,8 @@ qfs_status create_common(int n, int k, const int32_t *pairs, int device, qfs_ctx
   if (const char *sg = getenv("QFS_STAGGER")) c->stagger = atoi(sg);
   if (const char *fp = getenv("QFS_FWD_PAIRS")) c->fwd_pairs = atoi(fp) != 0;
   if (const char *pd = getenv("QFS_PDL")) set_pdl(atoi(pd) != 0);
+  if (const char *pa = getenv("QFS_PATH")) c->path = std::max(0, std::min(2, atoi(pa)));
+  if (const char *rp = getenv("QFS_RES_PER_SM")) c->res_per_sm = atoi(rp) == 2 ? 2 : 1;
   if (e != cudaSuccess) {
     c->err = std::string("device init: ") + cudaGetErrorString(e);
     *out = c;  // caller can read the error, then destroy
@@ -755,6 +819,8 @@ qfs_status create_common(int n, int k, const int32_t *pairs, int device, qfs_ctx
   }
   if (getenv("QFS_TAIL_TIMING")) {
     cudaMalloc(&c->d_dbg, (size_t)4 * k * sizeof(unsigned long long));
+    cudaMalloc(&c->d_res_dbg, 8 * sizeof(unsigned long long));
+    cudaMemset(c->d_res_dbg, 0, 8 * sizeof(unsigned long long));
   }
   *out = c;
   return QFS_OK;
@@ -1194,6 +1260,16 @@ qfs_status qfs_profile_read(qfs_ctx *c, int cap, const char **names, long long *
 }
 
 long long qfs_launch_count(const qfs_ctx *c) { return c ? c->launches : 0; }
+
+qfs_status qfs_set_path(qfs_ctx *c, int path) {
+  if (!c) return QFS_ERR_ARG;
+  if (path < 0 || path > 2) return fail(c, QFS_ERR_ARG, "path must be 0 (auto), 1 (streamed) or 2 (resident)");
+  if (path != c->path) {
+    c->path = path;
+    drop_graph(c);
+  }
+  return QFS_OK;
+}
 void *qfs_stream(const qfs_ctx *c) { return c ? (void *)c->st : nullptr; }
 const char *qfs_last_error(const qfs_ctx *c) { return c ? c->err.c_str() : "null context"; }
 
@@ -1206,6 +1282,15 @@ void qfs_destroy(qfs_ctx *c) {
             "partial reduce %.2f us, polar %.2f us\n", c->dbg_n, c->dbg_acc[0] / c->dbg_n / 1e3,
             c->dbg_acc[1] / c->dbg_n / 1e3, c->dbg_acc[2] / c->dbg_n / 1e3);
   dfree(c->d_dbg);
+  if (c->d_res_dbg && c->res_sweeps) {
+    unsigned long long h[8];
+    cudaMemcpy(h, c->d_res_dbg, sizeof h, cudaMemcpyDeviceToHost);
+    const char *nm[8] = {"load", "forward", "env", "reduce", "polar", "uncompute-wait", "chi", "validation"};
+    fprintf(stderr, "[qfs resident timing] cluster 0 rank 0, us per sweep (%lld sweeps; K=%d):", c->res_sweeps, c->K);
+    for (int q = 0; q < 8; ++q) fprintf(stderr, " %s %.2f", nm[q], h[q] / 1e3 / c->res_sweeps);
+    fprintf(stderr, "\n");
+  }
+  dfree(c->d_res_dbg);
   prof_collect(c);
   drop_graph(c);
   for (auto e : c->ev_pool) cudaEventDestroy(e);

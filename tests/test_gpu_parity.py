@@ -28,8 +28,13 @@ def qfs():
     return Q
 
 
-def _ctx(Q, n, pairs, **kw):
-    return Q.Context(n, pairs, **kw)
+PATHS = ["streamed", "auto"]   # auto = cluster-resident whenever the states fit
+
+
+def _ctx(Q, n, pairs, path="auto", **kw):
+    ctx = Q.Context(n, pairs, **kw)
+    ctx.set_path(path)
+    return ctx
 
 
 def rand_c(rng, shape):
@@ -146,18 +151,20 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("name,init,s,m,sweeps,k", CASES)
-def test_trace_parity(qfs, name, init, s, m, sweeps, k):
+def test_trace_parity(qfs, name, init, s, m, sweeps, k, path):
     p = I.make_problem(name, init=init, s=s, k=k)
     m = m or p.m_init
-    ctx = _ctx(qfs, p.n, p.pairs)
+    ctx = _ctx(qfs, p.n, p.pairs, path)
     ctx.set_samples(p.x, p.y, p.xv, p.yv)
     gt = ctx.trace_sweeps(p.init, m, sweeps)
     ot = oracle.trace_sweeps(p.n, p.pairs, p.init, p.x, p.y, m, sweeps)
     _compare_traces(gt, ot, f"{name}-{init}")
 
 
-def test_trace_parity_ragged_and_degenerate(qfs):
+@pytest.mark.parametrize("path", PATHS)
+def test_trace_parity_ragged_and_degenerate(qfs, path):
     """Ragged M (odd row counts), reversed / non-adjacent / repeated pairs, K=1, n=2."""
     rng = np.random.default_rng(5)
     for n, pairs, m in [(2, [[0, 1]], 3), (2, [[1, 0], [0, 1], [1, 0]], 4),
@@ -168,7 +175,7 @@ def test_trace_parity_ragged_and_degenerate(qfs):
         x = I.haar_states(rng, n, m)
         y = I.apply_circuit_tensor(n, pairs, target, x)
         init = np.stack([np.stack([unitary(rng) for _ in pairs]) for _ in range(3)])
-        ctx = _ctx(qfs, n, pairs)
+        ctx = _ctx(qfs, n, pairs, path)
         ctx.set_samples(x, y)
         gt = ctx.trace_sweeps(init, m, 4)
         ot = oracle.trace_sweeps(n, pairs, init, x, y, m, 4)
@@ -216,30 +223,32 @@ def test_full_size_c4_sampled_starts(qfs):
 
 
 # ----------------------------------------------------------- instantiation --
-def _inst_both(qfs, p, prm):
-    ctx = _ctx(qfs, p.n, p.pairs)
+def _inst_both(qfs, p, prm, path="auto"):
+    ctx = _ctx(qfs, p.n, p.pairs, path)
     ctx.set_samples(p.x, p.y, p.xv, p.yv)
     g1, r1, w1 = ctx.instantiate(p.init, prm)
     g2, r2, w2 = oracle.instantiate(p.n, p.pairs, p.x, p.y, p.xv, p.yv, p.init, prm, threads=8)
     return (g1, r1, w1), (g2, r2, w2)
 
 
-def test_instantiate_c1_parity(qfs):
+@pytest.mark.parametrize("path", PATHS)
+def test_instantiate_c1_parity(qfs, path):
     """C1 as configured (500 sweeps, plateau off): same termination, sweeps, final cost."""
     p = I.make_problem("c1", init="R")
-    (g1, r1, w1), (g2, r2, w2) = _inst_both(qfs, p, dict(p.params))
+    (g1, r1, w1), (g2, r2, w2) = _inst_both(qfs, p, dict(p.params), path)
     assert r1[0]["term"] == r2[0]["term"] and r1[0]["sweeps"] == r2[0]["sweeps"]
     assert abs(r1[0]["c_train"] - r2[0]["c_train"]) <= 1e-7 * r2[0]["c_train"] + 1e-14
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("name,s", [("c2", 4), ("c3", 2)])
-def test_instantiate_warm_converges_and_matches(qfs, name, s):
+def test_instantiate_warm_converges_and_matches(qfs, name, s, path):
     """Solvable-by-construction targets reach c_train <= 1e-8 on the GPU and the
     controller takes the same decisions as the oracle (termination, restarts,
     final M, sweep count within +-2; SURVEY §8(c) 'parity unpinned' rule)."""
     p = I.make_problem(name, init="W", s=s)
     prm = dict(p.params, max_iter=300)
-    (g1, r1, w1), (g2, r2, w2) = _inst_both(qfs, p, prm)
+    (g1, r1, w1), (g2, r2, w2) = _inst_both(qfs, p, prm, path)
     assert r1[w1]["term"] == "CONVERGED" and r1[w1]["c_train"] <= 1e-8
     assert w1 == w2
     for a, b in zip(r1, r2):
@@ -247,20 +256,22 @@ def test_instantiate_warm_converges_and_matches(qfs, name, s):
         assert abs(a["sweeps"] - b["sweeps"]) <= 2
 
 
-def test_instantiate_restart_geometry_gpu(qfs):
+@pytest.mark.parametrize("path", PATHS)
+def test_instantiate_restart_geometry_gpu(qfs, path):
     """Double-and-restart on the GPU path (C2 random init, per-start ragged M)."""
     p = I.make_problem("c2", init="R", s=6)
     prm = dict(p.params, max_iter=40, stop_on_first=0)
-    (g1, r1, w1), (g2, r2, w2) = _inst_both(qfs, p, prm)
+    (g1, r1, w1), (g2, r2, w2) = _inst_both(qfs, p, prm, path)
     assert any(r["restarts"] > 0 for r in r1)
     for a, b in zip(r1, r2):
         assert a["final_m"] == min(p.m_init * 2 ** a["restarts"], 64)
         assert a["term"] == b["term"] and a["restarts"] == b["restarts"]
 
 
-def test_deterministic_bitwise(qfs):
+@pytest.mark.parametrize("path", PATHS)
+def test_deterministic_bitwise(qfs, path):
     p = I.make_problem("c3", init="R", s=8)
-    ctx = _ctx(qfs, p.n, p.pairs)
+    ctx = _ctx(qfs, p.n, p.pairs, path)
     ctx.set_samples(p.x, p.y, p.xv, p.yv)
     a = ctx.trace_sweeps(p.init, 16, 2)
     b = ctx.trace_sweeps(p.init, 16, 2)
@@ -326,3 +337,28 @@ def test_multistart_dist_path_single_rank(qfs):
     assert w1 == w2 and r1[w1]["term"] == "CONVERGED"
     for a, b in zip(r1, r2):
         assert a["term"] == b["term"] and abs(a["sweeps"] - b["sweeps"]) <= 2
+
+
+def test_resident_path_selection_and_validation(qfs):
+    """Forced resident path: runs where the states fit (C3: cluster of 2 CTAs),
+    fails with QFS_ERR_CAPACITY where they do not (n = 12, M = 32); its fused
+    validation cost equals the oracle's."""
+    from paper_2405_12866_b200.qfs import QfsError
+    p = I.make_problem("c3", init="W", s=3)
+    ctx = _ctx(qfs, p.n, p.pairs, "resident")
+    ctx.set_samples(p.x, p.y, p.xv, p.yv)
+    prm = dict(p.params, max_iter=4, min_iter=100)
+    g1, r1, w1 = ctx.instantiate(p.init, prm)
+    g2, r2, w2 = oracle.instantiate(p.n, p.pairs, p.x, p.y, p.xv, p.yv, p.init, prm)
+    for a, b in zip(r1, r2):
+        assert abs(a["c_val"] - b["c_val"]) <= 1e-10 * b["c_val"]
+        assert abs(a["c_train"] - b["c_train"]) <= 1e-10 * b["c_train"]
+    q = I.make_problem("c4", init="R", s=1, k=8)
+    big = _ctx(qfs, q.n, q.pairs, "resident")
+    big.set_samples(q.x, q.y, q.xv, q.yv)
+    with pytest.raises(QfsError) as ei:
+        big.trace_sweeps(q.init, 32, 1)
+    assert ei.value.status == 2
+    with pytest.raises(QfsError) as ei:
+        big.set_path(7)
+    assert ei.value.status == 1
