@@ -41,6 +41,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "QFactor-Sample sweeps/sec + time-to-solution per instantiation; % HBM/FP64 peak"
 UNIT = "start-sweeps/s"
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2
 
 
 def load_peaks():
@@ -280,10 +281,21 @@ def main():
             traffic = tj.get(args.config, {}).get(dom)
         except Exception:
             traffic = None
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+    if dom == "resident":
+        # cluster-resident sweep: no HBM traffic inside the sweep; bound by the
+        # FP64 pipe: algorithmic flops (96 per amp-gate + 32 per
+        # validation amp-gate) / time against the unit-count peak
+        # 148 SMs x 64 DFMA/clk x 2 flop x 1.965 GHz (tools/peaks.cu measures 34.19)
+        achieved = pd["flops"] / (pd["ms"] * 1e-3) / 1e12
+        peak, peak_src = FP64_PEAK_TFLOPS, "derived: 148 SMs x 64 DFMA/clk x 2 x 1.965 GHz (DFMA microbenchmark 34.19)"
+        bound, unit = "alu", "TFLOP/s"
+    else:
+        bound, unit = "hbm", "GB/s"
+    roofline = {"bound": bound, "kernel": dom, "achieved": round(achieved, 3), "peak": peak, "unit": unit,
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                 "avg_launch_us": round(pd["ms"] / pd["launches"] * 1e3, 3),
-                "bytes_per_launch": pd["bytes"] / pd["launches"],
+                "bytes_per_launch": pd["bytes"] / pd["launches"], "flops_per_launch": pd["flops"] / pd["launches"],
+                "pipe": "fp64" if bound == "alu" else None,
                 "share_of_kernel_time": round(pd["ms"] / tot_ms, 4),
                 "profiled_ms_per_step": round(prof_step_ms, 4),
                 "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
