@@ -91,6 +91,21 @@ __device__ __forceinline__ int pidx(int v) {
   return ((v >> TP0) & 1) | (((v >> TP1) & 1) << 1);
 }
 
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// all threads of the CTA wait until *flag >= target (thread 0 polls)
+__device__ void cta_wait_flag(const unsigned *flag, unsigned target) {
+  if (threadIdx.x == 0)
+    while (ld_acquire(flag) < target) __nanosleep(32);
+  __syncthreads();
+}
+
 struct BwdShared {
   double2 sQ[16];                          // G_{i+1}^dag
   double2 red[BWD_THREADS / 32][4][16];    // per-warp (per lane-group) E partials
@@ -117,7 +132,8 @@ struct BwdShared {
 template <int NU, int TP0, int TP1, bool UPD>
 __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslot, int s,
                                  unsigned Ms, bool fence_chi, BwdShared &sh,
-                                 double2 *stage_buf) {
+                                 double2 *stage_buf, const unsigned *wflag = nullptr,
+                                 unsigned wtarget = 0) {
   constexpr int T = 1 << (NU - 2);
   constexpr int LPT = 32 / T;
   constexpr int NWARP = BWD_THREADS / 32;
@@ -200,7 +216,10 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
     for (int k = 0; k < BWD_STAGES - 1; ++k) issue_part(k, false, true);
     cp_async_commit();
   }
-  pdl_wait();
+  // dependence on the previous gate: kernel boundary (PDL) or, in the
+  // persistent kernel, the start's release flag
+  if (wflag) cta_wait_flag(wflag, wtarget);
+  else pdl_wait();
   if (UPD && threadIdx.x < 16) {
     const int a = threadIdx.x >> 2, b = threadIdx.x & 3;
     const double2 g = __ldcg(P.gates + ((long long)s * P.K + G.upd_gate) * 16 + 4 * b + a);
@@ -380,25 +399,11 @@ __global__ void __launch_bounds__(BWD_THREADS, QFS_BWD_MINB) bwd_kernel(const Bw
   bwd_finish(P, P.g, jslot, sl.s, sh);
 }
 
-__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-// all threads of the CTA wait until *flag >= target (thread 0 polls)
-__device__ void cta_wait_flag(const unsigned *flag, unsigned target) {
-  if (threadIdx.x == 0)
-    while (ld_acquire(flag) < target) __nanosleep(32);
-  __syncthreads();
-}
-
 template <int NU, int TP0, int TP1, bool UPD>
 __device__ __forceinline__ bool gate_dispatch_one(const BwdParams &P, const GateDesc &G, int j, int s,
-                                                  unsigned Ms, BwdShared &sh, double2 *buf) {
-  return bwd_gate_partial<NU, TP0, TP1, UPD>(P, G, j, s, Ms, true, sh, buf);
+                                                  unsigned Ms, BwdShared &sh, double2 *buf,
+                                                  const unsigned *wflag, unsigned wtarget) {
+  return bwd_gate_partial<NU, TP0, TP1, UPD>(P, G, j, s, Ms, true, sh, buf, wflag, wtarget);
 }
 
 // Whole backward pass of a sweep plus the sweep-end cost in ONE cooperative
@@ -417,22 +422,24 @@ __global__ void __launch_bounds__(BWD_THREADS, QFS_BWD_MINB) bwd_persistent_kern
   const int half = (int)gridDim.y / 2;
   if (P.stagger && half > 0 && j >= half && P.K > 1) cta_wait_flag(P.flags + (j - half), 1u);
   for (int i = P.K - 1; i >= 0; --i) {
-    if (i < P.K - 1) cta_wait_flag(P.flags + j, (unsigned)(P.K - 1 - i));
+    // wait for gate i+1's polar inside the gate step, after the phi prefetch
+    const unsigned *wf = i < P.K - 1 ? P.flags + j : nullptr;
+    const unsigned wt = (unsigned)(P.K - 1 - i);
     const GateDesc &G = P.desc[i];
     bool w0;
     if (!G.upd) {
-      w0 = gate_dispatch_one<2, 0, 1, false>(P, G, j, sl.s, Ms, sh, stage_buf);
+      w0 = gate_dispatch_one<2, 0, 1, false>(P, G, j, sl.s, Ms, sh, stage_buf, wf, wt);
     } else if (G.nu == 2) {
-      w0 = G.tp0 == 0 ? gate_dispatch_one<2, 0, 1, true>(P, G, j, sl.s, Ms, sh, stage_buf)
-                      : gate_dispatch_one<2, 1, 0, true>(P, G, j, sl.s, Ms, sh, stage_buf);
+      w0 = G.tp0 == 0 ? gate_dispatch_one<2, 0, 1, true>(P, G, j, sl.s, Ms, sh, stage_buf, wf, wt)
+                      : gate_dispatch_one<2, 1, 0, true>(P, G, j, sl.s, Ms, sh, stage_buf, wf, wt);
     } else if (G.nu == 3) {
-      if (G.tp0 == 0 && G.tp1 == 2) w0 = gate_dispatch_one<3, 0, 2, true>(P, G, j, sl.s, Ms, sh, stage_buf);
-      else if (G.tp0 == 2 && G.tp1 == 0) w0 = gate_dispatch_one<3, 2, 0, true>(P, G, j, sl.s, Ms, sh, stage_buf);
-      else if (G.tp0 == 1 && G.tp1 == 2) w0 = gate_dispatch_one<3, 1, 2, true>(P, G, j, sl.s, Ms, sh, stage_buf);
-      else w0 = gate_dispatch_one<3, 2, 1, true>(P, G, j, sl.s, Ms, sh, stage_buf);
+      if (G.tp0 == 0 && G.tp1 == 2) w0 = gate_dispatch_one<3, 0, 2, true>(P, G, j, sl.s, Ms, sh, stage_buf, wf, wt);
+      else if (G.tp0 == 2 && G.tp1 == 0) w0 = gate_dispatch_one<3, 2, 0, true>(P, G, j, sl.s, Ms, sh, stage_buf, wf, wt);
+      else if (G.tp0 == 1 && G.tp1 == 2) w0 = gate_dispatch_one<3, 1, 2, true>(P, G, j, sl.s, Ms, sh, stage_buf, wf, wt);
+      else w0 = gate_dispatch_one<3, 2, 1, true>(P, G, j, sl.s, Ms, sh, stage_buf, wf, wt);
     } else {
-      w0 = G.tp0 == 2 ? gate_dispatch_one<4, 2, 3, true>(P, G, j, sl.s, Ms, sh, stage_buf)
-                      : gate_dispatch_one<4, 3, 2, true>(P, G, j, sl.s, Ms, sh, stage_buf);
+      w0 = G.tp0 == 2 ? gate_dispatch_one<4, 2, 3, true>(P, G, j, sl.s, Ms, sh, stage_buf, wf, wt)
+                      : gate_dispatch_one<4, 3, 2, true>(P, G, j, sl.s, Ms, sh, stage_buf, wf, wt);
     }
     if (w0 && warp0_elect_last(&P.counters[j], (unsigned)P.nb)) {
       bwd_finish(P, G, j, sl.s, sh);

@@ -380,7 +380,88 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
   pdl_trigger();
 }
 
+// Validation cost of the streamed path: one CTA per (start,
+// block of ld validation rows); the rows sit in shared memory as a [2^n][ld]
+// block (same layout and gate routine as the resident sweep), all K
+// post-sweep gates are applied in order, then each row's ||C xv - yv||^2 goes
+// to row_out[j][row] (summed over rows in row order by row_reduce_kernel).
+__global__ void __launch_bounds__(RES_THREADS, 2) val_blk_kernel(const ValRowParams P, int ld) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double red[RES_WARPS];
+  const int K = P.K, n = P.n;
+  const unsigned N = 1u << n;
+  double2 *G = (double2 *)smem_raw;
+  int2 *pr = (int2 *)(G + K * 16);
+  double2 *st = (double2 *)((((uintptr_t)(pr + K)) + 15) & ~(uintptr_t)15);
+  const int j = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int r0 = blockIdx.x * ld, nb = min(ld, P.rows - r0);
+  for (unsigned q = tid; q < N * (unsigned)nb; q += RES_THREADS) {
+    const unsigned jj = q / N, a = q - jj * N;
+    st[a * ld + jj] = __ldg(P.xv + (long long)(r0 + jj) * N + a);
+  }
+  for (int k = tid; k < K; k += RES_THREADS) pr[k] = P.pairs[k];
+  pdl_wait();  // the gates are the ones the backward pass just wrote
+  const int s = P.slots[j].s;
+  for (int q = tid; q < K * 16; q += RES_THREADS) G[q] = P.gates[(long long)s * K * 16 + q];
+  __syncthreads();
+  for (int k = 0; k < K; ++k) {
+    res_apply(st, G + 16 * k, pr[k], false, nb, (unsigned)ld, n, tid, RES_THREADS);
+    __syncthreads();
+  }
+  for (int jj = 0; jj < nb; ++jj) {
+    double acc = 0.0;
+    const double2 *yr = P.yv + (long long)(r0 + jj) * N;
+    for (unsigned a = tid; a < N; a += RES_THREADS) {
+      const double2 u = st[a * ld + jj], w = __ldg(yr + a);
+      const double dr = u.x - w.x, di = u.y - w.y;
+      acc = fma(dr, dr, acc);
+      acc = fma(di, di, acc);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < RES_WARPS; ++w) t += red[w];
+      P.row_out[(long long)j * P.rows + r0 + jj] = t;
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
+
+size_t val_blk_smem(int n, int K, int ld) {
+  return (((size_t)K * 16 * sizeof(double2) + (size_t)K * sizeof(int2) + 15) & ~(size_t)15) +
+         ((size_t)ld << n) * sizeof(double2);
+}
+
+cudaError_t launch_val_block(const ValRowParams &p, int n_slots, cudaStream_t st) {
+  // rows per CTA: the most that fit in shared memory, reduced while the grid
+  // has fewer CTAs than SMs
+  constexpr size_t lim = RES_SMEM_MAX - 256;  // the kernel's static reduction array sits beside it
+  int ld = 1;
+  while (ld < p.rows && val_blk_smem(p.n, p.K, ld + 1) <= lim) ++ld;
+  while (ld > 1 && (long long)((p.rows + ld - 1) / ld) * n_slots < 148) --ld;
+  const size_t smem = val_blk_smem(p.n, p.K, ld);
+  if (smem > lim) return cudaErrorInvalidConfiguration;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(val_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((p.rows + ld - 1) / ld, n_slots);
+  cfg.blockDim = dim3(RES_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute a[1];
+  a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = a;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, val_blk_kernel, p, ld);
+}
 
 size_t res_smem_bytes(int n, int K, int ld) {
   size_t b = (size_t)K * 16 * sizeof(double2) + (RES_WARPS * 32 + 64 + 2) * sizeof(double) +

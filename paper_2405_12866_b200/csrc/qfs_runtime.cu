@@ -91,6 +91,7 @@ struct qfs_ctx {
   int stagger = 1;          // QFS_STAGGER: persistent kernel half-start offset
   bool fwd_pairs = true;    // QFS_FWD_PAIRS=0: one forward pass per gate
   bool persistent = false;  // QFS_PERSISTENT=1 selects the cooperative whole-backward kernel
+  bool val_block = true;    // QFS_VAL_BLOCK=0: one-row-per-CTA validation kernel
   int res_per_sm = 1;       // QFS_RES_PER_SM: resident CTAs per SM the cluster plan targets
   int path = 0;             // 0 auto, 1 streamed (B cache in HBM), 2 cluster-resident (qfs_set_path / QFS_PATH)
   size_t stage_bytes = 0;
@@ -646,7 +647,8 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
       f.n = n; f.K = K; f.rows = c->V; f.slots = slots; f.pairs = c->d_pairs;
       f.gates = c->d_gates; f.xv = c->d_xv; f.yv = c->d_yv; f.row_out = rowout;
       LaunchScope ls(c, K_VAL_ROW, vunits * 32.0, vunits * 32.0 * K);
-      CUDA_TRY(c, launch_val_row(f, ns, st));
+      if (c->val_block && val_blk_smem(n, K, 1) + 256 <= res_smem_limit(1)) CUDA_TRY(c, launch_val_block(f, ns, st));
+      else CUDA_TRY(c, launch_val_row(f, ns, st));
     } else {
       const long long VN = (long long)c->V * N;
       for (int k = 0; k < K; ++k) {
@@ -811,6 +813,7 @@ qfs_status create_common(int n, int k, const int32_t *pairs, int device, qfs_ctx
   if (const char *fp = getenv("QFS_FWD_PAIRS")) c->fwd_pairs = atoi(fp) != 0;
   if (const char *pd = getenv("QFS_PDL")) set_pdl(atoi(pd) != 0);
   if (const char *pa = getenv("QFS_PATH")) c->path = std::max(0, std::min(2, atoi(pa)));
+  if (const char *vb = getenv("QFS_VAL_BLOCK")) c->val_block = atoi(vb) != 0;
   if (const char *rp = getenv("QFS_RES_PER_SM")) c->res_per_sm = atoi(rp) == 2 ? 2 : 1;
   if (e != cudaSuccess) {
     c->err = std::string("device init: ") + cudaGetErrorString(e);
