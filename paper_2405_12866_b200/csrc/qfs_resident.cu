@@ -74,8 +74,8 @@ __device__ __forceinline__ double ld_remote(const double *p, unsigned rank) {
 // psi <- G psi (dag: G^dag psi) on the qubit pair pq for the rows jj < cnt of
 // a [2^n][ld] shared-memory state block (sample-minor: quadruple members of
 // consecutive items are consecutive samples).  Threads t0, t0 + nt, ...
-__device__ void res_apply(double2 *psi, const double2 *G, int2 pq, bool dag, int cnt, unsigned ld, int n,
-                          int t0, int nt) {
+__device__ void res_apply(double2 *psi, const double2 *G, int2 pq, bool dag, int cnt, const FastDiv &fd,
+                          unsigned ld, int n, int t0, int nt) {
   if (cnt <= 0) return;
   double2 g[16];
 #pragma unroll
@@ -83,7 +83,6 @@ __device__ void res_apply(double2 *psi, const double2 *G, int2 pq, bool dag, int
   const int lo = min(pq.x, pq.y), hi = max(pq.x, pq.y);
   const unsigned o1 = (1u << pq.x) * ld, o2 = (1u << pq.y) * ld;
   const unsigned items = (1u << (n - 2)) * (unsigned)cnt;
-  const FastDiv fd((unsigned)cnt);
   for (unsigned q = (unsigned)t0; q < items; q += (unsigned)nt) {
     const unsigned r = fd.div(q);
     const unsigned b = insert_zero32(insert_zero32(r, lo), hi) * ld + (q - r * (unsigned)cnt);
@@ -127,8 +126,8 @@ __device__ __forceinline__ double warp_sum(double v) {
 // E[l_in][l_out] += sum phi[idx(l_in)] conj(chi[idx(l_out)]) over this CTA's
 // items; every warp writes its reduced 32 doubles (re/im of the 16
 // entries, row-major) to red[warp][.]
-__device__ void res_env(const double2 *phi, const double2 *chi, int2 pq, int cnt, unsigned ld, int n,
-                        double *red) {
+__device__ void res_env(const double2 *phi, const double2 *chi, int2 pq, int cnt, const FastDiv &fd,
+                        unsigned ld, int n, double *red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double acc[32];
 #pragma unroll
@@ -137,7 +136,6 @@ __device__ void res_env(const double2 *phi, const double2 *chi, int2 pq, int cnt
     const int lo = min(pq.x, pq.y), hi = max(pq.x, pq.y);
     const unsigned o1 = (1u << pq.x) * ld, o2 = (1u << pq.y) * ld;
     const unsigned items = (1u << (n - 2)) * (unsigned)cnt;
-    const FastDiv fd((unsigned)cnt);
     for (unsigned q = threadIdx.x; q < items; q += RES_THREADS) {
       const unsigned r = fd.div(q);
       const unsigned b = insert_zero32(insert_zero32(r, lo), hi) * ld + (q - r * (unsigned)cnt);
@@ -215,6 +213,7 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
     const int ms = (M + (int)C - 1) / (int)C;
     const int m0 = (int)rank * ms;
     const int cnt = max(0, min(ms, M - m0));
+    const FastDiv fd((unsigned)max(cnt, 1));  // item -> (quadruple, row) of this CTA's rows
     double2 *gglob = P.gates + (long long)s * K * 16;
     for (int q = tid; q < K * 16; q += RES_THREADS) sm.G[q] = gglob[q];
     for (unsigned q = tid; q < N * (unsigned)cnt; q += RES_THREADS) {
@@ -227,14 +226,14 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
     stamp(0);  // [0] load
     // forward with the previous sweep's gates: phi = B_{K-1} = G_{K-2} ... G_0 x
     for (int k = 0; k + 1 < K; ++k) {
-      res_apply(sm.phi, sm.G + 16 * k, sm.pr[k], false, cnt, ld, n, tid, RES_THREADS);
+      res_apply(sm.phi, sm.G + 16 * k, sm.pr[k], false, cnt, fd, ld, n, tid, RES_THREADS);
       __syncthreads();
     }
     stamp(1);  // [1] forward
     double train = 0.0;
     for (int i = K - 1; i >= 0; --i) {
       const int par = i & 1;
-      res_env(sm.phi, sm.chi, sm.pr[i], cnt, ld, n, sm.red);
+      res_env(sm.phi, sm.chi, sm.pr[i], cnt, fd, ld, n, sm.red);
       __syncthreads();
       stamp(2);  // [2] environment pass
       if (warp == 0) {
@@ -274,13 +273,13 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
         stamp(4);  // [4] polar
       } else {
         // uncompute B_{i-1} = G_{i-1}^dag B_i with the old G_{i-1}, overlapping the polar
-        if (i > 0) res_apply(sm.phi, sm.G + 16 * (i - 1), sm.pr[i - 1], true, cnt, ld, n, tid - 32, RES_THREADS - 32);
+        if (i > 0) res_apply(sm.phi, sm.G + 16 * (i - 1), sm.pr[i - 1], true, cnt, fd, ld, n, tid - 32, RES_THREADS - 32);
         cl_wait();
       }
       __syncthreads();
       stamp(5);  // [5] wait for the uncompute warps
       if (i > 0) {
-        res_apply(sm.chi, sm.G + 16 * i, sm.pr[i], true, cnt, ld, n, tid, RES_THREADS);
+        res_apply(sm.chi, sm.G + 16 * i, sm.pr[i], true, cnt, fd, ld, n, tid, RES_THREADS);
       } else if (cnt > 0) {
         // chi' = G_0^dag chi and c_train = sum ||chi' - x||^2
         const double2 *G = sm.G;
@@ -291,7 +290,6 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
         const int lo = min(pq.x, pq.y), hi = max(pq.x, pq.y);
         const unsigned o[4] = {0u, (1u << pq.x), (1u << pq.y), (1u << pq.x) | (1u << pq.y)};
         const unsigned items = (N >> 2) * (unsigned)cnt;
-        const FastDiv fd((unsigned)cnt);
         for (unsigned q = tid; q < items; q += RES_THREADS) {
           const unsigned r = fd.div(q), jj = q - r * (unsigned)cnt;
           const unsigned base = insert_zero32(insert_zero32(r, lo), hi);
@@ -326,8 +324,9 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
           sm.phi[a * ld + jj] = __ldg(P.xv + row * N + a);
         }
         __syncthreads();
+        const FastDiv fdv((unsigned)nb);
         for (int k = 0; k < K; ++k) {
-          res_apply(sm.phi, sm.G + 16 * k, sm.pr[k], false, nb, ld, n, tid, RES_THREADS);
+          res_apply(sm.phi, sm.G + 16 * k, sm.pr[k], false, nb, fdv, ld, n, tid, RES_THREADS);
           __syncthreads();
         }
         for (unsigned q = tid; q < N * (unsigned)nb; q += RES_THREADS) {
@@ -404,8 +403,9 @@ __global__ void __launch_bounds__(RES_THREADS, 2) val_blk_kernel(const ValRowPar
   const int s = P.slots[j].s;
   for (int q = tid; q < K * 16; q += RES_THREADS) G[q] = P.gates[(long long)s * K * 16 + q];
   __syncthreads();
+  const FastDiv fdv((unsigned)nb);
   for (int k = 0; k < K; ++k) {
-    res_apply(st, G + 16 * k, pr[k], false, nb, (unsigned)ld, n, tid, RES_THREADS);
+    res_apply(st, G + 16 * k, pr[k], false, nb, fdv, (unsigned)ld, n, tid, RES_THREADS);
     __syncthreads();
   }
   for (int jj = 0; jj < nb; ++jj) {

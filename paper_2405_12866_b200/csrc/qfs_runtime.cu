@@ -893,6 +893,9 @@ static qfs_status set_samples_impl(qfs_ctx *c, int m_pool, const void *x, const 
   if ((long long)m_pool * (c->mode == 1 ? c->world : 1) > c->N)
     return fail(c, QFS_ERR_CAPACITY, "m_pool > 2^n");
   CUDA_TRY(c, cudaSetDevice(c->device));
+  // the cached sweep graph holds the pool pointers: it is rebuilt only when a
+  // buffer is reallocated (same shapes: the new contents are used in place)
+  const bool realloc = m_pool != c->m_pool || v != c->V;
   if (m_pool != c->m_pool) {
     dfree(c->d_x); dfree(c->d_y);
     CUDA_TRY(c, cudaMalloc(&c->d_x, (size_t)m_pool * c->N * sizeof(double2)));
@@ -935,7 +938,7 @@ static qfs_status set_samples_impl(qfs_ctx *c, int m_pool, const void *x, const 
     c->have_samples = false;
     return fail(c, QFS_ERR_NUMERIC, "non-finite sample");
   }
-  drop_graph(c);
+  if (realloc) drop_graph(c);
   return QFS_OK;
 }
 
