@@ -24,6 +24,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <utility>
+
 #include "qfs_device.cuh"
 #include "qfs_internal.h"
 
@@ -470,6 +473,7 @@ size_t res_smem_bytes(int n, int K, int ld) {
   b += 2 * ((size_t)ld << n) * sizeof(double2);
   return b;
 }
+int resident_max_clusters_query(int C, size_t smem);
 size_t res_smem_limit(int minb) { return minb >= 2 ? RES_SMEM_MAX2 : RES_SMEM_MAX; }
 
 namespace {
@@ -486,6 +490,19 @@ void res_set_attrs() {
 }  // namespace
 
 int resident_max_clusters(int C, size_t smem) {
+  // cudaOccupancyMaxActiveClusters is slow (it is queried at every graph
+  // capture, and captures follow every change of the active-start set): cache
+  // per (cluster size, shared memory)
+  static std::map<std::pair<int, size_t>, int> cache;
+  const auto key = std::make_pair(C, smem);
+  const auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  const int r = resident_max_clusters_query(C, smem);
+  cache[key] = r;
+  return r;
+}
+
+int resident_max_clusters_query(int C, size_t smem) {
   const int minb = smem <= RES_SMEM_MAX2 ? 2 : 1;
   if (minb == 2) res_set_attrs<2>();
   else res_set_attrs<1>();
