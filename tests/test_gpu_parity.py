@@ -362,3 +362,25 @@ def test_resident_path_selection_and_validation(qfs):
     with pytest.raises(QfsError) as ei:
         big.set_path(7)
     assert ei.value.status == 1
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_appendix_d_basis_vs_haar_training_states(qfs, path):
+    """P:458-464 (App. D) on the GPU path: M = 4 computational-basis training
+    states with qubit 0 fixed fit the R_z-first circuit without generalising
+    (c_val > 0.1), M = 4 Haar states generalise; the Haar run matches the oracle."""
+    from test_oracle_pins import _appendix_d_problem
+    n, pairs, target, alpha, xb, xh, xv, ys, init, prm = _appendix_d_problem()
+    for x, y, generalises in ((xb, ys["b"], False), (xh, ys["h"], True)):
+        ctx = _ctx(qfs, n, pairs, path)
+        ctx.set_samples(x, y, xv, ys["v"])
+        g1, r1, _ = ctx.instantiate(init, prm)
+        g2, r2, _ = oracle.instantiate(n, pairs, x, y, xv, ys["v"], init, prm)
+        for a, b in zip(r1, r2):
+            assert a["term"] == b["term"] == "MAX_ITER"
+            if generalises:
+                assert a["c_val"] < 1e-4
+                assert abs(a["c_val"] - b["c_val"]) <= 1e-3 * b["c_val"] + 1e-12
+                assert abs(a["c_train"] - b["c_train"]) <= 1e-3 * b["c_train"] + 1e-14
+            else:
+                assert a["c_train"] < 1e-5 and a["c_val"] > 0.1

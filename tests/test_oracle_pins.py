@@ -452,3 +452,50 @@ def test_controller_converges_warm_and_generalises():
     yc = oracle.circuit_forward(p.n, p.pairs, g[win], fresh)
     d = np.sum(np.abs(yt - yc) ** 2, axis=1)
     assert np.mean(d < prm["dist_tol"] * (1 + prm["overtrain_ratio"])) >= 0.9
+
+
+def _appendix_d_problem():
+    """n = 3, K = 4; the first block is R_z(alpha) on qubit 0 (local index l =
+    b(p0) + 2 b(p1), so the phase follows l & 1); the rest are Haar blocks."""
+    n, pairs = 3, np.array([[0, 1], [1, 2], [0, 1], [1, 2]], np.int32)
+    rng = np.random.default_rng(458)
+    alpha = 0.9
+    rz = np.diag(np.exp(0.5j * alpha * np.array([-1, 1, -1, 1])))
+    target = np.stack([rz] + [I.haar_unitary(rng) for _ in range(3)])
+    xb = np.zeros((4, 8), np.complex128)
+    for j, idx in enumerate([0, 2, 4, 6]):      # the basis states with qubit 0 = |0>
+        xb[j, idx] = 1.0
+    xh = I.haar_states(rng, n, 4)
+    xv = I.haar_states(np.random.default_rng(7), n, 6)
+    ys = {k: I.apply_circuit_tensor(n, pairs, target, v) for k, v in (("b", xb), ("h", xh), ("v", xv))}
+    init = np.stack([np.stack([I.warm_gate(np.random.default_rng(100 + s), target[j], 0.3) for j in range(4)])
+                     for s in range(2)])
+    prm = dict(dist_tol=1e-12, diff_tol_r=1e-3, plateau_window=0, min_iter=6, max_iter=300, m_init=4,
+               overtrain_ratio=1e300, beta=0.0, stop_on_first=0)
+    return n, pairs, target, alpha, xb, xh, xv, ys, init, prm
+
+
+def test_appendix_d_basis_training_states_blind_to_rz():
+    """P:458-464 (App. D): on computational-basis inputs |0 b1 b2> an R_z(alpha)
+    first gate on qubit 0 acts as the global phase e^{-i alpha/2}: the circuit with
+    that block replaced by e^{-i alpha/2} I has sample cost 0 on them (closed form),
+    but cost 2 sin^2(alpha/2) * 2 * <|amp(qubit 0 = 1)|^2> on Haar states.  Fitting
+    M = 4 such basis states therefore reaches a small training cost without
+    generalising, while M = 4 Haar states generalise (validation on 6 Haar states)."""
+    n, pairs, target, alpha, xb, xh, xv, ys, init, prm = _appendix_d_problem()
+    blind = target.copy()
+    blind[0] = np.exp(-0.5j * alpha) * np.eye(4)
+    d_basis = np.sum(np.abs(ys["b"] - oracle.circuit_forward(n, pairs, blind, xb)) ** 2) / 4
+    assert d_basis < 1e-28
+    # closed form on any state: ||(R_z - e^{-ia/2}) psi||^2 = |e^{ia/2} - e^{-ia/2}|^2 p1 = 4 sin^2(a/2) p1
+    p1 = np.sum(np.abs(xh[:, 1::2]) ** 2, axis=1)  # weight of qubit 0 = |1>
+    want = np.mean(4 * np.sin(alpha / 2) ** 2 * p1)
+    got = np.sum(np.abs(I.apply_circuit_tensor(n, pairs, target, xh)
+                        - oracle.circuit_forward(n, pairs, blind, xh)) ** 2) / 4
+    assert abs(got - want) <= 1e-12
+    _, rb, _ = oracle.instantiate(n, pairs, xb, ys["b"], xv, ys["v"], init, prm)
+    _, rh, _ = oracle.instantiate(n, pairs, xh, ys["h"], xv, ys["v"], init, prm)
+    for r in rb:
+        assert r["c_train"] < 1e-5 and r["c_val"] > 0.1
+    for r in rh:
+        assert r["c_val"] < 1e-4
