@@ -131,8 +131,16 @@ def distance(a, b):
     return lib().qfso_distance(n, aa.shape[0], ap, bp)
 
 
-def trace_sweeps(n, pairs, init_gates, x, y, m, n_sweeps, beta=0.0, g=1, threads=0):
-    """Fixed-M sweeps without controller.  Returns dict of traces (see qfso.h)."""
+def _kinds(kinds, k):
+    if kinds is None:
+        return None, None
+    kk, kp = _c(np.asarray(kinds).reshape(k), np.int32)
+    return kk, kp
+
+
+def trace_sweeps(n, pairs, init_gates, x, y, m, n_sweeps, beta=0.0, g=1, threads=0, kinds=None):
+    """Fixed-M sweeps without controller.  Returns dict of traces (see qfso.h).
+    kinds: per-gate kind (0 two-qubit variable, 1 fixed, 2 one-qubit variable)."""
     pr, prp = _c(pairs, np.int32)
     k = pr.shape[0]
     ig, igp = _c(init_gates)
@@ -144,12 +152,13 @@ def trace_sweeps(n, pairs, init_gates, x, y, m, n_sweeps, beta=0.0, g=1, threads
     cost = np.zeros((n_sweeps, s))
     sig = np.zeros((n_sweeps, k, s))
     vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)
-    _check(lib().qfso_trace_sweeps(n, k, prp, s, igp, m, xp, yp, ctypes.c_double(beta), n_sweeps, g,
-                                   vp(env), vp(gates), vp(cost), vp(sig), threads), "trace_sweeps")
+    kk, kp = _kinds(kinds, k)
+    _check(lib().qfso_trace_sweeps_kinds(n, k, prp, kp, s, igp, m, xp, yp, ctypes.c_double(beta), n_sweeps, g,
+                                         vp(env), vp(gates), vp(cost), vp(sig), threads), "trace_sweeps")
     return dict(env=env, gates=gates, cost=cost, sigma=sig)
 
 
-def instantiate(n, pairs, x, y, xv, yv, init_gates, params: dict, threads=0):
+def instantiate(n, pairs, x, y, xv, yv, init_gates, params: dict, threads=0, kinds=None):
     pr, prp = _c(pairs, np.int32)
     k = pr.shape[0]
     ig, igp = _c(init_gates)
@@ -166,8 +175,9 @@ def instantiate(n, pairs, x, y, xv, yv, init_gates, params: dict, threads=0):
     out_g = np.zeros((s, k, 4, 4), np.complex128)
     res = (_Result * s)()
     win = ctypes.c_int(-1)
-    _check(lib().qfso_instantiate(n, k, prp, xx.shape[0], xp, yp, v, xvp, yvp, s, igp, ctypes.byref(p),
-                                  out_g.ctypes.data_as(ctypes.c_void_p), res, ctypes.byref(win), threads),
+    kk, kp = _kinds(kinds, k)
+    _check(lib().qfso_instantiate_kinds(n, k, prp, kp, xx.shape[0], xp, yp, v, xvp, yvp, s, igp, ctypes.byref(p),
+                                        out_g.ctypes.data_as(ctypes.c_void_p), res, ctypes.byref(win), threads),
            "instantiate")
     results = [dict(c_train=r.c_train, c_val=r.c_val, sweeps=r.sweeps, restarts=r.restarts,
                     final_m=r.final_m, term=TERM_NAMES.get(r.term, str(r.term))) for r in res]

@@ -114,20 +114,22 @@ void environment(int n, int p0, int p1, int m0, int m1, int mstride, const doubl
 // sigma_j = ||a_j||, X_j = a_j / sigma_j, Y = V.  Columns with
 // sigma_j <= 1e-14 sigma_max are numerically null: X_j is completed by
 // Gram-Schmidt on e_0..e_3 against the other columns (R5).
-int svd4(const cd A_in[16], cd X[16], double sigma[4], cd Y[16]) {
-  cd A[16], V[16];
-  for (int i = 0; i < 16; ++i) { A[i] = A_in[i]; V[i] = (i % 5 == 0) ? cd(1, 0) : cd(0, 0); }
+// D x D (D = 4: two-qubit blocks; D = 2: one-qubit gates, reading R24), row-major.
+template <int D>
+int svd_jacobi(const cd *A_in, cd *X, double *sigma, cd *Y) {
+  cd A[D * D], V[D * D];
+  for (int i = 0; i < D * D; ++i) { A[i] = A_in[i]; V[i] = (i % (D + 1) == 0) ? cd(1, 0) : cd(0, 0); }
   int sweep = 0;
   for (; sweep < 30; ++sweep) {
     bool rotated = false;
-    for (int j = 0; j < 3; ++j)
-      for (int k = j + 1; k < 4; ++k) {
+    for (int j = 0; j < D - 1; ++j)
+      for (int k = j + 1; k < D; ++k) {
         double alpha = 0, beta = 0;
         cd gamma = 0;
-        for (int r = 0; r < 4; ++r) {
-          alpha += std::norm(A[4 * r + j]);
-          beta += std::norm(A[4 * r + k]);
-          gamma += std::conj(A[4 * r + j]) * A[4 * r + k];
+        for (int r = 0; r < D; ++r) {
+          alpha += std::norm(A[D * r + j]);
+          beta += std::norm(A[D * r + k]);
+          gamma += std::conj(A[D * r + j]) * A[D * r + k];
         }
         double ag = std::abs(gamma);
         if (ag == 0.0 || ag <= 1e-15 * std::sqrt(alpha) * std::sqrt(beta)) continue;
@@ -138,54 +140,55 @@ int svd4(const cd A_in[16], cd X[16], double sigma[4], cd Y[16]) {
         double c = 1.0 / std::sqrt(1.0 + t * t);
         double s = c * t;
         // [a_j' a_k'] = [a_j a_k] J,  J = [[c, s e^{i phi}], [-s e^{-i phi}, c]]
-        for (int r = 0; r < 4; ++r) {
-          cd aj = A[4 * r + j], ak = A[4 * r + k];
-          A[4 * r + j] = c * aj - s * std::conj(ph) * ak;
-          A[4 * r + k] = s * ph * aj + c * ak;
-          cd vj = V[4 * r + j], vk = V[4 * r + k];
-          V[4 * r + j] = c * vj - s * std::conj(ph) * vk;
-          V[4 * r + k] = s * ph * vj + c * vk;
+        for (int r = 0; r < D; ++r) {
+          cd aj = A[D * r + j], ak = A[D * r + k];
+          A[D * r + j] = c * aj - s * std::conj(ph) * ak;
+          A[D * r + k] = s * ph * aj + c * ak;
+          cd vj = V[D * r + j], vk = V[D * r + k];
+          V[D * r + j] = c * vj - s * std::conj(ph) * vk;
+          V[D * r + k] = s * ph * vj + c * vk;
         }
       }
     if (!rotated) break;
   }
   double smax = 0;
-  for (int j = 0; j < 4; ++j) {
+  for (int j = 0; j < D; ++j) {
     double nn = 0;
-    for (int r = 0; r < 4; ++r) nn += std::norm(A[4 * r + j]);
+    for (int r = 0; r < D; ++r) nn += std::norm(A[D * r + j]);
     sigma[j] = std::sqrt(nn);
     if (sigma[j] > smax) smax = sigma[j];
   }
-  bool null_col[4];
-  for (int j = 0; j < 4; ++j) {
+  bool null_col[D];
+  for (int j = 0; j < D; ++j) {
     null_col[j] = !(sigma[j] > 1e-14 * smax) || smax == 0.0;
-    for (int r = 0; r < 4; ++r) X[4 * r + j] = null_col[j] ? cd(0, 0) : A[4 * r + j] / sigma[j];
+    for (int r = 0; r < D; ++r) X[D * r + j] = null_col[j] ? cd(0, 0) : A[D * r + j] / sigma[j];
   }
-  // complete null columns: Gram-Schmidt of e_0..e_3 against the filled columns
-  for (int j = 0; j < 4; ++j) {
+  // complete null columns: Gram-Schmidt of e_0..e_{D-1} against the filled columns
+  for (int j = 0; j < D; ++j) {
     if (!null_col[j]) continue;
-    for (int e = 0; e < 4; ++e) {
-      cd v[4];
-      for (int r = 0; r < 4; ++r) v[r] = (r == e) ? cd(1, 0) : cd(0, 0);
+    for (int e = 0; e < D; ++e) {
+      cd v[D];
+      for (int r = 0; r < D; ++r) v[r] = (r == e) ? cd(1, 0) : cd(0, 0);
       for (int pass = 0; pass < 2; ++pass)
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < D; ++q) {
           if (q == j || (null_col[q] && q > j)) continue;
           cd d = 0;
-          for (int r = 0; r < 4; ++r) d += std::conj(X[4 * r + q]) * v[r];
-          for (int r = 0; r < 4; ++r) v[r] -= d * X[4 * r + q];
+          for (int r = 0; r < D; ++r) d += std::conj(X[D * r + q]) * v[r];
+          for (int r = 0; r < D; ++r) v[r] -= d * X[D * r + q];
         }
       double nv = 0;
-      for (int r = 0; r < 4; ++r) nv += std::norm(v[r]);
+      for (int r = 0; r < D; ++r) nv += std::norm(v[r]);
       nv = std::sqrt(nv);
       if (nv > 0.5) {
-        for (int r = 0; r < 4; ++r) X[4 * r + j] = v[r] / nv;
+        for (int r = 0; r < D; ++r) X[D * r + j] = v[r] / nv;
         break;
       }
     }
   }
-  for (int i = 0; i < 16; ++i) Y[i] = V[i];
+  for (int i = 0; i < D * D; ++i) Y[i] = V[i];
   return sweep;
 }
+int svd4(const cd A_in[16], cd X[16], double sigma[4], cd Y[16]) { return svd_jacobi<4>(A_in, X, sigma, Y); }
 
 // P:59-62 with the beta term of P:380-386 (R15: u = the current, old gate):
 // E' = (1 - beta) E + beta u^dag;  E' = X D Y^dag;  u_new = Y X^dag.
@@ -202,6 +205,47 @@ void polar_update(const cd E[16], const cd Gold[16], double beta, cd Gnew[16], d
       Gnew[4 * a + b] = acc;
     }
   if (sig_sum) *sig_sum = sg[0] + sg[1] + sg[2] + sg[3];
+}
+
+// Gate update by kind ("possibly multi-qubit
+// unitary gates", Table 1's U3 + CNOT circuits; readings R24-R25):
+//   kind 0 (two-qubit variable block): polar_update above;
+//   kind 1 (fixed gate, e.g. CNOT): never updated; *sig_sum = Re Tr(E G);
+//   kind 2 (one-qubit variable gate u on the pair's first qubit p0, stored as
+//     the block G = u (x) I on (p0, p1), l = b(p0) + 2 b(p1)): since
+//     Tr(E (u (x) I)) = Tr(E1 u) with E1[a][b] = sum_c E[a + 2c][b + 2c] (the
+//     partial trace over the p1 bit), u_new = Y X^dag from the 2x2 SVD of
+//     E1' = (1 - beta) E1 + beta u_old^dag, and G_new = u_new (x) I exactly.
+enum { KIND_VAR2 = 0, KIND_FIXED = 1, KIND_VAR1 = 2 };
+
+void gate_update(int kind, const cd E[16], const cd Gold[16], double beta, cd Gnew[16], double *sig_sum) {
+  if (kind == KIND_FIXED) {
+    cd tr = 0;
+    for (int a = 0; a < 4; ++a)
+      for (int b = 0; b < 4; ++b) tr += E[4 * a + b] * Gold[4 * b + a];
+    for (int i = 0; i < 16; ++i) Gnew[i] = Gold[i];
+    if (sig_sum) *sig_sum = tr.real();
+    return;
+  }
+  if (kind != KIND_VAR1) {
+    polar_update(E, Gold, beta, Gnew, sig_sum);
+    return;
+  }
+  cd E1[4], X[4], Y[4];
+  double sg[2];
+  for (int a = 0; a < 2; ++a)
+    for (int b = 0; b < 2; ++b) {
+      const cd uo_dag = std::conj(Gold[4 * b + a]);  // u_old^dag[a][b] = conj(u_old[b][a])
+      E1[2 * a + b] = (1.0 - beta) * (E[4 * a + b] + E[4 * (a + 2) + b + 2]) + beta * uo_dag;
+    }
+  svd_jacobi<2>(E1, X, sg, Y);
+  cd u[4];
+  for (int a = 0; a < 2; ++a)
+    for (int b = 0; b < 2; ++b) u[2 * a + b] = Y[2 * a + 0] * std::conj(X[2 * b + 0]) + Y[2 * a + 1] * std::conj(X[2 * b + 1]);
+  for (int lo = 0; lo < 4; ++lo)
+    for (int li = 0; li < 4; ++li)
+      Gnew[4 * lo + li] = ((lo >> 1) == (li >> 1)) ? u[2 * (lo & 1) + (li & 1)] : cd(0, 0);
+  if (sig_sum) *sig_sum = sg[0] + sg[1];
 }
 
 // ------------------------------------------------------------------ cost --
@@ -235,7 +279,7 @@ struct SweepOut {
   double c_train;
 };
 
-void sweep_one(int n, int K, const int32_t *pairs, cd *G /*[K][16] in/out*/, int M,
+void sweep_one(int n, int K, const int32_t *pairs, const int32_t *kinds, cd *G /*[K][16] in/out*/, int M,
                const double *x, const double *y, double beta, int g, SweepOut *out,
                std::vector<double> &Bbuf, std::vector<double> &chi) {
   const long N = 1L << n;
@@ -264,7 +308,7 @@ void sweep_one(int n, int K, const int32_t *pairs, cd *G /*[K][16] in/out*/, int
     for (int q = 0; q < 16; ++q) E[q] = cd((double)Etot[q].real(), (double)Etot[q].imag());
     cd Gn[16], Gd[16];
     double ss = 0;
-    polar_update(E, G + 16 * i, beta, Gn, &ss);
+    gate_update(kinds ? kinds[i] : KIND_VAR2, E, G + 16 * i, beta, Gn, &ss);
     for (int q = 0; q < 16; ++q) G[16 * i + q] = Gn[q];
     if (out) {
       for (int q = 0; q < 16; ++q) out->env[16 * i + q] = E[q];
@@ -286,10 +330,12 @@ double validation_cost(int n, int K, const int32_t *pairs, const cd *G, int V, c
   return (double)(sq_distance_sum(n, 0, V, 1, psi.data(), yv) / (long double)V);
 }
 
-int check_structure(int n, int k, const int32_t *pairs) {
+int check_structure(int n, int k, const int32_t *pairs, const int32_t *kinds = nullptr) {
   if (n < 2 || n > 30 || k < 1 || !pairs) return 1;
-  for (int i = 0; i < k; ++i)
+  for (int i = 0; i < k; ++i) {
     if (!valid_pair(n, pairs[2 * i], pairs[2 * i + 1])) return 1;
+    if (kinds && (kinds[i] < 0 || kinds[i] > 2)) return 1;
+  }
   return 0;
 }
 
@@ -407,7 +453,15 @@ int qfso_trace_sweeps(int n, int k, const int32_t *pairs, int s, const double *i
                       const double *x, const double *y, double beta, int n_sweeps, int g,
                       double *env_trace, double *gate_trace, double *cost_trace,
                       double *sigma_trace, int n_threads) {
-  if (check_structure(n, k, pairs) || s < 1 || m < 1 || m > (1 << n) || !init_gates || !x ||
+  return qfso_trace_sweeps_kinds(n, k, pairs, nullptr, s, init_gates, m, x, y, beta, n_sweeps, g,
+                                 env_trace, gate_trace, cost_trace, sigma_trace, n_threads);
+}
+
+int qfso_trace_sweeps_kinds(int n, int k, const int32_t *pairs, const int32_t *kinds, int s,
+                            const double *init_gates, int m, const double *x, const double *y,
+                            double beta, int n_sweeps, int g, double *env_trace, double *gate_trace,
+                            double *cost_trace, double *sigma_trace, int n_threads) {
+  if (check_structure(n, k, pairs, kinds) || s < 1 || m < 1 || m > (1 << n) || !init_gates || !x ||
       !y || n_sweeps < 0 || g < 1)
     return 1;
 #ifdef _OPENMP
@@ -421,7 +475,7 @@ int qfso_trace_sweeps(int n, int k, const int32_t *pairs, int s, const double *i
     std::vector<double> B, chi;
     SweepOut so;
     for (int t = 0; t < n_sweeps; ++t) {
-      sweep_one(n, k, pairs, G.data(), m, x, y, beta, g, &so, B, chi);
+      sweep_one(n, k, pairs, kinds, G.data(), m, x, y, beta, g, &so, B, chi);
       if (env_trace)
         for (int i = 0; i < k; ++i)
           for (int q = 0; q < 16; ++q) {
@@ -450,8 +504,16 @@ int qfso_instantiate(int n, int k, const int32_t *pairs, int m_pool, const doubl
                      const double *y, int v, const double *xv, const double *yv, int s,
                      const double *init_gates, const qfso_params *p, double *out_gates,
                      qfso_result *out, int *winner, int n_threads) {
+  return qfso_instantiate_kinds(n, k, pairs, nullptr, m_pool, x, y, v, xv, yv, s, init_gates, p,
+                                out_gates, out, winner, n_threads);
+}
+
+int qfso_instantiate_kinds(int n, int k, const int32_t *pairs, const int32_t *kinds, int m_pool,
+                           const double *x, const double *y, int v, const double *xv,
+                           const double *yv, int s, const double *init_gates, const qfso_params *p,
+                           double *out_gates, qfso_result *out, int *winner, int n_threads) {
   const long N = 1L << n;
-  if (check_structure(n, k, pairs) || s < 1 || !p || !init_gates || !x || !y || !out_gates ||
+  if (check_structure(n, k, pairs, kinds) || s < 1 || !p || !init_gates || !x || !y || !out_gates ||
       !out || m_pool < 1 || m_pool > N || p->m_init < 1 || p->m_init > m_pool || v < 0 ||
       (v > 0 && (!xv || !yv)) || p->max_iter < 1)
     return 1;
@@ -483,7 +545,7 @@ int qfso_instantiate(int n, int k, const int32_t *pairs, int m_pool, const doubl
       St &A = S[st];
       if (!A.active) continue;
       SweepOut so;
-      sweep_one(n, k, pairs, A.G.data(), A.M, x, y, p->beta, 1, &so, A.B, A.chi);  // step 1
+      sweep_one(n, k, pairs, kinds, A.G.data(), A.M, x, y, p->beta, 1, &so, A.B, A.chi);  // step 1
       A.c_train = so.c_train;
       A.c_val = v > 0 ? validation_cost(n, k, pairs, A.G.data(), v, xv, yv) : NAN;
     }

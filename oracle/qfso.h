@@ -74,11 +74,24 @@ int qfso_trace_sweeps(int n, int k, const int32_t *pairs, int s, const double *i
                       double *env_trace, double *gate_trace, double *cost_trace,
                       double *sigma_trace, int n_threads);
 
+/* Same with gate kinds (kinds[k]: 0 two-qubit variable block, 1 fixed gate,
+ * 2 one-qubit variable gate u on the pair's first qubit, stored as u (x) I;
+ * NULL = all 0).  SURVEY.md §8(f) NEXT-3; readings R24-R25. */
+int qfso_trace_sweeps_kinds(int n, int k, const int32_t *pairs, const int32_t *kinds, int s,
+                            const double *init_gates, int m, const double *x, const double *y,
+                            double beta, int n_sweeps, int g, double *env_trace, double *gate_trace,
+                            double *cost_trace, double *sigma_trace, int n_threads);
+
 /* Full instantiation with the controller. */
 int qfso_instantiate(int n, int k, const int32_t *pairs, int m_pool, const double *x,
                      const double *y, int v, const double *xv, const double *yv, int s,
                      const double *init_gates, const qfso_params *p, double *out_gates,
                      qfso_result *out, int *winner, int n_threads);
+
+int qfso_instantiate_kinds(int n, int k, const int32_t *pairs, const int32_t *kinds, int m_pool,
+                           const double *x, const double *y, int v, const double *xv,
+                           const double *yv, int s, const double *init_gates, const qfso_params *p,
+                           double *out_gates, qfso_result *out, int *winner, int n_threads);
 
 /* Sweep-throughput timing: n_sweeps sweeps at fixed M; *sec = wall seconds. */
 int qfso_bench_sweeps(int n, int k, const int32_t *pairs, int s, const double *init_gates, int m,

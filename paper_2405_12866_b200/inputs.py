@@ -43,6 +43,7 @@ import numpy as np
 __all__ = [
     "rng_for", "haar_unitary", "haar_states", "brick_pairs", "c4_pairs",
     "apply_circuit_tensor", "warm_gate", "Problem", "make_problem", "CONFIGS",
+    "GATE_VAR2", "GATE_FIXED", "GATE_VAR1", "CNOT", "u3_cnot_template", "u3_cnot_problem",
 ]
 
 
@@ -244,3 +245,68 @@ def make_problem(name: str, init: str = "R", s: int | None = None, m_pool: int |
                   stop_on_first=1)
     return Problem(name=name, n=n, pairs=pairs, target=target, x=x, y=y, xv=xv, yv=yv,
                    init=gates, m_init=mi, params=params)
+
+
+# ------------------------------------------------ U3 + CNOT templates (NEXT-3) --
+# Gate kinds of qfs_set_gate_kinds / the oracle's *_kinds entry points: a
+# two-qubit variable block, a fixed gate, and a one-qubit variable gate u on the
+# pair's first qubit stored as the block u (x) I (readings R24-R25).
+GATE_VAR2, GATE_FIXED, GATE_VAR1 = 0, 1, 2
+
+# CNOT with control p0 and target p1 in the local index l = b(p0) + 2 b(p1):
+# |b0 b1> -> |b0, b1 xor b0>, i.e. l: 0->0, 1->3, 2->2, 3->1; G[l_out][l_in].
+CNOT = np.zeros((4, 4), dtype=np.complex128)
+for _li, _lo in ((0, 0), (1, 3), (2, 2), (3, 1)):
+    CNOT[_lo, _li] = 1.0
+
+
+def u3_cnot_template(n: int, layers: int):
+    """The paper's circuit template (Table 1: U3 + CNOT): on every brick-wall
+    pair (q, q+1) of every layer, a one-qubit variable gate on q, one on q+1,
+    then a fixed CNOT(q -> q+1).  Returns (pairs [K][2], kinds [K])."""
+    pairs, kinds = [], []
+    for layer in range(layers):
+        for q in range(layer % 2, n - 1, 2):
+            pairs += [(q, q + 1), (q + 1, q), (q, q + 1)]
+            kinds += [GATE_VAR1, GATE_VAR1, GATE_FIXED]
+    return np.asarray(pairs, dtype=np.int32), np.asarray(kinds, dtype=np.int32)
+
+
+def _embed1(u: np.ndarray) -> np.ndarray:
+    """u (x) I in the block's local index l = b(p0) + 2 b(p1)."""
+    g = np.zeros((4, 4), dtype=np.complex128)
+    for lo in range(4):
+        for li in range(4):
+            if lo >> 1 == li >> 1:
+                g[lo, li] = u[lo & 1, li & 1]
+    return g
+
+
+def u3_cnot_problem(n: int, layers: int, s: int, m_pool: int, v: int, init: str = "W",
+                    eps: float = 0.3, seed: int = 11) -> tuple:
+    """Solvable U3 + CNOT instance: target = the template with seeded Haar 2x2
+    gates; W initial gates = exp(i eps H) u_target (2x2) per one-qubit slot, the
+    CNOTs as given.  Returns (pairs, kinds, target [K][4][4], x, y, xv, yv, init)."""
+    pairs, kinds = u3_cnot_template(n, layers)
+    k = len(kinds)
+    target = np.stack([_embed1(haar_unitary(rng_for(seed, 0, j), 2)) if kinds[j] == GATE_VAR1 else CNOT
+                       for j in range(k)])
+    x = haar_states(rng_for(seed, 1, 0), n, m_pool)
+    y = apply_circuit_tensor(n, pairs, target, x)
+    xv = haar_states(rng_for(seed, 2, 0), n, v) if v else np.zeros((0, 1 << n), np.complex128)
+    yv = apply_circuit_tensor(n, pairs, target, xv) if v else xv.copy()
+    gates = np.empty((s, k, 4, 4), dtype=np.complex128)
+    for st in range(s):
+        rng = rng_for(seed, 3, st)
+        for j in range(k):
+            if kinds[j] != GATE_VAR1:
+                gates[st, j] = target[j]
+            elif init == "W":
+                a = _complex_gaussian(rng, (2, 2))
+                h = 0.5 * (a + a.conj().T)
+                w, vv = np.linalg.eigh(h)
+                w = w / np.max(np.abs(w))
+                gates[st, j] = _embed1((vv * np.exp(1j * eps * w)[None, :]) @ vv.conj().T @ target[j][:2, :2])
+            else:
+                gates[st, j] = _embed1(haar_unitary(rng, 2))
+    return pairs, kinds, target, x, y, xv, yv, gates

@@ -499,3 +499,74 @@ def test_appendix_d_basis_training_states_blind_to_rz():
         assert r["c_train"] < 1e-5 and r["c_val"] > 0.1
     for r in rh:
         assert r["c_val"] < 1e-4
+
+
+# ------------------------------------------ gate kinds: fixed / one-qubit --
+def test_var1_full_basis_environment_and_one_sweep_solution():
+    """One one-qubit variable gate u on qubit 1 (carrier qubit 2), n = 3, full
+    basis (M = 2^n): the block environment is E = 2^{n-2} (u_t (x) I)^dag, its
+    partial trace over the carrier is E1 = 2^{n-1} u_t^dag (closed form), and one
+    sweep recovers u_t exactly (P:59-62 applied to the 2x2 E1; reading R24)."""
+    n = 3
+    pairs = np.array([[1, 2]], np.int32)
+    kinds = [I.GATE_VAR1]
+    ut = I.haar_unitary(np.random.default_rng(31), 2)
+    tgt = I._embed1(ut)[None]
+    x = np.eye(8, dtype=np.complex128)
+    y = I.apply_circuit_tensor(n, pairs, tgt, x)
+    init = I._embed1(I.haar_unitary(np.random.default_rng(32), 2))[None, None]
+    t = oracle.trace_sweeps(n, pairs, init, x, y, 8, 1, kinds=kinds)
+    E = t["env"][0, 0, 0]
+    assert np.abs(E - 2 * tgt[0].conj().T).max() < 1e-14
+    E1 = np.array([[E[a, b] + E[a + 2, b + 2] for b in range(2)] for a in range(2)])
+    assert np.abs(E1 - 4 * ut.conj().T).max() < 1e-14
+    assert np.abs(t["gates"][0, 0, 0] - tgt[0]).max() < 1e-14
+    assert t["cost"][0, 0] < 1e-28
+    assert abs(t["sigma"][0, 0, 0] - 8.0) < 1e-13   # sum of the singular values of 4 u_t^dag
+
+
+def test_var1_update_is_polar_of_partial_trace_and_fixed_gates_stay():
+    """U3 + CNOT template (Table 1), Haar training states: every one-qubit update
+    is u = Y X^dag of the SVD (LAPACK, test-only) of the partial-traced 2x2
+    environment, embedded as u (x) I with exact zeros; fixed CNOTs are never
+    changed and report sigma = Re Tr(E G); the per-gate cost monitor is
+    non-increasing for the variable gates."""
+    n, layers = 4, 3
+    pairs, kinds, target, x, y, xv, yv, init = I.u3_cnot_problem(n, layers, s=2, m_pool=6, v=0, init="R")
+    t = oracle.trace_sweeps(n, pairs, init, x, y, 6, 2, kinds=kinds)
+    K = len(kinds)
+    gprev = init
+    for sw in range(2):
+        for s in range(2):
+            for i in range(K):
+                E = t["env"][sw, i, s]
+                G = t["gates"][sw, s, i]
+                if kinds[i] == I.GATE_FIXED:
+                    assert np.array_equal(G, I.CNOT)
+                    assert abs(t["sigma"][sw, i, s] - np.trace(E @ G).real) < 1e-12 * np.abs(E).max()
+                    continue
+                E1 = np.array([[E[a, b] + E[a + 2, b + 2] for b in range(2)] for a in range(2)])
+                X, d, Yh = np.linalg.svd(E1)
+                u = Yh.conj().T @ X.conj().T
+                assert np.abs(G - I._embed1(u)).max() < 1e-12
+                assert G[0, 2] == 0 and G[1, 3] == 0 and G[2, 0] == 0 and G[3, 1] == 0
+                assert abs(t["sigma"][sw, i, s] - d.sum()) < 1e-12 * d.sum()
+        gprev = t["gates"][sw]
+    assert np.all(np.diff(t["cost"], axis=0) <= 1e-12)
+
+
+def test_u3_cnot_exact_init_fixed_point_and_warm_convergence():
+    """Exact initialisation is a fixed point (cost ~ 0, gates move <= 1e-13);
+    a warm start converges to c_train <= 1e-8 (solvable by construction)."""
+    n, layers = 5, 4
+    pairs, kinds, target, x, y, xv, yv, init = I.u3_cnot_problem(n, layers, s=2, m_pool=32, v=8, init="W")
+    t = oracle.trace_sweeps(n, pairs, target[None], x, y, 8, 2, kinds=kinds)
+    assert t["cost"].max() < 1e-26
+    assert np.abs(t["gates"][-1, 0] - target).max() < 1e-13
+    prm = dict(dist_tol=1e-8, diff_tol_r=1e-3, plateau_window=5, min_iter=6, max_iter=400, m_init=4,
+               overtrain_ratio=0.1, beta=0.0, stop_on_first=1)
+    g, res, win = oracle.instantiate(n, pairs, x, y, xv, yv, init, prm, kinds=kinds)
+    assert res[win]["term"] == "CONVERGED" and res[win]["c_train"] <= 1e-8
+    for i in range(len(kinds)):
+        if kinds[i] == I.GATE_FIXED:
+            assert np.array_equal(g[win, i], I.CNOT)
