@@ -151,6 +151,22 @@ qfs_status qfs_profile_enable(qfs_ctx *c, int on);
 qfs_status qfs_profile_read(qfs_ctx *c, int cap, const char **names, long long *launches,
                             double *ms, double *bytes, double *flops, int *count);
 
+/* Gate kinds ("possibly multi-qubit
+ * unitary gates", Table 1's U3 + CNOT circuits; readings R24-R25).
+ * Every slot is still a 4x4 block on its pair (p0, p1):
+ *   QFS_GATE_VAR2  two-qubit variable unitary (default): G <- Y X^dag, E = X D Y^dag;
+ *   QFS_GATE_FIXED constant gate (e.g. CNOT): applied, never updated; its sum
+ *                  sigma slot reports Re Tr(E G);
+ *   QFS_GATE_VAR1  one-qubit variable unitary u on p0, stored as u (x) I (p1 is a
+ *                  carrier the block acts trivially on): u <- Y X^dag from the SVD
+ *                  of E1[a][b] = E[a][b] + E[a+2][b+2] (Tr(E (u (x) I)) = Tr(E1 u)).
+ * qfs_set_gate_kinds(c, kinds[k]) sets them (NULL: all QFS_GATE_VAR2);
+ * QFS_ERR_ARG for another value.  Initial gates of QFS_GATE_VAR1 slots must be
+ * of the form u (x) I (else qfs_instantiate / qfs_trace_sweeps return
+ * QFS_ERR_NUMERIC); fixed slots take their constant from the initial gates. */
+enum { QFS_GATE_VAR2 = 0, QFS_GATE_FIXED = 1, QFS_GATE_VAR1 = 2 };
+qfs_status qfs_set_gate_kinds(qfs_ctx *c, const int32_t *kinds);
+
 /* Sweep implementation: 0 = auto (default; cluster-resident
  * whenever a start's states fit in the shared memory of a cluster of <= 16
  * CTAs, else streamed), 1 = streamed (B cache in HBM, one fused launch per

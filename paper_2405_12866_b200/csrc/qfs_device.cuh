@@ -327,5 +327,48 @@ __device__ void hw_polar(double2 e, double2 v0, double2 &g_out, double2 &v_out, 
 #endif
 }
 
+// Gate update by kind (readings R24-R25; the oracle's gate_update):
+//   kind 0: two-qubit variable block, G = polar update of E' (hw_polar);
+//   kind 1: fixed gate: G unchanged, ss = Re Tr(E G);
+//   kind 2: one-qubit variable gate u on the pair's first qubit, stored as
+//           u (x) I: E1[a][b] = E[a][b] + E[a+2][b+2] (partial trace over the
+//           p1 bit), the polar update of E1 (x) I is exactly u_new (x) I (its
+//           two diagonal copies are averaged so the zeros stay exact), ss = sum
+//           of the singular values of E1.
+// Half warp, lane l = 4r + c holds e = E[r][c] (before the beta term); gold is
+// the old gate (row-major, read-only); both halves may hold different matrices
+// but the kind must be warp-uniform.
+__device__ void gate_update(int kind, double2 e, const double2 *gold, double beta, double2 v0, double2 &g,
+                            double2 &v, double &ss, double2 *scratch) {
+  const int lane = threadIdx.x & 31, hb = lane & 16, l = lane & 15, r = l >> 2, c = l & 3;
+  if (kind == 1) {
+    g = gold[l];
+    v = v0;
+    const double2 gt = gold[4 * c + r];  // G[c][r]
+    ss = half_sum(e.x * gt.x - e.y * gt.y);
+    return;
+  }
+  const bool blk = (r >> 1) == (c >> 1);
+  if (kind == 2) {
+    const double2 ea = shfl_c(e, hb | (4 * (r & 1) + (c & 1)));
+    const double2 eb = shfl_c(e, hb | (4 * ((r & 1) + 2) + (c & 1) + 2));
+    e = blk ? make_double2(ea.x + eb.x, ea.y + eb.y) : make_double2(0.0, 0.0);
+    if (beta != 0.0 && blk) {  // (1 - beta) E1 + beta u_old^dag, u_old^dag[a][b] = conj(u_old[b][a])
+      const double2 go = gold[4 * (c & 1) + (r & 1)];
+      e = make_double2((1.0 - beta) * e.x + beta * go.x, (1.0 - beta) * e.y - beta * go.y);
+    }
+  } else if (beta != 0.0) {  // E' = (1 - beta) E + beta G_old^dag
+    const double2 go = gold[4 * c + r];  // (G^dag)[r][c] = conj(G[c][r])
+    e = make_double2((1.0 - beta) * e.x + beta * go.x, (1.0 - beta) * e.y - beta * go.y);
+  }
+  hw_polar(e, v0, g, v, ss, scratch);
+  if (kind == 2) {
+    const double2 ga = shfl_c(g, hb | (4 * (r & 1) + (c & 1)));
+    const double2 gb = shfl_c(g, hb | (4 * ((r & 1) + 2) + (c & 1) + 2));
+    g = blk ? make_double2(0.5 * (ga.x + gb.x), 0.5 * (ga.y + gb.y)) : make_double2(0.0, 0.0);
+    ss *= 0.5;
+  }
+}
+
 }  // namespace
 }  // namespace qfs

@@ -49,6 +49,7 @@ struct BwdParams {
   const GateDesc *desc;       // persistent kernel: [K] (device)
   const double2 *gates;       // [S][K][16]
   double2 *gates_w;           // same array (written by the polar step)
+  const int *kinds;           // [K] gate kinds (0 two-qubit variable, 1 fixed, 2 one-qubit), or nullptr
   double2 *vprev;             // [S][K][16] right singular vectors (warm start) or nullptr
   double *partials;           // [S_act][nb][32]
   unsigned *counters;         // [S_act]
@@ -72,6 +73,7 @@ struct BwdParams {
 struct PolarParams {
   int K, gate, S, n_slots;
   const Slot *slots;
+  const int *kinds;           // [K] or nullptr
   const double *e_red;        // [S_act][32]
   double2 *gates;             // [S][K][16]
   double2 *vprev;             // [S][K][16] or nullptr
@@ -141,6 +143,7 @@ struct ResParams {
   int n_slots;
   const Slot *slots;
   const int2 *pairs;          // [K]
+  const int *kinds;           // [K] gate kinds, or nullptr
   double2 *gates;             // [S][K][16]: old gates in, new gates out
   const double2 *x, *y;       // pools, sample-minor [2^n][m_pool]
   long long m_pool;

@@ -47,22 +47,19 @@ constexpr int RED_THREADS = 256;
 
 
 // Polar step of one start by one warp (lanes 16-31 mirror lanes 0-15):
-// E' = (1 - beta) E + beta G_old^dag; writes G_i, V_i, sum sigma, E trace.
-__device__ void polar_write(const double *e32, double2 *gout, double2 *vslot, double beta,
+// the kind-aware update of gate_update (E' = (1 - beta) E + beta G_old^dag for
+// variable gates); writes G_i, V_i, sum sigma, E trace.
+__device__ void polar_write(const double *e32, double2 *gout, double2 *vslot, double beta, int kind,
                             double *sig_out, double2 *env_out, double2 *scratch) {
   const int lane = threadIdx.x & 31, l = lane & 15;
-  double2 e = make_double2(e32[2 * l], e32[2 * l + 1]);
+  const double2 e = make_double2(e32[2 * l], e32[2 * l + 1]);
   if (env_out && lane < 16) env_out[l] = e;
-  if (beta != 0.0) {
-    const double2 go = gout[4 * (l & 3) + (l >> 2)];  // (G^dag)[r][j] = conj(G[j][r])
-    e = make_double2((1.0 - beta) * e.x + beta * go.x, (1.0 - beta) * e.y - beta * go.y);
-  }
   const double2 v0 = vslot ? vslot[l] : make_double2((l % 5 == 0) ? 1.0 : 0.0, 0.0);
   double2 g, v;
   double ss;
-  hw_polar(e, v0, g, v, ss, scratch + (lane & 16));
+  gate_update(kind, e, gout, beta, v0, g, v, ss, scratch + (lane & 16));
   __syncwarp();
-  if (lane < 16) {
+  if (lane < 16 && kind != 1) {
     gout[l] = g;
     if (vslot) vslot[l] = v;
   }
@@ -381,7 +378,7 @@ __device__ void bwd_finish(const BwdParams &P, const GateDesc &G, int jslot, int
   if (!P.fuse_polar) return;
   const long long gi = (long long)s * P.K + G.env_gate;
   polar_write(sh.sum32, P.gates_w + gi * 16, P.vprev ? P.vprev + gi * 16 : nullptr, P.beta,
-              P.sig ? P.sig + gi : nullptr,
+              P.kinds ? P.kinds[G.env_gate] : 0, P.sig ? P.sig + gi : nullptr,
               P.env_trace ? P.env_trace + ((long long)G.env_gate * P.S + s) * 16 : nullptr, sh.scratch);
   if (P.dbg && threadIdx.x == 0) atomicMax(P.dbg + 4 * G.env_gate + 3, gtimer());
 }
@@ -520,7 +517,7 @@ __global__ void polar_kernel(const PolarParams P) {
   __syncwarp();
   const long long gi = (long long)sl.s * P.K + P.gate;
   polar_write(e32[w], P.gates + gi * 16, P.vprev ? P.vprev + gi * 16 : nullptr, P.beta,
-              P.sig ? P.sig + gi : nullptr,
+              P.kinds ? P.kinds[P.gate] : 0, P.sig ? P.sig + gi : nullptr,
               P.env_trace ? P.env_trace + ((long long)P.gate * P.S + sl.s) * 16 : nullptr, scratch[w]);
 }
 

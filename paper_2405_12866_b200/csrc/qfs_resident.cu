@@ -260,17 +260,15 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
         double2 ev = make_double2(__shfl_sync(FULL, e, 2 * l), __shfl_sync(FULL, e, 2 * l + 1));
         double2 *gi = sm.G + 16 * i;
         if (P.env_trace && rank == 0 && lane < 16) P.env_trace[((long long)i * P.S + s) * 16 + l] = ev;
-        if (P.beta != 0.0) {  // E' = (1 - beta) E + beta G_old^dag
-          const double2 go = gi[4 * (l & 3) + (l >> 2)];
-          ev = make_double2((1.0 - P.beta) * ev.x + P.beta * go.x, (1.0 - P.beta) * ev.y - P.beta * go.y);
-        }
+        const int kind = P.kinds ? P.kinds[i] : 0;
         double2 g, v;
         double ss;
-        hw_polar(ev, make_double2((l % 5 == 0) ? 1.0 : 0.0, 0.0), g, v, ss, sm.scr + (lane & 16));
+        gate_update(kind, ev, gi, P.beta, make_double2((l % 5 == 0) ? 1.0 : 0.0, 0.0), g, v, ss,
+                    sm.scr + (lane & 16));
         __syncwarp();
-        if (lane < 16) gi[l] = g;
+        if (lane < 16 && kind != 1) gi[l] = g;
         if (rank == 0) {
-          if (lane < 16) gglob[16 * i + l] = g;
+          if (lane < 16 && kind != 1) gglob[16 * i + l] = g;
           if (lane == 0 && P.sig) P.sig[(long long)s * K + i] = ss;
         }
         stamp(4);  // [4] polar

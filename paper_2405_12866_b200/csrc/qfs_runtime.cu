@@ -51,6 +51,8 @@ struct qfs_ctx {
   long long N = 0;
   std::vector<int32_t> pairs;
   int2 *d_pairs = nullptr;
+  std::vector<int32_t> kinds;  // gate kinds (qfs_set_gate_kinds), default all QFS_GATE_VAR2
+  int *d_kinds = nullptr;
   cudaStream_t st = nullptr;
   cudaStream_t cur_st = nullptr;       // stream of the launches being issued
   // lockstep start groups on parallel streams (one group's polar tail overlaps
@@ -483,7 +485,7 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
   if (res_plan(c, M_max, ns, pl)) {
     // whole sweep + costs + validation in one cluster-resident launch
     ResParams r{};
-    r.n = n; r.K = K; r.S = sp.S; r.C = pl.C; r.ld = pl.ld; r.n_slots = ns;
+    r.n = n; r.K = K; r.S = sp.S; r.C = pl.C; r.ld = pl.ld; r.n_slots = ns; r.kinds = c->d_kinds;
     r.slots = c->d_slots + j0; r.pairs = c->d_pairs; r.gates = c->d_gates;
     r.x = c->d_x; r.y = c->d_y; r.m_pool = c->m_pool; r.xv = c->d_xv; r.yv = c->d_yv;
     r.V = c->V; r.want_val = sp.want_val ? 1 : 0; r.beta = sp.beta;
@@ -565,6 +567,7 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
   // (b, c) backward: gate i = K-1 .. 0 (P:112 right to left; Fig. env_calc)
   BwdParams b{};
   b.n = n; b.K = K; b.S = sp.S; b.slots = slots; b.gates = c->d_gates; b.gates_w = c->d_gates;
+  b.kinds = c->d_kinds;
   b.partials = partials; b.counters = cnt_b; b.e_red = ered;
   b.fuse_polar = (c->mode == 1 && c->world > 1) ? 0 : 1;
   b.beta = sp.beta; b.sig = c->d_sig; b.env_trace = sp.env_trace;
@@ -613,7 +616,7 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
                                   c->comm, st));
       }
       PolarParams pp{};
-      pp.K = K; pp.gate = i; pp.S = sp.S; pp.n_slots = ns; pp.slots = slots;
+      pp.K = K; pp.gate = i; pp.S = sp.S; pp.n_slots = ns; pp.slots = slots; pp.kinds = c->d_kinds;
       pp.e_red = ered; pp.gates = c->d_gates; pp.beta = sp.beta; pp.sig = c->d_sig;
       pp.env_trace = sp.env_trace; pp.vprev = c->d_vprev;
       LaunchScope ls(c, K_POLAR, 0, 0);
@@ -769,6 +772,24 @@ qfs_status run_sweep(qfs_ctx *c, const SweepSpec &sp, std::vector<double> &csum,
 qfs_status upload_gates(qfs_ctx *c, int s, const double *init) {
   if (!finite_all(init, (size_t)s * c->K * 32)) return fail(c, QFS_ERR_NUMERIC, "non-finite initial gate");
   if (!unitary_all(init, (size_t)s * c->K)) return fail(c, QFS_ERR_NUMERIC, "initial gate not unitary (tol 1e-10)");
+  // one-qubit variable slots must hold u (x) I: zero off the two diagonal 2x2
+  // blocks (local index l = b(p0) + 2 b(p1)), equal blocks (tol 1e-10)
+  for (int st = 0; st < s; ++st)
+    for (int k = 0; k < c->K; ++k) {
+      if (c->kinds[k] != QFS_GATE_VAR1) continue;
+      const double *g = init + ((size_t)st * c->K + k) * 32;
+      for (int lo = 0; lo < 4; ++lo)
+        for (int li = 0; li < 4; ++li) {
+          const double *e = g + 2 * (4 * lo + li);
+          bool ok;
+          if ((lo >> 1) != (li >> 1)) ok = std::fabs(e[0]) <= 1e-10 && std::fabs(e[1]) <= 1e-10;
+          else {
+            const double *f = g + 2 * (4 * (lo ^ 2) + (li ^ 2));  // same entry of the other block
+            ok = std::fabs(e[0] - f[0]) <= 1e-10 && std::fabs(e[1] - f[1]) <= 1e-10;
+          }
+          if (!ok) return fail(c, QFS_ERR_NUMERIC, "one-qubit gate slot is not of the form u (x) I (tol 1e-10)");
+        }
+    }
   CUDA_TRY(c, cudaMemcpyAsync(c->d_gates, init, (size_t)s * c->K * 16 * sizeof(double2),
                               cudaMemcpyHostToDevice, c->st));
   CUDA_TRY(c, launch_identity_fill(c->d_vprev, (long long)s * c->K, c->st));
@@ -799,6 +820,9 @@ qfs_status create_common(int n, int k, const int32_t *pairs, int device, qfs_ctx
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_pairs, k * sizeof(int2));
   if (e == cudaSuccess) e = cudaMemcpy(c->d_pairs, pairs, k * sizeof(int2), cudaMemcpyHostToDevice);
+  c->kinds.assign(k, QFS_GATE_VAR2);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_kinds, k * sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(c->d_kinds, 0, k * sizeof(int));
   if (e == cudaSuccess) e = cudaMalloc(&c->d_flag, 4 * sizeof(int));
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
   for (int g = 0; g < qfs_ctx::GMAX && e == cudaSuccess; ++g) {
@@ -1267,6 +1291,21 @@ qfs_status qfs_profile_read(qfs_ctx *c, int cap, const char **names, long long *
 
 long long qfs_launch_count(const qfs_ctx *c) { return c ? c->launches : 0; }
 
+qfs_status qfs_set_gate_kinds(qfs_ctx *c, const int32_t *kinds) {
+  if (!c) return QFS_ERR_ARG;
+  std::vector<int32_t> k(c->K, QFS_GATE_VAR2);
+  if (kinds)
+    for (int i = 0; i < c->K; ++i) {
+      if (kinds[i] < QFS_GATE_VAR2 || kinds[i] > QFS_GATE_VAR1)
+        return fail(c, QFS_ERR_ARG, "gate kind must be 0 (two-qubit variable), 1 (fixed) or 2 (one-qubit variable)");
+      k[i] = kinds[i];
+    }
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaMemcpy(c->d_kinds, k.data(), k.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  c->kinds.swap(k);
+  return QFS_OK;
+}
+
 qfs_status qfs_set_path(qfs_ctx *c, int path) {
   if (!c) return QFS_ERR_ARG;
   if (path < 0 || path > 2) return fail(c, QFS_ERR_ARG, "path must be 0 (auto), 1 (streamed) or 2 (resident)");
@@ -1300,7 +1339,7 @@ void qfs_destroy(qfs_ctx *c) {
   prof_collect(c);
   drop_graph(c);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
-  dfree(c->d_pairs); dfree(c->d_flag); dfree(c->d_x); dfree(c->d_y); dfree(c->d_xv); dfree(c->d_yv);
+  dfree(c->d_pairs); dfree(c->d_kinds); dfree(c->d_flag); dfree(c->d_x); dfree(c->d_y); dfree(c->d_xv); dfree(c->d_yv);
   dfree(c->d_gates); dfree(c->d_chi); dfree(c->d_B); dfree(c->d_vb0); dfree(c->d_vb1);
   dfree(c->d_partials); dfree(c->d_ered); dfree(c->d_sig); dfree(c->d_csum); dfree(c->d_rowout);
   dfree(c->d_cval); dfree(c->d_counters); dfree(c->d_slots); dfree(c->d_env_trace);

@@ -21,7 +21,7 @@ STATUS = {0: "QFS_OK", 1: "QFS_ERR_ARG", 2: "QFS_ERR_CAPACITY", 3: "QFS_ERR_NUME
 TERM_NAMES = {0: "CONVERGED", 1: "PLATEAU", 2: "MAX_ITER", 3: "POOL_EXHAUSTED", 4: "STOPPED"}
 SYMBOLS = ["qfs_create", "qfs_create_dist", "qfs_nccl_unique_id", "qfs_create_nccl", "qfs_set_samples", "qfs_set_samples_device",
            "qfs_instantiate", "qfs_trace_sweeps", "qfs_bench_sweeps", "qfs_op_apply",
-           "qfs_op_environment", "qfs_op_polar", "qfs_profile_enable", "qfs_profile_read", "qfs_set_path",
+           "qfs_op_environment", "qfs_op_polar", "qfs_profile_enable", "qfs_profile_read", "qfs_set_path", "qfs_set_gate_kinds",
            "qfs_launch_count", "qfs_stream", "qfs_last_error", "qfs_destroy"]
 
 
@@ -78,6 +78,7 @@ def load(path: str = LIB_PATH):
         lib.qfs_op_polar.argtypes = [vp, ip, vp, vp, dp, vp, vp]
         lib.qfs_profile_enable.argtypes = [vp, ip]
         lib.qfs_set_path.argtypes = [vp, ip]
+        lib.qfs_set_gate_kinds.argtypes = [vp, vp]
         lib.qfs_profile_read.argtypes = [vp, ip, vp, vp, vp, vp, vp, ctypes.POINTER(ip)]
         for name in SYMBOLS:
             if name not in ("qfs_last_error", "qfs_launch_count", "qfs_stream", "qfs_destroy"):
@@ -246,6 +247,14 @@ class Context:
                                               _ptr(by), _ptr(fl), ctypes.byref(cnt)))
         return {names[i].decode(): dict(launches=int(la[i]), ms=float(ms[i]), bytes=float(by[i]),
                                         flops=float(fl[i])) for i in range(cnt.value)}
+
+    def set_gate_kinds(self, kinds=None):
+        """Per-gate kinds: 0 two-qubit variable, 1 fixed, 2 one-qubit variable (u (x) I)."""
+        if kinds is None:
+            self._check(self.lib.qfs_set_gate_kinds(self.h, None))
+            return
+        k = np.ascontiguousarray(np.asarray(kinds, dtype=np.int32))
+        self._check(self.lib.qfs_set_gate_kinds(self.h, _ptr(k)))
 
     def set_path(self, path):
         """'auto' | 'streamed' | 'resident' (qfs_set_path)."""

@@ -384,3 +384,41 @@ def test_appendix_d_basis_vs_haar_training_states(qfs, path):
                 assert abs(a["c_train"] - b["c_train"]) <= 1e-3 * b["c_train"] + 1e-14
             else:
                 assert a["c_train"] < 1e-5 and a["c_val"] > 0.1
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_u3_cnot_template_gate_kinds(qfs, path):
+    """NEXT-3: the paper's U3 + CNOT templates (Table 1) through qfs_set_gate_kinds:
+    one-qubit variable gates (u (x) I, 2x2 polar of the partial-traced
+    environment) and fixed CNOTs; 4-sweep traces equal the oracle's, a warm
+    instance converges with the CNOTs untouched, bad kinds / non-u(x)I slots fail."""
+    from paper_2405_12866_b200.qfs import QfsError
+    n, layers = 6, 4
+    pairs, kinds, target, x, y, xv, yv, init = I.u3_cnot_problem(n, layers, s=3, m_pool=64, v=16, init="R")
+    ctx = _ctx(qfs, n, pairs, path)
+    ctx.set_gate_kinds(kinds)
+    ctx.set_samples(x, y, xv, yv)
+    gt = ctx.trace_sweeps(init, 8, 4)
+    ot = oracle.trace_sweeps(n, pairs, init, x, y, 8, 4, kinds=kinds)
+    _compare_traces(gt, ot, f"u3cnot-{path}")
+    fixed = np.nonzero(kinds == I.GATE_FIXED)[0]
+    assert np.array_equal(gt["gates"][:, :, fixed], np.broadcast_to(I.CNOT, gt["gates"][:, :, fixed].shape))
+    pw = I.u3_cnot_problem(n, layers, s=4, m_pool=64, v=16, init="W")
+    ctx.set_samples(pw[3], pw[4], pw[5], pw[6])
+    prm = dict(dist_tol=1e-8, diff_tol_r=1e-3, plateau_window=5, min_iter=6, max_iter=300, m_init=8,
+               overtrain_ratio=0.1, beta=0.0, stop_on_first=1)
+    g1, r1, w1 = ctx.instantiate(pw[7], prm)
+    g2, r2, w2 = oracle.instantiate(n, pairs, pw[3], pw[4], pw[5], pw[6], pw[7], prm, kinds=kinds)
+    assert r1[w1]["term"] == "CONVERGED" and r1[w1]["c_train"] <= 1e-8 and w1 == w2
+    for a, b in zip(r1, r2):
+        assert a["term"] == b["term"] and abs(a["sweeps"] - b["sweeps"]) <= 2
+    assert np.array_equal(g1[w1][fixed], np.broadcast_to(I.CNOT, g1[w1][fixed].shape))
+    with pytest.raises(QfsError) as ei:
+        ctx.set_gate_kinds(np.full(len(kinds), 7))
+    assert ei.value.status == 1
+    bad = pw[7].copy()
+    j = int(np.nonzero(kinds == I.GATE_VAR1)[0][0])
+    bad[0, j] = I.haar_unitary(np.random.default_rng(3))   # a general 4x4 in a one-qubit slot
+    with pytest.raises(QfsError) as ei:
+        ctx.instantiate(bad, prm)
+    assert ei.value.status == 3
