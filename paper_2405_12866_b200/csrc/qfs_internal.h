@@ -53,6 +53,8 @@ struct BwdParams {
   double2 *vprev;             // [S][K][16] right singular vectors (warm start) or nullptr
   double *partials;           // [S_act][nb][32]
   unsigned *counters;         // [S_act]
+  unsigned *counters1;        // [S_act][40] first-level group tickets (two-level reduction), or nullptr
+  double *gpartials;          // [S_act][40][32] group sums
   double *e_red;              // [S_act][32]: reduced E (sample mode: before all-reduce)
   int fuse_polar;             // 1: the last CTA of each start runs the polar update
   double beta;

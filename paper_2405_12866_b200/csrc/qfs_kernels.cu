@@ -44,6 +44,8 @@ constexpr int FWD_THREADS = 256;
 constexpr int FWD_STAGES = 4;   // LDGSTS pipeline depth of the forward kernel
 constexpr int VAL_THREADS = 512;
 constexpr int RED_THREADS = 256;
+constexpr int RED_GS = 16;    // CTAs per first-level group of the backward reduction
+constexpr int RED_GMAX = 40;  // >= ceil(max CTAs per start (148 * 4) / RED_GS)
 
 
 // Polar step of one start by one warp (lanes 16-31 mirror lanes 0-15):
@@ -359,18 +361,28 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
 
 // Warp 0 of the last CTA of a start: sum the CTA partials in CTA order, and
 // (fuse_polar) run the polar update of gate i.
+__device__ void bwd_finish_e(const BwdParams &P, const GateDesc &G, int jslot, int s, BwdShared &sh, double e);
 __device__ void bwd_finish(const BwdParams &P, const GateDesc &G, int jslot, int s, BwdShared &sh) {
   if (P.dbg && threadIdx.x == 0) atomicMax(P.dbg + 4 * G.env_gate + 1, gtimer());
   const double *pp = P.partials + (long long)jslot * P.nb * 32 + threadIdx.x;
   double e = 0.0;
-  for (int b0 = 0; b0 < P.nb; b0 += 16) {  // 16 loads in flight, adds in CTA order
-    double xb[16];
+  // 48 loads in flight per lane, adds in CTA order: one L2 round trip per 48
+  // CTAs (at C5, S = 1, nb = 148: 4 round trips instead of 10 with 16)
+  constexpr int FLIGHT = 48;
+  for (int b0 = 0; b0 < P.nb; b0 += FLIGHT) {
+    double xb[FLIGHT];
 #pragma unroll
-    for (int q = 0; q < 16; ++q) xb[q] = b0 + q < P.nb ? __ldcg(pp + (long long)(b0 + q) * 32) : 0.0;
+    for (int q = 0; q < FLIGHT; ++q) xb[q] = b0 + q < P.nb ? __ldcg(pp + (long long)(b0 + q) * 32) : 0.0;
 #pragma unroll
-    for (int q = 0; q < 16; ++q)
+    for (int q = 0; q < FLIGHT; ++q)
       if (b0 + q < P.nb) e += xb[q];
   }
+  bwd_finish_e(P, G, jslot, s, sh, e);
+}
+
+// Warp 0 of the finishing CTA holds the reduced E (lane = re/im of entry lane/2):
+// store it and (fuse_polar) run the gate update.
+__device__ void bwd_finish_e(const BwdParams &P, const GateDesc &G, int jslot, int s, BwdShared &sh, double e) {
   sh.sum32[threadIdx.x] = e;
   if (!P.fuse_polar) P.e_red[(long long)jslot * 32 + threadIdx.x] = e;
   __syncwarp();
@@ -392,8 +404,39 @@ __global__ void __launch_bounds__(BWD_THREADS, QFS_BWD_MINB) bwd_kernel(const Bw
   const Slot sl = P.slots[jslot];
   if (!bwd_gate_partial<NU, TP0, TP1, UPD>(P, P.g, jslot, sl.s, (unsigned)sl.m, false, sh, stage_buf))
     return;
-  if (!warp0_elect_last(&P.counters[jslot], (unsigned)P.nb)) return;
-  bwd_finish(P, P.g, jslot, sl.s, sh);
+  const int ng = (P.nb + RED_GS - 1) / RED_GS;
+  if (ng <= 1 || !P.counters1) {
+    if (!warp0_elect_last(&P.counters[jslot], (unsigned)P.nb)) return;
+    bwd_finish(P, P.g, jslot, sl.s, sh);
+    return;
+  }
+  // two-level ordered reduction of the CTA partials (many CTAs per start, e.g.
+  // S = 1): the last CTA of each group of RED_GS CTAs sums its group in CTA
+  // order, the last group to finish sums the group sums in group order — two
+  // L2 round trips on the critical path instead of nb / 48
+  const int lane = threadIdx.x;
+  const int g = blockIdx.x / RED_GS, g0 = g * RED_GS, gsz = min(RED_GS, P.nb - g0);
+  if (!warp0_elect_last(&P.counters1[jslot * RED_GMAX + g], (unsigned)gsz)) return;
+  if (P.dbg && lane == 0) atomicMax(P.dbg + 4 * P.g.env_gate + 1, gtimer());
+  const double *pp = P.partials + ((long long)jslot * P.nb + g0) * 32 + lane;
+  double xb[RED_GS];
+#pragma unroll
+  for (int q = 0; q < RED_GS; ++q) xb[q] = q < gsz ? __ldcg(pp + (long long)q * 32) : 0.0;
+  double e = 0.0;
+#pragma unroll
+  for (int q = 0; q < RED_GS; ++q)
+    if (q < gsz) e += xb[q];
+  P.gpartials[((long long)jslot * RED_GMAX + g) * 32 + lane] = e;
+  if (!warp0_elect_last(&P.counters[jslot], (unsigned)ng)) return;
+  const double *gp = P.gpartials + (long long)jslot * RED_GMAX * 32 + lane;
+  double yb[RED_GMAX];
+#pragma unroll
+  for (int q = 0; q < RED_GMAX; ++q) yb[q] = q < ng ? __ldcg(gp + (long long)q * 32) : 0.0;
+  e = 0.0;
+#pragma unroll
+  for (int q = 0; q < RED_GMAX; ++q)
+    if (q < ng) e += yb[q];
+  bwd_finish_e(P, P.g, jslot, sl.s, sh, e);
 }
 
 template <int NU, int TP0, int TP1, bool UPD>

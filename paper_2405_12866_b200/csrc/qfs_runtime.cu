@@ -78,6 +78,8 @@ struct qfs_ctx {
   double *d_partials = nullptr, *d_ered = nullptr, *d_sig = nullptr, *d_csum = nullptr,
          *d_rowout = nullptr, *d_cval = nullptr;
   unsigned *d_counters = nullptr;
+  unsigned *d_counters1 = nullptr;   // [S][40] group tickets of the two-level backward reduction
+  double *d_gpart = nullptr;         // [S][40][32] group sums
   Slot *d_slots = nullptr;
   double *h_csum = nullptr, *h_cval = nullptr;  // pinned
   double2 *d_env_trace = nullptr;
@@ -324,6 +326,7 @@ qfs_status ensure_state(qfs_ctx *c, int S, int M, int V) {
   dfree(c->d_partials); dfree(c->d_ered); dfree(c->d_sig); dfree(c->d_csum); dfree(c->d_rowout);
   dfree(c->d_cval); dfree(c->d_counters); dfree(c->d_slots);
   dfree(c->d_flags); dfree(c->d_counters2); dfree(c->d_partials2);
+  dfree(c->d_counters1); dfree(c->d_gpart);
   if (c->h_csum) cudaFreeHost(c->h_csum);
   if (c->h_cval) cudaFreeHost(c->h_cval);
   c->h_csum = c->h_cval = nullptr;
@@ -354,6 +357,9 @@ qfs_status ensure_state(qfs_ctx *c, int S, int M, int V) {
   CUDA_TRY(c, cudaMalloc(&c->d_counters, (size_t)S * 2 * sizeof(unsigned)));
   CUDA_TRY(c, cudaMemset(c->d_counters, 0, (size_t)S * 2 * sizeof(unsigned)));
   CUDA_TRY(c, cudaMalloc(&c->d_slots, (size_t)S * sizeof(Slot)));
+  CUDA_TRY(c, cudaMalloc(&c->d_counters1, (size_t)S * 40 * sizeof(unsigned)));
+  CUDA_TRY(c, cudaMemset(c->d_counters1, 0, (size_t)S * 40 * sizeof(unsigned)));
+  CUDA_TRY(c, cudaMalloc(&c->d_gpart, (size_t)S * 40 * 32 * sizeof(double)));
   CUDA_TRY(c, cudaMalloc(&c->d_flags, (size_t)S * sizeof(unsigned)));
   CUDA_TRY(c, cudaMalloc(&c->d_counters2, (size_t)S * sizeof(unsigned)));
   CUDA_TRY(c, cudaMemset(c->d_counters2, 0, (size_t)S * sizeof(unsigned)));
@@ -569,6 +575,7 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
   b.n = n; b.K = K; b.S = sp.S; b.slots = slots; b.gates = c->d_gates; b.gates_w = c->d_gates;
   b.kinds = c->d_kinds;
   b.partials = partials; b.counters = cnt_b; b.e_red = ered;
+  b.counters1 = c->d_counters1 + (long long)j0 * 40; b.gpartials = c->d_gpart + (long long)j0 * 40 * 32;
   b.fuse_polar = (c->mode == 1 && c->world > 1) ? 0 : 1;
   b.beta = sp.beta; b.sig = c->d_sig; b.env_trace = sp.env_trace;
   b.vprev = c->d_vprev;
@@ -1344,7 +1351,7 @@ void qfs_destroy(qfs_ctx *c) {
   dfree(c->d_partials); dfree(c->d_ered); dfree(c->d_sig); dfree(c->d_csum); dfree(c->d_rowout);
   dfree(c->d_cval); dfree(c->d_counters); dfree(c->d_slots); dfree(c->d_env_trace);
   dfree(c->d_stage); dfree(c->d_vprev); dfree(c->d_desc);
-  dfree(c->d_flags); dfree(c->d_counters2); dfree(c->d_partials2);
+  dfree(c->d_flags); dfree(c->d_counters2); dfree(c->d_partials2); dfree(c->d_counters1); dfree(c->d_gpart);
   if (c->h_csum) cudaFreeHost(c->h_csum);
   if (c->h_cval) cudaFreeHost(c->h_cval);
   for (int g = 0; g < qfs_ctx::GMAX; ++g) {
