@@ -192,7 +192,9 @@ size_t res_smem_limit(int minb);  // per-CTA limit when minb CTAs share an SM
 int resident_max_clusters(int C, size_t smem); // co-resident clusters of C CTAs (0: cannot launch)
 cudaError_t launch_resident(const ResParams &p, int clusters, cudaStream_t st);
 size_t val_blk_smem(int n, int K, int ld);     // shared memory of the block validation kernel
-cudaError_t launch_val_block(const ValRowParams &p, int n_slots, cudaStream_t st);        // largest n the shared-memory validation forward supports
+cudaError_t launch_val_block(const ValRowParams &p, int n_slots, cudaStream_t st);
+size_t val_cl_smem(int n, int K, int t);      // cluster validation, 2^t CTAs per row
+cudaError_t launch_val_cluster(const ValRowParams &p, int n_slots, cudaStream_t st);        // largest n the shared-memory validation forward supports
 int blocks_per_sm(int nu);  // resident CTAs per SM of the backward kernel
 
 }  // namespace qfs

@@ -430,7 +430,148 @@ __global__ void __launch_bounds__(RES_THREADS, 2) val_blk_kernel(const ValRowPar
   }
 }
 
+// st.shared::cluster of a complex value into CTA `rank` at the same offset
+__device__ __forceinline__ void st_remote_c(double2 *p, unsigned rank, double2 v) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+  unsigned ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(ra), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ double2 ld_remote_c(const double2 *p, unsigned rank) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+  unsigned ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  double2 v;
+  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(ra) : "memory");
+  return v;
+}
+__device__ __forceinline__ void cl_sync() {
+  cl_arrive();
+  cl_wait();
+}
+
+// Validation for rows too large for one CTA (n = 14: 256 KB): a cluster of C =
+// 2^t CTAs holds one row, CTA c the amplitudes whose top t qubits read c.  A
+// gate off the top qubits is applied by each CTA to its slice (the block
+// routine with n-t local qubits); a gate touching a top qubit is applied to
+// quadruples split evenly between the CTAs, members read / written locally or
+// over DSMEM, between cluster barriers.  Then each row's ||C xv - yv||^2
+// (slices summed in rank order) goes to row_out[j][row].
+__global__ void __launch_bounds__(RES_THREADS, 1) val_cl_kernel(const ValRowParams P, int t) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double red[RES_WARPS];
+  __shared__ double half_sum_v;
+  const int K = P.K, n = P.n;
+  const unsigned C = 1u << t, NH = 1u << (n - t), top = (unsigned)(n - t);
+  double2 *G = (double2 *)smem_raw;
+  int2 *pr = (int2 *)(G + K * 16);
+  double2 *st = (double2 *)((((uintptr_t)(pr + K)) + 15) & ~(uintptr_t)15);
+  const unsigned rank = cl_rank();
+  const int row = blockIdx.x >> t, j = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double2 *xr = P.xv + ((long long)row << n) + (long long)rank * NH;
+  for (unsigned a = tid; a < NH; a += RES_THREADS) st[a] = __ldg(xr + a);
+  for (int k = tid; k < K; k += RES_THREADS) pr[k] = P.pairs[k];
+  pdl_wait();  // the gates are the ones the backward pass just wrote
+  const int s = P.slots[j].s;
+  for (int q = tid; q < K * 16; q += RES_THREADS) G[q] = P.gates[(long long)s * K * 16 + q];
+  __syncthreads();
+  const FastDiv one(1u);
+  for (int k = 0; k < K; ++k) {
+    const int2 pq = pr[k];
+    if ((unsigned)max(pq.x, pq.y) < top) {
+      res_apply(st, G + 16 * k, pq, false, 1, one, 1u, n - t, tid, RES_THREADS);
+      __syncthreads();
+      continue;
+    }
+    cl_sync();  // the partner's half is complete
+    const int lo = min(pq.x, pq.y), hi = max(pq.x, pq.y);
+    const double2 *g = G + 16 * k;
+    const unsigned nq = NH >> 2;  // quadruples per CTA (N/4 = C NH/4 in total)
+    for (unsigned q = tid; q < nq; q += RES_THREADS) {
+      const unsigned r = rank * nq + q;
+      const unsigned base = insert_zero32(insert_zero32(r, lo), hi);
+      unsigned own[4], loc[4];
+      double2 v[4];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        const unsigned a = base | ((unsigned)(l & 1) << pq.x) | ((unsigned)(l >> 1) << pq.y);
+        own[l] = a >> top;
+        loc[l] = a & (NH - 1);
+        v[l] = own[l] == rank ? st[loc[l]] : ld_remote_c(st + loc[l], own[l]);
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        double2 o = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) cfma(o, g[4 * a + b], v[b]);
+        if (own[a] == rank) st[loc[a]] = o;
+        else st_remote_c(st + loc[a], own[a], o);
+      }
+    }
+    cl_sync();  // both halves updated before anyone reads them
+  }
+  double acc = 0.0;
+  const double2 *yr = P.yv + ((long long)row << n) + (long long)rank * NH;
+  for (unsigned a = tid; a < NH; a += RES_THREADS) {
+    const double2 u = st[a], w = __ldg(yr + a);
+    const double dr = u.x - w.x, di = u.y - w.y;
+    acc = fma(dr, dr, acc);
+    acc = fma(di, di, acc);
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) red[warp] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < RES_WARPS; ++w) t += red[w];
+    half_sum_v = t;
+  }
+  cl_sync();
+  if (rank == 0 && tid == 0) {
+    double t_sum = 0.0;
+    for (unsigned c = 0; c < C; ++c) t_sum += ld_remote(&half_sum_v, c);
+    P.row_out[(long long)j * P.rows + row] = t_sum;
+  }
+  cl_sync();  // rank 1 stays resident until rank 0 has read its sum
+}
+
 }  // namespace
+
+size_t val_cl_smem(int n, int K, int t) {
+  return (((size_t)K * 16 * sizeof(double2) + (size_t)K * sizeof(int2) + 15) & ~(size_t)15) +
+         ((size_t)1 << (n - t)) * sizeof(double2);
+}
+
+cudaError_t launch_val_cluster(const ValRowParams &p, int n_slots, cudaStream_t st) {
+  constexpr size_t lim = RES_SMEM_MAX - 256;
+  // cluster of 2^t CTAs per row: the smallest that fits, widened (up to 8)
+  // while the rows of all starts still fit on the 148 SMs
+  int t = 1;
+  while (t < 3 && val_cl_smem(p.n, p.K, t) > lim) ++t;
+  while (t < 3 && (long long)p.rows * n_slots * (2 << t) <= 148) ++t;
+  const size_t smem = val_cl_smem(p.n, p.K, t);
+  if (smem > lim) return cudaErrorInvalidConfiguration;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(val_cl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.rows << t, n_slots);
+  cfg.blockDim = dim3(RES_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute a[2];
+  a[0].id = cudaLaunchAttributeClusterDimension;
+  a[0].val.clusterDim.x = 1u << t;
+  a[0].val.clusterDim.y = 1;
+  a[0].val.clusterDim.z = 1;
+  a[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = a;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, val_cl_kernel, p, t);
+}
 
 size_t val_blk_smem(int n, int K, int ld) {
   return (((size_t)K * 16 * sizeof(double2) + (size_t)K * sizeof(int2) + 15) & ~(size_t)15) +

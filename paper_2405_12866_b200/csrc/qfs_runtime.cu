@@ -659,6 +659,13 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
       LaunchScope ls(c, K_VAL_ROW, vunits * 32.0, vunits * 32.0 * K);
       if (c->val_block && val_blk_smem(n, K, 1) + 256 <= res_smem_limit(1)) CUDA_TRY(c, launch_val_block(f, ns, st));
       else CUDA_TRY(c, launch_val_row(f, ns, st));
+    } else if (c->val_block && val_cl_smem(n, K, 3) + 256 <= res_smem_limit(1)) {
+      // one row per cluster of 2-8 CTAs (n >= 14 rows exceed one CTA's shared memory)
+      ValRowParams f{};
+      f.n = n; f.K = K; f.rows = c->V; f.slots = slots; f.pairs = c->d_pairs;
+      f.gates = c->d_gates; f.xv = c->d_xv; f.yv = c->d_yv; f.row_out = rowout;
+      LaunchScope ls(c, K_VAL_ROW, vunits * 32.0, vunits * 32.0 * K);
+      CUDA_TRY(c, launch_val_cluster(f, ns, st));
     } else {
       const long long VN = (long long)c->V * N;
       for (int k = 0; k < K; ++k) {
