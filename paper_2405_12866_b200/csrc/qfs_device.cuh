@@ -121,7 +121,8 @@ __device__ __forceinline__ double2 shfl_xor_c(double2 v, int m) {
 //   E = X D Y^dag, u = Y X^dag with Y = V).  Square roots and divisions are
 //   rsqrt-based (MUFU.RSQ64H + Newton) to keep the serial chain short.
 // E' is scaled by an exact power of two first (the polar factor is scale-free).
-// scratch: 16 double2 of shared memory per half (null-column path only).
+// scratch: 32 double2 of shared memory per half warp (Newton-Schulz operands;
+// the first 16 also serve the null-column completion).
 //
 // Fast path first (polar_ns): when E' is far enough from singular, its
 // unitary polar factor W = X Y^dag is reached by Newton-Schulz iterations
@@ -141,15 +142,23 @@ __device__ __forceinline__ double half_sum(double v) {
 // rounding).  Returns false (nothing written) when e_0 > 0.9647 for either
 // half of the warp: the Jacobi path below handles that (ill-conditioned or
 // singular E').  The decision and the count are warp-uniform.
-__device__ bool polar_ns(double2 e, int hb, int r, int c, double2 &g_out, double &ss_out) {
+// The 4x4 products exchange operands through shared memory (scr: 32 double2
+// of this half warp: X at [0, 16), T at [16, 32)): one store and eight
+// broadcast-friendly loads per product instead of eight 128-bit shuffles.
+__device__ bool polar_ns(double2 e, int hb, int r, int c, double2 &g_out, double &ss_out, double2 *scr) {
   const double fro2 = half_sum(e.x * e.x + e.y * e.y);
   if (!__all_sync(FULL, fro2 > 0.0)) return false;
   const double rs = 2.0 * rsqrt(fro2);
   double2 x = make_double2(e.x * rs, e.y * rs);
-  auto xhx = [&](double2 X) {  // (X^dag X)[r][c] = sum_q conj(X[q][r]) X[q][c]
+  const int l = 4 * r + c;
+  double2 *sx = scr, *sT = scr + 16;
+  auto xhx = [&](double2 X) {  // (X^dag X)[r][c] = sum_q conj(X[q][r]) X[q][c]; leaves X in sx
+    __syncwarp();
+    sx[l] = X;
+    __syncwarp();
     double2 y = make_double2(0.0, 0.0);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) cfma(y, cconj(shfl_c(X, hb | (4 * q + r))), shfl_c(X, hb | (4 * q + c)));
+    for (int q = 0; q < 4; ++q) cfma(y, cconj(sx[4 * q + r]), sx[4 * q + c]);
     return y;
   };
   double2 y = xhx(x);
@@ -167,9 +176,11 @@ __device__ bool polar_ns(double2 e, int hb, int r, int c, double2 &g_out, double
   for (int it = 0; it < k; ++it) {
     if (it > 0) y = xhx(x);
     const double2 t = make_double2(0.5 * ((r == c ? 3.0 : 0.0) - y.x), -0.5 * y.y);  // (3I - Y)/2
+    sT[l] = t;
+    __syncwarp();
     double2 z = make_double2(0.0, 0.0);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) cfma(z, shfl_c(x, hb | (4 * r + q)), shfl_c(t, hb | (4 * q + c)));
+    for (int q = 0; q < 4; ++q) cfma(z, sx[4 * r + q], sT[4 * q + c]);
     x = z;
   }
   // G = W^dag: G[r][c] = conj(W[c][r]);  sum sigma = Re Tr(W^dag E') = Re sum conj(W) o E'
@@ -196,7 +207,7 @@ __device__ void hw_polar(double2 e, double2 v0, double2 &g_out, double2 &v_out, 
 #endif
   {
     double ss_ns;
-    if (polar_ns(e, hb, r, j, g_out, ss_ns)) {
+    if (polar_ns(e, hb, r, j, g_out, ss_ns, scratch)) {
       v_out = v0;  // warm start of the Jacobi path left as it was
       sig_sum = scalbn(ss_ns, ex);
 #ifdef QFS_DIAG_POLAR

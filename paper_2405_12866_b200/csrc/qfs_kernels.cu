@@ -59,7 +59,7 @@ __device__ void polar_write(const double *e32, double2 *gout, double2 *vslot, do
   const double2 v0 = vslot ? vslot[l] : make_double2((l % 5 == 0) ? 1.0 : 0.0, 0.0);
   double2 g, v;
   double ss;
-  gate_update(kind, e, gout, beta, v0, g, v, ss, scratch + (lane & 16));
+  gate_update(kind, e, gout, beta, v0, g, v, ss, scratch + 2 * (lane & 16));
   __syncwarp();
   if (lane < 16 && kind != 1) {
     gout[l] = g;
@@ -109,7 +109,7 @@ struct BwdShared {
   double2 sQ[16];                          // G_{i+1}^dag
   double2 red[BWD_THREADS / 32][4][16];    // per-warp (per lane-group) E partials
   double sum32[32];
-  double2 scratch[32];
+  double2 scratch[64];                     // polar scratch: 32 per half warp
 };
 
 // ---------------------------------------------------------------- backward --
@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(BWD_THREADS, QFS_BWD_MINB) bwd_persistent_kern
 // polar step alone (sample-sharded mode, after the NCCL all-reduce of E): one warp per start
 __global__ void polar_kernel(const PolarParams P) {
   __shared__ double e32[4][32];
-  __shared__ double2 scratch[4][32];
+  __shared__ double2 scratch[4][64];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int j = blockIdx.x * 4 + w;
   pdl_wait();
@@ -956,7 +956,7 @@ __global__ void apply_kernel(const ApplyParams P) {
 // two matrices per warp (one per 16-lane half), cold start (V_0 = I)
 __global__ void polar_batch_kernel(const double2 *env, const double2 *g_old, double beta,
                                    double2 *g_new, double *sig, int count) {
-  __shared__ double2 scratch[4][32];
+  __shared__ double2 scratch[4][64];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, l = lane & 15;
   const int i = (blockIdx.x * 4 + w) * 2 + (lane >> 4);
   const bool valid = i < count;
@@ -969,7 +969,7 @@ __global__ void polar_batch_kernel(const double2 *env, const double2 *g_old, dou
   const double2 v0 = make_double2((l % 5 == 0) ? 1.0 : 0.0, 0.0);
   double2 g, v;
   double ss;
-  hw_polar(e, v0, g, v, ss, scratch[w] + (lane & 16));
+  hw_polar(e, v0, g, v, ss, scratch[w] + 2 * (lane & 16));
   if (valid) {
     g_new[(long long)i * 16 + l] = g;
     if (l == 0) sig[i] = ss;

@@ -164,7 +164,7 @@ struct ResSmem {
   double *red;    // [RES_WARPS][32]
   double *buf;    // [2][32] CTA partial of E (read by the cluster over DSMEM)
   double *cbuf;   // [2] CTA partial costs (train, validation)
-  double2 *scr;   // [32] polar scratch
+  double2 *scr;   // [64] polar scratch (32 per half warp)
   int2 *pr;       // [K] qubit pairs
   double2 *phi;   // [2^n][ld]
   double2 *chi;   // [2^n][ld]
@@ -177,7 +177,7 @@ __device__ ResSmem res_carve(unsigned char *base, int K, int n, int ld) {
   m.buf = m.red + RES_WARPS * 32;
   m.cbuf = m.buf + 64;
   m.scr = (double2 *)(m.cbuf + 2);
-  m.pr = (int2 *)(m.scr + 32);
+  m.pr = (int2 *)(m.scr + 64);
   uintptr_t p = (uintptr_t)(m.pr + K);
   p = (p + 15) & ~(uintptr_t)15;
   m.phi = (double2 *)p;
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
         double2 g, v;
         double ss;
         gate_update(kind, ev, gi, P.beta, make_double2((l % 5 == 0) ? 1.0 : 0.0, 0.0), g, v, ss,
-                    sm.scr + (lane & 16));
+                    sm.scr + 2 * (lane & 16));
         __syncwarp();
         if (lane < 16 && kind != 1) gi[l] = g;
         if (rank == 0) {
@@ -607,7 +607,7 @@ cudaError_t launch_val_block(const ValRowParams &p, int n_slots, cudaStream_t st
 
 size_t res_smem_bytes(int n, int K, int ld) {
   size_t b = (size_t)K * 16 * sizeof(double2) + (RES_WARPS * 32 + 64 + 2) * sizeof(double) +
-             32 * sizeof(double2) + (size_t)K * sizeof(int2);
+             64 * sizeof(double2) + (size_t)K * sizeof(int2);
   b = (b + 15) & ~(size_t)15;
   b += 2 * ((size_t)ld << n) * sizeof(double2);
   return b;
