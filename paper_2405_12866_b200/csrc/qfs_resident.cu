@@ -33,7 +33,10 @@
 namespace qfs {
 namespace {
 
-constexpr int RES_THREADS = 256;
+#ifndef QFS_RES_THREADS
+#define QFS_RES_THREADS 256
+#endif
+constexpr int RES_THREADS = QFS_RES_THREADS;
 constexpr int RES_WARPS = RES_THREADS / 32;
 constexpr size_t RES_SMEM_MAX = 232448;  // 227 KB opt-in dynamic shared memory per CTA
 constexpr size_t RES_SMEM_MAX2 = 113 * 1024;  // two CTAs per SM (228 KB per SM, 1 KB reserved per CTA)
