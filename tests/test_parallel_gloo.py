@@ -47,6 +47,19 @@ def _body(rank, world, kind, out_q):
         res, gates, win = PL.run_multistart(engine, p.init, prm, rank, world)
         flag = PL.any_flag(rank == 1, world)
         out_q.put((rank, res, gates, win, flag))
+    elif kind == "resynth":
+        from paper_2405_12866_b200 import resynth as R
+        from test_resynth import OracleContext, PRM
+        blocks = [R.redundant_block(3, 2, seed=10 + q, extra=1) for q in range(3)]
+
+        def gather(mine):
+            objs = [None] * world
+            dist.all_gather_object(objs, mine)
+            return objs
+
+        rep = R.resynth_partitions(blocks, PRM, rank, world, gather=gather, starts=2,
+                                   context_factory=OracleContext)
+        out_q.put((rank, [(p_, r.deleted, r.kept) for p_, r in rep]))
     else:
         import torch
         p = I.make_problem("c3", init="R", s=1)
@@ -112,3 +125,16 @@ def test_sample_shard_allreduce_gloo():
     outs = _run("sample")
     for _, err in outs:
         assert err < 1e-13
+
+
+def test_resynth_partitions_gloo():
+    """NEXT-4: partitions spread over two ranks (p mod world), reports gathered
+    in partition order, identical on both ranks and equal to one process."""
+    from paper_2405_12866_b200 import resynth as R
+    from test_resynth import OracleContext, PRM
+    outs = _run("resynth")
+    (r0, a), (r1, b) = outs
+    assert a == b and [t[0] for t in a] == [0, 1, 2]
+    blocks = [R.redundant_block(3, 2, seed=10 + q, extra=1) for q in range(3)]
+    one = R.resynth_partitions(blocks, PRM, starts=2, context_factory=OracleContext)
+    assert [(p_, r.deleted, r.kept) for p_, r in one] == a
