@@ -222,6 +222,21 @@ def test_full_size_c4_sampled_starts(qfs):
     _compare_traces(sub, ot, "c4-full")
 
 
+@pytest.mark.parametrize("name,pick", [("c3", [0, 37, 63]), ("c5c", [5, 50])])
+def test_full_size_resident_sampled_starts(qfs, name, pick):
+    """C3 and C5c at full size in the bench's launch configuration (auto path =
+    cluster-resident, all 64 starts in one launch); the oracle recomputes a few
+    sampled starts (starts are independent)."""
+    p = I.make_problem(name, init="R")
+    ctx = _ctx(qfs, p.n, p.pairs)
+    ctx.set_samples(p.x, p.y, p.xv, p.yv)
+    gt = ctx.trace_sweeps(p.init, p.m_init, 2)
+    ot = oracle.trace_sweeps(p.n, p.pairs, p.init[pick], p.x, p.y, p.m_init, 2, threads=len(pick))
+    sub = dict(env=gt["env"][:, :, pick], gates=gt["gates"][:, pick], cost=gt["cost"][:, pick],
+               sigma=gt["sigma"][:, :, pick])
+    _compare_traces(sub, ot, f"{name}-full")
+
+
 # ----------------------------------------------------------- instantiation --
 def _inst_both(qfs, p, prm, path="auto"):
     ctx = _ctx(qfs, p.n, p.pairs, path)
