@@ -30,9 +30,11 @@ def build(force: bool = False) -> str:
     """Compile the oracle (plain C++17, -O2, no -ffast-math, OpenMP over starts)."""
     if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < max(
             os.path.getmtime(SRC), os.path.getmtime(os.path.join(_HERE, "qfso.h"))):
+        tmp = f"{LIB_PATH}.tmp{os.getpid()}"
         cmd = ["g++", "-std=c++17", "-O2", "-fopenmp", "-fPIC", "-shared", "-Wall",
-               "-o", LIB_PATH, SRC]
+               "-o", tmp, SRC]
         subprocess.run(cmd, check=True, cwd=_HERE)
+        os.replace(tmp, LIB_PATH)  # atomic for concurrent test processes
     return LIB_PATH
 
 

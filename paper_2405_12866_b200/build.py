@@ -38,19 +38,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
     libs = glob.glob(os.path.join(nd, "lib", "libnccl.so*"))
     if not libs:
         raise RuntimeError("libnccl.so not found")
+    tmp = f"{LIB}.tmp{os.getpid()}"
     cmd = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
            "-Xptxas", "-v" if verbose else "-O3",
            f"-I{os.path.join(nd, 'include')}", f"-I{os.path.join(ROOT, 'include')}",
            f"-L{os.path.join(nd, 'lib')}", f"-l:{os.path.basename(sorted(libs)[0])}",
            "-Xlinker", f"-rpath={os.path.join(nd, 'lib')}",
            *os.environ.get("QFS_NVCC_DEFINES", "").split(),
-           "-o", LIB + ".tmp", *SOURCES]
+           "-o", tmp, *SOURCES]
     r = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed:\n{r.stdout}\n{r.stderr}")
     if verbose:
         print(r.stdout, r.stderr)
-    os.replace(LIB + ".tmp", LIB)
+    os.replace(tmp, LIB)  # atomic: concurrent builders (one process per GPU) never see a partial file
     return LIB
 
 
