@@ -103,6 +103,20 @@ qfs_status qfs_create_nccl(int n, int k, const int32_t *pairs, int device, const
 qfs_status qfs_set_samples(qfs_ctx *c, int m_pool, const double *x, const double *y, int v,
                            const double *xv, const double *yv);
 
+/* Asynchronous variant for pipelined callers: queues the sample set (same
+ * arguments and layout as qfs_set_samples) into one of two device staging
+ * slots with host->device copies on a separate copy stream, and returns at
+ * once; the next qfs_instantiate / qfs_trace_sweeps / qfs_bench_sweeps call
+ * consumes the oldest queued set (finite check, transpose to the sample-minor
+ * pools) before it runs.  So a caller can queue step t+1's samples while step
+ * t's instantiation runs.  The host buffers must stay valid and unmodified
+ * until the consuming call returns (pinned memory makes the copies overlap).
+ * QFS_ERR_STATE when two sets are already queued; argument errors as
+ * qfs_set_samples; a non-finite sample is reported (QFS_ERR_NUMERIC) by the
+ * consuming call. */
+qfs_status qfs_set_samples_async(qfs_ctx *c, int m_pool, const double *x, const double *y, int v,
+                                 const double *xv, const double *yv);
+
 /* Same, from DEVICE pointers (e.g. torch CUDA tensors) on cuda_stream
  * (cudaStream_t, NULL = legacy default stream).  Copies device-to-device. */
 qfs_status qfs_set_samples_device(qfs_ctx *c, int m_pool, const void *dx, const void *dy, int v,

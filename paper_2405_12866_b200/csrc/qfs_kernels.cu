@@ -20,6 +20,7 @@
 //
 // No code here is shared with the CPU oracle.
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <stdint.h>
 
 #include "qfs_device.cuh"
@@ -913,6 +914,24 @@ __global__ void transpose_kernel(const double2 *src, double2 *dst, int rows, lon
   }
 }
 
+__global__ void copy_kernel(double2 *dst, const double2 *src, long long count) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+__global__ void copy_words_kernel(unsigned *dst, const unsigned *src, long long count) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+__global__ void fill_words_kernel(unsigned *dst, unsigned value, long long count) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = value;
+}
+
 __global__ void identity_fill_kernel(double2 *v, long long count16) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count16 * 16;
        i += (long long)gridDim.x * blockDim.x)
@@ -1154,6 +1173,29 @@ cudaError_t launch_finite_check(const double *p, long long n, int *flag, cudaStr
   long long blocks = (n + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
   finite_check_kernel<<<(unsigned)blocks, 256, 0, st>>>(p, n, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy(double2 *dst, const double2 *src, long long count, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  long long blocks = (count + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  copy_kernel<<<(unsigned)blocks, 256, 0, st>>>(dst, src, count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy_bytes(void *dst, const void *src, size_t bytes, cudaStream_t st) {
+  const long long words = (long long)(bytes / 4);
+  if (words <= 0) return cudaSuccess;
+  const long long blocks = std::min<long long>((words + 255) / 256, 148 * 8);
+  copy_words_kernel<<<(unsigned)blocks, 256, 0, st>>>((unsigned *)dst, (const unsigned *)src, words);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_words(unsigned *dst, unsigned value, long long count, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  const long long blocks = std::min<long long>((count + 255) / 256, 148 * 8);
+  fill_words_kernel<<<(unsigned)blocks, 256, 0, st>>>(dst, value, count);
   return cudaGetLastError();
 }
 

@@ -99,6 +99,23 @@ struct qfs_ctx {
   int res_per_sm = 1;       // QFS_RES_PER_SM: resident CTAs per SM the cluster plan targets
   int path = 0;             // 0 auto, 1 streamed (B cache in HBM), 2 cluster-resident (qfs_set_path / QFS_PATH)
   size_t stage_bytes = 0;
+  // qfs_set_samples_async: up to two sample sets queued in device staging
+  // buffers (H2D on a copy stream, overlapping the running instantiation); the
+  // next instantiate / trace / bench call consumes the oldest one
+  struct Staged {
+    double2 *x = nullptr, *y = nullptr, *xv = nullptr, *yv = nullptr;
+    size_t cap_xy = 0, cap_v = 0;  // bytes per array
+    int m_pool = 0, v = 0;
+    cudaEvent_t ev = nullptr;
+  } stg[2];
+  int stg_head = 0, stg_count = 0;
+  // pinned host staging of the gates (upload / download through page-locked
+  // memory, so the small copies do not queue behind a pageable staging path)
+  double2 *h_gates = nullptr;
+  size_t h_gates_cap = 0;
+  Slot *h_slots = nullptr;  // mapped pinned slot table
+  size_t h_slots_cap = 0;
+  cudaStream_t st_copy = nullptr;
   // graph cache
   cudaGraphExec_t gexec = nullptr;
   long long gkey[8] = {0};
@@ -722,8 +739,22 @@ qfs_status run_sweep(qfs_ctx *c, const SweepSpec &sp, std::vector<double> &csum,
     qfs_status r = prepare_desc(c);
     if (r != QFS_OK) return r;
   }
-  CUDA_TRY(c, cudaMemcpyAsync(c->d_slots, sp.slots.data(), ns * sizeof(Slot),
-                              cudaMemcpyHostToDevice, c->st));
+  // slot table through a mapped pinned buffer and a copy kernel (see upload_gates)
+  if ((size_t)ns > c->h_slots_cap) {
+    if (c->h_slots) cudaFreeHost(c->h_slots);
+    c->h_slots = nullptr;
+    c->h_slots_cap = 0;
+    CUDA_TRY(c, cudaHostAlloc((void **)&c->h_slots, (size_t)std::max(ns, 64) * sizeof(Slot), cudaHostAllocMapped));
+    c->h_slots_cap = (size_t)std::max(ns, 64);
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(c->st));  // the previous table's reader is done
+  std::memcpy(c->h_slots, sp.slots.data(), ns * sizeof(Slot));
+  {
+    Slot *dh = nullptr;
+    CUDA_TRY(c, cudaHostGetDevicePointer((void **)&dh, c->h_slots, 0));
+    static_assert(sizeof(Slot) == 8, "Slot is copied as double2 halves");
+    CUDA_TRY(c, launch_copy_bytes(c->d_slots, dh, ns * sizeof(Slot), c->st));
+  }
   if (c->d_dbg) {
     std::vector<unsigned long long> init((size_t)4 * c->K);
     for (int i = 0; i < c->K; ++i) { init[4 * i] = ~0ull; init[4 * i + 1] = init[4 * i + 2] = init[4 * i + 3] = 0; }
@@ -804,15 +835,34 @@ qfs_status upload_gates(qfs_ctx *c, int s, const double *init) {
           if (!ok) return fail(c, QFS_ERR_NUMERIC, "one-qubit gate slot is not of the form u (x) I (tol 1e-10)");
         }
     }
-  CUDA_TRY(c, cudaMemcpyAsync(c->d_gates, init, (size_t)s * c->K * 16 * sizeof(double2),
-                              cudaMemcpyHostToDevice, c->st));
+  const size_t gb = (size_t)s * c->K * 16 * sizeof(double2);
+  if (gb > c->h_gates_cap) {
+    if (c->h_gates) cudaFreeHost(c->h_gates);
+    c->h_gates = nullptr;
+    c->h_gates_cap = 0;
+    CUDA_TRY(c, cudaHostAlloc((void **)&c->h_gates, gb, cudaHostAllocMapped));
+    c->h_gates_cap = gb;
+  }
+  std::memcpy(c->h_gates, init, gb);
+  // read by a kernel from the mapped pinned buffer: small uploads never queue
+  // on a copy engine behind a caller's large H2D (qfs_set_samples_async)
+  double2 *dh = nullptr;
+  CUDA_TRY(c, cudaHostGetDevicePointer((void **)&dh, c->h_gates, 0));
+  CUDA_TRY(c, launch_copy(c->d_gates, dh, (long long)s * c->K * 16, c->st));
   CUDA_TRY(c, launch_identity_fill(c->d_vprev, (long long)s * c->K, c->st));
   c->launches++;
   return QFS_OK;
 }
 
+}  // namespace
+qfs_status consume_staged(qfs_ctx *c);  // defined with the ABI below
+namespace {
 qfs_status check_ready(qfs_ctx *c, int s) {
   if (!c) return QFS_ERR_ARG;
+  if (c->stg_count > 0) {
+    const qfs_status st = consume_staged(c);
+    if (st != QFS_OK) return st;
+  }
   if (!c->have_samples) return fail(c, QFS_ERR_STATE, "set_samples has not been called");
   if (s < 1) return fail(c, QFS_ERR_ARG, "s must be >= 1");
   CUDA_TRY(c, cudaSetDevice(c->device));
@@ -955,15 +1005,27 @@ static qfs_status set_samples_impl(qfs_ctx *c, int m_pool, const void *x, const 
     CUDA_TRY(c, cudaMalloc(&c->d_stage, (size_t)m_pool * rb));
     c->stage_bytes = (size_t)m_pool * rb;
   }
-  CUDA_TRY(c, cudaMemsetAsync(c->d_flag, 0, sizeof(int), st));
+  CUDA_TRY(c, launch_fill_words((unsigned *)c->d_flag, 0u, 1, st));  // a kernel, not a copy-engine memset
+  // device sources (qfs_set_samples_device, queued async sets) are read in place
+  // by kernels: no copy-engine work that could queue behind a concurrent H2D
+  const bool dev = kind == cudaMemcpyDeviceToDevice;
   for (int q = 0; q < 2; ++q) {
-    CUDA_TRY(c, cudaMemcpyAsync(c->d_stage, q == 0 ? x : y, m_pool * rb, kind, st));
-    CUDA_TRY(c, launch_finite_check((const double *)c->d_stage, (long long)m_pool * c->N * 2, c->d_flag, st));
-    CUDA_TRY(c, launch_transpose(c->d_stage, q == 0 ? c->d_x : c->d_y, m_pool, c->N, st));
+    const double2 *src = (const double2 *)(q == 0 ? x : y);
+    if (!dev) {
+      CUDA_TRY(c, cudaMemcpyAsync(c->d_stage, src, m_pool * rb, kind, st));
+      src = c->d_stage;
+    }
+    CUDA_TRY(c, launch_finite_check((const double *)src, (long long)m_pool * c->N * 2, c->d_flag, st));
+    CUDA_TRY(c, launch_transpose(src, q == 0 ? c->d_x : c->d_y, m_pool, c->N, st));
   }
   if (v > 0) {
-    CUDA_TRY(c, cudaMemcpyAsync(c->d_xv, xv, v * rb, kind, st));
-    CUDA_TRY(c, cudaMemcpyAsync(c->d_yv, yv, v * rb, kind, st));
+    if (dev) {
+      CUDA_TRY(c, launch_copy(c->d_xv, (const double2 *)xv, (long long)v * c->N, st));
+      CUDA_TRY(c, launch_copy(c->d_yv, (const double2 *)yv, (long long)v * c->N, st));
+    } else {
+      CUDA_TRY(c, cudaMemcpyAsync(c->d_xv, xv, v * rb, kind, st));
+      CUDA_TRY(c, cudaMemcpyAsync(c->d_yv, yv, v * rb, kind, st));
+    }
     CUDA_TRY(c, launch_finite_check((const double *)c->d_xv, (long long)v * c->N * 2, c->d_flag, st));
     CUDA_TRY(c, launch_finite_check((const double *)c->d_yv, (long long)v * c->N * 2, c->d_flag, st));
   }
@@ -977,6 +1039,57 @@ static qfs_status set_samples_impl(qfs_ctx *c, int m_pool, const void *x, const 
     return fail(c, QFS_ERR_NUMERIC, "non-finite sample");
   }
   if (realloc) drop_graph(c);
+  return QFS_OK;
+}
+
+// Oldest queued sample set -> the pools (device-to-device through the same
+// staging, finite check and transpose as qfs_set_samples), after its H2D copy.
+}  // extern "C" (internal helper below has C++ linkage)
+qfs_status consume_staged(qfs_ctx *c) {
+  qfs_ctx::Staged &g = c->stg[c->stg_head];
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->st, g.ev, 0));
+  const qfs_status st = set_samples_impl(c, g.m_pool, g.x, g.y, g.v, g.xv, g.yv, cudaMemcpyDeviceToDevice, c->st);
+  c->stg_head = (c->stg_head + 1) % 2;
+  c->stg_count -= 1;
+  return st;
+}
+extern "C" {
+
+qfs_status qfs_set_samples_async(qfs_ctx *c, int m_pool, const double *x, const double *y, int v,
+                                 const double *xv, const double *yv) {
+  if (!c) return QFS_ERR_ARG;
+  if (m_pool < 1 || !x || !y || v < 0 || (v > 0 && (!xv || !yv)))
+    return fail(c, QFS_ERR_ARG, "bad sample arguments");
+  if ((long long)m_pool * (c->mode == 1 ? c->world : 1) > c->N) return fail(c, QFS_ERR_CAPACITY, "m_pool > 2^n");
+  if (c->stg_count == 2) return fail(c, QFS_ERR_STATE, "two sample sets are already queued");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  if (!c->st_copy) CUDA_TRY(c, cudaStreamCreateWithFlags(&c->st_copy, cudaStreamNonBlocking));
+  qfs_ctx::Staged &g = c->stg[(c->stg_head + c->stg_count) % 2];
+  const size_t bxy = (size_t)m_pool * c->N * sizeof(double2), bv = (size_t)v * c->N * sizeof(double2);
+  if (!g.ev) CUDA_TRY(c, cudaEventCreateWithFlags(&g.ev, cudaEventDisableTiming));
+  if (bxy > g.cap_xy) {
+    dfree(g.x); dfree(g.y);
+    CUDA_TRY(c, cudaMalloc(&g.x, bxy));
+    CUDA_TRY(c, cudaMalloc(&g.y, bxy));
+    g.cap_xy = bxy;
+  }
+  if (bv > g.cap_v) {
+    dfree(g.xv); dfree(g.yv);
+    CUDA_TRY(c, cudaMalloc(&g.xv, bv));
+    CUDA_TRY(c, cudaMalloc(&g.yv, bv));
+    g.cap_v = bv;
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(g.x, x, bxy, cudaMemcpyHostToDevice, c->st_copy));
+  CUDA_TRY(c, cudaMemcpyAsync(g.y, y, bxy, cudaMemcpyHostToDevice, c->st_copy));
+  if (v > 0) {
+    CUDA_TRY(c, cudaMemcpyAsync(g.xv, xv, bv, cudaMemcpyHostToDevice, c->st_copy));
+    CUDA_TRY(c, cudaMemcpyAsync(g.yv, yv, bv, cudaMemcpyHostToDevice, c->st_copy));
+  }
+  CUDA_TRY(c, cudaEventRecord(g.ev, c->st_copy));
+  g.m_pool = m_pool;
+  g.v = v;
+  c->stg_count += 1;
   return QFS_OK;
 }
 
@@ -1159,8 +1272,10 @@ qfs_status qfs_instantiate(qfs_ctx *c, int s, const double *init_gates, const qf
       if (A[q].c_train < bc) { bc = A[q].c_train; win = q; }
     if (win < 0) win = 0;
   }
-  CUDA_TRY(c, cudaMemcpy(out_gates, c->d_gates, (size_t)s * c->K * 16 * sizeof(double2),
-                         cudaMemcpyDeviceToHost));
+  CUDA_TRY(c, cudaMemcpyAsync(c->h_gates, c->d_gates, (size_t)s * c->K * 16 * sizeof(double2),
+                              cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(c, cudaStreamSynchronize(c->st));
+  std::memcpy(out_gates, c->h_gates, (size_t)s * c->K * 16 * sizeof(double2));
   for (int q = 0; q < s; ++q) {
     out[q].c_train = A[q].c_train; out[q].c_val = A[q].c_val; out[q].sweeps = A[q].total;
     out[q].restarts = A[q].restarts; out[q].final_m = A[q].M; out[q].term = (qfs_term)A[q].term;
@@ -1358,6 +1473,16 @@ void qfs_destroy(qfs_ctx *c) {
   dfree(c->d_partials); dfree(c->d_ered); dfree(c->d_sig); dfree(c->d_csum); dfree(c->d_rowout);
   dfree(c->d_cval); dfree(c->d_counters); dfree(c->d_slots); dfree(c->d_env_trace);
   dfree(c->d_stage); dfree(c->d_vprev); dfree(c->d_desc);
+  if (c->h_gates) cudaFreeHost(c->h_gates);
+  if (c->h_slots) cudaFreeHost(c->h_slots);
+  if (c->st_copy) {
+    cudaStreamSynchronize(c->st_copy);
+    cudaStreamDestroy(c->st_copy);
+  }
+  for (auto &g : c->stg) {
+    dfree(g.x); dfree(g.y); dfree(g.xv); dfree(g.yv);
+    if (g.ev) cudaEventDestroy(g.ev);
+  }
   dfree(c->d_flags); dfree(c->d_counters2); dfree(c->d_partials2); dfree(c->d_counters1); dfree(c->d_gpart);
   if (c->h_csum) cudaFreeHost(c->h_csum);
   if (c->h_cval) cudaFreeHost(c->h_cval);

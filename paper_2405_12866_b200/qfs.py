@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libqfs.so")
 STATUS = {0: "QFS_OK", 1: "QFS_ERR_ARG", 2: "QFS_ERR_CAPACITY", 3: "QFS_ERR_NUMERIC",
           4: "QFS_ERR_DEVICE", 5: "QFS_ERR_STATE"}
 TERM_NAMES = {0: "CONVERGED", 1: "PLATEAU", 2: "MAX_ITER", 3: "POOL_EXHAUSTED", 4: "STOPPED"}
-SYMBOLS = ["qfs_create", "qfs_create_dist", "qfs_nccl_unique_id", "qfs_create_nccl", "qfs_set_samples", "qfs_set_samples_device",
+SYMBOLS = ["qfs_create", "qfs_create_dist", "qfs_nccl_unique_id", "qfs_create_nccl", "qfs_set_samples", "qfs_set_samples_async", "qfs_set_samples_device",
            "qfs_instantiate", "qfs_trace_sweeps", "qfs_bench_sweeps", "qfs_op_apply",
            "qfs_op_environment", "qfs_op_polar", "qfs_profile_enable", "qfs_profile_read", "qfs_set_path", "qfs_set_gate_kinds",
            "qfs_launch_count", "qfs_stream", "qfs_last_error", "qfs_destroy"]
@@ -69,6 +69,7 @@ def load(path: str = LIB_PATH):
         lib.qfs_nccl_unique_id.argtypes = [vp]
         lib.qfs_create_nccl.argtypes = [ip, ip, vp, ip, vp, ip, ip, ip, ctypes.POINTER(vp)]
         lib.qfs_set_samples.argtypes = [vp, ip, vp, vp, ip, vp, vp]
+        lib.qfs_set_samples_async.argtypes = [vp, ip, vp, vp, ip, vp, vp]
         lib.qfs_set_samples_device.argtypes = [vp, ip, vp, vp, ip, vp, vp, vp]
         lib.qfs_instantiate.argtypes = [vp, ip, vp, ctypes.POINTER(Params), vp, vp, ctypes.POINTER(ip)]
         lib.qfs_trace_sweeps.argtypes = [vp, ip, vp, ip, dp, ip, vp, vp, vp, vp]
@@ -169,6 +170,13 @@ class Context:
         """Raw host pointers (e.g. pinned torch tensors' data_ptr())."""
         self._check(self.lib.qfs_set_samples(self.h, int(m_pool), ctypes.c_void_p(px), ctypes.c_void_p(py),
                                              int(v), ctypes.c_void_p(pxv or 0), ctypes.c_void_p(pyv or 0)))
+
+    def set_samples_async_host_ptr(self, m_pool, px, py, v, pxv, pyv):
+        """qfs_set_samples_async: queue a sample set (raw host pointers, ideally
+        pinned); the next instantiate / trace call consumes it.  The buffers
+        must stay alive and unchanged until then."""
+        self._check(self.lib.qfs_set_samples_async(self.h, int(m_pool), ctypes.c_void_p(px), ctypes.c_void_p(py),
+                                                   int(v), ctypes.c_void_p(pxv or 0), ctypes.c_void_p(pyv or 0)))
 
     def set_samples_device(self, dx, dy, dxv=None, dyv=None, stream=None):
         """torch CUDA tensors (complex128, contiguous) on the context's device."""

@@ -437,3 +437,39 @@ def test_u3_cnot_template_gate_kinds(qfs, path):
     with pytest.raises(QfsError) as ei:
         ctx.instantiate(bad, prm)
     assert ei.value.status == 3
+
+
+def test_set_samples_async_queue(qfs):
+    """qfs_set_samples_async: queued sets are consumed oldest first by the next
+    calls and give the same traces as qfs_set_samples; a third queued set is
+    refused (QFS_ERR_STATE); a non-finite queued set fails the consuming call."""
+    import torch
+    from paper_2405_12866_b200.qfs import QfsError
+    p = I.make_problem("c3", init="R", s=2, k=12)
+    q = I.make_problem("c3", init="R", s=2, k=12, m_pool=256)
+    ref = _ctx(qfs, p.n, p.pairs)
+    ref.set_samples(p.x, p.y, p.xv, p.yv)
+    want_p = ref.trace_sweeps(p.init, 16, 1)
+    ref.set_samples(q.x, q.y, q.xv, q.yv)
+    want_q = ref.trace_sweeps(p.init, 16, 1)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    hp = [pin(a) for a in (p.x, p.y, p.xv, p.yv)]
+    hq = [pin(a) for a in (q.x, q.y, q.xv, q.yv)]
+    ctx = _ctx(qfs, p.n, p.pairs)
+    for h in (hp, hq):
+        ctx.set_samples_async_host_ptr(h[0].shape[0], h[0].data_ptr(), h[1].data_ptr(), h[2].shape[0],
+                                       h[2].data_ptr(), h[3].data_ptr())
+    with pytest.raises(QfsError) as ei:
+        ctx.set_samples_async_host_ptr(hp[0].shape[0], hp[0].data_ptr(), hp[1].data_ptr(), 16,
+                                       hp[2].data_ptr(), hp[3].data_ptr())
+    assert ei.value.status == 5
+    got_p = ctx.trace_sweeps(p.init, 16, 1)
+    got_q = ctx.trace_sweeps(p.init, 16, 1)
+    assert np.array_equal(got_p["env"], want_p["env"]) and np.array_equal(got_q["env"], want_q["env"])
+    bad = pin(p.x)
+    bad[0, 0] = float("nan")
+    ctx.set_samples_async_host_ptr(bad.shape[0], bad.data_ptr(), hp[1].data_ptr(), 16, hp[2].data_ptr(),
+                                   hp[3].data_ptr())
+    with pytest.raises(QfsError) as ei:
+        ctx.trace_sweeps(p.init, 16, 1)
+    assert ei.value.status == 3

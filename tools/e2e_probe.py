@@ -1,0 +1,50 @@
+"""Where the end-to-end step time goes at C4: instantiate(max_iter=1) alone,
+with queued async samples, with synchronous samples; host-side checks timed."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from paper_2405_12866_b200 import build, inputs as I, qfs
+build.build()
+p = I.make_problem("c4", init="R")
+ctx = qfs.Context(p.n, p.pairs); ctx.set_samples(p.x, p.y, p.xv, p.yv)
+prm = dict(dist_tol=-1.0, diff_tol_r=1e-3, plateau_window=0, min_iter=6, max_iter=1, m_init=32,
+           overtrain_ratio=1e300, beta=0.0, stop_on_first=0)
+g = p.init
+for _ in range(3): g, _, _ = ctx.instantiate(g, prm)
+torch.cuda.synchronize()
+def timeit(f, n=10):
+    t0 = time.perf_counter()
+    for _ in range(n): f()
+    return (time.perf_counter() - t0) / n * 1e3
+print("instantiate only  %.3f ms" % timeit(lambda: ctx.instantiate(g, prm)))
+pin = [torch.from_numpy(a).pin_memory() for a in (p.x, p.y, p.xv, p.yv)]
+def sync_step():
+    ctx.set_samples_host_ptr(pin[0].shape[0], pin[0].data_ptr(), pin[1].data_ptr(), 16, pin[2].data_ptr(), pin[3].data_ptr())
+    ctx.instantiate(g, prm)
+print("sync set+inst     %.3f ms" % timeit(sync_step))
+def q(): ctx.set_samples_async_host_ptr(pin[0].shape[0], pin[0].data_ptr(), pin[1].data_ptr(), 16, pin[2].data_ptr(), pin[3].data_ptr())
+q()
+def async_step():
+    q(); ctx.instantiate(g, prm)
+print("async q+inst      %.3f ms" % timeit(async_step))
+ctx.instantiate(g, prm)
+t0 = time.perf_counter()
+for _ in range(10): ctx.set_samples_host_ptr(pin[0].shape[0], pin[0].data_ptr(), pin[1].data_ptr(), 16, pin[2].data_ptr(), pin[3].data_ptr())
+print("sync set only     %.3f ms" % ((time.perf_counter() - t0) * 100))
+# instantiate while an independent pinned H2D of the same size runs on another stream
+dst = torch.empty(pin[0].numel() * 2 + 4, dtype=torch.complex128, device="cuda")
+s2 = torch.cuda.Stream()
+def overlapped():
+    with torch.cuda.stream(s2):
+        dst[:pin[0].numel()].view(pin[0].shape).copy_(pin[0], non_blocking=True)
+        dst[pin[0].numel():2 * pin[0].numel()].view(pin[1].shape).copy_(pin[1], non_blocking=True)
+    ctx.instantiate(g, prm)
+    s2.synchronize()
+print("inst + torch H2D  %.3f ms" % timeit(overlapped))
+t0 = time.perf_counter()
+for _ in range(10):
+    with torch.cuda.stream(s2):
+        dst[:pin[0].numel()].view(pin[0].shape).copy_(pin[0], non_blocking=True)
+        dst[pin[0].numel():2 * pin[0].numel()].view(pin[1].shape).copy_(pin[1], non_blocking=True)
+    s2.synchronize()
+print("torch H2D only    %.3f ms" % ((time.perf_counter() - t0) * 100))
