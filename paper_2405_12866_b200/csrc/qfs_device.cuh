@@ -189,7 +189,11 @@ __device__ bool polar_ns(double2 e, int hb, int r, int c, double2 &g_out, double
   return true;
 }
 
-__device__ void hw_polar(double2 e, double2 v0, double2 &g_out, double2 &v_out, double &sig_sum,
+// v0p: warm start V_0 (row-major, this half's matrix) or nullptr for I; read
+// only on the Jacobi path, so the Newton-Schulz path has no global load on the
+// critical chain.  Returns true when v_out holds new right singular vectors
+// (Jacobi ran), false when V was not touched (Newton-Schulz).
+__device__ bool hw_polar(double2 e, const double2 *v0p, double2 &g_out, double2 &v_out, double &sig_sum,
                          double2 *scratch) {
   const int lane = threadIdx.x & 31;
   const int hb = lane & 16;         // half-warp base lane
@@ -208,14 +212,14 @@ __device__ void hw_polar(double2 e, double2 v0, double2 &g_out, double2 &v_out, 
   {
     double ss_ns;
     if (polar_ns(e, hb, r, j, g_out, ss_ns, scratch)) {
-      v_out = v0;  // warm start of the Jacobi path left as it was
       sig_sum = scalbn(ss_ns, ex);
 #ifdef QFS_DIAG_POLAR
       sig_sum = 100.0 * 1e7 + (double)(clock64() - t_ns);
 #endif
-      return;
+      return false;  // the warm start of the Jacobi path is left as it was
     }
   }
+  const double2 v0 = v0p ? v0p[l] : make_double2((l % 5 == 0) ? 1.0 : 0.0, 0.0);
   // A_0 = E' V_0
   double2 a = make_double2(0.0, 0.0);
 #pragma unroll
@@ -336,6 +340,7 @@ __device__ void hw_polar(double2 e, double2 v0, double2 &g_out, double2 &v_out, 
 #ifdef QFS_DIAG_POLAR  // diagnostic build: report sweeps * 1e7 + cycles instead of sum sigma
   sig_sum = (double)n_sweeps * 1e7 + (double)(clock64() - t_start);
 #endif
+  return true;
 }
 
 // Gate update by kind (readings R24-R25; the oracle's gate_update):
@@ -349,15 +354,14 @@ __device__ void hw_polar(double2 e, double2 v0, double2 &g_out, double2 &v_out, 
 // Half warp, lane l = 4r + c holds e = E[r][c] (before the beta term); gold is
 // the old gate (row-major, read-only); both halves may hold different matrices
 // but the kind must be warp-uniform.
-__device__ void gate_update(int kind, double2 e, const double2 *gold, double beta, double2 v0, double2 &g,
+__device__ bool gate_update(int kind, double2 e, const double2 *gold, double beta, const double2 *v0p, double2 &g,
                             double2 &v, double &ss, double2 *scratch) {
   const int lane = threadIdx.x & 31, hb = lane & 16, l = lane & 15, r = l >> 2, c = l & 3;
   if (kind == 1) {
     g = gold[l];
-    v = v0;
     const double2 gt = gold[4 * c + r];  // G[c][r]
     ss = half_sum(e.x * gt.x - e.y * gt.y);
-    return;
+    return false;
   }
   const bool blk = (r >> 1) == (c >> 1);
   if (kind == 2) {
@@ -372,13 +376,14 @@ __device__ void gate_update(int kind, double2 e, const double2 *gold, double bet
     const double2 go = gold[4 * c + r];  // (G^dag)[r][c] = conj(G[c][r])
     e = make_double2((1.0 - beta) * e.x + beta * go.x, (1.0 - beta) * e.y - beta * go.y);
   }
-  hw_polar(e, v0, g, v, ss, scratch);
+  const bool vnew = hw_polar(e, v0p, g, v, ss, scratch);
   if (kind == 2) {
     const double2 ga = shfl_c(g, hb | (4 * (r & 1) + (c & 1)));
     const double2 gb = shfl_c(g, hb | (4 * ((r & 1) + 2) + (c & 1) + 2));
     g = blk ? make_double2(0.5 * (ga.x + gb.x), 0.5 * (ga.y + gb.y)) : make_double2(0.0, 0.0);
     ss *= 0.5;
   }
+  return vnew;
 }
 
 }  // namespace

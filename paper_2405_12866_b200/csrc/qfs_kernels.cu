@@ -57,14 +57,13 @@ __device__ void polar_write(const double *e32, double2 *gout, double2 *vslot, do
   const int lane = threadIdx.x & 31, l = lane & 15;
   const double2 e = make_double2(e32[2 * l], e32[2 * l + 1]);
   if (env_out && lane < 16) env_out[l] = e;
-  const double2 v0 = vslot ? vslot[l] : make_double2((l % 5 == 0) ? 1.0 : 0.0, 0.0);
   double2 g, v;
   double ss;
-  gate_update(kind, e, gout, beta, v0, g, v, ss, scratch + 2 * (lane & 16));
+  const bool vnew = gate_update(kind, e, gout, beta, vslot, g, v, ss, scratch + 2 * (lane & 16));
   __syncwarp();
   if (lane < 16 && kind != 1) {
     gout[l] = g;
-    if (vslot) vslot[l] = v;
+    if (vslot && vnew) vslot[l] = v;
   }
   if (lane == 0 && sig_out) *sig_out = ss;
 }
@@ -362,8 +361,9 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
 
 // Warp 0 of the last CTA of a start: sum the CTA partials in CTA order, and
 // (fuse_polar) run the polar update of gate i.
-__device__ void bwd_finish_e(const BwdParams &P, const GateDesc &G, int jslot, int s, BwdShared &sh, double e);
-__device__ void bwd_finish(const BwdParams &P, const GateDesc &G, int jslot, int s, BwdShared &sh) {
+__device__ void bwd_finish_e(const BwdParams &P, const GateDesc &G, int jslot, int s, BwdShared &sh, double e,
+                             int kind);
+__device__ void bwd_finish(const BwdParams &P, const GateDesc &G, int jslot, int s, BwdShared &sh, int kind) {
   if (P.dbg && threadIdx.x == 0) atomicMax(P.dbg + 4 * G.env_gate + 1, gtimer());
   const double *pp = P.partials + (long long)jslot * P.nb * 32 + threadIdx.x;
   double e = 0.0;
@@ -378,12 +378,14 @@ __device__ void bwd_finish(const BwdParams &P, const GateDesc &G, int jslot, int
     for (int q = 0; q < FLIGHT; ++q)
       if (b0 + q < P.nb) e += xb[q];
   }
-  bwd_finish_e(P, G, jslot, s, sh, e);
+  bwd_finish_e(P, G, jslot, s, sh, e, kind);
 }
 
 // Warp 0 of the finishing CTA holds the reduced E (lane = re/im of entry lane/2):
-// store it and (fuse_polar) run the gate update.
-__device__ void bwd_finish_e(const BwdParams &P, const GateDesc &G, int jslot, int s, BwdShared &sh, double e) {
+// store it and (fuse_polar) run the gate update (kind: loaded before the
+// election so its global load is off the critical path).
+__device__ void bwd_finish_e(const BwdParams &P, const GateDesc &G, int jslot, int s, BwdShared &sh, double e,
+                             int kind) {
   sh.sum32[threadIdx.x] = e;
   if (!P.fuse_polar) P.e_red[(long long)jslot * 32 + threadIdx.x] = e;
   __syncwarp();
@@ -391,7 +393,7 @@ __device__ void bwd_finish_e(const BwdParams &P, const GateDesc &G, int jslot, i
   if (!P.fuse_polar) return;
   const long long gi = (long long)s * P.K + G.env_gate;
   polar_write(sh.sum32, P.gates_w + gi * 16, P.vprev ? P.vprev + gi * 16 : nullptr, P.beta,
-              P.kinds ? P.kinds[G.env_gate] : 0, P.sig ? P.sig + gi : nullptr,
+              kind, P.sig ? P.sig + gi : nullptr,
               P.env_trace ? P.env_trace + ((long long)G.env_gate * P.S + s) * 16 : nullptr, sh.scratch);
   if (P.dbg && threadIdx.x == 0) atomicMax(P.dbg + 4 * G.env_gate + 3, gtimer());
 }
@@ -405,10 +407,11 @@ __global__ void __launch_bounds__(BWD_THREADS, QFS_BWD_MINB) bwd_kernel(const Bw
   const Slot sl = P.slots[jslot];
   if (!bwd_gate_partial<NU, TP0, TP1, UPD>(P, P.g, jslot, sl.s, (unsigned)sl.m, false, sh, stage_buf))
     return;
+  const int kind = P.kinds ? __ldg(P.kinds + P.g.env_gate) : 0;
   const int ng = (P.nb + RED_GS - 1) / RED_GS;
   if (ng <= 1 || !P.counters1) {
     if (!warp0_elect_last(&P.counters[jslot], (unsigned)P.nb)) return;
-    bwd_finish(P, P.g, jslot, sl.s, sh);
+    bwd_finish(P, P.g, jslot, sl.s, sh, kind);
     return;
   }
   // two-level ordered reduction of the CTA partials (many CTAs per start, e.g.
@@ -437,7 +440,7 @@ __global__ void __launch_bounds__(BWD_THREADS, QFS_BWD_MINB) bwd_kernel(const Bw
 #pragma unroll
   for (int q = 0; q < RED_GMAX; ++q)
     if (q < ng) e += yb[q];
-  bwd_finish_e(P, P.g, jslot, sl.s, sh, e);
+  bwd_finish_e(P, P.g, jslot, sl.s, sh, e, kind);
 }
 
 template <int NU, int TP0, int TP1, bool UPD>
@@ -483,7 +486,7 @@ __global__ void __launch_bounds__(BWD_THREADS, QFS_BWD_MINB) bwd_persistent_kern
                       : gate_dispatch_one<4, 3, 2, true>(P, G, j, sl.s, Ms, sh, stage_buf, wf, wt);
     }
     if (w0 && warp0_elect_last(&P.counters[j], (unsigned)P.nb)) {
-      bwd_finish(P, G, j, sl.s, sh);
+      bwd_finish(P, G, j, sl.s, sh, P.kinds ? P.kinds[i] : 0);
       __threadfence();
       if (threadIdx.x == 0) st_release(P.flags + j, (unsigned)(P.K - i));
     }
@@ -985,10 +988,9 @@ __global__ void polar_batch_kernel(const double2 *env, const double2 *g_old, dou
     const double2 go = g_old[(long long)ii * 16 + 4 * (l & 3) + (l >> 2)];
     e = make_double2((1.0 - beta) * e.x + beta * go.x, (1.0 - beta) * e.y - beta * go.y);
   }
-  const double2 v0 = make_double2((l % 5 == 0) ? 1.0 : 0.0, 0.0);
   double2 g, v;
   double ss;
-  hw_polar(e, v0, g, v, ss, scratch[w] + 2 * (lane & 16));
+  hw_polar(e, nullptr, g, v, ss, scratch[w] + 2 * (lane & 16));
   if (valid) {
     g_new[(long long)i * 16 + l] = g;
     if (l == 0) sig[i] = ss;

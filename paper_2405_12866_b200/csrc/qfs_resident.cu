@@ -169,6 +169,7 @@ struct ResSmem {
   double *cbuf;   // [2] CTA partial costs (train, validation)
   double2 *scr;   // [64] polar scratch (32 per half warp)
   int2 *pr;       // [K] qubit pairs
+  int *kinds;     // [K] gate kinds
   double2 *phi;   // [2^n][ld]
   double2 *chi;   // [2^n][ld]
 };
@@ -181,7 +182,8 @@ __device__ ResSmem res_carve(unsigned char *base, int K, int n, int ld) {
   m.cbuf = m.buf + 64;
   m.scr = (double2 *)(m.cbuf + 2);
   m.pr = (int2 *)(m.scr + 64);
-  uintptr_t p = (uintptr_t)(m.pr + K);
+  m.kinds = (int *)(m.pr + K);
+  uintptr_t p = (uintptr_t)(m.kinds + K);
   p = (p + 15) & ~(uintptr_t)15;
   m.phi = (double2 *)p;
   m.chi = m.phi + ((size_t)ld << n);
@@ -201,7 +203,10 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
   const unsigned rank = cl_rank(), C = cl_size();
 
   pdl_wait();
-  for (int k = tid; k < K; k += RES_THREADS) sm.pr[k] = P.pairs[k];
+  for (int k = tid; k < K; k += RES_THREADS) {
+    sm.pr[k] = P.pairs[k];
+    sm.kinds[k] = P.kinds ? P.kinds[k] : 0;
+  }
   // diagnostics: phase times of cluster 0, rank 0 (thread 0), summed over gates
   const bool dbg = P.dbg && cl_id() == 0 && rank == 0 && tid == 0;
   unsigned long long t_prev = 0, ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -263,10 +268,10 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
         double2 ev = make_double2(__shfl_sync(FULL, e, 2 * l), __shfl_sync(FULL, e, 2 * l + 1));
         double2 *gi = sm.G + 16 * i;
         if (P.env_trace && rank == 0 && lane < 16) P.env_trace[((long long)i * P.S + s) * 16 + l] = ev;
-        const int kind = P.kinds ? P.kinds[i] : 0;
+        const int kind = sm.kinds[i];
         double2 g, v;
         double ss;
-        gate_update(kind, ev, gi, P.beta, make_double2((l % 5 == 0) ? 1.0 : 0.0, 0.0), g, v, ss,
+        gate_update(kind, ev, gi, P.beta, nullptr, g, v, ss,
                     sm.scr + 2 * (lane & 16));
         __syncwarp();
         if (lane < 16 && kind != 1) gi[l] = g;
@@ -610,7 +615,7 @@ cudaError_t launch_val_block(const ValRowParams &p, int n_slots, cudaStream_t st
 
 size_t res_smem_bytes(int n, int K, int ld) {
   size_t b = (size_t)K * 16 * sizeof(double2) + (RES_WARPS * 32 + 64 + 2) * sizeof(double) +
-             64 * sizeof(double2) + (size_t)K * sizeof(int2);
+             64 * sizeof(double2) + (size_t)K * (sizeof(int2) + sizeof(int));
   b = (b + 15) & ~(size_t)15;
   b += 2 * ((size_t)ld << n) * sizeof(double2);
   return b;
