@@ -97,6 +97,7 @@ struct qfs_ctx {
   bool persistent = false;  // QFS_PERSISTENT=1 selects the cooperative whole-backward kernel
   bool val_block = true;    // QFS_VAL_BLOCK=0: one-row-per-CTA validation kernel
   int res_per_sm = 1;       // QFS_RES_PER_SM: resident CTAs per SM the cluster plan targets
+  int res_cmax = 16;        // QFS_RES_CMAX: largest cluster the plan widens to
   int path = 0;             // 0 auto, 1 streamed (B cache in HBM), 2 cluster-resident (qfs_set_path / QFS_PATH)
   size_t stage_bytes = 0;
   // qfs_set_samples_async: up to two sample sets queued in device staging
@@ -486,7 +487,7 @@ bool res_plan(const qfs_ctx *c, int M_max, int ns, ResPlan &pl) {
       if (res_smem_bytes(c->n, c->K, (M_max + C - 1) / C) <= res_smem_limit(1)) break;
     if (C > 16) return false;
   }
-  while (C < 16 && (long long)ns * 2 * C <= 148LL * per_sm && (M_max + 2 * C - 1) / (2 * C) >= 2) C *= 2;
+  while (C < c->res_cmax && (long long)ns * 2 * C <= 148LL * per_sm && (M_max + 2 * C - 1) / (2 * C) >= 2) C *= 2;
   pl.C = C;
   pl.ld = (M_max + C - 1) / C;
   pl.smem = res_smem_bytes(c->n, c->K, pl.ld);
@@ -902,6 +903,7 @@ qfs_status create_common(int n, int k, const int32_t *pairs, int device, qfs_ctx
   if (const char *pd = getenv("QFS_PDL")) set_pdl(atoi(pd) != 0);
   if (const char *pa = getenv("QFS_PATH")) c->path = std::max(0, std::min(2, atoi(pa)));
   if (const char *vb = getenv("QFS_VAL_BLOCK")) c->val_block = atoi(vb) != 0;
+  if (const char *rc = getenv("QFS_RES_CMAX")) c->res_cmax = std::max(1, std::min(16, atoi(rc)));
   if (const char *rp = getenv("QFS_RES_PER_SM")) c->res_per_sm = atoi(rp) == 2 ? 2 : 1;
   if (e != cudaSuccess) {
     c->err = std::string("device init: ") + cudaGetErrorString(e);
