@@ -935,6 +935,49 @@ __global__ void fill_words_kernel(unsigned *dst, unsigned value, long long count
     dst[i] = value;
 }
 
+// Initial-gate validation on the device (one thread per gate): bit 0 a
+// non-finite entry, bit 1 ||G^dag G - I||_max > 1e-10, bit 2 a one-qubit slot
+// (kind 2) not of the form u (x) I (tol 1e-10).  OR-ed into *flag.
+__global__ void gate_check_kernel(const double2 *g, long long count, int K, const int *kinds, unsigned *flag) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    double2 G[16];
+    unsigned bad = 0;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      G[e] = g[i * 16 + e];
+      if (!isfinite(G[e].x) || !isfinite(G[e].y)) bad |= 1u;
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        double re = 0.0, im = 0.0;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {  // conj(G[r][a]) G[r][b]
+          re += G[4 * r + a].x * G[4 * r + b].x + G[4 * r + a].y * G[4 * r + b].y;
+          im += G[4 * r + a].x * G[4 * r + b].y - G[4 * r + a].y * G[4 * r + b].x;
+        }
+        if (fabs(re - (a == b ? 1.0 : 0.0)) > 1e-10 || fabs(im) > 1e-10) bad |= 2u;
+      }
+    if (kinds && kinds[i % K] == 2) {
+#pragma unroll
+      for (int lo = 0; lo < 4; ++lo)
+#pragma unroll
+        for (int li = 0; li < 4; ++li) {
+          const double2 e = G[4 * lo + li];
+          if ((lo >> 1) != (li >> 1)) {
+            if (fabs(e.x) > 1e-10 || fabs(e.y) > 1e-10) bad |= 4u;
+          } else {
+            const double2 f = G[4 * (lo ^ 2) + (li ^ 2)];
+            if (fabs(e.x - f.x) > 1e-10 || fabs(e.y - f.y) > 1e-10) bad |= 4u;
+          }
+        }
+    }
+    if (bad) atomicOr(flag, bad);
+  }
+}
+
 __global__ void identity_fill_kernel(double2 *v, long long count16) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count16 * 16;
        i += (long long)gridDim.x * blockDim.x)
@@ -1198,6 +1241,14 @@ cudaError_t launch_fill_words(unsigned *dst, unsigned value, long long count, cu
   if (count <= 0) return cudaSuccess;
   const long long blocks = std::min<long long>((count + 255) / 256, 148 * 8);
   fill_words_kernel<<<(unsigned)blocks, 256, 0, st>>>(dst, value, count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gate_check(const double2 *g, long long count, int K, const int *kinds, unsigned *flag,
+                              cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  const long long blocks = std::min<long long>((count + 127) / 128, 148 * 4);
+  gate_check_kernel<<<(unsigned)blocks, 128, 0, st>>>(g, count, K, kinds, flag);
   return cudaGetLastError();
 }
 

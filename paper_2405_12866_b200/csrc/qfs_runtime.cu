@@ -115,6 +115,9 @@ struct qfs_ctx {
   double2 *h_gates = nullptr;
   size_t h_gates_cap = 0;
   Slot *h_slots = nullptr;  // mapped pinned slot table
+  unsigned *h_check = nullptr;  // pinned read-back of the gate-check flag
+  unsigned *d_check = nullptr;
+  bool check_pending = false;
   size_t h_slots_cap = 0;
   cudaStream_t st_copy = nullptr;
   // graph cache
@@ -269,30 +272,6 @@ void prof_collect(qfs_ctx *c) {
   c->prec.clear();
 }
 
-bool finite_all(const double *p, size_t cnt) {
-  for (size_t i = 0; i < cnt; ++i)
-    if (!std::isfinite(p[i])) return false;
-  return true;
-}
-
-// initial gates must be unitary (||G^dag G - I||_max <= 1e-10)
-bool unitary_all(const double *g, size_t count) {
-  for (size_t q = 0; q < count; ++q) {
-    const double *G = g + q * 32;
-    for (int a = 0; a < 4; ++a)
-      for (int b = 0; b < 4; ++b) {
-        double re = 0, im = 0;
-        for (int r = 0; r < 4; ++r) {
-          double ar = G[2 * (4 * r + a)], ai = -G[2 * (4 * r + a) + 1];  // conj(G[r][a])
-          double br = G[2 * (4 * r + b)], bi = G[2 * (4 * r + b) + 1];
-          re += ar * br - ai * bi;
-          im += ar * bi + ai * br;
-        }
-        if (std::fabs(re - (a == b ? 1.0 : 0.0)) > 1e-10 || std::fabs(im) > 1e-10) return false;
-      }
-  }
-  return true;
-}
 
 // CTAs per start: one full wave over the 148 SMs (resident CTAs per SM = bpsm),
 // never more CTAs than 256-item chunks.
@@ -815,27 +794,27 @@ qfs_status run_sweep(qfs_ctx *c, const SweepSpec &sp, std::vector<double> &csum,
   return QFS_OK;
 }
 
+// The initial gates are validated on the device (gate_check_kernel: finite,
+// unitary to 1e-10, one-qubit slots of the form u (x) I) into a device flag;
+// gate_check_result reads it back after the first sweep's synchronisation
+// (the caller gets QFS_ERR_NUMERIC instead of results; no host-side O(S K)
+// pass on the critical path of every call).
+qfs_status gate_check_result(qfs_ctx *c) {
+  if (!c->check_pending) return QFS_OK;
+  c->check_pending = false;
+  CUDA_TRY(c, cudaMemcpyAsync(c->h_check, c->d_check, sizeof(unsigned), cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(c, cudaStreamSynchronize(c->st));
+  const unsigned bad = *c->h_check;
+  if (bad & 1u) return fail(c, QFS_ERR_NUMERIC, "non-finite initial gate");
+  if (bad & 2u) return fail(c, QFS_ERR_NUMERIC, "initial gate not unitary (tol 1e-10)");
+  if (bad & 4u) return fail(c, QFS_ERR_NUMERIC, "one-qubit gate slot is not of the form u (x) I (tol 1e-10)");
+  return QFS_OK;
+}
+
 qfs_status upload_gates(qfs_ctx *c, int s, const double *init) {
-  if (!finite_all(init, (size_t)s * c->K * 32)) return fail(c, QFS_ERR_NUMERIC, "non-finite initial gate");
-  if (!unitary_all(init, (size_t)s * c->K)) return fail(c, QFS_ERR_NUMERIC, "initial gate not unitary (tol 1e-10)");
-  // one-qubit variable slots must hold u (x) I: zero off the two diagonal 2x2
-  // blocks (local index l = b(p0) + 2 b(p1)), equal blocks (tol 1e-10)
-  for (int st = 0; st < s; ++st)
-    for (int k = 0; k < c->K; ++k) {
-      if (c->kinds[k] != QFS_GATE_VAR1) continue;
-      const double *g = init + ((size_t)st * c->K + k) * 32;
-      for (int lo = 0; lo < 4; ++lo)
-        for (int li = 0; li < 4; ++li) {
-          const double *e = g + 2 * (4 * lo + li);
-          bool ok;
-          if ((lo >> 1) != (li >> 1)) ok = std::fabs(e[0]) <= 1e-10 && std::fabs(e[1]) <= 1e-10;
-          else {
-            const double *f = g + 2 * (4 * (lo ^ 2) + (li ^ 2));  // same entry of the other block
-            ok = std::fabs(e[0] - f[0]) <= 1e-10 && std::fabs(e[1] - f[1]) <= 1e-10;
-          }
-          if (!ok) return fail(c, QFS_ERR_NUMERIC, "one-qubit gate slot is not of the form u (x) I (tol 1e-10)");
-        }
-    }
+  if (!c->h_check) {
+    CUDA_TRY(c, cudaMallocHost((void **)&c->h_check, sizeof(unsigned)));
+  }
   const size_t gb = (size_t)s * c->K * 16 * sizeof(double2);
   if (gb > c->h_gates_cap) {
     if (c->h_gates) cudaFreeHost(c->h_gates);
@@ -850,6 +829,13 @@ qfs_status upload_gates(qfs_ctx *c, int s, const double *init) {
   double2 *dh = nullptr;
   CUDA_TRY(c, cudaHostGetDevicePointer((void **)&dh, c->h_gates, 0));
   CUDA_TRY(c, launch_copy(c->d_gates, dh, (long long)s * c->K * 16, c->st));
+  {
+    // device-side flag, read back (device -> host, 4 bytes) after the first sweep
+    if (!c->d_check) CUDA_TRY(c, cudaMalloc(&c->d_check, sizeof(unsigned)));
+    CUDA_TRY(c, launch_fill_words(c->d_check, 0u, 1, c->st));
+    CUDA_TRY(c, launch_gate_check(c->d_gates, (long long)s * c->K, c->K, c->d_kinds, c->d_check, c->st));
+    c->check_pending = true;
+  }
   CUDA_TRY(c, launch_identity_fill(c->d_vprev, (long long)s * c->K, c->st));
   c->launches++;
   return QFS_OK;
@@ -1132,6 +1118,7 @@ qfs_status qfs_trace_sweeps(qfs_ctx *c, int s, const double *init_gates, int m, 
   std::vector<double> csum, cval;
   for (int t = 0; t < n_sweeps; ++t) {
     if ((st = run_sweep(c, sp, csum, cval)) != QFS_OK) return st;
+    if ((st = gate_check_result(c)) != QFS_OK) return st;
     if (env_trace)
       CUDA_TRY(c, cudaMemcpy(env_trace + (size_t)t * tr * 2, c->d_env_trace, tr * sizeof(double2),
                              cudaMemcpyDeviceToHost));
@@ -1147,7 +1134,7 @@ qfs_status qfs_trace_sweeps(qfs_ctx *c, int s, const double *init_gates, int m, 
         for (int q = 0; q < s; ++q) sigma_trace[((size_t)t * c->K + i) * s + q] = sg[(size_t)q * c->K + i];
     }
   }
-  return QFS_OK;
+  return gate_check_result(c);  // n_sweeps == 0: still report invalid gates
 }
 
 qfs_status qfs_bench_sweeps(qfs_ctx *c, int s, const double *init_gates, int m, int n_sweeps,
@@ -1171,6 +1158,7 @@ qfs_status qfs_bench_sweeps(qfs_ctx *c, int s, const double *init_gates, int m, 
   CUDA_TRY(c, cudaEventRecord(e0, c->st));
   for (int t = 0; t < n_sweeps; ++t)
     if ((st = run_sweep(c, sp, csum, cval)) != QFS_OK) return st;
+    if ((st = gate_check_result(c)) != QFS_OK) return st;
   CUDA_TRY(c, cudaEventRecord(e1, c->st));
   CUDA_TRY(c, cudaEventSynchronize(e1));
   float ms = 0;
@@ -1178,7 +1166,7 @@ qfs_status qfs_bench_sweeps(qfs_ctx *c, int s, const double *init_gates, int m, 
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (sec) *sec = ms * 1e-3;
-  return QFS_OK;
+  return gate_check_result(c);
 }
 
 // Controller (readings R7-R14, R16).
@@ -1221,6 +1209,7 @@ qfs_status qfs_instantiate(qfs_ctx *c, int s, const double *init_gates, const qf
     if (!sp.slots.empty()) {
       if ((st = ensure_state(c, s, sp.M_max, c->V)) != QFS_OK) return st;
       if ((st = run_sweep(c, sp, csum, cval)) != QFS_OK) return st;
+      if ((st = gate_check_result(c)) != QFS_OK) return st;
       for (size_t j = 0; j < sp.slots.size(); ++j) {
         S_ &a = A[sp.slots[j].s];
         a.c_train = csum[j] / a.M;
@@ -1475,6 +1464,8 @@ void qfs_destroy(qfs_ctx *c) {
   dfree(c->d_partials); dfree(c->d_ered); dfree(c->d_sig); dfree(c->d_csum); dfree(c->d_rowout);
   dfree(c->d_cval); dfree(c->d_counters); dfree(c->d_slots); dfree(c->d_env_trace);
   dfree(c->d_stage); dfree(c->d_vprev); dfree(c->d_desc);
+  if (c->h_check) cudaFreeHost(c->h_check);
+  dfree(c->d_check);
   if (c->h_gates) cudaFreeHost(c->h_gates);
   if (c->h_slots) cudaFreeHost(c->h_slots);
   if (c->st_copy) {
