@@ -125,7 +125,10 @@ qfs_status qfs_set_samples_device(qfs_ctx *c, int m_pool, const void *dx, const 
 /* Instantiate from s starts in lockstep (P:378 multistarts): init_gates host
  * [s][k][4][4][2]; out_gates host [s][k][4][4][2]; out host [s]; *winner = the
  * lowest-index start converged at the earliest converging sweep, else the
- * minimum c_train start (ties: lower index). */
+ * minimum c_train start (ties: lower index).  The initial gates are validated
+ * on the device (finite; ||G^dag G - I||_max <= 1e-10; QFS_GATE_VAR1 slots of
+ * the form u (x) I); a failure is reported as QFS_ERR_NUMERIC after the first
+ * sweep, and then out_gates / out are not written. */
 qfs_status qfs_instantiate(qfs_ctx *c, int s, const double *init_gates, const qfs_params *p,
                            double *out_gates, qfs_result *out, int *winner);
 
