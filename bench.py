@@ -44,6 +44,7 @@ sys.path.insert(0, ROOT)
 METRIC = "QFactor-Sample sweeps/sec + time-to-solution per instantiation; % HBM/FP64 peak"
 UNIT = "start-sweeps/s"
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2
+L2_RMW_64MIB_GBS = 9209.1  # profiles/r1_peaks_microbench.json (l2loop_64MiB_rmw_gbs)
 
 
 def load_peaks():
@@ -298,6 +299,11 @@ def main():
                 "avg_launch_us": round(pd["ms"] / pd["launches"] * 1e3, 3),
                 "bytes_per_launch": pd["bytes"] / pd["launches"], "flops_per_launch": pd["flops"] / pd["launches"],
                 "pipe": "fp64" if bound == "alu" else None,
+                # the streamed backward's working set (chi + B_i, ~67 MB at C4) is
+                # L2-resident in part: its algorithmic bytes against the measured
+                # L2 read+write bandwidth at a 64 MiB working set (tools/peaks.cu)
+                "l2_rmw_peak_gbs": L2_RMW_64MIB_GBS if bound == "hbm" else None,
+                "frac_of_l2_rmw": round(achieved / L2_RMW_64MIB_GBS, 4) if bound == "hbm" else None,
                 "share_of_kernel_time": round(pd["ms"] / tot_ms, 4),
                 "profiled_ms_per_step": round(prof_step_ms, 4),
                 "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
