@@ -205,9 +205,18 @@ def main():
     import torch.distributed as dist
     from paper_2405_12866_b200 import build, qfs
     build.build()
+    # one process per GPU; QFS_BENCH_PG=gloo is a functional check of the
+    # multi-rank path on a box with fewer GPUs (ranks share devices; its
+    # numbers are not measurements)
+    pg = os.environ.get("QFS_BENCH_PG", "nccl")
+    if pg != "nccl":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if pg == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(pg)
 
     # seeded synthetic problem; starts of rank r are [r*S, (r+1)*S) of the seeded stream
     prob = I.make_problem(args.config, init="R", s=s_per * world)
@@ -226,7 +235,7 @@ def main():
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if pg == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
