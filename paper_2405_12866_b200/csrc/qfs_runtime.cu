@@ -452,6 +452,9 @@ struct ResPlan {
 };
 bool res_plan(const qfs_ctx *c, int M_max, int ns, ResPlan &pl) {
   if (c->path == 1 || (c->mode == 1 && c->world > 1) || c->n > 13 || M_max < 1) return false;
+  // auto: resident only up to n = 10 — measured crossover (profiles/r1_sweep_map.jsonl:
+  // n <= 10 resident 1.3-1.9x faster, n = 11 / 12 streamed 1.14x / 1.40x faster)
+  if (c->path == 0 && c->n > 10) return false;
   // one CTA per SM (QFS_RES_PER_SM=2: two, <= 113 KB and <= 128 registers
   // each — measured slower: the per-gate chain is latency-bound, not
   // throughput-bound); then widen the cluster while the CTAs of all starts
