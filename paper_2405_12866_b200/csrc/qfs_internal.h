@@ -168,6 +168,7 @@ struct ApplyParams {
 // ---- launchers (qfs_kernels.cu); all return cudaGetLastError() ----
 cudaError_t launch_bwd(const BwdParams &p, int n_slots, cudaStream_t st);
 cudaError_t launch_bwd_persistent(const BwdParams &p, int n_slots, cudaStream_t st);
+int fwd2_min_blocks();             // CTAs per SM the two-gate forward kernel is compiled for
 int bwd_persistent_ctas_per_sm();  // co-resident CTAs per SM of the persistent kernel
 cudaError_t launch_polar(const PolarParams &p, int n_slots, cudaStream_t st);
 cudaError_t launch_final(const FinalParams &p, int n_slots, cudaStream_t st);

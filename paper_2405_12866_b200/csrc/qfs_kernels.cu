@@ -39,6 +39,18 @@ namespace {
 #ifndef QFS_BWD_MINB
 #define QFS_BWD_MINB 1
 #endif
+#ifndef QFS_FWD2_MINB
+#define QFS_FWD2_MINB 1
+#endif
+#ifndef QFS_FWD2_PF
+#define QFS_FWD2_PF 1      // two-gate forward: prefetch the next item's amplitudes into registers
+#endif
+#ifndef QFS_FWD2_GSMEM
+#define QFS_FWD2_GSMEM QFS_FWD2_PF  // re-read gate entries from shared memory (frees 128 registers)
+#endif
+#ifndef QFS_FWD2_HINT
+#define QFS_FWD2_HINT 1    // L2 hints: 1 B_{k+1} stores evict_first, 2 B_{k+2} evict_last, 4 B_k loads evict_first
+#endif
 constexpr int BWD_THREADS = QFS_BWD_THREADS;
 constexpr int BWD_STAGES = QFS_BWD_STAGES;  // LDGSTS pipeline depth of the backward kernel
 constexpr int FWD_THREADS = 256;
@@ -726,8 +738,21 @@ __global__ void __launch_bounds__(FWD_THREADS, 3) fwd_gate_kernel(const FwdGateP
 // warp accesses for any pair).  Local bits 0,1 = gate k's pair; gate k+1's pair
 // sits at local (TP0, TP1).  Per amplitude: 16 B read, 32 B written, instead of
 // 32 B read and 32 B written by two single-gate passes.
+// Gate entry from shared memory.  With QFS_FWD2_MINB > 1 the load is volatile
+// so it is re-issued per use (a broadcast LDS) instead of hoisted: hoisting
+// both gates costs 128 registers and pins the kernel at one CTA per SM.
+__device__ __forceinline__ double2 gval(const double2 *p) {
+#if QFS_FWD2_MINB > 1 || QFS_FWD2_GSMEM
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return v;
+#else
+  return *p;
+#endif
+}
+
 template <int NU, int TP0, int TP1>
-__global__ void __launch_bounds__(FWD_THREADS, 1) fwd2_kernel(const Fwd2Params P) {
+__global__ void __launch_bounds__(FWD_THREADS, QFS_FWD2_MINB) fwd2_kernel(const Fwd2Params P) {
   constexpr int NV = 1 << NU;
   constexpr int NQ = NV / 4;
   __shared__ double2 sG[2][16];
@@ -752,47 +777,84 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) fwd2_kernel(const Fwd2Params P
   uint32_t ins[NU];
 #pragma unroll
   for (int q = 0; q < NU; ++q) ins[q] = P.ins[q];
-  for (unsigned w = beg + threadIdx.x; w < end; w += blockDim.x) {
+  auto locate = [&](unsigned w) {  // (first amplitude, sample) of item w
     unsigned g = fdm.div(w);
     const unsigned m = w - g * Ms;
 #pragma unroll
     for (int q = 0; q < NU; ++q) g = insert_zero32(g, ins[q]);
-    const double2 *sp = src + (g * ssa + m);
-    double2 v[NV];
+    return make_uint2(g, m);
+  };
+#if QFS_FWD2_HINT
+  const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+#endif
+  auto load = [&](unsigned w, double2 *v) {
+    const uint2 gm = locate(w);
+    const double2 *sp = src + (gm.x * ssa + gm.y);
 #pragma unroll
-    for (int u = 0; u < NV; ++u) v[u] = sp[(unsigned)P.off[u] * ssa];
+    for (int u = 0; u < NV; ++u) {
+#if QFS_FWD2_HINT & 4
+      v[u] = ld_hint(sp + (unsigned)P.off[u] * ssa, pol_first);
+#else
+      v[u] = sp[(unsigned)P.off[u] * ssa];
+#endif
+    }
+  };
+  auto store = [&](double2 *p, const double2 *v, int which) {
+#pragma unroll
+    for (int u = 0; u < NV; ++u) {
+      double2 *q = p + (unsigned)P.off[u] * dsa;
+#if QFS_FWD2_HINT & 3
+      if ((QFS_FWD2_HINT & 1) && which == 1) st_hint(q, v[u], pol_first);
+      else if ((QFS_FWD2_HINT & 2) && which == 2) st_hint(q, v[u], pol_last);
+      else *q = v[u];
+#else
+      *q = v[u];
+#endif
+    }
+  };
+  double2 v[NV];
+#if QFS_FWD2_PF
+  double2 vn[NV];
+  if (beg + threadIdx.x < end) load(beg + threadIdx.x, vn);
+#endif
+  for (unsigned w = beg + threadIdx.x; w < end; w += blockDim.x) {
+    const uint2 gm = locate(w);  // recomputed (cheap) instead of carried in registers
+    const unsigned o = gm.x * dsa + gm.y;
+#if QFS_FWD2_PF
+#pragma unroll
+    for (int u = 0; u < NV; ++u) v[u] = vn[u];
+    if (w + blockDim.x < end) load(w + blockDim.x, vn);  // next item's loads in flight during this one
+#else
+    load(w, v);
+#endif
     // gate k on local bits (0,1)
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
-      double2 o[4];
+      double2 o4[4];
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
-        o[a] = make_double2(0.0, 0.0);
+        o4[a] = make_double2(0.0, 0.0);
 #pragma unroll
-        for (int b = 0; b < 4; ++b) cfma(o[a], sG[0][4 * a + b], v[4 * q + b]);
+        for (int b = 0; b < 4; ++b) cfma(o4[a], gval(&sG[0][4 * a + b]), v[4 * q + b]);
       }
 #pragma unroll
-      for (int a = 0; a < 4; ++a) v[4 * q + a] = o[a];
+      for (int a = 0; a < 4; ++a) v[4 * q + a] = o4[a];
     }
-    double2 *p1 = d1 + (g * dsa + m);
-#pragma unroll
-    for (int u = 0; u < NV; ++u) p1[(unsigned)P.off[u] * dsa] = v[u];
+    store(d1 + o, v, 1);
     // gate k+1 on local bits (TP0, TP1)
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
-      double2 o[4];
+      double2 o4[4];
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
-        o[a] = make_double2(0.0, 0.0);
+        o4[a] = make_double2(0.0, 0.0);
 #pragma unroll
-        for (int b = 0; b < 4; ++b) cfma(o[a], sG[1][4 * a + b], v[pv_idx<NU, TP0, TP1>(q, b)]);
+        for (int b = 0; b < 4; ++b) cfma(o4[a], gval(&sG[1][4 * a + b]), v[pv_idx<NU, TP0, TP1>(q, b)]);
       }
 #pragma unroll
-      for (int a = 0; a < 4; ++a) v[pv_idx<NU, TP0, TP1>(q, a)] = o[a];
+      for (int a = 0; a < 4; ++a) v[pv_idx<NU, TP0, TP1>(q, a)] = o4[a];
     }
-    double2 *p2 = d2 + (g * dsa + m);
-#pragma unroll
-    for (int u = 0; u < NV; ++u) p2[(unsigned)P.off[u] * dsa] = v[u];
+    store(d2 + o, v, 2);
   }
   pdl_trigger();
 }
@@ -1098,6 +1160,8 @@ cudaError_t launch_bwd(const BwdParams &p, int n_slots, cudaStream_t st) {
 #undef QFS_BWD
   return cudaGetLastError();
 }
+
+int fwd2_min_blocks() { return QFS_FWD2_MINB; }
 
 int bwd_persistent_ctas_per_sm() {
   static int cached = -1;

@@ -549,7 +549,7 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
           if ((v >> t) & 1) o |= 1LL << loc[t];
         f.off[v] = v < (1 << nu) ? o : 0;
       }
-      f.nb = blocks_per_start(((long long)M_max * N) >> nu, ns, 1);
+      f.nb = blocks_per_start(((long long)M_max * N) >> nu, ns, fwd2_min_blocks());
       f.src = src;
       f.dst1 = ViewW{Bk(k + 1), sS, Mc, 1};
       f.dst2 = ViewW{Bk(k + 2), sS, Mc, 1};
