@@ -329,12 +329,15 @@ def main():
     h2d = (hx.numel() + hy.numel() + hxv.numel() + hyv.numel()) * 16 + init.nbytes
     d2h = init.nbytes + s_per * 32
     g = gates
-    e2e_steps = max(3, min(args.steps, 10))
+    e2e_steps = max(3, args.steps)
 
     def queue_samples():  # qfs_set_samples_async: H2D on the copy stream, consumed by the next call
         ctx.set_samples_async_host_ptr(hx.shape[0], hx.data_ptr(), hy.data_ptr(), hxv.shape[0], hxv.data_ptr(),
                                        hyv.data_ptr())
 
+    for _ in range(2):                   # untimed warm-up of the e2e path (staging buffers, graphs)
+        queue_samples()
+        g, _, _ = ctx.instantiate(g, bench_params(1, m))
     barrier()
     t0 = time.perf_counter()
     queue_samples()                      # step 0's inputs

@@ -1058,18 +1058,24 @@ qfs_status qfs_set_samples_async(qfs_ctx *c, int m_pool, const double *x, const 
   if (!c->st_copy) CUDA_TRY(c, cudaStreamCreateWithFlags(&c->st_copy, cudaStreamNonBlocking));
   qfs_ctx::Staged &g = c->stg[(c->stg_head + c->stg_count) % 2];
   const size_t bxy = (size_t)m_pool * c->N * sizeof(double2), bv = (size_t)v * c->N * sizeof(double2);
-  if (!g.ev) CUDA_TRY(c, cudaEventCreateWithFlags(&g.ev, cudaEventDisableTiming));
-  if (bxy > g.cap_xy) {
-    dfree(g.x); dfree(g.y);
-    CUDA_TRY(c, cudaMalloc(&g.x, bxy));
-    CUDA_TRY(c, cudaMalloc(&g.y, bxy));
-    g.cap_xy = bxy;
-  }
-  if (bv > g.cap_v) {
-    dfree(g.xv); dfree(g.yv);
-    CUDA_TRY(c, cudaMalloc(&g.xv, bv));
-    CUDA_TRY(c, cudaMalloc(&g.yv, bv));
-    g.cap_v = bv;
+  // both staging slots are sized together: cudaMalloc / cudaFree synchronise,
+  // so a first-time allocation of the second slot must not land mid-pipeline
+  for (qfs_ctx::Staged &h : c->stg) {
+    if (!h.ev) CUDA_TRY(c, cudaEventCreateWithFlags(&h.ev, cudaEventDisableTiming));
+    if (bxy > h.cap_xy) {
+      if (&h != &g && c->stg_count > 0) continue;  // a queued set still lives there
+      dfree(h.x); dfree(h.y);
+      CUDA_TRY(c, cudaMalloc(&h.x, bxy));
+      CUDA_TRY(c, cudaMalloc(&h.y, bxy));
+      h.cap_xy = bxy;
+    }
+    if (bv > h.cap_v) {
+      if (&h != &g && c->stg_count > 0) continue;
+      dfree(h.xv); dfree(h.yv);
+      CUDA_TRY(c, cudaMalloc(&h.xv, bv));
+      CUDA_TRY(c, cudaMalloc(&h.yv, bv));
+      h.cap_v = bv;
+    }
   }
   CUDA_TRY(c, cudaMemcpyAsync(g.x, x, bxy, cudaMemcpyHostToDevice, c->st_copy));
   CUDA_TRY(c, cudaMemcpyAsync(g.y, y, bxy, cudaMemcpyHostToDevice, c->st_copy));

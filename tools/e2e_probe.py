@@ -48,3 +48,19 @@ for _ in range(10):
         dst[pin[0].numel():2 * pin[0].numel()].view(pin[1].shape).copy_(pin[1], non_blocking=True)
     s2.synchronize()
 print("torch H2D only    %.3f ms" % ((time.perf_counter() - t0) * 100))
+# the bench's e2e loop, per-step wall times (the first step pays the unhidden copy)
+ctx2 = qfs.Context(p.n, p.pairs); ctx2.set_samples(p.x, p.y, p.xv, p.yv)
+g2 = p.init
+for _ in range(3): g2, _, _ = ctx2.instantiate(g2, prm)
+torch.cuda.synchronize()
+ts = []
+t0 = time.perf_counter(); q2 = lambda: ctx2.set_samples_async_host_ptr(pin[0].shape[0], pin[0].data_ptr(), pin[1].data_ptr(), 16, pin[2].data_ptr(), pin[3].data_ptr())
+q2()
+for step in range(12):
+    ta = time.perf_counter()
+    if step + 1 < 12: q2()
+    tb = time.perf_counter()
+    g2, _, _ = ctx2.instantiate(g2, prm)
+    ts.append(((tb - ta) * 1e3, (time.perf_counter() - tb) * 1e3))
+print("bench-loop steps (queue ms, instantiate ms):", [(round(a, 3), round(b, 3)) for a, b in ts])
+print("bench-loop total %.3f ms/step" % ((time.perf_counter() - t0) * 1e3 / 12))
