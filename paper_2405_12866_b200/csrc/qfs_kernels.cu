@@ -39,6 +39,9 @@ namespace {
 #ifndef QFS_BWD_MINB
 #define QFS_BWD_MINB 1
 #endif
+#ifndef QFS_BWD_EDRING
+#define QFS_BWD_EDRING 1  // backward: chi store offsets carried from issue to use in registers
+#endif
 #ifndef QFS_FWD2_MINB
 #define QFS_FWD2_MINB 1
 #endif
@@ -201,9 +204,19 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
     ef = g * fsa + m;
     return m < Ms;
   };
+  // chi destination offset of the items in flight (EDRING: computed once, at
+  // issue, and rotated through registers; ~0xffffffff marks an invalid item)
+#if QFS_BWD_EDRING
+  unsigned edr[BWD_STAGES];
+#pragma unroll
+  for (int q = 0; q < BWD_STAGES; ++q) edr[q] = 0xffffffffu;
+#endif
   auto issue_part = [&](int k, bool chi, bool phi) {
     unsigned ec = 0, ed = 0, ef = 0;
     const bool ok = locate(k, ec, ed, ef);
+#if QFS_BWD_EDRING
+    if (chi) edr[BWD_STAGES - 1] = ok ? ed : 0xffffffffu;
+#endif
     double2 *st = stage_buf + (k % BWD_STAGES) * 8 * BWD_THREADS + threadIdx.x;
     if (chi) {
 #pragma unroll
@@ -241,14 +254,26 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
   for (int k = 0; k < BWD_STAGES - 1; ++k) {
     issue_part(k, true, !G.pre);
     cp_async_commit();
+#if QFS_BWD_EDRING
+#pragma unroll
+    for (int q = 0; q < BWD_STAGES - 1; ++q) edr[q] = edr[q + 1];
+#endif
   }
   __syncthreads();
 
   for (int k = 0; k < iters; ++k) {
     issue(k + BWD_STAGES - 1);
     cp_async_wait<BWD_STAGES - 1>();
+#if QFS_BWD_EDRING
+    // after the prologue's shifts edr[q] holds item k + q
+    const unsigned ed = edr[0];
+    const bool valid = ed != 0xffffffffu;
+#pragma unroll
+    for (int q = 0; q < BWD_STAGES - 1; ++q) edr[q] = edr[q + 1];
+#else
     unsigned ec = 0, ed = 0, ef = 0;
     const bool valid = locate(k, ec, ed, ef);
+#endif
     double2 *st = stage_buf + (k % BWD_STAGES) * 8 * BWD_THREADS + threadIdx.x;
     double2 c[4], f[4];
 #pragma unroll
