@@ -39,6 +39,9 @@ namespace {
 #ifndef QFS_BWD_MINB
 #define QFS_BWD_MINB 1
 #endif
+#ifndef QFS_BWD_BYTEOFF
+#define QFS_BWD_BYTEOFF 1  // backward: 32-bit byte offsets from per-start bases for LDGSTS / STG addresses
+#endif
 #ifndef QFS_BWD_EDRING
 #define QFS_BWD_EDRING 1  // backward: chi store offsets carried from issue to use in registers
 #endif
@@ -178,6 +181,10 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
   double2 *cdst = G.chi_dst.base ? G.chi_dst.base + (long long)s * G.chi_dst.ss : nullptr;
   const double2 *fsrc = G.phi.base + (long long)s * G.phi.ss;
   const unsigned csa = (unsigned)G.chi_src.sa, dsa = (unsigned)G.chi_dst.sa, fsa = (unsigned)G.phi.sa;
+#if QFS_BWD_BYTEOFF
+  const char *cbase = (const char *)csrc, *fbase = (const char *)fsrc;
+  char *dbase = (char *)cdst;
+#endif
   unsigned offc[4], offd[4], offf[4];
 #pragma unroll
   for (int l = 0; l < 4; ++l) {
@@ -218,6 +225,21 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
     if (chi) edr[BWD_STAGES - 1] = ok ? ed : 0xffffffffu;
 #endif
     double2 *st = stage_buf + (k % BWD_STAGES) * 8 * BWD_THREADS + threadIdx.x;
+#if QFS_BWD_BYTEOFF
+    // 32-bit byte offsets from the start's base (one start's block < 4 GB):
+    // one add per address instead of 64-bit element arithmetic per address
+    if (!ok) ec = ef = 0u;  // in bounds; nothing is read (src-size 0)
+    if (chi) {
+      const unsigned eb = ec << 4;
+#pragma unroll
+      for (int l = 0; l < 4; ++l) cp_async16(st + l * BWD_THREADS, cbase + (eb + (offc[l] << 4)), ok);
+    }
+    if (phi) {
+      const unsigned eb = ef << 4;
+#pragma unroll
+      for (int l = 0; l < 4; ++l) cp_async16(st + (4 + l) * BWD_THREADS, fbase + (eb + (offf[l] << 4)), ok);
+    }
+#else
     if (chi) {
 #pragma unroll
       for (int l = 0; l < 4; ++l) cp_async16(st + l * BWD_THREADS, csrc + (ok ? ec + offc[l] : 0u), ok);
@@ -226,6 +248,7 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
 #pragma unroll
       for (int l = 0; l < 4; ++l) cp_async16(st + (4 + l) * BWD_THREADS, fsrc + (ok ? ef + offf[l] : 0u), ok);
     }
+#endif
   };
   auto issue = [&](int k) {
     issue_part(k, true, true);
@@ -300,9 +323,15 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
 #pragma unroll
       for (int a = 0; a < 4; ++a) c[a] = o[a];
       if (cdst && valid) {
+#if QFS_BWD_BYTEOFF
+        const unsigned eb = ed << 4;
+#pragma unroll
+        for (int l = 0; l < 4; ++l) *(double2 *)(dbase + (eb + (offd[l] << 4))) = c[l];
+#else
         double2 *dp = cdst + ed;
 #pragma unroll
         for (int l = 0; l < 4; ++l) dp[offd[l]] = c[l];
+#endif
       }
     }
 #ifdef QFS_DIAG_NOCOMPUTE
