@@ -39,6 +39,9 @@ namespace {
 #ifndef QFS_BWD_MINB
 #define QFS_BWD_MINB 1
 #endif
+#ifndef QFS_WIDE_RED
+#define QFS_WIDE_RED 1  // backward, many CTAs per start: one-ticket reduction by all warps of the last CTA
+#endif
 #ifndef QFS_BWD_BYTEOFF
 #define QFS_BWD_BYTEOFF 1  // backward: 32-bit byte offsets from per-start bases for LDGSTS / STG addresses
 #endif
@@ -465,12 +468,53 @@ __device__ void bwd_finish_e(const BwdParams &P, const GateDesc &G, int jslot, i
 }
 
 // One launch per gate (used in sample-sharded mode and by the unit op).
-template <int NU, int TP0, int TP1, bool UPD>
+// WIDE (many CTAs per start, e.g. S = 1): the last CTA to finish sums all CTA
+// partials with all of its warps — warp w sums CTAs [w per, (w+1) per) in CTA
+// order (one L2 round trip for up to 8 x 24 CTAs), then warp 0 sums the warp
+// sums in warp order: deterministic, one ticket on the critical path (C5:
+// 2.7 -> 0.95 us per gate).  A separate instantiation, so the few-CTA path
+// compiles exactly as before.
+template <int NU, int TP0, int TP1, bool UPD, bool WIDE>
 __global__ void __launch_bounds__(BWD_THREADS, QFS_BWD_MINB) bwd_kernel(const BwdParams P) {
   __shared__ BwdShared sh;
   extern __shared__ double2 stage_buf[];  // [BWD_STAGES][8][BWD_THREADS]
   const int jslot = blockIdx.y;
   const Slot sl = P.slots[jslot];
+  if constexpr (WIDE) {
+    constexpr int NWARP = BWD_THREADS / 32, FL = 24;
+    __shared__ unsigned last_cta;  // (not in BwdShared: its size / the dynamic buffer's offset
+                                   // change the few-CTA instantiation's speed, measured)
+    const bool w0 = bwd_gate_partial<NU, TP0, TP1, UPD>(P, P.g, jslot, sl.s, (unsigned)sl.m, false, sh, stage_buf);
+    if (w0) {
+      const bool last = warp0_elect_last(&P.counters[jslot], (unsigned)P.nb);
+      if (threadIdx.x == 0) last_cta = last ? 1u : 0u;
+    }
+    __syncthreads();
+    if (!last_cta) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (P.dbg && threadIdx.x == 0) atomicMax(P.dbg + 4 * P.g.env_gate + 1, gtimer());
+    const int per = (P.nb + NWARP - 1) / NWARP, c0 = warp * per, c1 = min(P.nb, c0 + per);
+    const double *pp = P.partials + (long long)jslot * P.nb * 32 + lane;
+    double e = 0.0;
+    for (int b0 = c0; b0 < c1; b0 += FL) {
+      double xb[FL];
+#pragma unroll
+      for (int q = 0; q < FL; ++q) xb[q] = b0 + q < c1 ? __ldcg(pp + (long long)(b0 + q) * 32) : 0.0;
+#pragma unroll
+      for (int q = 0; q < FL; ++q)
+        if (b0 + q < c1) e += xb[q];
+    }
+    double *ws = reinterpret_cast<double *>(sh.red);  // free again: warp 0 has read its CTA partial
+    ws[warp * 32 + lane] = e;
+    __syncthreads();
+    if (warp != 0) return;
+    const int kind = P.kinds ? __ldg(P.kinds + P.g.env_gate) : 0;
+    e = 0.0;
+#pragma unroll
+    for (int w = 0; w < NWARP; ++w) e += ws[w * 32 + lane];
+    bwd_finish_e(P, P.g, jslot, sl.s, sh, e, kind);
+    return;
+  }
   if (!bwd_gate_partial<NU, TP0, TP1, UPD>(P, P.g, jslot, sl.s, (unsigned)sl.m, false, sh, stage_buf))
     return;
   const int kind = P.kinds ? __ldg(P.kinds + P.g.env_gate) : 0;
@@ -1188,14 +1232,20 @@ cudaError_t launch_bwd(const BwdParams &p, int n_slots, cudaStream_t st) {
   dim3 grid(p.nb, n_slots), block(BWD_THREADS);
   const int smem = BWD_STAGES * 8 * BWD_THREADS * (int)sizeof(double2);
   const GateDesc &g = p.g;
-#define QFS_BWD(NU, A, B, U)                                                                   \
+  const bool wide = QFS_WIDE_RED && p.counters1 && (p.nb + RED_GS - 1) / RED_GS > 1;
+#define QFS_BWD1(NU, A, B, U, W)                                                               \
   do {                                                                                         \
     static bool attr = false;                                                                  \
     if (!attr) {                                                                               \
-      cudaFuncSetAttribute(bwd_kernel<NU, A, B, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+      cudaFuncSetAttribute(bwd_kernel<NU, A, B, U, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
       attr = true;                                                                             \
     }                                                                                          \
-    launch_ex(bwd_kernel<NU, A, B, U>, grid, block, smem, st, p);                              \
+    launch_ex(bwd_kernel<NU, A, B, U, W>, grid, block, smem, st, p);                           \
+  } while (0)
+#define QFS_BWD(NU, A, B, U)            \
+  do {                                  \
+    if (wide) QFS_BWD1(NU, A, B, U, true); \
+    else QFS_BWD1(NU, A, B, U, false);  \
   } while (0)
   if (!g.upd) {
     QFS_BWD(2, 0, 1, false);
@@ -1212,6 +1262,7 @@ cudaError_t launch_bwd(const BwdParams &p, int n_slots, cudaStream_t st) {
     else QFS_BWD(4, 3, 2, true);
   }
 #undef QFS_BWD
+#undef QFS_BWD1
   return cudaGetLastError();
 }
 
