@@ -779,7 +779,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 3) fwd_gate_kernel(const FwdGateP
   const double2 *src = P.src.base + (long long)s * P.src.ss;
   double2 *dst = P.dst.base + (long long)s * P.dst.ss;
   // LDGSTS pipeline (FWD_STAGES-1 items ahead per thread, own slots only)
-  extern __shared__ double2 fstage[];  // [FWD_STAGES][4][FWD_THREADS]
+  extern __shared__ __align__(128) double2 fstage[];  // [FWD_STAGES][4][FWD_THREADS]
   const unsigned stride = blockDim.x;
   const int iters = beg + threadIdx.x < end ? (int)((end - beg - threadIdx.x + stride - 1) / stride) : 0;
   auto locate = [&](int k, unsigned &base, unsigned &m) -> bool {
@@ -963,7 +963,7 @@ __global__ void __launch_bounds__(FWD_THREADS, QFS_FWD2_MINB) fwd2_kernel(const 
 // memory, the K gates are applied in order (gate k+1 staged while gate k runs),
 // then the row's squared distance to yv.
 __global__ void __launch_bounds__(VAL_THREADS) val_row_kernel(const ValRowParams P) {
-  extern __shared__ double2 row[];
+  extern __shared__ __align__(128) double2 row[];
   __shared__ double2 sG[2][16];
   __shared__ double red[VAL_THREADS / 32];
   const int j = blockIdx.y;

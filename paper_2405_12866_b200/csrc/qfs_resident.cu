@@ -37,6 +37,9 @@ namespace {
 #define QFS_RES_THREADS 256
 #endif
 constexpr int RES_THREADS = QFS_RES_THREADS;
+#ifndef QFS_RES_ALIGN
+#define QFS_RES_ALIGN 128  // dynamic shared-memory alignment of the resident / validation kernels
+#endif
 constexpr int RES_WARPS = RES_THREADS / 32;
 constexpr size_t RES_SMEM_MAX = 232448;  // 227 KB opt-in dynamic shared memory per CTA
 constexpr size_t RES_SMEM_MAX2 = 113 * 1024;  // two CTAs per SM (228 KB per SM, 1 KB reserved per CTA)
@@ -195,7 +198,7 @@ __device__ ResSmem res_carve(unsigned char *base, int K, int n, int ld) {
 // start's contraction on the same SM).
 template <int MINB>
 __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResParams P) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(QFS_RES_ALIGN) unsigned char smem_raw[];
   const int K = P.K, n = P.n;
   const unsigned N = 1u << n, ld = (unsigned)P.ld;
   const ResSmem sm = res_carve(smem_raw, K, n, P.ld);
@@ -394,7 +397,7 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
 // post-sweep gates are applied in order, then each row's ||C xv - yv||^2 goes
 // to row_out[j][row] (summed over rows in row order by row_reduce_kernel).
 __global__ void __launch_bounds__(RES_THREADS, 2) val_blk_kernel(const ValRowParams P, int ld) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(QFS_RES_ALIGN) unsigned char smem_raw[];
   __shared__ double red[RES_WARPS];
   const int K = P.K, n = P.n;
   const unsigned N = 1u << n;
@@ -466,7 +469,7 @@ __device__ __forceinline__ void cl_sync() {
 // over DSMEM, between cluster barriers.  Then each row's ||C xv - yv||^2
 // (slices summed in rank order) goes to row_out[j][row].
 __global__ void __launch_bounds__(RES_THREADS, 1) val_cl_kernel(const ValRowParams P, int t) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(QFS_RES_ALIGN) unsigned char smem_raw[];
   __shared__ double red[RES_WARPS];
   __shared__ double half_sum_v;
   const int K = P.K, n = P.n;
