@@ -195,3 +195,88 @@ def bench_sweeps(n, pairs, init_gates, x, y, m, n_sweeps, threads=0):
     _check(lib().qfso_bench_sweeps(n, pr.shape[0], prp, ig.shape[0], igp, m, xp, yp, n_sweeps, threads,
                                    ctypes.byref(sec)), "bench")
     return sec.value
+
+
+# ------------------------------------------------------------------ blocks --
+# Multi-qubit blocks (qfso.h: arity 2 or 3, packed d x d gates).
+
+def _blocks(qubits, arity):
+    qq, qp = _c(np.asarray(qubits).reshape(-1, 3), np.int32)
+    aa, ap = _c(np.asarray(arity).reshape(-1), np.int32)
+    return qq, qp, aa, ap
+
+
+def apply_block(n, arity, q, g, states, dagger=False):
+    psi, pp = _c(np.array(states, dtype=np.complex128, copy=True))
+    qq, qp = _c(list(q) + [0] * (3 - len(q)), np.int32)
+    gg, gp = _c(g)
+    _check(lib().qfso_apply_block(n, arity, qp, gp, int(dagger), psi.shape[0], pp), "apply_block")
+    return psi
+
+
+def environment_block(n, arity, q, phi, chi):
+    f, fp = _c(phi)
+    c, cp = _c(chi)
+    qq, qp = _c(list(q) + [0] * (3 - len(q)), np.int32)
+    d = 1 << arity
+    e = np.zeros((d, d), dtype=np.complex128)
+    _check(lib().qfso_environment_block(n, arity, qp, f.shape[0], fp, cp, e.ctypes.data_as(ctypes.c_void_p)),
+           "environment_block")
+    return e
+
+
+def polar_update_block(env, g_old, beta=0.0):
+    e, ep = _c(env)
+    go, gop = _c(g_old)
+    d = e.shape[0]
+    gn = np.zeros((d, d), np.complex128)
+    ss = ctypes.c_double(0)
+    _check(lib().qfso_polar_update_block(d, ep, gop, ctypes.c_double(beta), gn.ctypes.data_as(ctypes.c_void_p),
+                                         ctypes.byref(ss)), "polar_update_block")
+    return gn, ss.value
+
+
+def trace_sweeps_blocks(n, qubits, arity, init_gates, x, y, m, n_sweeps, beta=0.0, threads=0, kinds=None):
+    """Fixed-M sweeps of a block circuit; init_gates packed [s][G] (inputs.pack_gates).
+    Returns env [t][s*G] (gate-major, qfso.h), gates [t][s][G], cost [t][s], sigma [t][k][s]."""
+    qq, qp, aa, ap = _blocks(qubits, arity)
+    k = aa.shape[0]
+    ig, igp = _c(init_gates)
+    s, gsz = ig.shape
+    xx, xp = _c(x[:m])
+    yy, yp = _c(y[:m])
+    env = np.zeros((n_sweeps, s * gsz), np.complex128)
+    gates = np.zeros((n_sweeps, s, gsz), np.complex128)
+    cost = np.zeros((n_sweeps, s))
+    sig = np.zeros((n_sweeps, k, s))
+    vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    kk, kp = _kinds(kinds, k)
+    _check(lib().qfso_trace_sweeps_blocks(n, k, qp, ap, kp, s, igp, m, xp, yp, ctypes.c_double(beta), n_sweeps,
+                                          vp(env), vp(gates), vp(cost), vp(sig), threads), "trace_sweeps_blocks")
+    return dict(env=env, gates=gates, cost=cost, sigma=sig)
+
+
+def instantiate_blocks(n, qubits, arity, x, y, xv, yv, init_gates, params: dict, threads=0, kinds=None):
+    qq, qp, aa, ap = _blocks(qubits, arity)
+    k = aa.shape[0]
+    ig, igp = _c(init_gates)
+    s, gsz = ig.shape
+    xx, xp = _c(x)
+    yy, yp = _c(y)
+    v = 0 if xv is None else int(np.asarray(xv).shape[0])
+    if v:
+        xvv, xvp = _c(xv)
+        yvv, yvp = _c(yv)
+    else:
+        xvp = yvp = None
+    p = _Params(**{f: params[f] for f, _ in _Params._fields_})
+    out_g = np.zeros((s, gsz), np.complex128)
+    res = (_Result * s)()
+    win = ctypes.c_int(-1)
+    kk, kp = _kinds(kinds, k)
+    _check(lib().qfso_instantiate_blocks(n, k, qp, ap, kp, xx.shape[0], xp, yp, v, xvp, yvp, s, igp,
+                                         ctypes.byref(p), out_g.ctypes.data_as(ctypes.c_void_p), res,
+                                         ctypes.byref(win), threads), "instantiate_blocks")
+    results = [dict(c_train=r.c_train, c_val=r.c_val, sweeps=r.sweeps, restarts=r.restarts,
+                    final_m=r.final_m, term=TERM_NAMES.get(r.term, str(r.term))) for r in res]
+    return out_g, results, win.value

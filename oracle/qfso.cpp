@@ -330,12 +330,291 @@ double validation_cost(int n, int K, const int32_t *pairs, const cd *G, int V, c
   return (double)(sq_distance_sum(n, 0, V, 1, psi.data(), yv) / (long double)V);
 }
 
+// ------------------------------------------------------------ blocks --
+// Multi-qubit blocks (P:57 QFactor updates "possibly
+// multi-qubit" unitary gates without parameterising them).  A block of arity
+// a in {2, 3} acts on qubits q_0..q_{a-1} (as given) with the d x d matrix
+// G[l_out][l_in], d = 2^a, local index l = sum_j b(q_j) 2^j (reading R1
+// extended: the first listed qubit is the least significant local bit).
+// Gates of a circuit are stored packed, gate k at complex offset off_k =
+// sum_{j<k} d_j^2.  Everything below is the same algorithm as the pair code
+// above with 4 replaced by d.
+struct Block {
+  int a;     // arity
+  int q[3];  // qubits (q[2] unused for a = 2)
+};
+inline long blk_base(long r, const Block &b) {
+  int srt[3] = {b.q[0], b.q[1], b.a > 2 ? b.q[2] : 0};
+  for (int i = 0; i < b.a; ++i)
+    for (int j = i + 1; j < b.a; ++j)
+      if (srt[j] < srt[i]) { int t = srt[i]; srt[i] = srt[j]; srt[j] = t; }
+  long v = r;
+  for (int i = 0; i < b.a; ++i) v = insert_zero_bit(v, srt[i]);
+  return v;
+}
+inline long blk_index(long base, int l, const Block &b) {
+  long v = base;
+  for (int j = 0; j < b.a; ++j) v |= (long)((l >> j) & 1) << b.q[j];
+  return v;
+}
+
+void apply_block(int n, const Block &b, const cd *G, int m, double *psi) {
+  const long N = 1L << n;
+  const int d = 1 << b.a;
+  for (int s = 0; s < m; ++s) {
+    double *row = psi + 2 * (long)s * N;
+    for (long r = 0; r < (N >> b.a); ++r) {
+      long base = blk_base(r, b);
+      cd v[8];
+      for (int l = 0; l < d; ++l) v[l] = ld(row, blk_index(base, l, b));
+      for (int lo = 0; lo < d; ++lo) {
+        cd acc = 0;
+        for (int l = 0; l < d; ++l) acc += G[d * lo + l] * v[l];
+        st(row, blk_index(base, lo, b), acc);
+      }
+    }
+  }
+}
+
+void adjoint_d(int d, const cd *A, cd *Ad) {
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j) Ad[d * i + j] = std::conj(A[d * j + i]);
+}
+
+// E[l_in][l_out] = sum_m sum_r phi_m[idx_r(l_in)] conj(chi_m[idx_r(l_out)]) (R4)
+void environment_block(int n, const Block &b, int m0, int m1, int mstride, const double *phi,
+                       const double *chi, cld *E) {
+  const long N = 1L << n;
+  const int d = 1 << b.a;
+  for (int m = m0; m < m1; m += mstride) {
+    const double *f = phi + 2 * (long)m * N;
+    const double *c = chi + 2 * (long)m * N;
+    for (long r = 0; r < (N >> b.a); ++r) {
+      long base = blk_base(r, b);
+      cd fv[8], cv[8];
+      for (int l = 0; l < d; ++l) {
+        fv[l] = ld(f, blk_index(base, l, b));
+        cv[l] = ld(c, blk_index(base, l, b));
+      }
+      for (int x = 0; x < d; ++x)
+        for (int y = 0; y < d; ++y) {
+          cd t = fv[x] * std::conj(cv[y]);
+          E[d * x + y] += cld(t.real(), t.imag());
+        }
+    }
+  }
+}
+
+// Gate update of a d x d block by kind: variable = Y X^dag from the SVD of
+// E' = (1 - beta) E + beta G_old^dag; fixed = unchanged,
+// *sig = Re Tr(E G); a two-qubit block keeps the kinds of gate_update (R24).
+void gate_update_block(int kind, int d, const cd *E, const cd *Gold, double beta, cd *Gnew, double *sig) {
+  if (d == 4) { gate_update(kind, E, Gold, beta, Gnew, sig); return; }
+  if (kind == KIND_FIXED) {
+    cd tr = 0;
+    for (int a = 0; a < d; ++a)
+      for (int c = 0; c < d; ++c) tr += E[d * a + c] * Gold[d * c + a];
+    for (int i = 0; i < d * d; ++i) Gnew[i] = Gold[i];
+    if (sig) *sig = tr.real();
+    return;
+  }
+  cd Ep[64], Gd[64], X[64], Y[64];
+  double sg[8];
+  adjoint_d(d, Gold, Gd);
+  for (int i = 0; i < d * d; ++i) Ep[i] = (1.0 - beta) * E[i] + beta * Gd[i];
+  svd_jacobi<8>(Ep, X, sg, Y);
+  for (int a = 0; a < d; ++a)
+    for (int c = 0; c < d; ++c) {
+      cd acc = 0;
+      for (int j = 0; j < d; ++j) acc += Y[d * a + j] * std::conj(X[d * c + j]);
+      Gnew[d * a + c] = acc;
+    }
+  double ss = 0;
+  for (int j = 0; j < d; ++j) ss += sg[j];
+  if (sig) *sig = ss;
+}
+
+struct BlockCircuit {
+  int n, K, gsz;
+  std::vector<Block> b;
+  std::vector<int> off;  // [K + 1]
+  const int32_t *kinds;
+};
+
+// one sweep of sweep_one's algorithm over blocks
+void sweep_blocks(const BlockCircuit &C, cd *G /*packed, in/out*/, int M, const double *x,
+                  const double *y, double beta, SweepOut *out, std::vector<double> &Bbuf,
+                  std::vector<double> &chi) {
+  const int n = C.n, K = C.K;
+  const long N = 1L << n;
+  const long rowlen = 2 * (long)M * N;
+  Bbuf.resize((size_t)K * rowlen);
+  chi.resize(rowlen);
+  std::memcpy(Bbuf.data(), x, sizeof(double) * rowlen);
+  for (int i = 1; i < K; ++i) {
+    double *Bi = Bbuf.data() + (size_t)i * rowlen;
+    std::memcpy(Bi, Bbuf.data() + (size_t)(i - 1) * rowlen, sizeof(double) * rowlen);
+    apply_block(n, C.b[i - 1], G + C.off[i - 1], M, Bi);
+  }
+  std::memcpy(chi.data(), y, sizeof(double) * rowlen);
+  if (out) { out->env.assign((size_t)C.gsz, cd(0, 0)); out->sig.assign(K, 0.0); }
+  for (int i = K - 1; i >= 0; --i) {
+    const int d = 1 << C.b[i].a;
+    cld Et[64];
+    for (int q = 0; q < d * d; ++q) Et[q] = 0;
+    environment_block(n, C.b[i], 0, M, 1, Bbuf.data() + (size_t)i * rowlen, chi.data(), Et);
+    cd E[64], Gn[64], Gd[64];
+    for (int q = 0; q < d * d; ++q) E[q] = cd((double)Et[q].real(), (double)Et[q].imag());
+    double ss = 0;
+    gate_update_block(C.kinds ? C.kinds[i] : KIND_VAR2, d, E, G + C.off[i], beta, Gn, &ss);
+    for (int q = 0; q < d * d; ++q) G[C.off[i] + q] = Gn[q];
+    if (out) {
+      for (int q = 0; q < d * d; ++q) out->env[C.off[i] + q] = E[q];
+      out->sig[i] = ss;
+    }
+    adjoint_d(d, Gn, Gd);
+    apply_block(n, C.b[i], Gd, M, chi.data());
+  }
+  if (out) out->c_train = (double)(sq_distance_sum(n, 0, M, 1, chi.data(), x) / (long double)M);
+}
+
+double validation_cost_blocks(const BlockCircuit &C, const cd *G, int V, const double *xv, const double *yv) {
+  const long N = 1L << C.n;
+  std::vector<double> psi(xv, xv + 2 * (long)V * N);
+  for (int i = 0; i < C.K; ++i) apply_block(C.n, C.b[i], G + C.off[i], V, psi.data());
+  return (double)(sq_distance_sum(C.n, 0, V, 1, psi.data(), yv) / (long double)V);
+}
+
+// structure check + packing offsets; kinds: 0 variable, 1 fixed, 2 one-qubit (arity 2 only)
+int make_blocks(int n, int k, const int32_t *qubits, const int32_t *arity, const int32_t *kinds,
+                BlockCircuit &C) {
+  if (n < 2 || n > 30 || k < 1 || !qubits || !arity) return 1;
+  C.n = n; C.K = k; C.kinds = kinds;
+  C.b.resize(k);
+  C.off.assign(k + 1, 0);
+  for (int i = 0; i < k; ++i) {
+    Block &b = C.b[i];
+    b.a = arity[i];
+    if (b.a != 2 && b.a != 3) return 1;
+    for (int j = 0; j < 3; ++j) b.q[j] = qubits[3 * i + j];
+    for (int j = 0; j < b.a; ++j) {
+      if (b.q[j] < 0 || b.q[j] >= n) return 1;
+      for (int t = 0; t < j; ++t)
+        if (b.q[t] == b.q[j]) return 1;
+    }
+    if (kinds && (kinds[i] < 0 || kinds[i] > 2 || (kinds[i] == KIND_VAR1 && b.a != 2))) return 1;
+    C.off[i + 1] = C.off[i] + (1 << (2 * b.a));
+  }
+  C.gsz = C.off[k];
+  return 0;
+}
+
 int check_structure(int n, int k, const int32_t *pairs, const int32_t *kinds = nullptr) {
   if (n < 2 || n > 30 || k < 1 || !pairs) return 1;
   for (int i = 0; i < k; ++i) {
     if (!valid_pair(n, pairs[2 * i], pairs[2 * i + 1])) return 1;
     if (kinds && (kinds[i] < 0 || kinds[i] > 2)) return 1;
   }
+  return 0;
+}
+
+// The controller, shared by the pair and block circuits: sweep(G, M, out, B, chi)
+// runs one sweep of one start, val(G) its validation cost; gsz = complex
+// entries of one start's gates.
+template <class SweepFn, class ValFn>
+int run_controller(long N, int gsz, int m_pool, int v, int s, const double *init_gates, const qfso_params *p,
+                   double *out_gates, qfso_result *out, int *winner, int n_threads, SweepFn sweep, ValFn val) {
+  struct St {
+    std::vector<cd> G;
+    int M, it, total, fails, restarts, term, conv_sweep;
+    bool has_prev, active;
+    double c_prev, c_train, c_val;
+    std::vector<double> B, chi;
+  };
+  std::vector<St> S(s);
+  for (int st = 0; st < s; ++st) {
+    S[st].G.resize((size_t)gsz);
+    for (int i = 0; i < gsz; ++i)
+      S[st].G[i] = cd(init_gates[2 * ((size_t)st * gsz + i)], init_gates[2 * ((size_t)st * gsz + i) + 1]);
+    S[st].M = p->m_init; S[st].it = 0; S[st].total = 0; S[st].fails = 0; S[st].restarts = 0;
+    S[st].term = -1; S[st].conv_sweep = -1; S[st].has_prev = false; S[st].active = true;
+    S[st].c_prev = 0; S[st].c_train = NAN; S[st].c_val = NAN;
+  }
+  const double otr = p->overtrain_ratio;
+#ifdef _OPENMP
+  if (n_threads > 0) omp_set_num_threads(n_threads);
+#endif
+  for (int t = 1;; ++t) {
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic, 1)
+#endif
+    for (int st = 0; st < s; ++st) {
+      St &A = S[st];
+      if (!A.active) continue;
+      SweepOut so;
+      sweep(A.G.data(), A.M, &so, A.B, A.chi);  // step 1
+      A.c_train = so.c_train;
+      A.c_val = v > 0 ? val(A.G.data()) : NAN;
+    }
+    bool any_conv = false;
+    for (int st = 0; st < s; ++st) {
+      St &A = S[st];
+      if (!A.active) continue;
+      A.it += 1; A.total += 1;
+      const double c = A.c_train;
+      const bool gen_check = v > 0 && std::isfinite(otr) && A.M < N;           // step 2
+      bool conv = false;                                                       // step 3
+      if (c <= p->dist_tol) {
+        if (!gen_check) conv = true;
+        else if (c < 1e-14) conv = A.c_val <= (1.0 + otr) * p->dist_tol;
+        else conv = A.c_val / c - 1.0 <= otr;
+      }
+      if (conv) {
+        A.term = 0; A.active = false; A.conv_sweep = t; any_conv = true;
+        continue;
+      }
+      if (gen_check && A.it >= p->min_iter && A.c_val / c - 1.0 > otr) {       // step 4
+        if (2 * A.M > m_pool && A.M < N) { A.term = 3; A.active = false; continue; }
+        A.M = (int)std::min<long>(2L * A.M, N);
+        A.it = 0; A.fails = 0; A.has_prev = false; A.restarts += 1;
+      } else if (p->plateau_window > 0) {                                      // step 5
+        if (A.has_prev)
+          A.fails = (std::fabs(A.c_prev) - std::fabs(c) > p->diff_tol_r * std::fabs(c)) ? 0 : A.fails + 1;
+        A.c_prev = c; A.has_prev = true;
+        if (A.it >= p->min_iter && A.fails >= p->plateau_window) { A.term = 1; A.active = false; continue; }
+      }
+      if (A.total >= p->max_iter) { A.term = 2; A.active = false; }            // step 6
+    }
+    bool any_active = false;
+    for (int st = 0; st < s; ++st) any_active |= S[st].active;
+    if (any_conv && p->stop_on_first) {
+      for (int st = 0; st < s; ++st)
+        if (S[st].active) { S[st].active = false; S[st].term = 4; }
+      any_active = false;
+    }
+    if (!any_active) break;
+  }
+  // winner (SURVEY.md §8(b)): lowest index among the earliest converged;
+  // else min c_train, ties to the lower index.
+  int win = -1, best_sweep = 1 << 30;
+  for (int st = 0; st < s; ++st)
+    if (S[st].term == 0 && S[st].conv_sweep < best_sweep) { best_sweep = S[st].conv_sweep; win = st; }
+  if (win < 0) {
+    double best = INFINITY;
+    for (int st = 0; st < s; ++st)
+      if (S[st].c_train < best) { best = S[st].c_train; win = st; }
+    if (win < 0) win = 0;
+  }
+  for (int st = 0; st < s; ++st) {
+    for (int i = 0; i < gsz; ++i) {
+      out_gates[2 * ((size_t)st * gsz + i)] = S[st].G[i].real();
+      out_gates[2 * ((size_t)st * gsz + i) + 1] = S[st].G[i].imag();
+    }
+    out[st].c_train = S[st].c_train; out[st].c_val = S[st].c_val;
+    out[st].sweeps = S[st].total; out[st].restarts = S[st].restarts;
+    out[st].final_m = S[st].M; out[st].term = S[st].term;
+  }
+  if (winner) *winner = win;
   return 0;
 }
 
@@ -517,98 +796,12 @@ int qfso_instantiate_kinds(int n, int k, const int32_t *pairs, const int32_t *ki
       !out || m_pool < 1 || m_pool > N || p->m_init < 1 || p->m_init > m_pool || v < 0 ||
       (v > 0 && (!xv || !yv)) || p->max_iter < 1)
     return 1;
-  struct St {
-    std::vector<cd> G;
-    int M, it, total, fails, restarts, term, conv_sweep;
-    bool has_prev, active;
-    double c_prev, c_train, c_val;
-    std::vector<double> B, chi;
-  };
-  std::vector<St> S(s);
-  for (int st = 0; st < s; ++st) {
-    S[st].G.resize((size_t)k * 16);
-    for (int i = 0; i < 16 * k; ++i)
-      S[st].G[i] = cd(init_gates[2 * ((size_t)st * k * 16 + i)], init_gates[2 * ((size_t)st * k * 16 + i) + 1]);
-    S[st].M = p->m_init; S[st].it = 0; S[st].total = 0; S[st].fails = 0; S[st].restarts = 0;
-    S[st].term = -1; S[st].conv_sweep = -1; S[st].has_prev = false; S[st].active = true;
-    S[st].c_prev = 0; S[st].c_train = NAN; S[st].c_val = NAN;
-  }
-  const double otr = p->overtrain_ratio;
-#ifdef _OPENMP
-  if (n_threads > 0) omp_set_num_threads(n_threads);
-#endif
-  for (int t = 1;; ++t) {
-#ifdef _OPENMP
-#pragma omp parallel for schedule(dynamic, 1)
-#endif
-    for (int st = 0; st < s; ++st) {
-      St &A = S[st];
-      if (!A.active) continue;
-      SweepOut so;
-      sweep_one(n, k, pairs, kinds, A.G.data(), A.M, x, y, p->beta, 1, &so, A.B, A.chi);  // step 1
-      A.c_train = so.c_train;
-      A.c_val = v > 0 ? validation_cost(n, k, pairs, A.G.data(), v, xv, yv) : NAN;
-    }
-    bool any_conv = false;
-    for (int st = 0; st < s; ++st) {
-      St &A = S[st];
-      if (!A.active) continue;
-      A.it += 1; A.total += 1;
-      const double c = A.c_train;
-      const bool gen_check = v > 0 && std::isfinite(otr) && A.M < N;           // step 2
-      bool conv = false;                                                       // step 3
-      if (c <= p->dist_tol) {
-        if (!gen_check) conv = true;
-        else if (c < 1e-14) conv = A.c_val <= (1.0 + otr) * p->dist_tol;
-        else conv = A.c_val / c - 1.0 <= otr;
-      }
-      if (conv) {
-        A.term = 0; A.active = false; A.conv_sweep = t; any_conv = true;
-        continue;
-      }
-      if (gen_check && A.it >= p->min_iter && A.c_val / c - 1.0 > otr) {       // step 4
-        if (2 * A.M > m_pool && A.M < N) { A.term = 3; A.active = false; continue; }
-        A.M = (int)std::min<long>(2L * A.M, N);
-        A.it = 0; A.fails = 0; A.has_prev = false; A.restarts += 1;
-      } else if (p->plateau_window > 0) {                                      // step 5
-        if (A.has_prev)
-          A.fails = (std::fabs(A.c_prev) - std::fabs(c) > p->diff_tol_r * std::fabs(c)) ? 0 : A.fails + 1;
-        A.c_prev = c; A.has_prev = true;
-        if (A.it >= p->min_iter && A.fails >= p->plateau_window) { A.term = 1; A.active = false; continue; }
-      }
-      if (A.total >= p->max_iter) { A.term = 2; A.active = false; }            // step 6
-    }
-    bool any_active = false;
-    for (int st = 0; st < s; ++st) any_active |= S[st].active;
-    if (any_conv && p->stop_on_first) {
-      for (int st = 0; st < s; ++st)
-        if (S[st].active) { S[st].active = false; S[st].term = 4; }
-      any_active = false;
-    }
-    if (!any_active) break;
-  }
-  // winner (SURVEY.md §8(b)): lowest index among the earliest converged;
-  // else min c_train, ties to the lower index.
-  int win = -1, best_sweep = 1 << 30;
-  for (int st = 0; st < s; ++st)
-    if (S[st].term == 0 && S[st].conv_sweep < best_sweep) { best_sweep = S[st].conv_sweep; win = st; }
-  if (win < 0) {
-    double best = INFINITY;
-    for (int st = 0; st < s; ++st)
-      if (S[st].c_train < best) { best = S[st].c_train; win = st; }
-    if (win < 0) win = 0;
-  }
-  for (int st = 0; st < s; ++st) {
-    for (int i = 0; i < 16 * k; ++i) {
-      out_gates[2 * ((size_t)st * k * 16 + i)] = S[st].G[i].real();
-      out_gates[2 * ((size_t)st * k * 16 + i) + 1] = S[st].G[i].imag();
-    }
-    out[st].c_train = S[st].c_train; out[st].c_val = S[st].c_val;
-    out[st].sweeps = S[st].total; out[st].restarts = S[st].restarts;
-    out[st].final_m = S[st].M; out[st].term = S[st].term;
-  }
-  if (winner) *winner = win;
-  return 0;
+  return run_controller(
+      N, 16 * k, m_pool, v, s, init_gates, p, out_gates, out, winner, n_threads,
+      [&](cd *G, int M, SweepOut *so, std::vector<double> &B, std::vector<double> &chi) {
+        sweep_one(n, k, pairs, kinds, G, M, x, y, p->beta, 1, so, B, chi);
+      },
+      [&](const cd *G) { return validation_cost(n, k, pairs, G, v, xv, yv); });
 }
 
 int qfso_bench_sweeps(int n, int k, const int32_t *pairs, int s, const double *init_gates, int m,
@@ -620,6 +813,104 @@ int qfso_bench_sweeps(int n, int k, const int32_t *pairs, int s, const double *i
   auto t1 = std::chrono::steady_clock::now();
   if (sec) *sec = std::chrono::duration<double>(t1 - t0).count();
   return rc;
+}
+
+// ---------------------------------------------------------------- blocks --
+int qfso_apply_block(int n, int arity, const int32_t *q, const double *g, int dagger, int m, double *psi) {
+  const int32_t ar[1] = {arity};
+  BlockCircuit C;
+  if (!q || !g || !psi || m < 0 || make_blocks(n, 1, q, ar, nullptr, C)) return 1;
+  const int d = 1 << arity;
+  cd G[64], Gd[64];
+  for (int i = 0; i < d * d; ++i) G[i] = cd(g[2 * i], g[2 * i + 1]);
+  if (dagger) { adjoint_d(d, G, Gd); apply_block(n, C.b[0], Gd, m, psi); }
+  else apply_block(n, C.b[0], G, m, psi);
+  return 0;
+}
+
+int qfso_environment_block(int n, int arity, const int32_t *q, int m, const double *phi,
+                           const double *chi, double *env) {
+  const int32_t ar[1] = {arity};
+  BlockCircuit C;
+  if (!q || !phi || !chi || !env || m < 0 || make_blocks(n, 1, q, ar, nullptr, C)) return 1;
+  const int d = 1 << arity;
+  cld E[64];
+  for (int i = 0; i < d * d; ++i) E[i] = 0;
+  environment_block(n, C.b[0], 0, m, 1, phi, chi, E);
+  for (int i = 0; i < d * d; ++i) { env[2 * i] = (double)E[i].real(); env[2 * i + 1] = (double)E[i].imag(); }
+  return 0;
+}
+
+int qfso_polar_update_block(int d, const double *env, const double *g_old, double beta, double *g_new,
+                            double *sigma_sum) {
+  if ((d != 4 && d != 8) || !env || !g_old || !g_new) return 1;
+  cd E[64], Go[64], Gn[64];
+  for (int i = 0; i < d * d; ++i) { E[i] = cd(env[2 * i], env[2 * i + 1]); Go[i] = cd(g_old[2 * i], g_old[2 * i + 1]); }
+  gate_update_block(KIND_VAR2, d, E, Go, beta, Gn, sigma_sum);
+  for (int i = 0; i < d * d; ++i) { g_new[2 * i] = Gn[i].real(); g_new[2 * i + 1] = Gn[i].imag(); }
+  return 0;
+}
+
+int qfso_trace_sweeps_blocks(int n, int k, const int32_t *qubits, const int32_t *arity, const int32_t *kinds,
+                             int s, const double *init_gates, int m, const double *x, const double *y,
+                             double beta, int n_sweeps, double *env_trace, double *gate_trace,
+                             double *cost_trace, double *sigma_trace, int n_threads) {
+  BlockCircuit C;
+  if (make_blocks(n, k, qubits, arity, kinds, C) || s < 1 || m < 1 || m > (1 << n) || !init_gates || !x ||
+      !y || n_sweeps < 0)
+    return 1;
+  const size_t gsz = (size_t)C.gsz;
+#ifdef _OPENMP
+  if (n_threads > 0) omp_set_num_threads(n_threads);
+#pragma omp parallel for schedule(dynamic, 1)
+#endif
+  for (int st = 0; st < s; ++st) {
+    std::vector<cd> G(gsz);
+    for (size_t i = 0; i < gsz; ++i)
+      G[i] = cd(init_gates[2 * ((size_t)st * gsz + i)], init_gates[2 * ((size_t)st * gsz + i) + 1]);
+    std::vector<double> B, chi;
+    SweepOut so;
+    for (int t = 0; t < n_sweeps; ++t) {
+      sweep_blocks(C, G.data(), m, x, y, beta, &so, B, chi);
+      if (env_trace)  // [t][gate-major: gate i at s * off_i, then start, then d_i^2 entries]
+        for (int i = 0; i < k; ++i) {
+          const int dd = C.off[i + 1] - C.off[i];
+          for (int q = 0; q < dd; ++q) {
+            size_t o = ((size_t)t * s * gsz + (size_t)s * C.off[i] + (size_t)st * dd + q) * 2;
+            env_trace[o] = so.env[C.off[i] + q].real();
+            env_trace[o + 1] = so.env[C.off[i] + q].imag();
+          }
+        }
+      if (gate_trace)
+        for (size_t i = 0; i < gsz; ++i) {
+          size_t o = (((size_t)t * s + st) * gsz + i) * 2;
+          gate_trace[o] = G[i].real();
+          gate_trace[o + 1] = G[i].imag();
+        }
+      if (cost_trace) cost_trace[(size_t)t * s + st] = so.c_train;
+      if (sigma_trace)
+        for (int i = 0; i < k; ++i) sigma_trace[((size_t)t * k + i) * s + st] = so.sig[i];
+    }
+  }
+  return 0;
+}
+
+int qfso_instantiate_blocks(int n, int k, const int32_t *qubits, const int32_t *arity, const int32_t *kinds,
+                            int m_pool, const double *x, const double *y, int v, const double *xv,
+                            const double *yv, int s, const double *init_gates, const qfso_params *p,
+                            double *out_gates, qfso_result *out, int *winner, int n_threads) {
+  const long N = 1L << n;
+  BlockCircuit C;
+  if (make_blocks(n, k, qubits, arity, kinds, C) || s < 1 || !p || !init_gates || !x || !y || !out_gates ||
+      !out || m_pool < 1 || m_pool > N || p->m_init < 1 || p->m_init > m_pool || v < 0 ||
+      (v > 0 && (!xv || !yv)) || p->max_iter < 1)
+    return 1;
+  return run_controller(
+      N, C.gsz, m_pool, v, s, init_gates, p, out_gates, out, winner, n_threads,
+      [&](cd *G, int M, SweepOut *so, std::vector<double> &B, std::vector<double> &chi) {
+        sweep_blocks(C, G, M, x, y, p->beta, so, B, chi);
+      },
+      [&](const cd *G) { return validation_cost_blocks(C, G, v, xv, yv); });
 }
 
 }  // extern "C"

@@ -93,6 +93,28 @@ int qfso_instantiate_kinds(int n, int k, const int32_t *pairs, const int32_t *ki
                            const double *yv, int s, const double *init_gates, const qfso_params *p,
                            double *out_gates, qfso_result *out, int *winner, int n_threads);
 
+/* Multi-qubit blocks ("possibly multi-qubit"
+ * gates).  Gate k has arity a_k in {2, 3} on qubits[3k .. 3k+a_k-1] (as given;
+ * local index l = sum_j b(q_j) 2^j), a d_k x d_k matrix G[l_out][l_in],
+ * d_k = 2^a_k.  Gates are PACKED: gate k of start s at complex offset
+ * s * G + off_k, off_k = sum_{j<k} d_j^2, G = off_K.  kinds as above (2 only
+ * for arity 2; NULL = all variable).  env_trace per sweep t is gate-major:
+ * gate i of start s at t * S * G + S * off_i + s * d_i^2. */
+int qfso_apply_block(int n, int arity, const int32_t *q, const double *g, int dagger, int m, double *psi);
+int qfso_environment_block(int n, int arity, const int32_t *q, int m, const double *phi,
+                           const double *chi, double *env);
+/* d in {4, 8}: g_new = Y X^dag from SVD((1-beta) E + beta g_old^dag), *sigma_sum = sum sigma */
+int qfso_polar_update_block(int d, const double *env, const double *g_old, double beta, double *g_new,
+                            double *sigma_sum);
+int qfso_trace_sweeps_blocks(int n, int k, const int32_t *qubits, const int32_t *arity, const int32_t *kinds,
+                             int s, const double *init_gates, int m, const double *x, const double *y,
+                             double beta, int n_sweeps, double *env_trace, double *gate_trace,
+                             double *cost_trace, double *sigma_trace, int n_threads);
+int qfso_instantiate_blocks(int n, int k, const int32_t *qubits, const int32_t *arity, const int32_t *kinds,
+                            int m_pool, const double *x, const double *y, int v, const double *xv,
+                            const double *yv, int s, const double *init_gates, const qfso_params *p,
+                            double *out_gates, qfso_result *out, int *winner, int n_threads);
+
 /* Sweep-throughput timing: n_sweeps sweeps at fixed M; *sec = wall seconds. */
 int qfso_bench_sweeps(int n, int k, const int32_t *pairs, int s, const double *init_gates, int m,
                       const double *x, const double *y, int n_sweeps, int n_threads,

@@ -310,3 +310,100 @@ def u3_cnot_problem(n: int, layers: int, s: int, m_pool: int, v: int, init: str 
             else:
                 gates[st, j] = _embed1(haar_unitary(rng, 2))
     return pairs, kinds, target, x, y, xv, yv, gates
+
+
+# ------------------------------------------------------- multi-qubit blocks --
+# Circuits of 2- and 3-qubit blocks ("possibly
+# multi-qubit" gates).  Gate k acts on qubits[k][:arity[k]] (local index
+# l = sum_j b(q_j) 2^j, first listed qubit least significant) with a d x d
+# matrix, d = 2^arity; a circuit's gates are stored PACKED: gate k at complex
+# offset off_k = sum_{j<k} d_j^2 (the layout of qfs_create_blocks and the
+# oracle's *_blocks functions).  Layout helpers and the harness simulator only.
+
+def gate_offsets(arity) -> np.ndarray:
+    d2 = [1 << (2 * int(a)) for a in np.asarray(arity).reshape(-1)]
+    return np.concatenate([[0], np.cumsum(d2)]).astype(np.int64)
+
+
+def pack_gates(mats) -> np.ndarray:
+    return np.concatenate([np.asarray(g, dtype=np.complex128).reshape(-1) for g in mats])
+
+
+def unpack_gates(vec, arity) -> list:
+    off = gate_offsets(arity)
+    out = []
+    for k, a in enumerate(np.asarray(arity).reshape(-1)):
+        d = 1 << int(a)
+        out.append(np.asarray(vec[off[k]:off[k + 1]]).reshape(d, d))
+    return out
+
+
+def apply_blocks_tensor(n: int, qubits, arity, packed, states: np.ndarray) -> np.ndarray:
+    """Harness simulator for block circuits (tensordot, like apply_circuit_tensor):
+    a gate on (q_0, .., q_{a-1}) with l = sum_j b(q_j) 2^j is the tensor
+    G[o_{a-1}, .., o_0, i_{a-1}, .., i_0]."""
+    m = states.shape[0]
+    psi = np.asarray(states, dtype=np.complex128).reshape((m,) + (2,) * n)
+    for q, a, g in zip(np.asarray(qubits).reshape(-1, 3), np.asarray(arity).reshape(-1),
+                       unpack_gates(packed, arity)):
+        a = int(a)
+        axes = [1 + (n - 1 - int(q[j])) for j in range(a)][::-1]  # tensor order: q_{a-1} .. q_0
+        ga = g.reshape((2,) * (2 * a))
+        res = np.tensordot(psi, ga, axes=(axes, list(range(a, 2 * a))))
+        psi = np.moveaxis(res, list(range(-a, 0)), axes)
+    return np.ascontiguousarray(psi.reshape(m, 1 << n))
+
+
+def block_structure(n: int, k: int, seed: int = 0):
+    """Synthetic mixed circuit: every third slot a two-qubit block on an
+    adjacent pair, the others three-qubit blocks on (q, q+1, q+2) sliding by
+    two, each block's qubit list in a seeded order.  Returns (qubits [k][3]
+    int32, arity [k] int32)."""
+    if n < 3:
+        raise ValueError("three-qubit blocks need n >= 3")
+    rng = rng_for(seed, 4, 0)
+    qubits = np.zeros((k, 3), np.int32)
+    arity = np.zeros(k, np.int32)
+    for j in range(k):
+        if j % 3 == 2:
+            q = (j * 3 + 1) % (n - 1)
+            qs = [q, q + 1]
+        else:
+            q = (2 * j) % (n - 2)
+            qs = [q, q + 1, q + 2]
+        qs = list(rng.permutation(qs))
+        arity[j] = len(qs)
+        qubits[j, :len(qs)] = qs
+    return qubits, arity
+
+
+def warm_gate_d(rng: np.random.Generator, target: np.ndarray, eps: float) -> np.ndarray:
+    """exp(i*eps*H) @ target (any d) with H = (A + A^dag)/2 scaled to spectral norm 1."""
+    d = target.shape[0]
+    a = _complex_gaussian(rng, (d, d))
+    h = 0.5 * (a + a.conj().T)
+    w, v = np.linalg.eigh(h)
+    w = w / np.max(np.abs(w))
+    return (v * np.exp(1j * eps * w)[None, :]) @ v.conj().T @ target
+
+
+def block_problem(n: int, k: int, s: int, m_pool: int, v: int = 16, init: str = "W", eps: float = 0.3,
+                  seed: int = 21):
+    """Solvable block-circuit instance: target = seeded Haar blocks on
+    block_structure(n, k); W initial gates = exp(i eps H) target per block, R =
+    Haar.  Returns (qubits, arity, target packed [G], x, y, xv, yv, init [s][G])."""
+    qubits, arity = block_structure(n, k, seed)
+    target = pack_gates([haar_unitary(rng_for(seed, 0, j), 1 << int(a)) for j, a in enumerate(arity)])
+    x = haar_states(rng_for(seed, 1, 0), n, m_pool)
+    y = apply_blocks_tensor(n, qubits, arity, target, x)
+    xv = haar_states(rng_for(seed, 2, 0), n, v) if v else np.zeros((0, 1 << n), np.complex128)
+    yv = apply_blocks_tensor(n, qubits, arity, target, xv) if v else xv.copy()
+    tg = unpack_gates(target, arity)
+    gates = []
+    for st in range(s):
+        rng = rng_for(seed, 3, st)
+        if init == "W":
+            gates.append(pack_gates([warm_gate_d(rng, t, eps) for t in tg]))
+        else:
+            gates.append(pack_gates([haar_unitary(rng, t.shape[0]) for t in tg]))
+    return qubits, arity, target, x, y, xv, yv, np.stack(gates)
