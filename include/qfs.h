@@ -78,6 +78,27 @@ typedef struct {
  * device: CUDA ordinal.  Structure only; no target. */
 qfs_status qfs_create(int n, int k, const int32_t *pairs, int device, qfs_ctx **out);
 
+/* Create a context for an n-qubit circuit of k multi-qubit blocks (SURVEY.md
+ * §8(f) NEXT-3; "possibly multi-qubit" unitary gates).
+ * qubits: host int32 [k][3]; block i acts on qubits[3i .. 3i+arity[i]-1] (distinct,
+ * < n; entry 3i+2 ignored for arity 2), local index l = sum_j b(q_j) 2^j.
+ * arity: host int32 [k], each 2 or 3.  Gate i is a d x d matrix G[l_out][l_in],
+ * d = 2^arity[i].  GATE LAYOUT of every call of this context (init_gates,
+ * out_gates, gate_trace): PACKED per start — gate i at complex offset
+ * off_i = sum_{j<i} d_j^2 of the start's block of G = off_k entries
+ * (all-two-qubit circuits: G = 16 k, the same layout as qfs_create, and the
+ * context IS a pair context).  env_trace per sweep: gate-major, gate i of start
+ * s at s_total * off_i + s * d_i^2.  Circuits with a 3-qubit block run the
+ * streamed sweep (B cache in HBM) with one launch per step, single GPU
+ * (qfs_create_dist / sample sharding are not available for them); the 8x8
+ * update is the Newton-Schulz polar factor (singular 8x8 environments are
+ * reported as QFS_ERR_NUMERIC by the next call that validates gates).  Gate
+ * kinds (qfs_set_gate_kinds) apply per block: VAR2 = variable (any arity),
+ * FIXED, VAR1 only on two-qubit blocks.  Errors: QFS_ERR_ARG for a bad
+ * structure (n < 3, arity not 2/3, repeated or out-of-range qubits). */
+qfs_status qfs_create_blocks(int n, int k, const int32_t *qubits, const int32_t *arity, int device,
+                             qfs_ctx **out);
+
 /* Distributed context.  nccl_comm: an ncclComm_t whose rank
  * and size equal (rank, world) (e.g. ProcessGroupNCCL._comm_ptr()), or NULL
  * when world == 1.  shard_mode 0 = multistart (each rank runs its own starts,

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libqfs.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("qfs_kernels.cu", "qfs_resident.cu", "qfs_runtime.cu")]
+SOURCES = [os.path.join(CSRC, f) for f in ("qfs_kernels.cu", "qfs_resident.cu", "qfs_blocks.cu", "qfs_runtime.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, "qfs_internal.h"), os.path.join(CSRC, "qfs_device.cuh"), os.path.join(ROOT, "include", "qfs.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -1,0 +1,416 @@
+// qfs_blocks.cu — sm_100a kernels for circuits of multi-qubit blocks
+// (qfs_create_blocks; "possibly
+// multi-qubit" unitary gates, updated without parameterisation).
+//
+// A block of arity A in {2, 3} acts on qubits q_0..q_{A-1} (as given; local
+// index l = sum_j b(q_j) 2^j) with a d x d matrix, d = 2^A.  The sweep is the
+// streamed algorithm of qfs_kernels.cu in its
+// plain form — one launch per step, no fusion:
+//   forward   B_{k+1} = G_k B_k                         (blk_apply_kernel)
+//   backward  chi <- G_{i+1}^dag chi                    (blk_apply_kernel, dagger)
+//             E_i = sum phi (x) conj(chi), ordered reduction, last CTA runs the
+//             gate update (d = 4: the half-warp polar of qfs_device.cuh;
+//             d = 8: warp Newton-Schulz polar below)   (blk_env_kernel)
+//   cost      sum ||a - b||^2, ordered reduction         (blk_dist_kernel)
+// States use the Views of qfs_internal.h (sample-minor work buffers).  No
+// code here is shared with the CPU oracle.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "qfs_device.cuh"
+#include "qfs_internal.h"
+
+namespace qfs {
+namespace {
+
+constexpr int BLK_THREADS = 128;
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+// first amplitude of block-group r: zeros inserted at the sorted qubit positions
+template <int A>
+__device__ __forceinline__ unsigned blk_base(unsigned r, const int (&srt)[3]) {
+#pragma unroll
+  for (int j = 0; j < A; ++j) r = insert_zero32(r, srt[j]);
+  return r;
+}
+
+struct BlkLocal {
+  int q[3], srt[3];
+  unsigned off[8];  // amplitude offset of local index l (sum_j b_j 2^{q_j})
+};
+template <int A>
+__device__ __forceinline__ BlkLocal blk_local(const BlkGate &g) {
+  BlkLocal b;
+#pragma unroll
+  for (int j = 0; j < 3; ++j) b.q[j] = b.srt[j] = g.q[j];
+#pragma unroll
+  for (int i = 0; i < A; ++i)
+#pragma unroll
+    for (int j = i + 1; j < A; ++j)
+      if (b.srt[j] < b.srt[i]) { int t = b.srt[i]; b.srt[i] = b.srt[j]; b.srt[j] = t; }
+#pragma unroll
+  for (int l = 0; l < (1 << A); ++l) {
+    unsigned o = 0;
+#pragma unroll
+    for (int j = 0; j < A; ++j) o |= (unsigned)((l >> j) & 1) << b.q[j];
+    b.off[l] = o;
+  }
+  return b;
+}
+
+// --------------------------------------------------------------- apply --
+// dst = G_k src (dagger: G_k^dag) for every (group, row) of every slot.
+template <int A>
+__global__ void __launch_bounds__(BLK_THREADS) blk_apply_kernel(const BlkApplyParams P) {
+  constexpr int D = 1 << A;
+  __shared__ double2 sG[D * D];
+  const int j = blockIdx.y;
+  const Slot sl = P.slots[j];
+  const int s = sl.s;
+  const unsigned rows = P.rows_fixed > 0 ? (unsigned)P.rows_fixed : (unsigned)sl.m;
+  const BlkGate bg = P.bg[P.k];
+  const double2 *gk = P.gates + (long long)s * P.gsz + bg.off;
+  for (int e = threadIdx.x; e < D * D; e += blockDim.x) {
+    const int a = e / D, b = e % D;
+    sG[e] = P.dagger ? cconj(gk[D * b + a]) : gk[e];  // (G^dag)[a][b] = conj(G[b][a])
+  }
+  __syncthreads();
+  const BlkLocal L = blk_local<A>(bg);
+  const unsigned items = (1u << (P.n - A)) * rows;
+  const unsigned chunk = (items + gridDim.x - 1) / gridDim.x;
+  const unsigned beg = blockIdx.x * chunk, end = min(items, beg + chunk);
+  const FastDiv fd(rows);
+  const double2 *src = P.src.base + (long long)s * P.src.ss;
+  double2 *dst = P.dst.base + (long long)s * P.dst.ss;
+  for (unsigned w = beg + threadIdx.x; w < end; w += blockDim.x) {
+    const unsigned r = fd.div(w), m = w - r * rows;  // row fastest: coalesced sample-minor access
+    const unsigned base = blk_base<A>(r, L.srt);
+    double2 v[D];
+#pragma unroll
+    for (int l = 0; l < D; ++l) v[l] = src[(long long)(base | L.off[l]) * P.src.sa + (long long)m * P.src.sm];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      double2 o = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int b = 0; b < D; ++b) cfma(o, sG[D * a + b], v[b]);
+      dst[(long long)(base | L.off[a]) * P.dst.sa + (long long)m * P.dst.sm] = o;
+    }
+  }
+}
+
+// ------------------------------------------------------------ 8x8 polar --
+// Unitary polar factor W of the 8x8 complex E' on one warp (lane holds
+// entries lane and lane + 32, row-major), Newton-Schulz X <- X (3I - X^dag X)/2
+// from X_0 = E' sqrt(2.9 / ||E'^dag E'||_F): every singular value of X_0 is
+// then below sqrt(2.9) < sqrt(3), where the iteration converges (to W for a
+// nonsingular E').  Stops when ||X^dag X - I||_F <= 1e-14; returns false if it
+// does not within 100 iterations (singular E').  G = W^dag = Y X^dag (eq:opt_u,
+// P:59-62, with E' = X D Y^dag), sum sigma = Re Tr(W^dag E').
+__device__ bool polar8(const double2 (&e)[2], double2 (&g)[2], double &ss, double2 *sm /*[2][64]*/) {
+  const int lane = threadIdx.x & 31;
+  double2 *sX = sm, *sT = sm + 64;
+  auto xhx = [&](const double2 (&X)[2], double2 (&Y)[2]) {  // Y = X^dag X, X left in sX
+    __syncwarp();
+    sX[lane] = X[0];
+    sX[lane + 32] = X[1];
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = (lane >> 3) + 4 * h, c = lane & 7;
+      double2 y = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) cfma(y, cconj(sX[8 * q + r]), sX[8 * q + c]);
+      Y[h] = y;
+    }
+  };
+  double2 x[2] = {e[0], e[1]}, y[2];
+  xhx(x, y);
+  const double fy = sqrt(warp_sum_d(y[0].x * y[0].x + y[0].y * y[0].y + y[1].x * y[1].x + y[1].y * y[1].y));
+  if (!(fy > 0.0)) return false;
+  const double sc = sqrt(2.9 / fy);
+  x[0].x *= sc; x[0].y *= sc; x[1].x *= sc; x[1].y *= sc;
+  bool ok = false;
+  for (int it = 0; it < 100; ++it) {
+    xhx(x, y);
+    double err = 0.0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = (lane >> 3) + 4 * h, c = lane & 7;
+      const double dr = y[h].x - (r == c ? 1.0 : 0.0);
+      err += dr * dr + y[h].y * y[h].y;
+    }
+    err = warp_sum_d(err);
+    if (err <= 1e-28) { ok = true; break; }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = (lane >> 3) + 4 * h, c = lane & 7;
+      sT[lane + 32 * h] = make_double2(0.5 * ((r == c ? 3.0 : 0.0) - y[h].x), -0.5 * y[h].y);
+    }
+    __syncwarp();
+    double2 z[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = (lane >> 3) + 4 * h, c = lane & 7;
+      z[h] = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) cfma(z[h], sX[8 * r + q], sT[8 * q + c]);
+    }
+    x[0] = z[0];
+    x[1] = z[1];
+  }
+  // G[r][c] = conj(W[c][r]);  sum sigma = Re sum conj(W) o E'
+  __syncwarp();
+  sX[lane] = x[0];
+  sX[lane + 32] = x[1];
+  __syncwarp();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int r = (lane >> 3) + 4 * h, c = lane & 7;
+    g[h] = cconj(sX[8 * c + r]);
+  }
+  ss = warp_sum_d(x[0].x * e[0].x + x[0].y * e[0].y + x[1].x * e[1].x + x[1].y * e[1].y);
+  return ok;
+}
+
+// ---------------------------------------------------------- environment --
+// E_i[l_in][l_out] = sum_m sum_r phi_m[idx_r(l_in)] conj(chi_m[idx_r(l_out)])
+// (R4): per-thread accumulators, warp butterflies, warps in order,
+// CTA partials summed in CTA order by the last CTA (ticket), which then runs
+// the gate update of gate i and writes G_i, sum sigma and the environment trace.
+template <int A>
+__global__ void __launch_bounds__(BLK_THREADS) blk_env_kernel(const BlkEnvParams P) {
+  constexpr int D = 1 << A, DD = D * D, NW = BLK_THREADS / 32;
+  __shared__ double2 red[NW][DD];
+  __shared__ double2 sE[DD];
+  __shared__ double2 scratch[128];
+  __shared__ unsigned last_cta;
+  const int j = blockIdx.y;
+  const Slot sl = P.slots[j];
+  const int s = sl.s;
+  const unsigned rows = (unsigned)sl.m;
+  const BlkGate bg = P.bg[P.i];
+  const BlkLocal L = blk_local<A>(bg);
+  double2 acc[DD];
+#pragma unroll
+  for (int e = 0; e < DD; ++e) acc[e] = make_double2(0.0, 0.0);
+  const unsigned items = (1u << (P.n - A)) * rows;
+  const unsigned chunk = (items + gridDim.x - 1) / gridDim.x;
+  const unsigned beg = blockIdx.x * chunk, end = min(items, beg + chunk);
+  const FastDiv fd(rows);
+  const double2 *ph = P.phi.base + (long long)s * P.phi.ss;
+  const double2 *ch = P.chi.base + (long long)s * P.chi.ss;
+  for (unsigned w = beg + threadIdx.x; w < end; w += blockDim.x) {
+    const unsigned r = fd.div(w), m = w - r * rows;
+    const unsigned base = blk_base<A>(r, L.srt);
+    double2 f[D], c[D];
+#pragma unroll
+    for (int l = 0; l < D; ++l) {
+      f[l] = ph[(long long)(base | L.off[l]) * P.phi.sa + (long long)m * P.phi.sm];
+      c[l] = ch[(long long)(base | L.off[l]) * P.chi.sa + (long long)m * P.chi.sm];
+    }
+#pragma unroll
+    for (int x = 0; x < D; ++x)
+#pragma unroll
+      for (int y = 0; y < D; ++y) {
+        double2 &e = acc[D * x + y];  // f[x] conj(c[y])
+        e.x = fma(f[x].x, c[y].x, e.x);
+        e.x = fma(f[x].y, c[y].y, e.x);
+        e.y = fma(f[x].y, c[y].x, e.y);
+        e.y = fma(-f[x].x, c[y].y, e.y);
+      }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int e = 0; e < DD; ++e) {
+    const double re = warp_sum_d(acc[e].x), im = warp_sum_d(acc[e].y);
+    if (lane == 0) red[warp][e] = make_double2(re, im);
+  }
+  __syncthreads();
+  double2 *part = reinterpret_cast<double2 *>(P.partials) + ((long long)j * gridDim.x + blockIdx.x) * DD;
+  for (int e = threadIdx.x; e < DD; e += blockDim.x) {
+    double2 t = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int w = 0; w < NW; ++w) { t.x += red[w][e].x; t.y += red[w][e].y; }
+    part[e] = t;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(P.counters + j, 1u);
+    last_cta = t == gridDim.x - 1 ? 1u : 0u;
+    if (last_cta) P.counters[j] = 0u;
+  }
+  __syncthreads();
+  if (!last_cta) return;
+  __threadfence();
+  const double2 *pp = reinterpret_cast<const double2 *>(P.partials) + (long long)j * gridDim.x * DD;
+  for (int e = threadIdx.x; e < DD; e += blockDim.x) {
+    double2 t = make_double2(0.0, 0.0);
+    for (unsigned b = 0; b < gridDim.x; ++b) {
+      const double2 v = __ldcg(pp + (long long)b * DD + e);
+      t.x += v.x;
+      t.y += v.y;
+    }
+    sE[e] = t;
+  }
+  __syncthreads();
+  if (warp != 0) return;
+  const long long gi = (long long)s * P.gsz + bg.off;
+  double2 *gw = P.gates + gi;
+  if (P.env_trace)  // gate-major trace: gate i of start s at S * off_i + s * d^2
+    for (int e = lane; e < DD; e += 32) P.env_trace[(long long)P.S * bg.off + (long long)s * DD + e] = sE[e];
+  double ss = 0.0;
+  if constexpr (D == 4) {
+    const int l = lane & 15;
+    double2 g, v;
+    gate_update(bg.kind, sE[l], gw, P.beta, nullptr, g, v, ss, scratch + 2 * (lane & 16));
+    __syncwarp();
+    if (lane < 16 && bg.kind != 1) gw[l] = g;
+  } else {
+    if (bg.kind == 1) {  // fixed: sum sigma slot = Re Tr(E G)
+      double t = 0.0;
+      for (int e = lane; e < DD; e += 32) {
+        const int a = e / D, b = e % D;
+        const double2 gg = gw[D * b + a];
+        t += sE[e].x * gg.x - sE[e].y * gg.y;
+      }
+      ss = warp_sum_d(t);
+    } else {
+      double2 e2[2], g2[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int e = lane + 32 * h, a = e / D, b = e % D;
+        e2[h] = sE[e];
+        if (P.beta != 0.0) {  // E' = (1 - beta) E + beta G_old^dag
+          const double2 go = gw[D * b + a];
+          e2[h] = make_double2((1.0 - P.beta) * e2[h].x + P.beta * go.x, (1.0 - P.beta) * e2[h].y - P.beta * go.y);
+        }
+      }
+      const bool ok = polar8(e2, g2, ss, scratch);
+      __syncwarp();
+      gw[lane] = g2[0];
+      gw[lane + 32] = g2[1];
+      if (!ok && lane == 0 && P.err) atomicOr(P.err, 8u);
+    }
+  }
+  if (lane == 0 && P.sig) P.sig[(long long)s * P.K + P.i] = ss;
+}
+
+// ---------------------------------------------------------------- cost --
+// out[j] = sum over rows and amplitudes of ||a - b||^2 (P:116-120 direct form;
+// P:184 validation), ordered: lanes, warps, CTAs.
+__global__ void __launch_bounds__(BLK_THREADS) blk_dist_kernel(const BlkDistParams P) {
+  constexpr int NW = BLK_THREADS / 32;
+  __shared__ double red[NW];
+  __shared__ unsigned last_cta;
+  const int j = blockIdx.y;
+  const Slot sl = P.slots[j];
+  const int s = sl.s;
+  const unsigned rows = P.rows_fixed > 0 ? (unsigned)P.rows_fixed : (unsigned)sl.m;
+  const unsigned items = (1u << P.n) * rows;
+  const unsigned chunk = (items + gridDim.x - 1) / gridDim.x;
+  const unsigned beg = blockIdx.x * chunk, end = min(items, beg + chunk);
+  const FastDiv fd(rows);
+  const double2 *a = P.a.base + (long long)s * P.a.ss, *b = P.b.base + (long long)s * P.b.ss;
+  double acc = 0.0;
+  for (unsigned w = beg + threadIdx.x; w < end; w += blockDim.x) {
+    const unsigned amp = fd.div(w), m = w - amp * rows;
+    const double2 u = a[(long long)amp * P.a.sa + (long long)m * P.a.sm];
+    const double2 v = b[(long long)amp * P.b.sa + (long long)m * P.b.sm];
+    const double dr = u.x - v.x, di = u.y - v.y;
+    acc = fma(dr, dr, acc);
+    acc = fma(di, di, acc);
+  }
+  acc = warp_sum_d(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) t += red[w];
+    P.partials[(long long)j * gridDim.x + blockIdx.x] = t;
+    __threadfence();
+    const unsigned tk = atomicAdd(P.counters + j, 1u);
+    last_cta = tk == gridDim.x - 1 ? 1u : 0u;
+    if (last_cta) {
+      P.counters[j] = 0u;
+      __threadfence();
+      double tot = 0.0;
+      for (unsigned c = 0; c < gridDim.x; ++c) tot += __ldcg(P.partials + (long long)j * gridDim.x + c);
+      P.out[j] = tot;
+    }
+  }
+}
+
+// ---------------------------------------------------------- gate check --
+// finite (bit 1) and unitary to 1e-10 (bit 2) for every block of every start
+__global__ void blk_gate_check_kernel(const double2 *g, const BlkGate *bg, int K, long long gsz, int s,
+                                      unsigned *flag) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)s * K;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(t % K);
+    const long long st = t / K;
+    const int D = 1 << bg[k].a;
+    const double2 *G = g + st * gsz + bg[k].off;
+    unsigned bad = 0;
+    for (int e = 0; e < D * D; ++e)
+      if (!isfinite(G[e].x) || !isfinite(G[e].y)) bad |= 1u;
+    for (int a = 0; a < D && !bad; ++a)
+      for (int b = 0; b < D; ++b) {
+        double re = 0.0, im = 0.0;
+        for (int r = 0; r < D; ++r) {  // conj(G[r][a]) G[r][b]
+          re += G[D * r + a].x * G[D * r + b].x + G[D * r + a].y * G[D * r + b].y;
+          im += G[D * r + a].x * G[D * r + b].y - G[D * r + a].y * G[D * r + b].x;
+        }
+        if (fabs(re - (a == b ? 1.0 : 0.0)) > 1e-10 || fabs(im) > 1e-10) bad |= 2u;
+      }
+    if (bad) atomicOr(flag, bad);
+  }
+}
+
+int blk_grid(long long items, int n_slots) {
+  long long nb = std::max(1, 148 * 4 / std::max(1, n_slots));
+  nb = std::min(nb, (items + BLK_THREADS - 1) / BLK_THREADS);
+  return (int)std::max(1LL, std::min<long long>(nb, kBlkMaxCtas));
+}
+
+}  // namespace
+
+int blk_ctas(long long items, int n_slots) { return blk_grid(items, n_slots); }
+
+cudaError_t launch_blk_apply(const BlkApplyParams &p, int arity, int nb, int n_slots, cudaStream_t st) {
+  dim3 grid(nb, n_slots);
+  if (arity == 3) blk_apply_kernel<3><<<grid, BLK_THREADS, 0, st>>>(p);
+  else blk_apply_kernel<2><<<grid, BLK_THREADS, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_blk_env(const BlkEnvParams &p, int arity, int nb, int n_slots, cudaStream_t st) {
+  dim3 grid(nb, n_slots);
+  if (arity == 3) blk_env_kernel<3><<<grid, BLK_THREADS, 0, st>>>(p);
+  else blk_env_kernel<2><<<grid, BLK_THREADS, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_blk_dist(const BlkDistParams &p, int nb, int n_slots, cudaStream_t st) {
+  blk_dist_kernel<<<dim3(nb, n_slots), BLK_THREADS, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_blk_gate_check(const double2 *g, const BlkGate *bg, int K, long long gsz, int s, unsigned *flag,
+                                  cudaStream_t st) {
+  const long long cnt = (long long)s * K;
+  if (cnt <= 0) return cudaSuccess;
+  const long long blocks = std::min<long long>((cnt + 127) / 128, 148 * 4);
+  blk_gate_check_kernel<<<(unsigned)blocks, 128, 0, st>>>(g, bg, K, gsz, s, flag);
+  return cudaGetLastError();
+}
+
+}  // namespace qfs

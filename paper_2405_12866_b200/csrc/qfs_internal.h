@@ -203,4 +203,51 @@ size_t val_cl_smem(int n, int K, int t);      // cluster validation, 2^t CTAs pe
 cudaError_t launch_val_cluster(const ValRowParams &p, int n_slots, cudaStream_t st);        // largest n the shared-memory validation forward supports
 int blocks_per_sm(int nu);  // resident CTAs per SM of the backward kernel
 
+
+// ---------------------------------------------------- multi-qubit blocks --
+// qfs_create_blocks circuits (qfs_blocks.cu).  Gate k:
+// arity a (2 or 3) on qubits q[0..a-1] (local l = sum_j b(q_j) 2^j), its d x d
+// matrix packed at complex offset off of the start's gate block (gsz entries).
+struct BlkGate {
+  int a, q[3], off, kind;
+};
+constexpr int kBlkMaxCtas = 148 * 4;  // CTAs per start of any block launch
+struct BlkApplyParams {
+  int n, k, dagger, rows_fixed;  // rows_fixed > 0: that many rows per start (validation)
+  const Slot *slots;
+  const BlkGate *bg;
+  const double2 *gates;
+  long long gsz;
+  View src;
+  ViewW dst;
+};
+struct BlkEnvParams {
+  int n, i, K, S;
+  const Slot *slots;
+  const BlkGate *bg;
+  double2 *gates;               // read (old gate) and written (update)
+  long long gsz;
+  View phi, chi;
+  double *partials;             // [S_act][nb][2 d^2]
+  unsigned *counters;           // [S_act]
+  double beta;
+  double *sig;                  // [S][K] or nullptr
+  double2 *env_trace;           // gate-major [S * gsz] for this sweep, or nullptr
+  unsigned *err;                // bit 8: the 8x8 polar iteration did not converge
+};
+struct BlkDistParams {
+  int n, rows_fixed;
+  const Slot *slots;
+  View a, b;
+  double *partials;             // [S_act][nb]
+  unsigned *counters;           // [S_act]
+  double *out;                  // [S_act]
+};
+int blk_ctas(long long items, int n_slots);
+cudaError_t launch_blk_apply(const BlkApplyParams &p, int arity, int nb, int n_slots, cudaStream_t st);
+cudaError_t launch_blk_env(const BlkEnvParams &p, int arity, int nb, int n_slots, cudaStream_t st);
+cudaError_t launch_blk_dist(const BlkDistParams &p, int nb, int n_slots, cudaStream_t st);
+cudaError_t launch_blk_gate_check(const double2 *g, const BlkGate *bg, int K, long long gsz, int s, unsigned *flag,
+                                  cudaStream_t st);
+
 }  // namespace qfs

@@ -52,6 +52,13 @@ struct qfs_ctx {
   std::vector<int32_t> pairs;
   int2 *d_pairs = nullptr;
   std::vector<int32_t> kinds;  // gate kinds (qfs_set_gate_kinds), default all QFS_GATE_VAR2
+  // multi-qubit blocks (qfs_create_blocks with at least one 3-qubit block):
+  // packed d x d gates, gsz complex entries per start (16 K for pair circuits)
+  bool blocks = false;
+  long long gsz = 0;
+  std::vector<BlkGate> bgh;
+  BlkGate *d_bg = nullptr;
+  double *d_bpart = nullptr;  // [S][kBlkMaxCtas][128] environment partials of the block path
   int *d_kinds = nullptr;
   cudaStream_t st = nullptr;
   cudaStream_t cur_st = nullptr;       // stream of the launches being issued
@@ -291,7 +298,8 @@ size_t plan_bytes(const qfs_ctx *c, int S, int M, int V, int nb) {
   size_t b = 0;
   b += (size_t)S * M * N * 16;                             // chi
   if (c->K > 1) b += (size_t)(c->K - 1) * S * M * N * 16;  // B cache
-  if (c->n > val_row_max_n() && V > 0) b += 2 * (size_t)S * V * N * 16;
+  if ((c->n > val_row_max_n() || c->blocks) && V > 0) b += 2 * (size_t)S * V * N * 16;
+  if (c->blocks) b += (size_t)S * kBlkMaxCtas * 128 * 8;
   b += (size_t)S * nb * 32 * 8 + (size_t)S * 64 * 8 + (size_t)S * c->K * 8 + (size_t)S * (V + 4) * 8;
   return b;
 }
@@ -301,7 +309,7 @@ qfs_status ensure_gates(qfs_ctx *c, int S) {
   dfree(c->d_gates);
   dfree(c->d_vprev);
   c->G_cap = 0;
-  CUDA_TRY(c, cudaMalloc(&c->d_gates, (size_t)S * c->K * 16 * sizeof(double2)));
+  CUDA_TRY(c, cudaMalloc(&c->d_gates, (size_t)S * c->gsz * sizeof(double2)));
   CUDA_TRY(c, cudaMalloc(&c->d_vprev, (size_t)S * c->K * 16 * sizeof(double2)));
   c->G_cap = S;
   drop_graph(c);
@@ -319,7 +327,7 @@ qfs_status ensure_state(qfs_ctx *c, int S, int M, int V) {
   V = std::max(V, c->V_cap);
   const int nbc = std::max(nb, c->nb_cap);
   CUDA_TRY(c, cudaStreamSynchronize(c->st));
-  dfree(c->d_chi); dfree(c->d_B); dfree(c->d_vb0); dfree(c->d_vb1);
+  dfree(c->d_chi); dfree(c->d_B); dfree(c->d_vb0); dfree(c->d_vb1); dfree(c->d_bpart);
   dfree(c->d_partials); dfree(c->d_ered); dfree(c->d_sig); dfree(c->d_csum); dfree(c->d_rowout);
   dfree(c->d_cval); dfree(c->d_counters); dfree(c->d_slots);
   dfree(c->d_flags); dfree(c->d_counters2); dfree(c->d_partials2);
@@ -341,10 +349,11 @@ qfs_status ensure_state(qfs_ctx *c, int S, int M, int V) {
   const size_t N = (size_t)c->N;
   CUDA_TRY(c, cudaMalloc(&c->d_chi, (size_t)S * M * N * sizeof(double2)));
   if (c->K > 1) CUDA_TRY(c, cudaMalloc(&c->d_B, (size_t)(c->K - 1) * S * M * N * sizeof(double2)));
-  if (c->n > val_row_max_n() && V > 0) {
+  if ((c->n > val_row_max_n() || c->blocks) && V > 0) {
     CUDA_TRY(c, cudaMalloc(&c->d_vb0, (size_t)S * V * N * sizeof(double2)));
     CUDA_TRY(c, cudaMalloc(&c->d_vb1, (size_t)S * V * N * sizeof(double2)));
   }
+  if (c->blocks) CUDA_TRY(c, cudaMalloc(&c->d_bpart, (size_t)S * kBlkMaxCtas * 128 * sizeof(double)));
   CUDA_TRY(c, cudaMalloc(&c->d_partials, (size_t)S * nbc * 32 * sizeof(double)));
   CUDA_TRY(c, cudaMalloc(&c->d_ered, (size_t)S * 32 * sizeof(double)));
   CUDA_TRY(c, cudaMalloc(&c->d_sig, (size_t)S * c->K * sizeof(double)));
@@ -438,7 +447,7 @@ qfs_status prepare_desc(qfs_ctx *c) {
   return QFS_OK;
 }
 
-bool use_persistent(const qfs_ctx *c) { return c->persistent && !(c->mode == 1 && c->world > 1); }
+bool use_persistent(const qfs_ctx *c) { return c->persistent && !c->blocks && !(c->mode == 1 && c->world > 1); }
 
 // Plan of the cluster-resident sweep (qfs_resident.cu) for ns starts of up to
 // M_max rows: the smallest power-of-two cluster whose CTAs hold their slice of
@@ -481,7 +490,97 @@ bool res_plan(const qfs_ctx *c, int M_max, int ns, ResPlan &pl) {
 
 // Issue the launches of one sweep for the slots [j0, j1) on stream st (no host
 // synchronisation).  Scratch arrays indexed by slot are offset by j0.
+
+// One sweep of a multi-qubit block circuit for slots [j0, j1) (qfs_blocks.cu):
+// the same steps as the streamed pair sweep below, one plain launch per step
+// (P:112 right to left; P:127 / P:165 B cache; P:172 environments).
+qfs_status issue_blocks(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStream_t st) {
+  const int ns = j1 - j0, K = c->K, n = c->n;
+  int M_max = 0;
+  for (int j = j0; j < j1; ++j) M_max = std::max(M_max, sp.slots[j].m);
+  const Slot *slots = c->d_slots + j0;
+  unsigned *cnt_b = c->d_counters + j0, *cnt_f = c->d_counters + c->S_cap + j0;
+  double *csum = c->d_csum + j0, *cval = c->d_cval + j0;
+  double *bpart = c->d_bpart + (long long)j0 * kBlkMaxCtas * 128;
+  double *dpart = c->d_partials + (long long)j0 * c->nb_cap * 32;
+  const long long N = c->N, Mc = c->M_cap, sS = N * Mc;
+  const View xpool{c->d_x, 0, c->m_pool, 1}, ypool{c->d_y, 0, c->m_pool, 1};
+  auto Bk = [&](int k) -> double2 * { return c->d_B + (long long)(k - 1) * c->S_cap * sS; };
+  double units = 0;
+  for (int j = j0; j < j1; ++j) units += (double)sp.slots[j].m * (double)N;
+  auto apply = [&](int k, int dagger, const View &src, const ViewW &dst, int rows_fixed, long long rows) -> qfs_status {
+    BlkApplyParams a{};
+    a.n = n; a.k = k; a.dagger = dagger; a.rows_fixed = rows_fixed; a.slots = slots; a.bg = c->d_bg;
+    a.gates = c->d_gates; a.gsz = c->gsz; a.src = src; a.dst = dst;
+    const int ar = c->bgh[k].a;
+    CUDA_TRY(c, launch_blk_apply(a, ar, blk_ctas((N >> ar) * rows, ns), ns, st));
+    c->launches++;
+    return QFS_OK;
+  };
+  qfs_status r;
+  // (a) forward: B_{k+1} = G_k B_k
+  {
+    PhaseScope phase(c, K_FWD_GATE);
+    LaunchScope ls(c, K_FWD_GATE, units * 32.0 * (K - 1), 0.0);
+    for (int k = 0; k + 1 < K; ++k)
+      if ((r = apply(k, 0, k == 0 ? xpool : View{Bk(k), sS, Mc, 1}, ViewW{Bk(k + 1), sS, Mc, 1}, 0, M_max)) != QFS_OK)
+        return r;
+  }
+  // (b, c) backward: chi <- G_{i+1}^dag chi, then E_i and the update of gate i
+  {
+    PhaseScope phase(c, K_BWD);
+    LaunchScope ls(c, K_BWD, units * 48.0 * K, 0.0);
+    for (int i = K - 1; i >= 0; --i) {
+      if (i < K - 1)
+        if ((r = apply(i + 1, 1, i == K - 2 ? ypool : View{c->d_chi, sS, Mc, 1}, ViewW{c->d_chi, sS, Mc, 1}, 0, M_max)) !=
+            QFS_OK)
+          return r;
+      BlkEnvParams e{};
+      e.n = n; e.i = i; e.K = K; e.S = sp.S; e.slots = slots; e.bg = c->d_bg; e.gates = c->d_gates; e.gsz = c->gsz;
+      e.phi = i == 0 ? xpool : View{Bk(i), sS, Mc, 1};
+      e.chi = i == K - 1 ? ypool : View{c->d_chi, sS, Mc, 1};
+      e.partials = bpart; e.counters = cnt_b; e.beta = sp.beta; e.sig = c->d_sig;
+      e.env_trace = sp.env_trace; e.err = c->d_check;
+      const int ar = c->bgh[i].a;
+      CUDA_TRY(c, launch_blk_env(e, ar, blk_ctas((N >> ar) * M_max, ns), ns, st));
+      c->launches++;
+    }
+  }
+  // (d) c_train: chi' = G_0^dag chi, sum ||chi' - x||^2 (P:116-120 direct form)
+  {
+    PhaseScope phase(c, K_FINAL);
+    LaunchScope ls(c, K_FINAL, units * 32.0, 0.0);
+    if ((r = apply(0, 1, K == 1 ? ypool : View{c->d_chi, sS, Mc, 1}, ViewW{c->d_chi, sS, Mc, 1}, 0, M_max)) != QFS_OK)
+      return r;
+    BlkDistParams d{};
+    d.n = n; d.rows_fixed = 0; d.slots = slots; d.a = View{c->d_chi, sS, Mc, 1}; d.b = xpool;
+    d.partials = dpart; d.counters = cnt_f; d.out = csum;
+    CUDA_TRY(c, launch_blk_dist(d, blk_ctas(N * M_max, ns), ns, st));
+    c->launches++;
+  }
+  // validation cost: V rows through the post-sweep gates
+  if (sp.want_val && c->V > 0) {
+    PhaseScope phase(c, K_VAL_ROW);
+    LaunchScope ls(c, K_VAL_ROW, (double)ns * c->V * N * 32.0 * K, 0.0);
+    const long long VN = (long long)c->V * N;
+    for (int k = 0; k < K; ++k) {
+      double2 *dst = (k & 1) ? c->d_vb1 : c->d_vb0;
+      const View src = k == 0 ? View{c->d_xv, 0, 1, N} : View{(k & 1) ? c->d_vb0 : c->d_vb1, VN, 1, N};
+      if ((r = apply(k, 0, src, ViewW{dst, VN, 1, N}, c->V, c->V)) != QFS_OK) return r;
+    }
+    BlkDistParams d{};
+    d.n = n; d.rows_fixed = c->V; d.slots = slots;
+    d.a = View{((K - 1) & 1) ? c->d_vb1 : c->d_vb0, VN, 1, N};
+    d.b = View{c->d_yv, 0, 1, N};
+    d.partials = dpart; d.counters = cnt_f; d.out = cval;
+    CUDA_TRY(c, launch_blk_dist(d, blk_ctas(VN, ns), ns, st));
+    c->launches++;
+  }
+  return QFS_OK;
+}
+
 qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStream_t st) {
+  if (c->blocks) return issue_blocks(c, sp, j0, j1, st);
   const int ns = j1 - j0;
   const int K = c->K, n = c->n;
   c->cur_st = st;
@@ -811,6 +910,7 @@ qfs_status gate_check_result(qfs_ctx *c) {
   if (bad & 1u) return fail(c, QFS_ERR_NUMERIC, "non-finite initial gate");
   if (bad & 2u) return fail(c, QFS_ERR_NUMERIC, "initial gate not unitary (tol 1e-10)");
   if (bad & 4u) return fail(c, QFS_ERR_NUMERIC, "one-qubit gate slot is not of the form u (x) I (tol 1e-10)");
+  if (bad & 8u) return fail(c, QFS_ERR_NUMERIC, "8x8 polar iteration did not converge (singular environment)");
   return QFS_OK;
 }
 
@@ -818,7 +918,7 @@ qfs_status upload_gates(qfs_ctx *c, int s, const double *init) {
   if (!c->h_check) {
     CUDA_TRY(c, cudaMallocHost((void **)&c->h_check, sizeof(unsigned)));
   }
-  const size_t gb = (size_t)s * c->K * 16 * sizeof(double2);
+  const size_t gb = (size_t)s * c->gsz * sizeof(double2);
   if (gb > c->h_gates_cap) {
     if (c->h_gates) cudaFreeHost(c->h_gates);
     c->h_gates = nullptr;
@@ -831,12 +931,13 @@ qfs_status upload_gates(qfs_ctx *c, int s, const double *init) {
   // on a copy engine behind a caller's large H2D (qfs_set_samples_async)
   double2 *dh = nullptr;
   CUDA_TRY(c, cudaHostGetDevicePointer((void **)&dh, c->h_gates, 0));
-  CUDA_TRY(c, launch_copy(c->d_gates, dh, (long long)s * c->K * 16, c->st));
+  CUDA_TRY(c, launch_copy(c->d_gates, dh, (long long)s * c->gsz, c->st));
   {
     // device-side flag, read back (device -> host, 4 bytes) after the first sweep
     if (!c->d_check) CUDA_TRY(c, cudaMalloc(&c->d_check, sizeof(unsigned)));
     CUDA_TRY(c, launch_fill_words(c->d_check, 0u, 1, c->st));
-    CUDA_TRY(c, launch_gate_check(c->d_gates, (long long)s * c->K, c->K, c->d_kinds, c->d_check, c->st));
+    if (c->blocks) CUDA_TRY(c, launch_blk_gate_check(c->d_gates, c->d_bg, c->K, c->gsz, s, c->d_check, c->st));
+    else CUDA_TRY(c, launch_gate_check(c->d_gates, (long long)s * c->K, c->K, c->d_kinds, c->d_check, c->st));
     c->check_pending = true;
   }
   CUDA_TRY(c, launch_identity_fill(c->d_vprev, (long long)s * c->K, c->st));
@@ -868,7 +969,7 @@ qfs_status create_common(int n, int k, const int32_t *pairs, int device, qfs_ctx
     if (a < 0 || b < 0 || a >= n || b >= n || a == b) return QFS_ERR_ARG;
   }
   qfs_ctx *c = new qfs_ctx();
-  c->n = n; c->K = k; c->N = 1LL << n; c->device = device;
+  c->n = n; c->K = k; c->N = 1LL << n; c->device = device; c->gsz = 16LL * k;
   c->pairs.assign(pairs, pairs + 2 * k);
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking);
@@ -915,6 +1016,44 @@ extern "C" {
 
 qfs_status qfs_create(int n, int k, const int32_t *pairs, int device, qfs_ctx **out) {
   return create_common(n, k, pairs, device, out);
+}
+
+qfs_status qfs_create_blocks(int n, int k, const int32_t *qubits, const int32_t *arity, int device,
+                             qfs_ctx **out) {
+  if (!out) return QFS_ERR_ARG;
+  *out = nullptr;
+  if (n < 3 || n > 26 || k < 1 || !qubits || !arity) return QFS_ERR_ARG;
+  std::vector<int32_t> pairs(2 * (size_t)k);
+  std::vector<BlkGate> bg(k);
+  long long off = 0;
+  bool any3 = false;
+  for (int i = 0; i < k; ++i) {
+    const int a = arity[i];
+    if (a != 2 && a != 3) return QFS_ERR_ARG;
+    for (int j = 0; j < a; ++j) {
+      const int q = qubits[3 * i + j];
+      if (q < 0 || q >= n) return QFS_ERR_ARG;
+      for (int t = 0; t < j; ++t)
+        if (qubits[3 * i + t] == q) return QFS_ERR_ARG;
+    }
+    bg[i].a = a;
+    for (int j = 0; j < 3; ++j) bg[i].q[j] = j < a ? qubits[3 * i + j] : 0;
+    bg[i].off = (int)off;
+    bg[i].kind = QFS_GATE_VAR2;
+    off += 1LL << (2 * a);
+    any3 = any3 || a == 3;
+    pairs[2 * i] = qubits[3 * i];
+    pairs[2 * i + 1] = qubits[3 * i + 1];
+  }
+  qfs_status s = create_common(n, k, pairs.data(), device, out);
+  if (s != QFS_OK || !any3) return s;  // all two-qubit: the pair circuit (same packed layout)
+  qfs_ctx *c = *out;
+  c->blocks = true;
+  c->gsz = off;
+  c->bgh = bg;
+  CUDA_TRY(c, cudaMalloc(&c->d_bg, (size_t)k * sizeof(BlkGate)));
+  CUDA_TRY(c, cudaMemcpy(c->d_bg, bg.data(), (size_t)k * sizeof(BlkGate), cudaMemcpyHostToDevice));
+  return QFS_OK;
 }
 
 qfs_status qfs_create_dist(int n, int k, const int32_t *pairs, int device, void *nccl_comm,
@@ -1114,7 +1253,7 @@ qfs_status qfs_trace_sweeps(qfs_ctx *c, int s, const double *init_gates, int m, 
   if ((st = ensure_gates(c, s)) != QFS_OK) return st;
   if ((st = ensure_state(c, s, ml, c->V)) != QFS_OK) return st;
   if ((st = upload_gates(c, s, init_gates)) != QFS_OK) return st;
-  const size_t tr = (size_t)c->K * s * 16;
+  const size_t tr = (size_t)s * c->gsz;  // gate-major: gate i of start q at s * off_i + q * d_i^2
   if (env_trace && tr > c->env_trace_cap) {
     dfree(c->d_env_trace);
     CUDA_TRY(c, cudaMalloc(&c->d_env_trace, tr * sizeof(double2)));
@@ -1132,8 +1271,8 @@ qfs_status qfs_trace_sweeps(qfs_ctx *c, int s, const double *init_gates, int m, 
       CUDA_TRY(c, cudaMemcpy(env_trace + (size_t)t * tr * 2, c->d_env_trace, tr * sizeof(double2),
                              cudaMemcpyDeviceToHost));
     if (gate_trace)
-      CUDA_TRY(c, cudaMemcpy(gate_trace + (size_t)t * s * c->K * 32, c->d_gates,
-                             (size_t)s * c->K * sizeof(double2) * 16, cudaMemcpyDeviceToHost));
+      CUDA_TRY(c, cudaMemcpy(gate_trace + (size_t)t * s * c->gsz * 2, c->d_gates,
+                             (size_t)s * c->gsz * sizeof(double2), cudaMemcpyDeviceToHost));
     if (cost_trace)
       for (int q = 0; q < s; ++q) cost_trace[(size_t)t * s + q] = csum[q] / m;
     if (sigma_trace) {
@@ -1272,10 +1411,10 @@ qfs_status qfs_instantiate(qfs_ctx *c, int s, const double *init_gates, const qf
       if (A[q].c_train < bc) { bc = A[q].c_train; win = q; }
     if (win < 0) win = 0;
   }
-  CUDA_TRY(c, cudaMemcpyAsync(c->h_gates, c->d_gates, (size_t)s * c->K * 16 * sizeof(double2),
+  CUDA_TRY(c, cudaMemcpyAsync(c->h_gates, c->d_gates, (size_t)s * c->gsz * sizeof(double2),
                               cudaMemcpyDeviceToHost, c->st));
   CUDA_TRY(c, cudaStreamSynchronize(c->st));
-  std::memcpy(out_gates, c->h_gates, (size_t)s * c->K * 16 * sizeof(double2));
+  std::memcpy(out_gates, c->h_gates, (size_t)s * c->gsz * sizeof(double2));
   for (int q = 0; q < s; ++q) {
     out[q].c_train = A[q].c_train; out[q].c_val = A[q].c_val; out[q].sweeps = A[q].total;
     out[q].restarts = A[q].restarts; out[q].final_m = A[q].M; out[q].term = (qfs_term)A[q].term;
@@ -1427,8 +1566,16 @@ qfs_status qfs_set_gate_kinds(qfs_ctx *c, const int32_t *kinds) {
     for (int i = 0; i < c->K; ++i) {
       if (kinds[i] < QFS_GATE_VAR2 || kinds[i] > QFS_GATE_VAR1)
         return fail(c, QFS_ERR_ARG, "gate kind must be 0 (two-qubit variable), 1 (fixed) or 2 (one-qubit variable)");
+      if (c->blocks && kinds[i] == QFS_GATE_VAR1 && c->bgh[i].a != 2)
+        return fail(c, QFS_ERR_ARG, "one-qubit variable slots must be two-qubit blocks");
       k[i] = kinds[i];
     }
+  if (c->blocks) {
+    for (int i = 0; i < c->K; ++i) c->bgh[i].kind = k[i];
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaMemcpy(c->d_bg, c->bgh.data(), (size_t)c->K * sizeof(BlkGate), cudaMemcpyHostToDevice));
+    drop_graph(c);
+  }
   CUDA_TRY(c, cudaSetDevice(c->device));
   CUDA_TRY(c, cudaMemcpy(c->d_kinds, k.data(), k.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
   c->kinds.swap(k);
@@ -1468,7 +1615,7 @@ void qfs_destroy(qfs_ctx *c) {
   prof_collect(c);
   drop_graph(c);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
-  dfree(c->d_pairs); dfree(c->d_kinds); dfree(c->d_flag); dfree(c->d_x); dfree(c->d_y); dfree(c->d_xv); dfree(c->d_yv);
+  dfree(c->d_pairs); dfree(c->d_kinds); dfree(c->d_bg); dfree(c->d_bpart); dfree(c->d_flag); dfree(c->d_x); dfree(c->d_y); dfree(c->d_xv); dfree(c->d_yv);
   dfree(c->d_gates); dfree(c->d_chi); dfree(c->d_B); dfree(c->d_vb0); dfree(c->d_vb1);
   dfree(c->d_partials); dfree(c->d_ered); dfree(c->d_sig); dfree(c->d_csum); dfree(c->d_rowout);
   dfree(c->d_cval); dfree(c->d_counters); dfree(c->d_slots); dfree(c->d_env_trace);

@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libqfs.so")
 STATUS = {0: "QFS_OK", 1: "QFS_ERR_ARG", 2: "QFS_ERR_CAPACITY", 3: "QFS_ERR_NUMERIC",
           4: "QFS_ERR_DEVICE", 5: "QFS_ERR_STATE"}
 TERM_NAMES = {0: "CONVERGED", 1: "PLATEAU", 2: "MAX_ITER", 3: "POOL_EXHAUSTED", 4: "STOPPED"}
-SYMBOLS = ["qfs_create", "qfs_create_dist", "qfs_nccl_unique_id", "qfs_create_nccl", "qfs_set_samples", "qfs_set_samples_async", "qfs_set_samples_device",
+SYMBOLS = ["qfs_create", "qfs_create_blocks", "qfs_create_dist", "qfs_nccl_unique_id", "qfs_create_nccl", "qfs_set_samples", "qfs_set_samples_async", "qfs_set_samples_device",
            "qfs_instantiate", "qfs_trace_sweeps", "qfs_bench_sweeps", "qfs_op_apply",
            "qfs_op_environment", "qfs_op_polar", "qfs_profile_enable", "qfs_profile_read", "qfs_set_path", "qfs_set_gate_kinds",
            "qfs_launch_count", "qfs_stream", "qfs_last_error", "qfs_destroy"]
@@ -65,6 +65,7 @@ def load(path: str = LIB_PATH):
         lib.qfs_destroy.argtypes = [vp]
         lib.qfs_destroy.restype = None
         lib.qfs_create.argtypes = [ip, ip, vp, ip, ctypes.POINTER(vp)]
+        lib.qfs_create_blocks.argtypes = [ip, ip, vp, vp, ip, ctypes.POINTER(vp)]
         lib.qfs_create_dist.argtypes = [ip, ip, vp, ip, vp, ip, ip, ip, ctypes.POINTER(vp)]
         lib.qfs_nccl_unique_id.argtypes = [vp]
         lib.qfs_create_nccl.argtypes = [ip, ip, vp, ip, vp, ip, ip, ip, ctypes.POINTER(vp)]
@@ -275,6 +276,44 @@ class Context:
     def stream_ptr(self):
         return self.lib.qfs_stream(self.h)
 
+
+
+class BlockContext(Context):
+    """qfs_create_blocks: a circuit of 2- and 3-qubit blocks (qubits [k][3],
+    arity [k]); gates are PACKED per start ([s][G] complex128, see
+    inputs.pack_gates and include/qfs.h)."""
+
+    def __init__(self, n, qubits, arity, device=0):
+        self.lib = load()
+        self.n = int(n)
+        self.qubits = np.ascontiguousarray(np.asarray(qubits).reshape(-1, 3), dtype=np.int32)
+        self.arity = np.ascontiguousarray(np.asarray(arity).reshape(-1), dtype=np.int32)
+        self.k = int(self.arity.shape[0])
+        self.gsz = int(sum(1 << (2 * int(a)) for a in self.arity))
+        self.pairs = np.ascontiguousarray(self.qubits[:, :2])
+        h = ctypes.c_void_p()
+        rc = self.lib.qfs_create_blocks(self.n, self.k, _ptr(self.qubits), _ptr(self.arity), int(device),
+                                        ctypes.byref(h))
+        self.h = h
+        if rc != 0:
+            msg = self.lib.qfs_last_error(h).decode() if h.value else "invalid arguments"
+            if h.value:
+                self.lib.qfs_destroy(h)
+            self.h = None
+            raise QfsError(rc, msg)
+        self.world = 1
+        self.shard_mode = 0
+
+    def trace_sweeps(self, init_gates, m, n_sweeps, beta=0.0, env=True, gates=True, cost=True, sigma=True):
+        g = _c128(np.asarray(init_gates).reshape(-1, self.gsz))
+        s, k = g.shape[0], self.k
+        e = np.zeros((n_sweeps, s * self.gsz), np.complex128) if env else None
+        gt = np.zeros((n_sweeps, s, self.gsz), np.complex128) if gates else None
+        ct = np.zeros((n_sweeps, s)) if cost else None
+        sg = np.zeros((n_sweeps, k, s)) if sigma else None
+        self._check(self.lib.qfs_trace_sweeps(self.h, s, _ptr(g), int(m), float(beta), int(n_sweeps),
+                                              _ptr(e), _ptr(gt), _ptr(ct), _ptr(sg)))
+        return dict(env=e, gates=gt, cost=ct, sigma=sg)
 
 def default_params(**kw) -> dict:
     d = dict(dist_tol=1e-8, diff_tol_r=1e-3, plateau_window=5, min_iter=6, max_iter=1000,
