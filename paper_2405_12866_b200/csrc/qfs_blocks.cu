@@ -65,6 +65,14 @@ __device__ __forceinline__ BlkLocal blk_local(const BlkGate &g) {
   return b;
 }
 
+// shared-memory load the compiler may not hoist out of the item loop (a
+// hoisted 8x8 gate would take 256 registers)
+__device__ __forceinline__ double2 lds_c(const double2 *p) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return v;
+}
+
 // --------------------------------------------------------------- apply --
 // dst = G_k src (dagger: G_k^dag) for every (group, row) of every slot.
 template <int A>
@@ -99,7 +107,7 @@ __global__ void __launch_bounds__(BLK_THREADS) blk_apply_kernel(const BlkApplyPa
     for (int a = 0; a < D; ++a) {
       double2 o = make_double2(0.0, 0.0);
 #pragma unroll
-      for (int b = 0; b < D; ++b) cfma(o, sG[D * a + b], v[b]);
+      for (int b = 0; b < D; ++b) cfma(o, lds_c(&sG[D * a + b]), v[b]);
       dst[(long long)(base | L.off[a]) * P.dst.sa + (long long)m * P.dst.sm] = o;
     }
   }
@@ -113,7 +121,7 @@ __global__ void __launch_bounds__(BLK_THREADS) blk_apply_kernel(const BlkApplyPa
 // nonsingular E').  Stops when ||X^dag X - I||_F <= 1e-14; returns false if it
 // does not within 100 iterations (singular E').  G = W^dag = Y X^dag (eq:opt_u,
 // P:59-62, with E' = X D Y^dag), sum sigma = Re Tr(W^dag E').
-__device__ bool polar8(const double2 (&e)[2], double2 (&g)[2], double &ss, double2 *sm /*[2][64]*/) {
+__device__ __noinline__ bool polar8(const double2 (&e)[2], double2 (&g)[2], double &ss, double2 *sm /*[2][64]*/) {
   const int lane = threadIdx.x & 31;
   double2 *sX = sm, *sT = sm + 64;
   auto xhx = [&](const double2 (&X)[2], double2 (&Y)[2]) {  // Y = X^dag X, X left in sX
@@ -197,29 +205,33 @@ __global__ void __launch_bounds__(BLK_THREADS) blk_env_kernel(const BlkEnvParams
   const unsigned rows = (unsigned)sl.m;
   const BlkGate bg = P.bg[P.i];
   const BlkLocal L = blk_local<A>(bg);
-  double2 acc[DD];
+  // PARTS lanes share an item, each owning XR rows of E (64 complex
+  // accumulators would take 256 registers for d = 8)
+  constexpr int PARTS = A == 3 ? 4 : 1, XR = D / PARTS;
+  const int part = threadIdx.x % PARTS;
+  double2 acc[XR * D];
 #pragma unroll
-  for (int e = 0; e < DD; ++e) acc[e] = make_double2(0.0, 0.0);
+  for (int e = 0; e < XR * D; ++e) acc[e] = make_double2(0.0, 0.0);
   const unsigned items = (1u << (P.n - A)) * rows;
   const unsigned chunk = (items + gridDim.x - 1) / gridDim.x;
   const unsigned beg = blockIdx.x * chunk, end = min(items, beg + chunk);
   const FastDiv fd(rows);
   const double2 *ph = P.phi.base + (long long)s * P.phi.ss;
   const double2 *ch = P.chi.base + (long long)s * P.chi.ss;
-  for (unsigned w = beg + threadIdx.x; w < end; w += blockDim.x) {
+  for (unsigned w = beg + threadIdx.x / PARTS; w < end; w += blockDim.x / PARTS) {
     const unsigned r = fd.div(w), m = w - r * rows;
     const unsigned base = blk_base<A>(r, L.srt);
-    double2 f[D], c[D];
+    double2 f[XR], c[D];
 #pragma unroll
-    for (int l = 0; l < D; ++l) {
-      f[l] = ph[(long long)(base | L.off[l]) * P.phi.sa + (long long)m * P.phi.sm];
-      c[l] = ch[(long long)(base | L.off[l]) * P.chi.sa + (long long)m * P.chi.sm];
-    }
+    for (int x = 0; x < XR; ++x)
+      f[x] = ph[(long long)(base | L.off[part * XR + x]) * P.phi.sa + (long long)m * P.phi.sm];
 #pragma unroll
-    for (int x = 0; x < D; ++x)
+    for (int l = 0; l < D; ++l) c[l] = ch[(long long)(base | L.off[l]) * P.chi.sa + (long long)m * P.chi.sm];
+#pragma unroll
+    for (int x = 0; x < XR; ++x)
 #pragma unroll
       for (int y = 0; y < D; ++y) {
-        double2 &e = acc[D * x + y];  // f[x] conj(c[y])
+        double2 &e = acc[D * x + y];  // f[x] conj(c[y]), row part * XR + x of E
         e.x = fma(f[x].x, c[y].x, e.x);
         e.x = fma(f[x].y, c[y].y, e.x);
         e.y = fma(f[x].y, c[y].x, e.y);
@@ -228,17 +240,22 @@ __global__ void __launch_bounds__(BLK_THREADS) blk_env_kernel(const BlkEnvParams
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int e = 0; e < DD; ++e) {
-    const double re = warp_sum_d(acc[e].x), im = warp_sum_d(acc[e].y);
-    if (lane == 0) red[warp][e] = make_double2(re, im);
+  for (int e = 0; e < XR * D; ++e) {  // sum over the lanes of this part (xor offsets keep lane % PARTS)
+    double re = acc[e].x, im = acc[e].y;
+#pragma unroll
+    for (int o = 16; o >= PARTS; o >>= 1) {
+      re += __shfl_xor_sync(FULL, re, o);
+      im += __shfl_xor_sync(FULL, im, o);
+    }
+    if (lane < PARTS) red[warp][part * XR * D + e] = make_double2(re, im);
   }
   __syncthreads();
-  double2 *part = reinterpret_cast<double2 *>(P.partials) + ((long long)j * gridDim.x + blockIdx.x) * DD;
+  double2 *cta_part = reinterpret_cast<double2 *>(P.partials) + ((long long)j * gridDim.x + blockIdx.x) * DD;
   for (int e = threadIdx.x; e < DD; e += blockDim.x) {
     double2 t = make_double2(0.0, 0.0);
 #pragma unroll
     for (int w = 0; w < NW; ++w) { t.x += red[w][e].x; t.y += red[w][e].y; }
-    part[e] = t;
+    cta_part[e] = t;
   }
   __threadfence();
   __syncthreads();
