@@ -91,8 +91,9 @@ qfs_status qfs_create(int n, int k, const int32_t *pairs, int device, qfs_ctx **
  * s at s_total * off_i + s * d_i^2.  Circuits with a 3-qubit block run the
  * streamed sweep (B cache in HBM) with one launch per step, single GPU
  * (qfs_create_dist / sample sharding are not available for them); the 8x8
- * update is the Newton-Schulz polar factor (singular 8x8 environments are
- * reported as QFS_ERR_NUMERIC by the next call that validates gates).  Gate
+ * update is the Newton-Schulz polar factor, with a one-sided Jacobi SVD for
+ * singular or very ill-conditioned environments (null columns completed as
+ * in the oracle; the gate is then not unique, only the cost is).  Gate
  * kinds (qfs_set_gate_kinds) apply per block: VAR2 = variable (any arity),
  * FIXED, VAR1 only on two-qubit blocks.  Errors: QFS_ERR_ARG for a bad
  * structure (n < 3, arity not 2/3, repeated or out-of-range qubits). */

@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(BLK_THREADS) blk_apply_kernel(const BlkApplyPa
 // from X_0 = E' sqrt(2.9 / ||E'^dag E'||_F): every singular value of X_0 is
 // then below sqrt(2.9) < sqrt(3), where the iteration converges (to W for a
 // nonsingular E').  Stops when ||X^dag X - I||_F <= 1e-14; returns false if it
-// does not within 100 iterations (singular E').  G = W^dag = Y X^dag (eq:opt_u,
+// does not within 60 iterations (singular or very ill-conditioned E').  G = W^dag = Y X^dag (eq:opt_u,
 // P:59-62, with E' = X D Y^dag), sum sigma = Re Tr(W^dag E').
 __device__ __noinline__ bool polar8(const double2 (&e)[2], double2 (&g)[2], double &ss, double2 *sm /*[2][64]*/) {
   const int lane = threadIdx.x & 31;
@@ -145,7 +145,7 @@ __device__ __noinline__ bool polar8(const double2 (&e)[2], double2 (&g)[2], doub
   const double sc = sqrt(2.9 / fy);
   x[0].x *= sc; x[0].y *= sc; x[1].x *= sc; x[1].y *= sc;
   bool ok = false;
-  for (int it = 0; it < 100; ++it) {
+  for (int it = 0; it < 60; ++it) {
     xhx(x, y);
     double err = 0.0;
 #pragma unroll
@@ -185,6 +185,134 @@ __device__ __noinline__ bool polar8(const double2 (&e)[2], double2 (&g)[2], doub
   }
   ss = warp_sum_d(x[0].x * e[0].x + x[0].y * e[0].y + x[1].x * e[1].x + x[1].y * e[1].y);
   return ok;
+}
+
+
+// Fallback for environments Newton-Schulz cannot handle (singular or very
+// ill-conditioned E'): one-sided Jacobi on a warp, the 8-column analogue of
+// hw_polar (qfs_device.cuh).  Lane l holds rows l>>3 and (l>>3)+4 of column
+// c = l & 7 of A = E' V and of V (V_0 = I); round x = 1..7 rotates the
+// disjoint column pairs (c, c ^ x) (the 28 pairs of a sweep), until no pair has
+// |gamma| > 1e-12 ||a_j|| ||a_k||; sigma_j = ||a_j||, X_j = a_j / sigma_j, null
+// columns (sigma_j <= 1e-14 sigma_max) completed by Gram-Schmidt on e_0..e_7
+// (as the oracle), G = V X^dag (eq:opt_u), sum sigma.
+__device__ __noinline__ void polar8_jacobi(const double2 (&e)[2], double2 (&g)[2], double &ss, double2 *sm) {
+  const int lane = threadIdx.x & 31, c = lane & 7, r0 = lane >> 3;
+  double mx = fmax(fmax(fabs(e[0].x), fabs(e[0].y)), fmax(fabs(e[1].x), fabs(e[1].y)));
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+  const int ex = mx > 0.0 ? ilogb(mx) : 0;
+  double2 a[2], v[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    a[h] = make_double2(scalbn(e[h].x, -ex), scalbn(e[h].y, -ex));
+    v[h] = make_double2(r0 + 4 * h == c ? 1.0 : 0.0, 0.0);
+  }
+  for (int sweep = 0; sweep < 30; ++sweep) {
+    bool big = false;
+#pragma unroll 1
+    for (int x = 1; x < 8; ++x) {
+      const bool lo = c < (c ^ x);
+      double2 aj[2], ak[2], vj[2], vk[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double2 ap = shfl_xor_c(a[h], x), vp = shfl_xor_c(v[h], x);
+        aj[h] = lo ? a[h] : ap; ak[h] = lo ? ap : a[h];
+        vj[h] = lo ? v[h] : vp; vk[h] = lo ? vp : v[h];
+      }
+      double al = 0.0, be = 0.0, gr = 0.0, gi = 0.0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        al += aj[h].x * aj[h].x + aj[h].y * aj[h].y;
+        be += ak[h].x * ak[h].x + ak[h].y * ak[h].y;
+        gr += aj[h].x * ak[h].x + aj[h].y * ak[h].y;
+        gi += aj[h].x * ak[h].y - aj[h].y * ak[h].x;
+      }
+#pragma unroll
+      for (int o = 8; o <= 16; o <<= 1) {
+        al += __shfl_xor_sync(FULL, al, o);
+        be += __shfl_xor_sync(FULL, be, o);
+        gr += __shfl_xor_sync(FULL, gr, o);
+        gi += __shfl_xor_sync(FULL, gi, o);
+      }
+      const double ag2 = gr * gr + gi * gi, ab = al * be;
+      big = big || ag2 > 1e-24 * ab;
+      if (ag2 > 0.0 && ag2 > 1e-30 * ab) {  // rotation of hw_polar (rsqrt form)
+        const double D = be - al, q4 = 4.0 * ag2, w = fma(D, D, q4), R = w * rsqrt(w);
+        const double den = fabs(D) + R, rr = rsqrt(fma(den, den, q4)), cc = den * rr;
+        const double f2 = (D >= 0.0 ? 2.0 : -2.0) * rr, spr = f2 * gr, spi = f2 * gi;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (lo) {
+            a[h] = make_double2(cc * aj[h].x - (spr * ak[h].x + spi * ak[h].y), cc * aj[h].y - (spr * ak[h].y - spi * ak[h].x));
+            v[h] = make_double2(cc * vj[h].x - (spr * vk[h].x + spi * vk[h].y), cc * vj[h].y - (spr * vk[h].y - spi * vk[h].x));
+          } else {
+            a[h] = make_double2((spr * aj[h].x - spi * aj[h].y) + cc * ak[h].x, (spr * aj[h].y + spi * aj[h].x) + cc * ak[h].y);
+            v[h] = make_double2((spr * vj[h].x - spi * vj[h].y) + cc * vk[h].x, (spr * vj[h].y + spi * vj[h].x) + cc * vk[h].y);
+          }
+        }
+      }
+    }
+    if (!__any_sync(FULL, big)) break;
+  }
+  double nn = a[0].x * a[0].x + a[0].y * a[0].y + a[1].x * a[1].x + a[1].y * a[1].y;
+  nn += __shfl_xor_sync(FULL, nn, 8);
+  nn += __shfl_xor_sync(FULL, nn, 16);
+  const double sig = sqrt(nn);
+  double smax = sig;
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1) smax = fmax(smax, __shfl_xor_sync(FULL, smax, o));
+  const bool nul = !(sig > 1e-14 * smax) || smax == 0.0;
+  double2 *sX = sm, *sV = sm + 64;
+  __syncwarp();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int idx = 8 * (r0 + 4 * h) + c;
+    sX[idx] = nul ? make_double2(0.0, 0.0) : make_double2(a[h].x / sig, a[h].y / sig);
+    sV[idx] = v[h];
+  }
+  __syncwarp();
+  const unsigned nm = __ballot_sync(FULL, nul && r0 == 0) & 0xffu;  // bit c: column c null
+  if (nm && lane == 0) {
+    for (int jj = 0; jj < 8; ++jj) {
+      if (!((nm >> jj) & 1)) continue;
+      for (int e0 = 0; e0 < 8; ++e0) {
+        double2 u[8];
+        for (int q = 0; q < 8; ++q) u[q] = make_double2(q == e0 ? 1.0 : 0.0, 0.0);
+        for (int pass = 0; pass < 2; ++pass)
+          for (int q = 0; q < 8; ++q) {
+            if (q == jj || (((nm >> q) & 1) && q > jj)) continue;
+            double2 d = make_double2(0.0, 0.0);
+            for (int rr = 0; rr < 8; ++rr) cfma(d, cconj(sX[8 * rr + q]), u[rr]);
+            for (int rr = 0; rr < 8; ++rr) {
+              const double2 t = cmul(d, sX[8 * rr + q]);
+              u[rr].x -= t.x;
+              u[rr].y -= t.y;
+            }
+          }
+        double nv = 0.0;
+        for (int rr = 0; rr < 8; ++rr) nv += u[rr].x * u[rr].x + u[rr].y * u[rr].y;
+        nv = sqrt(nv);
+        if (nv > 0.5) {
+          for (int rr = 0; rr < 8; ++rr) sX[8 * rr + jj] = make_double2(u[rr].x / nv, u[rr].y / nv);
+          break;
+        }
+      }
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {  // G[r][c] = sum_q V[r][q] conj(X[c][q])
+    const int r = r0 + 4 * h;
+    double2 t = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) cfma(t, sV[8 * r + q], cconj(sX[8 * c + q]));
+    g[h] = t;
+  }
+  double sg = r0 == 0 ? sig : 0.0;  // one lane per column
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) sg += __shfl_xor_sync(FULL, sg, o);
+  ss = scalbn(sg, ex);
 }
 
 // ---------------------------------------------------------- environment --
@@ -310,11 +438,11 @@ __global__ void __launch_bounds__(BLK_THREADS) blk_env_kernel(const BlkEnvParams
           e2[h] = make_double2((1.0 - P.beta) * e2[h].x + P.beta * go.x, (1.0 - P.beta) * e2[h].y - P.beta * go.y);
         }
       }
-      const bool ok = polar8(e2, g2, ss, scratch);
+      if (!polar8(e2, g2, ss, scratch)) polar8_jacobi(e2, g2, ss, scratch);
       __syncwarp();
+      // row-major G: lane holds entries lane (row lane>>3) and lane + 32 (row 4 + lane>>3)
       gw[lane] = g2[0];
       gw[lane + 32] = g2[1];
-      if (!ok && lane == 0 && P.err) atomicOr(P.err, 8u);
     }
   }
   if (lane == 0 && P.sig) P.sig[(long long)s * P.K + P.i] = ss;

@@ -150,3 +150,26 @@ def test_block_kinds_fixed_three_qubit_block_and_errors(qfs):
         qfs.BlockContext(n, [[0, 1, 5]], [3])
     with pytest.raises(qfs.QfsError):
         qfs.BlockContext(n, [[0, 1, 2]], [4])
+
+
+def test_block_rank_deficient_environment_jacobi_fallback(qfs):
+    """M = 2 states at n = 3: every 8x8 environment has rank <= 2, Newton-Schulz
+    cannot converge and the Jacobi fallback runs.  Gates are then not unique
+    (reading R5): compare costs, and check the gates stay unitary."""
+    n = 3
+    q = np.array([[0, 1, 2], [2, 0, 1]], np.int32)
+    ar = [3, 3]
+    rng = np.random.default_rng(8)
+    tgt = I.pack_gates([I.haar_unitary(rng, 8) for _ in ar])
+    x = I.haar_states(rng, n, 2)
+    y = I.apply_blocks_tensor(n, q, ar, tgt, x)
+    g0 = I.pack_gates([I.haar_unitary(rng, 8) for _ in ar])[None]
+    ctx = qfs.BlockContext(n, q, ar)
+    ctx.set_samples(x, y)
+    gpu = ctx.trace_sweeps(g0, 2, 1)
+    orc = O.trace_sweeps_blocks(n, q, ar, g0, x, y, 2, 1)
+    assert abs(gpu["cost"][0, 0] - orc["cost"][0, 0]) <= 1e-10 * orc["cost"][0, 0] + 1e-14
+    assert np.abs(gpu["sigma"] - orc["sigma"]).max() <= 1e-10 * np.abs(orc["sigma"]).max()
+    for gm in I.unpack_gates(gpu["gates"][0, 0], ar):
+        assert np.abs(gm.conj().T @ gm - np.eye(8)).max() < 1e-12
+    ctx.close()
