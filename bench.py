@@ -189,10 +189,12 @@ def main():
         cores = host_cores()
         prob = I.make_problem(args.config, init="R", s=max(cores, 1))
         starts = min(cores, s_per)
-        cpu_oracle_run(prob, cfgd["m_init"], starts, cores, steps=1)  # warm (one step)
+        warm = max(1, args.warmup)
+        cpu_oracle_run(prob, cfgd["m_init"], starts, cores, steps=warm)  # untimed warm-up steps
         v, dt = cpu_oracle_run(prob, cfgd["m_init"], starts, cores, steps=args.steps)
-        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0,
-                "steps": args.steps, "warmup": 1, "ms_per_step": dt / args.steps * 1e3,
+        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+                "device": "cpu (host cores; the oracle uses no GPU)",
+                "steps": args.steps, "warmup": warm, "ms_per_step": dt / args.steps * 1e3,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": config,
                 "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
