@@ -45,8 +45,7 @@ struct GateDesc {
 struct BwdParams {
   int n, nb, K, S;            // qubits, CTAs per start, gates, total starts (trace layout)
   const Slot *slots;
-  GateDesc g;                 // per-gate kernel: this gate
-  const GateDesc *desc;       // persistent kernel: [K] (device)
+  GateDesc g;                 // this launch's gate
   const double2 *gates;       // [S][K][16]
   double2 *gates_w;           // same array (written by the polar step)
   const int *kinds;           // [K] gate kinds (0 two-qubit variable, 1 fixed, 2 one-qubit), or nullptr
@@ -61,14 +60,6 @@ struct BwdParams {
   double *sig;                // [S][K] sum sigma, or nullptr
   double2 *env_trace;         // [K][S][16] for this sweep, or nullptr
   unsigned long long *dbg;    // diagnostics: [K][4] globaltimer stamps, or nullptr
-  // persistent kernel only
-  unsigned *flags;            // [S_act] gates completed this sweep (release/acquire)
-  int stagger;                // slots j >= n_slots/2 start after slot j - n_slots/2 finished a gate
-  View chi_final, x_final;    // sweep-end cost: chi' = G_0^dag chi vs x
-  int fp0, fp1;               // pair of gate 0
-  double *partials2;          // [S_act][nb]
-  unsigned *counters2;        // [S_act]
-  double *out_sum;            // [S_act] sum ||chi' - x||^2
 };
 
 // Polar update of E (already reduced / all-reduced) for each active start.
@@ -167,9 +158,7 @@ struct ApplyParams {
 
 // ---- launchers (qfs_kernels.cu); all return cudaGetLastError() ----
 cudaError_t launch_bwd(const BwdParams &p, int n_slots, cudaStream_t st);
-cudaError_t launch_bwd_persistent(const BwdParams &p, int n_slots, cudaStream_t st);
 int fwd2_min_blocks();             // CTAs per SM the two-gate forward kernel is compiled for
-int bwd_persistent_ctas_per_sm();  // co-resident CTAs per SM of the persistent kernel
 cudaError_t launch_polar(const PolarParams &p, int n_slots, cudaStream_t st);
 cudaError_t launch_final(const FinalParams &p, int n_slots, cudaStream_t st);
 cudaError_t launch_fwd_gate(const FwdGateParams &p, int n_slots, cudaStream_t st);

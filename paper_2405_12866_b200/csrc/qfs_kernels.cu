@@ -111,21 +111,6 @@ __device__ __forceinline__ int pidx(int v) {
   return ((v >> TP0) & 1) | (((v >> TP1) & 1) << 1);
 }
 
-__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-// all threads of the CTA wait until *flag >= target (thread 0 polls)
-__device__ void cta_wait_flag(const unsigned *flag, unsigned target) {
-  if (threadIdx.x == 0)
-    while (ld_acquire(flag) < target) __nanosleep(32);
-  __syncthreads();
-}
-
 struct BwdShared {
   double2 sQ[16];                          // G_{i+1}^dag
   double2 red[BWD_THREADS / 32][4][16];    // per-warp (per lane-group) E partials
@@ -151,9 +136,7 @@ struct BwdShared {
 // groups, warps), so the partial is deterministic for a given launch shape.
 template <int NU, int TP0, int TP1, bool UPD>
 __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslot, int s,
-                                 unsigned Ms, bool fence_chi, BwdShared &sh,
-                                 double2 *stage_buf, const unsigned *wflag = nullptr,
-                                 unsigned wtarget = 0) {
+                                 unsigned Ms, BwdShared &sh, double2 *stage_buf) {
   constexpr int T = 1 << (NU - 2);
   constexpr int LPT = 32 / T;
   constexpr int NWARP = BWD_THREADS / 32;
@@ -266,10 +249,8 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
     for (int k = 0; k < BWD_STAGES - 1; ++k) issue_part(k, false, true);
     cp_async_commit();
   }
-  // dependence on the previous gate: kernel boundary (PDL) or, in the
-  // persistent kernel, the start's release flag
-  if (wflag) cta_wait_flag(wflag, wtarget);
-  else pdl_wait();
+  // dependence on the previous gate: kernel boundary (PDL)
+  pdl_wait();
   if (UPD && threadIdx.x < 16) {
     const int a = threadIdx.x >> 2, b = threadIdx.x & 3;
     const double2 g = __ldcg(P.gates + ((long long)s * P.K + G.upd_gate) * 16 + 4 * b + a);
@@ -384,7 +365,6 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
     }
   }
   cp_async_wait<0>();
-  if (UPD && fence_chi) __threadfence();  // chi visible to the other CTAs before the ticket
   pdl_trigger();  // all of this CTA's reads of chi/phi are done
 
   // CTA reduction: over the sample lanes of each lane-group, then lane groups
@@ -485,7 +465,7 @@ __global__ void __launch_bounds__(BWD_THREADS, QFS_BWD_MINB) bwd_kernel(const Bw
   if constexpr (WIDE) {
     constexpr int NWARP = BWD_THREADS / 32, FL = 24;
     __shared__ unsigned last_cta;
-    const bool w0 = bwd_gate_partial<NU, TP0, TP1, UPD>(P, P.g, jslot, sl.s, (unsigned)sl.m, false, sh, stage_buf);
+    const bool w0 = bwd_gate_partial<NU, TP0, TP1, UPD>(P, P.g, jslot, sl.s, (unsigned)sl.m, sh, stage_buf);
     if (w0) {
       const bool last = warp0_elect_last(&P.counters[jslot], (unsigned)P.nb);
       if (threadIdx.x == 0) last_cta = last ? 1u : 0u;
@@ -516,7 +496,7 @@ __global__ void __launch_bounds__(BWD_THREADS, QFS_BWD_MINB) bwd_kernel(const Bw
     bwd_finish_e(P, P.g, jslot, sl.s, sh, e, kind);
     return;
   }
-  if (!bwd_gate_partial<NU, TP0, TP1, UPD>(P, P.g, jslot, sl.s, (unsigned)sl.m, false, sh, stage_buf))
+  if (!bwd_gate_partial<NU, TP0, TP1, UPD>(P, P.g, jslot, sl.s, (unsigned)sl.m, sh, stage_buf))
     return;
   const int kind = P.kinds ? __ldg(P.kinds + P.g.env_gate) : 0;
   const int ng = (P.nb + RED_GS - 1) / RED_GS;
@@ -554,113 +534,6 @@ __global__ void __launch_bounds__(BWD_THREADS, QFS_BWD_MINB) bwd_kernel(const Bw
   bwd_finish_e(P, P.g, jslot, sl.s, sh, e, kind);
 }
 
-template <int NU, int TP0, int TP1, bool UPD>
-__device__ __forceinline__ bool gate_dispatch_one(const BwdParams &P, const GateDesc &G, int j, int s,
-                                                  unsigned Ms, BwdShared &sh, double2 *buf,
-                                                  const unsigned *wflag, unsigned wtarget) {
-  return bwd_gate_partial<NU, TP0, TP1, UPD>(P, G, j, s, Ms, true, sh, buf, wflag, wtarget);
-}
-
-// Whole backward pass of a sweep plus the sweep-end cost in ONE cooperative
-// launch: CTAs (grid nb x slots, all co-resident) loop over the gates; per
-// start, the last CTA of a gate runs the polar update and releases a flag the
-// start's CTAs acquire before the next gate (they need G_{i+1} and the chi the
-// other CTAs wrote).  Starts progress independently; no kernel boundaries.
-__global__ void __launch_bounds__(BWD_THREADS, QFS_BWD_MINB) bwd_persistent_kernel(const BwdParams P) {
-  __shared__ BwdShared sh;
-  extern __shared__ __align__(128) double2 stage_buf[];
-  const int j = blockIdx.y;
-  const Slot sl = P.slots[j];
-  const unsigned Ms = (unsigned)sl.m;
-  // stagger: the second half of the starts lags the first by one gate, so one
-  // half's polar tail overlaps the other half's contraction on the same SMs
-  const int half = (int)gridDim.y / 2;
-  if (P.stagger && half > 0 && j >= half && P.K > 1) cta_wait_flag(P.flags + (j - half), 1u);
-  for (int i = P.K - 1; i >= 0; --i) {
-    // wait for gate i+1's polar inside the gate step, after the phi prefetch
-    const unsigned *wf = i < P.K - 1 ? P.flags + j : nullptr;
-    const unsigned wt = (unsigned)(P.K - 1 - i);
-    const GateDesc &G = P.desc[i];
-    bool w0;
-    if (!G.upd) {
-      w0 = gate_dispatch_one<2, 0, 1, false>(P, G, j, sl.s, Ms, sh, stage_buf, wf, wt);
-    } else if (G.nu == 2) {
-      w0 = G.tp0 == 0 ? gate_dispatch_one<2, 0, 1, true>(P, G, j, sl.s, Ms, sh, stage_buf, wf, wt)
-                      : gate_dispatch_one<2, 1, 0, true>(P, G, j, sl.s, Ms, sh, stage_buf, wf, wt);
-    } else if (G.nu == 3) {
-      if (G.tp0 == 0 && G.tp1 == 2) w0 = gate_dispatch_one<3, 0, 2, true>(P, G, j, sl.s, Ms, sh, stage_buf, wf, wt);
-      else if (G.tp0 == 2 && G.tp1 == 0) w0 = gate_dispatch_one<3, 2, 0, true>(P, G, j, sl.s, Ms, sh, stage_buf, wf, wt);
-      else if (G.tp0 == 1 && G.tp1 == 2) w0 = gate_dispatch_one<3, 1, 2, true>(P, G, j, sl.s, Ms, sh, stage_buf, wf, wt);
-      else w0 = gate_dispatch_one<3, 2, 1, true>(P, G, j, sl.s, Ms, sh, stage_buf, wf, wt);
-    } else {
-      w0 = G.tp0 == 2 ? gate_dispatch_one<4, 2, 3, true>(P, G, j, sl.s, Ms, sh, stage_buf, wf, wt)
-                      : gate_dispatch_one<4, 3, 2, true>(P, G, j, sl.s, Ms, sh, stage_buf, wf, wt);
-    }
-    if (w0 && warp0_elect_last(&P.counters[j], (unsigned)P.nb)) {
-      bwd_finish(P, G, j, sl.s, sh, P.kinds ? P.kinds[i] : 0);
-      __threadfence();
-      if (threadIdx.x == 0) st_release(P.flags + j, (unsigned)(P.K - i));
-    }
-  }
-  // sweep-end cost: chi' = G_0^dag chi, sum ||chi' - x||^2 over this
-  // CTA's units of pair 0 (one sample per lane), ordered reduction
-  cta_wait_flag(P.flags + j, (unsigned)P.K);
-  {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    constexpr int NWARP = BWD_THREADS / 32;
-    if (threadIdx.x < 16) {
-      const int a = threadIdx.x >> 2, b = threadIdx.x & 3;
-      sh.sQ[threadIdx.x] = cconj(__ldcg(P.gates + (long long)sl.s * P.K * 16 + 4 * b + a));
-    }
-    __syncthreads();
-    const unsigned nmb = (Ms + 31) / 32;
-    const unsigned units = (1u << (P.n - 2)) * nmb;
-    const unsigned chunk = (units + P.nb - 1) / P.nb;
-    const unsigned beg = blockIdx.x * chunk, end = min(units, beg + chunk);
-    const FastDiv fdu(nmb);
-    const int lo = min(P.fp0, P.fp1), hi = max(P.fp0, P.fp1);
-    const unsigned o[4] = {0u, 1u << P.fp0, 1u << P.fp1, (1u << P.fp0) | (1u << P.fp1)};
-    const double2 *cb = P.chi_final.base + (long long)sl.s * P.chi_final.ss;
-    const unsigned csa = (unsigned)P.chi_final.sa, xsa = (unsigned)P.x_final.sa;
-    double accd = 0.0;
-    for (unsigned u = beg + warp; u < end; u += NWARP) {
-      const unsigned q = fdu.div(u);
-      const unsigned m = (u - q * nmb) * 32 + lane;
-      if (m >= Ms) continue;
-      const unsigned base = insert_zero32(insert_zero32(q, lo), hi);
-      double2 v[4], xv[4];
-#pragma unroll
-      for (int l = 0; l < 4; ++l) v[l] = __ldcg(cb + (base + o[l]) * csa + m);
-#pragma unroll
-      for (int l = 0; l < 4; ++l) xv[l] = __ldcs(P.x_final.base + (base + o[l]) * xsa + m);
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        double2 r = make_double2(0.0, 0.0);
-#pragma unroll
-        for (int b = 0; b < 4; ++b) cfma(r, sh.sQ[4 * a + b], v[b]);
-        const double dr = r.x - xv[a].x, di = r.y - xv[a].y;
-        accd = fma(dr, dr, accd);
-        accd = fma(di, di, accd);
-      }
-    }
-#pragma unroll
-    for (int q = 16; q >= 1; q >>= 1) accd += __shfl_xor_sync(FULL, accd, q);
-    if (lane == 0) sh.sum32[warp] = accd;
-    __syncthreads();
-    if (threadIdx.x >= 32) return;
-    if (threadIdx.x == 0) {
-      double tsum = 0.0;
-      for (int q = 0; q < NWARP; ++q) tsum += sh.sum32[q];
-      P.partials2[(long long)j * P.nb + blockIdx.x] = tsum;
-    }
-    if (!warp0_elect_last(&P.counters2[j], (unsigned)P.nb)) return;
-    if (threadIdx.x == 0) {
-      double tsum = 0.0;
-      for (int b = 0; b < P.nb; ++b) tsum += __ldcg(P.partials2 + (long long)j * P.nb + b);
-      P.out_sum[j] = tsum;
-    }
-  }
-}
 
 // polar step alone (sample-sharded mode, after the NCCL all-reduce of E): one warp per start
 __global__ void polar_kernel(const PolarParams P) {
@@ -1268,36 +1141,6 @@ cudaError_t launch_bwd(const BwdParams &p, int n_slots, cudaStream_t st) {
 }
 
 int fwd2_min_blocks() { return QFS_FWD2_MINB; }
-
-int bwd_persistent_ctas_per_sm() {
-  static int cached = -1;
-  if (cached < 0) {
-    const int smem = BWD_STAGES * 8 * BWD_THREADS * (int)sizeof(double2);
-    cudaFuncSetAttribute(bwd_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, bwd_persistent_kernel, BWD_THREADS, smem) !=
-        cudaSuccess)
-      nb = 1;
-    cached = nb < 1 ? 1 : nb;
-  }
-  return cached;
-}
-
-cudaError_t launch_bwd_persistent(const BwdParams &p, int n_slots, cudaStream_t st) {
-  const int smem = BWD_STAGES * 8 * BWD_THREADS * (int)sizeof(double2);
-  bwd_persistent_ctas_per_sm();  // sets the shared-memory attribute
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.nb, n_slots);
-  cfg.blockDim = dim3(BWD_THREADS);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (they wait on each other)
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, bwd_persistent_kernel, p);
-}
 
 cudaError_t launch_polar(const PolarParams &p, int n_slots, cudaStream_t st) {
   launch_ex(polar_kernel, dim3((n_slots + 3) / 4), dim3(128), 0, st, p);

@@ -62,12 +62,6 @@ struct qfs_ctx {
   int *d_kinds = nullptr;
   cudaStream_t st = nullptr;
   cudaStream_t cur_st = nullptr;       // stream of the launches being issued
-  // lockstep start groups on parallel streams (one group's polar tail overlaps
-  // another group's contraction); QFS_GROUPS overrides the default
-  static constexpr int GMAX = 8;
-  int groups = 1;
-  cudaStream_t gst[GMAX] = {nullptr};
-  cudaEvent_t ev_fork = nullptr, ev_join[GMAX] = {nullptr};
   // distribution
   ncclComm_t comm = nullptr;
   bool owns_comm = false;
@@ -92,16 +86,8 @@ struct qfs_ctx {
   double2 *d_env_trace = nullptr;
   size_t env_trace_cap = 0;
   double2 *d_stage = nullptr;  // row-major staging of the pools for the transpose
-  // persistent backward kernel: gate descriptors, per-start release flags,
-  // sweep-end cost reduction scratch
-  GateDesc *d_desc = nullptr;
-  std::vector<GateDesc> h_desc;
-  unsigned *d_flags = nullptr, *d_counters2 = nullptr;
-  double *d_partials2 = nullptr;
   int fwd_cache_mode = 0;   // QFS_FWD_CACHE: L2 hints of the forward kernel (diagnostic)
-  int stagger = 1;          // QFS_STAGGER: persistent kernel half-start offset
   bool fwd_pairs = true;    // QFS_FWD_PAIRS=0: one forward pass per gate
-  bool persistent = false;  // QFS_PERSISTENT=1 selects the cooperative whole-backward kernel
   bool val_block = true;    // QFS_VAL_BLOCK=0: one-row-per-CTA validation kernel
   int res_per_sm = 1;       // QFS_RES_PER_SM: resident CTAs per SM the cluster plan targets
   int res_cmax = 16;        // QFS_RES_CMAX: largest cluster the plan widens to
@@ -330,7 +316,6 @@ qfs_status ensure_state(qfs_ctx *c, int S, int M, int V) {
   dfree(c->d_chi); dfree(c->d_B); dfree(c->d_vb0); dfree(c->d_vb1); dfree(c->d_bpart);
   dfree(c->d_partials); dfree(c->d_ered); dfree(c->d_sig); dfree(c->d_csum); dfree(c->d_rowout);
   dfree(c->d_cval); dfree(c->d_counters); dfree(c->d_slots);
-  dfree(c->d_flags); dfree(c->d_counters2); dfree(c->d_partials2);
   dfree(c->d_counters1); dfree(c->d_gpart);
   if (c->h_csum) cudaFreeHost(c->h_csum);
   if (c->h_cval) cudaFreeHost(c->h_cval);
@@ -366,10 +351,6 @@ qfs_status ensure_state(qfs_ctx *c, int S, int M, int V) {
   CUDA_TRY(c, cudaMalloc(&c->d_counters1, (size_t)S * 40 * sizeof(unsigned)));
   CUDA_TRY(c, cudaMemset(c->d_counters1, 0, (size_t)S * 40 * sizeof(unsigned)));
   CUDA_TRY(c, cudaMalloc(&c->d_gpart, (size_t)S * 40 * 32 * sizeof(double)));
-  CUDA_TRY(c, cudaMalloc(&c->d_flags, (size_t)S * sizeof(unsigned)));
-  CUDA_TRY(c, cudaMalloc(&c->d_counters2, (size_t)S * sizeof(unsigned)));
-  CUDA_TRY(c, cudaMemset(c->d_counters2, 0, (size_t)S * sizeof(unsigned)));
-  CUDA_TRY(c, cudaMalloc(&c->d_partials2, (size_t)S * nbc * sizeof(double)));
   CUDA_TRY(c, cudaMallocHost(&c->h_csum, (size_t)S * sizeof(double)));
   CUDA_TRY(c, cudaMallocHost(&c->h_cval, (size_t)S * sizeof(double)));
   c->S_cap = S; c->M_cap = M; c->V_cap = V; c->nb_cap = nbc;
@@ -433,21 +414,6 @@ GateDesc make_desc(const qfs_ctx *c, int i) {
   return d;
 }
 
-// Upload the gate descriptors of the persistent kernel when the buffer layout
-// changed (never during stream capture).
-qfs_status prepare_desc(qfs_ctx *c) {
-  std::vector<GateDesc> h(c->K);
-  for (int i = 0; i < c->K; ++i) h[i] = make_desc(c, i);
-  if (c->d_desc && h.size() == c->h_desc.size() &&
-      std::memcmp(h.data(), c->h_desc.data(), h.size() * sizeof(GateDesc)) == 0)
-    return QFS_OK;
-  if (!c->d_desc) CUDA_TRY(c, cudaMalloc(&c->d_desc, (size_t)c->K * sizeof(GateDesc)));
-  CUDA_TRY(c, cudaMemcpy(c->d_desc, h.data(), h.size() * sizeof(GateDesc), cudaMemcpyHostToDevice));
-  c->h_desc.swap(h);
-  return QFS_OK;
-}
-
-bool use_persistent(const qfs_ctx *c) { return c->persistent && !c->blocks && !(c->mode == 1 && c->world > 1); }
 
 // Plan of the cluster-resident sweep (qfs_resident.cu) for ns starts of up to
 // M_max rows: the smallest power-of-two cluster whose CTAs hold their slice of
@@ -684,22 +650,6 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
     bwd_bytes += units * (i < K - 1 ? 48.0 : 32.0);
     bwd_flops += units * (i < K - 1 ? 64.0 : 32.0);
   }
-  if (use_persistent(c)) {
-    // whole backward pass + sweep-end cost: one cooperative launch
-    PhaseScope phase_bwd(c, K_BWD);
-    b.desc = c->d_desc;
-    b.nb = std::max(1, std::min(148 * bwd_persistent_ctas_per_sm() / ns, kMaxBlocksPerStart));
-    b.flags = c->d_flags + j0;
-    b.stagger = c->stagger;
-    b.chi_final = K == 1 ? ypool : View{c->d_chi, sS, Mc, 1};
-    b.x_final = xpool; b.fp0 = c->pairs[0]; b.fp1 = c->pairs[1];
-    b.partials2 = c->d_partials2 + (long long)j0 * c->nb_cap;
-    b.counters2 = c->d_counters2 + j0;
-    b.out_sum = csum;
-    CUDA_TRY(c, cudaMemsetAsync(c->d_flags + j0, 0, ns * sizeof(unsigned), st));
-    LaunchScope ls(c, K_BWD, bwd_bytes + units * 32.0, bwd_flops + units * 35.0);
-    CUDA_TRY(c, launch_bwd_persistent(b, ns, st));
-  } else {
   {
   PhaseScope phase_bwd(c, K_BWD);
   for (int i = K - 1; i >= 0; --i) {
@@ -741,7 +691,6 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
     fp.nb = blocks_per_start(((long long)M_max * N) >> 2, ns);
     LaunchScope ls(c, K_FINAL, units * 32.0, units * 35.0);
     CUDA_TRY(c, launch_final(fp, ns, st));
-  }
   }
   if (c->mode == 1 && c->world > 1) {
     LaunchScope ls(c, K_NCCL, 0, 0);
@@ -792,24 +741,9 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
   return QFS_OK;
 }
 
-// Issue one sweep: the active slots are split into lockstep groups, each on
-// its own stream (parallel graph branches), joined back into c->st.
+// Issue one sweep on the context stream (all active starts in lockstep).
 qfs_status issue_sweep(qfs_ctx *c, const SweepSpec &sp) {
-  const int ns = (int)sp.slots.size();
-  int G = std::min(c->groups, ns);
-  if (c->mode == 1 && c->world > 1) G = 1;  // NCCL calls stay on one stream, one order
-  if (G <= 1) return issue_group(c, sp, 0, ns, c->st);
-  CUDA_TRY(c, cudaEventRecord(c->ev_fork, c->st));
-  for (int g = 0; g < G; ++g) {
-    const int j0 = (int)((long long)ns * g / G), j1 = (int)((long long)ns * (g + 1) / G);
-    CUDA_TRY(c, cudaStreamWaitEvent(c->gst[g], c->ev_fork, 0));
-    qfs_status r = issue_group(c, sp, j0, j1, c->gst[g]);
-    if (r != QFS_OK) return r;
-    CUDA_TRY(c, cudaEventRecord(c->ev_join[g], c->gst[g]));
-  }
-  for (int g = 0; g < G; ++g) CUDA_TRY(c, cudaStreamWaitEvent(c->st, c->ev_join[g], 0));
-  c->cur_st = c->st;
-  return QFS_OK;
+  return issue_group(c, sp, 0, (int)sp.slots.size(), c->st);
 }
 
 // Run one sweep: upload the slot table, issue (graph-captured when not
@@ -817,10 +751,6 @@ qfs_status issue_sweep(qfs_ctx *c, const SweepSpec &sp) {
 qfs_status run_sweep(qfs_ctx *c, const SweepSpec &sp, std::vector<double> &csum,
                      std::vector<double> &cval) {
   const int ns = (int)sp.slots.size();
-  if (use_persistent(c)) {
-    qfs_status r = prepare_desc(c);
-    if (r != QFS_OK) return r;
-  }
   // slot table through a mapped pinned buffer and a copy kernel (see upload_gates)
   if ((size_t)ns > c->h_slots_cap) {
     if (c->h_slots) cudaFreeHost(c->h_slots);
@@ -845,7 +775,7 @@ qfs_status run_sweep(qfs_ctx *c, const SweepSpec &sp, std::vector<double> &csum,
   const bool use_graph = sp.env_trace == nullptr;
   if (use_graph) {
     long long key[8] = {ns, sp.M_max, sp.want_val, (long long)(sp.beta * 1e15), sp.S, c->S_cap,
-                        c->M_cap, (c->prof ? 2 : 1) + 4 * c->groups};
+                        c->M_cap, (c->prof ? 2 : 1)};
     if (!c->gexec || std::memcmp(key, c->gkey, sizeof key) != 0) {
       drop_graph(c);
       cudaGraph_t g;
@@ -979,16 +909,8 @@ qfs_status create_common(int n, int k, const int32_t *pairs, int device, qfs_ctx
   if (e == cudaSuccess) e = cudaMalloc(&c->d_kinds, k * sizeof(int));
   if (e == cudaSuccess) e = cudaMemset(c->d_kinds, 0, k * sizeof(int));
   if (e == cudaSuccess) e = cudaMalloc(&c->d_flag, 4 * sizeof(int));
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
-  for (int g = 0; g < qfs_ctx::GMAX && e == cudaSuccess; ++g) {
-    e = cudaStreamCreateWithFlags(&c->gst[g], cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join[g], cudaEventDisableTiming);
-  }
   c->cur_st = c->st;
-  if (const char *gs = getenv("QFS_GROUPS")) c->groups = std::max(1, std::min(qfs_ctx::GMAX, atoi(gs)));
-  if (const char *ps = getenv("QFS_PERSISTENT")) c->persistent = atoi(ps) != 0;
   if (const char *fc = getenv("QFS_FWD_CACHE")) c->fwd_cache_mode = atoi(fc);
-  if (const char *sg = getenv("QFS_STAGGER")) c->stagger = atoi(sg);
   if (const char *fp = getenv("QFS_FWD_PAIRS")) c->fwd_pairs = atoi(fp) != 0;
   if (const char *pd = getenv("QFS_PDL")) set_pdl(atoi(pd) != 0);
   if (const char *pa = getenv("QFS_PATH")) c->path = std::max(0, std::min(2, atoi(pa)));
@@ -1619,7 +1541,7 @@ void qfs_destroy(qfs_ctx *c) {
   dfree(c->d_gates); dfree(c->d_chi); dfree(c->d_B); dfree(c->d_vb0); dfree(c->d_vb1);
   dfree(c->d_partials); dfree(c->d_ered); dfree(c->d_sig); dfree(c->d_csum); dfree(c->d_rowout);
   dfree(c->d_cval); dfree(c->d_counters); dfree(c->d_slots); dfree(c->d_env_trace);
-  dfree(c->d_stage); dfree(c->d_vprev); dfree(c->d_desc);
+  dfree(c->d_stage); dfree(c->d_vprev);
   if (c->h_check) cudaFreeHost(c->h_check);
   dfree(c->d_check);
   if (c->h_gates) cudaFreeHost(c->h_gates);
@@ -1632,14 +1554,9 @@ void qfs_destroy(qfs_ctx *c) {
     dfree(g.x); dfree(g.y); dfree(g.xv); dfree(g.yv);
     if (g.ev) cudaEventDestroy(g.ev);
   }
-  dfree(c->d_flags); dfree(c->d_counters2); dfree(c->d_partials2); dfree(c->d_counters1); dfree(c->d_gpart);
+  dfree(c->d_counters1); dfree(c->d_gpart);
   if (c->h_csum) cudaFreeHost(c->h_csum);
   if (c->h_cval) cudaFreeHost(c->h_cval);
-  for (int g = 0; g < qfs_ctx::GMAX; ++g) {
-    if (c->gst[g]) cudaStreamDestroy(c->gst[g]);
-    if (c->ev_join[g]) cudaEventDestroy(c->ev_join[g]);
-  }
-  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->st) cudaStreamDestroy(c->st);
   if (c->owns_comm && c->comm) ncclCommDestroy(c->comm);
   delete c;
