@@ -37,6 +37,9 @@ namespace {
 #define QFS_RES_THREADS 256
 #endif
 constexpr int RES_THREADS = QFS_RES_THREADS;
+#ifndef QFS_RES_SPARE_SMSP
+#define QFS_RES_SPARE_SMSP 1  // resident: the uncompute beside the polar leaves warp 0's scheduler alone
+#endif
 #ifndef QFS_RES_ALIGN
 #define QFS_RES_ALIGN 128  // dynamic shared-memory alignment of the resident / validation kernels
 #endif
@@ -285,7 +288,16 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
         stamp(4);  // [4] polar
       } else {
         // uncompute B_{i-1} = G_{i-1}^dag B_i with the old G_{i-1}, overlapping the polar
+#if QFS_RES_SPARE_SMSP
+        // not warp 4: it shares warp 0's scheduler (warp w -> SMSP w % 4), whose
+        // polar is a latency-bound chain the uncompute's DFMA would slow down
+        if (i > 0 && warp != 4) {
+          const int t = tid - 32 - (warp > 4 ? 32 : 0);
+          res_apply(sm.phi, sm.G + 16 * (i - 1), sm.pr[i - 1], true, cnt, fd, ld, n, t, RES_THREADS - 64);
+        }
+#else
         if (i > 0) res_apply(sm.phi, sm.G + 16 * (i - 1), sm.pr[i - 1], true, cnt, fd, ld, n, tid - 32, RES_THREADS - 32);
+#endif
         cl_wait();
       }
       __syncthreads();
