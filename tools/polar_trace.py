@@ -6,7 +6,8 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2405_12866_b200 import build, inputs as I, qfs
 build.build()
-for cfg, init in (("c4", "R"), ("c3", "R"), ("c3", "W"), ("c2", "R")):
+CASES = [tuple(a.split(":")) for a in sys.argv[1:]] or [("c4", "R"), ("c3", "R"), ("c3", "W"), ("c2", "R")]
+for cfg, init in CASES:
     p = I.make_problem(cfg, init=init)
     ctx = qfs.Context(p.n, p.pairs)
     ctx.set_samples(p.x, p.y, p.xv, p.yv)
