@@ -37,6 +37,9 @@ namespace {
 #define QFS_RES_THREADS 256
 #endif
 constexpr int RES_THREADS = QFS_RES_THREADS;
+#ifndef QFS_RES_PAIRS
+#define QFS_RES_PAIRS 1  // resident forward / validation: two gates per shared-memory pass
+#endif
 #ifndef QFS_RES_SPARE_SMSP
 #define QFS_RES_SPARE_SMSP 1  // resident: the uncompute beside the polar leaves warp 0's scheduler alone
 #endif
@@ -110,6 +113,110 @@ __device__ void res_apply(double2 *psi, const double2 *G, int2 pq, bool dag, int
     psi[b + o1] = o[1];
     psi[b + o2] = o[2];
     psi[b + o1 + o2] = o[3];
+  }
+}
+
+
+// Two consecutive gates in one pass over a [2^n][ld] shared-memory block: each
+// item holds the 2^NU amplitudes spanned by both pairs in registers (gate k on
+// local bits (0, 1), gate k+1 on (TP0, TP1)), so the state is read and written
+// once per two gates with one barrier instead of two.  Gate entries are
+// re-read from shared memory per use.
+template <int NU, int TP0, int TP1>
+__device__ __forceinline__ constexpr int pair_idx(int q, int l) {
+  int v = ((l & 1) << TP0) | (((l >> 1) & 1) << TP1);
+  int bit = 0;
+  for (int t = 0; t < NU; ++t) {
+    if (t == TP0 || t == TP1) continue;
+    v |= ((q >> bit) & 1) << t;
+    ++bit;
+  }
+  return v;
+}
+__device__ __forceinline__ double2 lds_c2(const double2 *p) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return v;
+}
+template <int NU, int TP0, int TP1>
+__device__ void res_apply_pair_t(double2 *psi, const double2 *G1, const double2 *G2, const int (&loc)[4],
+                                 const int (&srt)[4], int cnt, const FastDiv &fd, unsigned ld, int n, int t0, int nt) {
+  constexpr int NV = 1 << NU, NQ = NV / 4;
+  unsigned ob[NU];  // shared-memory offset of local bit t
+#pragma unroll
+  for (int t = 0; t < NU; ++t) ob[t] = (1u << loc[t]) * ld;
+  auto offs = [&](int u) {  // u is a compile-time constant after unrolling
+    unsigned o = 0;
+#pragma unroll
+    for (int t = 0; t < NU; ++t)
+      if ((u >> t) & 1) o += ob[t];
+    return o;
+  };
+  const unsigned items = (1u << (n - NU)) * (unsigned)cnt;
+  for (unsigned q = (unsigned)t0; q < items; q += (unsigned)nt) {
+    const unsigned r = fd.div(q);
+    unsigned g = r;
+#pragma unroll
+    for (int t = 0; t < NU; ++t) g = insert_zero32(g, srt[t]);
+    const unsigned b = g * ld + (q - r * (unsigned)cnt);
+    double2 v[NV];
+#pragma unroll
+    for (int u = 0; u < NV; ++u) v[u] = psi[b + offs(u)];
+#pragma unroll
+    for (int qq = 0; qq < NQ; ++qq) {
+      double2 o[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        o[a] = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) cfma(o[a], lds_c2(G1 + 4 * a + c), v[4 * qq + c]);
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) v[4 * qq + a] = o[a];
+    }
+#pragma unroll
+    for (int qq = 0; qq < NQ; ++qq) {
+      double2 o[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        o[a] = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) cfma(o[a], lds_c2(G2 + 4 * a + c), v[pair_idx<NU, TP0, TP1>(qq, c)]);
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) v[pair_idx<NU, TP0, TP1>(qq, a)] = o[a];
+    }
+#pragma unroll
+    for (int u = 0; u < NV; ++u) psi[b + offs(u)] = v[u];
+  }
+}
+__device__ void res_apply_pair(double2 *psi, const double2 *G1, int2 p1, const double2 *G2, int2 p2, int cnt,
+                               const FastDiv &fd, unsigned ld, int n, int t0, int nt) {
+  // union of the pairs in local order (gate k's pair first, then gate k+1's new
+  // qubits ascending) and gate k+1's local positions; fixed-index code only
+  const bool x_new = p2.x != p1.x && p2.x != p1.y, y_new = p2.y != p1.x && p2.y != p1.y;
+  int l2 = 0, l3 = 0, nu = 2;
+  if (x_new && y_new) { l2 = min(p2.x, p2.y); l3 = max(p2.x, p2.y); nu = 4; }
+  else if (x_new) { l2 = p2.x; nu = 3; }
+  else if (y_new) { l2 = p2.y; nu = 3; }
+  auto pos = [&](int q) { return q == p1.x ? 0 : q == p1.y ? 1 : q == l2 ? 2 : 3; };
+  const int tp0 = pos(p2.x), tp1 = pos(p2.y);
+  const int loc[4] = {p1.x, p1.y, l2, l3};
+  int a0 = p1.x, a1 = p1.y, a2 = nu > 2 ? l2 : 31, a3 = nu > 3 ? l3 : 31;  // ascending union bits
+  auto cs = [](int &u, int &v) { if (v < u) { const int t = u; u = v; v = t; } };
+  cs(a0, a1); cs(a2, a3); cs(a0, a2); cs(a1, a3); cs(a1, a2);
+  const int srt[4] = {a0, a1, a2, a3};
+  if (nu == 2) {
+    if (tp0 == 0) res_apply_pair_t<2, 0, 1>(psi, G1, G2, loc, srt, cnt, fd, ld, n, t0, nt);
+    else res_apply_pair_t<2, 1, 0>(psi, G1, G2, loc, srt, cnt, fd, ld, n, t0, nt);
+  } else if (nu == 3) {
+    if (tp0 == 0 && tp1 == 2) res_apply_pair_t<3, 0, 2>(psi, G1, G2, loc, srt, cnt, fd, ld, n, t0, nt);
+    else if (tp0 == 2 && tp1 == 0) res_apply_pair_t<3, 2, 0>(psi, G1, G2, loc, srt, cnt, fd, ld, n, t0, nt);
+    else if (tp0 == 1 && tp1 == 2) res_apply_pair_t<3, 1, 2>(psi, G1, G2, loc, srt, cnt, fd, ld, n, t0, nt);
+    else res_apply_pair_t<3, 2, 1>(psi, G1, G2, loc, srt, cnt, fd, ld, n, t0, nt);
+  } else {
+    if (tp0 == 2) res_apply_pair_t<4, 2, 3>(psi, G1, G2, loc, srt, cnt, fd, ld, n, t0, nt);
+    else res_apply_pair_t<4, 3, 2>(psi, G1, G2, loc, srt, cnt, fd, ld, n, t0, nt);
   }
 }
 
@@ -242,9 +349,22 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
     __syncthreads();
     stamp(0);  // [0] load
     // forward with the previous sweep's gates: phi = B_{K-1} = G_{K-2} ... G_0 x
-    for (int k = 0; k + 1 < K; ++k) {
-      res_apply(sm.phi, sm.G + 16 * k, sm.pr[k], false, cnt, fd, ld, n, tid, RES_THREADS);
-      __syncthreads();
+    if constexpr (QFS_RES_PAIRS && MINB == 1) {  // (the 128-register variant would spill)
+      int k = 0;
+      for (; k + 2 < K; k += 2) {  // gates k, k+1 (the last gate, K-1, is not applied)
+        res_apply_pair(sm.phi, sm.G + 16 * k, sm.pr[k], sm.G + 16 * (k + 1), sm.pr[k + 1], cnt, fd, ld, n, tid,
+                       RES_THREADS);
+        __syncthreads();
+      }
+      if (k + 1 < K) {
+        res_apply(sm.phi, sm.G + 16 * k, sm.pr[k], false, cnt, fd, ld, n, tid, RES_THREADS);
+        __syncthreads();
+      }
+    } else {
+      for (int k = 0; k + 1 < K; ++k) {
+        res_apply(sm.phi, sm.G + 16 * k, sm.pr[k], false, cnt, fd, ld, n, tid, RES_THREADS);
+        __syncthreads();
+      }
     }
     stamp(1);  // [1] forward
     double train = 0.0;
@@ -349,9 +469,22 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
         }
         __syncthreads();
         const FastDiv fdv((unsigned)nb);
-        for (int k = 0; k < K; ++k) {
-          res_apply(sm.phi, sm.G + 16 * k, sm.pr[k], false, nb, fdv, ld, n, tid, RES_THREADS);
-          __syncthreads();
+        if constexpr (QFS_RES_PAIRS && MINB == 1) {
+          int k = 0;
+          for (; k + 1 < K; k += 2) {
+            res_apply_pair(sm.phi, sm.G + 16 * k, sm.pr[k], sm.G + 16 * (k + 1), sm.pr[k + 1], nb, fdv, ld, n,
+                           tid, RES_THREADS);
+            __syncthreads();
+          }
+          if (k < K) {
+            res_apply(sm.phi, sm.G + 16 * k, sm.pr[k], false, nb, fdv, ld, n, tid, RES_THREADS);
+            __syncthreads();
+          }
+        } else {
+          for (int k = 0; k < K; ++k) {
+            res_apply(sm.phi, sm.G + 16 * k, sm.pr[k], false, nb, fdv, ld, n, tid, RES_THREADS);
+            __syncthreads();
+          }
         }
         for (unsigned q = tid; q < N * (unsigned)nb; q += RES_THREADS) {
           const unsigned jj = q / N, a = q - jj * N;
