@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <map>
 #include <utility>
 
@@ -607,7 +608,7 @@ __device__ __forceinline__ void cl_sync() {
 }
 
 // Validation for rows too large for one CTA (n = 14: 256 KB): a cluster of C =
-// 2^t CTAs holds one row, CTA c the amplitudes whose top t qubits read c.  A
+// 2^t CTAs (t <= 2 unless shared memory needs 3) holds one row, CTA c the amplitudes whose top t qubits read c.  A
 // gate off the top qubits is applied by each CTA to its slice (the block
 // routine with n-t local qubits); a gate touching a top qubit is applied to
 // quadruples split evenly between the CTAs, members read / written locally or
@@ -702,9 +703,15 @@ cudaError_t launch_val_cluster(const ValRowParams &p, int n_slots, cudaStream_t 
   constexpr size_t lim = RES_SMEM_MAX - 256;
   // cluster of 2^t CTAs per row: the smallest that fits, widened (up to 8)
   // while the rows of all starts still fit on the 148 SMs
+  // measured at n = 14 (C5, S = 1 / 2 / 4): 4-CTA clusters beat 8-CTA ones
+  // (fewer gates on distributed qubits) even with half the SMs idle
   int t = 1;
   while (t < 3 && val_cl_smem(p.n, p.K, t) > lim) ++t;
-  while (t < 3 && (long long)p.rows * n_slots * (2 << t) <= 148) ++t;
+  while (t < 2 && (long long)p.rows * n_slots * (2 << t) <= 148) ++t;
+  if (const char *e = getenv("QFS_VAL_CL_T")) {  // diagnostic override (A/B of the cluster width)
+    const int tt = atoi(e);
+    if (tt >= 1 && tt <= 3 && val_cl_smem(p.n, p.K, tt) <= lim) t = tt;
+  }
   const size_t smem = val_cl_smem(p.n, p.K, t);
   if (smem > lim) return cudaErrorInvalidConfiguration;
   static bool attr = false;
