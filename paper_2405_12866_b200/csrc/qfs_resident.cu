@@ -743,11 +743,16 @@ size_t val_blk_smem(int n, int K, int ld) {
 
 cudaError_t launch_val_block(const ValRowParams &p, int n_slots, cudaStream_t st) {
   // rows per CTA: the most that fit in shared memory, reduced while the grid
-  // has fewer CTAs than SMs
+  // has fewer CTAs than half the SMs
   constexpr size_t lim = RES_SMEM_MAX - 256;  // the kernel's static reduction array sits beside it
   int ld = 1;
   while (ld < p.rows && val_blk_smem(p.n, p.K, ld + 1) <= lim) ++ld;
-  while (ld > 1 && (long long)((p.rows + ld - 1) / ld) * n_slots < 148) --ld;
+  // (fewer, fuller CTAs down to half the SMs: C4, 16 x 16 rows, ld = 2 beats 1 by 3 %)
+  while (ld > 1 && (long long)((p.rows + ld - 1) / ld) * n_slots < 74) --ld;
+  if (const char *e = getenv("QFS_VAL_BLK_LD")) {  // diagnostic override (A/B)
+    const int l = atoi(e);
+    if (l >= 1 && l <= p.rows && val_blk_smem(p.n, p.K, l) <= lim) ld = l;
+  }
   const size_t smem = val_blk_smem(p.n, p.K, ld);
   if (smem > lim) return cudaErrorInvalidConfiguration;
   static bool attr = false;
