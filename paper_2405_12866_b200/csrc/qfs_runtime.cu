@@ -772,7 +772,12 @@ qfs_status run_sweep(qfs_ctx *c, const SweepSpec &sp, std::vector<double> &csum,
     for (int i = 0; i < c->K; ++i) { init[4 * i] = ~0ull; init[4 * i + 1] = init[4 * i + 2] = init[4 * i + 3] = 0; }
     CUDA_TRY(c, cudaMemcpy(c->d_dbg, init.data(), init.size() * 8, cudaMemcpyHostToDevice));
   }
-  const bool use_graph = sp.env_trace == nullptr;
+  // CUDA graph for the streamed sweep (hundreds of launches); the resident
+  // sweep is one launch, where a capture per new (slots, M) shape only costs
+  // (C2 cold instantiate 30 -> 8 ms without it)
+  ResPlan pl;
+  const bool resident = !c->blocks && res_plan(c, sp.M_max, ns, pl);
+  const bool use_graph = sp.env_trace == nullptr && !resident && !getenv("QFS_NO_GRAPH");
   if (use_graph) {
     long long key[8] = {ns, sp.M_max, sp.want_val, (long long)(sp.beta * 1e15), sp.S, c->S_cap,
                         c->M_cap, (c->prof ? 2 : 1)};
