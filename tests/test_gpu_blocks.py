@@ -173,3 +173,25 @@ def test_block_rank_deficient_environment_jacobi_fallback(qfs):
     for gm in I.unpack_gates(gpu["gates"][0, 0], ar):
         assert np.abs(gm.conj().T @ gm - np.eye(8)).max() < 1e-12
     ctx.close()
+
+
+def test_block_trace_parity_n12_sampled(qfs):
+    """n = 12 (streamed block path at the bench's sizes per start: M = 32, 16 starts,
+    K = 24 with 16 three-qubit blocks); the oracle recomputes two sampled starts."""
+    n, k, m, s = 12, 24, 32, 16
+    qubits, arity, tgt, x, y, xv, yv, g0 = I.block_problem(n, k, s=s, m_pool=m, v=0, init="R")
+    ctx = qfs.BlockContext(n, qubits, arity)
+    ctx.set_samples(x, y)
+    gpu = ctx.trace_sweeps(g0, m, 2)
+    ctx.close()
+    off = I.gate_offsets(arity)
+    for st in (0, 11):
+        orc = O.trace_sweeps_blocks(n, qubits, arity, g0[st:st + 1], x, y, m, 2)
+        for t in range(2):
+            assert abs(gpu["cost"][t, st] - orc["cost"][t, 0]) <= 1e-10 * orc["cost"][t, 0] + 1e-15
+            for i in range(k):
+                d = 1 << int(arity[i])
+                eg = gpu["env"][t, s * off[i] + st * d * d: s * off[i] + (st + 1) * d * d]
+                eo = orc["env"][t, off[i]:off[i + 1]]
+                assert np.linalg.norm(eg - eo) <= 1e-10 * np.linalg.norm(eo)
+            assert np.linalg.norm(gpu["gates"][t, st] - orc["gates"][t, 0]) <= 2e-10 * np.sqrt(k)
