@@ -97,12 +97,21 @@ __global__ void __launch_bounds__(BLK_THREADS) blk_apply_kernel(const BlkApplyPa
   const FastDiv fd(rows);
   const double2 *src = P.src.base + (long long)s * P.src.ss;
   double2 *dst = P.dst.base + (long long)s * P.dst.ss;
-  for (unsigned w = beg + threadIdx.x; w < end; w += blockDim.x) {
+  auto load = [&](unsigned w, double2 (&v)[D]) {
     const unsigned r = fd.div(w), m = w - r * rows;  // row fastest: coalesced sample-minor access
+    const unsigned base = blk_base<A>(r, L.srt);
+#pragma unroll
+    for (int l = 0; l < D; ++l) v[l] = src[(long long)(base | L.off[l]) * P.src.sa + (long long)m * P.src.sm];
+  };
+  double2 vn[D];  // next item's amplitudes, loaded while this one computes
+  if (beg + threadIdx.x < end) load(beg + threadIdx.x, vn);
+  for (unsigned w = beg + threadIdx.x; w < end; w += blockDim.x) {
+    const unsigned r = fd.div(w), m = w - r * rows;
     const unsigned base = blk_base<A>(r, L.srt);
     double2 v[D];
 #pragma unroll
-    for (int l = 0; l < D; ++l) v[l] = src[(long long)(base | L.off[l]) * P.src.sa + (long long)m * P.src.sm];
+    for (int l = 0; l < D; ++l) v[l] = vn[l];
+    if (w + blockDim.x < end) load(w + blockDim.x, vn);
 #pragma unroll
     for (int a = 0; a < D; ++a) {
       double2 o = make_double2(0.0, 0.0);
@@ -346,15 +355,25 @@ __global__ void __launch_bounds__(BLK_THREADS) blk_env_kernel(const BlkEnvParams
   const FastDiv fd(rows);
   const double2 *ph = P.phi.base + (long long)s * P.phi.ss;
   const double2 *ch = P.chi.base + (long long)s * P.chi.ss;
-  for (unsigned w = beg + threadIdx.x / PARTS; w < end; w += blockDim.x / PARTS) {
+  auto load = [&](unsigned w, double2 (&f)[XR], double2 (&c)[D]) {
     const unsigned r = fd.div(w), m = w - r * rows;
     const unsigned base = blk_base<A>(r, L.srt);
-    double2 f[XR], c[D];
 #pragma unroll
     for (int x = 0; x < XR; ++x)
       f[x] = ph[(long long)(base | L.off[part * XR + x]) * P.phi.sa + (long long)m * P.phi.sm];
 #pragma unroll
     for (int l = 0; l < D; ++l) c[l] = ch[(long long)(base | L.off[l]) * P.chi.sa + (long long)m * P.chi.sm];
+  };
+  const unsigned step = blockDim.x / PARTS;
+  double2 fn[XR], cn[D];  // next item's amplitudes, loaded while this one accumulates
+  if (beg + threadIdx.x / PARTS < end) load(beg + threadIdx.x / PARTS, fn, cn);
+  for (unsigned w = beg + threadIdx.x / PARTS; w < end; w += step) {
+    double2 f[XR], c[D];
+#pragma unroll
+    for (int x = 0; x < XR; ++x) f[x] = fn[x];
+#pragma unroll
+    for (int l = 0; l < D; ++l) c[l] = cn[l];
+    if (w + step < end) load(w + step, fn, cn);
 #pragma unroll
     for (int x = 0; x < XR; ++x)
 #pragma unroll
