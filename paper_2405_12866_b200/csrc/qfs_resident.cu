@@ -26,6 +26,7 @@
 
 #include <cstdlib>
 #include <map>
+#include <mutex>
 #include <utility>
 
 #include "qfs_device.cuh"
@@ -800,8 +801,11 @@ int resident_max_clusters(int C, size_t smem) {
   // cudaOccupancyMaxActiveClusters is slow (it is queried at every graph
   // capture, and captures follow every change of the active-start set): cache
   // per (cluster size, shared memory)
+  // per (cluster size, shared memory); contexts may be driven from several host threads
   static std::map<std::pair<int, size_t>, int> cache;
+  static std::mutex mu;
   const auto key = std::make_pair(C, smem);
+  std::lock_guard<std::mutex> lock(mu);
   const auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   const int r = resident_max_clusters_query(C, smem);

@@ -129,11 +129,21 @@ def partitions_for_rank(n_parts: int, rank: int, world: int) -> List[int]:
 
 
 def resynth_partitions(blocks: Sequence[Block], params: dict, rank: int = 0, world: int = 1,
-                       gather: Callable | None = None, **kw) -> list:
+                       gather: Callable | None = None, workers: int = 1, **kw) -> list:
     """Run delete_gates_pass on this rank's partitions; ``gather`` (e.g. a
     torch.distributed all_gather_object wrapper) merges the per-rank reports
-    into partition order.  Returns [(partition index, DeletionReport)]."""
-    mine = [(p, delete_gates_pass(blocks[p], params, seed=p, **kw)) for p in partitions_for_rank(len(blocks), rank, world)]
+    into partition order.  ``workers`` > 1 runs that many partitions at once
+    from host threads (each with its own contexts and stream; small
+    partitions are latency-bound, so they overlap on one GPU).  Returns
+    [(partition index, DeletionReport)]."""
+    parts = partitions_for_rank(len(blocks), rank, world)
+    if workers > 1:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=workers) as ex:
+            reps = list(ex.map(lambda p: delete_gates_pass(blocks[p], params, seed=p, **kw), parts))
+        mine = list(zip(parts, reps))
+    else:
+        mine = [(p, delete_gates_pass(blocks[p], params, seed=p, **kw)) for p in parts]
     if gather is None or world == 1:
         return mine
     allr = gather(mine)

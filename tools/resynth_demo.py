@@ -29,3 +29,13 @@ for q, (n, layers, extra) in enumerate([(4, 4, 2), (5, 4, 3), (6, 5, 3), (7, 5, 
                           constructed_redundant=extra, deleted=len(rep.deleted), attempts=rep.attempts,
                           seconds=round(dt, 3), instantiate_seconds=round(rep.instantiations_s, 3),
                           c_train=rep.c_train)), flush=True)
+
+# all partitions at once from host threads (resynth_partitions(workers=...)): wall time
+blocks = [R.redundant_block(n, layers, seed=100 + q, extra=extra)
+          for q, (n, layers, extra) in enumerate([(4, 4, 2), (5, 4, 3), (6, 5, 3), (7, 5, 4), (8, 6, 4), (9, 6, 4)])]
+for workers in (1, 6):
+    t0 = time.perf_counter()
+    out = R.resynth_partitions(blocks, prm, workers=workers, starts=4)
+    dt = time.perf_counter() - t0
+    print(json.dumps(dict(workers=workers, partitions=len(blocks), seconds=round(dt, 3),
+                          deleted=[len(r.deleted) for _, r in out])), flush=True)
