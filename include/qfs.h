@@ -100,6 +100,15 @@ qfs_status qfs_create(int n, int k, const int32_t *pairs, int device, qfs_ctx **
 qfs_status qfs_create_blocks(int n, int k, const int32_t *qubits, const int32_t *arity, int device,
                              qfs_ctx **out);
 
+/* Replace the circuit structure of a pair context (same n): k gates on pairs
+ * [k][2].  Samples, device buffers and streams are kept (re-planned only when
+ * k exceeds what they were sized for); gate kinds reset to all QFS_GATE_VAR2;
+ * the cached sweep graph is dropped.  For re-instantiating many structures on
+ * the same samples (the gate-deletion flow) without a context per
+ * structure.  Waits for the context's in-flight work.  Errors: QFS_ERR_ARG
+ * (bad pairs, block context). */
+qfs_status qfs_set_structure(qfs_ctx *c, int k, const int32_t *pairs);
+
 /* Distributed context.  nccl_comm: an ncclComm_t whose rank
  * and size equal (rank, world) (e.g. ProcessGroupNCCL._comm_ptr()), or NULL
  * when world == 1.  shard_mode 0 = multistart (each rank runs its own starts,

@@ -74,6 +74,7 @@ struct qfs_ctx {
   double2 *d_xv = nullptr, *d_yv = nullptr;  // validation, row-major [V][2^n]
   // work buffers
   int G_cap = 0, S_cap = 0, M_cap = 0, V_cap = 0, nb_cap = 0;
+  int K_alloc = 0;  // gates the structure-dependent buffers were sized for (qfs_set_structure)
   double2 *d_vprev = nullptr;  // [S][K][16] right singular vectors of the last polar step (warm start)
   double2 *d_gates = nullptr, *d_chi = nullptr, *d_B = nullptr, *d_vb0 = nullptr, *d_vb1 = nullptr;
   double *d_partials = nullptr, *d_ered = nullptr, *d_sig = nullptr, *d_csum = nullptr,
@@ -904,7 +905,7 @@ qfs_status create_common(int n, int k, const int32_t *pairs, int device, qfs_ctx
     if (a < 0 || b < 0 || a >= n || b >= n || a == b) return QFS_ERR_ARG;
   }
   qfs_ctx *c = new qfs_ctx();
-  c->n = n; c->K = k; c->N = 1LL << n; c->device = device; c->gsz = 16LL * k;
+  c->n = n; c->K = k; c->K_alloc = k; c->N = 1LL << n; c->device = device; c->gsz = 16LL * k;
   c->pairs.assign(pairs, pairs + 2 * k);
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking);
@@ -1506,6 +1507,40 @@ qfs_status qfs_set_gate_kinds(qfs_ctx *c, const int32_t *kinds) {
   CUDA_TRY(c, cudaSetDevice(c->device));
   CUDA_TRY(c, cudaMemcpy(c->d_kinds, k.data(), k.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
   c->kinds.swap(k);
+  return QFS_OK;
+}
+
+qfs_status qfs_set_structure(qfs_ctx *c, int k, const int32_t *pairs) {
+  if (!c) return QFS_ERR_ARG;
+  if (c->blocks) return fail(c, QFS_ERR_ARG, "qfs_set_structure: not available for block circuits");
+  if (k < 1 || !pairs) return fail(c, QFS_ERR_ARG, "bad structure");
+  for (int i = 0; i < k; ++i) {
+    const int a = pairs[2 * i], b = pairs[2 * i + 1];
+    if (a < 0 || b < 0 || a >= c->n || b >= c->n || a == b) return fail(c, QFS_ERR_ARG, "bad qubit pair");
+  }
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaStreamSynchronize(c->st));  // no launch of the old structure is in flight
+  if (k > c->K_alloc) {
+    // structure-dependent buffers are re-planned by the next call (gates, B cache, sigma)
+    dfree(c->d_pairs);
+    dfree(c->d_kinds);
+    CUDA_TRY(c, cudaMalloc(&c->d_pairs, (size_t)k * sizeof(int2)));
+    CUDA_TRY(c, cudaMalloc(&c->d_kinds, (size_t)k * sizeof(int)));
+    if (c->d_dbg) {
+      dfree(c->d_dbg);
+      CUDA_TRY(c, cudaMalloc(&c->d_dbg, (size_t)4 * k * sizeof(unsigned long long)));
+    }
+    c->G_cap = 0;
+    c->S_cap = 0;
+    c->K_alloc = k;
+  }
+  CUDA_TRY(c, cudaMemcpy(c->d_pairs, pairs, (size_t)k * sizeof(int2), cudaMemcpyHostToDevice));
+  CUDA_TRY(c, cudaMemset(c->d_kinds, 0, (size_t)k * sizeof(int)));
+  c->K = k;
+  c->gsz = 16LL * k;
+  c->pairs.assign(pairs, pairs + 2 * k);
+  c->kinds.assign(k, QFS_GATE_VAR2);
+  drop_graph(c);
   return QFS_OK;
 }
 

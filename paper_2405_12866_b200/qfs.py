@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libqfs.so")
 STATUS = {0: "QFS_OK", 1: "QFS_ERR_ARG", 2: "QFS_ERR_CAPACITY", 3: "QFS_ERR_NUMERIC",
           4: "QFS_ERR_DEVICE", 5: "QFS_ERR_STATE"}
 TERM_NAMES = {0: "CONVERGED", 1: "PLATEAU", 2: "MAX_ITER", 3: "POOL_EXHAUSTED", 4: "STOPPED"}
-SYMBOLS = ["qfs_create", "qfs_create_blocks", "qfs_create_dist", "qfs_nccl_unique_id", "qfs_create_nccl", "qfs_set_samples", "qfs_set_samples_async", "qfs_set_samples_device",
+SYMBOLS = ["qfs_create", "qfs_create_blocks", "qfs_set_structure", "qfs_create_dist", "qfs_nccl_unique_id", "qfs_create_nccl", "qfs_set_samples", "qfs_set_samples_async", "qfs_set_samples_device",
            "qfs_instantiate", "qfs_trace_sweeps", "qfs_bench_sweeps", "qfs_op_apply",
            "qfs_op_environment", "qfs_op_polar", "qfs_profile_enable", "qfs_profile_read", "qfs_set_path", "qfs_set_gate_kinds",
            "qfs_launch_count", "qfs_stream", "qfs_last_error", "qfs_destroy"]
@@ -66,6 +66,7 @@ def load(path: str = LIB_PATH):
         lib.qfs_destroy.restype = None
         lib.qfs_create.argtypes = [ip, ip, vp, ip, ctypes.POINTER(vp)]
         lib.qfs_create_blocks.argtypes = [ip, ip, vp, vp, ip, ctypes.POINTER(vp)]
+        lib.qfs_set_structure.argtypes = [vp, ip, vp]
         lib.qfs_create_dist.argtypes = [ip, ip, vp, ip, vp, ip, ip, ip, ctypes.POINTER(vp)]
         lib.qfs_nccl_unique_id.argtypes = [vp]
         lib.qfs_create_nccl.argtypes = [ip, ip, vp, ip, vp, ip, ip, ip, ctypes.POINTER(vp)]
@@ -264,6 +265,13 @@ class Context:
             return
         k = np.ascontiguousarray(np.asarray(kinds, dtype=np.int32))
         self._check(self.lib.qfs_set_gate_kinds(self.h, _ptr(k)))
+
+    def set_structure(self, pairs):
+        """qfs_set_structure: a new circuit structure (same n) on this context."""
+        pr = np.ascontiguousarray(pairs, dtype=np.int32)
+        self._check(self.lib.qfs_set_structure(self.h, int(pr.shape[0]), _ptr(pr)))
+        self.pairs = pr
+        self.k = int(pr.shape[0])
 
     def set_path(self, path):
         """'auto' | 'streamed' | 'resident' (qfs_set_path)."""

@@ -65,9 +65,21 @@ def delete_gates_pass(block: Block, params: dict, starts: int = 4, m_pool: int |
 
     ``context_factory(n, pairs)`` returns a fresh qfs.Context (default: the GPU
     library); ``params`` are qfs_instantiate parameters (m_init, dist_tol, ...)."""
+    shared = None
     if context_factory is None:
+        # one GPU context per partition: each attempt swaps the structure in
+        # (qfs_set_structure) and keeps the samples and device buffers
         from . import qfs
-        context_factory = lambda n, pairs: qfs.Context(n, pairs)  # noqa: E731
+        shared = {}
+
+        def context_factory(n, pairs):
+            if "ctx" not in shared:
+                shared["ctx"] = qfs.Context(n, pairs)
+                shared["fresh"] = True
+            else:
+                shared["ctx"].set_structure(pairs)
+                shared["fresh"] = False
+            return shared["ctx"]
     n = block.n
     N = 1 << n
     m_pool = min(N, m_pool or N)
@@ -102,12 +114,13 @@ def delete_gates_pass(block: Block, params: dict, starts: int = 4, m_pool: int |
         try:
             if hasattr(ctx, "set_gate_kinds"):
                 ctx.set_gate_kinds(kinds)
-            ctx.set_samples(x, y, xv, yv)
+            if shared is None or shared["fresh"]:  # the samples stay on a shared context
+                ctx.set_samples(x, y, xv, yv)
             t0 = time.perf_counter()
             g, res, win = ctx.instantiate(init, params)
             t_inst += time.perf_counter() - t0
         finally:
-            if hasattr(ctx, "close"):
+            if shared is None and hasattr(ctx, "close"):
                 ctx.close()
         if res[win]["term"] == "CONVERGED":
             deleted.append(idx[pos])
@@ -116,6 +129,8 @@ def delete_gates_pass(block: Block, params: dict, starts: int = 4, m_pool: int |
             c_last = res[win]["c_train"]
         else:
             pos += 1
+    if shared and "ctx" in shared:
+        shared["ctx"].close()
     out = Block(n=n, pairs=block.pairs[idx], kinds=block.kinds[idx], gates=cur_gates)
     return DeletionReport(kept=idx, deleted=deleted, attempts=attempts, instantiations_s=t_inst,
                           c_train=c_last, block=out)

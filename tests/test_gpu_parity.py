@@ -473,3 +473,27 @@ def test_set_samples_async_queue(qfs):
     with pytest.raises(QfsError) as ei:
         ctx.trace_sweeps(p.init, 16, 1)
     assert ei.value.status == 3
+
+
+@pytest.mark.gpu
+def test_set_structure_matches_fresh_context():
+    """qfs_set_structure on a used context gives the same traces as a new context
+    (smaller and larger gate counts, gate kinds reset)."""
+    from paper_2405_12866_b200 import build, qfs
+    build.build()
+    p = I.make_problem("c2", init="R", s=3)
+    ctx = qfs.Context(p.n, p.pairs)
+    ctx.set_samples(p.x, p.y, p.xv, p.yv)
+    ctx.trace_sweeps(p.init, p.m_init, 1)
+    rng = np.random.default_rng(3)
+    for k in (7, p.k + 6):
+        pairs = I.brick_pairs(p.n, k)
+        g0 = np.stack([[I.haar_unitary(rng) for _ in range(k)] for _ in range(3)])
+        ctx.set_structure(pairs)
+        a = ctx.trace_sweeps(g0, p.m_init, 2)
+        fresh = qfs.Context(p.n, pairs)
+        fresh.set_samples(p.x, p.y, p.xv, p.yv)
+        b = fresh.trace_sweeps(g0, p.m_init, 2)
+        fresh.close()
+        assert np.array_equal(a["cost"], b["cost"]) and np.array_equal(a["gates"], b["gates"])
+    ctx.close()
