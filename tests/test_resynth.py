@@ -81,3 +81,19 @@ def test_delete_gates_pass_gpu():
     b = R.redundant_block(5, 4, seed=2, extra=3)
     rep = R.delete_gates_pass(b, PRM, starts=4, seed=4)
     _check_report(b, rep, 3)
+
+
+@pytest.mark.gpu
+def test_resynth_partitions_threads_match_sequential_gpu():
+    """Partitions processed from host threads (shared-context reuse per partition,
+    qfs_set_structure) give the same deletions and gates as the sequential pass."""
+    from paper_2405_12866_b200 import build
+    build.build()
+    blocks = [R.redundant_block(4, 3, seed=5, extra=2), R.redundant_block(5, 3, seed=6, extra=2),
+              R.redundant_block(4, 4, seed=7, extra=1)]
+    seq = R.resynth_partitions(blocks, PRM, workers=1, starts=4)
+    par = R.resynth_partitions(blocks, PRM, workers=3, starts=4)
+    for (p1, r1), (p2, r2), b in zip(seq, par, blocks):
+        assert p1 == p2
+        assert r1.deleted == r2.deleted and r1.kept == r2.kept
+        assert np.array_equal(r1.block.gates, r2.block.gates)  # deterministic kernels, same inputs
