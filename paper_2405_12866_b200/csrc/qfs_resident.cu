@@ -39,6 +39,10 @@ namespace {
 #define QFS_RES_THREADS 256
 #endif
 constexpr int RES_THREADS = QFS_RES_THREADS;
+#ifndef QFS_RES_ENV_UNROLL
+#define QFS_RES_ENV_UNROLL 2  // res_env items per unrolled iteration (loads of the next item above the FMAs)
+#endif
+constexpr int RES_ENV_UNROLL = QFS_RES_ENV_UNROLL;
 #ifndef QFS_RES_PAIRS
 #define QFS_RES_PAIRS 1  // resident forward / validation: two gates per shared-memory pass
 #endif
@@ -257,6 +261,7 @@ __device__ void res_env(const double2 *phi, const double2 *chi, int2 pq, int cnt
     const int lo = min(pq.x, pq.y), hi = max(pq.x, pq.y);
     const unsigned o1 = (1u << pq.x) * ld, o2 = (1u << pq.y) * ld;
     const unsigned items = (1u << (n - 2)) * (unsigned)cnt;
+#pragma unroll RES_ENV_UNROLL
     for (unsigned q = threadIdx.x; q < items; q += RES_THREADS) {
       const unsigned r = fd.div(q);
       const unsigned b = insert_zero32(insert_zero32(r, lo), hi) * ld + (q - r * (unsigned)cnt);
