@@ -195,3 +195,17 @@ def test_block_trace_parity_n12_sampled(qfs):
                 eo = orc["env"][t, off[i]:off[i + 1]]
                 assert np.linalg.norm(eg - eo) <= 1e-10 * np.linalg.norm(eo)
             assert np.linalg.norm(gpu["gates"][t, st] - orc["gates"][t, 0]) <= 2e-10 * np.sqrt(k)
+
+
+@pytest.mark.parametrize("n,k,m", [(3, 4, 3), (4, 7, 5), (5, 9, 7), (7, 11, 13)])
+def test_block_trace_parity_ragged(qfs, n, k, m):
+    """Ragged sample counts (not multiples of a warp or tile), small n, unsorted
+    qubit lists; 3 sweeps, costs and environments against the oracle (gates only
+    where the environment is well conditioned, as everywhere)."""
+    qubits, arity, tgt, x, y, xv, yv, g0 = I.block_problem(n, k, s=2, m_pool=m, v=0, init="R", seed=30 + n)
+    ctx = qfs.BlockContext(n, qubits, arity)
+    ctx.set_samples(x, y)
+    gpu = ctx.trace_sweeps(g0, m, 3)
+    ctx.close()
+    orc = O.trace_sweeps_blocks(n, qubits, arity, g0, x, y, m, 3)
+    _compare(n, qubits, arity, g0, x, y, m, 3, gpu, orc)
