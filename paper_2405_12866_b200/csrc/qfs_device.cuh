@@ -126,7 +126,7 @@ __device__ __forceinline__ double2 shfl_xor_c(double2 v, int m) {
 //   Gram-Schmidt on e_0..e_3; R5) and G = V X^dag (eq:opt_u:
 //   E = X D Y^dag, u = Y X^dag with Y = V).  Square roots and divisions are
 //   rsqrt-based (MUFU.RSQ64H + Newton) to keep the serial chain short.
-// E' is scaled by an exact power of two first (the polar factor is scale-free).
+// On the Jacobi path E' is scaled by an exact power of two first (the polar factor is scale-free).
 // scratch: 32 double2 of shared memory per half warp (Newton-Schulz operands;
 // the first 16 also serve the null-column completion).
 //
@@ -205,26 +205,30 @@ __device__ bool hw_polar(double2 e, const double2 *v0p, double2 &g_out, double2 
   const int hb = lane & 16;         // half-warp base lane
   const int l = lane & 15;
   const int r = l >> 2, j = l & 3;
-  // exact power-of-two scaling of E'
-  double mx = fmax(fabs(e.x), fabs(e.y));
-#pragma unroll
-  for (int o = 1; o < 16; o <<= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
-  const int ex = mx > 0.0 ? ilogb(mx) : 0;
-  e.x = scalbn(e.x, -ex);
-  e.y = scalbn(e.y, -ex);
 #ifdef QFS_DIAG_POLAR
   const long long t_ns = clock64();
 #endif
   {
+    // Newton-Schulz on E' as is: it is scale-free (X_0 = E'/(||E'||_F/2)) and
+    // |E'| <= M 2^n cannot overflow the squares.  (The exact power-of-two
+    // prescale used to run first for both paths: ilogb / scalbn on the serial
+    // chain cost C4 1.4 %, C5 3 %, C3 3 %, C2 5 %; now only the Jacobi path pays.)
     double ss_ns;
     if (polar_ns(e, hb, r, j, g_out, ss_ns, scratch)) {
-      sig_sum = scalbn(ss_ns, ex);
+      sig_sum = ss_ns;
 #ifdef QFS_DIAG_POLAR
       sig_sum = 100.0 * 1e7 + (double)(clock64() - t_ns);
 #endif
       return false;  // the warm start of the Jacobi path is left as it was
     }
   }
+  // Jacobi path: exact power-of-two scaling of E'
+  double mx = fmax(fabs(e.x), fabs(e.y));
+#pragma unroll
+  for (int o = 1; o < 16; o <<= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+  const int ex = mx > 0.0 ? ilogb(mx) : 0;
+  e.x = scalbn(e.x, -ex);
+  e.y = scalbn(e.y, -ex);
   const double2 v0 = v0p ? v0p[l] : make_double2((l % 5 == 0) ? 1.0 : 0.0, 0.0);
   // A_0 = E' V_0
   double2 a = make_double2(0.0, 0.0);
