@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(BLK_THREADS) blk_env_kernel(const BlkEnvParams
   if constexpr (D == 4) {
     const int l = lane & 15;
     double2 g, v;
-    gate_update(bg.kind, sE[l], gw, P.beta, nullptr, g, v, ss, scratch + 2 * (lane & 16));
+    gate_update(bg.kind, sE[l], gw, P.beta, nullptr, g, v, ss, scratch + 2 * (lane & 16), P.sig != nullptr);
     __syncwarp();
     if (lane < 16 && bg.kind != 1) gw[l] = g;
   } else {

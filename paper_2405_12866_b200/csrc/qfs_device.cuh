@@ -151,7 +151,8 @@ __device__ __forceinline__ double half_sum(double v) {
 // The 4x4 products exchange operands through shared memory (scr: 32 double2
 // of this half warp: X at [0, 16), T at [16, 32)): one store and eight
 // broadcast-friendly loads per product instead of eight 128-bit shuffles.
-__device__ bool polar_ns(double2 e, int hb, int r, int c, double2 &g_out, double &ss_out, double2 *scr) {
+__device__ bool polar_ns(double2 e, int hb, int r, int c, double2 &g_out, double &ss_out, double2 *scr,
+                         bool need_ss = true) {
   const double fro2 = half_sum(e.x * e.x + e.y * e.y);
   if (!__all_sync(FULL, fro2 > 0.0)) return false;
   const double rs = 2.0 * rsqrt(fro2);
@@ -191,7 +192,7 @@ __device__ bool polar_ns(double2 e, int hb, int r, int c, double2 &g_out, double
   }
   // G = W^dag: G[r][c] = conj(W[c][r]);  sum sigma = Re Tr(W^dag E') = Re sum conj(W) o E'
   g_out = cconj(shfl_c(x, hb | (4 * c + r)));
-  ss_out = half_sum(x.x * e.x + x.y * e.y);
+  ss_out = need_ss ? half_sum(x.x * e.x + x.y * e.y) : 0.0;  // (skipped when nobody reads it)
   return true;
 }
 
@@ -200,7 +201,7 @@ __device__ bool polar_ns(double2 e, int hb, int r, int c, double2 &g_out, double
 // critical chain.  Returns true when v_out holds new right singular vectors
 // (Jacobi ran), false when V was not touched (Newton-Schulz).
 __device__ bool hw_polar(double2 e, const double2 *v0p, double2 &g_out, double2 &v_out, double &sig_sum,
-                         double2 *scratch) {
+                         double2 *scratch, bool need_ss = true) {
   const int lane = threadIdx.x & 31;
   const int hb = lane & 16;         // half-warp base lane
   const int l = lane & 15;
@@ -214,7 +215,7 @@ __device__ bool hw_polar(double2 e, const double2 *v0p, double2 &g_out, double2 
     // prescale used to run first for both paths: ilogb / scalbn on the serial
     // chain cost C4 1.4 %, C5 3 %, C3 3 %, C2 5 %; now only the Jacobi path pays.)
     double ss_ns;
-    if (polar_ns(e, hb, r, j, g_out, ss_ns, scratch)) {
+    if (polar_ns(e, hb, r, j, g_out, ss_ns, scratch, need_ss)) {
       sig_sum = ss_ns;
 #ifdef QFS_DIAG_POLAR
       sig_sum = 100.0 * 1e7 + (double)(clock64() - t_ns);
@@ -365,12 +366,12 @@ __device__ bool hw_polar(double2 e, const double2 *v0p, double2 &g_out, double2 
 // the old gate (row-major, read-only); both halves may hold different matrices
 // but the kind must be warp-uniform.
 __device__ bool gate_update(int kind, double2 e, const double2 *gold, double beta, const double2 *v0p, double2 &g,
-                            double2 &v, double &ss, double2 *scratch) {
+                            double2 &v, double &ss, double2 *scratch, bool need_ss = true) {
   const int lane = threadIdx.x & 31, hb = lane & 16, l = lane & 15, r = l >> 2, c = l & 3;
   if (kind == 1) {
     g = gold[l];
     const double2 gt = gold[4 * c + r];  // G[c][r]
-    ss = half_sum(e.x * gt.x - e.y * gt.y);
+    ss = need_ss ? half_sum(e.x * gt.x - e.y * gt.y) : 0.0;
     return false;
   }
   const bool blk = (r >> 1) == (c >> 1);
@@ -386,7 +387,7 @@ __device__ bool gate_update(int kind, double2 e, const double2 *gold, double bet
     const double2 go = gold[4 * c + r];  // (G^dag)[r][c] = conj(G[c][r])
     e = make_double2((1.0 - beta) * e.x + beta * go.x, (1.0 - beta) * e.y - beta * go.y);
   }
-  const bool vnew = hw_polar(e, v0p, g, v, ss, scratch);
+  const bool vnew = hw_polar(e, v0p, g, v, ss, scratch, need_ss);
   if (kind == 2) {
     const double2 ga = shfl_c(g, hb | (4 * (r & 1) + (c & 1)));
     const double2 gb = shfl_c(g, hb | (4 * ((r & 1) + 2) + (c & 1) + 2));

@@ -80,7 +80,7 @@ __device__ void polar_write(const double *e32, double2 *gout, double2 *vslot, do
   if (env_out && lane < 16) env_out[l] = e;
   double2 g, v;
   double ss;
-  const bool vnew = gate_update(kind, e, gout, beta, vslot, g, v, ss, scratch + 2 * (lane & 16));
+  const bool vnew = gate_update(kind, e, gout, beta, vslot, g, v, ss, scratch + 2 * (lane & 16), sig_out != nullptr);
   __syncwarp();
   if (lane < 16 && kind != 1) {
     gout[l] = g;

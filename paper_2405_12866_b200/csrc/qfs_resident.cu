@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
         double2 g, v;
         double ss;
         gate_update(kind, ev, gi, P.beta, nullptr, g, v, ss,
-                    sm.scr + 2 * (lane & 16));
+                    sm.scr + 2 * (lane & 16), P.sig != nullptr);
         __syncwarp();
         if (lane < 16 && kind != 1) gi[l] = g;
         if (rank == 0) {

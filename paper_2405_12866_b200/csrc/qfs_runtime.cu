@@ -363,6 +363,7 @@ struct SweepSpec {
   std::vector<Slot> slots;   // active starts (local rows per start)
   int M_max = 0;
   bool want_val = false;
+  bool want_sig = false;         // write sum sigma per gate (sigma traces only)
   double beta = 0.0;
   double2 *env_trace = nullptr;  // device [K][S][16] or nullptr
   int S = 0;                     // total starts (trace layout / strides)
@@ -506,7 +507,7 @@ qfs_status issue_blocks(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStr
       e.n = n; e.i = i; e.K = K; e.S = sp.S; e.slots = slots; e.bg = c->d_bg; e.gates = c->d_gates; e.gsz = c->gsz;
       e.phi = i == 0 ? xpool : View{Bk(i), sS, Mc, 1};
       e.chi = i == K - 1 ? ypool : View{c->d_chi, sS, Mc, 1};
-      e.partials = bpart; e.counters = cnt_b; e.beta = sp.beta; e.sig = c->d_sig;
+      e.partials = bpart; e.counters = cnt_b; e.beta = sp.beta; e.sig = sp.want_sig ? c->d_sig : nullptr;
       e.env_trace = sp.env_trace; e.err = c->d_check;
       const int ar = c->bgh[i].a;
       CUDA_TRY(c, launch_blk_env(e, ar, blk_ctas((N >> ar) * M_max, ns), ns, st));
@@ -561,7 +562,7 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
     r.slots = c->d_slots + j0; r.pairs = c->d_pairs; r.gates = c->d_gates;
     r.x = c->d_x; r.y = c->d_y; r.m_pool = c->m_pool; r.xv = c->d_xv; r.yv = c->d_yv;
     r.V = c->V; r.want_val = sp.want_val ? 1 : 0; r.beta = sp.beta;
-    r.csum = c->d_csum + j0; r.cval = c->d_cval + j0; r.sig = c->d_sig; r.env_trace = sp.env_trace;
+    r.csum = c->d_csum + j0; r.cval = c->d_cval + j0; r.sig = sp.want_sig ? c->d_sig : nullptr; r.env_trace = sp.env_trace;
     r.dbg = c->d_res_dbg;
     double units = 0;
     for (int j = j0; j < j1; ++j) units += (double)sp.slots[j].m * (double)c->N;
@@ -643,7 +644,7 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
   b.partials = partials; b.counters = cnt_b; b.e_red = ered;
   b.counters1 = c->d_counters1 + (long long)j0 * 40; b.gpartials = c->d_gpart + (long long)j0 * 40 * 32;
   b.fuse_polar = (c->mode == 1 && c->world > 1) ? 0 : 1;
-  b.beta = sp.beta; b.sig = c->d_sig; b.env_trace = sp.env_trace;
+  b.beta = sp.beta; b.sig = sp.want_sig ? c->d_sig : nullptr; b.env_trace = sp.env_trace;
   b.vprev = c->d_vprev;
   b.dbg = c->d_dbg;
   double bwd_bytes = 0, bwd_flops = 0;
@@ -674,7 +675,7 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
       }
       PolarParams pp{};
       pp.K = K; pp.gate = i; pp.S = sp.S; pp.n_slots = ns; pp.slots = slots; pp.kinds = c->d_kinds;
-      pp.e_red = ered; pp.gates = c->d_gates; pp.beta = sp.beta; pp.sig = c->d_sig;
+      pp.e_red = ered; pp.gates = c->d_gates; pp.beta = sp.beta; pp.sig = sp.want_sig ? c->d_sig : nullptr;
       pp.env_trace = sp.env_trace; pp.vprev = c->d_vprev;
       LaunchScope ls(c, K_POLAR, 0, 0);
       CUDA_TRY(c, launch_polar(pp, ns, st));
@@ -780,7 +781,7 @@ qfs_status run_sweep(qfs_ctx *c, const SweepSpec &sp, std::vector<double> &csum,
   const bool resident = !c->blocks && res_plan(c, sp.M_max, ns, pl);
   const bool use_graph = sp.env_trace == nullptr && !resident && !getenv("QFS_NO_GRAPH");
   if (use_graph) {
-    long long key[8] = {ns, sp.M_max, sp.want_val, (long long)(sp.beta * 1e15), sp.S, c->S_cap,
+    long long key[8] = {ns, sp.M_max, sp.want_val + 2 * sp.want_sig, (long long)(sp.beta * 1e15), sp.S, c->S_cap,
                         c->M_cap, (c->prof ? 2 : 1)};
     if (!c->gexec || std::memcmp(key, c->gkey, sizeof key) != 0) {
       drop_graph(c);
@@ -1189,7 +1190,7 @@ qfs_status qfs_trace_sweeps(qfs_ctx *c, int s, const double *init_gates, int m, 
   }
   SweepSpec sp;
   for (int q = 0; q < s; ++q) sp.slots.push_back({q, ml});
-  sp.M_max = ml; sp.want_val = false; sp.beta = beta; sp.S = s;
+  sp.M_max = ml; sp.want_val = false; sp.beta = beta; sp.S = s; sp.want_sig = sigma_trace != nullptr;
   sp.env_trace = env_trace ? c->d_env_trace : nullptr;
   std::vector<double> csum, cval;
   for (int t = 0; t < n_sweeps; ++t) {
