@@ -7,7 +7,9 @@ library ``oracle/libqfs_oracle.so`` built from ``oracle/qfso.cpp``.
 
 Parity status of each function (DESIGN.md §4 lists the pins):
   apply_gate, circuit_forward, environment, svd4, polar_update, distance,
-  trace_sweeps, instantiate — pinned by tests/test_oracle_pins.py.
+  trace_sweeps, instantiate — pinned by tests/test_oracle_pins.py;
+  apply_block, environment_block, polar_update_block, trace_sweeps_blocks,
+  instantiate_blocks (multi-qubit blocks) — pinned by tests/test_blocks_oracle.py.
   Long-run trajectories beyond the first sweeps on hard landscapes: parity
   unpinned (same termination class + final-cost tolerance only).
 """
