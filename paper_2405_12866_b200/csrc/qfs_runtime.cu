@@ -112,6 +112,7 @@ struct qfs_ctx {
   unsigned *h_check = nullptr;  // pinned read-back of the gate-check flag
   unsigned *d_check = nullptr;
   bool check_pending = false;
+  bool check_fetched = false;   // h_check already read back with the last sweep's costs
   size_t h_slots_cap = 0;
   cudaStream_t st_copy = nullptr;
   // graph cache
@@ -761,7 +762,8 @@ qfs_status run_sweep(qfs_ctx *c, const SweepSpec &sp, std::vector<double> &csum,
     CUDA_TRY(c, cudaHostAlloc((void **)&c->h_slots, (size_t)std::max(ns, 64) * sizeof(Slot), cudaHostAllocMapped));
     c->h_slots_cap = (size_t)std::max(ns, 64);
   }
-  CUDA_TRY(c, cudaStreamSynchronize(c->st));  // the previous table's reader is done
+  // (the previous table's reader, a copy kernel, finished before the previous
+  // run_sweep returned: it ends with a stream synchronisation)
   std::memcpy(c->h_slots, sp.slots.data(), ns * sizeof(Slot));
   {
     Slot *dh = nullptr;
@@ -811,6 +813,10 @@ qfs_status run_sweep(qfs_ctx *c, const SweepSpec &sp, std::vector<double> &csum,
   CUDA_TRY(c, cudaMemcpyAsync(c->h_csum, c->d_csum, ns * sizeof(double), cudaMemcpyDeviceToHost, c->st));
   if (sp.want_val && c->V > 0)
     CUDA_TRY(c, cudaMemcpyAsync(c->h_cval, c->d_cval, ns * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  if (c->check_pending && !c->check_fetched) {  // the gate-check flag rides on the same synchronisation
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_check, c->d_check, sizeof(unsigned), cudaMemcpyDeviceToHost, c->st));
+    c->check_fetched = true;
+  }
   CUDA_TRY(c, cudaStreamSynchronize(c->st));
   csum.assign(c->h_csum, c->h_csum + ns);
   if (sp.want_val && c->V > 0) cval.assign(c->h_cval, c->h_cval + ns);
@@ -841,8 +847,11 @@ qfs_status run_sweep(qfs_ctx *c, const SweepSpec &sp, std::vector<double> &csum,
 qfs_status gate_check_result(qfs_ctx *c) {
   if (!c->check_pending) return QFS_OK;
   c->check_pending = false;
-  CUDA_TRY(c, cudaMemcpyAsync(c->h_check, c->d_check, sizeof(unsigned), cudaMemcpyDeviceToHost, c->st));
-  CUDA_TRY(c, cudaStreamSynchronize(c->st));
+  if (!c->check_fetched) {
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_check, c->d_check, sizeof(unsigned), cudaMemcpyDeviceToHost, c->st));
+    CUDA_TRY(c, cudaStreamSynchronize(c->st));
+  }
+  c->check_fetched = false;
   const unsigned bad = *c->h_check;
   if (bad & 1u) return fail(c, QFS_ERR_NUMERIC, "non-finite initial gate");
   if (bad & 2u) return fail(c, QFS_ERR_NUMERIC, "initial gate not unitary (tol 1e-10)");
@@ -876,6 +885,7 @@ qfs_status upload_gates(qfs_ctx *c, int s, const double *init) {
     if (c->blocks) CUDA_TRY(c, launch_blk_gate_check(c->d_gates, c->d_bg, c->K, c->gsz, s, c->d_check, c->st));
     else CUDA_TRY(c, launch_gate_check(c->d_gates, (long long)s * c->K, c->K, c->d_kinds, c->d_check, c->st));
     c->check_pending = true;
+    c->check_fetched = false;
   }
   CUDA_TRY(c, launch_identity_fill(c->d_vprev, (long long)s * c->K, c->st));
   c->launches++;
