@@ -497,3 +497,21 @@ def test_set_structure_matches_fresh_context():
         fresh.close()
         assert np.array_equal(a["cost"], b["cost"]) and np.array_equal(a["gates"], b["gates"])
     ctx.close()
+
+
+@pytest.mark.gpu
+def test_set_structure_errors():
+    from paper_2405_12866_b200 import build, qfs
+    build.build()
+    ctx = qfs.Context(4, I.brick_pairs(4, 3))
+    with pytest.raises(qfs.QfsError):
+        ctx.set_structure(np.array([[0, 0]], np.int32))      # repeated qubit
+    with pytest.raises(qfs.QfsError):
+        ctx.set_structure(np.array([[0, 4]], np.int32))      # qubit out of range
+    ctx.set_structure(np.array([[1, 3], [0, 2]], np.int32))  # valid: accepted
+    ctx.close()
+    bq, ba = I.block_structure(5, 3)
+    bctx = qfs.BlockContext(5, bq, ba)
+    with pytest.raises(qfs.QfsError):
+        bctx.set_structure(np.array([[0, 1]], np.int32))     # not for block circuits
+    bctx.close()
