@@ -43,6 +43,9 @@ constexpr int RES_THREADS = QFS_RES_THREADS;
 #define QFS_RES_ENV_UNROLL 2  // res_env items per unrolled iteration (loads of the next item above the FMAs)
 #endif
 constexpr int RES_ENV_UNROLL = QFS_RES_ENV_UNROLL;
+#ifndef QFS_RES_PUSH
+#define QFS_RES_PUSH 1  // resident: CTA partials pushed over DSMEM before the cluster barrier
+#endif
 #ifndef QFS_RES_PAIRS
 #define QFS_RES_PAIRS 1  // resident forward / validation: two gates per shared-memory pass
 #endif
@@ -83,6 +86,12 @@ __device__ __forceinline__ void cl_wait() { asm volatile("barrier.cluster.wait.a
 // load a double from the same shared-memory offset in CTA `rank` of the cluster
 // (volatile without a memory clobber: kept after the cluster barrier's wait,
 // which clobbers memory, but independent loads can be in flight together)
+__device__ __forceinline__ void st_remote_d(double *p, unsigned rank, double v) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+  unsigned ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
+}
 __device__ __forceinline__ double ld_remote(const double *p, unsigned rank) {
   const unsigned a = (unsigned)__cvta_generic_to_shared(p);
   unsigned ra;
@@ -299,7 +308,7 @@ __device__ ResSmem res_carve(unsigned char *base, int K, int n, int ld) {
   m.G = (double2 *)base;
   m.red = (double *)(m.G + K * 16);
   m.buf = m.red + RES_WARPS * 32;
-  m.cbuf = m.buf + 64;
+  m.cbuf = m.buf + (QFS_RES_PUSH ? 2 * 16 * 32 : 64);
   m.scr = (double2 *)(m.cbuf + 2);
   m.pr = (int2 *)(m.scr + 64);
   m.kinds = (int *)(m.pr + K);
@@ -380,6 +389,21 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
       res_env(sm.phi, sm.chi, sm.pr[i], cnt, fd, ld, n, sm.red);
       __syncthreads();
       stamp(2);  // [2] environment pass
+#if QFS_RES_PUSH
+      // push this CTA's partial into slot [rank] of every cluster CTA's buffer
+      // (remote stores overlap the barrier); after it, all partials are local
+      if (warp == 0) {
+        double e = 0.0;
+#pragma unroll
+        for (int w = 0; w < RES_WARPS; ++w) e += sm.red[w * 32 + lane];
+        for (unsigned c = 0; c < C; ++c) st_remote_d(sm.buf + par * 512 + rank * 32 + lane, c, e);
+      }
+      cl_arrive();
+      if (warp == 0) {
+        cl_wait();
+        double e = 0.0;
+        for (unsigned c = 0; c < C; ++c) e += sm.buf[par * 512 + c * 32 + lane];  // rank order
+#else
       if (warp == 0) {
         double e = 0.0;
 #pragma unroll
@@ -396,6 +420,7 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
 #pragma unroll
         for (unsigned c = 0; c < 16; ++c)
           if (c < C) e += rv[c];
+#endif
         stamp(3);  // [3] CTA + cluster reduction
         const int l = lane & 15;
         double2 ev = make_double2(__shfl_sync(FULL, e, 2 * l), __shfl_sync(FULL, e, 2 * l + 1));
@@ -780,7 +805,7 @@ cudaError_t launch_val_block(const ValRowParams &p, int n_slots, cudaStream_t st
 }
 
 size_t res_smem_bytes(int n, int K, int ld) {
-  size_t b = (size_t)K * 16 * sizeof(double2) + (RES_WARPS * 32 + 64 + 2) * sizeof(double) +
+  size_t b = (size_t)K * 16 * sizeof(double2) + (RES_WARPS * 32 + (QFS_RES_PUSH ? 2 * 16 * 32 : 64) + 2) * sizeof(double) +
              64 * sizeof(double2) + (size_t)K * (sizeof(int2) + sizeof(int));
   b = (b + 15) & ~(size_t)15;
   b += 2 * ((size_t)ld << n) * sizeof(double2);
