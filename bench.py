@@ -377,9 +377,16 @@ def main():
         cores = host_cores()
         starts = min(cores, s_per)
         v, cdt = cpu_oracle_run(prob, m, starts, cores, steps=1)
+        csteps = 1
+        if cdt < 0.5:  # short configs: enough steps for about a second of wall time (bounded)
+            csteps = int(min(50, max(2, 1.0 / max(cdt, 1e-3))))
+            v, cdt = cpu_oracle_run(prob, m, starts, cores, steps=csteps)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"{starts} starts x 1 controller step (sweep + validation) of {args.config.upper()}, "
-                         f"{cdt:.1f} s wall"}
+               "sample": f"{starts} starts x {csteps} controller step(s) (sweep + validation) of "
+                         f"{args.config.upper()}, {cdt:.1f} s wall"}
+        if cdt / max(1, starts) * cores < 5.0:  # 1-thread figure when it stays short
+            v1, dt1 = cpu_oracle_run(prob, m, 1, 1, steps=1)
+            cpu["single_thread"] = {"value": v1, "unit": UNIT, "sample": f"1 start x 1 controller step, {dt1:.1f} s"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
