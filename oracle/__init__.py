@@ -5,11 +5,28 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
 CUDA product path (``paper_2405_12866_b200``); it loads its own plain C++17
 library ``oracle/libqfs_oracle.so`` built from ``oracle/qfso.cpp``.
 
-Parity status of each function (DESIGN.md §4 lists the pins):
-  apply_gate, circuit_forward, environment, svd4, polar_update, distance,
-  trace_sweeps, instantiate — pinned by tests/test_oracle_pins.py;
-  apply_block, environment_block, polar_update_block, trace_sweeps_blocks,
-  instantiate_blocks (multi-qubit blocks) — pinned by tests/test_blocks_oracle.py.
+Pin of each function (DESIGN.md §6 lists them; every pin compares with
+something other than the oracle itself):
+  apply_gate        dense Kronecker embeddings (n <= 4, all ordered pairs), CNOT / X
+                    truth tables (tests/golden), SWAP identity, norm, inverse
+  circuit_forward   dense product of embedded gates; the tensordot harness
+  environment       brute-force d^2 probe circuits; K=1 full-basis closed form E = U^dag;
+                    Tr(E I) = M at the perfect match
+  svd4 / polar_update / newton_polar
+                    LAPACK singular values and polar factor, von Neumann optimality vs
+                    1000 random unitaries, beta = 1 -> no update, golden svd_known.json
+  distance          closed forms (CNOT vs identity golden cost; M = 2^n Hilbert-Schmidt
+                    identity eq:qfactor_cost_func <-> eq:qfactor_sample_cost_function)
+  trace_sweeps      chain invariant, per-gate monotone cost, exact-initialisation
+                    fixed point, one-sweep solutions, g-shard emulation
+  instantiate       controller replays (PLATEAU at sweep 6, restart geometry,
+                    POOL_EXHAUSTED, MAX_ITER), winner rule (earliest, then lowest
+                    index, min c_train) on constructed multistarts, c_train and the
+                    validation cost (validation_cost: post-sweep gates, / V) against a
+                    dense U and C (n = 5), warm convergence, generalisation statistic
+  *_block / *_blocks  (multi-qubit blocks) tests/test_blocks_oracle.py: dense
+                    embeddings from the index definition, probe circuits, LAPACK, the
+                    pair oracle; validation_cost_blocks against a dense U and C
   Long-run trajectories beyond the first sweeps on hard landscapes: parity
   unpinned (same termination class + final-cost tolerance only).
 """

@@ -322,6 +322,9 @@ void sweep_one(int n, int K, const int32_t *pairs, const int32_t *kinds, cd *G /
   if (out) out->c_train = (double)(tot / (long double)M);
 }
 
+// c_val = (1/V) sum_v ||y_v - C x_v||^2 through all K gates G
+// (the caller passes the post-sweep gates, R7).  Pinned against a dense U and C
+// (tests/test_oracle_pins.py::test_validation_cost_dense_brute_force).
 double validation_cost(int n, int K, const int32_t *pairs, const cd *G, int V, const double *xv,
                        const double *yv) {
   const long N = 1L << n;

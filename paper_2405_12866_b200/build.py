@@ -29,31 +29,37 @@ def nccl_dir() -> str:
     raise RuntimeError("NCCL headers not found under nvidia/nccl")
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(LIB):
-        t = os.path.getmtime(LIB)
+LIB_DEBUG = os.path.join(HERE, "libqfs_debug.so")
+
+
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+    """Compile libqfs.so (or, with ``debug``, libqfs_debug.so: -DQFS_DEBUG device
+    bounds checks of the streamed kernels' offsets; same ABI)."""
+    lib = LIB_DEBUG if debug else LIB
+    if not force and os.path.exists(lib):
+        t = os.path.getmtime(lib)
         if all(os.path.getmtime(d) <= t for d in DEPS):
-            return LIB
+            return lib
     nd = nccl_dir()
     libs = glob.glob(os.path.join(nd, "lib", "libnccl.so*"))
     if not libs:
         raise RuntimeError("libnccl.so not found")
-    tmp = f"{LIB}.tmp{os.getpid()}"
+    tmp = f"{lib}.tmp{os.getpid()}"
     cmd = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
            "-Xptxas", "-v" if verbose else "-O3",
            f"-I{os.path.join(nd, 'include')}", f"-I{os.path.join(ROOT, 'include')}",
            f"-L{os.path.join(nd, 'lib')}", f"-l:{os.path.basename(sorted(libs)[0])}",
            "-Xlinker", f"-rpath={os.path.join(nd, 'lib')}",
-           *os.environ.get("QFS_NVCC_DEFINES", "").split(),
+           *os.environ.get("QFS_NVCC_DEFINES", "").split(), *(["-DQFS_DEBUG"] if debug else []),
            "-o", tmp, *SOURCES]
     r = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed:\n{r.stdout}\n{r.stderr}")
     if verbose:
         print(r.stdout, r.stderr)
-    os.replace(tmp, LIB)  # atomic: concurrent builders (one process per GPU) never see a partial file
-    return LIB
+    os.replace(tmp, lib)  # atomic: concurrent builders (one process per GPU) never see a partial file
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, debug="--debug" in sys.argv))

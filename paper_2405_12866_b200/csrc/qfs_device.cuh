@@ -7,11 +7,30 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 namespace qfs {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
+
+// Debug build (build.py --debug: -DQFS_DEBUG, libqfs_debug.so): device-side
+// bounds checks of the streamed kernels' 32-bit offsets (compute-sanitizer is
+// closed on this pool).  A failed check traps the kernel (the launch reports
+// cudaErrorAssert / a device fault) instead of touching memory out of range.
+#ifdef QFS_DEBUG
+#define QFS_DASSERT(cond)                                                       \
+  do {                                                                          \
+    if (!(cond)) {                                                              \
+      printf("QFS_DASSERT failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__);   \
+      __trap();                                                                 \
+    }                                                                           \
+  } while (0)
+#else
+#define QFS_DASSERT(cond) \
+  do {                    \
+  } while (0)
+#endif
 constexpr int JACOBI_MAX_SWEEPS = 20;
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {

@@ -195,6 +195,9 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
     ec = g * csa + m;
     ed = g * dsa + m;
     ef = g * fsa + m;
+    // every member offset stays inside one start's [2^n][sa] block (32-bit guard, runtime offsets_fit)
+    QFS_DASSERT(m >= Ms || ((unsigned long long)(g | (unsigned)G.off[(1 << NU) - 1]) << 0) < (1ull << P.n));
+    QFS_DASSERT(m >= Ms || (unsigned long long)(g + (unsigned)G.off[(1 << NU) - 1]) * fsa + m < ((unsigned long long)fsa << P.n));
     return m < Ms;
   };
   // chi destination offset of the items in flight (EDRING: computed once, at
@@ -759,6 +762,7 @@ __global__ void __launch_bounds__(FWD_THREADS, QFS_FWD2_MINB) fwd2_kernel(const 
     const unsigned m = w - g * Ms;
 #pragma unroll
     for (int q = 0; q < NU; ++q) g = insert_zero32(g, ins[q]);
+    QFS_DASSERT((unsigned long long)(g + (unsigned)P.off[(1 << NU) - 1]) * ssa + m < ((unsigned long long)ssa << P.n));
     return make_uint2(g, m);
   };
 #if QFS_FWD2_HINT

@@ -74,7 +74,11 @@ struct qfs_ctx {
   double2 *d_xv = nullptr, *d_yv = nullptr;  // validation, row-major [V][2^n]
   // work buffers
   int G_cap = 0, S_cap = 0, M_cap = 0, V_cap = 0, nb_cap = 0;
-  int K_alloc = 0;  // gates the structure-dependent buffers were sized for (qfs_set_structure)
+  int K_alloc = 0;  // gates d_pairs / d_kinds were sized for (qfs_set_structure)
+  int K_g = 0;      // gates d_gates / d_vprev were sized for (ensure_gates)
+  int K_s = 0;      // gates d_B / d_sig were sized for (ensure_state)
+  bool force_unfused = false;  // QFS_UNFUSED_POLAR=1: separate polar launch (sample-mode code path at world 1)
+  int V_glob = 0;   // validation rows over all ranks (sample mode: sum of the ranks' V)
   double2 *d_vprev = nullptr;  // [S][K][16] right singular vectors of the last polar step (warm start)
   double2 *d_gates = nullptr, *d_chi = nullptr, *d_B = nullptr, *d_vb0 = nullptr, *d_vb1 = nullptr;
   double *d_partials = nullptr, *d_ered = nullptr, *d_sig = nullptr, *d_csum = nullptr,
@@ -280,6 +284,11 @@ int blocks_per_start(long long items, int n_slots, int bpsm = 4) {
   return (int)nb;
 }
 
+// 32-bit addressing limit of the streamed kernels (bwd / fwd2 byte and element
+// offsets inside one start's [2^n][rows] block, FastDiv numerators < 2^31):
+// 2^n * rows * 16 B must stay below 4 GiB.
+bool offsets_fit(const qfs_ctx *c, long long rows) { return ((long long)c->N * rows) < (1LL << 28); }
+
 // memory plan (bytes) for S starts, M_cap rows per start, V validation rows
 size_t plan_bytes(const qfs_ctx *c, int S, int M, int V, int nb) {
   size_t N = (size_t)c->N;
@@ -293,13 +302,23 @@ size_t plan_bytes(const qfs_ctx *c, int S, int M, int V, int nb) {
 }
 
 qfs_status ensure_gates(qfs_ctx *c, int S) {
-  if (S <= c->G_cap) return QFS_OK;
+  // sized for G_cap starts of K_g gates: a structure with more gates
+  // (qfs_set_structure) must reallocate even when S fits
+  if (S <= c->G_cap && c->K <= c->K_g) return QFS_OK;
+  S = std::max(S, c->G_cap);
+  const int K = std::max(c->K, c->K_g);
+  CUDA_TRY(c, cudaStreamSynchronize(c->st));
   dfree(c->d_gates);
   dfree(c->d_vprev);
   c->G_cap = 0;
-  CUDA_TRY(c, cudaMalloc(&c->d_gates, (size_t)S * c->gsz * sizeof(double2)));
-  CUDA_TRY(c, cudaMalloc(&c->d_vprev, (size_t)S * c->K * 16 * sizeof(double2)));
+  c->K_g = 0;
+  drop_graph(c);
+  // gsz = 16 K for pair circuits; block circuits never change structure
+  const long long gsz = c->blocks ? c->gsz : 16LL * K;
+  CUDA_TRY(c, cudaMalloc(&c->d_gates, (size_t)S * gsz * sizeof(double2)));
+  CUDA_TRY(c, cudaMalloc(&c->d_vprev, (size_t)S * K * 16 * sizeof(double2)));
   c->G_cap = S;
+  c->K_g = K;
   drop_graph(c);
   return QFS_OK;
 }
@@ -309,7 +328,12 @@ qfs_status ensure_gates(qfs_ctx *c, int S) {
 // (on a double-and-restart) may discard them; the gates live elsewhere.
 qfs_status ensure_state(qfs_ctx *c, int S, int M, int V) {
   const int nb = kMaxBlocksPerStart;  // any launch: nb <= 148 * 4 (blocks_per_start)
-  if (S <= c->S_cap && M <= c->M_cap && V <= c->V_cap && nb <= c->nb_cap) return QFS_OK;
+  if (S <= c->S_cap && M <= c->M_cap && V <= c->V_cap && nb <= c->nb_cap && c->K <= c->K_s) return QFS_OK;
+  // the streamed kernels address one start's [2^n][rows] block with 32-bit
+  // element / byte offsets and 32-bit FastDiv numerators: refuse shapes
+  // where 2^n * rows * 16 B reaches 4 GiB instead of wrapping silently
+  if (!offsets_fit(c, std::max(M, c->M_cap)))
+    return fail(c, QFS_ERR_CAPACITY, "2^n * M * 16 B >= 4 GiB: beyond the 32-bit offsets of the streamed kernels");
   S = std::max(S, c->S_cap);
   M = std::max(M, c->M_cap);
   V = std::max(V, c->V_cap);
@@ -323,6 +347,7 @@ qfs_status ensure_state(qfs_ctx *c, int S, int M, int V) {
   if (c->h_cval) cudaFreeHost(c->h_cval);
   c->h_csum = c->h_cval = nullptr;
   c->S_cap = c->M_cap = c->V_cap = c->nb_cap = 0;
+  c->K_s = 0;
   drop_graph(c);
   size_t need = plan_bytes(c, S, M, V, nbc);
   size_t fr = 0, tot = 0;
@@ -356,6 +381,7 @@ qfs_status ensure_state(qfs_ctx *c, int S, int M, int V) {
   CUDA_TRY(c, cudaMallocHost(&c->h_csum, (size_t)S * sizeof(double)));
   CUDA_TRY(c, cudaMallocHost(&c->h_cval, (size_t)S * sizeof(double)));
   c->S_cap = S; c->M_cap = M; c->V_cap = V; c->nb_cap = nbc;
+  c->K_s = c->K;
   return QFS_OK;
 }
 
@@ -429,7 +455,7 @@ struct ResPlan {
   size_t smem = 0;
 };
 bool res_plan(const qfs_ctx *c, int M_max, int ns, ResPlan &pl) {
-  if (c->path == 1 || (c->mode == 1 && c->world > 1) || c->n > 13 || M_max < 1) return false;
+  if (c->path == 1 || (c->mode == 1 && c->world > 1) || c->force_unfused || c->n > 13 || M_max < 1) return false;
   // auto: resident only up to n = 10 — measured crossover (profiles/r1_sweep_map.jsonl:
   // n <= 10 resident 1.3-1.9x faster, n = 11 / 12 streamed 1.14x / 1.40x faster)
   if (c->path == 0 && c->n > 10) return false;
@@ -644,7 +670,8 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
   b.kinds = c->d_kinds;
   b.partials = partials; b.counters = cnt_b; b.e_red = ered;
   b.counters1 = c->d_counters1 + (long long)j0 * 40; b.gpartials = c->d_gpart + (long long)j0 * 40 * 32;
-  b.fuse_polar = (c->mode == 1 && c->world > 1) ? 0 : 1;
+  const bool sample_ar = c->mode == 1 && c->world > 1;  // per-gate NCCL all-reduce of E
+  b.fuse_polar = (sample_ar || c->force_unfused) ? 0 : 1;
   b.beta = sp.beta; b.sig = sp.want_sig ? c->d_sig : nullptr; b.env_trace = sp.env_trace;
   b.vprev = c->d_vprev;
   b.dbg = c->d_dbg;
@@ -669,7 +696,7 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
       CUDA_TRY(c, launch_bwd(b, ns, st));
     }
     if (!b.fuse_polar) {
-      {
+      if (c->mode == 1 && c->comm) {  // (a one-rank communicator too, with QFS_UNFUSED_POLAR)
         LaunchScope ls(c, K_NCCL, 0, 0);
         NCCL_TRY(c, ncclAllReduce(ered, ered, (size_t)ns * 32, ncclFloat64, ncclSum,
                                   c->comm, st));
@@ -695,7 +722,7 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
     LaunchScope ls(c, K_FINAL, units * 32.0, units * 35.0);
     CUDA_TRY(c, launch_final(fp, ns, st));
   }
-  if (c->mode == 1 && c->world > 1) {
+  if (c->mode == 1 && c->comm && (sample_ar || c->force_unfused)) {
     LaunchScope ls(c, K_NCCL, 0, 0);
     NCCL_TRY(c, ncclAllReduce(csum, csum, ns, ncclFloat64, ncclSum, c->comm, st));
   }
@@ -738,8 +765,16 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
       LaunchScope ls(c, K_DIST, vunits * 32.0, vunits * 3.0);
       CUDA_TRY(c, launch_dist(d, ns, st));
     }
-    LaunchScope ls(c, K_REDUCE, 0, 0);
-    CUDA_TRY(c, launch_row_reduce(rowout, c->V, cval, ns, st));
+    {
+      LaunchScope ls(c, K_REDUCE, 0, 0);
+      CUDA_TRY(c, launch_row_reduce(rowout, c->V, cval, ns, st));
+    }
+    if (c->mode == 1 && c->comm && (sample_ar || c->force_unfused)) {
+      // sample mode: every rank holds its own validation shard; the sums are
+      // all-reduced so all ranks take identical controller decisions
+      LaunchScope ls(c, K_NCCL, 0, 0);
+      NCCL_TRY(c, ncclAllReduce(cval, cval, ns, ncclFloat64, ncclSum, c->comm, st));
+    }
   }
   return QFS_OK;
 }
@@ -934,6 +969,7 @@ qfs_status create_common(int n, int k, const int32_t *pairs, int device, qfs_ctx
   if (const char *vb = getenv("QFS_VAL_BLOCK")) c->val_block = atoi(vb) != 0;
   if (const char *rc = getenv("QFS_RES_CMAX")) c->res_cmax = std::max(1, std::min(16, atoi(rc)));
   if (const char *rp = getenv("QFS_RES_PER_SM")) c->res_per_sm = atoi(rp) == 2 ? 2 : 1;
+  if (const char *uf = getenv("QFS_UNFUSED_POLAR")) c->force_unfused = atoi(uf) != 0;
   if (e != cudaSuccess) {
     c->err = std::string("device init: ") + cudaGetErrorString(e);
     *out = c;  // caller can read the error, then destroy
@@ -1049,10 +1085,18 @@ static qfs_status set_samples_impl(qfs_ctx *c, int m_pool, const void *x, const 
     return fail(c, QFS_ERR_ARG, "bad sample arguments");
   if ((long long)m_pool * (c->mode == 1 ? c->world : 1) > c->N)
     return fail(c, QFS_ERR_CAPACITY, "m_pool > 2^n");
+  if (!offsets_fit(c, std::max(m_pool, v)))
+    return fail(c, QFS_ERR_CAPACITY, "2^n * rows * 16 B >= 4 GiB: beyond the 32-bit offsets of the streamed kernels");
   CUDA_TRY(c, cudaSetDevice(c->device));
   // the cached sweep graph holds the pool pointers: it is rebuilt only when a
-  // buffer is reallocated (same shapes: the new contents are used in place)
+  // buffer is reallocated (same shapes: the new contents are used in place).
+  // Dropped BEFORE any buffer is freed, so an early return below (non-finite
+  // sample, allocation failure) can never leave a graph over freed pools.
   const bool realloc = m_pool != c->m_pool || v != c->V;
+  if (realloc) {
+    CUDA_TRY(c, cudaStreamSynchronize(c->st));
+    drop_graph(c);
+  }
   if (m_pool != c->m_pool) {
     dfree(c->d_x); dfree(c->d_y);
     CUDA_TRY(c, cudaMalloc(&c->d_x, (size_t)m_pool * c->N * sizeof(double2)));
@@ -1107,7 +1151,23 @@ static qfs_status set_samples_impl(qfs_ctx *c, int m_pool, const void *x, const 
     c->have_samples = false;
     return fail(c, QFS_ERR_NUMERIC, "non-finite sample");
   }
-  if (realloc) drop_graph(c);
+  // validation rows over all ranks (sample mode: each rank holds its own
+  // validation shard; c_val = (sum over ranks) / V_glob, R11)
+  c->V_glob = v;
+  if (c->mode == 1 && c->world > 1 && c->comm) {
+    // every rank must hold the same number of validation rows (each its own
+    // shard): the per-sweep validation all-reduce is then issued by all ranks
+    int h[2] = {v, -v};
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_flag + 2, h, sizeof h, cudaMemcpyHostToDevice, c->st));
+    NCCL_TRY(c, ncclAllReduce(c->d_flag + 2, c->d_flag + 2, 2, ncclInt32, ncclMax, c->comm, c->st));
+    CUDA_TRY(c, cudaMemcpyAsync(h, c->d_flag + 2, sizeof h, cudaMemcpyDeviceToHost, c->st));
+    CUDA_TRY(c, cudaStreamSynchronize(c->st));
+    if (h[0] != -h[1]) {
+      c->have_samples = false;
+      return fail(c, QFS_ERR_ARG, "sample mode: every rank must pass the same number of validation rows");
+    }
+    c->V_glob = v * c->world;
+  }
   return QFS_OK;
 }
 
@@ -1243,9 +1303,10 @@ qfs_status qfs_bench_sweeps(qfs_ctx *c, int s, const double *init_gates, int m, 
   CUDA_TRY(c, cudaEventCreate(&e0));
   CUDA_TRY(c, cudaEventCreate(&e1));
   CUDA_TRY(c, cudaEventRecord(e0, c->st));
-  for (int t = 0; t < n_sweeps; ++t)
+  for (int t = 0; t < n_sweeps; ++t) {
     if ((st = run_sweep(c, sp, csum, cval)) != QFS_OK) return st;
     if ((st = gate_check_result(c)) != QFS_OK) return st;
+  }
   CUDA_TRY(c, cudaEventRecord(e1, c->st));
   CUDA_TRY(c, cudaEventSynchronize(e1));
   float ms = 0;
@@ -1300,10 +1361,10 @@ qfs_status qfs_instantiate(qfs_ctx *c, int s, const double *init_gates, const qf
       for (size_t j = 0; j < sp.slots.size(); ++j) {
         S_ &a = A[sp.slots[j].s];
         a.c_train = csum[j] / a.M;
-        a.c_val = c->V > 0 ? cval[j] / c->V : NAN;
+        a.c_val = c->V_glob > 0 ? cval[j] / c->V_glob : NAN;
         a.it += 1; a.total += 1;                                               // step 1
         const double cc = a.c_train;
-        const bool gen_check = c->V > 0 && std::isfinite(otr) && a.M < Nfull;  // step 2
+        const bool gen_check = c->V_glob > 0 && std::isfinite(otr) && a.M < Nfull;  // step 2
         bool conv = false;                                                     // step 3
         if (cc <= p->dist_tol) {
           if (!gen_check) conv = true;
@@ -1541,9 +1602,7 @@ qfs_status qfs_set_structure(qfs_ctx *c, int k, const int32_t *pairs) {
       dfree(c->d_dbg);
       CUDA_TRY(c, cudaMalloc(&c->d_dbg, (size_t)4 * k * sizeof(unsigned long long)));
     }
-    c->G_cap = 0;
-    c->S_cap = 0;
-    c->K_alloc = k;
+    c->K_alloc = k;  // gates / B cache / sigma: ensure_gates / ensure_state compare K with K_g / K_s
   }
   CUDA_TRY(c, cudaMemcpy(c->d_pairs, pairs, (size_t)k * sizeof(int2), cudaMemcpyHostToDevice));
   CUDA_TRY(c, cudaMemset(c->d_kinds, 0, (size_t)k * sizeof(int)));

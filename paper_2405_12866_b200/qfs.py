@@ -14,7 +14,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqfs.so")
+# QFS_LIB=debug selects libqfs_debug.so (build.py --debug: device bounds checks); same ABI
+LIB_PATH = os.path.join(_HERE, "libqfs_debug.so" if os.environ.get("QFS_LIB") == "debug" else "libqfs.so")
 
 STATUS = {0: "QFS_OK", 1: "QFS_ERR_ARG", 2: "QFS_ERR_CAPACITY", 3: "QFS_ERR_NUMERIC",
           4: "QFS_ERR_DEVICE", 5: "QFS_ERR_STATE"}

@@ -57,15 +57,24 @@ def _samples(n: int, m: int, v: int, seed: int):
     return x, xv
 
 
+def _local_device() -> int:
+    """This process's GPU: LOCAL_RANK under torchrun (one process per GPU), else 0."""
+    import os
+    return int(os.environ.get("LOCAL_RANK", "0"))
+
+
 def delete_gates_pass(block: Block, params: dict, starts: int = 4, m_pool: int | None = None,
-                      v: int = 16, seed: int = 0, context_factory: Callable | None = None) -> DeletionReport:
+                      v: int = 16, seed: int = 0, context_factory: Callable | None = None,
+                      device: int | None = None) -> DeletionReport:
     """Single left-to-right pass: tentatively remove each gate and keep the
     removal if the reduced block re-instantiates (CONVERGED) to the original
     block's action on the training states (the re-instantiate protocol of P:198).
 
     ``context_factory(n, pairs)`` returns a fresh qfs.Context (default: the GPU
-    library); ``params`` are qfs_instantiate parameters (m_init, dist_tol, ...)."""
+    library on ``device``, default LOCAL_RANK); ``params`` are qfs_instantiate
+    parameters (m_init, dist_tol, ...)."""
     shared = None
+    dev = _local_device() if device is None else int(device)
     if context_factory is None:
         # one GPU context per partition: each attempt swaps the structure in
         # (qfs_set_structure) and keeps the samples and device buffers
@@ -74,7 +83,7 @@ def delete_gates_pass(block: Block, params: dict, starts: int = 4, m_pool: int |
 
         def context_factory(n, pairs):
             if "ctx" not in shared:
-                shared["ctx"] = qfs.Context(n, pairs)
+                shared["ctx"] = qfs.Context(n, pairs, device=dev)
                 shared["fresh"] = True
             else:
                 shared["ctx"].set_structure(pairs)

@@ -209,17 +209,74 @@ def test_trace_parity_streamed_forward_n14(qfs):
 
 
 def test_full_size_c4_sampled_starts(qfs):
-    """C4 at full size (S=16, M=32, K=150, n=12) in the bench's launch shape;
-    the oracle recomputes two of the 16 starts (starts are independent)."""
+    """C4 at full size (S=16, M=32, K=150, n=12) in the bench's launch shape,
+    the first 5 sweeps (north_star); the oracle recomputes two of the 16 starts
+    (starts are independent)."""
     p = I.make_problem("c4", init="R")
     ctx = _ctx(qfs, p.n, p.pairs)
     ctx.set_samples(p.x, p.y, p.xv, p.yv)
-    gt = ctx.trace_sweeps(p.init, p.m_init, 2)
+    gt = ctx.trace_sweeps(p.init, p.m_init, 5)
     pick = [0, 11]
-    ot = oracle.trace_sweeps(p.n, p.pairs, p.init[pick], p.x, p.y, p.m_init, 2)
+    ot = oracle.trace_sweeps(p.n, p.pairs, p.init[pick], p.x, p.y, p.m_init, 5, threads=2)
     sub = dict(env=gt["env"][:, :, pick], gates=gt["gates"][:, pick], cost=gt["cost"][:, pick],
                sigma=gt["sigma"][:, :, pick])
     _compare_traces(sub, ot, "c4-full")
+
+
+def _no_stop(m, sweeps, otr=1e300):
+    """Controller parameters that run exactly ``sweeps`` sweeps (validation every sweep)."""
+    return dict(dist_tol=-1.0, diff_tol_r=1e-3, plateau_window=0, min_iter=10 ** 6, max_iter=sweeps,
+                m_init=m, overtrain_ratio=otr, beta=0.0, stop_on_first=0)
+
+
+def test_full_size_c4_validation_cost_streamed(qfs):
+    """c_val on the streamed path's block validation kernel at
+    the C4 bench shape (S=16, V=16, K=150): two sampled starts' c_val and
+    c_train after 2 controller steps equal the oracle's within 1e-10."""
+    p = I.make_problem("c4", init="R")
+    ctx = _ctx(qfs, p.n, p.pairs)
+    ctx.set_samples(p.x, p.y, p.xv, p.yv)
+    prm = _no_stop(p.m_init, 2, otr=0.1)
+    g1, r1, _ = ctx.instantiate(p.init, prm)
+    pick = [3, 14]
+    g2, r2, _ = oracle.instantiate(p.n, p.pairs, p.x, p.y, p.xv, p.yv, p.init[pick], prm, threads=2)
+    for j, s in enumerate(pick):
+        assert abs(r1[s]["c_val"] - r2[j]["c_val"]) <= COST_TOL * r2[j]["c_val"] + 1e-15, (s, r1[s], r2[j])
+        assert abs(r1[s]["c_train"] - r2[j]["c_train"]) <= COST_TOL * r2[j]["c_train"] + 1e-15
+        assert np.abs(g1[s] - g2[j]).max() <= GATE_TOL
+
+
+def test_full_size_c5_first_sweeps(qfs):
+    """C5 at full size (n=14, K=300, M=64, V=16, S=1; BASELINE.json configs[4]):
+    the first 3 sweeps' environments, gates, costs and sigma sums, then c_val /
+    c_train after 3 controller steps (the cluster validation kernel at the real
+    K, the WIDE backward reduction at the real M) — all against the oracle."""
+    p = I.make_problem("c5", init="R", s=1)
+    assert (p.n, p.k, p.m_init, p.xv.shape[0]) == (14, 300, 64, 16)
+    ctx = _ctx(qfs, p.n, p.pairs)
+    ctx.set_samples(p.x, p.y, p.xv, p.yv)
+    gt = ctx.trace_sweeps(p.init, p.m_init, 3)
+    ot = oracle.trace_sweeps(p.n, p.pairs, p.init, p.x, p.y, p.m_init, 3)
+    _compare_traces(gt, ot, "c5-full")
+    prm = _no_stop(p.m_init, 2)
+    g1, r1, _ = ctx.instantiate(p.init, prm)
+    g2, r2, _ = oracle.instantiate(p.n, p.pairs, p.x, p.y, p.xv, p.yv, p.init, prm)
+    assert abs(r1[0]["c_val"] - r2[0]["c_val"]) <= COST_TOL * r2[0]["c_val"]
+    assert abs(r1[0]["c_train"] - r2[0]["c_train"]) <= COST_TOL * r2[0]["c_train"]
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("name,init,s,m,k", [("c3", "R", 4, 16, None), ("c3", "W", 3, 32, None),
+                                             ("c4", "R", 2, 32, 24)])
+def test_trace_parity_beta(qfs, name, init, s, m, k, path):
+    """beta-regularised update (reading R15): E' = (1 - beta) E +
+    beta G_old^dag traced through whole sweeps at beta = 0.3 on both paths."""
+    p = I.make_problem(name, init=init, s=s, k=k)
+    ctx = _ctx(qfs, p.n, p.pairs, path)
+    ctx.set_samples(p.x, p.y, p.xv, p.yv)
+    gt = ctx.trace_sweeps(p.init, m, 4, beta=0.3)
+    ot = oracle.trace_sweeps(p.n, p.pairs, p.init, p.x, p.y, m, 4, beta=0.3)
+    _compare_traces(gt, ot, f"beta-{name}-{init}")
 
 
 @pytest.mark.parametrize("name,pick", [("c3", [0, 37, 63]), ("c5c", [5, 50])])
@@ -265,6 +322,7 @@ def test_instantiate_warm_converges_and_matches(qfs, name, s, path):
     prm = dict(p.params, max_iter=300)
     (g1, r1, w1), (g2, r2, w2) = _inst_both(qfs, p, prm, path)
     assert r1[w1]["term"] == "CONVERGED" and r1[w1]["c_train"] <= 1e-8
+    assert r2[w2]["term"] == "CONVERGED" and r2[w2]["c_train"] <= 1e-8   # the oracle too
     assert w1 == w2
     for a, b in zip(r1, r2):
         assert a["term"] == b["term"] and a["restarts"] == b["restarts"] and a["final_m"] == b["final_m"]
@@ -281,6 +339,27 @@ def test_instantiate_restart_geometry_gpu(qfs, path):
     for a, b in zip(r1, r2):
         assert a["final_m"] == min(p.m_init * 2 ** a["restarts"], 64)
         assert a["term"] == b["term"] and a["restarts"] == b["restarts"]
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_winner_rule_gpu(qfs, path):
+    """Winner rule on the constructed multistarts of the oracle pin
+    (tests/test_oracle_pins.py::test_winner_rule_earliest_then_lowest_index):
+    the earliest converged start wins over a later one with a lower c_train,
+    identical starts tie to the lower index — the same winner and terminations
+    as the oracle, with and without stop_on_first."""
+    from test_oracle_pins import _winner_problem
+    p, a, b = _winner_problem()
+    init = np.stack([a, b, b])
+    ctx = _ctx(qfs, p.n, p.pairs, path)
+    ctx.set_samples(p.x, p.y, p.xv, p.yv)
+    for sof in (0, 1):
+        prm = dict(p.params, max_iter=300, stop_on_first=sof)
+        g1, r1, w1 = ctx.instantiate(init, prm)
+        g2, r2, w2 = oracle.instantiate(p.n, p.pairs, p.x, p.y, p.xv, p.yv, init, prm, threads=3)
+        assert w1 == w2 == 1
+        assert [r["term"] for r in r1] == [r["term"] for r in r2]
+        assert r1[1]["sweeps"] == r1[2]["sweeps"] and abs(r1[1]["sweeps"] - r2[1]["sweeps"]) <= 2
 
 
 @pytest.mark.parametrize("path", PATHS)
@@ -321,12 +400,21 @@ def test_errors(qfs):
 
 
 # ------------------------------------------------------------- distributed --
-def test_sample_sharded_path_single_rank(qfs):
-    """qfs_create_nccl in sample mode (per-gate NCCL all-reduce of E + polar
-    kernel) with a one-rank communicator equals the oracle and the fused path."""
+def test_sample_sharded_path_single_rank(qfs, monkeypatch):
+    """qfs_create_nccl in sample mode with a one-rank communicator and
+    QFS_UNFUSED_POLAR=1, so the multi-rank code path runs: per-gate NCCL
+    all-reduce of E, separate polar kernel, all-reduced cost and validation
+    sums — equal to the oracle and to the fused path."""
     p = I.make_problem("c3", init="W", s=4)
     nid = qfs.nccl_unique_id()
+    monkeypatch.setenv("QFS_UNFUSED_POLAR", "1")       # read when the context is created
     ctx = qfs.Context(p.n, p.pairs, nccl_id=nid, rank=0, world=1, shard_mode=1)
+    monkeypatch.delenv("QFS_UNFUSED_POLAR")
+    ctx.profile_enable(True)
+    ctx.trace_sweeps(p.init, 32, 1)
+    prof = ctx.profile_read()
+    ctx.profile_enable(False)
+    assert prof["polar"]["launches"] == p.k and prof["nccl_allreduce"]["launches"] >= p.k
     ctx.set_samples(p.x, p.y, p.xv, p.yv)
     gt = ctx.trace_sweeps(p.init, 32, 3)
     ot = oracle.trace_sweeps(p.n, p.pairs, p.init, p.x, p.y, 32, 3)

@@ -570,3 +570,109 @@ def test_u3_cnot_exact_init_fixed_point_and_warm_convergence():
     for i in range(len(kinds)):
         if kinds[i] == I.GATE_FIXED:
             assert np.array_equal(g[win, i], I.CNOT)
+
+
+# --------------------------------------- validation cost, winner --
+def _dense_cost(n, pairs, gates, target_gates, states):
+    """(1/rows) sum ||U psi - C psi||^2 with U, C the DENSE 2^n x 2^n products of
+    embedded gates (tests/qfs_dense.py: permutation + Kronecker, independent of
+    the oracle's bit-insertion loops and of the harness's tensordot)."""
+    from qfs_dense import circuit_matrix
+    U = circuit_matrix(n, pairs, target_gates)
+    C = circuit_matrix(n, pairs, gates)
+    d = (U - C) @ states.T
+    return float(np.sum(np.abs(d) ** 2) / states.shape[0])
+
+
+@pytest.mark.parametrize("sweeps", [1, 3])
+def test_validation_cost_dense_brute_force(sweeps):
+    """P:114, P:184 (SURVEY §8(c) pin table "Validation"): c_val =
+    (1/V) sum_v ||y_v - C x_v||^2 with the POST-sweep gates (reading R7), by a
+    dense U and C at n = 5.  V = 5 != M = 8 and the pre-sweep gates give a
+    visibly different value, so dividing by M or using the gates before the
+    sweep fails this pin; c_train is pinned the same way (direct form R6)."""
+    n, k, m, v = 5, 10, 8, 5
+    rng = np.random.default_rng(184)
+    pairs = I.brick_pairs(n, k)
+    target = np.stack([I.haar_unitary(rng) for _ in range(k)])
+    x = I.haar_states(rng, n, m)
+    xv = I.haar_states(np.random.default_rng(185), n, v)
+    y = I.apply_circuit_tensor(n, pairs, target, x)
+    yv = I.apply_circuit_tensor(n, pairs, target, xv)
+    init = np.stack([np.stack([I.warm_gate(np.random.default_rng(200 + s * k + j), target[j], 0.6)
+                               for j in range(k)]) for s in range(2)])
+    prm = dict(dist_tol=-1.0, diff_tol_r=1e-3, plateau_window=0, min_iter=10 ** 6, max_iter=sweeps,
+               m_init=m, overtrain_ratio=0.1, beta=0.0, stop_on_first=0)
+    g, res, _ = oracle.instantiate(n, pairs, x, y, xv, yv, init, prm)
+    for s in range(2):
+        want_v = _dense_cost(n, pairs, g[s], target, xv)
+        want_t = _dense_cost(n, pairs, g[s], target, x)
+        assert res[s]["sweeps"] == sweeps and res[s]["term"] == "MAX_ITER"
+        assert abs(res[s]["c_val"] - want_v) <= 1e-12 * want_v, (res[s]["c_val"], want_v)
+        assert abs(res[s]["c_train"] - want_t) <= 1e-12 * want_t, (res[s]["c_train"], want_t)
+        # discriminating: the plausible misreadings give other values
+        assert abs(want_v * v / m - want_v) > 1e-3 * want_v                 # / M instead of / V
+        pre = init[s] if sweeps == 1 else oracle.trace_sweeps(n, pairs, init[s:s + 1], x, y, m,
+                                                              sweeps - 1)["gates"][-1, 0]
+        assert abs(_dense_cost(n, pairs, pre, target, xv) - want_v) > 1e-3 * want_v   # pre-sweep gates
+
+
+def test_validation_cost_blocks_dense_brute_force():
+    """The block-circuit validation cost (validation_cost_blocks) against a dense
+    U and C of 2- and 3-qubit blocks built from the index definition (n = 5)."""
+    from test_blocks_oracle import dense_block
+    n, k, m, v = 5, 6, 8, 6
+    qubits, arity = I.block_structure(n, k, seed=11)
+    rng = np.random.default_rng(186)
+    tgt = [I.haar_unitary(rng, 1 << int(a)) for a in arity]
+    x = I.haar_states(rng, n, m)
+    xv = I.haar_states(np.random.default_rng(187), n, v)
+    tp = I.pack_gates(tgt)
+    y = I.apply_blocks_tensor(n, qubits, arity, tp, x)
+    yv = I.apply_blocks_tensor(n, qubits, arity, tp, xv)
+    init = I.pack_gates([I.haar_unitary(rng, 1 << int(a)) for a in arity])[None]
+    prm = dict(dist_tol=-1.0, diff_tol_r=1e-3, plateau_window=0, min_iter=10 ** 6, max_iter=2,
+               m_init=m, overtrain_ratio=0.1, beta=0.0, stop_on_first=0)
+    g, res, _ = oracle.instantiate_blocks(n, qubits, arity, x, y, xv, yv, init, prm)
+
+    def dense(gl):
+        C = np.eye(1 << n, dtype=complex)
+        for i, gi in enumerate(gl):
+            C = dense_block(n, list(qubits[i][:int(arity[i])]), gi) @ C
+        return C
+    U, C = dense(tgt), dense(I.unpack_gates(g[0], arity))
+    want = float(np.sum(np.abs((U - C) @ xv.T) ** 2) / v)
+    assert abs(res[0]["c_val"] - want) <= 1e-12 * want, (res[0]["c_val"], want)
+
+
+def _winner_problem():
+    """C2 warm starts whose trajectories are known to differ (see the premise
+    asserts): start a converges LATER than start b but with a LOWER c_train."""
+    p = I.make_problem("c2", init="W", s=8)
+    return p, p.init[2], p.init[1]
+
+
+def test_winner_rule_earliest_then_lowest_index():
+    """Winner rule (DESIGN R16): the lowest index among the
+    starts converged at the EARLIEST converging sweep — not the lowest c_train,
+    not the lowest index overall; identical starts tie to the lower index; with
+    no converged start, the minimum c_train, ties to the lower index."""
+    p, a, b = _winner_problem()
+    prm = dict(p.params, max_iter=300, stop_on_first=0)
+    init = np.stack([a, b, b])
+    g, res, win = oracle.instantiate(p.n, p.pairs, p.x, p.y, p.xv, p.yv, init, prm, threads=3)
+    assert all(r["term"] == "CONVERGED" for r in res)
+    # premise: start 0 converges later with the lower cost; 1 and 2 are identical
+    assert res[0]["sweeps"] > res[1]["sweeps"] and res[0]["c_train"] < res[1]["c_train"]
+    assert res[1] == res[2] and np.array_equal(g[1], g[2])
+    assert win == 1
+    # stop_on_first: the others are STOPPED at the winner's sweep, the winner is the same
+    g2, r2, w2 = oracle.instantiate(p.n, p.pairs, p.x, p.y, p.xv, p.yv, init, dict(prm, stop_on_first=1))
+    assert w2 == 1 and r2[0]["term"] == "STOPPED" and r2[2]["term"] == "CONVERGED"
+    assert r2[0]["sweeps"] == r2[1]["sweeps"] == res[1]["sweeps"]
+    # nobody converged: minimum c_train, ties to the lower index
+    init3 = np.stack([p.init[5], b, b, a])
+    g3, r3, w3 = oracle.instantiate(p.n, p.pairs, p.x, p.y, p.xv, p.yv, init3, dict(prm, max_iter=4), threads=4)
+    assert all(r["term"] == "MAX_ITER" for r in r3)
+    cs = [r["c_train"] for r in r3]
+    assert cs[1] == cs[2] < min(cs[0], cs[3]) and w3 == 1
