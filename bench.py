@@ -1,7 +1,12 @@
 #!/usr/bin/env python
 """QFactor-Sample instantiation benchmark on B200 (one JSON line on rank 0).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--shard multistart|sample]
+                    [--impl reference]
+
+--gpus N (N > 1) outside torchrun re-executes this script under
+torch.distributed.run with N processes, one per GPU (NCCL_DEBUG=INFO on
+stderr); under torchrun WORLD_SIZE must equal N.
 
 Workload: BASELINE.json config C4 — n = 12 qubits, K = 150
 two-qubit blocks (brick wall + seeded random non-adjacent pairs), M = 32
@@ -13,8 +18,12 @@ validation forward, and the host controller's decision — i.e. one iteration
 of qfs_instantiate with its stopping rules unable to fire.
 
 value  = start-sweeps per second, whole job (sum over ranks / max-over-ranks
-         device time).  Multi-GPU: multistarts sharded across ranks (weak
-         scaling, no data-path collective).
+         device time).  Multi-GPU, --shard multistart (default): S starts per
+         rank (weak scaling, no data-path collective).  --shard sample
+         (default config C5, BASELINE.json configs[4]): ONE job's S starts, the
+         pool and validation rows m = rank (mod N) on each rank, per-gate NCCL
+         all-reduce of the 4x4 environments inside libqfs (qfs_create_nccl
+         mode 1; strong scaling).
 e2e    = the same metric through the public API from host buffers: every step
          the step's samples are copied from pinned host memory
          (qfs_set_samples_async, queued one step ahead so the copy overlaps the
@@ -153,19 +162,56 @@ def host_cores():
         return os.cpu_count() or 1
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def torchrun_cmd(nproc: int, port: int, argv: list) -> list:
+    """The launch the driver uses (one process per GPU, rendezvous on 127.0.0.1)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *argv]
+
+
+def maybe_relaunch(gpus: int, argv: list):
+    """--gpus N > 1 without a torchrun environment: re-exec under torchrun with N
+    ranks and return its exit code (None: run in this process)."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is not None:
+        if int(ws) != gpus and gpus > 1:
+            raise SystemExit(f"bench.py: --gpus {gpus} but WORLD_SIZE={ws}")
+        return None
+    if gpus <= 1:
+        return None
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")              # NCCL init lines (transport, NVLS) ...
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # ... on stderr: stdout keeps the one JSON line
+    return subprocess.call(torchrun_cmd(gpus, free_port(), argv), env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c4")
-    ap.add_argument("--starts", type=int, default=None, help="multistarts per GPU (default: config S)")
+    ap.add_argument("--config", default=None, help="c1..c5, c5b, c5c (default c4; c5 with --shard sample)")
+    ap.add_argument("--shard", default="multistart", choices=["multistart", "sample"])
+    ap.add_argument("--starts", type=int, default=None,
+                    help="multistarts per GPU (default: config S); with --shard sample: starts of the job")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tts", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    rc = maybe_relaunch(args.gpus, sys.argv[1:])
+    if rc is not None:
+        sys.exit(rc)
+    sample = args.shard == "sample"
+    if args.config is None:
+        args.config = "c5" if sample else "c4"
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -174,13 +220,20 @@ def main():
     from paper_2405_12866_b200 import inputs as I
     cfgd = I.CONFIGS[args.config]
     s_per = args.starts or cfgd["s"]
+    # sample mode: one job of s_per starts whose rows are split over the ranks
+    s_tot = s_per if sample else s_per * world
+    m_loc = cfgd["m_init"] // world if sample else cfgd["m_init"]
+    if sample and (cfgd["m_init"] % world or cfgd["v"] % world):
+        raise SystemExit(f"--shard sample: M={cfgd['m_init']} and V={cfgd['v']} must be divisible by {world}")
     config = {"workload": f"{args.config.upper()}: n={cfgd['n']} K={cfgd['k']} M={cfgd['m_init']} "
-                          f"V={cfgd['v']} S={s_per}/GPU complex128 (BASELINE.json configs[{cfgd['cfg'] - 1}])",
+                          f"V={cfgd['v']} S={s_per}{'' if sample else '/GPU'} complex128 "
+                          f"(BASELINE.json configs[{min(cfgd['cfg'], 5) - 1}])",
               "n": cfgd["n"], "k": cfgd["k"], "m": cfgd["m_init"], "v": cfgd["v"],
-              "starts_per_gpu": s_per, "starts_total": s_per * world,
-              "parallelism": f"multistart x{world}",
+              "starts_per_gpu": s_per if not sample else s_per, "starts_total": s_tot,
+              "parallelism": (f"sample x{world} (M/rank={m_loc}, NCCL all-reduce of E per gate)" if sample
+                              else f"multistart x{world}"),
               "l2": "inputs larger than L2 (B cache %.1f GB/GPU > 126 MB)" % (
-                  (cfgd["k"] - 1) * s_per * cfgd["m_init"] * (16 << cfgd["n"]) / 1e9)}
+                  (cfgd["k"] - 1) * s_per * m_loc * (16 << cfgd["n"]) / 1e9)}
 
     if args.impl == "reference":
         # the reference arm is the CPU oracle (no reference code exists for this paper)
@@ -220,12 +273,25 @@ def main():
         else:
             dist.init_process_group(pg)
 
-    # seeded synthetic problem; starts of rank r are [r*S, (r+1)*S) of the seeded stream
-    prob = I.make_problem(args.config, init="R", s=s_per * world)
-    init = np.ascontiguousarray(prob.init[rank * s_per:(rank + 1) * s_per])
-    m = cfgd["m_init"]
-    ctx = qfs.Context(prob.n, prob.pairs, device=local)
-    ctx.set_samples(prob.x, prob.y, prob.xv, prob.yv)
+    # seeded synthetic problem; multistart: starts of rank r are [r*S, (r+1)*S)
+    # of the seeded stream; sample: every rank runs all S starts on its rows
+    prob = I.make_problem(args.config, init="R", s=s_tot)
+    init = np.ascontiguousarray(prob.init if sample else prob.init[rank * s_per:(rank + 1) * s_per])
+    m = cfgd["m_init"]                      # global M (qfs_instantiate's m_init is global in sample mode)
+    from paper_2405_12866_b200 import parallel as PL
+    rows = PL.sample_rows(prob.x.shape[0], rank, world) if sample else slice(None)
+    vrows = PL.sample_rows(prob.xv.shape[0], rank, world) if sample else slice(None)
+    lx, ly = np.ascontiguousarray(prob.x[rows]), np.ascontiguousarray(prob.y[rows])
+    lxv, lyv = np.ascontiguousarray(prob.xv[vrows]), np.ascontiguousarray(prob.yv[vrows])
+    if sample:
+        # the library owns the NCCL communicator: rank 0's unique id, broadcast over torch.distributed
+        obj = [qfs.nccl_unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0)
+        ctx = qfs.Context(prob.n, prob.pairs, device=local, nccl_id=obj[0], rank=rank, world=world, shard_mode=1)
+    else:
+        ctx = qfs.Context(prob.n, prob.pairs, device=local)
+    ctx.set_samples(lx, ly, lxv, lyv)
     stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=local)
 
     def barrier():
@@ -259,7 +325,7 @@ def main():
     barrier()
     launches = ctx.launch_count() - l0
     dt = max_over_ranks(ev0.elapsed_time(ev1) / 1e3)
-    value = s_per * world * args.steps / dt
+    value = s_tot * args.steps / dt
     assert all(r["sweeps"] == args.steps for r in res), res
 
     # ---- per-kernel CUDA-event durations: the same K steps again with one event
@@ -324,10 +390,10 @@ def main():
 
     # ---- e2e: through the public API from pinned host buffers, copies in the timed region
     N = 1 << prob.n
-    hx = torch.from_numpy(prob.x).pin_memory()
-    hy = torch.from_numpy(prob.y).pin_memory()
-    hxv = torch.from_numpy(prob.xv).pin_memory()
-    hyv = torch.from_numpy(prob.yv).pin_memory()
+    hx = torch.from_numpy(lx).pin_memory()
+    hy = torch.from_numpy(ly).pin_memory()
+    hxv = torch.from_numpy(lxv).pin_memory()
+    hyv = torch.from_numpy(lyv).pin_memory()
     h2d = (hx.numel() + hy.numel() + hxv.numel() + hyv.numel()) * 16 + init.nbytes
     d2h = init.nbytes + s_per * 32
     g = gates
@@ -349,15 +415,16 @@ def main():
         g, _, _ = ctx.instantiate(g, bench_params(1, m))
     barrier()
     e2e_dt = max_over_ranks(time.perf_counter() - t0)
-    e2e = {"value": s_per * world * e2e_steps / e2e_dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-           "d2h_bytes_per_step": int(d2h), "steps": e2e_steps}
+    e2e = {"value": s_tot * e2e_steps / e2e_dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
+           "note": "bytes per rank" if world > 1 else "single GPU"}
 
     # ---- time to solution (rank 0): warm-start instance of the same config, real stopping rules
     tts = None
-    if rank == 0 and not args.no_tts:
+    if (rank == 0 or sample) and not args.no_tts:   # sample mode: a collective call on every rank
         pw = I.make_problem(args.config, init="W", s=s_per)
         prm = dict(pw.params, max_iter=300)
-        ctx.set_samples(pw.x, pw.y, pw.xv, pw.yv)
+        ctx.set_samples(pw.x[rows], pw.y[rows], pw.xv[vrows], pw.yv[vrows])
         # one warm-up call (allocations and graph shapes of the
         # restarts), then the median of 3 timed calls
         ctx.instantiate(pw.init, prm)
@@ -365,7 +432,7 @@ def main():
         for _ in range(3):
             t0 = time.perf_counter()
             gw, rw, ww = ctx.instantiate(pw.init, prm)
-            times.append(time.perf_counter() - t0)
+            times.append(max_over_ranks(time.perf_counter() - t0) if sample else time.perf_counter() - t0)
         tsec = statistics.median(times)
         tts = {"seconds": round(tsec, 4), "seconds_runs": [round(t, 4) for t in times],
                "sweeps": rw[ww]["sweeps"], "term": rw[ww]["term"],
@@ -391,7 +458,7 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "scaling": "strong" if sample else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": config, "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline,
                 "cpu_baseline": cpu, "clocks": clk.summary(), "time_to_solution": tts,
                 "amp_gate_updates_per_s": value * m * N * prob.k}

@@ -56,6 +56,7 @@ struct BwdParams {
   double *gpartials;          // [S_act][40][32] group sums
   double *e_red;              // [S_act][32]: reduced E (sample mode: before all-reduce)
   int fuse_polar;             // 1: the last CTA of each start runs the polar update
+  int bulk;                   // 1: bwdt_kernel (bulk copies + mbarrier ring), 0: bwd_kernel (LDGSTS)
   double beta;
   double *sig;                // [S][K] sum sigma, or nullptr
   double2 *env_trace;         // [K][S][16] for this sweep, or nullptr
@@ -191,6 +192,8 @@ cudaError_t launch_val_block(const ValRowParams &p, int n_slots, cudaStream_t st
 size_t val_cl_smem(int n, int K, int t);      // cluster validation, 2^t CTAs per row
 cudaError_t launch_val_cluster(const ValRowParams &p, int n_slots, cudaStream_t st);        // largest n the shared-memory validation forward supports
 int blocks_per_sm(int nu);  // resident CTAs per SM of the backward kernel
+size_t bt_smem_bytes(int nu);     // dynamic shared memory of the bulk-copy backward kernel
+int bwdt_units_per_cta_min();     // fewest stages a bulk-copy backward CTA is given
 
 
 // ---------------------------------------------------- multi-qubit blocks --

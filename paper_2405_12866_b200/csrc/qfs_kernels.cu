@@ -111,6 +111,20 @@ __device__ __forceinline__ int pidx(int v) {
   return ((v >> TP0) & 1) | (((v >> TP1) & 1) << 1);
 }
 
+// local index of member l of quadruple q for the pair at local bits (TP0, TP1)
+// (the other local bits, ascending, take the bits of q)
+template <int NU, int TP0, int TP1>
+__host__ __device__ constexpr int pv_idx(int q, int l) {
+  int v = ((l & 1) << TP0) | (((l >> 1) & 1) << TP1);
+  int bit = 0;
+  for (int t = 0; t < NU; ++t) {
+    if (t == TP0 || t == TP1) continue;
+    v |= ((q >> bit) & 1) << t;
+    ++bit;
+  }
+  return v;
+}
+
 struct BwdShared {
   double2 sQ[16];                          // G_{i+1}^dag
   double2 red[BWD_THREADS / 32][4][16];    // per-warp (per lane-group) E partials
@@ -416,10 +430,25 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
   return true;
 }
 
+// Warp 0 of the finishing CTA holds the reduced E (lane = re/im of entry lane/2):
+// store it and (fuse_polar) run the gate update (kind: loaded before the
+// election so its global load is off the critical path).
+template <class SH>  // shared-memory struct with sum32[32] and scratch[64]
+__device__ void bwd_finish_e(const BwdParams &P, const GateDesc &G, int jslot, int s, SH &sh, double e, int kind) {
+  sh.sum32[threadIdx.x] = e;
+  if (!P.fuse_polar) P.e_red[(long long)jslot * 32 + threadIdx.x] = e;
+  __syncwarp();
+  if (P.dbg && threadIdx.x == 0) atomicMax(P.dbg + 4 * G.env_gate + 2, gtimer());
+  if (!P.fuse_polar) return;
+  const long long gi = (long long)s * P.K + G.env_gate;
+  polar_write(sh.sum32, P.gates_w + gi * 16, P.vprev ? P.vprev + gi * 16 : nullptr, P.beta,
+              kind, P.sig ? P.sig + gi : nullptr,
+              P.env_trace ? P.env_trace + ((long long)G.env_gate * P.S + s) * 16 : nullptr, sh.scratch);
+  if (P.dbg && threadIdx.x == 0) atomicMax(P.dbg + 4 * G.env_gate + 3, gtimer());
+}
+
 // Warp 0 of the last CTA of a start: sum the CTA partials in CTA order, and
 // (fuse_polar) run the polar update of gate i.
-__device__ void bwd_finish_e(const BwdParams &P, const GateDesc &G, int jslot, int s, BwdShared &sh, double e,
-                             int kind);
 __device__ void bwd_finish(const BwdParams &P, const GateDesc &G, int jslot, int s, BwdShared &sh, int kind) {
   if (P.dbg && threadIdx.x == 0) atomicMax(P.dbg + 4 * G.env_gate + 1, gtimer());
   const double *pp = P.partials + (long long)jslot * P.nb * 32 + threadIdx.x;
@@ -438,22 +467,6 @@ __device__ void bwd_finish(const BwdParams &P, const GateDesc &G, int jslot, int
   bwd_finish_e(P, G, jslot, s, sh, e, kind);
 }
 
-// Warp 0 of the finishing CTA holds the reduced E (lane = re/im of entry lane/2):
-// store it and (fuse_polar) run the gate update (kind: loaded before the
-// election so its global load is off the critical path).
-__device__ void bwd_finish_e(const BwdParams &P, const GateDesc &G, int jslot, int s, BwdShared &sh, double e,
-                             int kind) {
-  sh.sum32[threadIdx.x] = e;
-  if (!P.fuse_polar) P.e_red[(long long)jslot * 32 + threadIdx.x] = e;
-  __syncwarp();
-  if (P.dbg && threadIdx.x == 0) atomicMax(P.dbg + 4 * G.env_gate + 2, gtimer());
-  if (!P.fuse_polar) return;
-  const long long gi = (long long)s * P.K + G.env_gate;
-  polar_write(sh.sum32, P.gates_w + gi * 16, P.vprev ? P.vprev + gi * 16 : nullptr, P.beta,
-              kind, P.sig ? P.sig + gi : nullptr,
-              P.env_trace ? P.env_trace + ((long long)G.env_gate * P.S + s) * 16 : nullptr, sh.scratch);
-  if (P.dbg && threadIdx.x == 0) atomicMax(P.dbg + 4 * G.env_gate + 3, gtimer());
-}
 
 // One launch per gate (used in sample-sharded mode and by the unit op).
 // WIDE (many CTAs per start, e.g. S = 1): the last CTA to finish sums all CTA
@@ -543,6 +556,304 @@ __global__ void __launch_bounds__(BWD_THREADS, QFS_BWD_MINB) bwd_kernel(const Bw
 }
 
 
+// ------------------------------------------------- backward, bulk-copy path --
+// bwdt_kernel: the same fused step as bwd_kernel (chi <- G_{i+1}^dag chi, E_i,
+// last-CTA ordered reduction + polar update of gate i; P:112, P:121-125,
+// P:172, eq:opt_u P:59-62), with the tiles moved by the copy engine instead of
+// per-thread LDGSTS (B200: cp.async.bulk -> SASS UBLKCP, mbarrier -> SYNCS).
+//
+// Work unit ("stage") = one amplitude group of 2^NU rows (the union of gate
+// i's and gate i+1's qubits; local bits 0,1 = gate i+1's pair, the rest gate
+// i's other bits ascending) x a block of up to 32 consecutive samples.  In the
+// sample-minor layout every (row, sample block) is ONE contiguous run of
+// Mr * 16 bytes (512 B at M = 32, two runs at M = 64), so a stage is 2 * 2^NU
+// bulk copies (chi rows and phi = B_i rows) issued by one producer warp into a
+// ring of BT_STAGES shared-memory stages, each guarded by a full / empty
+// mbarrier pair.  Consumer warp w takes stages w, w + BT_CW, ...: lane = one
+// sample, all 2^NU amplitudes of it in registers, so the chi update and all 16
+// entries of E are lane-local (no transposes, no shuffles in the loop; 16
+// independent accumulators of ILP), and the only per-stage integer work is one
+// bit insertion.  Addresses are 64-bit (no 4 GiB block limit).  phi does not
+// depend on the previous launch: with G.pre the producer issues the first
+// stages' phi copies before griddepcontrol.wait (PDL), and it prefetches phi
+// rows BT_PF stages ahead into L2 (cp.async.bulk.prefetch.L2) so each ring
+// slot waits on L2 latency, not DRAM latency.
+#ifndef QFS_BT_WARPS
+#define QFS_BT_WARPS 7   // 7 + 1 producer = 256 threads: up to 255 registers (8 consumers cap at 168 and spill)
+#endif
+#ifndef QFS_BT_STAGES
+#define QFS_BT_STAGES 12
+#endif
+#ifndef QFS_BT_PF
+#define QFS_BT_PF 8       // phi rows prefetched into L2 this many stages ahead (0: off)
+#endif
+#ifndef QFS_BT_HINT
+#define QFS_BT_HINT 1     // bit 0: phi (B_i, read once) copies L2::evict_first
+#endif
+constexpr int BT_CW = QFS_BT_WARPS;           // consumer warps
+constexpr int BT_STAGES = QFS_BT_STAGES;
+constexpr int BT_THREADS = (BT_CW + 1) * 32;  // + one producer warp
+constexpr int BT_SROW = 32;                   // samples per stage row (one per lane)
+
+struct BtShared {
+  uint64_t full[BT_STAGES], empty[BT_STAGES];
+  double2 red[BT_CW][16];
+  double wsum[(BT_CW + 1) * 32];  // WIDE reduction: per-warp sums of CTA partials
+  double sum32[32];
+  double2 scratch[64];
+  unsigned last_cta;
+};
+
+}  // namespace
+size_t bt_smem_bytes(int nu) { return (size_t)BT_STAGES * 2 * (1 << nu) * BT_SROW * sizeof(double2); }
+namespace {
+
+template <int NU, int TP0, int TP1, bool UPD, bool WIDE>
+__global__ void __launch_bounds__(BT_THREADS, 1) bwdt_kernel(const BwdParams P) {
+  constexpr int NV = 1 << NU;
+  constexpr int NQ = NV / 4;
+  constexpr int STAGE = 2 * NV * BT_SROW;  // double2 per stage: [chi|phi][v][lane]
+  __shared__ BtShared sh;
+  extern __shared__ __align__(128) double2 ring[];
+  const GateDesc &G = P.g;
+  const int jslot = blockIdx.y;
+  const Slot sl = P.slots[jslot];
+  const int s = sl.s;
+  const unsigned Ms = (unsigned)sl.m;
+  const unsigned nmb = (Ms + BT_SROW - 1) / BT_SROW;
+  const unsigned units = (1u << (P.n - NU)) * nmb;
+  const unsigned chunk = (units + P.nb - 1) / P.nb;
+  const unsigned beg = min(units, blockIdx.x * chunk), end = min(units, beg + chunk);
+  const int nitems = (int)(end - beg);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const FastDiv fdu(nmb);
+  uint32_t ins[NU];
+#pragma unroll
+  for (int q = 0; q < NU; ++q) ins[q] = G.ins[q];
+  // first amplitude of the group and first sample of item k
+  auto item = [&](int k, unsigned &g, unsigned &m0) {
+    const unsigned u = beg + (unsigned)k;
+    g = fdu.div(u);
+    m0 = (u - g * nmb) * BT_SROW;
+#pragma unroll
+    for (int q = 0; q < NU; ++q) g = insert_zero32(g, ins[q]);
+  };
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < BT_STAGES; ++q) {
+      mbar_init(&sh.full[q], 1);
+      mbar_init(&sh.empty[q], 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp == BT_CW) {
+    // ------------------------------------------------------------ producer
+    const double2 *csrc = G.chi_src.base + (long long)s * G.chi_src.ss;
+    const double2 *fsrc = G.phi.base + (long long)s * G.phi.ss;
+    const long long csa = G.chi_src.sa, fsa = G.phi.sa;
+#if QFS_BT_HINT & 1
+    const uint64_t pol_f = policy_evict_first();
+#endif
+    // lane l < NV copies chi row l, NV <= l < 2 NV phi row l - NV
+    const bool is_phi = lane >= NV;
+    const int v = lane & (NV - 1);
+    const long long offv = G.off[v];
+    auto issue = [&](int k, bool chi, bool phi) {
+      unsigned g, m0;
+      item(k, g, m0);
+      const unsigned mr = min((unsigned)BT_SROW, Ms - m0);
+      double2 *dst = ring + (k % BT_STAGES) * STAGE + (is_phi ? NV * BT_SROW : 0) + v * BT_SROW;
+      if (lane < 2 * NV && (is_phi ? phi : chi)) {
+        if (is_phi) {
+          const double2 *src = fsrc + ((long long)g + offv) * fsa + m0;
+#if QFS_BT_HINT & 1
+          bulk_g2s_hint(dst, src, mr * 16u, &sh.full[k % BT_STAGES], pol_f);
+#else
+          bulk_g2s(dst, src, mr * 16u, &sh.full[k % BT_STAGES]);
+#endif
+        } else {
+          bulk_g2s(dst, csrc + ((long long)g + offv) * csa + m0, mr * 16u, &sh.full[k % BT_STAGES]);
+        }
+      }
+    };
+    auto arm = [&](int k) {  // expect the stage's bytes (chi and phi rows)
+      if (lane == 0) {
+        unsigned g, m0;
+        item(k, g, m0);
+        mbar_arrive_tx(&sh.full[k % BT_STAGES], 2u * NV * min((unsigned)BT_SROW, Ms - m0) * 16u);
+      }
+      __syncwarp();
+    };
+    auto prefetch = [&](int k) {
+#if QFS_BT_PF
+      if (k < nitems && is_phi && lane < 2 * NV) {
+        unsigned g, m0;
+        item(k, g, m0);
+        bulk_prefetch_l2(fsrc + ((long long)g + offv) * fsa + m0, min((unsigned)BT_SROW, Ms - m0) * 16u);
+      }
+#endif
+    };
+    const int npre = min(nitems, BT_STAGES);
+    if (G.pre) {  // phi of the first stages before the dependence on the previous launch
+      for (int k = 0; k < npre; ++k) {
+        arm(k);
+        issue(k, false, true);
+      }
+      for (int k = npre; k < npre + QFS_BT_PF; ++k) prefetch(k);
+    }
+    pdl_wait();
+    for (int k = 0; k < npre; ++k) {
+      if (!G.pre) arm(k);
+      issue(k, true, !G.pre);
+    }
+    if (!G.pre)
+      for (int k = npre; k < npre + QFS_BT_PF; ++k) prefetch(k);
+    for (int k = npre; k < nitems; ++k) {
+      prefetch(k + QFS_BT_PF);
+      mbar_wait(&sh.empty[k % BT_STAGES], ((k / BT_STAGES) - 1) & 1);
+      arm(k);
+      issue(k, true, true);
+    }
+  } else {
+    // ------------------------------------------------------------ consumers
+    pdl_wait();  // G_{i+1} was written by the previous launch's polar update
+    double2 Q[16];
+    if (UPD) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)  // (G^dag)[a][b] = conj(G[b][a])
+          Q[4 * a + b] = cconj(__ldcg(P.gates + ((long long)s * P.K + G.upd_gate) * 16 + 4 * b + a));
+    }
+    double2 *cdst = G.chi_dst.base ? G.chi_dst.base + (long long)s * G.chi_dst.ss : nullptr;
+    const long long dsa = G.chi_dst.sa;
+    double2 acc[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) acc[e] = make_double2(0.0, 0.0);
+    for (int k = warp; k < nitems; k += BT_CW) {
+      unsigned g, m0;
+      item(k, g, m0);
+      const bool valid = m0 + lane < Ms;
+      mbar_wait(&sh.full[k % BT_STAGES], (k / BT_STAGES) & 1);
+      const double2 *sc = ring + (k % BT_STAGES) * STAGE + lane;
+      double2 c[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) c[v] = valid ? sc[v * BT_SROW] : make_double2(0.0, 0.0);
+      if (UPD) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          double2 o[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            o[a] = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int b = 0; b < 4; ++b) cfma(o[a], Q[4 * a + b], c[4 * q + b]);
+          }
+#pragma unroll
+          for (int a = 0; a < 4; ++a) c[4 * q + a] = o[a];
+        }
+        if (cdst && valid) {
+          double2 *dp = cdst + (long long)g * dsa + m0 + lane;
+#pragma unroll
+          for (int v = 0; v < NV; ++v) dp[G.off[v] * dsa] = c[v];
+        }
+      }
+      // E[l_in][l_out] += phi[v(p, l_in)] conj(chi'[v(p, l_out)]) over the P-quadruples p
+#pragma unroll
+      for (int p = 0; p < NQ; ++p) {
+        double2 f[4];
+#pragma unroll
+        for (int l = 0; l < 4; ++l)
+          f[l] = valid ? sc[(NV + pv_idx<NU, TP0, TP1>(p, l)) * BT_SROW] : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const double2 cb = c[pv_idx<NU, TP0, TP1>(p, b)];
+            double2 &e = acc[4 * a + b];
+            e.x = fma(f[a].x, cb.x, e.x);
+            e.x = fma(f[a].y, cb.y, e.x);
+            e.y = fma(f[a].y, cb.x, e.y);
+            e.y = fma(-f[a].x, cb.y, e.y);
+          }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.empty[k % BT_STAGES]);
+    }
+    // warp sum over the 32 samples (fixed butterfly order)
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        acc[e].x += __shfl_xor_sync(FULL, acc[e].x, o);
+        acc[e].y += __shfl_xor_sync(FULL, acc[e].y, o);
+      }
+    }
+    if (lane < 16) {
+      double2 w = acc[0];
+#pragma unroll
+      for (int e = 1; e < 16; ++e)
+        if (lane == e) w = acc[e];
+      sh.red[warp][lane] = w;
+    }
+  }
+  pdl_trigger();
+  __syncthreads();
+  // CTA partial: consumer warps in order (warp 0, lane = re / im of entry lane / 2)
+  if (warp == 0) {
+    const int e = lane >> 1, im = lane & 1;
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < BT_CW; ++w) v += im ? sh.red[w][e].y : sh.red[w][e].x;
+    P.partials[((long long)jslot * P.nb + blockIdx.x) * 32 + lane] = v;
+  }
+  const int kind = P.kinds ? __ldg(P.kinds + G.env_gate) : 0;
+  if constexpr (WIDE) {
+    constexpr int NW = BT_CW + 1, FL = 24;
+    if (warp == 0) {
+      const bool last = warp0_elect_last(&P.counters[jslot], (unsigned)P.nb);
+      if (lane == 0) sh.last_cta = last ? 1u : 0u;
+    }
+    __syncthreads();
+    if (!sh.last_cta) return;
+    const int per = (P.nb + NW - 1) / NW, c0 = warp * per, c1 = min(P.nb, c0 + per);
+    const double *pp = P.partials + (long long)jslot * P.nb * 32 + lane;
+    double e = 0.0;
+    for (int b0 = c0; b0 < c1; b0 += FL) {
+      double xb[FL];
+#pragma unroll
+      for (int q = 0; q < FL; ++q) xb[q] = b0 + q < c1 ? __ldcg(pp + (long long)(b0 + q) * 32) : 0.0;
+#pragma unroll
+      for (int q = 0; q < FL; ++q)
+        if (b0 + q < c1) e += xb[q];
+    }
+    double *ws = sh.wsum;
+    ws[warp * 32 + lane] = e;
+    __syncthreads();
+    if (warp != 0) return;
+    e = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) e += ws[w * 32 + lane];
+    bwd_finish_e(P, G, jslot, s, sh, e, kind);
+  } else {
+    if (warp != 0) return;
+    if (!warp0_elect_last(&P.counters[jslot], (unsigned)P.nb)) return;
+    const double *pp = P.partials + (long long)jslot * P.nb * 32 + lane;
+    double e = 0.0;
+    constexpr int FLIGHT = 16;
+    for (int b0 = 0; b0 < P.nb; b0 += FLIGHT) {
+      double xb[FLIGHT];
+#pragma unroll
+      for (int q = 0; q < FLIGHT; ++q) xb[q] = b0 + q < P.nb ? __ldcg(pp + (long long)(b0 + q) * 32) : 0.0;
+#pragma unroll
+      for (int q = 0; q < FLIGHT; ++q)
+        if (b0 + q < P.nb) e += xb[q];
+    }
+    bwd_finish_e(P, G, jslot, s, sh, e, kind);
+  }
+}
+
 // polar step alone (sample-sharded mode, after the NCCL all-reduce of E): one warp per start
 __global__ void polar_kernel(const PolarParams P) {
   __shared__ double e32[4][32];
@@ -624,19 +935,6 @@ __global__ void __launch_bounds__(RED_THREADS, 4) final_kernel(const FinalParams
   }
 }
 
-// local index of member l of quadruple q for the pair at local bits (TP0, TP1)
-// (the other local bits, ascending, take the bits of q)
-template <int NU, int TP0, int TP1>
-__host__ __device__ constexpr int pv_idx(int q, int l) {
-  int v = ((l & 1) << TP0) | (((l >> 1) & 1) << TP1);
-  int bit = 0;
-  for (int t = 0; t < NU; ++t) {
-    if (t == TP0 || t == TP1) continue;
-    v |= ((q >> bit) & 1) << t;
-    ++bit;
-  }
-  return v;
-}
 
 // ------------------------------------------------------ forward (per gate) --
 // B_{k+1} = G_k B_k for every (quadruple, sample) of every active start.
@@ -1111,7 +1409,49 @@ bool pdl_enabled() { return g_pdl; }
 int val_row_max_n() { return 13; }
 int blocks_per_sm(int nu) { (void)nu; return QFS_BWD_MINB; }
 
+cudaError_t launch_bwdt(const BwdParams &p, int n_slots, cudaStream_t st) {
+  dim3 grid(p.nb, n_slots), block(BT_THREADS);
+  const GateDesc &g = p.g;
+  const int smem = (int)bt_smem_bytes(g.nu);
+  const bool wide = p.nb > RED_GS;
+#define QFS_BT1(NU, A, B, U, W)                                                                  \
+  do {                                                                                           \
+    static bool attr = false;                                                                    \
+    if (!attr) {                                                                                 \
+      cudaFuncSetAttribute(bwdt_kernel<NU, A, B, U, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           (int)bt_smem_bytes(4));                                               \
+      attr = true;                                                                               \
+    }                                                                                            \
+    launch_ex(bwdt_kernel<NU, A, B, U, W>, grid, block, smem, st, p);                            \
+  } while (0)
+#define QFS_BT(NU, A, B, U)              \
+  do {                                   \
+    if (wide) QFS_BT1(NU, A, B, U, true); \
+    else QFS_BT1(NU, A, B, U, false);    \
+  } while (0)
+  if (!g.upd) {
+    QFS_BT(2, 0, 1, false);
+  } else if (g.nu == 2) {
+    if (g.tp0 == 0) QFS_BT(2, 0, 1, true);
+    else QFS_BT(2, 1, 0, true);
+  } else if (g.nu == 3) {
+    if (g.tp0 == 0 && g.tp1 == 2) QFS_BT(3, 0, 2, true);
+    else if (g.tp0 == 2 && g.tp1 == 0) QFS_BT(3, 2, 0, true);
+    else if (g.tp0 == 1 && g.tp1 == 2) QFS_BT(3, 1, 2, true);
+    else QFS_BT(3, 2, 1, true);
+  } else {
+    if (g.tp0 == 2) QFS_BT(4, 2, 3, true);
+    else QFS_BT(4, 3, 2, true);
+  }
+#undef QFS_BT
+#undef QFS_BT1
+  return cudaGetLastError();
+}
+
+int bwdt_units_per_cta_min() { return 4; }
+
 cudaError_t launch_bwd(const BwdParams &p, int n_slots, cudaStream_t st) {
+  if (p.bulk) return launch_bwdt(p, n_slots, st);
   dim3 grid(p.nb, n_slots), block(BWD_THREADS);
   const int smem = BWD_STAGES * 8 * BWD_THREADS * (int)sizeof(double2);
   const GateDesc &g = p.g;

@@ -78,6 +78,8 @@ struct qfs_ctx {
   int K_g = 0;      // gates d_gates / d_vprev were sized for (ensure_gates)
   int K_s = 0;      // gates d_B / d_sig were sized for (ensure_state)
   bool force_unfused = false;  // QFS_UNFUSED_POLAR=1: separate polar launch (sample-mode code path at world 1)
+  bool bwd_bulk = true;        // QFS_BWD_BULK=0: LDGSTS backward kernel instead of the bulk-copy one
+  int bulk_min_m = 16;         // QFS_BULK_MIN_M: smallest M_max that takes the bulk-copy backward
   int V_glob = 0;   // validation rows over all ranks (sample mode: sum of the ranks' V)
   double2 *d_vprev = nullptr;  // [S][K][16] right singular vectors of the last polar step (warm start)
   double2 *d_gates = nullptr, *d_chi = nullptr, *d_B = nullptr, *d_vb0 = nullptr, *d_vb1 = nullptr;
@@ -219,9 +221,11 @@ struct LaunchScope {
   LaunchScope(qfs_ctx *c_, int cls_, double b, double f) : c(c_), cls(cls_), bytes(b), flops(f) {
     c->launches++;
     if (c->phase) {
+      // a phase's launch count is its own kernel class (sample mode: the
+      // all-reduce and polar launches inside the backward phase add time, not launches)
       c->phase->bytes += b;
       c->phase->flops += f;
-      c->phase->n += 1;
+      if (cls != K_NCCL && cls != K_POLAR) c->phase->n += 1;
     } else if (c->prof) {
       e0 = take_event(c);
       record_event(c, e0);
@@ -686,7 +690,14 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
     b.g = make_desc(c, i);
     const bool upd = b.g.upd != 0;
     const int nu = b.g.nu;
-    {
+    b.bulk = c->bwd_bulk && M_max >= c->bulk_min_m;
+    if (b.bulk) {
+      // one CTA per SM over all starts (the ring of stages fills the SM's shared memory)
+      const long long un = (N >> nu) * ((M_max + 31) / 32);
+      long long nb = std::max(1, 148 / ns);
+      nb = std::min(nb, std::max(1LL, un / bwdt_units_per_cta_min()));
+      b.nb = (int)nb;
+    } else {
       const long long lpt = 32 >> (nu - 2);
       const long long un = (N >> nu) * ((M_max + lpt - 1) / lpt);
       b.nb = blocks_per_start(un * 32, ns, blocks_per_sm(nu));
@@ -970,6 +981,8 @@ qfs_status create_common(int n, int k, const int32_t *pairs, int device, qfs_ctx
   if (const char *rc = getenv("QFS_RES_CMAX")) c->res_cmax = std::max(1, std::min(16, atoi(rc)));
   if (const char *rp = getenv("QFS_RES_PER_SM")) c->res_per_sm = atoi(rp) == 2 ? 2 : 1;
   if (const char *uf = getenv("QFS_UNFUSED_POLAR")) c->force_unfused = atoi(uf) != 0;
+  if (const char *bb = getenv("QFS_BWD_BULK")) c->bwd_bulk = atoi(bb) != 0;
+  if (const char *bm = getenv("QFS_BULK_MIN_M")) c->bulk_min_m = std::max(1, atoi(bm));
   if (e != cudaSuccess) {
     c->err = std::string("device init: ") + cudaGetErrorString(e);
     *out = c;  // caller can read the error, then destroy

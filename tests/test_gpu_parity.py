@@ -410,12 +410,15 @@ def test_sample_sharded_path_single_rank(qfs, monkeypatch):
     monkeypatch.setenv("QFS_UNFUSED_POLAR", "1")       # read when the context is created
     ctx = qfs.Context(p.n, p.pairs, nccl_id=nid, rank=0, world=1, shard_mode=1)
     monkeypatch.delenv("QFS_UNFUSED_POLAR")
-    ctx.profile_enable(True)
-    ctx.trace_sweeps(p.init, 32, 1)
-    prof = ctx.profile_read()
-    ctx.profile_enable(False)
-    assert prof["polar"]["launches"] == p.k and prof["nccl_allreduce"]["launches"] >= p.k
     ctx.set_samples(p.x, p.y, p.xv, p.yv)
+    fused = qfs.Context(p.n, p.pairs, nccl_id=qfs.nccl_unique_id(), rank=0, world=1, shard_mode=1)
+    fused.set_samples(p.x, p.y, p.xv, p.yv)
+    l0, f0 = ctx.launch_count(), fused.launch_count()
+    ctx.trace_sweeps(p.init, 32, 1)
+    fused.trace_sweeps(p.init, 32, 1)
+    # per sweep: K polar launches + K all-reduces of E + 1 of the cost sums
+    assert (ctx.launch_count() - l0) - (fused.launch_count() - f0) == 2 * p.k + 1
+    fused.close()
     gt = ctx.trace_sweeps(p.init, 32, 3)
     ot = oracle.trace_sweeps(p.n, p.pairs, p.init, p.x, p.y, 32, 3)
     _compare_traces(gt, ot, "sample-mode")
