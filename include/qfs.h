@@ -118,6 +118,32 @@ qfs_status qfs_set_structure(qfs_ctx *c, int k, const int32_t *pairs);
 qfs_status qfs_create_dist(int n, int k, const int32_t *pairs, int device, void *nccl_comm,
                            int rank, int world, int shard_mode, qfs_ctx **out);
 
+/* Exchange of the partial environments in sample mode (
+ * E is a sum over samples, so the ranks' partials add up):
+ *   0 = host-enqueued ncclAllReduce of E per gate, then a separate polar launch
+ *       (default);
+ *   1 = device-initiated: the last CTA of each start's environment reduction
+ *       stores its partial E into every rank's mailbox (CUDA-IPC-mapped peer
+ *       memory over NVLink), raises an epoch flag there, waits for all ranks'
+ *       flags and sums the partials in rank order, then runs the polar update
+ *       itself — one launch per gate, no host involvement, identical bits on
+ *       all ranks.
+ * Collective in sample mode with world > 1 (the mailboxes are set up with the
+ * context's NCCL communicator at the next call); QFS_ERR_STATE without one,
+ * QFS_ERR_ARG for another value, a block context, or more than 32 ranks. */
+qfs_status qfs_set_exchange(qfs_ctx *c, int mode);
+
+/* Sample mode with `ranks` (2..32) EMULATED ranks on one device, for testing
+ * and measuring the device-initiated exchange where fewer GPUs than ranks
+ * exist: rank r holds pool rows m = r (mod ranks) (the caller passes ALL rows
+ * to set_samples; m_pool divisible by ranks) with its own states and gate
+ * copy; all ranks run in the same launches and exchange E through local
+ * mailboxes with exactly the protocol of qfs_set_exchange(c, 1).  Every rank
+ * evaluates the full validation set.  One start per call (s == 1, else
+ * QFS_ERR_ARG).  Results equal the single-rank sweep up to the summation
+ * order of E. */
+qfs_status qfs_create_emulated(int n, int k, const int32_t *pairs, int device, int ranks, qfs_ctx **out);
+
 /* NCCL bootstrap owned by the library: rank 0 calls qfs_nccl_unique_id
  * (128 opaque bytes), the caller broadcasts them (e.g. torch.distributed), and
  * every rank calls qfs_create_nccl; the context creates and owns the

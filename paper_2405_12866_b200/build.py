@@ -32,10 +32,12 @@ def nccl_dir() -> str:
 LIB_DEBUG = os.path.join(HERE, "libqfs_debug.so")
 
 
-def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, debug: bool = False, out: str | None = None,
+          defines: list | None = None) -> str:
     """Compile libqfs.so (or, with ``debug``, libqfs_debug.so: -DQFS_DEBUG device
-    bounds checks of the streamed kernels' offsets; same ABI)."""
-    lib = LIB_DEBUG if debug else LIB
+    bounds checks of the streamed kernels' offsets; same ABI).  ``out`` /
+    ``defines``: an A/B variant of the same sources (tools/)."""
+    lib = out or (LIB_DEBUG if debug else LIB)
     if not force and os.path.exists(lib):
         t = os.path.getmtime(lib)
         if all(os.path.getmtime(d) <= t for d in DEPS):
@@ -50,7 +52,7 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False) -> st
            f"-I{os.path.join(nd, 'include')}", f"-I{os.path.join(ROOT, 'include')}",
            f"-L{os.path.join(nd, 'lib')}", f"-l:{os.path.basename(sorted(libs)[0])}",
            "-Xlinker", f"-rpath={os.path.join(nd, 'lib')}",
-           *os.environ.get("QFS_NVCC_DEFINES", "").split(), *(["-DQFS_DEBUG"] if debug else []),
+           *os.environ.get("QFS_NVCC_DEFINES", "").split(), *(["-DQFS_DEBUG"] if debug else []), *(defines or []),
            "-o", tmp, *SOURCES]
     r = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
     if r.returncode != 0:

@@ -28,6 +28,20 @@ struct ViewW {
   long long ss, sa, sm;
 };
 
+// Layout-permuted, sample-blocked state arrays ("perm mode"):
+// a start's block holds M_cap / sb sample blocks of [2^n rows][sb samples]
+// (elements per block: blk = 2^n sb); in the layout L_i of gate i the
+// physical row of natural amplitude a is pi_i(a), with the union bits of
+// gates i and i+1 at rows' lowest bits, so the 2^nu rows of one environment
+// group are ONE contiguous run of 2^nu * sb * 16 bytes (a single bulk copy).
+// A group index G (the source layout's other bits, ascending) and local index
+// v map to the destination row  sum_j bit_j(G) << dpos[j]  |  dv[v].
+constexpr int kMaxQubits = 26;
+struct Scatter {
+  int dv[16];
+  unsigned char dpos[kMaxQubits];
+};
+
 // Per-gate description of the fused backward step for gate i:
 //   chi <- G_{i+1}^dag chi (if upd) and E_i += phi_i (x) conj(chi)
 // over the 2^nu-amplitude groups spanned by the union of both gates' bits.
@@ -40,6 +54,12 @@ struct GateDesc {
   View chi_src;
   ViewW chi_dst;              // base == nullptr: do not write chi back
   View phi;
+  // perm mode (bwdt_kernel only): chi_src / phi in permuted blocked layout L_i
+  // (one copy per stage) unless *_nat (a natural pool: one copy per row);
+  // chi_dst permuted blocked in L_{i-1} through xs
+  int perm, chi_nat, phi_nat, sb, n_oth;
+  long long blk;
+  Scatter xs;
 };
 
 struct BwdParams {
@@ -57,6 +77,16 @@ struct BwdParams {
   double *e_red;              // [S_act][32]: reduced E (sample mode: before all-reduce)
   int fuse_polar;             // 1: the last CTA of each start runs the polar update
   int bulk;                   // 1: bwdt_kernel (bulk copies + mbarrier ring), 0: bwd_kernel (LDGSTS)
+  // Device-initiated exchange of the partial environments across the xg ranks
+  // of sample mode, done by the last CTA of each start
+  // before its polar update: store E into every rank's mailbox, raise a flag
+  // there, wait for all ranks' flags, sum the xg partials in rank order.
+  int xg;                              // > 1: exchange on; ranks
+  int xrank;                           // this context's rank; -1: emulated ranks (rank = slot start index)
+  int xS;                              // starts per mailbox
+  double *const *xmbox;                // [xg] rank q's mailbox [2 parity][xg src][xS][32]
+  unsigned long long *const *xflag;    // [xg] rank q's flags [xg src][xS] (epoch of the last write)
+  unsigned long long *xepoch;          // this context's epoch counters [xS] (emulated: [xg][xS])
   double beta;
   double *sig;                // [S][K] sum sigma, or nullptr
   double2 *env_trace;         // [K][S][16] for this sweep, or nullptr
@@ -82,6 +112,8 @@ struct FinalParams {
   const Slot *slots;
   View chi, x;
   int p0, p1;
+  int sb;                     // > 0: chi is sample-blocked (natural rows): (m / sb) blk + a sb + m % sb
+  long long blk;
   const double2 *gates;       // gate 0 of start s: gates + s*K*16
   double *partials;           // [S_act][nb]
   unsigned *counters;         // [S_act]
@@ -109,6 +141,22 @@ struct Fwd2Params {
   long long off[16];          // amplitude offset of local index v
   View src;                   // B_k (sample-minor, sm == 1)
   ViewW dst1, dst2;           // B_{k+1}, B_{k+2}
+};
+
+// Two-gate forward in perm mode (fwdp_kernel): reads B_k (permuted blocked
+// layout L_k; k = 0: the natural x pool through ins / off), writes B_{k+1}
+// in L_{k+1} and B_{k+2} in L_{k+2} (dst2.base == nullptr: gate k only).
+struct FwdpParams {
+  int n, nb, k, K, nu, tp0, tp1, sb, src_nat, n_oth;
+  long long blk;
+  const Slot *slots;
+  const double2 *gates;
+  uint32_t ins[4];            // natural source: union bit positions, ascending
+  long long off[16];          // natural source: amplitude offset of local v
+  int tau[16];                // permuted source: row of local v within the group
+  View src;
+  ViewW dst1, dst2;           // per-start strides only (ss); rows addressed through the scatters
+  Scatter s1, s2;
 };
 
 // Whole-row validation forward in shared memory (n <= 13): one CTA per
@@ -164,6 +212,7 @@ cudaError_t launch_polar(const PolarParams &p, int n_slots, cudaStream_t st);
 cudaError_t launch_final(const FinalParams &p, int n_slots, cudaStream_t st);
 cudaError_t launch_fwd_gate(const FwdGateParams &p, int n_slots, cudaStream_t st);
 cudaError_t launch_fwd2(const Fwd2Params &p, int n_slots, cudaStream_t st);
+cudaError_t launch_fwdp(const FwdpParams &p, int n_slots, cudaStream_t st);
 cudaError_t launch_val_row(const ValRowParams &p, int n_slots, cudaStream_t st);
 cudaError_t launch_dist(const DistParams &p, int n_slots, cudaStream_t st);
 cudaError_t launch_row_reduce(const double *row_in, int rows, double *out, int n_slots,

@@ -433,8 +433,44 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
 // Warp 0 of the finishing CTA holds the reduced E (lane = re/im of entry lane/2):
 // store it and (fuse_polar) run the gate update (kind: loaded before the
 // election so its global load is off the critical path).
+// Device-initiated all-reduce of the 4x4 environment over the ranks of sample
+// mode (NEXT-2; E is a sum over samples, so the ranks' partials add
+// up to the full E).  Warp 0 of the last CTA of start s, lane = real / imag
+// part of entry lane / 2.  Each rank writes its partial into parity slot
+// (epoch & 1) of EVERY rank's mailbox (peer stores over NVLink; emulated ranks:
+// local memory), releases a per-(source, start) epoch flag there, waits until
+// all ranks' flags for this epoch are up, and sums the partials in rank order
+// — so every rank gets identical bits and computes the identical polar
+// update.  Two parity slots suffice: a rank writes epoch t+2 only after every
+// rank raised its flag for t+1, which each does only after reading epoch t.
+__device__ double xchg_env(const BwdParams &P, int s, double e) {
+  const int lane = threadIdx.x & 31;
+  const int r = P.xrank >= 0 ? P.xrank : s;   // emulated: the slot's start index is its rank
+  const int sx = P.xrank >= 0 ? s : 0;
+  unsigned long long *ep = P.xepoch + (P.xrank >= 0 ? sx : (long long)r * P.xS + sx);
+  unsigned long long epn = 0;
+  if (lane == 0) {
+    epn = *ep + 1;
+    *ep = epn;
+  }
+  epn = __shfl_sync(FULL, epn, 0);
+  const long long par = (long long)(epn & 1ull);
+  for (int q = 0; q < P.xg; ++q) P.xmbox[q][((par * P.xg + r) * P.xS + sx) * 32 + lane] = e;
+  __threadfence_system();
+  __syncwarp();
+  if (lane < P.xg) st_release_sys(P.xflag[lane] + (long long)r * P.xS + sx, epn);
+  if (lane < P.xg)
+    while (ld_acquire_sys(P.xflag[r] + (long long)lane * P.xS + sx) < epn) __nanosleep(32);
+  __syncwarp();
+  __threadfence_system();
+  double t = 0.0;
+  for (int q = 0; q < P.xg; ++q) t += ld_relaxed_sys(P.xmbox[r] + ((par * P.xg + q) * P.xS + sx) * 32 + lane);
+  return t;
+}
+
 template <class SH>  // shared-memory struct with sum32[32] and scratch[64]
 __device__ void bwd_finish_e(const BwdParams &P, const GateDesc &G, int jslot, int s, SH &sh, double e, int kind) {
+  if (P.xg > 1) e = xchg_env(P, s, e);
   sh.sum32[threadIdx.x] = e;
   if (!P.fuse_polar) P.e_red[(long long)jslot * 32 + threadIdx.x] = e;
   __syncwarp();
@@ -559,33 +595,37 @@ __global__ void __launch_bounds__(BWD_THREADS, QFS_BWD_MINB) bwd_kernel(const Bw
 // ------------------------------------------------- backward, bulk-copy path --
 // bwdt_kernel: the same fused step as bwd_kernel (chi <- G_{i+1}^dag chi, E_i,
 // last-CTA ordered reduction + polar update of gate i; P:112, P:121-125,
-// P:172, eq:opt_u P:59-62), with the tiles moved by the copy engine instead of
-// per-thread LDGSTS (B200: cp.async.bulk -> SASS UBLKCP, mbarrier -> SYNCS).
+// P:172, eq:opt_u P:59-62), with the tiles moved by the copy engine (B200:
+// cp.async.bulk -> SASS UBLKCP, mbarrier -> SYNCS) instead of per-thread LDGSTS.
 //
-// Work unit ("stage") = one amplitude group of 2^NU rows (the union of gate
-// i's and gate i+1's qubits; local bits 0,1 = gate i+1's pair, the rest gate
-// i's other bits ascending) x a block of up to 32 consecutive samples.  In the
-// sample-minor layout every (row, sample block) is ONE contiguous run of
-// Mr * 16 bytes (512 B at M = 32, two runs at M = 64), so a stage is 2 * 2^NU
-// bulk copies (chi rows and phi = B_i rows) issued by one producer warp into a
-// ring of BT_STAGES shared-memory stages, each guarded by a full / empty
-// mbarrier pair.  Consumer warp w takes stages w, w + BT_CW, ...: lane = one
-// sample, all 2^NU amplitudes of it in registers, so the chi update and all 16
-// entries of E are lane-local (no transposes, no shuffles in the loop; 16
-// independent accumulators of ILP), and the only per-stage integer work is one
-// bit insertion.  Addresses are 64-bit (no 4 GiB block limit).  phi does not
-// depend on the previous launch: with G.pre the producer issues the first
-// stages' phi copies before griddepcontrol.wait (PDL), and it prefetches phi
-// rows BT_PF stages ahead into L2 (cp.async.bulk.prefetch.L2) so each ring
-// slot waits on L2 latency, not DRAM latency.
+// Layouts (perm mode, qfs_internal.h): B_i and the incoming chi are stored in
+// gate i's permuted sample-blocked layout L_i, whose lowest row bits are the
+// 2^NU-row union of gates i and i+1 — so a work unit ("stage": one amplitude
+// group x one block of sb <= 32 samples) is ONE contiguous 2^NU * sb * 16-byte
+// run per array (8 KB at NU = 4, sb = 32): one bulk copy for chi and one for
+// phi, where the natural sample-minor layout needed 2^NU row copies of 512 B
+// (measured: 512-byte bulk copies are bound by the copy engine's issue rate,
+// 3x slower than LDGSTS).  The natural pools (x as phi at i = 0, y as chi at
+// i >= K-2) still come row by row.  The updated chi is stored by the
+// consumers, one coalesced 32-sample row per STG, straight into the NEXT
+// gate's layout L_{i-1} (rows: the Scatter of G and v), so the next launch's
+// tiles are contiguous too.
+//
+// One producer warp fills a ring of BT_STAGES stages (full / empty mbarrier
+// pair per stage); consumer warp w owns the stages w, w + BT_CW, ...; lane =
+// one sample, all 2^NU amplitudes of it in registers: the chi update and all
+// 16 entries of E are lane-local (no transposes, no shuffles; 16 independent
+// accumulators).  phi does not depend on the previous launch: with G.pre the
+// producer issues the first stages' phi before griddepcontrol.wait (PDL), and
+// prefetches phi BT_PF stages ahead into L2 (cp.async.bulk.prefetch.L2).
 #ifndef QFS_BT_WARPS
-#define QFS_BT_WARPS 7   // 7 + 1 producer = 256 threads: up to 255 registers (8 consumers cap at 168 and spill)
+#define QFS_BT_WARPS 6   // + 1 producer = 224 threads: up to 255 registers (8 consumers cap at 168 and spill)
 #endif
 #ifndef QFS_BT_STAGES
 #define QFS_BT_STAGES 12
 #endif
 #ifndef QFS_BT_PF
-#define QFS_BT_PF 8       // phi rows prefetched into L2 this many stages ahead (0: off)
+#define QFS_BT_PF 4       // phi prefetched into L2 this many stages ahead (0: off)
 #endif
 #ifndef QFS_BT_HINT
 #define QFS_BT_HINT 1     // bit 0: phi (B_i, read once) copies L2::evict_first
@@ -593,7 +633,12 @@ __global__ void __launch_bounds__(BWD_THREADS, QFS_BWD_MINB) bwd_kernel(const Bw
 constexpr int BT_CW = QFS_BT_WARPS;           // consumer warps
 constexpr int BT_STAGES = QFS_BT_STAGES;
 constexpr int BT_THREADS = (BT_CW + 1) * 32;  // + one producer warp
-constexpr int BT_SROW = 32;                   // samples per stage row (one per lane)
+constexpr int BT_SROW = 32;                   // largest sample block (one sample per lane)
+// Consumer warp w owns the ring slots w, w + BT_CW, ...: a slot's full barrier
+// is then waited on by ONE warp in consecutive rounds, so its phase parity is
+// never ambiguous (a warp waiting on a slot two phases ahead of the barrier
+// would pass at once — mbarrier parity waits only distinguish adjacent phases).
+static_assert(BT_STAGES % BT_CW == 0, "each consumer warp must own whole ring slots");
 
 struct BtShared {
   uint64_t full[BT_STAGES], empty[BT_STAGES];
@@ -608,11 +653,17 @@ struct BtShared {
 size_t bt_smem_bytes(int nu) { return (size_t)BT_STAGES * 2 * (1 << nu) * BT_SROW * sizeof(double2); }
 namespace {
 
+// destination row of group G, local v (perm-mode scatter)
+__device__ __forceinline__ unsigned scatter_base(const Scatter &X, unsigned G, int n_oth) {
+  unsigned p = 0;
+  for (int j = 0; j < n_oth; ++j) p |= ((G >> j) & 1u) << X.dpos[j];
+  return p;
+}
+
 template <int NU, int TP0, int TP1, bool UPD, bool WIDE>
 __global__ void __launch_bounds__(BT_THREADS, 1) bwdt_kernel(const BwdParams P) {
   constexpr int NV = 1 << NU;
   constexpr int NQ = NV / 4;
-  constexpr int STAGE = 2 * NV * BT_SROW;  // double2 per stage: [chi|phi][v][lane]
   __shared__ BtShared sh;
   extern __shared__ __align__(128) double2 ring[];
   const GateDesc &G = P.g;
@@ -620,23 +671,20 @@ __global__ void __launch_bounds__(BT_THREADS, 1) bwdt_kernel(const BwdParams P) 
   const Slot sl = P.slots[jslot];
   const int s = sl.s;
   const unsigned Ms = (unsigned)sl.m;
-  const unsigned nmb = (Ms + BT_SROW - 1) / BT_SROW;
+  const int sb = G.sb;                     // sample block (16 or 32)
+  const int STAGE = 2 * NV * sb;           // double2 per stage: [chi | phi][v][sb]
+  const unsigned nmb = (Ms + sb - 1) / sb;
   const unsigned units = (1u << (P.n - NU)) * nmb;
   const unsigned chunk = (units + P.nb - 1) / P.nb;
   const unsigned beg = min(units, blockIdx.x * chunk), end = min(units, beg + chunk);
   const int nitems = (int)(end - beg);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const FastDiv fdu(nmb);
-  uint32_t ins[NU];
-#pragma unroll
-  for (int q = 0; q < NU; ++q) ins[q] = G.ins[q];
-  // first amplitude of the group and first sample of item k
-  auto item = [&](int k, unsigned &g, unsigned &m0) {
+  // group index G (other bits, ascending) and sample block b of item k
+  auto item = [&](int k, unsigned &Gi, unsigned &b) {
     const unsigned u = beg + (unsigned)k;
-    g = fdu.div(u);
-    m0 = (u - g * nmb) * BT_SROW;
-#pragma unroll
-    for (int q = 0; q < NU; ++q) g = insert_zero32(g, ins[q]);
+    Gi = fdu.div(u);
+    b = u - Gi * nmb;
   };
   if (threadIdx.x == 0) {
     for (int q = 0; q < BT_STAGES; ++q) {
@@ -651,46 +699,64 @@ __global__ void __launch_bounds__(BT_THREADS, 1) bwdt_kernel(const BwdParams P) 
     // ------------------------------------------------------------ producer
     const double2 *csrc = G.chi_src.base + (long long)s * G.chi_src.ss;
     const double2 *fsrc = G.phi.base + (long long)s * G.phi.ss;
-    const long long csa = G.chi_src.sa, fsa = G.phi.sa;
 #if QFS_BT_HINT & 1
     const uint64_t pol_f = policy_evict_first();
 #endif
-    // lane l < NV copies chi row l, NV <= l < 2 NV phi row l - NV
-    const bool is_phi = lane >= NV;
+    uint32_t ins[NU];
+#pragma unroll
+    for (int q = 0; q < NU; ++q) ins[q] = G.ins[q];
     const int v = lane & (NV - 1);
     const long long offv = G.off[v];
+    // lane l < NV: natural chi row l, NV <= l < 2 NV: natural phi row l - NV;
+    // lane 0 / 1: the single permuted chi / phi run
     auto issue = [&](int k, bool chi, bool phi) {
-      unsigned g, m0;
-      item(k, g, m0);
-      const unsigned mr = min((unsigned)BT_SROW, Ms - m0);
-      double2 *dst = ring + (k % BT_STAGES) * STAGE + (is_phi ? NV * BT_SROW : 0) + v * BT_SROW;
-      if (lane < 2 * NV && (is_phi ? phi : chi)) {
-        if (is_phi) {
-          const double2 *src = fsrc + ((long long)g + offv) * fsa + m0;
+      unsigned Gi, b;
+      item(k, Gi, b);
+      const unsigned cnt = min((unsigned)sb, Ms - b * sb);
+      double2 *stg = ring + (k % BT_STAGES) * STAGE;
+      uint64_t *bar = &sh.full[k % BT_STAGES];
+      unsigned g = Gi;
+#pragma unroll
+      for (int q = 0; q < NU; ++q) g = insert_zero32(g, ins[q]);
+      if (chi) {
+        if (G.chi_nat) {
+          if (lane < NV)
+            bulk_g2s(stg + v * sb, csrc + ((long long)g + offv) * G.chi_src.sa + b * sb, cnt * 16u, bar);
+        } else if (lane == 0) {
+          bulk_g2s(stg, csrc + (long long)b * G.blk + ((long long)Gi << NU) * sb, NV * sb * 16u, bar);
+        }
+      }
+      if (phi) {
+        double2 *dst = stg + NV * sb;
+        if (G.phi_nat) {
+          if (lane >= NV && lane < 2 * NV)
+            bulk_g2s(dst + v * sb, fsrc + ((long long)g + offv) * G.phi.sa + b * sb, cnt * 16u, bar);
+        } else if (lane == 1) {
+          const double2 *src = fsrc + (long long)b * G.blk + ((long long)Gi << NU) * sb;
 #if QFS_BT_HINT & 1
-          bulk_g2s_hint(dst, src, mr * 16u, &sh.full[k % BT_STAGES], pol_f);
+          bulk_g2s_hint(dst, src, NV * sb * 16u, bar, pol_f);
 #else
-          bulk_g2s(dst, src, mr * 16u, &sh.full[k % BT_STAGES]);
+          bulk_g2s(dst, src, NV * sb * 16u, bar);
 #endif
-        } else {
-          bulk_g2s(dst, csrc + ((long long)g + offv) * csa + m0, mr * 16u, &sh.full[k % BT_STAGES]);
         }
       }
     };
-    auto arm = [&](int k) {  // expect the stage's bytes (chi and phi rows)
+    auto arm = [&](int k) {  // expect the stage's bytes (chi and phi)
       if (lane == 0) {
-        unsigned g, m0;
-        item(k, g, m0);
-        mbar_arrive_tx(&sh.full[k % BT_STAGES], 2u * NV * min((unsigned)BT_SROW, Ms - m0) * 16u);
+        unsigned Gi, b;
+        item(k, Gi, b);
+        const unsigned cnt = min((unsigned)sb, Ms - b * sb);
+        const unsigned bytes = ((G.chi_nat ? cnt : (unsigned)sb) + (G.phi_nat ? cnt : (unsigned)sb)) * NV * 16u;
+        mbar_arrive_tx(&sh.full[k % BT_STAGES], bytes);
       }
       __syncwarp();
     };
     auto prefetch = [&](int k) {
 #if QFS_BT_PF
-      if (k < nitems && is_phi && lane < 2 * NV) {
-        unsigned g, m0;
-        item(k, g, m0);
-        bulk_prefetch_l2(fsrc + ((long long)g + offv) * fsa + m0, min((unsigned)BT_SROW, Ms - m0) * 16u);
+      if (k < nitems && lane == 0 && !G.phi_nat) {
+        unsigned Gi, b;
+        item(k, Gi, b);
+        bulk_prefetch_l2(fsrc + (long long)b * G.blk + ((long long)Gi << NU) * sb, NV * sb * 16u);
       }
 #endif
     };
@@ -727,19 +793,18 @@ __global__ void __launch_bounds__(BT_THREADS, 1) bwdt_kernel(const BwdParams P) 
           Q[4 * a + b] = cconj(__ldcg(P.gates + ((long long)s * P.K + G.upd_gate) * 16 + 4 * b + a));
     }
     double2 *cdst = G.chi_dst.base ? G.chi_dst.base + (long long)s * G.chi_dst.ss : nullptr;
-    const long long dsa = G.chi_dst.sa;
     double2 acc[16];
 #pragma unroll
     for (int e = 0; e < 16; ++e) acc[e] = make_double2(0.0, 0.0);
     for (int k = warp; k < nitems; k += BT_CW) {
-      unsigned g, m0;
-      item(k, g, m0);
-      const bool valid = m0 + lane < Ms;
+      unsigned Gi, b;
+      item(k, Gi, b);
+      const bool valid = lane < sb && b * sb + lane < Ms;
       mbar_wait(&sh.full[k % BT_STAGES], (k / BT_STAGES) & 1);
       const double2 *sc = ring + (k % BT_STAGES) * STAGE + lane;
       double2 c[NV];
 #pragma unroll
-      for (int v = 0; v < NV; ++v) c[v] = valid ? sc[v * BT_SROW] : make_double2(0.0, 0.0);
+      for (int v = 0; v < NV; ++v) c[v] = valid ? sc[v * sb] : make_double2(0.0, 0.0);
       if (UPD) {
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
@@ -748,15 +813,16 @@ __global__ void __launch_bounds__(BT_THREADS, 1) bwdt_kernel(const BwdParams P) 
           for (int a = 0; a < 4; ++a) {
             o[a] = make_double2(0.0, 0.0);
 #pragma unroll
-            for (int b = 0; b < 4; ++b) cfma(o[a], Q[4 * a + b], c[4 * q + b]);
+            for (int bb = 0; bb < 4; ++bb) cfma(o[a], Q[4 * a + bb], c[4 * q + bb]);
           }
 #pragma unroll
           for (int a = 0; a < 4; ++a) c[4 * q + a] = o[a];
         }
-        if (cdst && valid) {
-          double2 *dp = cdst + (long long)g * dsa + m0 + lane;
+        if (cdst && valid) {  // into the next gate's layout L_{i-1}
+          const unsigned pg = scatter_base(G.xs, Gi, G.n_oth);
+          double2 *dp = cdst + (long long)b * G.blk + lane;
 #pragma unroll
-          for (int v = 0; v < NV; ++v) dp[G.off[v] * dsa] = c[v];
+          for (int v = 0; v < NV; ++v) dp[(long long)(pg | (unsigned)G.xs.dv[v]) * sb] = c[v];
         }
       }
       // E[l_in][l_out] += phi[v(p, l_in)] conj(chi'[v(p, l_out)]) over the P-quadruples p
@@ -765,13 +831,13 @@ __global__ void __launch_bounds__(BT_THREADS, 1) bwdt_kernel(const BwdParams P) 
         double2 f[4];
 #pragma unroll
         for (int l = 0; l < 4; ++l)
-          f[l] = valid ? sc[(NV + pv_idx<NU, TP0, TP1>(p, l)) * BT_SROW] : make_double2(0.0, 0.0);
+          f[l] = valid ? sc[(NV + pv_idx<NU, TP0, TP1>(p, l)) * sb] : make_double2(0.0, 0.0);
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            const double2 cb = c[pv_idx<NU, TP0, TP1>(p, b)];
-            double2 &e = acc[4 * a + b];
+          for (int bb = 0; bb < 4; ++bb) {
+            const double2 cb = c[pv_idx<NU, TP0, TP1>(p, bb)];
+            double2 &e = acc[4 * a + bb];
             e.x = fma(f[a].x, cb.x, e.x);
             e.x = fma(f[a].y, cb.y, e.x);
             e.y = fma(f[a].y, cb.x, e.y);
@@ -781,7 +847,7 @@ __global__ void __launch_bounds__(BT_THREADS, 1) bwdt_kernel(const BwdParams P) 
       __syncwarp();
       if (lane == 0) mbar_arrive(&sh.empty[k % BT_STAGES]);
     }
-    // warp sum over the 32 samples (fixed butterfly order)
+    // warp sum over the samples (fixed butterfly order)
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
 #pragma unroll
@@ -898,11 +964,17 @@ __global__ void __launch_bounds__(RED_THREADS, 4) final_kernel(const FinalParams
     const unsigned q = fdm.div(w);
     const unsigned m = w - q * Ms;
     const unsigned base = insert_zero32(insert_zero32(q, lo), hi);
-    const double2 *cp = cb + (long long)base * P.chi.sa + (long long)m * P.chi.sm;
     const double2 *xp = xb + (long long)base * P.x.sa + (long long)m * P.x.sm;
     double2 v[4], xv[4];
+    if (P.sb > 0) {  // perm mode: chi sample-blocked, natural rows (layout L_{-1})
+      const double2 *cp = cb + (long long)(m / P.sb) * P.blk + (long long)base * P.sb + m % P.sb;
 #pragma unroll
-    for (int l = 0; l < 4; ++l) v[l] = cp[(long long)o[l] * P.chi.sa];
+      for (int l = 0; l < 4; ++l) v[l] = cp[(long long)o[l] * P.sb];
+    } else {
+      const double2 *cp = cb + (long long)base * P.chi.sa + (long long)m * P.chi.sm;
+#pragma unroll
+      for (int l = 0; l < 4; ++l) v[l] = cp[(long long)o[l] * P.chi.sa];
+    }
 #pragma unroll
     for (int l = 0; l < 4; ++l) xv[l] = __ldcs(xp + (long long)o[l] * P.x.sa);
 #pragma unroll
@@ -1134,6 +1206,128 @@ __global__ void __launch_bounds__(FWD_THREADS, QFS_FWD2_MINB) fwd2_kernel(const 
       for (int a = 0; a < 4; ++a) v[pv_idx<NU, TP0, TP1>(q, a)] = o4[a];
     }
     store(d2 + o, v, 2);
+  }
+  pdl_trigger();
+}
+
+// ------------------------------------------- forward, perm-mode layouts --
+// fwdp_kernel: fwd2_kernel's two gates per pass (B_{k+1} = G_k B_k, B_{k+2} =
+// G_{k+1} B_{k+1}) on the layout-permuted sample-blocked arrays of
+// perm mode (qfs_internal.h): the source group's 2^NU rows are contiguous in
+// B_k's layout L_k (row G 2^NU + tau[v]; at k = 0 the natural x pool through
+// ins / off), and each destination row is scattered into the layout of the
+// gate that will read it (B_{k+1} in L_{k+1}, B_{k+2} in L_{k+2}) — the layout
+// the backward kernel's single contiguous bulk copies need.  The scatter of
+// the group index G is a byte-wise table lookup in shared memory (3 x 256
+// entries per destination, built before the PDL wait).  dst2.base == nullptr:
+// gate k only (the odd tail of the forward pass).
+template <int NU, int TP0, int TP1>
+__global__ void __launch_bounds__(FWD_THREADS, QFS_FWD2_MINB) fwdp_kernel(const FwdpParams P) {
+  constexpr int NV = 1 << NU;
+  constexpr int NQ = NV / 4;
+  __shared__ double2 sG[2][16];
+  __shared__ unsigned tab[2][3][256];
+  const int j = blockIdx.y;
+  const Slot sl = P.slots[j];
+  const int s = sl.s;
+  const unsigned Ms = (unsigned)sl.m;
+  const unsigned items = Ms << (P.n - NU);
+  const unsigned chunk = (items + P.nb - 1) / P.nb;
+  const unsigned beg = blockIdx.x * chunk, end = min(items, beg + chunk);
+  const FastDiv fdm(Ms);
+  const bool two = P.dst2.base != nullptr;
+  for (int e = threadIdx.x; e < 2 * 3 * 256; e += blockDim.x) {  // scatter tables (launch constants)
+    const int d = e / 768, byte = (e >> 8) % 3, val = e & 255;
+    const Scatter &X = d ? P.s2 : P.s1;
+    unsigned p = 0;
+    for (int bit = 0; bit < 8; ++bit) {
+      const int jj = byte * 8 + bit;
+      if (jj < P.n_oth && ((val >> bit) & 1)) p |= 1u << X.dpos[jj];
+    }
+    tab[d][byte][val] = p;
+  }
+  pdl_wait();
+  if (threadIdx.x < 32) {
+    const int q = threadIdx.x >> 4, e = threadIdx.x & 15;
+    sG[q][e] = P.gates[((long long)s * P.K + P.k + q) * 16 + e];
+  }
+  __syncthreads();
+  const double2 *src = P.src.base + (long long)s * P.src.ss;
+  double2 *d1 = P.dst1.base + (long long)s * P.dst1.ss;
+  double2 *d2 = two ? P.dst2.base + (long long)s * P.dst2.ss : nullptr;
+  const int sb = P.sb, lsb = sb == 32 ? 5 : 4;
+  const long long blk = P.blk;
+  uint32_t ins[NU];
+#pragma unroll
+  for (int q = 0; q < NU; ++q) ins[q] = P.ins[q];
+#if QFS_FWD2_HINT
+  const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+#endif
+  auto load = [&](unsigned w, double2 *v) {
+    const unsigned G = fdm.div(w), m = w - G * Ms;
+    if (P.src_nat) {
+      unsigned g = G;
+#pragma unroll
+      for (int q = 0; q < NU; ++q) g = insert_zero32(g, ins[q]);
+      const double2 *sp = src + (long long)g * P.src.sa + m;
+#pragma unroll
+      for (int u = 0; u < NV; ++u) v[u] = sp[P.off[u] * P.src.sa];
+    } else {
+      const double2 *sp = src + (long long)(m >> lsb) * blk + ((long long)G << NU) * sb + (m & (sb - 1));
+#pragma unroll
+      for (int u = 0; u < NV; ++u) v[u] = sp[P.tau[u] * sb];
+    }
+  };
+  auto store = [&](double2 *base, const Scatter &X, const unsigned (&tb)[3][256], unsigned G, unsigned m,
+                   const double2 *v, int which) {
+    const unsigned pg = tb[0][G & 255u] | tb[1][(G >> 8) & 255u] | tb[2][G >> 16];
+    double2 *bp = base + (long long)(m >> lsb) * blk + (m & (sb - 1));
+#pragma unroll
+    for (int u = 0; u < NV; ++u) {
+      double2 *q = bp + (long long)(pg | (unsigned)X.dv[u]) * sb;
+#if QFS_FWD2_HINT & 3
+      if ((QFS_FWD2_HINT & 1) && which == 1) st_hint(q, v[u], pol_first);
+      else if ((QFS_FWD2_HINT & 2) && which == 2) st_hint(q, v[u], pol_last);
+      else *q = v[u];
+#else
+      *q = v[u];
+#endif
+    }
+  };
+  double2 v[NV], vn[NV];
+  if (beg + threadIdx.x < end) load(beg + threadIdx.x, vn);
+  for (unsigned w = beg + threadIdx.x; w < end; w += blockDim.x) {
+    const unsigned G = fdm.div(w), m = w - G * Ms;
+#pragma unroll
+    for (int u = 0; u < NV; ++u) v[u] = vn[u];
+    if (w + blockDim.x < end) load(w + blockDim.x, vn);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {  // gate k on local bits (0, 1)
+      double2 o4[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        o4[a] = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) cfma(o4[a], gval(&sG[0][4 * a + b]), v[4 * q + b]);
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) v[4 * q + a] = o4[a];
+    }
+    store(d1, P.s1, tab[0], G, m, v, 1);
+    if (!two) continue;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {  // gate k+1 on local bits (TP0, TP1)
+      double2 o4[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        o4[a] = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) cfma(o4[a], gval(&sG[1][4 * a + b]), v[pv_idx<NU, TP0, TP1>(q, b)]);
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) v[pv_idx<NU, TP0, TP1>(q, a)] = o4[a];
+    }
+    store(d2, P.s2, tab[1], G, m, v, 2);
   }
   pdl_trigger();
 }
@@ -1413,7 +1607,10 @@ cudaError_t launch_bwdt(const BwdParams &p, int n_slots, cudaStream_t st) {
   dim3 grid(p.nb, n_slots), block(BT_THREADS);
   const GateDesc &g = p.g;
   const int smem = (int)bt_smem_bytes(g.nu);
-  const bool wide = p.nb > RED_GS;
+#ifndef QFS_BT_WIDE
+#define QFS_BT_WIDE 1
+#endif
+  const bool wide = QFS_BT_WIDE && p.nb > RED_GS;
 #define QFS_BT1(NU, A, B, U, W)                                                                  \
   do {                                                                                           \
     static bool attr = false;                                                                    \
@@ -1528,6 +1725,25 @@ cudaError_t launch_fwd2(const Fwd2Params &p, int n_slots, cudaStream_t st) {
     else QFS_FWD2(4, 3, 2);
   }
 #undef QFS_FWD2
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fwdp(const FwdpParams &p, int n_slots, cudaStream_t st) {
+  dim3 grid(p.nb, n_slots), block(FWD_THREADS);
+#define QFS_FWDP(NU, A, B) launch_ex(fwdp_kernel<NU, A, B>, grid, block, 0, st, p)
+  if (p.nu == 2) {
+    if (p.tp0 == 0) QFS_FWDP(2, 0, 1);
+    else QFS_FWDP(2, 1, 0);
+  } else if (p.nu == 3) {
+    if (p.tp0 == 0 && p.tp1 == 2) QFS_FWDP(3, 0, 2);
+    else if (p.tp0 == 2 && p.tp1 == 0) QFS_FWDP(3, 2, 0);
+    else if (p.tp0 == 1 && p.tp1 == 2) QFS_FWDP(3, 1, 2);
+    else QFS_FWDP(3, 2, 1);
+  } else {
+    if (p.tp0 == 2) QFS_FWDP(4, 2, 3);
+    else QFS_FWDP(4, 3, 2);
+  }
+#undef QFS_FWDP
   return cudaGetLastError();
 }
 

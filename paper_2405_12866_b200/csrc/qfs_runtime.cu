@@ -78,11 +78,25 @@ struct qfs_ctx {
   int K_g = 0;      // gates d_gates / d_vprev were sized for (ensure_gates)
   int K_s = 0;      // gates d_B / d_sig were sized for (ensure_state)
   bool force_unfused = false;  // QFS_UNFUSED_POLAR=1: separate polar launch (sample-mode code path at world 1)
-  bool bwd_bulk = true;        // QFS_BWD_BULK=0: LDGSTS backward kernel instead of the bulk-copy one
+  // QFS_BWD_BULK=1: perm mode — bulk-copy backward (bwdt_kernel) on per-gate
+  // permuted layouts; measured 1.3x slower than the LDGSTS kernel at C4 / C5
+  // (profiles/r2_bulk_summary.md), so off by default
+  bool bwd_bulk = false;
   int bulk_min_m = 16;         // QFS_BULK_MIN_M: smallest M_max that takes the bulk-copy backward
   int V_glob = 0;   // validation rows over all ranks (sample mode: sum of the ranks' V)
+  // sample mode, device-initiated exchange of E (qfs_set_exchange / NEXT-2)
+  int vr = 1;       // emulated ranks on this device (qfs_create_emulated); 1 otherwise
+  int xchg = 0;     // 0: host-enqueued NCCL all-reduce + polar launch per gate; 1: device exchange
+  int xS = 0;       // starts the mailboxes were sized for
+  double *d_xmbox = nullptr;              // own mailbox + flags block (emulated: every rank's)
+  unsigned long long *d_xflag = nullptr;  // (inside d_xmbox's allocation)
+  unsigned long long *d_xepoch = nullptr;
+  double **d_xmbox_tab = nullptr;         // [world] rank q's mailbox (IPC-mapped peers)
+  unsigned long long **d_xflag_tab = nullptr;
+  std::vector<void *> x_mapped;           // IPC-opened peer blocks
   double2 *d_vprev = nullptr;  // [S][K][16] right singular vectors of the last polar step (warm start)
   double2 *d_gates = nullptr, *d_chi = nullptr, *d_B = nullptr, *d_vb0 = nullptr, *d_vb1 = nullptr;
+  double2 *d_chi2 = nullptr;   // perm mode: chi ping-pongs between d_chi / d_chi2 (its layout changes per gate)
   double *d_partials = nullptr, *d_ered = nullptr, *d_sig = nullptr, *d_csum = nullptr,
          *d_rowout = nullptr, *d_cval = nullptr;
   unsigned *d_counters = nullptr;
@@ -297,7 +311,7 @@ bool offsets_fit(const qfs_ctx *c, long long rows) { return ((long long)c->N * r
 size_t plan_bytes(const qfs_ctx *c, int S, int M, int V, int nb) {
   size_t N = (size_t)c->N;
   size_t b = 0;
-  b += (size_t)S * M * N * 16;                             // chi
+  b += (size_t)S * M * N * 16 * (c->K > 1 ? 2 : 1);        // chi (two buffers: perm mode)
   if (c->K > 1) b += (size_t)(c->K - 1) * S * M * N * 16;  // B cache
   if ((c->n > val_row_max_n() || c->blocks) && V > 0) b += 2 * (size_t)S * V * N * 16;
   if (c->blocks) b += (size_t)S * kBlkMaxCtas * 128 * 8;
@@ -340,10 +354,13 @@ qfs_status ensure_state(qfs_ctx *c, int S, int M, int V) {
     return fail(c, QFS_ERR_CAPACITY, "2^n * M * 16 B >= 4 GiB: beyond the 32-bit offsets of the streamed kernels");
   S = std::max(S, c->S_cap);
   M = std::max(M, c->M_cap);
+  // perm mode's sample blocks (16 or 32 samples) must tile M_cap exactly
+  if (M > 16) M = (M + 31) / 32 * 32;
+  else if (M > 8) M = 16;
   V = std::max(V, c->V_cap);
   const int nbc = std::max(nb, c->nb_cap);
   CUDA_TRY(c, cudaStreamSynchronize(c->st));
-  dfree(c->d_chi); dfree(c->d_B); dfree(c->d_vb0); dfree(c->d_vb1); dfree(c->d_bpart);
+  dfree(c->d_chi); dfree(c->d_chi2); dfree(c->d_B); dfree(c->d_vb0); dfree(c->d_vb1); dfree(c->d_bpart);
   dfree(c->d_partials); dfree(c->d_ered); dfree(c->d_sig); dfree(c->d_csum); dfree(c->d_rowout);
   dfree(c->d_cval); dfree(c->d_counters); dfree(c->d_slots);
   dfree(c->d_counters1); dfree(c->d_gpart);
@@ -364,6 +381,7 @@ qfs_status ensure_state(qfs_ctx *c, int S, int M, int V) {
   }
   const size_t N = (size_t)c->N;
   CUDA_TRY(c, cudaMalloc(&c->d_chi, (size_t)S * M * N * sizeof(double2)));
+  if (c->K > 1) CUDA_TRY(c, cudaMalloc(&c->d_chi2, (size_t)S * M * N * sizeof(double2)));
   if (c->K > 1) CUDA_TRY(c, cudaMalloc(&c->d_B, (size_t)(c->K - 1) * S * M * N * sizeof(double2)));
   if ((c->n > val_row_max_n() || c->blocks) && V > 0) {
     CUDA_TRY(c, cudaMalloc(&c->d_vb0, (size_t)S * V * N * sizeof(double2)));
@@ -389,6 +407,86 @@ qfs_status ensure_state(qfs_ctx *c, int S, int M, int V) {
   return QFS_OK;
 }
 
+void xchg_release(qfs_ctx *c) {
+  for (void *p : c->x_mapped) cudaIpcCloseMemHandle(p);
+  c->x_mapped.clear();
+  dfree(c->d_xmbox); dfree(c->d_xepoch); dfree(c->d_xmbox_tab); dfree(c->d_xflag_tab);
+  c->d_xflag = nullptr;
+  c->xS = 0;
+}
+
+// Mailboxes of the device-initiated exchange (sample mode, qfs_set_exchange):
+// per rank a block [2 parity][world src][S][32] doubles + flags [world src][S]
+// (epochs), zeroed; emulated ranks: all blocks in one local allocation;
+// real ranks: each rank's own block, CUDA-IPC handles all-gathered over the
+// context's NCCL communicator and the peers' blocks mapped (peer stores over
+// NVLink).  Collective over the ranks (called in the same order by all).
+qfs_status ensure_xchg(qfs_ctx *c, int S) {
+  if (!(c->mode == 1 && c->world > 1 && c->xchg == 1) || S <= c->xS) return QFS_OK;
+  const int g = c->world;
+  CUDA_TRY(c, cudaStreamSynchronize(c->st));
+  if (c->comm && c->xS > 0) {  // every rank is done with the old mailboxes before they go
+    NCCL_TRY(c, ncclAllReduce(c->d_flag + 2, c->d_flag + 2, 1, ncclInt32, ncclMax, c->comm, c->st));
+    CUDA_TRY(c, cudaStreamSynchronize(c->st));
+  }
+  xchg_release(c);
+  drop_graph(c);
+  const size_t mb = (size_t)2 * g * S * 32 * sizeof(double), fb = (size_t)g * S * sizeof(unsigned long long);
+  const size_t blk = (mb + fb + 255) / 256 * 256;
+  const int nblk = c->vr > 1 ? g : 1;
+  char *base = nullptr;
+  CUDA_TRY(c, cudaMalloc(&base, blk * nblk));
+  CUDA_TRY(c, cudaMemsetAsync(base, 0, blk * nblk, c->st));
+  c->d_xmbox = (double *)base;
+  c->d_xflag = (unsigned long long *)(base + mb);
+  CUDA_TRY(c, cudaMalloc(&c->d_xepoch, (size_t)nblk * S * sizeof(unsigned long long)));
+  CUDA_TRY(c, cudaMemsetAsync(c->d_xepoch, 0, (size_t)nblk * S * sizeof(unsigned long long), c->st));
+  std::vector<double *> mt(g);
+  std::vector<unsigned long long *> ft(g);
+  if (c->vr > 1) {
+    for (int q = 0; q < g; ++q) {
+      mt[q] = (double *)(base + q * blk);
+      ft[q] = (unsigned long long *)(base + q * blk + mb);
+    }
+  } else {
+    if (!c->comm) return fail(c, QFS_ERR_STATE, "device exchange needs the NCCL communicator of the ranks");
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(c, cudaIpcGetMemHandle(&h, base));
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    char *d_h = nullptr;
+    CUDA_TRY(c, cudaMalloc(&d_h, (size_t)64 * g));
+    CUDA_TRY(c, cudaMemcpyAsync(d_h + 64 * c->rank, &h, 64, cudaMemcpyHostToDevice, c->st));
+    NCCL_TRY(c, ncclAllGather(d_h + 64 * c->rank, d_h, 64, ncclChar, c->comm, c->st));
+    std::vector<cudaIpcMemHandle_t> all(g);
+    CUDA_TRY(c, cudaMemcpyAsync(all.data(), d_h, (size_t)64 * g, cudaMemcpyDeviceToHost, c->st));
+    CUDA_TRY(c, cudaStreamSynchronize(c->st));
+    cudaFree(d_h);
+    for (int q = 0; q < g; ++q) {
+      char *pq = base;
+      if (q != c->rank) {
+        void *mp = nullptr;
+        CUDA_TRY(c, cudaIpcOpenMemHandle(&mp, all[q], cudaIpcMemLazyEnablePeerAccess));
+        c->x_mapped.push_back(mp);
+        pq = (char *)mp;
+      }
+      mt[q] = (double *)pq;
+      ft[q] = (unsigned long long *)(pq + mb);
+    }
+  }
+  CUDA_TRY(c, cudaMalloc(&c->d_xmbox_tab, g * sizeof(double *)));
+  CUDA_TRY(c, cudaMalloc(&c->d_xflag_tab, g * sizeof(unsigned long long *)));
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_xmbox_tab, mt.data(), g * sizeof(double *), cudaMemcpyHostToDevice, c->st));
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_xflag_tab, ft.data(), g * sizeof(unsigned long long *), cudaMemcpyHostToDevice,
+                              c->st));
+  CUDA_TRY(c, cudaStreamSynchronize(c->st));
+  if (c->comm) {  // every rank's zeroed mailbox exists before anyone writes into it
+    NCCL_TRY(c, ncclAllReduce(c->d_flag + 2, c->d_flag + 2, 1, ncclInt32, ncclMax, c->comm, c->st));
+    CUDA_TRY(c, cudaStreamSynchronize(c->st));
+  }
+  c->xS = S;
+  return QFS_OK;
+}
+
 // ---------------------------------------------------------------- sweep ----
 struct SweepSpec {
   std::vector<Slot> slots;   // active starts (local rows per start)
@@ -402,10 +500,16 @@ struct SweepSpec {
 
 // Descriptor of the fused backward step for gate i (union of gate i's pair
 // with gate i+1's; local order: Q pair first, then gate i's other bits).
+// The transposed pools [2^n][m_pool]; with emulated ranks one such block per
+// rank (rank r = slot start r, qfs_create_emulated: one start only).
+View pool_view(const qfs_ctx *c, const double2 *base) {
+  return View{base, c->vr > 1 ? c->N * c->m_pool : 0, c->m_pool, 1};
+}
+
 GateDesc make_desc(const qfs_ctx *c, int i) {
   const int K = c->K;
   const long long N = c->N, Mc = c->M_cap, sS = N * Mc;
-  const View xpool{c->d_x, 0, c->m_pool, 1}, ypool{c->d_y, 0, c->m_pool, 1};
+  const View xpool = pool_view(c, c->d_x), ypool = pool_view(c, c->d_y);
   GateDesc d{};
   const bool upd = i < K - 1;
   d.upd = upd ? 1 : 0;
@@ -447,6 +551,59 @@ GateDesc make_desc(const qfs_ctx *c, int i) {
   return d;
 }
 
+
+// ---- perm mode layouts (qfs_internal.h Scatter) ----------------
+// L_i (0 <= i < K): the rows of gate i's environment group lowest, in the
+// backward kernel's local order (make_desc: gate i+1's pair, then gate i's
+// other qubits ascending; gate K-1: its own pair), the other qubits ascending
+// above them.  L_{-1}: natural order.
+struct Lay {
+  int nu = 0;
+  int loc[4] = {0, 0, 0, 0};
+  int pos[kMaxQubits];  // natural qubit -> physical row bit
+  int oth[kMaxQubits];  // the other qubits, ascending (the group index bits)
+};
+Lay layout_of(const qfs_ctx *c, int i) {
+  Lay L;
+  const int n = c->n, K = c->K;
+  if (i < 0) {
+    for (int b = 0; b < n; ++b) L.pos[b] = L.oth[b] = b;
+    return L;
+  }
+  const int p0 = c->pairs[2 * i], p1 = c->pairs[2 * i + 1];
+  if (i == K - 1) {
+    L.loc[0] = p0; L.loc[1] = p1; L.nu = 2;
+  } else {
+    L.loc[0] = c->pairs[2 * (i + 1)]; L.loc[1] = c->pairs[2 * (i + 1) + 1]; L.nu = 2;
+    int ex[2], ne = 0;
+    for (int q : {p0, p1})
+      if (q != L.loc[0] && q != L.loc[1]) ex[ne++] = q;
+    if (ne == 2 && ex[0] > ex[1]) std::swap(ex[0], ex[1]);
+    for (int t = 0; t < ne; ++t) L.loc[L.nu++] = ex[t];
+  }
+  bool in_u[kMaxQubits] = {false};
+  for (int t = 0; t < L.nu; ++t) {
+    in_u[L.loc[t]] = true;
+    L.pos[L.loc[t]] = t;
+  }
+  int j = 0;
+  for (int b = 0; b < n; ++b)
+    if (!in_u[b]) { L.pos[b] = L.nu + j; L.oth[j++] = b; }
+  return L;
+}
+// rows of (group G of src, local v over the qubits lloc[0..nl-1]) in layout dst
+Scatter make_scatter(const Lay &src, const int *lloc, int nl, const Lay &dst, int n) {
+  Scatter X{};
+  for (int v = 0; v < 16; ++v) {
+    int r = 0;
+    if (v < (1 << nl))
+      for (int t = 0; t < nl; ++t)
+        if ((v >> t) & 1) r |= 1 << dst.pos[lloc[t]];
+    X.dv[v] = r;
+  }
+  for (int j = 0; j < n - src.nu; ++j) X.dpos[j] = (unsigned char)dst.pos[src.oth[j]];
+  return X;
+}
 
 // Plan of the cluster-resident sweep (qfs_resident.cu) for ns starts of up to
 // M_max rows: the smallest power-of-two cluster whose CTAs hold their slice of
@@ -503,7 +660,7 @@ qfs_status issue_blocks(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStr
   double *bpart = c->d_bpart + (long long)j0 * kBlkMaxCtas * 128;
   double *dpart = c->d_partials + (long long)j0 * c->nb_cap * 32;
   const long long N = c->N, Mc = c->M_cap, sS = N * Mc;
-  const View xpool{c->d_x, 0, c->m_pool, 1}, ypool{c->d_y, 0, c->m_pool, 1};
+  const View xpool = pool_view(c, c->d_x), ypool = pool_view(c, c->d_y);
   auto Bk = [&](int k) -> double2 * { return c->d_B + (long long)(k - 1) * c->S_cap * sS; };
   double units = 0;
   for (int j = j0; j < j1; ++j) units += (double)sp.slots[j].m * (double)N;
@@ -611,14 +768,71 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
   double *rowout = c->d_rowout + (long long)j0 * std::max(c->V, 1);
   const long long N = c->N;
   const long long Mc = c->M_cap;
-  const View xpool{c->d_x, 0, c->m_pool, 1}, ypool{c->d_y, 0, c->m_pool, 1};
+  const View xpool = pool_view(c, c->d_x), ypool = pool_view(c, c->d_y);
   const long long sS = N * Mc;                      // per-start stride of chi / B
   auto Bk = [&](int k) -> double2 * { return c->d_B + (long long)(k - 1) * c->S_cap * sS; };
   double units = 0;  // amplitudes of all active training rows
   for (int j = j0; j < j1; ++j) units += (double)sp.slots[j].m * (double)N;
+  // perm mode (bulk-copy backward): B cache and chi in the per-gate permuted
+  // sample-blocked layouts L_i (qfs_internal.h); else natural sample-minor
+  const bool perm = c->bwd_bulk && M_max >= c->bulk_min_m && M_max >= 16;
+  const int psb = c->M_cap >= 32 ? 32 : 16;
+  const long long pblk = N * psb;
+  std::vector<Lay> lays;
+  if (perm) {
+    lays.reserve(K + 1);
+    for (int i = -1; i < K; ++i) lays.push_back(layout_of(c, i));
+  }
+  auto LY = [&](int i) -> const Lay & { return lays[i + 1]; };
+  auto chibuf = [&](int i) -> double2 * { return (i & 1) ? c->d_chi2 : c->d_chi; };
   // (a) forward: B_1 .. B_{K-1}: two gates per coalesced pass
   // (a single-gate pass for an odd tail)
-  if (K > 1) {
+  if (K > 1 && perm) {
+    PhaseScope phase_fwd(c, K_FWD_GATE);
+    for (int k = 0; k + 1 < K; k += 2) {
+      FwdpParams f{};
+      f.n = n; f.k = k; f.K = K; f.slots = slots; f.gates = c->d_gates; f.sb = psb; f.blk = pblk;
+      int loc[4] = {c->pairs[2 * k], c->pairs[2 * k + 1], 0, 0}, nu = 2;
+      const int q0 = c->pairs[2 * (k + 1)], q1 = c->pairs[2 * (k + 1) + 1];
+      int ex[2], ne = 0;
+      for (int q : {q0, q1})
+        if (q != loc[0] && q != loc[1]) ex[ne++] = q;
+      if (ne == 2 && ex[0] > ex[1]) std::swap(ex[0], ex[1]);
+      for (int t = 0; t < ne; ++t) loc[nu++] = ex[t];
+      f.nu = nu;
+      for (int t = 0; t < nu; ++t) {
+        if (loc[t] == q0) f.tp0 = t;
+        if (loc[t] == q1) f.tp1 = t;
+      }
+      const Lay &Lk = LY(k);  // the group's qubit set = gates k, k+1 (L_k's low bits)
+      f.n_oth = n - Lk.nu;
+      f.src_nat = k == 0 ? 1 : 0;
+      int srt[4];
+      for (int t = 0; t < nu; ++t) srt[t] = loc[t];
+      std::sort(srt, srt + nu);
+      for (int t = 0; t < 4; ++t) f.ins[t] = t < nu ? srt[t] : 0;
+      for (int v = 0; v < 16; ++v) {
+        long long o = 0;
+        int r = 0;
+        for (int t = 0; t < nu && v < (1 << nu); ++t)
+          if ((v >> t) & 1) { o |= 1LL << loc[t]; r |= 1 << Lk.pos[loc[t]]; }
+        f.off[v] = o;
+        f.tau[v] = r;
+      }
+      f.src = k == 0 ? xpool : View{Bk(k), sS, Mc, 1};
+      f.dst1 = ViewW{Bk(k + 1), sS, Mc, 1};
+      f.s1 = make_scatter(Lk, loc, nu, LY(k + 1), n);
+      if (k + 2 < K) {
+        f.dst2 = ViewW{Bk(k + 2), sS, Mc, 1};
+        f.s2 = make_scatter(Lk, loc, nu, LY(k + 2), n);
+      }
+      f.nb = blocks_per_start(((long long)M_max * N) >> nu, ns, fwd2_min_blocks());
+      const double fb = k + 2 < K ? 48.0 : 32.0;
+      LaunchScope ls(c, K_FWD_GATE, units * fb, units * (k + 2 < K ? 64.0 : 32.0));
+      CUDA_TRY(c, launch_fwdp(f, ns, st));
+    }
+  }
+  if (K > 1 && !perm) {
   PhaseScope phase_fwd(c, K_FWD_GATE);
   for (int k = 0; k + 1 < K;) {
     const View src = k == 0 ? xpool : View{Bk(k), sS, Mc, 1};
@@ -674,8 +888,13 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
   b.kinds = c->d_kinds;
   b.partials = partials; b.counters = cnt_b; b.e_red = ered;
   b.counters1 = c->d_counters1 + (long long)j0 * 40; b.gpartials = c->d_gpart + (long long)j0 * 40 * 32;
-  const bool sample_ar = c->mode == 1 && c->world > 1;  // per-gate NCCL all-reduce of E
-  b.fuse_polar = (sample_ar || c->force_unfused) ? 0 : 1;
+  const bool sample_ar = c->mode == 1 && c->world > 1;  // per-gate exchange of E
+  const bool dev_x = sample_ar && c->xchg == 1;         // ... device-initiated (NEXT-2)
+  b.fuse_polar = ((sample_ar && !dev_x) || c->force_unfused) ? 0 : 1;
+  if (dev_x) {
+    b.xg = c->world; b.xrank = c->vr > 1 ? -1 : c->rank; b.xS = c->xS;
+    b.xmbox = c->d_xmbox_tab; b.xflag = c->d_xflag_tab; b.xepoch = c->d_xepoch;
+  }
   b.beta = sp.beta; b.sig = sp.want_sig ? c->d_sig : nullptr; b.env_trace = sp.env_trace;
   b.vprev = c->d_vprev;
   b.dbg = c->d_dbg;
@@ -690,7 +909,19 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
     b.g = make_desc(c, i);
     const bool upd = b.g.upd != 0;
     const int nu = b.g.nu;
-    b.bulk = c->bwd_bulk && M_max >= c->bulk_min_m;
+    b.bulk = perm ? 1 : 0;
+    if (perm) {
+      GateDesc &d = b.g;
+      d.perm = 1; d.sb = psb; d.blk = pblk; d.n_oth = n - nu;
+      d.chi_nat = i >= K - 2 ? 1 : 0;   // chi = the y pool
+      d.phi_nat = i == 0 ? 1 : 0;       // phi = the x pool
+      // chi changes layout every gate, so it cannot be updated in place (a
+      // group's rows in L_{i-1} belong to other groups of L_i): launch i
+      // reads buffer i & 1 and writes buffer (i - 1) & 1
+      if (!d.chi_nat) d.chi_src = View{chibuf(i), sS, Mc, 1};
+      if (upd) d.chi_dst = ViewW{chibuf(i - 1), sS, Mc, 1};
+      if (upd) d.xs = make_scatter(LY(i), LY(i).loc, nu, LY(i - 1), n);
+    }
     if (b.bulk) {
       // one CTA per SM over all starts (the ring of stages fills the SM's shared memory)
       const long long un = (N >> nu) * ((M_max + 31) / 32);
@@ -728,6 +959,9 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
     fp.n = n; fp.slots = slots;
     fp.chi = K == 1 ? ypool : View{c->d_chi, sS, Mc, 1};
     fp.x = xpool; fp.p0 = c->pairs[0]; fp.p1 = c->pairs[1]; fp.gates = c->d_gates; fp.K = K;
+    fp.sb = (perm && K > 1) ? psb : 0;  // chi after gate 0: layout L_{-1}, sample-blocked
+    fp.blk = pblk;
+    if (perm && K > 1) fp.chi = View{chibuf(-1), sS, Mc, 1};
     fp.partials = partials; fp.counters = cnt_f; fp.out_sum = csum;
     fp.nb = blocks_per_start(((long long)M_max * N) >> 2, ns);
     LaunchScope ls(c, K_FINAL, units * 32.0, units * 35.0);
@@ -938,6 +1172,34 @@ qfs_status upload_gates(qfs_ctx *c, int s, const double *init) {
   return QFS_OK;
 }
 
+// Emulated ranks (qfs_create_emulated; one start): the start's slots are the
+// ranks 0..vr-1, each with its own pool block, states and gate copy.
+void push_slots(const qfs_ctx *c, std::vector<Slot> &v, int q, int ml) {
+  for (int r = 0; r < c->vr; ++r) v.push_back({q * c->vr + r, ml});
+}
+const double *replicate_init(const qfs_ctx *c, int s, const double *init, std::vector<double> &buf) {
+  if (c->vr == 1) return init;
+  const size_t g = (size_t)c->gsz * 2;
+  buf.resize((size_t)s * c->vr * g);
+  for (int q = 0; q < s; ++q)
+    for (int r = 0; r < c->vr; ++r) std::memcpy(buf.data() + ((size_t)q * c->vr + r) * g, init + (size_t)q * g, g * sizeof(double));
+  return buf.data();
+}
+// per-slot cost sums -> per-start: the ranks' training sums add up (each holds
+// its own rows); every rank evaluates the full validation set, rank 0's is used
+void fold_sums(const qfs_ctx *c, std::vector<double> &csum, std::vector<double> &cval) {
+  if (c->vr == 1) return;
+  const size_t ns = csum.size() / c->vr;
+  for (size_t q = 0; q < ns; ++q) {
+    double t = 0.0;
+    for (int r = 0; r < c->vr; ++r) t += csum[q * c->vr + r];
+    csum[q] = t;
+    cval[q] = cval[q * c->vr];
+  }
+  csum.resize(ns);
+  cval.resize(ns);
+}
+
 }  // namespace
 qfs_status consume_staged(qfs_ctx *c);  // defined with the ABI below
 namespace {
@@ -949,6 +1211,7 @@ qfs_status check_ready(qfs_ctx *c, int s) {
   }
   if (!c->have_samples) return fail(c, QFS_ERR_STATE, "set_samples has not been called");
   if (s < 1) return fail(c, QFS_ERR_ARG, "s must be >= 1");
+  if (c->vr > 1 && s != 1) return fail(c, QFS_ERR_ARG, "emulated ranks: one start per call");
   CUDA_TRY(c, cudaSetDevice(c->device));
   return QFS_OK;
 }
@@ -1063,6 +1326,33 @@ qfs_status qfs_create_dist(int n, int k, const int32_t *pairs, int device, void 
   return QFS_OK;
 }
 
+qfs_status qfs_create_emulated(int n, int k, const int32_t *pairs, int device, int ranks, qfs_ctx **out) {
+  if (ranks < 2 || ranks > 32) return QFS_ERR_ARG;
+  qfs_status s = create_common(n, k, pairs, device, out);
+  if (s != QFS_OK) return s;
+  qfs_ctx *c = *out;
+  c->vr = ranks; c->mode = 1; c->world = ranks; c->rank = 0; c->xchg = 1;
+  return QFS_OK;
+}
+
+qfs_status qfs_set_exchange(qfs_ctx *c, int mode) {
+  if (!c) return QFS_ERR_ARG;
+  if (mode != 0 && mode != 1) return fail(c, QFS_ERR_ARG, "exchange mode must be 0 (NCCL) or 1 (device)");
+  if (c->vr > 1 && mode != 1) return fail(c, QFS_ERR_ARG, "emulated ranks exchange on the device only");
+  if (c->blocks) return fail(c, QFS_ERR_ARG, "block circuits run single-GPU");
+  if (mode == 1 && c->world > 32) return fail(c, QFS_ERR_ARG, "device exchange: at most 32 ranks");
+  if (mode == 1 && c->mode == 1 && c->world > 1 && !c->comm && c->vr == 1)
+    return fail(c, QFS_ERR_STATE, "device exchange needs the ranks' NCCL communicator");
+  if (mode != c->xchg) {
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaStreamSynchronize(c->st));
+    xchg_release(c);
+    c->xchg = mode;
+    drop_graph(c);
+  }
+  return QFS_OK;
+}
+
 qfs_status qfs_nccl_unique_id(void *id128) {
   if (!id128) return QFS_ERR_ARG;
   ncclUniqueId id;
@@ -1096,9 +1386,14 @@ static qfs_status set_samples_impl(qfs_ctx *c, int m_pool, const void *x, const 
   if (!c) return QFS_ERR_ARG;
   if (m_pool < 1 || !x || !y || v < 0 || (v > 0 && (!xv || !yv)))
     return fail(c, QFS_ERR_ARG, "bad sample arguments");
-  if ((long long)m_pool * (c->mode == 1 ? c->world : 1) > c->N)
-    return fail(c, QFS_ERR_CAPACITY, "m_pool > 2^n");
-  if (!offsets_fit(c, std::max(m_pool, v)))
+  // emulated ranks (qfs_create_emulated): the caller passes ALL pool rows; rank
+  // r keeps rows m = r (mod ranks) as its own [2^n][m_pool / ranks] block
+  const int vr = c->vr;
+  if (vr > 1 && m_pool % vr) return fail(c, QFS_ERR_CAPACITY, "emulated ranks: m_pool must be divisible by the ranks");
+  const long long m_glob = vr > 1 ? m_pool : (long long)m_pool * (c->mode == 1 ? c->world : 1);
+  if (m_glob > c->N) return fail(c, QFS_ERR_CAPACITY, "m_pool > 2^n");
+  if (vr > 1) m_pool /= vr;  // rows per rank from here on
+  if (!offsets_fit(c, std::max((long long)m_pool * vr, (long long)v)))
     return fail(c, QFS_ERR_CAPACITY, "2^n * rows * 16 B >= 4 GiB: beyond the 32-bit offsets of the streamed kernels");
   CUDA_TRY(c, cudaSetDevice(c->device));
   // the cached sweep graph holds the pool pointers: it is rebuilt only when a
@@ -1112,8 +1407,8 @@ static qfs_status set_samples_impl(qfs_ctx *c, int m_pool, const void *x, const 
   }
   if (m_pool != c->m_pool) {
     dfree(c->d_x); dfree(c->d_y);
-    CUDA_TRY(c, cudaMalloc(&c->d_x, (size_t)m_pool * c->N * sizeof(double2)));
-    CUDA_TRY(c, cudaMalloc(&c->d_y, (size_t)m_pool * c->N * sizeof(double2)));
+    CUDA_TRY(c, cudaMalloc(&c->d_x, (size_t)m_pool * vr * c->N * sizeof(double2)));
+    CUDA_TRY(c, cudaMalloc(&c->d_y, (size_t)m_pool * vr * c->N * sizeof(double2)));
     c->m_pool = 0;
   }
   if (v != c->V) {
@@ -1136,13 +1431,20 @@ static qfs_status set_samples_impl(qfs_ctx *c, int m_pool, const void *x, const 
   // by kernels: no copy-engine work that could queue behind a concurrent H2D
   const bool dev = kind == cudaMemcpyDeviceToDevice;
   for (int q = 0; q < 2; ++q) {
-    const double2 *src = (const double2 *)(q == 0 ? x : y);
-    if (!dev) {
-      CUDA_TRY(c, cudaMemcpyAsync(c->d_stage, src, m_pool * rb, kind, st));
-      src = c->d_stage;
+    const double2 *src0 = (const double2 *)(q == 0 ? x : y);
+    for (int r = 0; r < vr; ++r) {
+      const double2 *src = src0;
+      if (vr > 1) {  // rank r's rows r, r + vr, ... gathered into the stage
+        CUDA_TRY(c, cudaMemcpy2DAsync(c->d_stage, rb, src0 + (long long)r * c->N, vr * rb, rb, m_pool, kind, st));
+        src = c->d_stage;
+      } else if (!dev) {
+        CUDA_TRY(c, cudaMemcpyAsync(c->d_stage, src, m_pool * rb, kind, st));
+        src = c->d_stage;
+      }
+      CUDA_TRY(c, launch_finite_check((const double *)src, (long long)m_pool * c->N * 2, c->d_flag, st));
+      CUDA_TRY(c, launch_transpose(src, (q == 0 ? c->d_x : c->d_y) + (long long)r * m_pool * c->N, m_pool, c->N,
+                                   st));
     }
-    CUDA_TRY(c, launch_finite_check((const double *)src, (long long)m_pool * c->N * 2, c->d_flag, st));
-    CUDA_TRY(c, launch_transpose(src, q == 0 ? c->d_x : c->d_y, m_pool, c->N, st));
   }
   if (v > 0) {
     if (dev) {
@@ -1203,7 +1505,8 @@ qfs_status qfs_set_samples_async(qfs_ctx *c, int m_pool, const double *x, const 
   if (!c) return QFS_ERR_ARG;
   if (m_pool < 1 || !x || !y || v < 0 || (v > 0 && (!xv || !yv)))
     return fail(c, QFS_ERR_ARG, "bad sample arguments");
-  if ((long long)m_pool * (c->mode == 1 ? c->world : 1) > c->N) return fail(c, QFS_ERR_CAPACITY, "m_pool > 2^n");
+  if ((long long)m_pool * (c->vr > 1 ? 1 : c->mode == 1 ? c->world : 1) > c->N)
+    return fail(c, QFS_ERR_CAPACITY, "m_pool > 2^n");
   if (c->stg_count == 2) return fail(c, QFS_ERR_STATE, "two sample sets are already queued");
   CUDA_TRY(c, cudaSetDevice(c->device));
   if (!c->st_copy) CUDA_TRY(c, cudaStreamCreateWithFlags(&c->st_copy, cudaStreamNonBlocking));
@@ -1262,36 +1565,51 @@ qfs_status qfs_trace_sweeps(qfs_ctx *c, int s, const double *init_gates, int m, 
   if (m < 1 || m % wm != 0) return fail(c, QFS_ERR_CAPACITY, "M must be >= 1 and divisible by world");
   const int ml = m / wm;
   if (ml > c->m_pool) return fail(c, QFS_ERR_CAPACITY, "M exceeds the pool");
-  if ((st = ensure_gates(c, s)) != QFS_OK) return st;
-  if ((st = ensure_state(c, s, ml, c->V)) != QFS_OK) return st;
-  if ((st = upload_gates(c, s, init_gates)) != QFS_OK) return st;
-  const size_t tr = (size_t)s * c->gsz;  // gate-major: gate i of start q at s * off_i + q * d_i^2
+  const int se = s * c->vr;  // slots (emulated ranks: one per rank)
+  std::vector<double> rep;
+  if ((st = ensure_gates(c, se)) != QFS_OK) return st;
+  if ((st = ensure_state(c, se, ml, c->V)) != QFS_OK) return st;
+  if ((st = ensure_xchg(c, s)) != QFS_OK) return st;
+  if ((st = upload_gates(c, se, replicate_init(c, s, init_gates, rep))) != QFS_OK) return st;
+  const size_t tr = (size_t)se * c->gsz;  // gate-major: gate i of start q at s * off_i + q * d_i^2
   if (env_trace && tr > c->env_trace_cap) {
     dfree(c->d_env_trace);
     CUDA_TRY(c, cudaMalloc(&c->d_env_trace, tr * sizeof(double2)));
     c->env_trace_cap = tr;
   }
   SweepSpec sp;
-  for (int q = 0; q < s; ++q) sp.slots.push_back({q, ml});
-  sp.M_max = ml; sp.want_val = false; sp.beta = beta; sp.S = s; sp.want_sig = sigma_trace != nullptr;
+  for (int q = 0; q < s; ++q) push_slots(c, sp.slots, q, ml);
+  sp.M_max = ml; sp.want_val = false; sp.beta = beta; sp.S = se; sp.want_sig = sigma_trace != nullptr;
   sp.env_trace = env_trace ? c->d_env_trace : nullptr;
-  std::vector<double> csum, cval;
+  std::vector<double> csum, cval, hbuf;
+  const int vr = c->vr;
   for (int t = 0; t < n_sweeps; ++t) {
     if ((st = run_sweep(c, sp, csum, cval)) != QFS_OK) return st;
     if ((st = gate_check_result(c)) != QFS_OK) return st;
-    if (env_trace)
-      CUDA_TRY(c, cudaMemcpy(env_trace + (size_t)t * tr * 2, c->d_env_trace, tr * sizeof(double2),
-                             cudaMemcpyDeviceToHost));
+    fold_sums(c, csum, cval);
+    if (env_trace) {
+      double *dst = env_trace + (size_t)t * s * c->gsz * 2;
+      if (vr == 1) {
+        CUDA_TRY(c, cudaMemcpy(dst, c->d_env_trace, tr * sizeof(double2), cudaMemcpyDeviceToHost));
+      } else {  // [K][s vr][16] -> rank 0's [K][s][16] (pair circuits)
+        hbuf.resize(tr * 2);
+        CUDA_TRY(c, cudaMemcpy(hbuf.data(), c->d_env_trace, tr * sizeof(double2), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < c->K; ++i)
+          for (int q = 0; q < s; ++q)
+            std::memcpy(dst + ((size_t)i * s + q) * 32, hbuf.data() + ((size_t)i * se + q * vr) * 32, 32 * sizeof(double));
+      }
+    }
     if (gate_trace)
-      CUDA_TRY(c, cudaMemcpy(gate_trace + (size_t)t * s * c->gsz * 2, c->d_gates,
-                             (size_t)s * c->gsz * sizeof(double2), cudaMemcpyDeviceToHost));
+      for (int q = 0; q < s; ++q)
+        CUDA_TRY(c, cudaMemcpy(gate_trace + ((size_t)t * s + q) * c->gsz * 2, c->d_gates + (size_t)q * vr * c->gsz,
+                               (size_t)c->gsz * sizeof(double2), cudaMemcpyDeviceToHost));
     if (cost_trace)
       for (int q = 0; q < s; ++q) cost_trace[(size_t)t * s + q] = csum[q] / m;
     if (sigma_trace) {
-      std::vector<double> sg((size_t)s * c->K);
+      std::vector<double> sg((size_t)se * c->K);
       CUDA_TRY(c, cudaMemcpy(sg.data(), c->d_sig, sg.size() * sizeof(double), cudaMemcpyDeviceToHost));
       for (int i = 0; i < c->K; ++i)
-        for (int q = 0; q < s; ++q) sigma_trace[((size_t)t * c->K + i) * s + q] = sg[(size_t)q * c->K + i];
+        for (int q = 0; q < s; ++q) sigma_trace[((size_t)t * c->K + i) * s + q] = sg[(size_t)q * vr * c->K + i];
     }
   }
   return gate_check_result(c);  // n_sweeps == 0: still report invalid gates
@@ -1305,12 +1623,15 @@ qfs_status qfs_bench_sweeps(qfs_ctx *c, int s, const double *init_gates, int m, 
   if (!init_gates || n_sweeps < 1 || m < 1 || m % wm || m / wm > c->m_pool)
     return fail(c, QFS_ERR_ARG, "bad bench arguments");
   const int ml = m / wm;
-  if ((st = ensure_gates(c, s)) != QFS_OK) return st;
-  if ((st = ensure_state(c, s, ml, c->V)) != QFS_OK) return st;
-  if ((st = upload_gates(c, s, init_gates)) != QFS_OK) return st;
+  const int se = s * c->vr;
+  std::vector<double> rep;
+  if ((st = ensure_gates(c, se)) != QFS_OK) return st;
+  if ((st = ensure_state(c, se, ml, c->V)) != QFS_OK) return st;
+  if ((st = ensure_xchg(c, s)) != QFS_OK) return st;
+  if ((st = upload_gates(c, se, replicate_init(c, s, init_gates, rep))) != QFS_OK) return st;
   SweepSpec sp;
-  for (int q = 0; q < s; ++q) sp.slots.push_back({q, ml});
-  sp.M_max = ml; sp.S = s;
+  for (int q = 0; q < s; ++q) push_slots(c, sp.slots, q, ml);
+  sp.M_max = ml; sp.S = se;
   std::vector<double> csum, cval;
   cudaEvent_t e0, e1;
   CUDA_TRY(c, cudaEventCreate(&e0));
@@ -1342,8 +1663,11 @@ qfs_status qfs_instantiate(qfs_ctx *c, int s, const double *init_gates, const qf
   if (p->m_init < 1 || p->m_init > pool_g) return fail(c, QFS_ERR_CAPACITY, "m_init > m_pool");
   if (p->m_init % wm) return fail(c, QFS_ERR_CAPACITY, "m_init not divisible by world");
   if (p->max_iter < 1) return fail(c, QFS_ERR_ARG, "max_iter < 1");
-  if ((st = ensure_gates(c, s)) != QFS_OK) return st;
-  if ((st = upload_gates(c, s, init_gates)) != QFS_OK) return st;
+  const int se = s * c->vr;  // slots (emulated ranks: one per rank)
+  std::vector<double> rep;
+  if ((st = ensure_gates(c, se)) != QFS_OK) return st;
+  if ((st = ensure_xchg(c, s)) != QFS_OK) return st;
+  if ((st = upload_gates(c, se, replicate_init(c, s, init_gates, rep))) != QFS_OK) return st;
   struct S_ {
     int M, it, total, fails, restarts, term, conv_sweep;
     bool has_prev, active;
@@ -1359,20 +1683,23 @@ qfs_status qfs_instantiate(qfs_ctx *c, int s, const double *init_gates, const qf
   std::vector<double> csum, cval;
   for (int t = 1;; ++t) {
     SweepSpec sp;
-    sp.S = s; sp.beta = p->beta;
+    sp.S = se; sp.beta = p->beta;
+    std::vector<int> act;  // active starts, in slot order
     for (int q = 0; q < s; ++q)
       if (A[q].active) {
-        sp.slots.push_back({q, A[q].M / wm});
+        push_slots(c, sp.slots, q, A[q].M / wm);
+        act.push_back(q);
         sp.M_max = std::max(sp.M_max, A[q].M / wm);
       }
     sp.want_val = c->V > 0;
     bool any_conv = false, any_active = false;
     if (!sp.slots.empty()) {
-      if ((st = ensure_state(c, s, sp.M_max, c->V)) != QFS_OK) return st;
+      if ((st = ensure_state(c, se, sp.M_max, c->V)) != QFS_OK) return st;
       if ((st = run_sweep(c, sp, csum, cval)) != QFS_OK) return st;
       if ((st = gate_check_result(c)) != QFS_OK) return st;
-      for (size_t j = 0; j < sp.slots.size(); ++j) {
-        S_ &a = A[sp.slots[j].s];
+      fold_sums(c, csum, cval);
+      for (size_t j = 0; j < act.size(); ++j) {
+        S_ &a = A[act[j]];
         a.c_train = csum[j] / a.M;
         a.c_val = c->V_glob > 0 ? cval[j] / c->V_glob : NAN;
         a.it += 1; a.total += 1;                                               // step 1
@@ -1424,10 +1751,12 @@ qfs_status qfs_instantiate(qfs_ctx *c, int s, const double *init_gates, const qf
       if (A[q].c_train < bc) { bc = A[q].c_train; win = q; }
     if (win < 0) win = 0;
   }
-  CUDA_TRY(c, cudaMemcpyAsync(c->h_gates, c->d_gates, (size_t)s * c->gsz * sizeof(double2),
+  CUDA_TRY(c, cudaMemcpyAsync(c->h_gates, c->d_gates, (size_t)se * c->gsz * sizeof(double2),
                               cudaMemcpyDeviceToHost, c->st));
   CUDA_TRY(c, cudaStreamSynchronize(c->st));
-  std::memcpy(out_gates, c->h_gates, (size_t)s * c->gsz * sizeof(double2));
+  for (int q = 0; q < s; ++q)  // (emulated ranks: rank 0's copy; all ranks hold identical bits)
+    std::memcpy(out_gates + (size_t)q * c->gsz * 2, c->h_gates + (size_t)q * c->vr * c->gsz,
+                (size_t)c->gsz * sizeof(double2));
   for (int q = 0; q < s; ++q) {
     out[q].c_train = A[q].c_train; out[q].c_val = A[q].c_val; out[q].sweeps = A[q].total;
     out[q].restarts = A[q].restarts; out[q].final_m = A[q].M; out[q].term = (qfs_term)A[q].term;
@@ -1661,7 +1990,7 @@ void qfs_destroy(qfs_ctx *c) {
   drop_graph(c);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   dfree(c->d_pairs); dfree(c->d_kinds); dfree(c->d_bg); dfree(c->d_bpart); dfree(c->d_flag); dfree(c->d_x); dfree(c->d_y); dfree(c->d_xv); dfree(c->d_yv);
-  dfree(c->d_gates); dfree(c->d_chi); dfree(c->d_B); dfree(c->d_vb0); dfree(c->d_vb1);
+  dfree(c->d_gates); dfree(c->d_chi); dfree(c->d_chi2); dfree(c->d_B); dfree(c->d_vb0); dfree(c->d_vb1);
   dfree(c->d_partials); dfree(c->d_ered); dfree(c->d_sig); dfree(c->d_csum); dfree(c->d_rowout);
   dfree(c->d_cval); dfree(c->d_counters); dfree(c->d_slots); dfree(c->d_env_trace);
   dfree(c->d_stage); dfree(c->d_vprev);
@@ -1678,6 +2007,7 @@ void qfs_destroy(qfs_ctx *c) {
     if (g.ev) cudaEventDestroy(g.ev);
   }
   dfree(c->d_counters1); dfree(c->d_gpart);
+  xchg_release(c);
   if (c->h_csum) cudaFreeHost(c->h_csum);
   if (c->h_cval) cudaFreeHost(c->h_cval);
   if (c->st) cudaStreamDestroy(c->st);

@@ -14,13 +14,16 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# QFS_LIB=debug selects libqfs_debug.so (build.py --debug: device bounds checks); same ABI
-LIB_PATH = os.path.join(_HERE, "libqfs_debug.so" if os.environ.get("QFS_LIB") == "debug" else "libqfs.so")
+# QFS_LIB=debug selects libqfs_debug.so (build.py --debug: device bounds checks); QFS_LIB=<path>.so
+# an A/B build of the same sources (tools/); same ABI
+_sel = os.environ.get("QFS_LIB", "")
+LIB_PATH = (os.path.join(_HERE, "libqfs_debug.so") if _sel == "debug" else
+            os.path.abspath(_sel) if _sel.endswith(".so") else os.path.join(_HERE, "libqfs.so"))
 
 STATUS = {0: "QFS_OK", 1: "QFS_ERR_ARG", 2: "QFS_ERR_CAPACITY", 3: "QFS_ERR_NUMERIC",
           4: "QFS_ERR_DEVICE", 5: "QFS_ERR_STATE"}
 TERM_NAMES = {0: "CONVERGED", 1: "PLATEAU", 2: "MAX_ITER", 3: "POOL_EXHAUSTED", 4: "STOPPED"}
-SYMBOLS = ["qfs_create", "qfs_create_blocks", "qfs_set_structure", "qfs_create_dist", "qfs_nccl_unique_id", "qfs_create_nccl", "qfs_set_samples", "qfs_set_samples_async", "qfs_set_samples_device",
+SYMBOLS = ["qfs_create", "qfs_create_blocks", "qfs_create_emulated", "qfs_set_exchange", "qfs_set_structure", "qfs_create_dist", "qfs_nccl_unique_id", "qfs_create_nccl", "qfs_set_samples", "qfs_set_samples_async", "qfs_set_samples_device",
            "qfs_instantiate", "qfs_trace_sweeps", "qfs_bench_sweeps", "qfs_op_apply",
            "qfs_op_environment", "qfs_op_polar", "qfs_profile_enable", "qfs_profile_read", "qfs_set_path", "qfs_set_gate_kinds",
            "qfs_launch_count", "qfs_stream", "qfs_last_error", "qfs_destroy"]
@@ -70,6 +73,8 @@ def load(path: str = LIB_PATH):
         lib.qfs_set_structure.argtypes = [vp, ip, vp]
         lib.qfs_create_dist.argtypes = [ip, ip, vp, ip, vp, ip, ip, ip, ctypes.POINTER(vp)]
         lib.qfs_nccl_unique_id.argtypes = [vp]
+        lib.qfs_create_emulated.argtypes = [ip, ip, vp, ip, ip, ctypes.POINTER(vp)]
+        lib.qfs_set_exchange.argtypes = [vp, ip]
         lib.qfs_create_nccl.argtypes = [ip, ip, vp, ip, vp, ip, ip, ip, ctypes.POINTER(vp)]
         lib.qfs_set_samples.argtypes = [vp, ip, vp, vp, ip, vp, vp]
         lib.qfs_set_samples_async.argtypes = [vp, ip, vp, vp, ip, vp, vp]
@@ -116,13 +121,17 @@ class Context:
     """One qfs_ctx: a circuit structure on one device (qfs_create / qfs_create_dist /
     qfs_create_nccl when ``nccl_id`` is given)."""
 
-    def __init__(self, n, pairs, device=0, nccl_comm=None, rank=0, world=1, shard_mode=0, nccl_id=None):
+    def __init__(self, n, pairs, device=0, nccl_comm=None, rank=0, world=1, shard_mode=0, nccl_id=None,
+                 emulated_ranks=0):
         self.lib = load()
         self.n = int(n)
         self.pairs = np.ascontiguousarray(pairs, dtype=np.int32)
         self.k = int(self.pairs.shape[0])
         h = ctypes.c_void_p()
-        if nccl_id is not None:
+        if emulated_ranks:
+            rc = self.lib.qfs_create_emulated(self.n, self.k, _ptr(self.pairs), int(device), int(emulated_ranks),
+                                              ctypes.byref(h))
+        elif nccl_id is not None:
             idb = ctypes.create_string_buffer(bytes(nccl_id), 128)
             rc = self.lib.qfs_create_nccl(self.n, self.k, _ptr(self.pairs), int(device),
                                           ctypes.cast(idb, ctypes.c_void_p), int(rank), int(world),
@@ -273,6 +282,11 @@ class Context:
         self._check(self.lib.qfs_set_structure(self.h, int(pr.shape[0]), _ptr(pr)))
         self.pairs = pr
         self.k = int(pr.shape[0])
+
+    def set_exchange(self, mode):
+        """Sample mode: 0 / "nccl" host NCCL all-reduce per gate, 1 / "device" device-initiated exchange."""
+        m = {"nccl": 0, "device": 1}.get(mode, mode)
+        self._check(self.lib.qfs_set_exchange(self.h, int(m)))
 
     def set_path(self, path):
         """'auto' | 'streamed' | 'resident' (qfs_set_path)."""

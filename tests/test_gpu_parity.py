@@ -412,6 +412,7 @@ def test_sample_sharded_path_single_rank(qfs, monkeypatch):
     monkeypatch.delenv("QFS_UNFUSED_POLAR")
     ctx.set_samples(p.x, p.y, p.xv, p.yv)
     fused = qfs.Context(p.n, p.pairs, nccl_id=qfs.nccl_unique_id(), rank=0, world=1, shard_mode=1)
+    fused.set_path("streamed")           # same sweep path as the unfused context (never resident)
     fused.set_samples(p.x, p.y, p.xv, p.yv)
     l0, f0 = ctx.launch_count(), fused.launch_count()
     ctx.trace_sweeps(p.init, 32, 1)
@@ -606,3 +607,29 @@ def test_set_structure_errors():
     with pytest.raises(qfs.QfsError):
         bctx.set_structure(np.array([[0, 1]], np.int32))     # not for block circuits
     bctx.close()
+
+
+@pytest.mark.parametrize("name,init,s,m,sweeps,k", [("c4", "W", 2, 32, 3, 40), ("c4", "R", 16, 32, 2, None),
+                                                    ("c5", "R", 1, 64, 2, 60), ("c3", "R", 4, 16, 3, None),
+                                                    ("c2", "W", 4, 48, 3, None)])
+def test_trace_parity_bulk_copy_path(qfs, monkeypatch, name, init, s, m, sweeps, k):
+    """Perm mode (QFS_BWD_BULK=1): B cache and chi in per-gate
+    permuted sample-blocked layouts, the backward tiles moved by cp.async.bulk
+    into an mbarrier ring (bwdt_kernel), the forward scattered into the next
+    gates' layouts (fwdp_kernel) — equal to the oracle like the default path
+    (ragged M = 48: a partial sample block)."""
+    monkeypatch.setenv("QFS_BWD_BULK", "1")              # read when the context is created
+    p = I.make_problem(name, init=init, s=s, k=k)
+    ctx = _ctx(qfs, p.n, p.pairs, "streamed")
+    ctx.set_samples(p.x, p.y, p.xv, p.yv)
+    gt = ctx.trace_sweeps(p.init, m, sweeps)
+    pick = list(range(s)) if s <= 4 else [0, s - 1]
+    ot = oracle.trace_sweeps(p.n, p.pairs, p.init[pick], p.x, p.y, m, sweeps, threads=len(pick))
+    sub = dict(env=gt["env"][:, :, pick], gates=gt["gates"][:, pick], cost=gt["cost"][:, pick],
+               sigma=gt["sigma"][:, :, pick])
+    _compare_traces(sub, ot, f"bulk-{name}")
+    prm = dict(p.params, max_iter=2, stop_on_first=0, dist_tol=-1.0, plateau_window=0, m_init=m)
+    g1, r1, _ = ctx.instantiate(p.init, prm)
+    g2, r2, _ = oracle.instantiate(p.n, p.pairs, p.x, p.y, p.xv, p.yv, p.init[pick], prm, threads=len(pick))
+    for j, q in enumerate(pick):
+        assert abs(r1[q]["c_train"] - r2[j]["c_train"]) <= COST_TOL * r2[j]["c_train"]
