@@ -198,6 +198,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default=None, help="c1..c5, c5b, c5c (default c4; c5 with --shard sample)")
     ap.add_argument("--shard", default="multistart", choices=["multistart", "sample"])
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "device"],
+                    help="sample mode: per-gate E all-reduce by host-enqueued NCCL or device-initiated (NEXT-2)")
+    ap.add_argument("--emulate-ranks", type=int, default=0,
+                    help="sample mode on ONE GPU with G emulated ranks (device exchange; one start)")
     ap.add_argument("--starts", type=int, default=None,
                     help="multistarts per GPU (default: config S); with --shard sample: starts of the job")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -209,7 +213,10 @@ def main():
     rc = maybe_relaunch(args.gpus, sys.argv[1:])
     if rc is not None:
         sys.exit(rc)
-    sample = args.shard == "sample"
+    sample = args.shard == "sample" or args.emulate_ranks > 1
+    emul = args.emulate_ranks if args.emulate_ranks > 1 else 0
+    if emul:
+        args.exchange = "device"
     if args.config is None:
         args.config = "c5" if sample else "c4"
 
@@ -222,16 +229,22 @@ def main():
     s_per = args.starts or cfgd["s"]
     # sample mode: one job of s_per starts whose rows are split over the ranks
     s_tot = s_per if sample else s_per * world
-    m_loc = cfgd["m_init"] // world if sample else cfgd["m_init"]
-    if sample and (cfgd["m_init"] % world or cfgd["v"] % world):
-        raise SystemExit(f"--shard sample: M={cfgd['m_init']} and V={cfgd['v']} must be divisible by {world}")
+    ranks = emul or world                    # sample-mode ranks (emulated: on this one GPU)
+    m_loc = cfgd["m_init"] // ranks if sample else cfgd["m_init"]
+    if sample and (cfgd["m_init"] % ranks or cfgd["v"] % ranks):
+        raise SystemExit(f"--shard sample: M={cfgd['m_init']} and V={cfgd['v']} must be divisible by {ranks}")
+    if emul and (world > 1 or s_per != 1):
+        raise SystemExit("--emulate-ranks: one process and one start")
     config = {"workload": f"{args.config.upper()}: n={cfgd['n']} K={cfgd['k']} M={cfgd['m_init']} "
                           f"V={cfgd['v']} S={s_per}{'' if sample else '/GPU'} complex128 "
                           f"(BASELINE.json configs[{min(cfgd['cfg'], 5) - 1}])",
               "n": cfgd["n"], "k": cfgd["k"], "m": cfgd["m_init"], "v": cfgd["v"],
               "starts_per_gpu": s_per if not sample else s_per, "starts_total": s_tot,
-              "parallelism": (f"sample x{world} (M/rank={m_loc}, NCCL all-reduce of E per gate)" if sample
-                              else f"multistart x{world}"),
+              "parallelism": ((f"sample: {emul} emulated ranks on 1 GPU (M/rank={m_loc}, device-initiated "
+                               f"exchange of E per gate)") if emul else
+                              (f"sample x{world} (M/rank={m_loc}, "
+                               f"{'device-initiated exchange' if args.exchange == 'device' else 'NCCL all-reduce'}"
+                               f" of E per gate)") if sample else f"multistart x{world}"),
               "l2": "inputs larger than L2 (B cache %.1f GB/GPU > 126 MB)" % (
                   (cfgd["k"] - 1) * s_per * m_loc * (16 << cfgd["n"]) / 1e9)}
 
@@ -279,16 +292,20 @@ def main():
     init = np.ascontiguousarray(prob.init if sample else prob.init[rank * s_per:(rank + 1) * s_per])
     m = cfgd["m_init"]                      # global M (qfs_instantiate's m_init is global in sample mode)
     from paper_2405_12866_b200 import parallel as PL
-    rows = PL.sample_rows(prob.x.shape[0], rank, world) if sample else slice(None)
-    vrows = PL.sample_rows(prob.xv.shape[0], rank, world) if sample else slice(None)
+    rows = PL.sample_rows(prob.x.shape[0], rank, world) if sample and not emul else slice(None)
+    vrows = PL.sample_rows(prob.xv.shape[0], rank, world) if sample and not emul else slice(None)
     lx, ly = np.ascontiguousarray(prob.x[rows]), np.ascontiguousarray(prob.y[rows])
     lxv, lyv = np.ascontiguousarray(prob.xv[vrows]), np.ascontiguousarray(prob.yv[vrows])
-    if sample:
+    if emul:
+        ctx = qfs.Context(prob.n, prob.pairs, device=local, emulated_ranks=emul)
+    elif sample:
         # the library owns the NCCL communicator: rank 0's unique id, broadcast over torch.distributed
         obj = [qfs.nccl_unique_id() if rank == 0 else None]
         if world > 1:
             dist.broadcast_object_list(obj, src=0)
         ctx = qfs.Context(prob.n, prob.pairs, device=local, nccl_id=obj[0], rank=rank, world=world, shard_mode=1)
+        if args.exchange == "device":
+            ctx.set_exchange(1)
     else:
         ctx = qfs.Context(prob.n, prob.pairs, device=local)
     ctx.set_samples(lx, ly, lxv, lyv)

@@ -79,13 +79,13 @@ struct BwdParams {
   int bulk;                   // 1: bwdt_kernel (bulk copies + mbarrier ring), 0: bwd_kernel (LDGSTS)
   // Device-initiated exchange of the partial environments across the xg ranks
   // of sample mode, done by the last CTA of each start
-  // before its polar update: store E into every rank's mailbox, raise a flag
-  // there, wait for all ranks' flags, sum the xg partials in rank order.
+  // before its polar update: store E into every rank's mailbox as
+  // self-validating (32-bit half, epoch) words, wait until all ranks' words of
+  // this epoch have landed, sum the xg partials in rank order.
   int xg;                              // > 1: exchange on; ranks
   int xrank;                           // this context's rank; -1: emulated ranks (rank = slot start index)
   int xS;                              // starts per mailbox
-  double *const *xmbox;                // [xg] rank q's mailbox [2 parity][xg src][xS][32]
-  unsigned long long *const *xflag;    // [xg] rank q's flags [xg src][xS] (epoch of the last write)
+  unsigned long long *const *xmbox;    // [xg] rank q's mailbox [2 parity][xg src][xS][64 words]
   unsigned long long *xepoch;          // this context's epoch counters [xS] (emulated: [xg][xS])
   double beta;
   double *sig;                // [S][K] sum sigma, or nullptr

@@ -437,12 +437,16 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
 // mode (NEXT-2; E is a sum over samples, so the ranks' partials add
 // up to the full E).  Warp 0 of the last CTA of start s, lane = real / imag
 // part of entry lane / 2.  Each rank writes its partial into parity slot
-// (epoch & 1) of EVERY rank's mailbox (peer stores over NVLink; emulated ranks:
-// local memory), releases a per-(source, start) epoch flag there, waits until
-// all ranks' flags for this epoch are up, and sums the partials in rank order
-// — so every rank gets identical bits and computes the identical polar
-// update.  Two parity slots suffice: a rank writes epoch t+2 only after every
-// rank raised its flag for t+1, which each does only after reading epoch t.
+// (epoch & 1) of EVERY rank's mailbox (peer stores over NVLink; emulated
+// ranks: local memory) as two 8-byte words per value, each word = one 32-bit
+// half of the double | the 32-bit epoch (the LL protocol: an aligned 8-byte
+// store is single-copy atomic, so a word carrying this epoch is complete and
+// no memory fence sits on the path — measured: system-scope fences cost ~11 us
+// per gate here).  Every rank then polls its own mailbox until all words of
+// this epoch have landed and sums the partials in rank order: identical bits
+// on all ranks, identical polar updates.  Two parity slots suffice: a rank
+// writes epoch t+2 only after it has read every rank's epoch t+1 words, which
+// each rank writes only after finishing its epoch t reads.
 __device__ double xchg_env(const BwdParams &P, int s, double e) {
   const int lane = threadIdx.x & 31;
   const int r = P.xrank >= 0 ? P.xrank : s;   // emulated: the slot's start index is its rank
@@ -454,17 +458,32 @@ __device__ double xchg_env(const BwdParams &P, int s, double e) {
     *ep = epn;
   }
   epn = __shfl_sync(FULL, epn, 0);
+  const unsigned long long tag = (epn & 0xffffffffull) << 32;
   const long long par = (long long)(epn & 1ull);
-  for (int q = 0; q < P.xg; ++q) P.xmbox[q][((par * P.xg + r) * P.xS + sx) * 32 + lane] = e;
-  __threadfence_system();
-  __syncwarp();
-  if (lane < P.xg) st_release_sys(P.xflag[lane] + (long long)r * P.xS + sx, epn);
-  if (lane < P.xg)
-    while (ld_acquire_sys(P.xflag[r] + (long long)lane * P.xS + sx) < epn) __nanosleep(32);
-  __syncwarp();
-  __threadfence_system();
+#ifdef QFS_XCHG_FORCE_SYS  // measurement build: system scope for emulated ranks too
+  const bool local = false;
+#else
+  const bool local = P.xrank < 0;  // real ranks: peer memory over NVLink, system scope
+#endif
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(e);
+  const unsigned long long w0 = (bits & 0xffffffffull) | tag, w1 = (bits >> 32) | tag;
+  for (int q = 0; q < P.xg; ++q) {
+    unsigned long long *dst = P.xmbox[q] + ((par * P.xg + r) * P.xS + sx) * 64 + 2 * lane;
+    if (local) st_ll_gpu(dst, w0, w1);
+    else st_ll_sys(dst, w0, w1);
+  }
   double t = 0.0;
-  for (int q = 0; q < P.xg; ++q) t += ld_relaxed_sys(P.xmbox[r] + ((par * P.xg + q) * P.xS + sx) * 32 + lane);
+  for (int q = 0; q < P.xg; ++q) {  // rank order: identical sums everywhere
+    const unsigned long long *src = P.xmbox[r] + ((par * P.xg + q) * P.xS + sx) * 64 + 2 * lane;
+    unsigned long long a, b;
+    for (;;) {
+      if (local) ld_ll_gpu(src, a, b);
+      else ld_ll_sys(src, a, b);
+      if ((a & 0xffffffff00000000ull) == tag && (b & 0xffffffff00000000ull) == tag) break;
+      __nanosleep(8);
+    }
+    t += __longlong_as_double((long long)((a & 0xffffffffull) | (b << 32)));
+  }
   return t;
 }
 

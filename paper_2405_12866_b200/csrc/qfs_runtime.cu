@@ -88,11 +88,9 @@ struct qfs_ctx {
   int vr = 1;       // emulated ranks on this device (qfs_create_emulated); 1 otherwise
   int xchg = 0;     // 0: host-enqueued NCCL all-reduce + polar launch per gate; 1: device exchange
   int xS = 0;       // starts the mailboxes were sized for
-  double *d_xmbox = nullptr;              // own mailbox + flags block (emulated: every rank's)
-  unsigned long long *d_xflag = nullptr;  // (inside d_xmbox's allocation)
+  unsigned long long *d_xmbox = nullptr;  // own mailbox (emulated: every rank's)
   unsigned long long *d_xepoch = nullptr;
-  double **d_xmbox_tab = nullptr;         // [world] rank q's mailbox (IPC-mapped peers)
-  unsigned long long **d_xflag_tab = nullptr;
+  unsigned long long **d_xmbox_tab = nullptr;  // [world] rank q's mailbox (IPC-mapped peers)
   std::vector<void *> x_mapped;           // IPC-opened peer blocks
   double2 *d_vprev = nullptr;  // [S][K][16] right singular vectors of the last polar step (warm start)
   double2 *d_gates = nullptr, *d_chi = nullptr, *d_B = nullptr, *d_vb0 = nullptr, *d_vb1 = nullptr;
@@ -410,14 +408,12 @@ qfs_status ensure_state(qfs_ctx *c, int S, int M, int V) {
 void xchg_release(qfs_ctx *c) {
   for (void *p : c->x_mapped) cudaIpcCloseMemHandle(p);
   c->x_mapped.clear();
-  dfree(c->d_xmbox); dfree(c->d_xepoch); dfree(c->d_xmbox_tab); dfree(c->d_xflag_tab);
-  c->d_xflag = nullptr;
+  dfree(c->d_xmbox); dfree(c->d_xepoch); dfree(c->d_xmbox_tab);
   c->xS = 0;
 }
 
 // Mailboxes of the device-initiated exchange (sample mode, qfs_set_exchange):
-// per rank a block [2 parity][world src][S][32] doubles + flags [world src][S]
-// (epochs), zeroed; emulated ranks: all blocks in one local allocation;
+// per rank a block [2 parity][world src][S][64] self-validating words, zeroed; emulated ranks: all blocks in one local allocation;
 // real ranks: each rank's own block, CUDA-IPC handles all-gathered over the
 // context's NCCL communicator and the peers' blocks mapped (peer stores over
 // NVLink).  Collective over the ranks (called in the same order by all).
@@ -431,23 +427,17 @@ qfs_status ensure_xchg(qfs_ctx *c, int S) {
   }
   xchg_release(c);
   drop_graph(c);
-  const size_t mb = (size_t)2 * g * S * 32 * sizeof(double), fb = (size_t)g * S * sizeof(unsigned long long);
-  const size_t blk = (mb + fb + 255) / 256 * 256;
+  const size_t blk = ((size_t)2 * g * S * 64 * sizeof(unsigned long long) + 255) / 256 * 256;
   const int nblk = c->vr > 1 ? g : 1;
   char *base = nullptr;
   CUDA_TRY(c, cudaMalloc(&base, blk * nblk));
-  CUDA_TRY(c, cudaMemsetAsync(base, 0, blk * nblk, c->st));
-  c->d_xmbox = (double *)base;
-  c->d_xflag = (unsigned long long *)(base + mb);
+  CUDA_TRY(c, cudaMemsetAsync(base, 0, blk * nblk, c->st));  // epoch 0: no valid word
+  c->d_xmbox = (unsigned long long *)base;
   CUDA_TRY(c, cudaMalloc(&c->d_xepoch, (size_t)nblk * S * sizeof(unsigned long long)));
   CUDA_TRY(c, cudaMemsetAsync(c->d_xepoch, 0, (size_t)nblk * S * sizeof(unsigned long long), c->st));
-  std::vector<double *> mt(g);
-  std::vector<unsigned long long *> ft(g);
+  std::vector<unsigned long long *> mt(g);
   if (c->vr > 1) {
-    for (int q = 0; q < g; ++q) {
-      mt[q] = (double *)(base + q * blk);
-      ft[q] = (unsigned long long *)(base + q * blk + mb);
-    }
+    for (int q = 0; q < g; ++q) mt[q] = (unsigned long long *)(base + q * blk);
   } else {
     if (!c->comm) return fail(c, QFS_ERR_STATE, "device exchange needs the NCCL communicator of the ranks");
     cudaIpcMemHandle_t h;
@@ -469,14 +459,11 @@ qfs_status ensure_xchg(qfs_ctx *c, int S) {
         c->x_mapped.push_back(mp);
         pq = (char *)mp;
       }
-      mt[q] = (double *)pq;
-      ft[q] = (unsigned long long *)(pq + mb);
+      mt[q] = (unsigned long long *)pq;
     }
   }
-  CUDA_TRY(c, cudaMalloc(&c->d_xmbox_tab, g * sizeof(double *)));
-  CUDA_TRY(c, cudaMalloc(&c->d_xflag_tab, g * sizeof(unsigned long long *)));
-  CUDA_TRY(c, cudaMemcpyAsync(c->d_xmbox_tab, mt.data(), g * sizeof(double *), cudaMemcpyHostToDevice, c->st));
-  CUDA_TRY(c, cudaMemcpyAsync(c->d_xflag_tab, ft.data(), g * sizeof(unsigned long long *), cudaMemcpyHostToDevice,
+  CUDA_TRY(c, cudaMalloc(&c->d_xmbox_tab, g * sizeof(unsigned long long *)));
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_xmbox_tab, mt.data(), g * sizeof(unsigned long long *), cudaMemcpyHostToDevice,
                               c->st));
   CUDA_TRY(c, cudaStreamSynchronize(c->st));
   if (c->comm) {  // every rank's zeroed mailbox exists before anyone writes into it
@@ -893,7 +880,7 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
   b.fuse_polar = ((sample_ar && !dev_x) || c->force_unfused) ? 0 : 1;
   if (dev_x) {
     b.xg = c->world; b.xrank = c->vr > 1 ? -1 : c->rank; b.xS = c->xS;
-    b.xmbox = c->d_xmbox_tab; b.xflag = c->d_xflag_tab; b.xepoch = c->d_xepoch;
+    b.xmbox = c->d_xmbox_tab; b.xepoch = c->d_xepoch;
   }
   b.beta = sp.beta; b.sig = sp.want_sig ? c->d_sig : nullptr; b.env_trace = sp.env_trace;
   b.vprev = c->d_vprev;
