@@ -174,6 +174,19 @@ qfs_status qfs_set_samples(qfs_ctx *c, int m_pool, const double *x, const double
 qfs_status qfs_set_samples_async(qfs_ctx *c, int m_pool, const double *x, const double *y, int v,
                                  const double *xv, const double *yv);
 
+/* QFactor's full-unitary inputs without storing them (
+ * with M = 2^n orthonormal inputs the sample cost is the full
+ * Hilbert-Schmidt cost): training input m is the computational basis state
+ * x_m = e_m (|m>, little-endian) for m < m_pool, generated inside the kernels
+ * that read x (the first forward pass, gate 0's environment, the sweep-end
+ * cost) — the 2^n x m_pool x pool is never stored or copied.  y [m_pool][2^n][2]
+ * holds the targets y_m = U e_m (the columns of U; host, copied); validation as
+ * qfs_set_samples.  Pair contexts on one rank only (QFS_ERR_ARG in sample mode,
+ * for emulated ranks or block circuits); the sweep runs on the streamed path.
+ * A later qfs_set_samples returns to stored inputs. */
+qfs_status qfs_set_samples_basis(qfs_ctx *c, int m_pool, const double *y, int v, const double *xv,
+                                 const double *yv);
+
 /* Same, from DEVICE pointers (e.g. torch CUDA tensors) on cuda_stream
  * (cudaStream_t, NULL = legacy default stream).  Copies device-to-device. */
 qfs_status qfs_set_samples_device(qfs_ctx *c, int m_pool, const void *dx, const void *dy, int v,

@@ -22,6 +22,7 @@ struct Slot {
 struct View {
   const double2 *base;
   long long ss, sa, sm;
+  int ident;  // 1: the implicit computational basis (qfs_set_samples_basis): element (a, m) = [a == m]; base unused
 };
 struct ViewW {
   double2 *base;

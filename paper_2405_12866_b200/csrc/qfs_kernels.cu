@@ -199,19 +199,22 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
 
   const unsigned ustart = beg + warp;
   const int iters = ustart < end ? (int)((end - ustart + NWARP - 1) / NWARP) : 0;
+  unsigned lg = 0, lm = 0;  // group base amplitude and sample of the last located item (implicit basis phi)
   auto locate = [&](int k, unsigned &ec, unsigned &ed, unsigned &ef) -> bool {
     const unsigned u = ustart + (unsigned)k * NWARP;
     if (k >= iters) return false;
     unsigned g = fdu.div(u);
     const unsigned m = (u - g * nmb) * LPT + ml;
+    lm = m;
 #pragma unroll
     for (int q = 0; q < NU; ++q) g = insert_zero32(g, ins[q]);
+    lg = g;
     ec = g * csa + m;
     ed = g * dsa + m;
     ef = g * fsa + m;
     // every member offset stays inside one start's [2^n][sa] block (32-bit guard, runtime offsets_fit)
     QFS_DASSERT(m >= Ms || ((unsigned long long)(g | (unsigned)G.off[(1 << NU) - 1]) << 0) < (1ull << P.n));
-    QFS_DASSERT(m >= Ms || (unsigned long long)(g + (unsigned)G.off[(1 << NU) - 1]) * fsa + m < ((unsigned long long)fsa << P.n));
+    QFS_DASSERT(m >= Ms || G.phi.ident || (unsigned long long)(g + (unsigned)G.off[(1 << NU) - 1]) * fsa + m < ((unsigned long long)fsa << P.n));
     return m < Ms;
   };
   // chi destination offset of the items in flight (EDRING: computed once, at
@@ -237,7 +240,13 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
 #pragma unroll
       for (int l = 0; l < 4; ++l) cp_async16(st + l * BWD_THREADS, cbase + (eb + (offc[l] << 4)), ok);
     }
-    if (phi) {
+    if (phi && G.phi.ident) {  // implicit basis x_m = e_m (gate 0 of a QF sweep): synthesised, not loaded
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        const unsigned a = lg + (unsigned)G.off[XPOSE ? (t + 4 * (t ^ l)) : (4 * t + l)];
+        st[(4 + l) * BWD_THREADS] = make_double2(ok && a == lm ? 1.0 : 0.0, 0.0);
+      }
+    } else if (phi) {
       const unsigned eb = ef << 4;
 #pragma unroll
       for (int l = 0; l < 4; ++l) cp_async16(st + (4 + l) * BWD_THREADS, fbase + (eb + (offf[l] << 4)), ok);
@@ -983,7 +992,7 @@ __global__ void __launch_bounds__(RED_THREADS, 4) final_kernel(const FinalParams
     const unsigned q = fdm.div(w);
     const unsigned m = w - q * Ms;
     const unsigned base = insert_zero32(insert_zero32(q, lo), hi);
-    const double2 *xp = xb + (long long)base * P.x.sa + (long long)m * P.x.sm;
+    const double2 *xp = P.x.ident ? nullptr : xb + (long long)base * P.x.sa + (long long)m * P.x.sm;
     double2 v[4], xv[4];
     if (P.sb > 0) {  // perm mode: chi sample-blocked, natural rows (layout L_{-1})
       const double2 *cp = cb + (long long)(m / P.sb) * P.blk + (long long)base * P.sb + m % P.sb;
@@ -995,7 +1004,8 @@ __global__ void __launch_bounds__(RED_THREADS, 4) final_kernel(const FinalParams
       for (int l = 0; l < 4; ++l) v[l] = cp[(long long)o[l] * P.chi.sa];
     }
 #pragma unroll
-    for (int l = 0; l < 4; ++l) xv[l] = __ldcs(xp + (long long)o[l] * P.x.sa);
+    for (int l = 0; l < 4; ++l)
+      xv[l] = P.x.ident ? make_double2(base + o[l] == m ? 1.0 : 0.0, 0.0) : __ldcs(xp + (long long)o[l] * P.x.sa);
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
       double2 r = make_double2(0.0, 0.0);
@@ -1067,7 +1077,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 3) fwd_gate_kernel(const FwdGateP
     const bool ok = locate(k, base, m);
     double2 *stp = fstage + (k % FWD_STAGES) * 4 * FWD_THREADS + threadIdx.x;
     const double2 *sp = src + (long long)base * P.src.sa + (long long)m * P.src.sm;
-    if (cm & 2) {
+    if (P.src.ident) {  // implicit basis x_m = e_m
+      const unsigned ob[4] = {0u, 1u << P.p0, 1u << P.p1, (1u << P.p0) | (1u << P.p1)};
+#pragma unroll
+      for (int l = 0; l < 4; ++l) stp[l * FWD_THREADS] = make_double2(ok && base + ob[l] == m ? 1.0 : 0.0, 0.0);
+    } else if (cm & 2) {
 #pragma unroll
       for (int l = 0; l < 4; ++l) cp_async16_hint(stp + l * FWD_THREADS, ok ? sp + soff[l] : src, ok, pol_ld);
     } else {
@@ -1151,7 +1165,7 @@ __global__ void __launch_bounds__(FWD_THREADS, QFS_FWD2_MINB) fwd2_kernel(const 
     const unsigned m = w - g * Ms;
 #pragma unroll
     for (int q = 0; q < NU; ++q) g = insert_zero32(g, ins[q]);
-    QFS_DASSERT((unsigned long long)(g + (unsigned)P.off[(1 << NU) - 1]) * ssa + m < ((unsigned long long)ssa << P.n));
+    QFS_DASSERT(P.src.ident || (unsigned long long)(g + (unsigned)P.off[(1 << NU) - 1]) * ssa + m < ((unsigned long long)ssa << P.n));
     return make_uint2(g, m);
   };
 #if QFS_FWD2_HINT
@@ -1159,6 +1173,11 @@ __global__ void __launch_bounds__(FWD_THREADS, QFS_FWD2_MINB) fwd2_kernel(const 
 #endif
   auto load = [&](unsigned w, double2 *v) {
     const uint2 gm = locate(w);
+    if (P.src.ident) {  // implicit basis x_m = e_m (the first pass of a QF sweep)
+#pragma unroll
+      for (int u = 0; u < NV; ++u) v[u] = make_double2(gm.x + (unsigned)P.off[u] == gm.y ? 1.0 : 0.0, 0.0);
+      return;
+    }
     const double2 *sp = src + (gm.x * ssa + gm.y);
 #pragma unroll
     for (int u = 0; u < NV; ++u) {

@@ -85,6 +85,7 @@ struct qfs_ctx {
   int bulk_min_m = 16;         // QFS_BULK_MIN_M: smallest M_max that takes the bulk-copy backward
   int V_glob = 0;   // validation rows over all ranks (sample mode: sum of the ranks' V)
   // sample mode, device-initiated exchange of E (qfs_set_exchange / NEXT-2)
+  bool x_basis = false;  // qfs_set_samples_basis: x_m = e_m implicit (QFactor's full basis, NEXT-1); d_x unused
   int vr = 1;       // emulated ranks on this device (qfs_create_emulated); 1 otherwise
   int xchg = 0;     // 0: host-enqueued NCCL all-reduce + polar launch per gate; 1: device exchange
   int xS = 0;       // starts the mailboxes were sized for
@@ -490,6 +491,7 @@ struct SweepSpec {
 // The transposed pools [2^n][m_pool]; with emulated ranks one such block per
 // rank (rank r = slot start r, qfs_create_emulated: one start only).
 View pool_view(const qfs_ctx *c, const double2 *base) {
+  if (base == c->d_x && c->x_basis) return View{nullptr, 0, 0, 0, 1};  // implicit x_m = e_m
   return View{base, c->vr > 1 ? c->N * c->m_pool : 0, c->m_pool, 1};
 }
 
@@ -603,7 +605,8 @@ struct ResPlan {
   size_t smem = 0;
 };
 bool res_plan(const qfs_ctx *c, int M_max, int ns, ResPlan &pl) {
-  if (c->path == 1 || (c->mode == 1 && c->world > 1) || c->force_unfused || c->n > 13 || M_max < 1) return false;
+  if (c->path == 1 || (c->mode == 1 && c->world > 1) || c->force_unfused || c->x_basis || c->n > 13 || M_max < 1)
+    return false;
   // auto: resident only up to n = 10 — measured crossover (profiles/r1_sweep_map.jsonl:
   // n <= 10 resident 1.3-1.9x faster, n = 11 / 12 streamed 1.14x / 1.40x faster)
   if (c->path == 0 && c->n > 10) return false;
@@ -762,7 +765,7 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
   for (int j = j0; j < j1; ++j) units += (double)sp.slots[j].m * (double)N;
   // perm mode (bulk-copy backward): B cache and chi in the per-gate permuted
   // sample-blocked layouts L_i (qfs_internal.h); else natural sample-minor
-  const bool perm = c->bwd_bulk && M_max >= c->bulk_min_m && M_max >= 16;
+  const bool perm = c->bwd_bulk && M_max >= c->bulk_min_m && M_max >= 16 && !c->x_basis;
   const int psb = c->M_cap >= 32 ? 32 : 16;
   const long long pblk = N * psb;
   std::vector<Lay> lays;
@@ -1371,8 +1374,11 @@ static qfs_status set_samples_impl(qfs_ctx *c, int m_pool, const void *x, const 
                                    const void *xv, const void *yv, cudaMemcpyKind kind,
                                    cudaStream_t ust) {
   if (!c) return QFS_ERR_ARG;
-  if (m_pool < 1 || !x || !y || v < 0 || (v > 0 && (!xv || !yv)))
+  const bool basis = x == nullptr;  // qfs_set_samples_basis: x_m = e_m (computational basis), not stored
+  if (m_pool < 1 || !y || v < 0 || (v > 0 && (!xv || !yv)))
     return fail(c, QFS_ERR_ARG, "bad sample arguments");
+  if (basis && (c->mode == 1 || c->vr > 1 || c->blocks))
+    return fail(c, QFS_ERR_ARG, "implicit basis inputs: single-rank pair contexts only");
   // emulated ranks (qfs_create_emulated): the caller passes ALL pool rows; rank
   // r keeps rows m = r (mod ranks) as its own [2^n][m_pool / ranks] block
   const int vr = c->vr;
@@ -1387,17 +1393,18 @@ static qfs_status set_samples_impl(qfs_ctx *c, int m_pool, const void *x, const 
   // buffer is reallocated (same shapes: the new contents are used in place).
   // Dropped BEFORE any buffer is freed, so an early return below (non-finite
   // sample, allocation failure) can never leave a graph over freed pools.
-  const bool realloc = m_pool != c->m_pool || v != c->V;
+  const bool realloc = m_pool != c->m_pool || v != c->V || basis != c->x_basis;
   if (realloc) {
     CUDA_TRY(c, cudaStreamSynchronize(c->st));
     drop_graph(c);
   }
-  if (m_pool != c->m_pool) {
+  if (m_pool != c->m_pool || basis != c->x_basis || (!basis && !c->d_x)) {
     dfree(c->d_x); dfree(c->d_y);
-    CUDA_TRY(c, cudaMalloc(&c->d_x, (size_t)m_pool * vr * c->N * sizeof(double2)));
+    if (!basis) CUDA_TRY(c, cudaMalloc(&c->d_x, (size_t)m_pool * vr * c->N * sizeof(double2)));
     CUDA_TRY(c, cudaMalloc(&c->d_y, (size_t)m_pool * vr * c->N * sizeof(double2)));
     c->m_pool = 0;
   }
+  c->x_basis = basis;
   if (v != c->V) {
     dfree(c->d_xv); dfree(c->d_yv);
     if (v > 0) {
@@ -1417,7 +1424,7 @@ static qfs_status set_samples_impl(qfs_ctx *c, int m_pool, const void *x, const 
   // device sources (qfs_set_samples_device, queued async sets) are read in place
   // by kernels: no copy-engine work that could queue behind a concurrent H2D
   const bool dev = kind == cudaMemcpyDeviceToDevice;
-  for (int q = 0; q < 2; ++q) {
+  for (int q = basis ? 1 : 0; q < 2; ++q) {
     const double2 *src0 = (const double2 *)(q == 0 ? x : y);
     for (int r = 0; r < vr; ++r) {
       const double2 *src = src0;
@@ -1533,11 +1540,20 @@ qfs_status qfs_set_samples_async(qfs_ctx *c, int m_pool, const double *x, const 
 
 qfs_status qfs_set_samples(qfs_ctx *c, int m_pool, const double *x, const double *y, int v,
                            const double *xv, const double *yv) {
+  if (c && !x) return fail(c, QFS_ERR_ARG, "bad sample arguments");
   return set_samples_impl(c, m_pool, x, y, v, xv, yv, cudaMemcpyHostToDevice, nullptr);
+}
+
+qfs_status qfs_set_samples_basis(qfs_ctx *c, int m_pool, const double *y, int v, const double *xv,
+                                 const double *yv) {
+  if (!c) return QFS_ERR_ARG;
+  if (!y) return fail(c, QFS_ERR_ARG, "bad sample arguments");
+  return set_samples_impl(c, m_pool, nullptr, y, v, xv, yv, cudaMemcpyHostToDevice, nullptr);
 }
 
 qfs_status qfs_set_samples_device(qfs_ctx *c, int m_pool, const void *dx, const void *dy, int v,
                                   const void *dxv, const void *dyv, void *cuda_stream) {
+  if (c && !dx) return fail(c, QFS_ERR_ARG, "bad sample arguments");
   return set_samples_impl(c, m_pool, dx, dy, v, dxv, dyv, cudaMemcpyDeviceToDevice,
                           (cudaStream_t)cuda_stream);
 }

@@ -23,7 +23,7 @@ LIB_PATH = (os.path.join(_HERE, "libqfs_debug.so") if _sel == "debug" else
 STATUS = {0: "QFS_OK", 1: "QFS_ERR_ARG", 2: "QFS_ERR_CAPACITY", 3: "QFS_ERR_NUMERIC",
           4: "QFS_ERR_DEVICE", 5: "QFS_ERR_STATE"}
 TERM_NAMES = {0: "CONVERGED", 1: "PLATEAU", 2: "MAX_ITER", 3: "POOL_EXHAUSTED", 4: "STOPPED"}
-SYMBOLS = ["qfs_create", "qfs_create_blocks", "qfs_create_emulated", "qfs_set_exchange", "qfs_set_structure", "qfs_create_dist", "qfs_nccl_unique_id", "qfs_create_nccl", "qfs_set_samples", "qfs_set_samples_async", "qfs_set_samples_device",
+SYMBOLS = ["qfs_create", "qfs_create_blocks", "qfs_create_emulated", "qfs_set_exchange", "qfs_set_samples_basis", "qfs_set_structure", "qfs_create_dist", "qfs_nccl_unique_id", "qfs_create_nccl", "qfs_set_samples", "qfs_set_samples_async", "qfs_set_samples_device",
            "qfs_instantiate", "qfs_trace_sweeps", "qfs_bench_sweeps", "qfs_op_apply",
            "qfs_op_environment", "qfs_op_polar", "qfs_profile_enable", "qfs_profile_read", "qfs_set_path", "qfs_set_gate_kinds",
            "qfs_launch_count", "qfs_stream", "qfs_last_error", "qfs_destroy"]
@@ -75,6 +75,7 @@ def load(path: str = LIB_PATH):
         lib.qfs_nccl_unique_id.argtypes = [vp]
         lib.qfs_create_emulated.argtypes = [ip, ip, vp, ip, ip, ctypes.POINTER(vp)]
         lib.qfs_set_exchange.argtypes = [vp, ip]
+        lib.qfs_set_samples_basis.argtypes = [vp, ip, vp, ip, vp, vp]
         lib.qfs_create_nccl.argtypes = [ip, ip, vp, ip, vp, ip, ip, ip, ctypes.POINTER(vp)]
         lib.qfs_set_samples.argtypes = [vp, ip, vp, vp, ip, vp, vp]
         lib.qfs_set_samples_async.argtypes = [vp, ip, vp, vp, ip, vp, vp]
@@ -177,6 +178,16 @@ class Context:
         yv = _c128(yv) if v else None
         self._keep = (x, y, xv, yv)
         self._check(self.lib.qfs_set_samples(self.h, x.shape[0], _ptr(x), _ptr(y), v, _ptr(xv), _ptr(yv)))
+
+    def set_samples_basis(self, y, xv=None, yv=None):
+        """qfs_set_samples_basis: training inputs x_m = e_m (implicit, never stored),
+        y [m_pool][2^n] their images (the first m_pool columns of U, as rows)."""
+        y = _c128(y)
+        v = 0 if xv is None else int(np.asarray(xv).shape[0])
+        xv = _c128(xv) if v else None
+        yv = _c128(yv) if v else None
+        self._keep = (y, xv, yv)
+        self._check(self.lib.qfs_set_samples_basis(self.h, y.shape[0], _ptr(y), v, _ptr(xv), _ptr(yv)))
 
     def set_samples_host_ptr(self, m_pool, px, py, v, pxv, pyv):
         """Raw host pointers (e.g. pinned torch tensors' data_ptr())."""

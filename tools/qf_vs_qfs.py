@@ -5,8 +5,9 @@ QFS-J on A100) on synthetic solvable block circuits, both modes through the
 same libqfs (qfs_instantiate):
 
   QF  : training inputs = the computational basis (M = 2^n: the sample
-        cost is then the full Hilbert-Schmidt cost), no validation, QFactor's
-        single-iteration plateau rule (plateau_window = 1)
+        cost is then the full Hilbert-Schmidt cost), IMPLICIT (qfs_set_samples_basis:
+        x_m = e_m generated in the kernels, only y = U's columns stored), no
+        validation, QFactor's single-iteration plateau rule (plateau_window = 1)
   QFS : Haar training states, number_of_training_states = 2, double-and-restart
         on overtrain_ratio = 0.1 with min(16, 2^n) validation states, plateau window 5
 
@@ -37,8 +38,9 @@ def problem(n, k, s):
     init = np.stack([np.stack([I.warm_gate(I.rng_for(CFG + n, 3, st), target[j], 0.3) for j in range(k)])
                      for st in range(s)])
     basis = np.eye(N, dtype=np.complex128)
-    qf = dict(x=basis, y=I.apply_circuit_tensor(n, pairs, target, basis))
-    xs = I.haar_states(I.rng_for(CFG + n, 1, 0), n, N)
+    qf = dict(y=I.apply_circuit_tensor(n, pairs, target, basis))
+    del basis
+    xs = I.haar_states(I.rng_for(CFG + n, 1, 0), n, min(N, 512))   # QFS pool (final M was <= 32 at n >= 9)
     xv = I.haar_states(I.rng_for(CFG + n, 2, 0), n, min(16, N))
     qs = dict(x=xs, y=I.apply_circuit_tensor(n, pairs, target, xs), xv=xv,
               yv=I.apply_circuit_tensor(n, pairs, target, xv))
@@ -58,7 +60,7 @@ def run(ctx, init, prm):
 
 def main():
     build.build()
-    ns = [int(a) for a in sys.argv[1:]] or list(range(3, 13))
+    ns = [int(a) for a in sys.argv[1:]] or list(range(3, 14))
     s = 4
     base = dict(dist_tol=1e-10, diff_tol_r=1e-3, min_iter=6, max_iter=3000, beta=0.0, stop_on_first=1)
     for n in ns:
@@ -66,7 +68,7 @@ def main():
         pairs, init, qf, qs = problem(n, k, s)
         N = 1 << n
         ctx = qfs.Context(n, pairs)
-        ctx.set_samples(qf["x"], qf["y"])
+        ctx.set_samples_basis(qf["y"])
         r_qf = run(ctx, init, dict(base, plateau_window=1, m_init=N, overtrain_ratio=1e300))
         ctx.close()
         ctx = qfs.Context(n, pairs)
