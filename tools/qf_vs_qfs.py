@@ -61,10 +61,10 @@ def run(ctx, init, prm):
 def main():
     build.build()
     ns = [int(a) for a in sys.argv[1:]] or list(range(3, 14))
-    s = 4
     base = dict(dist_tol=1e-10, diff_tol_r=1e-3, min_iter=6, max_iter=3000, beta=0.0, stop_on_first=1)
     for n in ns:
         k = 4 * n
+        s = 4 if n <= 12 else 1   # n = 13: the QF B cache is (K-1) GB per start
         pairs, init, qf, qs = problem(n, k, s)
         N = 1 << n
         ctx = qfs.Context(n, pairs)
