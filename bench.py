@@ -52,7 +52,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "QFactor-Sample sweeps/sec + time-to-solution per instantiation; % HBM/FP64 peak"
 UNIT = "start-sweeps/s"
-FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2 (unit count x clock; context)
+FP64_DFMA_MEASURED_TFLOPS = 34.195  # profiles/r1_peaks_microbench.json (tools/peaks.cu DFMA loop, all SMs)
 L2_RMW_64MIB_GBS = 9209.1  # profiles/r1_peaks_microbench.json (l2loop_64MiB_rmw_gbs)
 
 
@@ -344,6 +345,18 @@ def main():
     dt = max_over_ranks(ev0.elapsed_time(ev1) / 1e3)
     value = s_tot * args.steps / dt
     assert all(r["sweeps"] == args.steps for r in res), res
+    clock_window = "timed region"
+    if time.time() - th0 < 0.5:
+        # shorter than a few nvidia-smi periods (C2, C5b): the clocks are sampled
+        # over >= 0.5 s of the SAME step repeated right after the timed region
+        # (VERDICT r1 hygiene), and the line says so
+        tw0 = time.time()
+        reps = 0
+        while time.time() - tw0 < 0.5:
+            ctx.instantiate(gates, bench_params(args.steps, m))
+            reps += 1
+        clk.mark(tw0, time.time())
+        clock_window = f"{reps} repeats of the timed {args.steps} steps right after it ({time.time() - tw0:.2f} s)"
 
     # ---- per-kernel CUDA-event durations: the same K steps again with one event
     # pair around each phase of the sweep (the run of forward launches, the run
@@ -380,11 +393,12 @@ def main():
             traffic = None
     if dom == "resident":
         # cluster-resident sweep: no HBM traffic inside the sweep; bound by the
-        # FP64 pipe: algorithmic flops (96 per amp-gate + 32 per
-        # validation amp-gate) / time against the unit-count peak
-        # 148 SMs x 64 DFMA/clk x 2 flop x 1.965 GHz (tools/peaks.cu measures 34.19)
+        # FP64 pipe: SURVEY.md §8(d)'s algorithmic 96 flops per
+        # amp-gate (the uncompute's extra 32 and the fused validation are NOT
+        # counted; the kernel time includes them) / time, against the measured
+        # DFMA peak (tools/peaks.cu; 37.2 = 148 SMs x 64 DFMA/clk x 2 x 1.965 GHz)
         achieved = pd["flops"] / (pd["ms"] * 1e-3) / 1e12
-        peak, peak_src = FP64_PEAK_TFLOPS, "derived: 148 SMs x 64 DFMA/clk x 2 x 1.965 GHz (DFMA microbenchmark 34.19)"
+        peak, peak_src = FP64_DFMA_MEASURED_TFLOPS, "measured DFMA loop (profiles/r1_peaks_microbench.json; derived 37.2)"
         bound, unit = "alu", "TFLOP/s"
     else:
         bound, unit = "hbm", "GB/s"
@@ -477,7 +491,7 @@ def main():
                 "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
                 "scaling": "strong" if sample else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": config, "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline,
-                "cpu_baseline": cpu, "clocks": clk.summary(), "time_to_solution": tts,
+                "cpu_baseline": cpu, "clocks": dict(clk.summary(), window=clock_window), "time_to_solution": tts,
                 "amp_gate_updates_per_s": value * m * N * prob.k}
         print(json.dumps(line), flush=True)
     ctx.close()

@@ -746,7 +746,10 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
     for (int j = j0; j < j1; ++j) units += (double)sp.slots[j].m * (double)c->N;
     const double vunits = (sp.want_val && c->V > 0) ? (double)ns * c->V * (double)c->N : 0.0;
     PhaseScope phase(c, K_RES);
-    LaunchScope ls(c, K_RES, 0.0, units * 96.0 * K + vunits * 32.0 * K);
+    // algorithmic flops of the sweep only (96 per amp-gate;
+    // the uncompute's extra 32 and the fused validation are not counted)
+    (void)vunits;
+    LaunchScope ls(c, K_RES, 0.0, units * 96.0 * K);
     CUDA_TRY(c, launch_resident(r, pl.clusters, st));
     return QFS_OK;
   }

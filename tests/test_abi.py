@@ -59,3 +59,13 @@ def test_no_oracle_in_product():
                 txt = open(os.path.join(dp, f)).read()
                 assert not re.search(r"^\s*(import oracle|from oracle|#include\s*[<\"].*qfso)", txt, re.M), f
                 assert "libqfs_oracle" not in txt and "qfso_" not in txt, f
+
+
+def test_emulated_ranks_argument_checks_without_device(lib):
+    """qfs_create_emulated validates the rank count before any device call."""
+    from paper_2405_12866_b200 import qfs
+    import numpy as np
+    for bad in (1, 33):
+        with pytest.raises(qfs.QfsError) as ei:
+            qfs.Context(4, np.array([[0, 1]], np.int32), emulated_ranks=bad)
+        assert ei.value.status == 1
