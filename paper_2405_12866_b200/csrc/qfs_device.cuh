@@ -212,6 +212,13 @@ __device__ __forceinline__ double ld_relaxed_sys(const double *p) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// shared-memory load that is re-issued per use (not hoisted into registers)
+__device__ __forceinline__ double2 lds_v2(const double2 *p) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return v;
+}
+
 __device__ __forceinline__ double2 shfl_c(double2 v, int src) {
   return make_double2(__shfl_sync(FULL, v.x, src), __shfl_sync(FULL, v.y, src));
 }

@@ -148,7 +148,7 @@ struct BwdShared {
 // chi/phi of the next items are staged into shared memory by LDGSTS,
 // BWD_STAGES-1 items ahead.  Reductions run in a fixed order (lanes, lane
 // groups, warps), so the partial is deterministic for a given launch shape.
-template <int NU, int TP0, int TP1, bool UPD>
+template <int NU, int TP0, int TP1, bool UPD, bool IDENT>
 __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslot, int s,
                                  unsigned Ms, BwdShared &sh, double2 *stage_buf) {
   constexpr int T = 1 << (NU - 2);
@@ -205,10 +205,10 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
     if (k >= iters) return false;
     unsigned g = fdu.div(u);
     const unsigned m = (u - g * nmb) * LPT + ml;
-    lm = m;
+    if (IDENT) lm = m;
 #pragma unroll
     for (int q = 0; q < NU; ++q) g = insert_zero32(g, ins[q]);
-    lg = g;
+    if (IDENT) lg = g;
     ec = g * csa + m;
     ed = g * dsa + m;
     ef = g * fsa + m;
@@ -240,7 +240,7 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
 #pragma unroll
       for (int l = 0; l < 4; ++l) cp_async16(st + l * BWD_THREADS, cbase + (eb + (offc[l] << 4)), ok);
     }
-    if (phi && G.phi.ident) {  // implicit basis x_m = e_m (gate 0 of a QF sweep): synthesised, not loaded
+    if (IDENT && phi) {  // implicit basis x_m = e_m (gate 0 of a QF sweep): synthesised, not loaded
 #pragma unroll
       for (int l = 0; l < 4; ++l) {
         const unsigned a = lg + (unsigned)G.off[XPOSE ? (t + 4 * (t ^ l)) : (4 * t + l)];
@@ -295,9 +295,17 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
   __syncthreads();
   // G_{i+1}^dag in registers for the whole loop (214 registers, no spill); read
   // from shared memory per item it cost 16 LDS per item (C4 bwd -2.4 % with it here)
+#ifndef QFS_BWD_GREG
+#define QFS_BWD_GREG 1  // 1: G_{i+1}^dag in registers for the loop; 0: broadcast shared-memory loads per use
+#endif
+#if QFS_BWD_GREG
   double2 sqr[16];
 #pragma unroll
   for (int e = 0; e < 16; ++e) sqr[e] = sh.sQ[e];
+#define QFS_SQ(e) sqr[e]
+#else
+#define QFS_SQ(e) lds_v2(&sh.sQ[e])
+#endif
 
   for (int k = 0; k < iters; ++k) {
     issue(k + BWD_STAGES - 1);
@@ -333,7 +341,7 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
       for (int a = 0; a < 4; ++a) {
         o[a] = make_double2(0.0, 0.0);
 #pragma unroll
-        for (int b = 0; b < 4; ++b) cfma(o[a], sqr[4 * a + b], c[b]);
+        for (int b = 0; b < 4; ++b) cfma(o[a], QFS_SQ(4 * a + b), c[b]);
       }
 #pragma unroll
       for (int a = 0; a < 4; ++a) c[a] = o[a];
@@ -539,7 +547,7 @@ __device__ void bwd_finish(const BwdParams &P, const GateDesc &G, int jslot, int
 // sums in warp order: deterministic, one ticket on the critical path (C5:
 // 2.7 -> 0.95 us per gate).  A separate instantiation, so the few-CTA path
 // compiles exactly as before.
-template <int NU, int TP0, int TP1, bool UPD, bool WIDE>
+template <int NU, int TP0, int TP1, bool UPD, bool WIDE, bool IDENT = false>
 __global__ void __launch_bounds__(BWD_THREADS, QFS_BWD_MINB) bwd_kernel(const BwdParams P) {
   __shared__ BwdShared sh;
   // [BWD_STAGES][8][BWD_THREADS]; 128-byte alignment measured to matter: with
@@ -550,7 +558,7 @@ __global__ void __launch_bounds__(BWD_THREADS, QFS_BWD_MINB) bwd_kernel(const Bw
   if constexpr (WIDE) {
     constexpr int NWARP = BWD_THREADS / 32, FL = 24;
     __shared__ unsigned last_cta;
-    const bool w0 = bwd_gate_partial<NU, TP0, TP1, UPD>(P, P.g, jslot, sl.s, (unsigned)sl.m, sh, stage_buf);
+    const bool w0 = bwd_gate_partial<NU, TP0, TP1, UPD, IDENT>(P, P.g, jslot, sl.s, (unsigned)sl.m, sh, stage_buf);
     if (w0) {
       const bool last = warp0_elect_last(&P.counters[jslot], (unsigned)P.nb);
       if (threadIdx.x == 0) last_cta = last ? 1u : 0u;
@@ -581,7 +589,7 @@ __global__ void __launch_bounds__(BWD_THREADS, QFS_BWD_MINB) bwd_kernel(const Bw
     bwd_finish_e(P, P.g, jslot, sl.s, sh, e, kind);
     return;
   }
-  if (!bwd_gate_partial<NU, TP0, TP1, UPD>(P, P.g, jslot, sl.s, (unsigned)sl.m, sh, stage_buf))
+  if (!bwd_gate_partial<NU, TP0, TP1, UPD, IDENT>(P, P.g, jslot, sl.s, (unsigned)sl.m, sh, stage_buf))
     return;
   const int kind = P.kinds ? __ldg(P.kinds + P.g.env_gate) : 0;
   const int ng = (P.nb + RED_GS - 1) / RED_GS;
@@ -1134,7 +1142,7 @@ __device__ __forceinline__ double2 gval(const double2 *p) {
 #endif
 }
 
-template <int NU, int TP0, int TP1>
+template <int NU, int TP0, int TP1, bool IDENT = false>
 __global__ void __launch_bounds__(FWD_THREADS, QFS_FWD2_MINB) fwd2_kernel(const Fwd2Params P) {
   constexpr int NV = 1 << NU;
   constexpr int NQ = NV / 4;
@@ -1173,7 +1181,7 @@ __global__ void __launch_bounds__(FWD_THREADS, QFS_FWD2_MINB) fwd2_kernel(const 
 #endif
   auto load = [&](unsigned w, double2 *v) {
     const uint2 gm = locate(w);
-    if (P.src.ident) {  // implicit basis x_m = e_m (the first pass of a QF sweep)
+    if (IDENT) {  // implicit basis x_m = e_m (the first pass of a QF sweep)
 #pragma unroll
       for (int u = 0; u < NV; ++u) v[u] = make_double2(gm.x + (unsigned)P.off[u] == gm.y ? 1.0 : 0.0, 0.0);
       return;
@@ -1700,10 +1708,24 @@ cudaError_t launch_bwd(const BwdParams &p, int n_slots, cudaStream_t st) {
     }                                                                                          \
     launch_ex(bwd_kernel<NU, A, B, U, W>, grid, block, smem, st, p);                           \
   } while (0)
-#define QFS_BWD(NU, A, B, U)            \
-  do {                                  \
-    if (wide) QFS_BWD1(NU, A, B, U, true); \
-    else QFS_BWD1(NU, A, B, U, false);  \
+#define QFS_BWD1I(NU, A, B, U, W)                                                              \
+  do {                                                                                         \
+    static bool attr = false;                                                                  \
+    if (!attr) {                                                                               \
+      cudaFuncSetAttribute(bwd_kernel<NU, A, B, U, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+      attr = true;                                                                             \
+    }                                                                                          \
+    launch_ex(bwd_kernel<NU, A, B, U, W, true>, grid, block, smem, st, p);                     \
+  } while (0)
+  // IDENT: phi is the implicit basis (gate 0 of a QFactor sweep, qfs_set_samples_basis) —
+  // its own instantiation so the common kernels keep their register budget
+#define QFS_BWD(NU, A, B, U)                                  \
+  do {                                                        \
+    if (g.phi.ident) {                                        \
+      if (wide) QFS_BWD1I(NU, A, B, U, true);                 \
+      else QFS_BWD1I(NU, A, B, U, false);                     \
+    } else if (wide) QFS_BWD1(NU, A, B, U, true);             \
+    else QFS_BWD1(NU, A, B, U, false);                        \
   } while (0)
   if (!g.upd) {
     QFS_BWD(2, 0, 1, false);
@@ -1721,6 +1743,7 @@ cudaError_t launch_bwd(const BwdParams &p, int n_slots, cudaStream_t st) {
   }
 #undef QFS_BWD
 #undef QFS_BWD1
+#undef QFS_BWD1I
   return cudaGetLastError();
 }
 
@@ -1749,7 +1772,11 @@ cudaError_t launch_fwd_gate(const FwdGateParams &p, int n_slots, cudaStream_t st
 
 cudaError_t launch_fwd2(const Fwd2Params &p, int n_slots, cudaStream_t st) {
   dim3 grid(p.nb, n_slots), block(FWD_THREADS);
-#define QFS_FWD2(NU, A, B) launch_ex(fwd2_kernel<NU, A, B>, grid, block, 0, st, p)
+#define QFS_FWD2(NU, A, B)                                                \
+  do {                                                                    \
+    if (p.src.ident) launch_ex(fwd2_kernel<NU, A, B, true>, grid, block, 0, st, p); \
+    else launch_ex(fwd2_kernel<NU, A, B, false>, grid, block, 0, st, p);  \
+  } while (0)
   if (p.nu == 2) {
     if (p.tp0 == 0) QFS_FWD2(2, 0, 1);
     else QFS_FWD2(2, 1, 0);

@@ -573,7 +573,11 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
 // block (same layout and gate routine as the resident sweep), all K
 // post-sweep gates are applied in order, then each row's ||C xv - yv||^2 goes
 // to row_out[j][row] (summed over rows in row order by row_reduce_kernel).
-__global__ void __launch_bounds__(RES_THREADS, 2) val_blk_kernel(const ValRowParams P, int ld) {
+// MINB = 2: two CTAs per SM (<= 128 registers, one gate per pass); MINB = 1
+// (when the rows' shared memory admits one CTA per SM anyway, e.g. C4's
+// ld = 2): two gates per shared-memory pass, half the passes and barriers.
+template <int MINB>
+__global__ void __launch_bounds__(RES_THREADS, MINB) val_blk_kernel(const ValRowParams P, int ld) {
   extern __shared__ __align__(QFS_RES_ALIGN) unsigned char smem_raw[];
   __shared__ double red[RES_WARPS];
   const int K = P.K, n = P.n;
@@ -593,7 +597,15 @@ __global__ void __launch_bounds__(RES_THREADS, 2) val_blk_kernel(const ValRowPar
   for (int q = tid; q < K * 16; q += RES_THREADS) G[q] = P.gates[(long long)s * K * 16 + q];
   __syncthreads();
   const FastDiv fdv((unsigned)nb);
-  for (int k = 0; k < K; ++k) {
+  int k0 = 0;
+  if constexpr (MINB == 1) {
+    for (; k0 + 1 < K; k0 += 2) {
+      res_apply_pair(st, G + 16 * k0, pr[k0], G + 16 * (k0 + 1), pr[k0 + 1], nb, fdv, (unsigned)ld, n, tid,
+                     RES_THREADS);
+      __syncthreads();
+    }
+  }
+  for (int k = k0; k < K; ++k) {
     res_apply(st, G + 16 * k, pr[k], false, nb, fdv, (unsigned)ld, n, tid, RES_THREADS);
     __syncthreads();
   }
@@ -788,9 +800,15 @@ cudaError_t launch_val_block(const ValRowParams &p, int n_slots, cudaStream_t st
   if (smem > lim) return cudaErrorInvalidConfiguration;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(val_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim);
+    cudaFuncSetAttribute(val_blk_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim);
+    cudaFuncSetAttribute(val_blk_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim);
     attr = true;
   }
+#ifndef QFS_VAL_PAIRS
+#define QFS_VAL_PAIRS 1
+#endif
+  // one CTA per SM either way (shared memory over half the SM's): the pair variant
+  const bool one = QFS_VAL_PAIRS && smem + 1024 > RES_SMEM_MAX2;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((p.rows + ld - 1) / ld, n_slots);
   cfg.blockDim = dim3(RES_THREADS);
@@ -801,7 +819,7 @@ cudaError_t launch_val_block(const ValRowParams &p, int n_slots, cudaStream_t st
   a[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = a;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, val_blk_kernel, p, ld);
+  return one ? cudaLaunchKernelEx(&cfg, val_blk_kernel<1>, p, ld) : cudaLaunchKernelEx(&cfg, val_blk_kernel<2>, p, ld);
 }
 
 size_t res_smem_bytes(int n, int K, int ld) {
