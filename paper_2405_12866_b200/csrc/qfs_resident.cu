@@ -46,6 +46,12 @@ constexpr int RES_ENV_UNROLL = QFS_RES_ENV_UNROLL;
 #ifndef QFS_RES_PUSH
 #define QFS_RES_PUSH 1  // resident: CTA partials pushed over DSMEM before the cluster barrier
 #endif
+#ifndef QFS_RES_FUSE
+// resident: chi update of gate i fused with the environment of gate i-1 (one
+// pass and one barrier less per gate) — measured slower (C3 442.8 -> 450.9 us
+// per sweep, C5c 1452 -> 1501 us: 255 registers and spills), so off
+#define QFS_RES_FUSE 0
+#endif
 #ifndef QFS_RES_PAIRS
 #define QFS_RES_PAIRS 1  // resident forward / validation: two gates per shared-memory pass
 #endif
@@ -291,6 +297,104 @@ __device__ void res_env(const double2 *phi, const double2 *chi, int2 pq, int cnt
   red[warp * 32 + lane] = warp_reduce_scatter32(acc, lane);
 }
 
+// Fused backward pass of the resident sweep (QFS_RES_FUSE): chi <- G_i^dag chi
+// (gate i on local bits 0, 1) and, from the same registers, the environment of
+// gate i-1 (its pair at local (TP0, TP1); phi = B_{i-1} already
+// uncomputed) — one shared-memory pass and one barrier instead of two.  Every
+// warp writes its reduced 32 doubles (re/im of E_{i-1}'s 16 entries) to
+// red[warp][.] like res_env.
+template <int NU, int TP0, int TP1>
+__device__ void res_chi_env_t(double2 *chi, const double2 *phi, const double2 *G, const int (&loc)[4],
+                              const int (&srt)[4], int cnt, const FastDiv &fd, unsigned ld, int n, double *red) {
+  constexpr int NV = 1 << NU, NQ = NV / 4;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double acc[32];
+#pragma unroll
+  for (int e = 0; e < 32; ++e) acc[e] = 0.0;
+  unsigned ob[NU];
+#pragma unroll
+  for (int t = 0; t < NU; ++t) ob[t] = (1u << loc[t]) * ld;
+  auto offs = [&](int u) {
+    unsigned o = 0;
+#pragma unroll
+    for (int t = 0; t < NU; ++t)
+      if ((u >> t) & 1) o += ob[t];
+    return o;
+  };
+  const unsigned items = cnt > 0 ? (1u << (n - NU)) * (unsigned)cnt : 0u;
+  for (unsigned q = threadIdx.x; q < items; q += RES_THREADS) {
+    const unsigned r = fd.div(q);
+    unsigned g = r;
+#pragma unroll
+    for (int t = 0; t < NU; ++t) g = insert_zero32(g, srt[t]);
+    const unsigned b = g * ld + (q - r * (unsigned)cnt);
+    double2 v[NV];
+#pragma unroll
+    for (int u = 0; u < NV; ++u) v[u] = chi[b + offs(u)];
+#pragma unroll
+    for (int qq = 0; qq < NQ; ++qq) {  // chi' = G^dag chi, (G^dag)[a][c] = conj(G[c][a])
+      double2 o[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        o[a] = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) cfma(o[a], cconj(lds_c2(G + 4 * c + a)), v[4 * qq + c]);
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) v[4 * qq + a] = o[a];
+    }
+#pragma unroll
+    for (int u = 0; u < NV; ++u) chi[b + offs(u)] = v[u];
+#pragma unroll
+    for (int p = 0; p < NQ; ++p) {  // E[a][k] += phi[a] conj(chi'[k]) on gate i-1's quadruples
+      double2 f[4];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) f[l] = phi[b + offs(pair_idx<NU, TP0, TP1>(p, l))];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double2 ck = v[pair_idx<NU, TP0, TP1>(p, k)];
+          double &re = acc[2 * (4 * a + k)], &im = acc[2 * (4 * a + k) + 1];
+          re = fma(f[a].x, ck.x, re);
+          re = fma(f[a].y, ck.y, re);
+          im = fma(f[a].y, ck.x, im);
+          im = fma(-f[a].x, ck.y, im);
+        }
+    }
+  }
+  red[warp * 32 + lane] = warp_reduce_scatter32(acc, lane);
+}
+// dispatch on the union of gate i's pair p1 and gate i-1's pair p2 (the local
+// order and template keys of res_apply_pair)
+__device__ void res_chi_env(double2 *chi, const double2 *phi, const double2 *G, int2 p1, int2 p2, int cnt,
+                            const FastDiv &fd, unsigned ld, int n, double *red) {
+  const bool x_new = p2.x != p1.x && p2.x != p1.y, y_new = p2.y != p1.x && p2.y != p1.y;
+  int l2 = 0, l3 = 0, nu = 2;
+  if (x_new && y_new) { l2 = min(p2.x, p2.y); l3 = max(p2.x, p2.y); nu = 4; }
+  else if (x_new) { l2 = p2.x; nu = 3; }
+  else if (y_new) { l2 = p2.y; nu = 3; }
+  auto pos = [&](int q) { return q == p1.x ? 0 : q == p1.y ? 1 : q == l2 ? 2 : 3; };
+  const int tp0 = pos(p2.x), tp1 = pos(p2.y);
+  const int loc[4] = {p1.x, p1.y, l2, l3};
+  int a0 = p1.x, a1 = p1.y, a2 = nu > 2 ? l2 : 31, a3 = nu > 3 ? l3 : 31;
+  auto cs = [](int &u, int &v) { if (v < u) { const int t = u; u = v; v = t; } };
+  cs(a0, a1); cs(a2, a3); cs(a0, a2); cs(a1, a3); cs(a1, a2);
+  const int srt[4] = {a0, a1, a2, a3};
+  if (nu == 2) {
+    if (tp0 == 0) res_chi_env_t<2, 0, 1>(chi, phi, G, loc, srt, cnt, fd, ld, n, red);
+    else res_chi_env_t<2, 1, 0>(chi, phi, G, loc, srt, cnt, fd, ld, n, red);
+  } else if (nu == 3) {
+    if (tp0 == 0 && tp1 == 2) res_chi_env_t<3, 0, 2>(chi, phi, G, loc, srt, cnt, fd, ld, n, red);
+    else if (tp0 == 2 && tp1 == 0) res_chi_env_t<3, 2, 0>(chi, phi, G, loc, srt, cnt, fd, ld, n, red);
+    else if (tp0 == 1 && tp1 == 2) res_chi_env_t<3, 1, 2>(chi, phi, G, loc, srt, cnt, fd, ld, n, red);
+    else res_chi_env_t<3, 2, 1>(chi, phi, G, loc, srt, cnt, fd, ld, n, red);
+  } else {
+    if (tp0 == 2) res_chi_env_t<4, 2, 3>(chi, phi, G, loc, srt, cnt, fd, ld, n, red);
+    else res_chi_env_t<4, 3, 2>(chi, phi, G, loc, srt, cnt, fd, ld, n, red);
+  }
+}
+
 struct ResSmem {
   double2 *G;     // [K][16] gate table of the current start (old -> new in place)
   double *red;    // [RES_WARPS][32]
@@ -384,9 +488,11 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
     }
     stamp(1);  // [1] forward
     double train = 0.0;
+    constexpr bool FUSE = QFS_RES_FUSE && MINB == 1;  // (the 128-register variant would spill)
+    if (FUSE) res_env(sm.phi, sm.chi, sm.pr[K - 1], cnt, fd, ld, n, sm.red);  // E_{K-1}; the rest fused below
     for (int i = K - 1; i >= 0; --i) {
       const int par = i & 1;
-      res_env(sm.phi, sm.chi, sm.pr[i], cnt, fd, ld, n, sm.red);
+      if (!FUSE) res_env(sm.phi, sm.chi, sm.pr[i], cnt, fd, ld, n, sm.red);
       __syncthreads();
       stamp(2);  // [2] environment pass
 #if QFS_RES_PUSH
@@ -455,7 +561,10 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
       __syncthreads();
       stamp(5);  // [5] wait for the uncompute warps
       if (i > 0) {
-        res_apply(sm.chi, sm.G + 16 * i, sm.pr[i], true, cnt, fd, ld, n, tid, RES_THREADS);
+        if constexpr (FUSE)  // chi <- G_i^dag chi fused with the environment of gate i-1 (phi = B_{i-1} now)
+          res_chi_env(sm.chi, sm.phi, sm.G + 16 * i, sm.pr[i], sm.pr[i - 1], cnt, fd, ld, n, sm.red);
+        else
+          res_apply(sm.chi, sm.G + 16 * i, sm.pr[i], true, cnt, fd, ld, n, tid, RES_THREADS);
       } else if (cnt > 0) {
         // chi' = G_0^dag chi and c_train = sum ||chi' - x||^2
         const double2 *G = sm.G;
