@@ -9,6 +9,9 @@ test_gpu_parity.py::test_sample_sharded_path_single_rank).
   E differs) and the oracle within the parity tolerances.
 * multistart mode: each rank runs its starts; results are bitwise identical
   to one rank running the same starts.
+* sample mode with the device-initiated exchange (qfs_set_exchange, NEXT-2):
+  the ranks' mailboxes mapped over CUDA IPC; identical gate bits on both
+  ranks, equal to the NCCL path within 1e-12.
 """
 import os
 import pickle
@@ -47,6 +50,14 @@ def _worker(rank, world, port, out_dir):
     tr = ctx.trace_sweeps(p.init, 32, 3)
     g, res, win = ctx.instantiate(p.init, dict(p.params, max_iter=200))
     ctx.close()
+    # the device-initiated exchange (NEXT-2): peer mailboxes mapped with CUDA IPC
+    obj = [qfs.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    dx = qfs.Context(p.n, p.pairs, device=rank, nccl_id=obj[0], rank=rank, world=world, shard_mode=1)
+    dx.set_exchange("device")
+    dx.set_samples(p.x[rows], p.y[rows], p.xv[vrows], p.yv[vrows])
+    trx = dx.trace_sweeps(p.init, 32, 3)
+    dx.close()
     # multistart: this rank's slice of 4 starts
     sl = PL.start_slice(4, rank, world)
     q = I.make_problem("c3", init="R", s=4, k=24)
@@ -55,7 +66,7 @@ def _worker(rank, world, port, out_dir):
     mt = mc.trace_sweeps(q.init[sl.start:sl.stop], 16, 2)
     mc.close()
     with open(os.path.join(out_dir, f"r{rank}.pkl"), "wb") as f:
-        pickle.dump(dict(tr=tr, res=res, win=win, mt=mt, sl=(sl.start, sl.stop)), f)
+        pickle.dump(dict(tr=tr, trx=trx, res=res, win=win, mt=mt, sl=(sl.start, sl.stop)), f)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -85,6 +96,10 @@ def test_two_ranks_sample_and_multistart(tmp_path):
         assert abs(r[k]["res"][w1]["c_val"] - res1[w1]["c_val"]) <= 1e-9 * res1[w1]["c_val"]
     ot = oracle.trace_sweeps(p.n, p.pairs, p.init, p.x, p.y, 32, 3)
     assert np.abs(r[0]["tr"]["env"] - ot["env"]).max() <= 1e-10 * np.abs(ot["env"]).max()
+    for k in range(2):   # device exchange: identical bits on both ranks, = the NCCL path within 1e-12
+        assert np.array_equal(r[k]["trx"]["gates"], r[0]["trx"]["gates"])
+        assert np.abs(r[k]["trx"]["gates"] - r[k]["tr"]["gates"]).max() <= 1e-12
+        assert np.abs(r[k]["trx"]["env"] - ot["env"]).max() <= 1e-10 * np.abs(ot["env"]).max()
     q = I.make_problem("c3", init="R", s=4, k=24)
     mq = qfs.Context(q.n, q.pairs)
     mq.set_samples(q.x, q.y, q.xv, q.yv)
