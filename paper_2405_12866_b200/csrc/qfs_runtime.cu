@@ -310,7 +310,7 @@ bool offsets_fit(const qfs_ctx *c, long long rows) { return ((long long)c->N * r
 size_t plan_bytes(const qfs_ctx *c, int S, int M, int V, int nb) {
   size_t N = (size_t)c->N;
   size_t b = 0;
-  b += (size_t)S * M * N * 16 * (c->K > 1 ? 2 : 1);        // chi (two buffers: perm mode)
+  b += (size_t)S * M * N * 16 * (c->K > 1 && c->bwd_bulk ? 2 : 1);  // chi (two buffers in perm mode)
   if (c->K > 1) b += (size_t)(c->K - 1) * S * M * N * 16;  // B cache
   if ((c->n > val_row_max_n() || c->blocks) && V > 0) b += 2 * (size_t)S * V * N * 16;
   if (c->blocks) b += (size_t)S * kBlkMaxCtas * 128 * 8;
@@ -354,8 +354,10 @@ qfs_status ensure_state(qfs_ctx *c, int S, int M, int V) {
   S = std::max(S, c->S_cap);
   M = std::max(M, c->M_cap);
   // perm mode's sample blocks (16 or 32 samples) must tile M_cap exactly
-  if (M > 16) M = (M + 31) / 32 * 32;
-  else if (M > 8) M = 16;
+  if (c->bwd_bulk) {
+    if (M > 16) M = (M + 31) / 32 * 32;
+    else if (M > 8) M = 16;
+  }
   V = std::max(V, c->V_cap);
   const int nbc = std::max(nb, c->nb_cap);
   CUDA_TRY(c, cudaStreamSynchronize(c->st));
@@ -380,7 +382,7 @@ qfs_status ensure_state(qfs_ctx *c, int S, int M, int V) {
   }
   const size_t N = (size_t)c->N;
   CUDA_TRY(c, cudaMalloc(&c->d_chi, (size_t)S * M * N * sizeof(double2)));
-  if (c->K > 1) CUDA_TRY(c, cudaMalloc(&c->d_chi2, (size_t)S * M * N * sizeof(double2)));
+  if (c->K > 1 && c->bwd_bulk) CUDA_TRY(c, cudaMalloc(&c->d_chi2, (size_t)S * M * N * sizeof(double2)));
   if (c->K > 1) CUDA_TRY(c, cudaMalloc(&c->d_B, (size_t)(c->K - 1) * S * M * N * sizeof(double2)));
   if ((c->n > val_row_max_n() || c->blocks) && V > 0) {
     CUDA_TRY(c, cudaMalloc(&c->d_vb0, (size_t)S * V * N * sizeof(double2)));
@@ -768,7 +770,8 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
   for (int j = j0; j < j1; ++j) units += (double)sp.slots[j].m * (double)N;
   // perm mode (bulk-copy backward): B cache and chi in the per-gate permuted
   // sample-blocked layouts L_i (qfs_internal.h); else natural sample-minor
-  const bool perm = c->bwd_bulk && M_max >= c->bulk_min_m && M_max >= 16 && !c->x_basis;
+  const bool perm = c->bwd_bulk && M_max >= c->bulk_min_m && M_max >= 16 && !c->x_basis && c->d_chi2 &&
+                    c->M_cap % (c->M_cap >= 32 ? 32 : 16) == 0;
   const int psb = c->M_cap >= 32 ? 32 : 16;
   const long long pblk = N * psb;
   std::vector<Lay> lays;
