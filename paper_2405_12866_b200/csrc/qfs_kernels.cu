@@ -45,6 +45,9 @@ namespace {
 #ifndef QFS_BWD_BYTEOFF
 #define QFS_BWD_BYTEOFF 1  // backward: 32-bit byte offsets from per-start bases for LDGSTS / STG addresses
 #endif
+#ifndef QFS_BWD_HINT
+#define QFS_BWD_HINT 0  // backward L2 hints: 1 phi loads evict_first, 2 chi stores evict_last (A/B)
+#endif
 #ifndef QFS_BWD_EDRING
 #define QFS_BWD_EDRING 1  // backward: chi store offsets carried from issue to use in registers
 #endif
@@ -167,6 +170,12 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
   const unsigned beg = blockIdx.x * chunk;
   const unsigned end = min(units, beg + chunk);
   const FastDiv fdu(nmb);
+#if QFS_BWD_HINT & 1
+  const uint64_t pol_phi = policy_evict_first();
+#endif
+#if QFS_BWD_HINT & 2
+  const uint64_t pol_chi = policy_evict_last();
+#endif
 
   double2 acc[4][4][AZ];
 #pragma unroll
@@ -249,7 +258,12 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
     } else if (phi) {
       const unsigned eb = ef << 4;
 #pragma unroll
+#if QFS_BWD_HINT & 1  // phi = B_i is read once: L2 evict_first
+      for (int l = 0; l < 4; ++l)
+        cp_async16_hint(st + (4 + l) * BWD_THREADS, fbase + (eb + (offf[l] << 4)), ok, pol_phi);
+#else
       for (int l = 0; l < 4; ++l) cp_async16(st + (4 + l) * BWD_THREADS, fbase + (eb + (offf[l] << 4)), ok);
+#endif
     }
 #else
     if (chi) {
@@ -349,7 +363,11 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
 #if QFS_BWD_BYTEOFF
         const unsigned eb = ed << 4;
 #pragma unroll
+#if QFS_BWD_HINT & 2  // chi is re-read by the next launch: L2 evict_last
+        for (int l = 0; l < 4; ++l) st_hint((double2 *)(dbase + (eb + (offd[l] << 4))), c[l], pol_chi);
+#else
         for (int l = 0; l < 4; ++l) *(double2 *)(dbase + (eb + (offd[l] << 4))) = c[l];
+#endif
 #else
         double2 *dp = cdst + ed;
 #pragma unroll
