@@ -213,7 +213,7 @@ class Context:
     def instantiate(self, init_gates, params: dict):
         g = _c128(init_gates)
         s = g.shape[0]
-        out = np.zeros_like(g)
+        out = np.empty_like(g)  # filled by qfs_instantiate (no zeroing pass)
         res = (Result * s)()
         win = ctypes.c_int(-1)
         p = make_params(params)
