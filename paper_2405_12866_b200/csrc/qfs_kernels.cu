@@ -694,8 +694,15 @@ constexpr int BT_SROW = 32;                   // largest sample block (one sampl
 // would pass at once — mbarrier parity waits only distinguish adjacent phases).
 static_assert(BT_STAGES % BT_CW == 0, "each consumer warp must own whole ring slots");
 
+#ifndef QFS_BT_EARLY
+// 1: consumers copy a whole stage (chi and phi) into registers and release the
+// slot BEFORE computing (deeper copy pipeline; G^dag from shared memory):
+// measured C4 21.1 -> 22.7 us (255 registers, spills), C5 16.5 -> 14.2 us — off
+#define QFS_BT_EARLY 0
+#endif
 struct BtShared {
   uint64_t full[BT_STAGES], empty[BT_STAGES];
+  double2 sQ[BT_CW][16];  // QFS_BT_EARLY: G_{i+1}^dag, one copy per consumer warp
   double2 red[BT_CW][16];
   double wsum[(BT_CW + 1) * 32];  // WIDE reduction: per-warp sums of CTA partials
   double sum32[32];
@@ -838,6 +845,15 @@ __global__ void __launch_bounds__(BT_THREADS, 1) bwdt_kernel(const BwdParams P) 
   } else {
     // ------------------------------------------------------------ consumers
     pdl_wait();  // G_{i+1} was written by the previous launch's polar update
+#if QFS_BT_EARLY
+    // G_{i+1}^dag in this warp's shared-memory copy (registers go to the stage copy)
+    if (UPD && lane < 16) {
+      const int a = lane >> 2, b = lane & 3;  // (G^dag)[a][b] = conj(G[b][a])
+      sh.sQ[warp][lane] = cconj(__ldcg(P.gates + ((long long)s * P.K + G.upd_gate) * 16 + 4 * b + a));
+    }
+    __syncwarp();
+#define QFS_BTQ(e) lds_v2(&sh.sQ[warp][e])
+#else
     double2 Q[16];
     if (UPD) {
 #pragma unroll
@@ -846,6 +862,8 @@ __global__ void __launch_bounds__(BT_THREADS, 1) bwdt_kernel(const BwdParams P) 
         for (int b = 0; b < 4; ++b)  // (G^dag)[a][b] = conj(G[b][a])
           Q[4 * a + b] = cconj(__ldcg(P.gates + ((long long)s * P.K + G.upd_gate) * 16 + 4 * b + a));
     }
+#define QFS_BTQ(e) Q[e]
+#endif
     double2 *cdst = G.chi_dst.base ? G.chi_dst.base + (long long)s * G.chi_dst.ss : nullptr;
     double2 acc[16];
 #pragma unroll
@@ -859,6 +877,13 @@ __global__ void __launch_bounds__(BT_THREADS, 1) bwdt_kernel(const BwdParams P) 
       double2 c[NV];
 #pragma unroll
       for (int v = 0; v < NV; ++v) c[v] = valid ? sc[v * sb] : make_double2(0.0, 0.0);
+#if QFS_BT_EARLY
+      double2 fr[NV];  // phi too, then the slot goes back to the producer before any arithmetic
+#pragma unroll
+      for (int v = 0; v < NV; ++v) fr[v] = valid ? sc[(NV + v) * sb] : make_double2(0.0, 0.0);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.empty[k % BT_STAGES]);
+#endif
       if (UPD) {
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
@@ -867,7 +892,7 @@ __global__ void __launch_bounds__(BT_THREADS, 1) bwdt_kernel(const BwdParams P) 
           for (int a = 0; a < 4; ++a) {
             o[a] = make_double2(0.0, 0.0);
 #pragma unroll
-            for (int bb = 0; bb < 4; ++bb) cfma(o[a], Q[4 * a + bb], c[4 * q + bb]);
+            for (int bb = 0; bb < 4; ++bb) cfma(o[a], QFS_BTQ(4 * a + bb), c[4 * q + bb]);
           }
 #pragma unroll
           for (int a = 0; a < 4; ++a) c[4 * q + a] = o[a];
@@ -885,7 +910,11 @@ __global__ void __launch_bounds__(BT_THREADS, 1) bwdt_kernel(const BwdParams P) 
         double2 f[4];
 #pragma unroll
         for (int l = 0; l < 4; ++l)
+#if QFS_BT_EARLY
+          f[l] = fr[pv_idx<NU, TP0, TP1>(p, l)];
+#else
           f[l] = valid ? sc[(NV + pv_idx<NU, TP0, TP1>(p, l)) * sb] : make_double2(0.0, 0.0);
+#endif
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -898,9 +927,12 @@ __global__ void __launch_bounds__(BT_THREADS, 1) bwdt_kernel(const BwdParams P) 
             e.y = fma(-f[a].x, cb.y, e.y);
           }
       }
+#if !QFS_BT_EARLY
       __syncwarp();
       if (lane == 0) mbar_arrive(&sh.empty[k % BT_STAGES]);
+#endif
     }
+#undef QFS_BTQ
     // warp sum over the samples (fixed butterfly order)
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
