@@ -634,3 +634,30 @@ def test_trace_parity_bulk_copy_path(qfs, monkeypatch, name, init, s, m, sweeps,
     g2, r2, _ = oracle.instantiate(p.n, p.pairs, p.x, p.y, p.xv, p.yv, p.init[pick], prm, threads=len(pick))
     for j, q in enumerate(pick):
         assert abs(r1[q]["c_train"] - r2[j]["c_train"]) <= COST_TOL * r2[j]["c_train"]
+
+
+@pytest.mark.parametrize("n,k,m,v", [(16, 14, 32, 8), (18, 10, 16, 4)])
+def test_large_n_streamed_with_validation(qfs, n, k, m, v):
+    """Beyond the configs: n = 16 (validation on 8-CTA clusters, 1 MB rows) and
+    n = 18 (rows too large for a cluster: the streamed per-gate validation +
+    distance kernels), brick pairs plus a reversed long-range pair; two traced
+    sweeps and the controller's c_val / c_train after two steps vs the oracle."""
+    rng = np.random.default_rng(n)
+    pairs = I.brick_pairs(n, k)
+    pairs[k // 2] = [n - 1, 1]
+    target = np.stack([unitary(rng) for _ in pairs])
+    x = I.haar_states(rng, n, m)
+    y = I.apply_circuit_tensor(n, pairs, target, x)
+    xv = I.haar_states(np.random.default_rng(n + 1), n, v)
+    yv = I.apply_circuit_tensor(n, pairs, target, xv)
+    init = np.stack([I.warm_gate(rng, target[j], 0.3) for j in range(k)])[None]
+    ctx = _ctx(qfs, n, pairs)
+    ctx.set_samples(x, y, xv, yv)
+    gt = ctx.trace_sweeps(init, m, 2)
+    ot = oracle.trace_sweeps(n, pairs, init, x, y, m, 2)
+    _compare_traces(gt, ot, f"n{n}")
+    prm = _no_stop(m, 2)
+    g1, r1, _ = ctx.instantiate(init, prm)
+    g2, r2, _ = oracle.instantiate(n, pairs, x, y, xv, yv, init, prm)
+    assert abs(r1[0]["c_val"] - r2[0]["c_val"]) <= COST_TOL * r2[0]["c_val"] + 1e-15
+    assert abs(r1[0]["c_train"] - r2[0]["c_train"]) <= COST_TOL * r2[0]["c_train"] + 1e-15
