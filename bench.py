@@ -434,16 +434,19 @@ def main():
         ctx.set_samples_async_host_ptr(hx.shape[0], hx.data_ptr(), hy.data_ptr(), hxv.shape[0], hxv.data_ptr(),
                                        hyv.data_ptr())
 
-    for _ in range(2):                   # untimed warm-up of the e2e path (staging buffers, graphs)
+    # two caller-owned host gate buffers, alternating as input and output (the
+    # C ABI's out_gates): no fresh allocation per step
+    gbuf = [np.ascontiguousarray(g).copy(), np.empty_like(np.ascontiguousarray(g))]
+    for w in range(2):                   # untimed warm-up of the e2e path (staging buffers, graphs)
         queue_samples()
-        g, _, _ = ctx.instantiate(g, bench_params(1, m))
+        ctx.instantiate(gbuf[w % 2], bench_params(1, m), out=gbuf[(w + 1) % 2])
     barrier()
     t0 = time.perf_counter()
     queue_samples()                      # step 0's inputs
     for step in range(e2e_steps):
         if step + 1 < e2e_steps:
             queue_samples()              # step t+1's inputs copy while step t runs
-        g, _, _ = ctx.instantiate(g, bench_params(1, m))
+        ctx.instantiate(gbuf[step % 2], bench_params(1, m), out=gbuf[(step + 1) % 2])
     barrier()
     e2e_dt = max_over_ranks(time.perf_counter() - t0)
     e2e = {"value": s_tot * e2e_steps / e2e_dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),

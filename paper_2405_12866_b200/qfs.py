@@ -210,10 +210,16 @@ class Context:
             ctypes.c_void_p(dxv.data_ptr() if v else 0), ctypes.c_void_p(dyv.data_ptr() if v else 0), st))
 
     # -- instantiation -----------------------------------------------------
-    def instantiate(self, init_gates, params: dict):
+    def instantiate(self, init_gates, params: dict, out=None):
+        """qfs_instantiate.  ``out``: optional caller-owned complex128 array of the
+        gates' shape to receive the result (the C ABI's out_gates), e.g. reused
+        across calls to avoid allocating (and page-faulting) a fresh array."""
         g = _c128(init_gates)
         s = g.shape[0]
-        out = np.empty_like(g)  # filled by qfs_instantiate (no zeroing pass)
+        if out is None:
+            out = np.empty_like(g)  # filled by qfs_instantiate (no zeroing pass)
+        elif out.shape != g.shape or out.dtype != np.complex128 or not out.flags.c_contiguous or out is g:
+            raise ValueError("out must be a distinct C-contiguous complex128 array of the gates' shape")
         res = (Result * s)()
         win = ctypes.c_int(-1)
         p = make_params(params)
