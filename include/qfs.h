@@ -163,7 +163,9 @@ qfs_status qfs_set_samples(qfs_ctx *c, int m_pool, const double *x, const double
 /* Asynchronous variant for pipelined callers: queues the sample set (same
  * arguments and layout as qfs_set_samples) into one of two device staging
  * slots with host->device copies on a separate copy stream, and returns at
- * once; the next qfs_instantiate / qfs_trace_sweeps / qfs_bench_sweeps call
+ * once; the copies start behind the forward phase of the next sweep the
+ * context runs (or at once if no sweep runs before the set is needed); the
+ * next qfs_instantiate / qfs_trace_sweeps / qfs_bench_sweeps call
  * consumes the oldest queued set (finite check, transpose to the sample-minor
  * pools) before it runs.  So a caller can queue step t+1's samples while step
  * t's instantiation runs.  The host buffers must stay valid and unmodified

@@ -121,8 +121,15 @@ struct qfs_ctx {
     size_t cap_xy = 0, cap_v = 0;  // bytes per array
     int m_pool = 0, v = 0;
     cudaEvent_t ev = nullptr;
+    const void *hx = nullptr, *hy = nullptr, *hxv = nullptr, *hyv = nullptr;  // caller's host buffers
+    bool issued = false;           // H2D copies enqueued on st_copy
   } stg[2];
   int stg_head = 0, stg_count = 0;
+  // QFS_COPY_DEFER=1: a queued set's H2D copies start only after the forward
+  // phase of the next sweep (event recorded inside the sweep graph), i.e.
+  // during the latency-bound backward instead of the write-bound forward
+  bool copy_defer = true;
+  cudaEvent_t ev_fwd = nullptr;
   // pinned host staging of the gates (upload / download through page-locked
   // memory, so the small copies do not queue behind a pageable staging path)
   double2 *h_gates = nullptr;
@@ -155,6 +162,8 @@ struct qfs_ctx {
   long long res_sweeps = 0;
   long long dbg_n = 0;
 };
+
+qfs_status issue_deferred(qfs_ctx *c);  // queued sample sets' copies (defined with the ABI below)
 
 namespace {
 
@@ -878,6 +887,10 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
     }
   }
   }
+  if (c->copy_defer && c->ev_fwd) {  // queued sample sets start copying from here (QFS_COPY_DEFER)
+    if (c->capturing) CUDA_TRY(c, cudaEventRecordWithFlags(c->ev_fwd, st, cudaEventRecordExternal));
+    else CUDA_TRY(c, cudaEventRecord(c->ev_fwd, st));
+  }
   // (b, c) backward: gate i = K-1 .. 0 (P:112 right to left; Fig. env_calc)
   BwdParams b{};
   b.n = n; b.K = K; b.S = sp.S; b.slots = slots; b.gates = c->d_gates; b.gates_w = c->d_gates;
@@ -1086,6 +1099,10 @@ qfs_status run_sweep(qfs_ctx *c, const SweepSpec &sp, std::vector<double> &csum,
     if (s != QFS_OK) return s;
     c->res_sweeps++;
   }
+  if (c->copy_defer && c->stg_count > 0) {  // queued sample sets: copy during this sweep's backward
+    const qfs_status s = issue_deferred(c);
+    if (s != QFS_OK) return s;
+  }
   CUDA_TRY(c, cudaMemcpyAsync(c->h_csum, c->d_csum, ns * sizeof(double), cudaMemcpyDeviceToHost, c->st));
   if (sp.want_val && c->V > 0)
     CUDA_TRY(c, cudaMemcpyAsync(c->h_cval, c->d_cval, ns * sizeof(double), cudaMemcpyDeviceToHost, c->st));
@@ -1240,6 +1257,8 @@ qfs_status create_common(int n, int k, const int32_t *pairs, int device, qfs_ctx
   if (const char *rc = getenv("QFS_RES_CMAX")) c->res_cmax = std::max(1, std::min(16, atoi(rc)));
   if (const char *rp = getenv("QFS_RES_PER_SM")) c->res_per_sm = atoi(rp) == 2 ? 2 : 1;
   if (const char *uf = getenv("QFS_UNFUSED_POLAR")) c->force_unfused = atoi(uf) != 0;
+  if (const char *cd = getenv("QFS_COPY_DEFER")) c->copy_defer = atoi(cd) != 0;
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fwd, cudaEventDisableTiming);
   if (const char *bb = getenv("QFS_BWD_BULK")) c->bwd_bulk = atoi(bb) != 0;
   if (const char *bm = getenv("QFS_BULK_MIN_M")) c->bulk_min_m = std::max(1, atoi(bm));
   if (e != cudaSuccess) {
@@ -1488,10 +1507,41 @@ static qfs_status set_samples_impl(qfs_ctx *c, int m_pool, const void *x, const 
 
 // Oldest queued sample set -> the pools (device-to-device through the same
 // staging, finite check and transpose as qfs_set_samples), after its H2D copy.
-}  // extern "C" (internal helper below has C++ linkage)
+}  // extern "C" (internal helpers below have C++ linkage)
+// Enqueue a staged set's H2D copies on the copy stream (after `after`, if given).
+qfs_status issue_staged(qfs_ctx *c, qfs_ctx::Staged &g, cudaEvent_t after) {
+  if (g.issued) return QFS_OK;
+  if (after) CUDA_TRY(c, cudaStreamWaitEvent(c->st_copy, after, 0));
+  const size_t bxy = (size_t)g.m_pool * c->N * sizeof(double2), bv = (size_t)g.v * c->N * sizeof(double2);
+  CUDA_TRY(c, cudaMemcpyAsync(g.x, g.hx, bxy, cudaMemcpyHostToDevice, c->st_copy));
+  CUDA_TRY(c, cudaMemcpyAsync(g.y, g.hy, bxy, cudaMemcpyHostToDevice, c->st_copy));
+  if (g.v > 0) {
+    CUDA_TRY(c, cudaMemcpyAsync(g.xv, g.hxv, bv, cudaMemcpyHostToDevice, c->st_copy));
+    CUDA_TRY(c, cudaMemcpyAsync(g.yv, g.hyv, bv, cudaMemcpyHostToDevice, c->st_copy));
+  }
+  CUDA_TRY(c, cudaEventRecord(g.ev, c->st_copy));
+  g.issued = true;
+  return QFS_OK;
+}
+// After a sweep's graph is enqueued: start the copies of the queued sets not
+// yet consumed, behind the sweep's forward phase (QFS_COPY_DEFER).
+qfs_status issue_deferred(qfs_ctx *c) {
+  for (int q = 0; q < c->stg_count; ++q) {
+    qfs_ctx::Staged &g = c->stg[(c->stg_head + q) % 2];
+    if (!g.issued) {
+      const qfs_status st = issue_staged(c, g, c->ev_fwd);
+      if (st != QFS_OK) return st;
+    }
+  }
+  return QFS_OK;
+}
 qfs_status consume_staged(qfs_ctx *c) {
   qfs_ctx::Staged &g = c->stg[c->stg_head];
   CUDA_TRY(c, cudaSetDevice(c->device));
+  if (!g.issued) {
+    const qfs_status st = issue_staged(c, g, nullptr);  // nothing ran since it was queued
+    if (st != QFS_OK) return st;
+  }
   CUDA_TRY(c, cudaStreamWaitEvent(c->st, g.ev, 0));
   const qfs_status st = set_samples_impl(c, g.m_pool, g.x, g.y, g.v, g.xv, g.yv, cudaMemcpyDeviceToDevice, c->st);
   c->stg_head = (c->stg_head + 1) % 2;
@@ -1531,16 +1581,12 @@ qfs_status qfs_set_samples_async(qfs_ctx *c, int m_pool, const double *x, const 
       h.cap_v = bv;
     }
   }
-  CUDA_TRY(c, cudaMemcpyAsync(g.x, x, bxy, cudaMemcpyHostToDevice, c->st_copy));
-  CUDA_TRY(c, cudaMemcpyAsync(g.y, y, bxy, cudaMemcpyHostToDevice, c->st_copy));
-  if (v > 0) {
-    CUDA_TRY(c, cudaMemcpyAsync(g.xv, xv, bv, cudaMemcpyHostToDevice, c->st_copy));
-    CUDA_TRY(c, cudaMemcpyAsync(g.yv, yv, bv, cudaMemcpyHostToDevice, c->st_copy));
-  }
-  CUDA_TRY(c, cudaEventRecord(g.ev, c->st_copy));
+  g.hx = x; g.hy = y; g.hxv = xv; g.hyv = yv;
   g.m_pool = m_pool;
   g.v = v;
+  g.issued = false;
   c->stg_count += 1;
+  if (!c->copy_defer) return issue_staged(c, g, nullptr);
   return QFS_OK;
 }
 
@@ -2015,6 +2061,7 @@ void qfs_destroy(qfs_ctx *c) {
     dfree(g.x); dfree(g.y); dfree(g.xv); dfree(g.yv);
     if (g.ev) cudaEventDestroy(g.ev);
   }
+  if (c->ev_fwd) cudaEventDestroy(c->ev_fwd);
   dfree(c->d_counters1); dfree(c->d_gpart);
   xchg_release(c);
   if (c->h_csum) cudaFreeHost(c->h_csum);
