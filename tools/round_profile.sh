@@ -22,6 +22,11 @@ summ gpurun_out/bench_c5_sample.json c5-sample1 || tail -3 gpurun_out/bench_c5_s
 timeout 600 python bench.py --config c5 --emulate-ranks 8 --steps 5 --no-cpu-baseline > gpurun_out/bench_c5_emul8.json 2> gpurun_out/bench_c5_emul8.err
 summ gpurun_out/bench_c5_emul8.json c5-emul8 || tail -3 gpurun_out/bench_c5_emul8.err
 timeout 600 python tools/xchg_bench.py c5 10 > gpurun_out/xchg_c5.jsonl 2>/dev/null; cat gpurun_out/xchg_c5.jsonl
+for s in 8; do
+  timeout 600 python bench.py --config c5 --starts $s --steps 5 --no-cpu-baseline --no-tts > gpurun_out/bench_c5_s$s.json 2> gpurun_out/bench_c5_s$s.err
+  summ gpurun_out/bench_c5_s$s.json c5-s$s || tail -3 gpurun_out/bench_c5_s$s.err
+done
+if [ -n "$NO_NCU" ]; then echo done; exit 0; fi
 timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-tts > gpurun_out/bench_short.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-tts > gpurun_out/ncu_launch.log 2>&1
