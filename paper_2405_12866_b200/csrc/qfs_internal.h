@@ -77,6 +77,7 @@ struct BwdParams {
   double *gpartials;          // [S_act][40][32] group sums
   double *e_red;              // [S_act][32]: reduced E (sample mode: before all-reduce)
   int fuse_polar;             // 1: the last CTA of each start runs the polar update
+  int nt;                     // threads per CTA of bwd_kernel (bwd_threads; 0 = default)
   int bulk;                   // 1: bwdt_kernel (bulk copies + mbarrier ring), 0: bwd_kernel (LDGSTS)
   // Device-initiated exchange of the partial environments across the xg ranks
   // of sample mode, done by the last CTA of each start
@@ -241,7 +242,8 @@ size_t val_blk_smem(int n, int K, int ld);     // shared memory of the block val
 cudaError_t launch_val_block(const ValRowParams &p, int n_slots, cudaStream_t st);
 size_t val_cl_smem(int n, int K, int t);      // cluster validation, 2^t CTAs per row
 cudaError_t launch_val_cluster(const ValRowParams &p, int n_slots, cudaStream_t st);        // largest n the shared-memory validation forward supports
-int blocks_per_sm(int nu);  // resident CTAs per SM of the backward kernel
+int bwd_threads(int n_slots);  // threads per CTA of the LDGSTS backward launch
+int blocks_per_sm(int nt);  // resident CTAs per SM of the backward kernel at nt threads
 size_t bt_smem_bytes(int nu);     // dynamic shared memory of the bulk-copy backward kernel
 int bwdt_units_per_cta_min();     // fewest stages a bulk-copy backward CTA is given
 

@@ -39,6 +39,9 @@ namespace {
 #ifndef QFS_BWD_MINB
 #define QFS_BWD_MINB 1
 #endif
+#ifndef QFS_BWD_HALF_SLOTS
+#define QFS_BWD_HALF_SLOTS 2  // starts per launch from which the backward runs 128-thread CTAs, 2 per SM
+#endif
 #ifndef QFS_WIDE_RED
 #define QFS_WIDE_RED 1  // backward, many CTAs per start: one-ticket reduction by all warps of the last CTA
 #endif
@@ -128,9 +131,10 @@ __host__ __device__ constexpr int pv_idx(int q, int l) {
   return v;
 }
 
+template <int NT>
 struct BwdShared {
   double2 sQ[16];                          // G_{i+1}^dag
-  double2 red[BWD_THREADS / 32][4][16];    // per-warp (per lane-group) E partials
+  double2 red[NT / 32][4][16];            // per-warp (per lane-group) E partials
   double sum32[32];
   double2 scratch[64];                     // polar scratch: 32 per half warp
 };
@@ -151,12 +155,12 @@ struct BwdShared {
 // chi/phi of the next items are staged into shared memory by LDGSTS,
 // BWD_STAGES-1 items ahead.  Reductions run in a fixed order (lanes, lane
 // groups, warps), so the partial is deterministic for a given launch shape.
-template <int NU, int TP0, int TP1, bool UPD, bool IDENT>
+template <int NT, int NU, int TP0, int TP1, bool UPD, bool IDENT>
 __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslot, int s,
-                                 unsigned Ms, BwdShared &sh, double2 *stage_buf) {
+                                 unsigned Ms, BwdShared<NT> &sh, double2 *stage_buf) {
   constexpr int T = 1 << (NU - 2);
   constexpr int LPT = 32 / T;
-  constexpr int NWARP = BWD_THREADS / 32;
+  constexpr int NWARP = NT / 32;
   constexpr int PLO = ((TP0 < 2) ? (1 << TP0) : 0) | ((TP1 < 2) ? (1 << TP1) : 0);
   constexpr int NPT_T = (((1 << NU) - 1) & ~((1 << TP0) | (1 << TP1))) >> 2;
   constexpr bool XPOSE = (NU == 4);
@@ -239,7 +243,7 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
 #if QFS_BWD_EDRING
     if (chi) edr[BWD_STAGES - 1] = ok ? ed : 0xffffffffu;
 #endif
-    double2 *st = stage_buf + (k % BWD_STAGES) * 8 * BWD_THREADS + threadIdx.x;
+    double2 *st = stage_buf + (k % BWD_STAGES) * 8 * NT + threadIdx.x;
 #if QFS_BWD_BYTEOFF
     // 32-bit byte offsets from the start's base (one start's block < 4 GB):
     // one add per address instead of 64-bit element arithmetic per address
@@ -247,32 +251,32 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
     if (chi) {
       const unsigned eb = ec << 4;
 #pragma unroll
-      for (int l = 0; l < 4; ++l) cp_async16(st + l * BWD_THREADS, cbase + (eb + (offc[l] << 4)), ok);
+      for (int l = 0; l < 4; ++l) cp_async16(st + l * NT, cbase + (eb + (offc[l] << 4)), ok);
     }
     if (IDENT && phi) {  // implicit basis x_m = e_m (gate 0 of a QF sweep): synthesised, not loaded
 #pragma unroll
       for (int l = 0; l < 4; ++l) {
         const unsigned a = lg + (unsigned)G.off[XPOSE ? (t + 4 * (t ^ l)) : (4 * t + l)];
-        st[(4 + l) * BWD_THREADS] = make_double2(ok && a == lm ? 1.0 : 0.0, 0.0);
+        st[(4 + l) * NT] = make_double2(ok && a == lm ? 1.0 : 0.0, 0.0);
       }
     } else if (phi) {
       const unsigned eb = ef << 4;
 #pragma unroll
 #if QFS_BWD_HINT & 1  // phi = B_i is read once: L2 evict_first
       for (int l = 0; l < 4; ++l)
-        cp_async16_hint(st + (4 + l) * BWD_THREADS, fbase + (eb + (offf[l] << 4)), ok, pol_phi);
+        cp_async16_hint(st + (4 + l) * NT, fbase + (eb + (offf[l] << 4)), ok, pol_phi);
 #else
-      for (int l = 0; l < 4; ++l) cp_async16(st + (4 + l) * BWD_THREADS, fbase + (eb + (offf[l] << 4)), ok);
+      for (int l = 0; l < 4; ++l) cp_async16(st + (4 + l) * NT, fbase + (eb + (offf[l] << 4)), ok);
 #endif
     }
 #else
     if (chi) {
 #pragma unroll
-      for (int l = 0; l < 4; ++l) cp_async16(st + l * BWD_THREADS, csrc + (ok ? ec + offc[l] : 0u), ok);
+      for (int l = 0; l < 4; ++l) cp_async16(st + l * NT, csrc + (ok ? ec + offc[l] : 0u), ok);
     }
     if (phi) {
 #pragma unroll
-      for (int l = 0; l < 4; ++l) cp_async16(st + (4 + l) * BWD_THREADS, fsrc + (ok ? ef + offf[l] : 0u), ok);
+      for (int l = 0; l < 4; ++l) cp_async16(st + (4 + l) * NT, fsrc + (ok ? ef + offf[l] : 0u), ok);
     }
 #endif
   };
@@ -334,12 +338,12 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
     unsigned ec = 0, ed = 0, ef = 0;
     const bool valid = locate(k, ec, ed, ef);
 #endif
-    double2 *st = stage_buf + (k % BWD_STAGES) * 8 * BWD_THREADS + threadIdx.x;
+    double2 *st = stage_buf + (k % BWD_STAGES) * 8 * NT + threadIdx.x;
     double2 c[4], f[4];
 #pragma unroll
-    for (int l = 0; l < 4; ++l) c[l] = st[l * BWD_THREADS];
+    for (int l = 0; l < 4; ++l) c[l] = st[l * NT];
 #pragma unroll
-    for (int l = 0; l < 4; ++l) f[l] = st[(4 + l) * BWD_THREADS];
+    for (int l = 0; l < 4; ++l) f[l] = st[(4 + l) * NT];
 #ifdef QFS_DIAG_NOCOMPUTE  // diagnostic build: memory traffic only (results invalid)
     if (UPD && cdst && valid) {
       double2 *dp = cdst + ed;
@@ -382,13 +386,13 @@ __device__ bool bwd_gate_partial(const BwdParams &P, const GateDesc &G, int jslo
       // transpose through this stage's (already consumed) chi slots
       __syncwarp();
 #pragma unroll
-      for (int l = 0; l < 4; ++l) st[l * BWD_THREADS] = c[l];
+      for (int l = 0; l < 4; ++l) st[l * NT] = c[l];
       __syncwarp();
       double2 r[4];
       const int lane_base = threadIdx.x - lane;
 #pragma unroll
       for (int x = 0; x < 4; ++x)
-        r[x] = stage_buf[(k % BWD_STAGES) * 8 * BWD_THREADS + t * BWD_THREADS + lane_base + (lane ^ (x * LPT))];
+        r[x] = stage_buf[(k % BWD_STAGES) * 8 * NT + t * NT + lane_base + (lane ^ (x * LPT))];
 #pragma unroll
       for (int x = 0; x < 4; ++x)
 #pragma unroll
@@ -539,7 +543,8 @@ __device__ void bwd_finish_e(const BwdParams &P, const GateDesc &G, int jslot, i
 
 // Warp 0 of the last CTA of a start: sum the CTA partials in CTA order, and
 // (fuse_polar) run the polar update of gate i.
-__device__ void bwd_finish(const BwdParams &P, const GateDesc &G, int jslot, int s, BwdShared &sh, int kind) {
+template <int NT>
+__device__ void bwd_finish(const BwdParams &P, const GateDesc &G, int jslot, int s, BwdShared<NT> &sh, int kind) {
   if (P.dbg && threadIdx.x == 0) atomicMax(P.dbg + 4 * G.env_gate + 1, gtimer());
   const double *pp = P.partials + (long long)jslot * P.nb * 32 + threadIdx.x;
   double e = 0.0;
@@ -565,18 +570,18 @@ __device__ void bwd_finish(const BwdParams &P, const GateDesc &G, int jslot, int
 // sums in warp order: deterministic, one ticket on the critical path (C5:
 // 2.7 -> 0.95 us per gate).  A separate instantiation, so the few-CTA path
 // compiles exactly as before.
-template <int NU, int TP0, int TP1, bool UPD, bool WIDE, bool IDENT = false>
-__global__ void __launch_bounds__(BWD_THREADS, QFS_BWD_MINB) bwd_kernel(const BwdParams P) {
-  __shared__ BwdShared sh;
-  // [BWD_STAGES][8][BWD_THREADS]; 128-byte alignment measured to matter: with
+template <int NU, int TP0, int TP1, bool UPD, bool WIDE, bool IDENT = false, int NT = BWD_THREADS>
+__global__ void __launch_bounds__(NT, NT == BWD_THREADS ? QFS_BWD_MINB : 2) bwd_kernel(const BwdParams P) {
+  __shared__ BwdShared<NT> sh;
+  // [BWD_STAGES][8][NT]; 128-byte alignment measured to matter: with
   // static shared memory of 16 * odd bytes in front of it the kernel ran 12 % slower
   extern __shared__ __align__(128) double2 stage_buf[];
   const int jslot = blockIdx.y;
   const Slot sl = P.slots[jslot];
   if constexpr (WIDE) {
-    constexpr int NWARP = BWD_THREADS / 32, FL = 24;
+    constexpr int NWARP = NT / 32, FL = 24;
     __shared__ unsigned last_cta;
-    const bool w0 = bwd_gate_partial<NU, TP0, TP1, UPD, IDENT>(P, P.g, jslot, sl.s, (unsigned)sl.m, sh, stage_buf);
+    const bool w0 = bwd_gate_partial<NT, NU, TP0, TP1, UPD, IDENT>(P, P.g, jslot, sl.s, (unsigned)sl.m, sh, stage_buf);
     if (w0) {
       const bool last = warp0_elect_last(&P.counters[jslot], (unsigned)P.nb);
       if (threadIdx.x == 0) last_cta = last ? 1u : 0u;
@@ -607,7 +612,7 @@ __global__ void __launch_bounds__(BWD_THREADS, QFS_BWD_MINB) bwd_kernel(const Bw
     bwd_finish_e(P, P.g, jslot, sl.s, sh, e, kind);
     return;
   }
-  if (!bwd_gate_partial<NU, TP0, TP1, UPD, IDENT>(P, P.g, jslot, sl.s, (unsigned)sl.m, sh, stage_buf))
+  if (!bwd_gate_partial<NT, NU, TP0, TP1, UPD, IDENT>(P, P.g, jslot, sl.s, (unsigned)sl.m, sh, stage_buf))
     return;
   const int kind = P.kinds ? __ldg(P.kinds + P.g.env_gate) : 0;
   const int ng = (P.nb + RED_GS - 1) / RED_GS;
@@ -1697,7 +1702,12 @@ cudaError_t launch_ex(void (*k)(Prm), dim3 grid, dim3 block, size_t smem, cudaSt
 void set_pdl(bool on) { g_pdl = on; }
 bool pdl_enabled() { return g_pdl; }
 int val_row_max_n() { return 13; }
-int blocks_per_sm(int nu) { (void)nu; return QFS_BWD_MINB; }
+// LDGSTS backward shape: 128 threads x 2 CTAs per SM when the launch carries
+// at least QFS_BWD_HALF_SLOTS starts (C4, 16 starts: bwd 16.0 -> 15.5 us; the
+// finer CTAs overlap one another's reduction tail), else 256 x 1 (C5, one
+// start: twice the CTA partials on the per-gate critical path, 11.4 -> 13.5 us)
+int bwd_threads(int n_slots) { return n_slots >= QFS_BWD_HALF_SLOTS ? 128 : BWD_THREADS; }
+int blocks_per_sm(int nt) { return nt == BWD_THREADS ? QFS_BWD_MINB : 2; }
 
 cudaError_t launch_bwdt(const BwdParams &p, int n_slots, cudaStream_t st) {
   dim3 grid(p.nb, n_slots), block(BT_THREADS);
@@ -1745,27 +1755,40 @@ int bwdt_units_per_cta_min() { return 4; }
 
 cudaError_t launch_bwd(const BwdParams &p, int n_slots, cudaStream_t st) {
   if (p.bulk) return launch_bwdt(p, n_slots, st);
-  dim3 grid(p.nb, n_slots), block(BWD_THREADS);
-  const int smem = BWD_STAGES * 8 * BWD_THREADS * (int)sizeof(double2);
   const GateDesc &g = p.g;
+  // two-CTA-per-SM shape (128 threads; runtime bwd_threads)
+  const bool half = p.nt == 128 && BWD_THREADS != 128;
+  const int nt = half ? 128 : BWD_THREADS;
+  dim3 grid(p.nb, n_slots), block(nt);
+  const int smem = BWD_STAGES * 8 * nt * (int)sizeof(double2);
   const bool wide = QFS_WIDE_RED && p.counters1 && (p.nb + RED_GS - 1) / RED_GS > 1;
-#define QFS_BWD1(NU, A, B, U, W)                                                               \
+#define QFS_BWD1N(NU, A, B, U, W, NT)                                                          \
   do {                                                                                         \
     static bool attr = false;                                                                  \
     if (!attr) {                                                                               \
-      cudaFuncSetAttribute(bwd_kernel<NU, A, B, U, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+      cudaFuncSetAttribute(bwd_kernel<NU, A, B, U, W, false, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
       attr = true;                                                                             \
     }                                                                                          \
-    launch_ex(bwd_kernel<NU, A, B, U, W>, grid, block, smem, st, p);                           \
+    launch_ex(bwd_kernel<NU, A, B, U, W, false, NT>, grid, block, smem, st, p);                \
   } while (0)
-#define QFS_BWD1I(NU, A, B, U, W)                                                              \
+#define QFS_BWD1(NU, A, B, U, W)                    \
+  do {                                              \
+    if (half) QFS_BWD1N(NU, A, B, U, W, 128);       \
+    else QFS_BWD1N(NU, A, B, U, W, BWD_THREADS);    \
+  } while (0)
+#define QFS_BWD1IN(NU, A, B, U, W, NT)                                                         \
   do {                                                                                         \
     static bool attr = false;                                                                  \
     if (!attr) {                                                                               \
-      cudaFuncSetAttribute(bwd_kernel<NU, A, B, U, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+      cudaFuncSetAttribute(bwd_kernel<NU, A, B, U, W, true, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
       attr = true;                                                                             \
     }                                                                                          \
-    launch_ex(bwd_kernel<NU, A, B, U, W, true>, grid, block, smem, st, p);                     \
+    launch_ex(bwd_kernel<NU, A, B, U, W, true, NT>, grid, block, smem, st, p);                 \
+  } while (0)
+#define QFS_BWD1I(NU, A, B, U, W)                   \
+  do {                                              \
+    if (half) QFS_BWD1IN(NU, A, B, U, W, 128);      \
+    else QFS_BWD1IN(NU, A, B, U, W, BWD_THREADS);   \
   } while (0)
   // IDENT: phi is the implicit basis (gate 0 of a QFactor sweep, qfs_set_samples_basis) —
   // its own instantiation so the common kernels keep their register budget
@@ -1793,7 +1816,9 @@ cudaError_t launch_bwd(const BwdParams &p, int n_slots, cudaStream_t st) {
   }
 #undef QFS_BWD
 #undef QFS_BWD1
+#undef QFS_BWD1N
 #undef QFS_BWD1I
+#undef QFS_BWD1IN
   return cudaGetLastError();
 }
 

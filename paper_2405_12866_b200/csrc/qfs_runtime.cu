@@ -940,7 +940,8 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
     } else {
       const long long lpt = 32 >> (nu - 2);
       const long long un = (N >> nu) * ((M_max + lpt - 1) / lpt);
-      b.nb = blocks_per_start(un * 32, ns, blocks_per_sm(nu));
+      b.nt = bwd_threads(ns);
+      b.nb = blocks_per_start(un * 32, ns, blocks_per_sm(b.nt));
     }
     {
       LaunchScope ls(c, K_BWD, units * (upd ? 48.0 : 32.0), units * (upd ? 64.0 : 32.0));
