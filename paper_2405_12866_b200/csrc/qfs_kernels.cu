@@ -42,6 +42,9 @@ namespace {
 #ifndef QFS_BWD_HALF_SLOTS
 #define QFS_BWD_HALF_SLOTS 2  // starts per launch from which the backward runs 128-thread CTAs, 2 per SM
 #endif
+#ifndef QFS_BWD_HALF_MINB
+#define QFS_BWD_HALF_MINB 2   // resident 128-thread backward CTAs per SM
+#endif
 #ifndef QFS_WIDE_RED
 #define QFS_WIDE_RED 1  // backward, many CTAs per start: one-ticket reduction by all warps of the last CTA
 #endif
@@ -571,7 +574,7 @@ __device__ void bwd_finish(const BwdParams &P, const GateDesc &G, int jslot, int
 // 2.7 -> 0.95 us per gate).  A separate instantiation, so the few-CTA path
 // compiles exactly as before.
 template <int NU, int TP0, int TP1, bool UPD, bool WIDE, bool IDENT = false, int NT = BWD_THREADS>
-__global__ void __launch_bounds__(NT, NT == BWD_THREADS ? QFS_BWD_MINB : 2) bwd_kernel(const BwdParams P) {
+__global__ void __launch_bounds__(NT, NT == BWD_THREADS ? QFS_BWD_MINB : QFS_BWD_HALF_MINB) bwd_kernel(const BwdParams P) {
   __shared__ BwdShared<NT> sh;
   // [BWD_STAGES][8][NT]; 128-byte alignment measured to matter: with
   // static shared memory of 16 * odd bytes in front of it the kernel ran 12 % slower
@@ -1707,7 +1710,7 @@ int val_row_max_n() { return 13; }
 // finer CTAs overlap one another's reduction tail), else 256 x 1 (C5, one
 // start: twice the CTA partials on the per-gate critical path, 11.4 -> 13.5 us)
 int bwd_threads(int n_slots) { return n_slots >= QFS_BWD_HALF_SLOTS ? 128 : BWD_THREADS; }
-int blocks_per_sm(int nt) { return nt == BWD_THREADS ? QFS_BWD_MINB : 2; }
+int blocks_per_sm(int nt) { return nt == BWD_THREADS ? QFS_BWD_MINB : QFS_BWD_HALF_MINB; }
 
 cudaError_t launch_bwdt(const BwdParams &p, int n_slots, cudaStream_t st) {
   dim3 grid(p.nb, n_slots), block(BT_THREADS);
