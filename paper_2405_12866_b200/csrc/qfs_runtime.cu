@@ -831,7 +831,7 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
         f.dst2 = ViewW{Bk(k + 2), sS, Mc, 1};
         f.s2 = make_scatter(Lk, loc, nu, LY(k + 2), n);
       }
-      f.nb = blocks_per_start(((long long)M_max * N) >> nu, ns, fwd2_min_blocks());
+      f.nb = blocks_per_start(((long long)M_max * N) >> nu, ns, 1);  // fwdp_kernel: 256 threads, one CTA per SM
       const double fb = k + 2 < K ? 48.0 : 32.0;
       LaunchScope ls(c, K_FWD_GATE, units * fb, units * (k + 2 < K ? 64.0 : 32.0));
       CUDA_TRY(c, launch_fwdp(f, ns, st));
