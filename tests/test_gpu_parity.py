@@ -373,6 +373,29 @@ def test_deterministic_bitwise(qfs, path):
     assert np.array_equal(a["gates"], b["gates"]) and np.array_equal(a["cost"], b["cost"])
 
 
+def test_launch_shape_independence(qfs):
+    """A start's sweep does not depend on the batch it runs in beyond summation
+    order: 4 starts in one launch (128-thread backward CTAs, 2 per SM, 37 per
+    start) vs each start alone (256-thread CTAs, 148 per start, the all-warp
+    WIDE reduction), streamed path; both within the oracle tolerances."""
+    p = I.make_problem("c4", init="R", s=4, k=14)
+    m = 32
+    ctx = _ctx(qfs, p.n, p.pairs, "streamed")
+    ctx.set_samples(p.x, p.y, p.xv, p.yv)
+    tb = ctx.trace_sweeps(p.init, m, 3)
+    ot = oracle.trace_sweeps(p.n, p.pairs, p.init, p.x, p.y, m, 3)
+    for s in range(4):
+        ts = ctx.trace_sweeps(p.init[s:s + 1], m, 3)
+        for t in range(3):
+            for i in range(p.k):
+                eo = ot["env"][t, i, s]
+                assert np.linalg.norm(tb["env"][t, i, s] - eo) <= ENV_TOL * np.linalg.norm(eo)
+                assert np.linalg.norm(ts["env"][t, i, 0] - eo) <= ENV_TOL * np.linalg.norm(eo)
+                assert np.linalg.norm(ts["env"][t, i, 0] - tb["env"][t, i, s]) <= 1e-12 * np.linalg.norm(eo)
+            assert abs(ts["cost"][t, 0] - tb["cost"][t, s]) <= 1e-12 * tb["cost"][t, s] + 1e-15
+    ctx.close()
+
+
 def test_errors(qfs):
     from paper_2405_12866_b200.qfs import QfsError
     p = I.make_problem("c1")
