@@ -229,6 +229,9 @@ cudaError_t launch_identity_fill(double2 *v, long long count16, cudaStream_t st)
 cudaError_t launch_copy(double2 *dst, const double2 *src, long long count, cudaStream_t st);  // device copy by a kernel
 cudaError_t launch_copy_bytes(void *dst, const void *src, size_t bytes, cudaStream_t st);  // 4-byte granular
 cudaError_t launch_fill_words(unsigned *dst, unsigned value, long long count, cudaStream_t st);
+// hdst / hcheck / hflag: device pointers of mapped pinned host memory
+cudaError_t launch_publish(const double *src, int count, const unsigned *check, double *hdst, unsigned *hcheck,
+                           unsigned long long *hflag, unsigned long long seq, cudaStream_t st);
 cudaError_t launch_gate_check(const double2 *g, long long count, int K, const int *kinds, unsigned *flag,
                               cudaStream_t st);  // initial-gate validation bits into *flag
 void set_pdl(bool on);     // launch with programmatic dependent launch (default on)

@@ -1572,6 +1572,21 @@ __global__ void copy_words_kernel(unsigned *dst, const unsigned *src, long long 
     dst[i] = src[i];
 }
 
+// End of a sweep: the per-start cost sums (and, once per call, the gate-check
+// flag) written straight into mapped pinned host memory, then the sweep's
+// sequence number — the host spins on it (run_sweep) instead of a
+// device-to-host copy plus a stream synchronisation (C2: ~10 us less per
+// controller step).  One CTA; every value store is ordered before the flag by
+// the system-scope fence of its own thread and the CTA barrier.
+__global__ void publish_kernel(const double *src, int count, const unsigned *check, double *hdst,
+                               unsigned *hcheck, unsigned long long *hflag, unsigned long long seq) {
+  for (int i = threadIdx.x; i < count; i += blockDim.x) hdst[i] = src[i];
+  if (check && threadIdx.x == 0) *hcheck = *check;
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) st_release_sys(hflag, seq);
+}
+
 __global__ void fill_words_kernel(unsigned *dst, unsigned value, long long count) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
        i += (long long)gridDim.x * blockDim.x)
@@ -1959,6 +1974,12 @@ cudaError_t launch_copy_bytes(void *dst, const void *src, size_t bytes, cudaStre
   if (words <= 0) return cudaSuccess;
   const long long blocks = std::min<long long>((words + 255) / 256, 148 * 8);
   copy_words_kernel<<<(unsigned)blocks, 256, 0, st>>>((unsigned *)dst, (const unsigned *)src, words);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_publish(const double *src, int count, const unsigned *check, double *hdst, unsigned *hcheck,
+                           unsigned long long *hflag, unsigned long long seq, cudaStream_t st) {
+  publish_kernel<<<1, 256, 0, st>>>(src, count, check, hdst, hcheck, hflag, seq);
   return cudaGetLastError();
 }
 

@@ -129,6 +129,7 @@ struct qfs_ctx {
   // phase of the next sweep (event recorded inside the sweep graph), i.e.
   // during the latency-bound backward instead of the write-bound forward
   bool copy_defer = true;
+  bool pub_off = false;     // QFS_PUBLISH=0: results by D2H copy + stream synchronisation (A/B)
   cudaEvent_t ev_fwd = nullptr;
   // pinned host staging of the gates (upload / download through page-locked
   // memory, so the small copies do not queue behind a pageable staging path)
@@ -140,6 +141,9 @@ struct qfs_ctx {
   bool check_pending = false;
   bool check_fetched = false;   // h_check already read back with the last sweep's costs
   size_t h_slots_cap = 0;
+  int slots_on_dev = 0;
+  unsigned long long *h_pubflag = nullptr;  // mapped pinned: sequence number of the last published sweep
+  unsigned long long pub_seq = 0;     // d_slots holds h_slots[0, slots_on_dev) (skip the upload when unchanged)
   cudaStream_t st_copy = nullptr;
   // graph cache
   cudaGraphExec_t gexec = nullptr;
@@ -372,10 +376,9 @@ qfs_status ensure_state(qfs_ctx *c, int S, int M, int V) {
   CUDA_TRY(c, cudaStreamSynchronize(c->st));
   dfree(c->d_chi); dfree(c->d_chi2); dfree(c->d_B); dfree(c->d_vb0); dfree(c->d_vb1); dfree(c->d_bpart);
   dfree(c->d_partials); dfree(c->d_ered); dfree(c->d_sig); dfree(c->d_csum); dfree(c->d_rowout);
-  dfree(c->d_cval); dfree(c->d_counters); dfree(c->d_slots);
+  c->d_cval = nullptr; dfree(c->d_counters); dfree(c->d_slots);
   dfree(c->d_counters1); dfree(c->d_gpart);
   if (c->h_csum) cudaFreeHost(c->h_csum);
-  if (c->h_cval) cudaFreeHost(c->h_cval);
   c->h_csum = c->h_cval = nullptr;
   c->S_cap = c->M_cap = c->V_cap = c->nb_cap = 0;
   c->K_s = 0;
@@ -401,8 +404,10 @@ qfs_status ensure_state(qfs_ctx *c, int S, int M, int V) {
   CUDA_TRY(c, cudaMalloc(&c->d_partials, (size_t)S * nbc * 32 * sizeof(double)));
   CUDA_TRY(c, cudaMalloc(&c->d_ered, (size_t)S * 32 * sizeof(double)));
   CUDA_TRY(c, cudaMalloc(&c->d_sig, (size_t)S * c->K * sizeof(double)));
-  CUDA_TRY(c, cudaMalloc(&c->d_csum, (size_t)S * sizeof(double)));
-  CUDA_TRY(c, cudaMalloc(&c->d_cval, (size_t)S * sizeof(double)));
+  // per-start cost sums: csum [S] then cval [S] in ONE buffer (device and
+  // pinned host), so a sweep's results come back in one copy
+  CUDA_TRY(c, cudaMalloc(&c->d_csum, (size_t)2 * S * sizeof(double)));
+  c->d_cval = c->d_csum + S;
   CUDA_TRY(c, cudaMalloc(&c->d_rowout, (size_t)S * std::max(V, 1) * sizeof(double)));
   CUDA_TRY(c, cudaMalloc(&c->d_counters, (size_t)S * 2 * sizeof(unsigned)));
   CUDA_TRY(c, cudaMemset(c->d_counters, 0, (size_t)S * 2 * sizeof(unsigned)));
@@ -410,8 +415,9 @@ qfs_status ensure_state(qfs_ctx *c, int S, int M, int V) {
   CUDA_TRY(c, cudaMalloc(&c->d_counters1, (size_t)S * 40 * sizeof(unsigned)));
   CUDA_TRY(c, cudaMemset(c->d_counters1, 0, (size_t)S * 40 * sizeof(unsigned)));
   CUDA_TRY(c, cudaMalloc(&c->d_gpart, (size_t)S * 40 * 32 * sizeof(double)));
-  CUDA_TRY(c, cudaMallocHost(&c->h_csum, (size_t)S * sizeof(double)));
-  CUDA_TRY(c, cudaMallocHost(&c->h_cval, (size_t)S * sizeof(double)));
+  CUDA_TRY(c, cudaHostAlloc((void **)&c->h_csum, (size_t)2 * S * sizeof(double), cudaHostAllocMapped));
+  c->h_cval = c->h_csum + S;
+  c->slots_on_dev = 0;  // d_slots is new
   c->S_cap = S; c->M_cap = M; c->V_cap = V; c->nb_cap = nbc;
   c->K_s = c->K;
   return QFS_OK;
@@ -1039,6 +1045,26 @@ qfs_status issue_sweep(qfs_ctx *c, const SweepSpec &sp) {
   return issue_group(c, sp, 0, (int)sp.slots.size(), c->st);
 }
 
+// Spin until the publish kernel of sweep `seq` has written its results (see
+// publish_kernel); every 256 polls the stream is queried, so a failed launch
+// or a sticky device error is reported instead of spinning forever.
+qfs_status wait_published(qfs_ctx *c, unsigned long long seq) {
+  for (unsigned it = 1;; ++it) {
+    if (__atomic_load_n(c->h_pubflag, __ATOMIC_ACQUIRE) == seq) return QFS_OK;
+    if ((it & 255u) == 0) {
+      const cudaError_t e = cudaStreamQuery(c->st);
+      if (e == cudaSuccess) {
+        if (__atomic_load_n(c->h_pubflag, __ATOMIC_ACQUIRE) == seq) return QFS_OK;
+        return fail(c, QFS_ERR_DEVICE, "sweep finished without publishing its results");
+      }
+      if (e != cudaErrorNotReady) return fail(c, QFS_ERR_DEVICE, cudaGetErrorString(e));
+    }
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+  }
+}
+
 // Run one sweep: upload the slot table, issue (graph-captured when not
 // profiling and not tracing), and copy the per-start cost sums back.
 qfs_status run_sweep(qfs_ctx *c, const SweepSpec &sp, std::vector<double> &csum,
@@ -1051,15 +1077,20 @@ qfs_status run_sweep(qfs_ctx *c, const SweepSpec &sp, std::vector<double> &csum,
     c->h_slots_cap = 0;
     CUDA_TRY(c, cudaHostAlloc((void **)&c->h_slots, (size_t)std::max(ns, 64) * sizeof(Slot), cudaHostAllocMapped));
     c->h_slots_cap = (size_t)std::max(ns, 64);
+    c->slots_on_dev = 0;
   }
   // (the previous table's reader, a copy kernel, finished before the previous
-  // run_sweep returned: it ends with a stream synchronisation)
-  std::memcpy(c->h_slots, sp.slots.data(), ns * sizeof(Slot));
-  {
+  // run_sweep returned: it ends with a stream synchronisation).  Unchanged
+  // table (the same active starts and M as the last sweep): nothing to copy —
+  // one launch less on the per-sweep host round trip of the short sweeps
+  if (ns != c->slots_on_dev || std::memcmp(c->h_slots, sp.slots.data(), ns * sizeof(Slot)) != 0) {
+    std::memcpy(c->h_slots, sp.slots.data(), ns * sizeof(Slot));
+    c->slots_on_dev = 0;
     Slot *dh = nullptr;
     CUDA_TRY(c, cudaHostGetDevicePointer((void **)&dh, c->h_slots, 0));
     static_assert(sizeof(Slot) == 8, "Slot is copied as double2 halves");
     CUDA_TRY(c, launch_copy_bytes(c->d_slots, dh, ns * sizeof(Slot), c->st));
+    c->slots_on_dev = ns;
   }
   if (c->d_dbg) {
     std::vector<unsigned long long> init((size_t)4 * c->K);
@@ -1104,14 +1135,32 @@ qfs_status run_sweep(qfs_ctx *c, const SweepSpec &sp, std::vector<double> &csum,
     const qfs_status s = issue_deferred(c);
     if (s != QFS_OK) return s;
   }
-  CUDA_TRY(c, cudaMemcpyAsync(c->h_csum, c->d_csum, ns * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-  if (sp.want_val && c->V > 0)
-    CUDA_TRY(c, cudaMemcpyAsync(c->h_cval, c->d_cval, ns * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-  if (c->check_pending && !c->check_fetched) {  // the gate-check flag rides on the same synchronisation
-    CUDA_TRY(c, cudaMemcpyAsync(c->h_check, c->d_check, sizeof(unsigned), cudaMemcpyDeviceToHost, c->st));
-    c->check_fetched = true;
+  // csum [0, ns) and cval [S_cap, S_cap + ns) in one copy
+  const size_t nrb = sp.want_val && c->V > 0 ? (size_t)c->S_cap + ns : (size_t)ns;
+  const bool with_check = c->check_pending && !c->check_fetched;  // the gate-check flag rides along
+  if (c->prof || c->d_dbg || c->pub_off) {
+    // profiling / debug timing read events and buffers right after: a full synchronisation
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_csum, c->d_csum, nrb * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    if (with_check) CUDA_TRY(c, cudaMemcpyAsync(c->h_check, c->d_check, sizeof(unsigned), cudaMemcpyDeviceToHost, c->st));
+    CUDA_TRY(c, cudaStreamSynchronize(c->st));
+  } else {
+    // results published by a kernel into mapped pinned memory; the host spins on the sequence number
+    if (!c->h_pubflag) {
+      CUDA_TRY(c, cudaHostAlloc((void **)&c->h_pubflag, 64, cudaHostAllocMapped));
+      *c->h_pubflag = c->pub_seq;
+    }
+    double *dh = nullptr;
+    unsigned *dchk = nullptr;
+    unsigned long long *dflag = nullptr;
+    CUDA_TRY(c, cudaHostGetDevicePointer((void **)&dh, c->h_csum, 0));
+    CUDA_TRY(c, cudaHostGetDevicePointer((void **)&dchk, c->h_check, 0));
+    CUDA_TRY(c, cudaHostGetDevicePointer((void **)&dflag, c->h_pubflag, 0));
+    const unsigned long long seq = ++c->pub_seq;
+    CUDA_TRY(c, launch_publish(c->d_csum, (int)nrb, with_check ? c->d_check : nullptr, dh, dchk, dflag, seq, c->st));
+    const qfs_status ws = wait_published(c, seq);
+    if (ws != QFS_OK) return ws;
   }
-  CUDA_TRY(c, cudaStreamSynchronize(c->st));
+  if (with_check) c->check_fetched = true;
   csum.assign(c->h_csum, c->h_csum + ns);
   if (sp.want_val && c->V > 0) cval.assign(c->h_cval, c->h_cval + ns);
   else cval.assign(ns, NAN);
@@ -1156,7 +1205,7 @@ qfs_status gate_check_result(qfs_ctx *c) {
 
 qfs_status upload_gates(qfs_ctx *c, int s, const double *init) {
   if (!c->h_check) {
-    CUDA_TRY(c, cudaMallocHost((void **)&c->h_check, sizeof(unsigned)));
+    CUDA_TRY(c, cudaHostAlloc((void **)&c->h_check, sizeof(unsigned), cudaHostAllocMapped));
   }
   const size_t gb = (size_t)s * c->gsz * sizeof(double2);
   if (gb > c->h_gates_cap) {
@@ -1259,6 +1308,7 @@ qfs_status create_common(int n, int k, const int32_t *pairs, int device, qfs_ctx
   if (const char *rp = getenv("QFS_RES_PER_SM")) c->res_per_sm = atoi(rp) == 2 ? 2 : 1;
   if (const char *uf = getenv("QFS_UNFUSED_POLAR")) c->force_unfused = atoi(uf) != 0;
   if (const char *cd = getenv("QFS_COPY_DEFER")) c->copy_defer = atoi(cd) != 0;
+  if (const char *pb = getenv("QFS_PUBLISH")) c->pub_off = atoi(pb) == 0;
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fwd, cudaEventDisableTiming);
   if (const char *bb = getenv("QFS_BWD_BULK")) c->bwd_bulk = atoi(bb) != 0;
   if (const char *bm = getenv("QFS_BULK_MIN_M")) c->bulk_min_m = std::max(1, atoi(bm));
@@ -2048,9 +2098,10 @@ void qfs_destroy(qfs_ctx *c) {
   dfree(c->d_pairs); dfree(c->d_kinds); dfree(c->d_bg); dfree(c->d_bpart); dfree(c->d_flag); dfree(c->d_x); dfree(c->d_y); dfree(c->d_xv); dfree(c->d_yv);
   dfree(c->d_gates); dfree(c->d_chi); dfree(c->d_chi2); dfree(c->d_B); dfree(c->d_vb0); dfree(c->d_vb1);
   dfree(c->d_partials); dfree(c->d_ered); dfree(c->d_sig); dfree(c->d_csum); dfree(c->d_rowout);
-  dfree(c->d_cval); dfree(c->d_counters); dfree(c->d_slots); dfree(c->d_env_trace);
+  c->d_cval = nullptr; dfree(c->d_counters); dfree(c->d_slots); dfree(c->d_env_trace);
   dfree(c->d_stage); dfree(c->d_vprev);
   if (c->h_check) cudaFreeHost(c->h_check);
+  if (c->h_pubflag) cudaFreeHost(c->h_pubflag);
   dfree(c->d_check);
   if (c->h_gates) cudaFreeHost(c->h_gates);
   if (c->h_slots) cudaFreeHost(c->h_slots);
@@ -2066,7 +2117,6 @@ void qfs_destroy(qfs_ctx *c) {
   dfree(c->d_counters1); dfree(c->d_gpart);
   xchg_release(c);
   if (c->h_csum) cudaFreeHost(c->h_csum);
-  if (c->h_cval) cudaFreeHost(c->h_cval);
   if (c->st) cudaStreamDestroy(c->st);
   if (c->owns_comm && c->comm) ncclCommDestroy(c->comm);
   delete c;
