@@ -1090,6 +1090,7 @@ qfs_status run_sweep(qfs_ctx *c, const SweepSpec &sp, std::vector<double> &csum,
     CUDA_TRY(c, cudaHostGetDevicePointer((void **)&dh, c->h_slots, 0));
     static_assert(sizeof(Slot) == 8, "Slot is copied as double2 halves");
     CUDA_TRY(c, launch_copy_bytes(c->d_slots, dh, ns * sizeof(Slot), c->st));
+    c->launches++;
     c->slots_on_dev = ns;
   }
   if (c->d_dbg) {
@@ -1157,6 +1158,7 @@ qfs_status run_sweep(qfs_ctx *c, const SweepSpec &sp, std::vector<double> &csum,
     CUDA_TRY(c, cudaHostGetDevicePointer((void **)&dflag, c->h_pubflag, 0));
     const unsigned long long seq = ++c->pub_seq;
     CUDA_TRY(c, launch_publish(c->d_csum, (int)nrb, with_check ? c->d_check : nullptr, dh, dchk, dflag, seq, c->st));
+    c->launches++;
     const qfs_status ws = wait_published(c, seq);
     if (ws != QFS_OK) return ws;
   }
@@ -1231,7 +1233,7 @@ qfs_status upload_gates(qfs_ctx *c, int s, const double *init) {
     c->check_fetched = false;
   }
   CUDA_TRY(c, launch_identity_fill(c->d_vprev, (long long)s * c->K, c->st));
-  c->launches++;
+  c->launches += 4;  // copy, flag fill, gate check, identity fill
   return QFS_OK;
 }
 
