@@ -412,6 +412,10 @@ def main():
                 # L2 read+write bandwidth at a 64 MiB working set (tools/peaks.cu)
                 "l2_rmw_peak_gbs": L2_RMW_64MIB_GBS if bound == "hbm" else None,
                 "frac_of_l2_rmw": round(achieved / L2_RMW_64MIB_GBS, 4) if bound == "hbm" else None,
+                "note": ("algorithmic bytes per launch exceed the kernel's DRAM bytes (traffic): part of "
+                         "its working set (chi) is L2-resident, so frac against HBM can reach 1; "
+                         "frac_of_l2_rmw is the L2-side figure (DESIGN.md section 5)")
+                if bound == "hbm" and traffic and traffic < pd["bytes"] / pd["launches"] else None,
                 "share_of_kernel_time": round(pd["ms"] / tot_ms, 4),
                 "profiled_ms_per_step": round(prof_step_ms, 4),
                 "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),

@@ -13,8 +13,11 @@ timeout 600 python bench.py > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.er
 summ() {
   python -c "import json,sys; d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); r=d['roofline']; print(sys.argv[2], round(d['value'],1), d['unit'], round(d['ms_per_step'],3), 'e2e', round(d['e2e']['value'],1), r['kernel'], 'frac', r['frac'], r['unit'], 'clocks', d['clocks'], 'tts', d['time_to_solution'])" "$1" "$2"
 }
+# short-sweep configs: 50 steps, so the per-call fixed cost (gate upload / download,
+# ~0.1-0.25 ms, tools/step_overhead.py) and timer noise stay small against the timed region
 for c in c2 c3 c5 c5b c5c; do
-  timeout 600 python bench.py --config $c --steps 10 --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
+  st=50; [ $c = c5 ] && st=10
+  timeout 600 python bench.py --config $c --steps $st --no-cpu-baseline > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
   summ gpurun_out/bench_$c.json $c || tail -3 gpurun_out/bench_$c.err
 done
 timeout 600 python bench.py --shard sample --steps 5 --no-cpu-baseline > gpurun_out/bench_c5_sample.json 2> gpurun_out/bench_c5_sample.err
