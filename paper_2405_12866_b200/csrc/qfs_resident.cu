@@ -407,18 +407,28 @@ struct ResSmem {
   double2 *chi;   // [2^n][ld]
 };
 
-__device__ ResSmem res_carve(unsigned char *base, int K, int n, int ld) {
+// (offsets from the __shared__ base, no integer casts: the compiler keeps the
+// shared state space and emits LDS/STS with 32-bit addresses, not generic
+// LD/ST with 64-bit ones)
+__device__ __forceinline__ ResSmem res_carve(unsigned char *base, int K, int n, int ld) {
   ResSmem m;
+  size_t off = 0;
   m.G = (double2 *)base;
-  m.red = (double *)(m.G + K * 16);
-  m.buf = m.red + RES_WARPS * 32;
-  m.cbuf = m.buf + (QFS_RES_PUSH ? 2 * 16 * 32 : 64);
-  m.scr = (double2 *)(m.cbuf + 2);
-  m.pr = (int2 *)(m.scr + 64);
-  m.kinds = (int *)(m.pr + K);
-  uintptr_t p = (uintptr_t)(m.kinds + K);
-  p = (p + 15) & ~(uintptr_t)15;
-  m.phi = (double2 *)p;
+  off += (size_t)K * 16 * sizeof(double2);
+  m.red = (double *)(base + off);
+  off += RES_WARPS * 32 * sizeof(double);
+  m.buf = (double *)(base + off);
+  off += (QFS_RES_PUSH ? 2 * 16 * 32 : 64) * sizeof(double);
+  m.cbuf = (double *)(base + off);
+  off += 2 * sizeof(double);
+  m.scr = (double2 *)(base + off);
+  off += 64 * sizeof(double2);
+  m.pr = (int2 *)(base + off);
+  off += (size_t)K * sizeof(int2);
+  m.kinds = (int *)(base + off);
+  off += (size_t)K * sizeof(int);
+  off = (off + 15) & ~(size_t)15;
+  m.phi = (double2 *)(base + off);
   m.chi = m.phi + ((size_t)ld << n);
   return m;
 }
@@ -450,6 +460,7 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
       t_prev = t;
     }
   };
+  stamp(-1);  // start of the launch
 
   for (int j = (int)cl_id(); j < P.n_slots; j += (int)cl_count()) {
     const Slot sl = P.slots[j];
@@ -639,8 +650,6 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
       }
     }
     stamp(7);  // [7] validation
-    if (dbg)
-      for (int q = 0; q < 8; ++q) atomicAdd(P.dbg + q, ph[q]);
     // costs: threads -> warps (in order) -> CTA -> cluster ranks (in order)
     train = warp_sum(train);
     val = warp_sum(val);
@@ -674,6 +683,8 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
     cl_arrive();
     cl_wait();
   }
+  if (dbg)  // once per launch: the sums over this cluster's slots
+    for (int q = 0; q < 8; ++q) atomicAdd(P.dbg + q, ph[q]);
   pdl_trigger();
 }
 
@@ -693,7 +704,7 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) val_blk_kernel(const ValRow
   const unsigned N = 1u << n;
   double2 *G = (double2 *)smem_raw;
   int2 *pr = (int2 *)(G + K * 16);
-  double2 *st = (double2 *)((((uintptr_t)(pr + K)) + 15) & ~(uintptr_t)15);
+  double2 *st = (double2 *)(smem_raw + (((size_t)K * (16 * sizeof(double2) + sizeof(int2)) + 15) & ~(size_t)15));
   const int j = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r0 = blockIdx.x * ld, nb = min(ld, P.rows - r0);
   for (unsigned q = tid; q < N * (unsigned)nb; q += RES_THREADS) {
@@ -774,7 +785,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1) val_cl_kernel(const ValRowPara
   const unsigned C = 1u << t, NH = 1u << (n - t), top = (unsigned)(n - t);
   double2 *G = (double2 *)smem_raw;
   int2 *pr = (int2 *)(G + K * 16);
-  double2 *st = (double2 *)((((uintptr_t)(pr + K)) + 15) & ~(uintptr_t)15);
+  double2 *st = (double2 *)(smem_raw + (((size_t)K * (16 * sizeof(double2) + sizeof(int2)) + 15) & ~(size_t)15));
   const unsigned rank = cl_rank();
   const int row = blockIdx.x >> t, j = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double2 *xr = P.xv + ((long long)row << n) + (long long)rank * NH;

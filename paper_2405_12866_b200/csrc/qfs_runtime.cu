@@ -2089,7 +2089,7 @@ void qfs_destroy(qfs_ctx *c) {
     unsigned long long h[8];
     cudaMemcpy(h, c->d_res_dbg, sizeof h, cudaMemcpyDeviceToHost);
     const char *nm[8] = {"load", "forward", "env", "reduce", "polar", "uncompute-wait", "chi", "validation"};
-    fprintf(stderr, "[qfs resident timing] cluster 0 rank 0, us per sweep (%lld sweeps; K=%d):", c->res_sweeps, c->K);
+    fprintf(stderr, "[qfs resident timing] cluster 0 rank 0, us per launch summed over its slots (%lld launches; K=%d):", c->res_sweeps, c->K);
     for (int q = 0; q < 8; ++q) fprintf(stderr, " %s %.2f", nm[q], h[q] / 1e3 / c->res_sweeps);
     fprintf(stderr, "\n");
   }
