@@ -440,7 +440,9 @@ def main():
 
     # two caller-owned host gate buffers, alternating as input and output (the
     # C ABI's out_gates): no fresh allocation per step
-    gbuf = [np.ascontiguousarray(g).copy(), np.empty_like(np.ascontiguousarray(g))]
+    # pinned (page-locked) like the sample buffers: libqfs reads / writes them in place
+    gbuf = [torch.from_numpy(np.ascontiguousarray(g)).pin_memory().numpy(),
+            torch.empty(tuple(np.shape(g)), dtype=torch.complex128, pin_memory=True).numpy()]
     for w in range(2):                   # untimed warm-up of the e2e path (staging buffers, graphs)
         queue_samples()
         ctx.instantiate(gbuf[w % 2], bench_params(1, m), out=gbuf[(w + 1) % 2])

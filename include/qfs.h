@@ -172,7 +172,9 @@ qfs_status qfs_set_samples(qfs_ctx *c, int m_pool, const double *x, const double
  * until the consuming call returns (pinned memory makes the copies overlap).
  * QFS_ERR_STATE when two sets are already queued; argument errors as
  * qfs_set_samples; a non-finite sample is reported (QFS_ERR_NUMERIC) by the
- * consuming call. */
+ * consuming call after its first sweep (the check rides on the initial-gate
+ * check's read-back, no extra host round trip; outputs are not written and
+ * the context has no samples until the next qfs_set_samples*). */
 qfs_status qfs_set_samples_async(qfs_ctx *c, int m_pool, const double *x, const double *y, int v,
                                  const double *xv, const double *yv);
 
@@ -200,7 +202,10 @@ qfs_status qfs_set_samples_device(qfs_ctx *c, int m_pool, const void *dx, const 
  * minimum c_train start (ties: lower index).  The initial gates are validated
  * on the device (finite; ||G^dag G - I||_max <= 1e-10; QFS_GATE_VAR1 slots of
  * the form u (x) I); a failure is reported as QFS_ERR_NUMERIC after the first
- * sweep, and then out_gates / out are not written. */
+ * sweep, and then out_gates / out are not written.  Page-locked (pinned,
+ * mapped) init_gates / out_gates buffers are read / written by the device in
+ * place; pageable ones go through the context's pinned staging buffer.  Both
+ * are owned by the caller and not retained after the call returns. */
 qfs_status qfs_instantiate(qfs_ctx *c, int s, const double *init_gates, const qfs_params *p,
                            double *out_gates, qfs_result *out, int *winner);
 

@@ -229,6 +229,7 @@ cudaError_t launch_identity_fill(double2 *v, long long count16, cudaStream_t st)
 cudaError_t launch_copy(double2 *dst, const double2 *src, long long count, cudaStream_t st);  // device copy by a kernel
 cudaError_t launch_copy_bytes(void *dst, const void *src, size_t bytes, cudaStream_t st);  // 4-byte granular
 cudaError_t launch_fill_words(unsigned *dst, unsigned value, long long count, cudaStream_t st);
+cudaError_t launch_flag_bit(const unsigned *src, unsigned *dst, unsigned bit, cudaStream_t st);
 // hdst / hcheck / hflag: device pointers of mapped pinned host memory
 cudaError_t launch_publish(const double *src, int count, const unsigned *check, double *hdst, unsigned *hcheck,
                            unsigned long long *hflag, unsigned long long seq, cudaStream_t st);
@@ -241,6 +242,10 @@ size_t res_smem_bytes(int n, int K, int ld);  // dynamic shared memory of the re
 size_t res_smem_limit(int minb);  // per-CTA limit when minb CTAs share an SM
 int resident_max_clusters(int C, size_t smem); // co-resident clusters of C CTAs (0: cannot launch)
 cudaError_t launch_resident(const ResParams &p, int clusters, cudaStream_t st);
+// two starts per cluster, one start's polar overlapped with the other's passes
+size_t res2_smem_bytes(int n, int K, int ld);
+int resident2_max_clusters(int C, size_t smem);
+cudaError_t launch_resident_pair(const ResParams &p, int clusters, cudaStream_t st);  // clusters: of start PAIRS
 size_t val_blk_smem(int n, int K, int ld);     // shared memory of the block validation kernel
 cudaError_t launch_val_block(const ValRowParams &p, int n_slots, cudaStream_t st);
 size_t val_cl_smem(int n, int K, int t);      // cluster validation, 2^t CTAs per row

@@ -1587,6 +1587,10 @@ __global__ void publish_kernel(const double *src, int count, const unsigned *che
   if (threadIdx.x == 0) st_release_sys(hflag, seq);
 }
 
+// *dst = (*src != 0) ? bit : 0 (one thread): a deferred check's flag moved
+// into the word read back after the first sweep
+__global__ void flag_bit_kernel(const unsigned *src, unsigned *dst, unsigned bit) { *dst = *src ? bit : 0u; }
+
 __global__ void fill_words_kernel(unsigned *dst, unsigned value, long long count) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
        i += (long long)gridDim.x * blockDim.x)
@@ -1980,6 +1984,11 @@ cudaError_t launch_copy_bytes(void *dst, const void *src, size_t bytes, cudaStre
 cudaError_t launch_publish(const double *src, int count, const unsigned *check, double *hdst, unsigned *hcheck,
                            unsigned long long *hflag, unsigned long long seq, cudaStream_t st) {
   publish_kernel<<<1, 256, 0, st>>>(src, count, check, hdst, hcheck, hflag, seq);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_flag_bit(const unsigned *src, unsigned *dst, unsigned bit, cudaStream_t st) {
+  flag_bit_kernel<<<1, 1, 0, st>>>(src, dst, bit);
   return cudaGetLastError();
 }
 

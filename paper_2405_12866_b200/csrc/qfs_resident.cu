@@ -58,6 +58,12 @@ constexpr int RES_ENV_UNROLL = QFS_RES_ENV_UNROLL;
 #ifndef QFS_RES_SPARE_SMSP
 #define QFS_RES_SPARE_SMSP 1  // resident: the uncompute beside the polar leaves warp 0's scheduler alone
 #endif
+#ifndef QFS_RES_MBAR
+// resident: the per-gate cluster exchange of E partials as st.async stores that
+// complete on the receiving CTA's mbarrier (only warp 0 waits), instead of a
+// cluster-wide barrier.arrive / wait of all threads
+#define QFS_RES_MBAR 1
+#endif
 #ifndef QFS_RES_ALIGN
 #define QFS_RES_ALIGN 128  // dynamic shared-memory alignment of the resident / validation kernels
 #endif
@@ -98,6 +104,16 @@ __device__ __forceinline__ void st_remote_d(double *p, unsigned rank, double v) 
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
   asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
 }
+// 8-byte store into CTA `rank`'s shared memory at the same offset, completing
+// `bytes` on that CTA's mbarrier (same offset) when it has landed
+__device__ __forceinline__ void st_async_remote_d(double *p, uint64_t *bar, unsigned rank, double v) {
+  unsigned ra, rb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(p)), "r"(rank));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(ra), "d"(v), "r"(rb)
+               : "memory");
+}
+
 __device__ __forceinline__ double ld_remote(const double *p, unsigned rank) {
   const unsigned a = (unsigned)__cvta_generic_to_shared(p);
   unsigned ra;
@@ -159,10 +175,24 @@ __device__ __forceinline__ double2 lds_c2(const double2 *p) {
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"((unsigned)__cvta_generic_to_shared(p)));
   return v;
 }
+#ifndef QFS_PAIR_GREG
+#define QFS_PAIR_GREG 3  // gate entries of the two-gate pass: 3 read once per item for all its quadruples (default), 0 re-read per use, 1 G1 in registers, 2 both (1, 2 spill)
+#endif
 template <int NU, int TP0, int TP1>
 __device__ void res_apply_pair_t(double2 *psi, const double2 *G1, const double2 *G2, const int (&loc)[4],
                                  const int (&srt)[4], int cnt, const FastDiv &fd, unsigned ld, int n, int t0, int nt) {
   constexpr int NV = 1 << NU, NQ = NV / 4;
+  double2 g1r[QFS_PAIR_GREG >= 1 ? 16 : 1], g2r[QFS_PAIR_GREG >= 2 ? 16 : 1];
+  if constexpr (QFS_PAIR_GREG >= 1) {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) g1r[e] = G1[e];
+  }
+  if constexpr (QFS_PAIR_GREG >= 2) {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) g2r[e] = G2[e];
+  }
+  auto ge1 = [&](int e) { if constexpr (QFS_PAIR_GREG >= 1) return g1r[e]; else return lds_c2(G1 + e); };
+  auto ge2 = [&](int e) { if constexpr (QFS_PAIR_GREG >= 2) return g2r[e]; else return lds_c2(G2 + e); };
   unsigned ob[NU];  // shared-memory offset of local bit t
 #pragma unroll
   for (int t = 0; t < NU; ++t) ob[t] = (1u << loc[t]) * ld;
@@ -183,30 +213,68 @@ __device__ void res_apply_pair_t(double2 *psi, const double2 *G1, const double2 
     double2 v[NV];
 #pragma unroll
     for (int u = 0; u < NV; ++u) v[u] = psi[b + offs(u)];
+    if constexpr (QFS_PAIR_GREG == 3) {
+      // each gate entry read once per item and applied to all NQ quadruples
+      // (same summation order per output as below: bit-identical)
+      double2 o[NQ][4];
 #pragma unroll
-    for (int qq = 0; qq < NQ; ++qq) {
-      double2 o[4];
+      for (int qq = 0; qq < NQ; ++qq)
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        o[a] = make_double2(0.0, 0.0);
+        for (int a = 0; a < 4; ++a) o[qq][a] = make_double2(0.0, 0.0);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) cfma(o[a], lds_c2(G1 + 4 * a + c), v[4 * qq + c]);
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double2 g = lds_c2(G1 + 4 * a + c);
+#pragma unroll
+          for (int qq = 0; qq < NQ; ++qq) cfma(o[qq][a], g, v[4 * qq + c]);
+        }
+#pragma unroll
+      for (int qq = 0; qq < NQ; ++qq)
+#pragma unroll
+        for (int a = 0; a < 4; ++a) v[4 * qq + a] = o[qq][a];
+#pragma unroll
+      for (int qq = 0; qq < NQ; ++qq)
+#pragma unroll
+        for (int a = 0; a < 4; ++a) o[qq][a] = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double2 g = lds_c2(G2 + 4 * a + c);
+#pragma unroll
+          for (int qq = 0; qq < NQ; ++qq) cfma(o[qq][a], g, v[pair_idx<NU, TP0, TP1>(qq, c)]);
+        }
+#pragma unroll
+      for (int qq = 0; qq < NQ; ++qq)
+#pragma unroll
+        for (int a = 0; a < 4; ++a) v[pair_idx<NU, TP0, TP1>(qq, a)] = o[qq][a];
+    } else {
+#pragma unroll
+      for (int qq = 0; qq < NQ; ++qq) {
+        double2 o[4];
+  #pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          o[a] = make_double2(0.0, 0.0);
+  #pragma unroll
+          for (int c = 0; c < 4; ++c) cfma(o[a], ge1(4 * a + c), v[4 * qq + c]);
+        }
+  #pragma unroll
+        for (int a = 0; a < 4; ++a) v[4 * qq + a] = o[a];
       }
-#pragma unroll
-      for (int a = 0; a < 4; ++a) v[4 * qq + a] = o[a];
-    }
-#pragma unroll
-    for (int qq = 0; qq < NQ; ++qq) {
-      double2 o[4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        o[a] = make_double2(0.0, 0.0);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) cfma(o[a], lds_c2(G2 + 4 * a + c), v[pair_idx<NU, TP0, TP1>(qq, c)]);
+  #pragma unroll
+      for (int qq = 0; qq < NQ; ++qq) {
+        double2 o[4];
+  #pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          o[a] = make_double2(0.0, 0.0);
+  #pragma unroll
+          for (int c = 0; c < 4; ++c) cfma(o[a], ge2(4 * a + c), v[pair_idx<NU, TP0, TP1>(qq, c)]);
+        }
+  #pragma unroll
+        for (int a = 0; a < 4; ++a) v[pair_idx<NU, TP0, TP1>(qq, a)] = o[a];
       }
-#pragma unroll
-      for (int a = 0; a < 4; ++a) v[pair_idx<NU, TP0, TP1>(qq, a)] = o[a];
-    }
+  }
 #pragma unroll
     for (int u = 0; u < NV; ++u) psi[b + offs(u)] = v[u];
   }
@@ -405,6 +473,7 @@ struct ResSmem {
   int *kinds;     // [K] gate kinds
   double2 *phi;   // [2^n][ld]
   double2 *chi;   // [2^n][ld]
+  uint64_t *mbar; // [2] per gate parity (QFS_RES_MBAR)
 };
 
 // (offsets from the __shared__ base, no integer casts: the compiler keeps the
@@ -427,6 +496,9 @@ __device__ __forceinline__ ResSmem res_carve(unsigned char *base, int K, int n, 
   off += (size_t)K * sizeof(int2);
   m.kinds = (int *)(base + off);
   off += (size_t)K * sizeof(int);
+  off = (off + 7) & ~(size_t)7;
+  m.mbar = (uint64_t *)(base + off);
+  off += 2 * sizeof(uint64_t);
   off = (off + 15) & ~(size_t)15;
   m.phi = (double2 *)(base + off);
   m.chi = m.phi + ((size_t)ld << n);
@@ -445,11 +517,21 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned rank = cl_rank(), C = cl_size();
 
+  if (QFS_RES_MBAR && tid == 0) {
+    mbar_init(sm.mbar, 1);
+    mbar_init(sm.mbar + 1, 1);
+    mbar_fence_init();
+  }
   pdl_wait();
   for (int k = tid; k < K; k += RES_THREADS) {
     sm.pr[k] = P.pairs[k];
     sm.kinds[k] = P.kinds ? P.kinds[k] : 0;
   }
+  if (QFS_RES_MBAR) {  // every CTA's mbarriers initialised before any CTA pushes to them
+    cl_arrive();
+    cl_wait();
+  }
+  unsigned mph = 0;  // warp 0: phase parity of mbar[g] in bit g
   // diagnostics: phase times of cluster 0, rank 0 (thread 0), summed over gates
   const bool dbg = P.dbg && cl_id() == 0 && rank == 0 && tid == 0;
   unsigned long long t_prev = 0, ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -506,7 +588,21 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
       if (!FUSE) res_env(sm.phi, sm.chi, sm.pr[i], cnt, fd, ld, n, sm.red);
       __syncthreads();
       stamp(2);  // [2] environment pass
-#if QFS_RES_PUSH
+#if QFS_RES_MBAR
+      if (warp == 0) {
+        // push this CTA's partial into slot [rank] of every cluster CTA's
+        // buffer; the stores complete C*256 bytes on each receiver's mbar[par]
+        double e = 0.0;
+#pragma unroll
+        for (int w = 0; w < RES_WARPS; ++w) e += sm.red[w * 32 + lane];
+        if (lane == 0) mbar_arrive_tx(sm.mbar + par, C * 32 * (unsigned)sizeof(double));
+        __syncwarp();
+        for (unsigned c = 0; c < C; ++c) st_async_remote_d(sm.buf + par * 512 + rank * 32 + lane, sm.mbar + par, c, e);
+        mbar_wait(sm.mbar + par, (mph >> par) & 1u);
+        mph ^= 1u << par;
+        e = 0.0;
+        for (unsigned c = 0; c < C; ++c) e += sm.buf[par * 512 + c * 32 + lane];  // rank order
+#elif QFS_RES_PUSH
       // push this CTA's partial into slot [rank] of every cluster CTA's buffer
       // (remote stores overlap the barrier); after it, all partials are local
       if (warp == 0) {
@@ -567,7 +663,9 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
 #else
         if (i > 0) res_apply(sm.phi, sm.G + 16 * (i - 1), sm.pr[i - 1], true, cnt, fd, ld, n, tid - 32, RES_THREADS - 32);
 #endif
+#if !QFS_RES_MBAR
         cl_wait();
+#endif
       }
       __syncthreads();
       stamp(5);  // [5] wait for the uncompute warps
@@ -685,6 +783,346 @@ __global__ void __launch_bounds__(RES_THREADS, MINB) res_sweep_kernel(const ResP
   }
   if (dbg)  // once per launch: the sums over this cluster's slots
     for (int q = 0; q < 8; ++q) atomicAdd(P.dbg + q, ph[q]);
+  pdl_trigger();
+}
+
+// ---------------------------------------------------------------------------
+// Two starts per cluster, staggered (the default resident kernel when a
+// cluster can hold two starts' states; QFS_RES_PAIR).  The per-gate chain of
+// one start — E_i partials -> cluster sum -> polar -> chi <- G_i^dag chi ->
+// E_{i-1} partials — is serial (the gates are updated one after the
+// other, each from the environment of the already-updated ones to its left of
+// chi), and its polar / cluster-sum part leaves the FP64 pipe idle.  Here each
+// CTA holds its slice of TWO starts A and B and overlaps one start's polar
+// with the other start's FP64 passes:
+//   warp 0 (PW_A): sums A's CTA partials, pushes them to every CTA of the
+//                  cluster (st.async over DSMEM completing on an mbarrier),
+//                  waits for the C partials, sums them in rank order, polar
+//                  update of A's gate;
+//   warp 4 (PW_B): the same for B (warps 0 and 4 share SMSP 0, so the FP64
+//                  passes keep two warps on each of the other three);
+//   warps 1-3, 5-7 (CW): every FP64 pass of both starts, in the order
+//     ... chi_A(i), E_A(i-1) | chi_B(i), E_B(i-1) | phi_A, phi_B <- G(i-2)^dag .. | wait G_A(i-1) ...
+//   so B's passes run while A's polar does, and the other way round.
+// Named barriers order the roles: ENV_X (CW arrive, PW_X sync: partials of
+// E_i written), GATE_X (PW_X arrive, CW sync: new G_i in the gate table), CW
+// (the six pass warps among themselves).  Forward, validation and the costs
+// run on all eight warps before / after the backward loop, per start.  Every
+// reduction keeps a fixed order (warps in order, then cluster ranks in order),
+// so results are deterministic for a given cluster size.
+constexpr int PW_A = 0, PW_B = 4;
+constexpr int CW_THREADS = RES_THREADS - 64;
+constexpr int CW_WARPS = CW_THREADS / 32;
+enum { NB_CW = 1, NB_ENV_A = 2, NB_ENV_B = 3, NB_GATE_A = 4, NB_GATE_B = 5 };
+__device__ __forceinline__ void nb_sync(int id, int cnt) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory"); }
+__device__ __forceinline__ void nb_arrive(int id, int cnt) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(cnt) : "memory");
+}
+// E partial over the items t0, t0 + nt, ... (res_env with a thread subset);
+// the warp writes its 32 reduced doubles to red_row[lane]
+__device__ void res_env_sub(const double2 *phi, const double2 *chi, int2 pq, int cnt, const FastDiv &fd, unsigned ld,
+                            int n, int t0, int nt, double *red_row) {
+  const int lane = threadIdx.x & 31;
+  double acc[32];
+#pragma unroll
+  for (int e = 0; e < 32; ++e) acc[e] = 0.0;
+  if (cnt > 0) {
+    const int lo = min(pq.x, pq.y), hi = max(pq.x, pq.y);
+    const unsigned o1 = (1u << pq.x) * ld, o2 = (1u << pq.y) * ld;
+    const unsigned items = (1u << (n - 2)) * (unsigned)cnt;
+#pragma unroll RES_ENV_UNROLL
+    for (unsigned q = (unsigned)t0; q < items; q += (unsigned)nt) {
+      const unsigned r = fd.div(q);
+      const unsigned b = insert_zero32(insert_zero32(r, lo), hi) * ld + (q - r * (unsigned)cnt);
+      const double2 f[4] = {phi[b], phi[b + o1], phi[b + o2], phi[b + o1 + o2]};
+      const double2 c[4] = {chi[b], chi[b + o1], chi[b + o2], chi[b + o1 + o2]};
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {  // f[a] * conj(c[k])
+          double &re = acc[2 * (4 * a + k)], &im = acc[2 * (4 * a + k) + 1];
+          re = fma(f[a].x, c[k].x, re);
+          re = fma(f[a].y, c[k].y, re);
+          im = fma(f[a].y, c[k].x, im);
+          im = fma(-f[a].x, c[k].y, im);
+        }
+    }
+  }
+  red_row[lane] = warp_reduce_scatter32(acc, lane);
+}
+
+// chi' = G_0^dag chi and this thread's share of c_train = sum ||chi' - x||^2
+// over the items t0, t0 + nt, ...
+__device__ double res_chi0_cost(const double2 *chi, const double2 *G, int2 pq, int cnt, const FastDiv &fd, unsigned ld,
+                                int n, const double2 *x, long long m_pool, int m0, int t0, int nt) {
+  double train = 0.0;
+  if (cnt <= 0) return train;
+  double2 g[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) g[e] = cconj(G[4 * (e & 3) + (e >> 2)]);
+  const int lo = min(pq.x, pq.y), hi = max(pq.x, pq.y);
+  const unsigned o[4] = {0u, (1u << pq.x), (1u << pq.y), (1u << pq.x) | (1u << pq.y)};
+  const unsigned items = (1u << (n - 2)) * (unsigned)cnt;
+  for (unsigned q = (unsigned)t0; q < items; q += (unsigned)nt) {
+    const unsigned r = fd.div(q), jj = q - r * (unsigned)cnt;
+    const unsigned base = insert_zero32(insert_zero32(r, lo), hi);
+    double2 v[4];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) v[l] = chi[(base | o[l]) * ld + jj];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      double2 rr = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) cfma(rr, g[4 * a + k], v[k]);
+      const double2 xv = __ldg(x + (long long)(base | o[a]) * m_pool + m0 + jj);
+      const double dr = rr.x - xv.x, di = rr.y - xv.y;
+      train = fma(dr, dr, train);
+      train = fma(di, di, train);
+    }
+  }
+  return train;
+}
+
+struct Res2Start {  // one start's view inside the CTA
+  double2 *G, *phi, *chi, *scr;
+  double *red, *buf;  // [CW_WARPS][32] pass partials; [2][16][32] cluster partials (by rank)
+  uint64_t *mbar;     // [2] (gate parity)
+  double2 *gglob;
+  int j, s, M, cnt, m0;
+};
+
+size_t res2_fixed_bytes(int K) {
+  size_t b = 2 * (size_t)K * 16 * sizeof(double2)            // gate tables
+             + 2 * (CW_WARPS * 32 + 2 * 16 * 32) * sizeof(double)  // red, buf
+             + 40 * sizeof(double)                           // cost reduction
+             + 4 * sizeof(uint64_t)                          // mbarriers
+             + 2 * 64 * sizeof(double2)                      // polar scratch
+             + (size_t)K * (sizeof(int2) + sizeof(int));
+  return (b + 15) & ~(size_t)15;
+}
+
+__global__ void __launch_bounds__(RES_THREADS, 1) res_pair_kernel(const ResParams P) {
+  extern __shared__ __align__(QFS_RES_ALIGN) unsigned char smem_raw[];
+  const int K = P.K, n = P.n;
+  const unsigned N = 1u << n, ld = (unsigned)P.ld;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned rank = cl_rank(), C = cl_size();
+  // carve (offsets from the __shared__ base: LDS/STS addressing)
+  size_t off = 0;
+  double2 *Gt[2];
+  Gt[0] = (double2 *)(smem_raw + off); off += (size_t)K * 16 * sizeof(double2);
+  Gt[1] = (double2 *)(smem_raw + off); off += (size_t)K * 16 * sizeof(double2);
+  double *redt[2], *buft[2];
+  redt[0] = (double *)(smem_raw + off); off += CW_WARPS * 32 * sizeof(double);
+  redt[1] = (double *)(smem_raw + off); off += CW_WARPS * 32 * sizeof(double);
+  buft[0] = (double *)(smem_raw + off); off += 2 * 16 * 32 * sizeof(double);
+  buft[1] = (double *)(smem_raw + off); off += 2 * 16 * 32 * sizeof(double);
+  double *cred = (double *)(smem_raw + off); off += 40 * sizeof(double);
+  uint64_t *mbar = (uint64_t *)(smem_raw + off); off += 4 * sizeof(uint64_t);
+  double2 *scrt[2];
+  scrt[0] = (double2 *)(smem_raw + off); off += 64 * sizeof(double2);
+  scrt[1] = (double2 *)(smem_raw + off); off += 64 * sizeof(double2);
+  int2 *pr = (int2 *)(smem_raw + off); off += (size_t)K * sizeof(int2);
+  int *kinds = (int *)(smem_raw + off); off += (size_t)K * sizeof(int);
+  off = (off + 15) & ~(size_t)15;
+  double2 *st0 = (double2 *)(smem_raw + off);
+  const size_t SZ = (size_t)ld << n;  // one [2^n][ld] state block
+
+  if (tid == 0) {
+    for (int q = 0; q < 4; ++q) mbar_init(mbar + q, 1);
+    mbar_fence_init();
+  }
+  pdl_wait();
+  for (int k = tid; k < K; k += RES_THREADS) {
+    pr[k] = P.pairs[k];
+    kinds[k] = P.kinds ? P.kinds[k] : 0;
+  }
+  cl_arrive();  // the mbarriers are initialised before any CTA of the cluster pushes to them
+  cl_wait();
+  unsigned mph = 0;  // PW: parity bits of the two mbarriers of its start (bit g: gate parity g)
+
+  const int n_pairs = (P.n_slots + 1) / 2;
+  for (int pj = (int)cl_id(); pj < n_pairs; pj += (int)cl_count()) {
+    Res2Start S[2];
+    const bool hasB = 2 * pj + 1 < P.n_slots;
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      Res2Start &t = S[x];
+      t.j = 2 * pj + x;
+      const bool present = x == 0 || hasB;
+      const Slot sl = present ? P.slots[t.j] : Slot{};
+      t.s = present ? sl.s : 0;
+      t.M = present ? sl.m : 0;
+      t.m0 = (int)rank * (int)ld;
+      t.cnt = max(0, min((int)ld, t.M - t.m0));
+      t.G = Gt[x]; t.red = redt[x]; t.buf = buft[x]; t.scr = scrt[x]; t.mbar = mbar + 2 * x;
+      t.phi = st0 + (2 * x) * SZ;
+      t.chi = st0 + (2 * x + 1) * SZ;
+      t.gglob = P.gates + (long long)t.s * K * 16;
+    }
+    const FastDiv fdA((unsigned)max(S[0].cnt, 1)), fdB((unsigned)max(S[1].cnt, 1));
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {  // (unrolled: S[] stays in registers)
+      if (x == 1 && !hasB) continue;
+      for (int q = tid; q < K * 16; q += RES_THREADS) S[x].G[q] = S[x].gglob[q];
+      for (unsigned q = tid; q < N * (unsigned)S[x].cnt; q += RES_THREADS) {
+        const unsigned a = q / (unsigned)S[x].cnt, jj = q - a * (unsigned)S[x].cnt;
+        const long long gi = (long long)a * P.m_pool + S[x].m0 + jj;
+        S[x].phi[a * ld + jj] = __ldg(P.x + gi);
+        S[x].chi[a * ld + jj] = __ldg(P.y + gi);
+      }
+    }
+    __syncthreads();
+    // forward with the previous sweep's gates, both starts: phi = B_{K-1}
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      if (x == 1 && !hasB) continue;
+      const FastDiv &fd = x ? fdB : fdA;
+      int k = 0;
+      for (; k + 2 < K; k += 2) {
+        res_apply_pair(S[x].phi, S[x].G + 16 * k, pr[k], S[x].G + 16 * (k + 1), pr[k + 1], S[x].cnt, fd, ld, n, tid,
+                       RES_THREADS);
+        __syncthreads();
+      }
+      if (k + 1 < K) {
+        res_apply(S[x].phi, S[x].G + 16 * k, pr[k], false, S[x].cnt, fd, ld, n, tid, RES_THREADS);
+        __syncthreads();
+      }
+    }
+    // ---- backward, right to left, roles as above ----
+    double train[2] = {0.0, 0.0};
+    if (warp == PW_A || warp == PW_B) {
+      auto pw_run = [&](Res2Start &t, const int ENV, const int GATE) {
+        for (int i = K - 1; i >= 0; --i) {
+          const int par = i & 1;
+          nb_sync(ENV, CW_THREADS + 32);  // the pass warps' partials of E_i are in t.red
+          double e = 0.0;
+#pragma unroll
+          for (int w = 0; w < CW_WARPS; ++w) e += t.red[w * 32 + lane];
+          if (lane == 0) mbar_arrive_tx(t.mbar + par, C * 32 * (unsigned)sizeof(double));
+          __syncwarp();
+          for (unsigned c = 0; c < C; ++c) st_async_remote_d(t.buf + par * 512 + rank * 32 + lane, t.mbar + par, c, e);
+          mbar_wait(t.mbar + par, (mph >> par) & 1u);
+          mph ^= 1u << par;
+          e = 0.0;
+          for (unsigned c = 0; c < C; ++c) e += t.buf[par * 512 + c * 32 + lane];  // rank order
+          const int l = lane & 15;
+          double2 ev = make_double2(__shfl_sync(FULL, e, 2 * l), __shfl_sync(FULL, e, 2 * l + 1));
+          double2 *gi = t.G + 16 * i;
+          if (P.env_trace && rank == 0 && lane < 16) P.env_trace[((long long)i * P.S + t.s) * 16 + l] = ev;
+          const int kind = kinds[i];
+          double2 g, v;
+          double ss;
+          gate_update(kind, ev, gi, P.beta, nullptr, g, v, ss, t.scr + 2 * (lane & 16), P.sig != nullptr);
+          __syncwarp();
+          if (lane < 16 && kind != 1) gi[l] = g;
+          if (rank == 0) {
+            if (lane < 16 && kind != 1) t.gglob[16 * i + l] = g;
+            if (lane == 0 && P.sig) P.sig[(long long)t.s * K + i] = ss;
+          }
+          nb_arrive(GATE, CW_THREADS + 32);  // new G_i in the gate table
+        }
+      };
+      if (warp == PW_A) pw_run(S[0], NB_ENV_A, NB_GATE_A);
+      else if (hasB) pw_run(S[1], NB_ENV_B, NB_GATE_B);
+    } else {
+      const int ct = tid - 32 - (warp > PW_B ? 32 : 0);  // 0 .. CW_THREADS-1
+      const int cw = ct >> 5;
+      auto env = [&](int x, int i) {
+        res_env_sub(S[x].phi, S[x].chi, pr[i], S[x].cnt, x ? fdB : fdA, ld, n, ct, CW_THREADS, S[x].red + cw * 32);
+        nb_arrive(x ? NB_ENV_B : NB_ENV_A, CW_THREADS + 32);
+      };
+      env(0, K - 1);
+      if (hasB) env(1, K - 1);
+      for (int i = K - 1; i >= 0; --i) {
+        nb_sync(NB_CW, CW_THREADS);  // E_i passes of both starts done reading phi / chi
+        if (i > 0) {  // uncompute B_{i-1} = G_{i-1}^dag B_i with the old G_{i-1}
+          res_apply(S[0].phi, S[0].G + 16 * (i - 1), pr[i - 1], true, S[0].cnt, fdA, ld, n, ct, CW_THREADS);
+          if (hasB) res_apply(S[1].phi, S[1].G + 16 * (i - 1), pr[i - 1], true, S[1].cnt, fdB, ld, n, ct, CW_THREADS);
+        }
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+          if (x == 1 && !hasB) continue;
+          nb_sync(x ? NB_GATE_B : NB_GATE_A, CW_THREADS + 32);  // new G_i of start x
+          if (i > 0)
+            res_apply(S[x].chi, S[x].G + 16 * i, pr[i], true, S[x].cnt, x ? fdB : fdA, ld, n, ct, CW_THREADS);
+          else
+            train[x] = res_chi0_cost(S[x].chi, S[x].G, pr[0], S[x].cnt, x ? fdB : fdA, ld, n, P.x, P.m_pool,
+                                     S[x].m0, ct, CW_THREADS);
+          nb_sync(NB_CW, CW_THREADS);  // chi_x(i) and phi_x(i-1) complete
+          if (i > 0) env(x, i - 1);
+        }
+      }
+    }
+    __syncthreads();
+    // validation cost with the post-sweep gates, per start:
+    // this CTA's rows v = rank, rank + C, ... in batches of ld rows (phi buffer)
+    double val[2] = {0.0, 0.0};
+    if (P.want_val && P.V > 0) {
+      const int rows = (P.V - (int)rank + (int)C - 1) / (int)C;
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        if (x == 1 && !hasB) continue;
+        for (int b0 = 0; b0 < rows; b0 += (int)ld) {
+          const int nb = min((int)ld, rows - b0);
+          for (unsigned q = tid; q < N * (unsigned)nb; q += RES_THREADS) {
+            const unsigned jj = q / N, a = q - jj * N;
+            const long long row = (long long)rank + (long long)C * (b0 + jj);
+            S[x].phi[a * ld + jj] = __ldg(P.xv + row * N + a);
+          }
+          __syncthreads();
+          const FastDiv fdv((unsigned)nb);
+          int k = 0;
+          for (; k + 1 < K; k += 2) {
+            res_apply_pair(S[x].phi, S[x].G + 16 * k, pr[k], S[x].G + 16 * (k + 1), pr[k + 1], nb, fdv, ld, n, tid,
+                           RES_THREADS);
+            __syncthreads();
+          }
+          if (k < K) {
+            res_apply(S[x].phi, S[x].G + 16 * k, pr[k], false, nb, fdv, ld, n, tid, RES_THREADS);
+            __syncthreads();
+          }
+          for (unsigned q = tid; q < N * (unsigned)nb; q += RES_THREADS) {
+            const unsigned jj = q / N, a = q - jj * N;
+            const long long row = (long long)rank + (long long)C * (b0 + jj);
+            const double2 u = S[x].phi[a * ld + jj], w = __ldg(P.yv + row * N + a);
+            const double dr = u.x - w.x, di = u.y - w.y;
+            val[x] = fma(dr, dr, val[x]);
+            val[x] = fma(di, di, val[x]);
+          }
+          __syncthreads();
+        }
+      }
+    }
+    // costs: threads -> warps (in order) -> CTA -> cluster ranks (in order)
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      const double t = warp_sum(train[x]), v = warp_sum(val[x]);
+      if (lane == 0) {
+        cred[(2 * x) * RES_WARPS + warp] = t;
+        cred[(2 * x + 1) * RES_WARPS + warp] = v;
+      }
+    }
+    __syncthreads();
+    if (tid < 4) {  // cost (tid & 1: validation) of start tid >> 1
+      double a = 0.0;
+      for (int w = 0; w < RES_WARPS; ++w) a += cred[tid * RES_WARPS + w];
+      cred[32 + tid] = a;
+    }
+    cl_arrive();
+    cl_wait();
+    if (rank == 0 && tid < (hasB ? 4 : 2)) {
+      const int j = 2 * pj + (tid >> 1);
+      double a = 0.0;
+      for (unsigned c = 0; c < C; ++c) a += ld_remote(cred + 32 + tid, c);
+      if ((tid & 1) == 0) P.csum[j] = a;
+      else if (P.want_val && P.V > 0) P.cval[j] = a;
+    }
+    // the next pair rewrites the gate tables and cred: every CTA waits until
+    // rank 0 has read the remote costs
+    cl_arrive();
+    cl_wait();
+  }
   pdl_trigger();
 }
 
@@ -946,7 +1384,7 @@ size_t res_smem_bytes(int n, int K, int ld) {
   size_t b = (size_t)K * 16 * sizeof(double2) + (RES_WARPS * 32 + (QFS_RES_PUSH ? 2 * 16 * 32 : 64) + 2) * sizeof(double) +
              64 * sizeof(double2) + (size_t)K * (sizeof(int2) + sizeof(int));
   b = (b + 15) & ~(size_t)15;
-  b += 2 * ((size_t)ld << n) * sizeof(double2);
+  b += 2 * ((size_t)ld << n) * sizeof(double2) + 32;  // (+ mbarriers and their alignment)
   return b;
 }
 int resident_max_clusters_query(int C, size_t smem);
@@ -1004,6 +1442,61 @@ int resident_max_clusters_query(int C, size_t smem) {
     return 0;
   }
   return num;
+}
+
+size_t res2_smem_bytes(int n, int K, int ld) { return res2_fixed_bytes(K) + 4 * ((size_t)ld << n) * sizeof(double2); }
+
+int resident2_max_clusters(int C, size_t smem) {
+  static std::map<std::pair<int, size_t>, int> cache;
+  static std::mutex mu;
+  const auto key = std::make_pair(C, smem);
+  std::lock_guard<std::mutex> lock(mu);
+  const auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(res_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RES_SMEM_MAX);
+    cudaFuncSetAttribute(res_pair_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C * 148);
+  cfg.blockDim = dim3(RES_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute a[1];
+  a[0].id = cudaLaunchAttributeClusterDimension;
+  a[0].val.clusterDim.x = C;
+  a[0].val.clusterDim.y = 1;
+  a[0].val.clusterDim.z = 1;
+  cfg.attrs = a;
+  cfg.numAttrs = 1;
+  int num = 0;
+  if (cudaOccupancyMaxActiveClusters(&num, res_pair_kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    num = 0;
+  }
+  cache[key] = num;
+  return num;
+}
+
+cudaError_t launch_resident_pair(const ResParams &p, int clusters, cudaStream_t st) {
+  const size_t smem = res2_smem_bytes(p.n, p.K, p.ld);
+  resident2_max_clusters(p.C, smem);  // sets the function attributes
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.C * clusters);
+  cfg.blockDim = dim3(RES_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute a[2];
+  a[0].id = cudaLaunchAttributeClusterDimension;
+  a[0].val.clusterDim.x = p.C;
+  a[0].val.clusterDim.y = 1;
+  a[0].val.clusterDim.z = 1;
+  a[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = a;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, res_pair_kernel, p);
 }
 
 cudaError_t launch_resident(const ResParams &p, int clusters, cudaStream_t st) {

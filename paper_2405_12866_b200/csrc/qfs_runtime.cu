@@ -111,6 +111,8 @@ struct qfs_ctx {
   bool val_block = true;    // QFS_VAL_BLOCK=0: one-row-per-CTA validation kernel
   int res_per_sm = 1;       // QFS_RES_PER_SM: resident CTAs per SM the cluster plan targets
   int res_cmax = 16;        // QFS_RES_CMAX: largest cluster the plan widens to
+  bool sample_check_pending = false;  // a consumed queued sample set's finite check, read back after the first sweep
+  int res_pair = 0;         // QFS_RES_PAIR: two starts per cluster, staggered (0 off (default: measured slower), 1 auto, 2 wherever it fits)
   int path = 0;             // 0 auto, 1 streamed (B cache in HBM), 2 cluster-resident (qfs_set_path / QFS_PATH)
   size_t stage_bytes = 0;
   // qfs_set_samples_async: up to two sample sets queued in device staging
@@ -620,6 +622,7 @@ Scatter make_scatter(const Lay &src, const int *lloc, int nl, const Lay &dst, in
 struct ResPlan {
   int C = 0, ld = 0, clusters = 0;
   size_t smem = 0;
+  bool pair = false;  // res_pair_kernel: clusters of start pairs
 };
 bool res_plan(const qfs_ctx *c, int M_max, int ns, ResPlan &pl) {
   if (c->path == 1 || (c->mode == 1 && c->world > 1) || c->force_unfused || c->x_basis || c->n > 13 || M_max < 1)
@@ -627,6 +630,30 @@ bool res_plan(const qfs_ctx *c, int M_max, int ns, ResPlan &pl) {
   // auto: resident only up to n = 10 — measured crossover (profiles/r1_sweep_map.jsonl:
   // n <= 10 resident 1.3-1.9x faster, n = 11 / 12 streamed 1.14x / 1.40x faster)
   if (c->path == 0 && c->n > 10) return false;
+  // two starts per cluster (res_pair_kernel, one start's polar overlapped with
+  // the other's passes) when there are at least two starts with enough work
+  // per start for the passes to matter (auto: M 2^n >= 2^12); the smallest
+  // power-of-two cluster that holds both starts' slices, widened like below
+  if (c->res_pair && ns >= 2 && (c->res_pair == 2 || (((long long)M_max << c->n) >= 4096 && !c->d_res_dbg))) {
+    int C2 = 1;
+    for (; C2 <= 16; C2 *= 2)
+      if (res2_smem_bytes(c->n, c->K, (M_max + C2 - 1) / C2) <= res_smem_limit(1)) break;
+    if (C2 <= 16) {
+      const int np = (ns + 1) / 2;
+      while (C2 < c->res_cmax && (long long)np * 2 * C2 <= 148LL && (M_max + 2 * C2 - 1) / (2 * C2) >= 2) C2 *= 2;
+      const int ld2 = (M_max + C2 - 1) / C2;
+      const size_t sm2 = res2_smem_bytes(c->n, c->K, ld2);
+      const int mx2 = resident2_max_clusters(C2, sm2);
+      if (mx2 >= 1) {
+        pl.pair = true;
+        pl.C = C2;
+        pl.ld = ld2;
+        pl.smem = sm2;
+        pl.clusters = std::min(np, mx2);
+        return true;
+      }
+    }
+  }
   // one CTA per SM (QFS_RES_PER_SM=2: two, <= 113 KB and <= 128 registers
   // each — measured slower: the per-gate chain is latency-bound, not
   // throughput-bound); then widen the cluster while the CTAs of all starts
@@ -767,7 +794,7 @@ qfs_status issue_group(qfs_ctx *c, const SweepSpec &sp, int j0, int j1, cudaStre
     // the uncompute's extra 32 and the fused validation are not counted)
     (void)vunits;
     LaunchScope ls(c, K_RES, 0.0, units * 96.0 * K);
-    CUDA_TRY(c, launch_resident(r, pl.clusters, st));
+    CUDA_TRY(c, pl.pair ? launch_resident_pair(r, pl.clusters, st) : launch_resident(r, pl.clusters, st));
     return QFS_OK;
   }
   if (c->path == 2) return fail(c, QFS_ERR_CAPACITY, "resident path requested but the state does not fit");
@@ -1198,6 +1225,10 @@ qfs_status gate_check_result(qfs_ctx *c) {
   }
   c->check_fetched = false;
   const unsigned bad = *c->h_check;
+  if (bad & 16u) {
+    c->have_samples = false;
+    return fail(c, QFS_ERR_NUMERIC, "non-finite sample");
+  }
   if (bad & 1u) return fail(c, QFS_ERR_NUMERIC, "non-finite initial gate");
   if (bad & 2u) return fail(c, QFS_ERR_NUMERIC, "initial gate not unitary (tol 1e-10)");
   if (bad & 4u) return fail(c, QFS_ERR_NUMERIC, "one-qubit gate slot is not of the form u (x) I (tol 1e-10)");
@@ -1205,11 +1236,29 @@ qfs_status gate_check_result(qfs_ctx *c) {
   return QFS_OK;
 }
 
+// Device address of a page-locked, mapped host buffer (cudaHostAlloc /
+// cudaHostRegister memory, e.g. torch pin_memory(); under unified addressing
+// every such buffer is mapped), or nullptr for pageable memory.
+const void *pinned_device_ptr(const void *host) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, host) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
 qfs_status upload_gates(qfs_ctx *c, int s, const double *init) {
   if (!c->h_check) {
     CUDA_TRY(c, cudaHostAlloc((void **)&c->h_check, sizeof(unsigned), cudaHostAllocMapped));
   }
   const size_t gb = (size_t)s * c->gsz * sizeof(double2);
+  // a pinned caller buffer is read by the copy kernel in place (no host memcpy
+  // into the context's staging buffer; the call is synchronous, so the buffer
+  // is not reused before the kernel has read it)
+  if (const void *dp = pinned_device_ptr(init)) {
+    CUDA_TRY(c, launch_copy(c->d_gates, (const double2 *)dp, (long long)s * c->gsz, c->st));
+  } else {
   if (gb > c->h_gates_cap) {
     if (c->h_gates) cudaFreeHost(c->h_gates);
     c->h_gates = nullptr;
@@ -1223,10 +1272,15 @@ qfs_status upload_gates(qfs_ctx *c, int s, const double *init) {
   double2 *dh = nullptr;
   CUDA_TRY(c, cudaHostGetDevicePointer((void **)&dh, c->h_gates, 0));
   CUDA_TRY(c, launch_copy(c->d_gates, dh, (long long)s * c->gsz, c->st));
+  }
   {
     // device-side flag, read back (device -> host, 4 bytes) after the first sweep
     if (!c->d_check) CUDA_TRY(c, cudaMalloc(&c->d_check, sizeof(unsigned)));
-    CUDA_TRY(c, launch_fill_words(c->d_check, 0u, 1, c->st));
+    if (c->sample_check_pending)  // the queued sample set's finite check (set_samples_impl, deferred) as bit 4
+      CUDA_TRY(c, launch_flag_bit((const unsigned *)c->d_flag, c->d_check, 16u, c->st));
+    else
+      CUDA_TRY(c, launch_fill_words(c->d_check, 0u, 1, c->st));
+    c->sample_check_pending = false;
     if (c->blocks) CUDA_TRY(c, launch_blk_gate_check(c->d_gates, c->d_bg, c->K, c->gsz, s, c->d_check, c->st));
     else CUDA_TRY(c, launch_gate_check(c->d_gates, (long long)s * c->K, c->K, c->d_kinds, c->d_check, c->st));
     c->check_pending = true;
@@ -1308,6 +1362,7 @@ qfs_status create_common(int n, int k, const int32_t *pairs, int device, qfs_ctx
   if (const char *vb = getenv("QFS_VAL_BLOCK")) c->val_block = atoi(vb) != 0;
   if (const char *rc = getenv("QFS_RES_CMAX")) c->res_cmax = std::max(1, std::min(16, atoi(rc)));
   if (const char *rp = getenv("QFS_RES_PER_SM")) c->res_per_sm = atoi(rp) == 2 ? 2 : 1;
+  if (const char *rq = getenv("QFS_RES_PAIR")) c->res_pair = std::max(0, std::min(2, atoi(rq)));
   if (const char *uf = getenv("QFS_UNFUSED_POLAR")) c->force_unfused = atoi(uf) != 0;
   if (const char *cd = getenv("QFS_COPY_DEFER")) c->copy_defer = atoi(cd) != 0;
   if (const char *pb = getenv("QFS_PUBLISH")) c->pub_off = atoi(pb) == 0;
@@ -1450,7 +1505,7 @@ qfs_status qfs_create_nccl(int n, int k, const int32_t *pairs, int device, const
 
 static qfs_status set_samples_impl(qfs_ctx *c, int m_pool, const void *x, const void *y, int v,
                                    const void *xv, const void *yv, cudaMemcpyKind kind,
-                                   cudaStream_t ust) {
+                                   cudaStream_t ust, bool defer_check = false) {
   if (!c) return QFS_ERR_ARG;
   const bool basis = x == nullptr;  // qfs_set_samples_basis: x_m = e_m (computational basis), not stored
   if (m_pool < 1 || !y || v < 0 || (v > 0 && (!xv || !yv)))
@@ -1530,8 +1585,15 @@ static qfs_status set_samples_impl(qfs_ctx *c, int m_pool, const void *x, const 
     CUDA_TRY(c, launch_finite_check((const double *)c->d_yv, (long long)v * c->N * 2, c->d_flag, st));
   }
   int bad = 0;
-  CUDA_TRY(c, cudaMemcpyAsync(&bad, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(c, cudaStreamSynchronize(st));
+  // a queued set consumed by qfs_instantiate (defer_check; single-rank contexts):
+  // no host round trip here — the flag travels with the initial-gate check,
+  // read back after the first sweep (QFS_ERR_NUMERIC "non-finite sample")
+  const bool defer = defer_check && !(c->mode == 1 && c->world > 1 && c->comm);
+  if (!defer) {
+    CUDA_TRY(c, cudaMemcpyAsync(&bad, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(c, cudaStreamSynchronize(st));
+  }
+  c->sample_check_pending = defer;
   c->launches += v > 0 ? 6 : 4;
   c->m_pool = m_pool; c->V = v; c->have_samples = true;
   if (bad) {
@@ -1596,7 +1658,8 @@ qfs_status consume_staged(qfs_ctx *c) {
     if (st != QFS_OK) return st;
   }
   CUDA_TRY(c, cudaStreamWaitEvent(c->st, g.ev, 0));
-  const qfs_status st = set_samples_impl(c, g.m_pool, g.x, g.y, g.v, g.xv, g.yv, cudaMemcpyDeviceToDevice, c->st);
+  const qfs_status st =
+      set_samples_impl(c, g.m_pool, g.x, g.y, g.v, g.xv, g.yv, cudaMemcpyDeviceToDevice, c->st, true);
   c->stg_head = (c->stg_head + 1) % 2;
   c->stg_count -= 1;
   return st;
@@ -1859,12 +1922,25 @@ qfs_status qfs_instantiate(qfs_ctx *c, int s, const double *init_gates, const qf
       if (A[q].c_train < bc) { bc = A[q].c_train; win = q; }
     if (win < 0) win = 0;
   }
-  CUDA_TRY(c, cudaMemcpyAsync(c->h_gates, c->d_gates, (size_t)se * c->gsz * sizeof(double2),
-                              cudaMemcpyDeviceToHost, c->st));
-  CUDA_TRY(c, cudaStreamSynchronize(c->st));
-  for (int q = 0; q < s; ++q)  // (emulated ranks: rank 0's copy; all ranks hold identical bits)
-    std::memcpy(out_gates + (size_t)q * c->gsz * 2, c->h_gates + (size_t)q * c->vr * c->gsz,
-                (size_t)c->gsz * sizeof(double2));
+  if (c->vr == 1 && pinned_device_ptr(out_gates)) {  // pinned caller buffer: one DMA straight into it
+    CUDA_TRY(c, cudaMemcpyAsync(out_gates, c->d_gates, (size_t)s * c->gsz * sizeof(double2), cudaMemcpyDeviceToHost,
+                                c->st));
+    CUDA_TRY(c, cudaStreamSynchronize(c->st));
+  } else {
+    if ((size_t)se * c->gsz * sizeof(double2) > c->h_gates_cap) {  // (only the pinned-input path ran so far)
+      if (c->h_gates) cudaFreeHost(c->h_gates);
+      c->h_gates = nullptr;
+      c->h_gates_cap = 0;
+      CUDA_TRY(c, cudaHostAlloc((void **)&c->h_gates, (size_t)se * c->gsz * sizeof(double2), cudaHostAllocMapped));
+      c->h_gates_cap = (size_t)se * c->gsz * sizeof(double2);
+    }
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_gates, c->d_gates, (size_t)se * c->gsz * sizeof(double2),
+                                cudaMemcpyDeviceToHost, c->st));
+    CUDA_TRY(c, cudaStreamSynchronize(c->st));
+    for (int q = 0; q < s; ++q)  // (emulated ranks: rank 0's copy; all ranks hold identical bits)
+      std::memcpy(out_gates + (size_t)q * c->gsz * 2, c->h_gates + (size_t)q * c->vr * c->gsz,
+                  (size_t)c->gsz * sizeof(double2));
+  }
   for (int q = 0; q < s; ++q) {
     out[q].c_train = A[q].c_train; out[q].c_val = A[q].c_val; out[q].sweeps = A[q].total;
     out[q].restarts = A[q].restarts; out[q].final_m = A[q].M; out[q].term = (qfs_term)A[q].term;

@@ -295,6 +295,33 @@ def test_full_size_resident_sampled_starts(qfs, name):
     _compare_traces(sub, ot, f"{name}-full")
 
 
+@pytest.mark.parametrize("name,init,s,m", [("c3", "R", 8, None), ("c3", "W", 5, 32), ("c2", "R", 3, None)])
+def test_trace_parity_resident_pair_kernel(qfs, monkeypatch, name, init, s, m):
+    """The two-starts-per-cluster resident kernel (QFS_RES_PAIR=2: one start's
+    polar overlapped with the other's passes; measured slower, not the
+    default): traces vs the oracle, odd start counts (a pair with one start),
+    and the validation cost of an instantiation step vs the default kernel."""
+    p = I.make_problem(name, init=init, s=s)
+    m = m or p.m_init
+    monkeypatch.setenv("QFS_RES_PAIR", "2")            # read when the context is created
+    ctx = qfs.Context(p.n, p.pairs)
+    monkeypatch.delenv("QFS_RES_PAIR")
+    ctx.set_samples(p.x, p.y, p.xv, p.yv)
+    gt = ctx.trace_sweeps(p.init, m, 4)
+    ot = oracle.trace_sweeps(p.n, p.pairs, p.init, p.x, p.y, m, 4)
+    _compare_traces(gt, ot, f"{name}-{init}-pair")
+    ref = qfs.Context(p.n, p.pairs)
+    ref.set_samples(p.x, p.y, p.xv, p.yv)
+    prm = dict(p.params, max_iter=3, m_init=m)
+    _, r1, _ = ctx.instantiate(p.init, prm)
+    _, r2, _ = ref.instantiate(p.init, prm)
+    for a, b in zip(r1, r2):
+        assert abs(a["c_val"] - b["c_val"]) <= 1e-10 * max(b["c_val"], 1e-300)
+        assert abs(a["c_train"] - b["c_train"]) <= 1e-10 * max(b["c_train"], 1e-300) + 1e-15
+    ctx.close()
+    ref.close()
+
+
 # ----------------------------------------------------------- instantiation --
 def _inst_both(qfs, p, prm, path="auto"):
     ctx = _ctx(qfs, p.n, p.pairs, path)
