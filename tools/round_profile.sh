@@ -29,6 +29,8 @@ for s in 8; do
   timeout 600 python bench.py --config c5 --starts $s --steps 5 --no-cpu-baseline --no-tts > gpurun_out/bench_c5_s$s.json 2> gpurun_out/bench_c5_s$s.err
   summ gpurun_out/bench_c5_s$s.json c5-s$s || tail -3 gpurun_out/bench_c5_s$s.err
 done
+# resident-kernel pass costs in isolation (tools/res_pass_bench.cu, built beforehand into tools/res_pass_bench.bin)
+[ -x tools/res_pass_bench.bin ] && timeout 120 tools/res_pass_bench.bin > gpurun_out/res_pass_bench.txt 2>&1 && cat gpurun_out/res_pass_bench.txt
 if [ -n "$NO_NCU" ]; then echo done; exit 0; fi
 timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-tts > gpurun_out/bench_short.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches.csv \
