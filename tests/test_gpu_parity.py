@@ -400,6 +400,24 @@ def test_deterministic_bitwise(qfs, path):
     assert np.array_equal(a["gates"], b["gates"]) and np.array_equal(a["cost"], b["cost"])
 
 
+@pytest.mark.parametrize("path", PATHS)
+def test_instantiate_pinned_gate_buffers(qfs, path):
+    """Pinned (page-locked) init / out gate buffers are read and written by the
+    device in place; pageable ones go through the staging buffer: same bits,
+    same results, and the caller's input buffer is left unchanged."""
+    import torch
+    p = I.make_problem("c3", init="R", s=4)
+    prm = dict(p.params, max_iter=3)
+    ctx = _ctx(qfs, p.n, p.pairs, path)
+    ctx.set_samples(p.x, p.y, p.xv, p.yv)
+    g_pageable, r1, w1 = ctx.instantiate(p.init, prm)
+    gin = torch.from_numpy(np.ascontiguousarray(p.init)).pin_memory().numpy()
+    gout = torch.empty(tuple(p.init.shape), dtype=torch.complex128, pin_memory=True).numpy()
+    _, r2, w2 = ctx.instantiate(gin, prm, out=gout)
+    assert np.array_equal(gout, g_pageable) and w1 == w2 and r1 == r2
+    assert np.array_equal(gin, p.init)
+
+
 def test_launch_shape_independence(qfs):
     """A start's sweep does not depend on the batch it runs in beyond summation
     order: 4 starts in one launch (128-thread backward CTAs, 2 per SM, 37 per
