@@ -23,8 +23,8 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
     pass_bench(int n, int cnt, int ld, int which, int reps, unsigned long long *out, double *sink) {
   extern __shared__ __align__(128) unsigned char sm[];
   double2 *phi = (double2 *)sm;
-  double2 *chi = phi + ((size_t)ld << n);
-  double2 *G = chi + ((size_t)ld << n);
+  double2 *chi = phi + (2 * ((size_t)ld << n) * 16 <= 200 * 1024 ? ((size_t)ld << n) : 0);  // (large shapes: one buffer)
+  double2 *G = phi + (chi == phi ? 1 : 2) * ((size_t)ld << n);
   double *red = (double *)(G + 32);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (unsigned q = tid; q < ((unsigned)ld << n); q += RES_THREADS) {
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
 
 int main() {
   using namespace qfs;
-  const int shapes[3][2] = {{9, 8}, {10, 4}, {9, 4}};  // (n, rows per CTA): C3, C5c, C3 at C = 4
+  const int shapes[4][2] = {{9, 8}, {10, 4}, {9, 4}, {12, 2}};  // (n, rows per CTA): C3, C5c, C3 at C = 4, C4 validation
   const char *nm[6] = {"env", "env-loop-only", "reduce-scatter", "apply", "apply-pair", "syncthreads"};
   unsigned long long *d_out;
   double *d_sink;
@@ -103,11 +103,13 @@ int main() {
   cudaFuncSetAttribute(pass_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   for (auto &sh : shapes) {
     const int n = sh[0], cnt = sh[1], ld = cnt;
-    const size_t smem = 2 * ((size_t)ld << n) * 16 + 32 * 16 + RES_THREADS * 8;
+    const bool one = ((size_t)ld << n) * 2 * 16 > 200 * 1024;  // C4 validation shape: one state buffer (env rows skipped)
+    const size_t smem = (one ? 1 : 2) * ((size_t)ld << n) * 16 + 32 * 16 + RES_THREADS * 8;
     const double items = (double)(1 << (n - 2)) * cnt;
     printf("n=%d rows=%d: %.0f items per pass, %.1f per thread; ideal FP64 %.0f cycles (64 DFMA/item)\n", n, cnt, items,
            items / RES_THREADS, items * 64 / 64.0);
     for (int w = 0; w < 6; ++w) {
+      if (one && w < 3) continue;
       pass_bench<<<148, RES_THREADS, smem>>>(n, cnt, ld, w == 5 ? 99 : w, 600, d_out, d_sink);
       if (cudaDeviceSynchronize() != cudaSuccess) {
         printf("error %s\n", cudaGetErrorString(cudaGetLastError()));
