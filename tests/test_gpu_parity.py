@@ -149,6 +149,7 @@ CASES = [
     ("c3", "W", 4, 32, 5, None),
     ("c4", "W", 2, None, 3, 40),
     ("c5b", "W", 1, 16, 3, 30),
+    ("c5b", "W", 1, 32, 2, 30),   # resident: a 16-CTA cluster (the largest), mbarrier exchange over 16 ranks
 ]
 
 
