@@ -111,7 +111,8 @@ struct qfs_ctx {
   bool val_block = true;    // QFS_VAL_BLOCK=0: one-row-per-CTA validation kernel
   int res_per_sm = 1;       // QFS_RES_PER_SM: resident CTAs per SM the cluster plan targets
   int res_cmax = 16;        // QFS_RES_CMAX: largest cluster the plan widens to
-  bool sample_check_pending = false;  // a consumed queued sample set's finite check, read back after the first sweep
+  bool sample_check_pending = false;
+  bool host_read_pending = false;     // a kernel may still read a caller's pinned buffer (upload_gates)  // a consumed queued sample set's finite check, read back after the first sweep
   int res_pair = 0;         // QFS_RES_PAIR: two starts per cluster, staggered (0 off (default: measured slower), 1 auto, 2 wherever it fits)
   int path = 0;             // 0 auto, 1 streamed (B cache in HBM), 2 cluster-resident (qfs_set_path / QFS_PATH)
   size_t stage_bytes = 0;
@@ -174,7 +175,13 @@ qfs_status issue_deferred(qfs_ctx *c);  // queued sample sets' copies (defined w
 namespace {
 
 qfs_status fail(qfs_ctx *c, qfs_status s, const std::string &msg) {
-  if (c) c->err = msg;
+  if (c) {
+    c->err = msg;
+    // an error return must not leave a kernel reading the caller's pinned gate
+    // buffer after the call (the caller may free or overwrite it)
+    if (c->host_read_pending && c->st) cudaStreamSynchronize(c->st);
+    c->host_read_pending = false;
+  }
   return s;
 }
 
@@ -1190,6 +1197,7 @@ qfs_status run_sweep(qfs_ctx *c, const SweepSpec &sp, std::vector<double> &csum,
     if (ws != QFS_OK) return ws;
   }
   if (with_check) c->check_fetched = true;
+  c->host_read_pending = false;  // the sweep's work, and the gate copy before it, has completed
   csum.assign(c->h_csum, c->h_csum + ns);
   if (sp.want_val && c->V > 0) cval.assign(c->h_cval, c->h_cval + ns);
   else cval.assign(ns, NAN);
@@ -1238,14 +1246,15 @@ qfs_status gate_check_result(qfs_ctx *c) {
 
 // Device address of a page-locked, mapped host buffer (cudaHostAlloc /
 // cudaHostRegister memory, e.g. torch pin_memory(); under unified addressing
-// every such buffer is mapped), or nullptr for pageable memory.
-const void *pinned_device_ptr(const void *host) {
+// every such buffer is mapped) pinned for this context's device, or nullptr
+// (pageable memory, or pinned under another device: staged as before).
+const void *pinned_device_ptr(const void *host, int device) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, host) != cudaSuccess) {
     cudaGetLastError();
     return nullptr;
   }
-  return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+  return a.type == cudaMemoryTypeHost && a.device == device ? a.devicePointer : nullptr;
 }
 
 qfs_status upload_gates(qfs_ctx *c, int s, const double *init) {
@@ -1256,7 +1265,8 @@ qfs_status upload_gates(qfs_ctx *c, int s, const double *init) {
   // a pinned caller buffer is read by the copy kernel in place (no host memcpy
   // into the context's staging buffer; the call is synchronous, so the buffer
   // is not reused before the kernel has read it)
-  if (const void *dp = pinned_device_ptr(init)) {
+  if (const void *dp = pinned_device_ptr(init, c->device)) {
+    c->host_read_pending = true;
     CUDA_TRY(c, launch_copy(c->d_gates, (const double2 *)dp, (long long)s * c->gsz, c->st));
   } else {
   if (gb > c->h_gates_cap) {
@@ -1922,7 +1932,7 @@ qfs_status qfs_instantiate(qfs_ctx *c, int s, const double *init_gates, const qf
       if (A[q].c_train < bc) { bc = A[q].c_train; win = q; }
     if (win < 0) win = 0;
   }
-  if (c->vr == 1 && pinned_device_ptr(out_gates)) {  // pinned caller buffer: one DMA straight into it
+  if (c->vr == 1 && pinned_device_ptr(out_gates, c->device)) {  // pinned caller buffer: one DMA straight into it
     CUDA_TRY(c, cudaMemcpyAsync(out_gates, c->d_gates, (size_t)s * c->gsz * sizeof(double2), cudaMemcpyDeviceToHost,
                                 c->st));
     CUDA_TRY(c, cudaStreamSynchronize(c->st));
