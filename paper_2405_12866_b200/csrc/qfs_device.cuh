@@ -262,9 +262,10 @@ __device__ __forceinline__ double half_sum(double v) {
 //   X_0 = E' / s, s = ||E'||_F / 2 (RMS singular value),
 //   X_{k+1} = X_k (3I - X_k^dag X_k) / 2   ->  W, the unitary polar factor of E'.
 // Per singular value u = sigma^2 of X_k, f = u - 1 maps to f' = u(3-u)^2/4 - 1
-// with |f'| <= f^2 for 0 < u < 2, so e_k = ||X_k^dag X_k - I||_F <= e_0^(2^k):
-// when e_0 <= 10^(-16/2^k) (k <= 10), k iterations reach e <= 1e-16 (unitary to
-// rounding).  Returns false (nothing written) when e_0 > 0.9647 for either
+// = -f^2 (3 - f) / 4, |f'| <= f^2 (3 + |f|) / 4 <= f^2 for 0 < u < 2, so
+// e_k = ||X_k^dag X_k - I||_F follows e_{k+1} <= e_k^2 (3 + e_k) / 4: the
+// iteration count (k <= 10) is the smallest that takes this bound from e_0 to
+// <= 1e-16 (unitary to rounding).  Returns false (nothing written) when e_0 > 0.9647 for either
 // half of the warp: the Jacobi path below handles that (ill-conditioned or
 // singular E').  The decision and the count are warp-uniform.
 // The 4x4 products exchange operands through shared memory (scr: 32 double2
@@ -290,9 +291,13 @@ __device__ bool polar_ns(double2 e, int hb, int r, int c, double2 &g_out, double
   double2 y = xhx(x);
   const double dre = y.x - (r == c ? 1.0 : 0.0);
   const double e02 = half_sum(dre * dre + y.y * y.y);  // e_0^2
-  // iterations needed: smallest k with e_0 <= 10^(-16/2^k)
-  constexpr double th2[10] = {1e-16, 1e-8, 1e-4, 1e-2, 0.1, 0.31622776601683794, 0.5623413251903491,
-                              0.7498942093324559, 0.8659643233600653, 0.9305720409296991};
+  // iterations needed: smallest k with g_k <= 1e-16, g_0 = e_0, g_{j+1} =
+  // g_j^2 (3 + g_j) / 4 — the exact per-value map is f' = -f^2 (3 - f) / 4, so
+  // |f'| <= f^2 (3 + |f|) / 4 and e' <= e^2 (3 + e) / 4 (the plain e' <= e^2
+  // bound costs ~0.3 iterations more on average at C3 / C4); thresholds on
+  // e_0^2, computed offline by bisection and rounded down
+  constexpr double th2[10] = {1.33333e-16, 1.53954e-08, 0.000164733, 0.0164122, 0.151213, 0.425849, 0.682251,
+                              0.843214, 0.926897, 0.9305720409296991};
   int k = 11;
 #pragma unroll
   for (int q = 9; q >= 0; --q)
