@@ -289,6 +289,13 @@ __device__ bool polar_ns(double2 e, int hb, int r, int c, double2 &g_out, double
     return y;
   };
   double2 y = xhx(x);
+  // iteration 0's product X_0 (3I - Y_0)/2 does not depend on e_0 (k >= 1
+  // always): issued before e_0's reduction so the shuffles overlap it
+  sT[l] = make_double2(0.5 * ((r == c ? 3.0 : 0.0) - y.x), -0.5 * y.y);
+  __syncwarp();
+  double2 z0 = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) cfma(z0, sx[4 * r + q], sT[4 * q + c]);
   const double dre = y.x - (r == c ? 1.0 : 0.0);
   const double e02 = half_sum(dre * dre + y.y * y.y);  // e_0^2
   // iterations needed: smallest k with g_k <= 1e-16, g_0 = e_0, g_{j+1} =
@@ -304,8 +311,9 @@ __device__ bool polar_ns(double2 e, int hb, int r, int c, double2 &g_out, double
     if (e02 <= th2[q]) k = q + 1;
   k = max(k, __shfl_xor_sync(FULL, k, 16));
   if (!__all_sync(FULL, k <= 10)) return false;
-  for (int it = 0; it < k; ++it) {
-    if (it > 0) y = xhx(x);
+  x = z0;
+  for (int it = 1; it < k; ++it) {
+    y = xhx(x);
     const double2 t = make_double2(0.5 * ((r == c ? 3.0 : 0.0) - y.x), -0.5 * y.y);  // (3I - Y)/2
     sT[l] = t;
     __syncwarp();
