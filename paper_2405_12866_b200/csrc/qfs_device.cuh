@@ -273,10 +273,6 @@ __device__ __forceinline__ double half_sum(double v) {
 // broadcast-friendly loads per product instead of eight 128-bit shuffles.
 __device__ bool polar_ns(double2 e, int hb, int r, int c, double2 &g_out, double &ss_out, double2 *scr,
                          bool need_ss = true) {
-  const double fro2 = half_sum(e.x * e.x + e.y * e.y);
-  if (!__all_sync(FULL, fro2 > 0.0)) return false;
-  const double rs = 2.0 * rsqrt(fro2);
-  double2 x = make_double2(e.x * rs, e.y * rs);
   const int l = 4 * r + c;
   double2 *sx = scr, *sT = scr + 16;
   auto xhx = [&](double2 X) {  // (X^dag X)[r][c] = sum_q conj(X[q][r]) X[q][c]; leaves X in sx
@@ -288,14 +284,22 @@ __device__ bool polar_ns(double2 e, int hb, int r, int c, double2 &g_out, double
     for (int q = 0; q < 4; ++q) cfma(y, cconj(sx[4 * q + r]), sx[4 * q + c]);
     return y;
   };
-  double2 y = xhx(x);
-  // iteration 0's product X_0 (3I - Y_0)/2 does not depend on e_0 (k >= 1
-  // always): issued before e_0's reduction so the shuffles overlap it
+  // E^dag E on the unscaled E' while the Frobenius norm is reduced (the two
+  // overlap): X_0 = rs E', Y_0 = rs^2 E'^dag E', rs = 2 / ||E'||_F
+  const double2 yp = xhx(e);
+  const double fro2 = half_sum(e.x * e.x + e.y * e.y);
+  if (!__all_sync(FULL, fro2 > 0.0)) return false;
+  const double rs = 2.0 * rsqrt(fro2), rs2 = rs * rs;
+  double2 y = make_double2(yp.x * rs2, yp.y * rs2);
+  // iteration 0's product X_0 (3I - Y_0)/2 = rs E' (3I - Y_0)/2 does not depend
+  // on e_0 (k >= 1 always): issued before e_0's reduction so the shuffles overlap it
   sT[l] = make_double2(0.5 * ((r == c ? 3.0 : 0.0) - y.x), -0.5 * y.y);
   __syncwarp();
   double2 z0 = make_double2(0.0, 0.0);
 #pragma unroll
   for (int q = 0; q < 4; ++q) cfma(z0, sx[4 * r + q], sT[4 * q + c]);
+  z0 = make_double2(z0.x * rs, z0.y * rs);
+  double2 x;
   const double dre = y.x - (r == c ? 1.0 : 0.0);
   const double e02 = half_sum(dre * dre + y.y * y.y);  // e_0^2
   // iterations needed: smallest k with g_k <= 1e-16, g_0 = e_0, g_{j+1} =
