@@ -105,7 +105,26 @@ __device__ void polar_write(const double *e32, double2 *gout, double2 *vslot, do
 // Last-CTA election for the per-start reduction of CTA partials, by warp 0
 // only (the warp that wrote this CTA's partial): release fence, ticket, and an
 // acquire fence in the last CTA.  The other warps never fence or wait.
+#ifndef QFS_ELECT_ACQREL
+#define QFS_ELECT_ACQREL 1  // ticket as one acq_rel atomic (after a warp barrier) instead of fence + atomic + fence
+#endif
 __device__ bool warp0_elect_last(unsigned *counter, unsigned nb) {
+#if QFS_ELECT_ACQREL
+  // the warp's partial stores are ordered before lane 0's release by the warp
+  // barrier (release is cumulative); the last CTA's acquire orders the reads of
+  // every CTA's partial after it, for all lanes through the second warp barrier
+  __syncwarp();
+  unsigned last = 0;
+  if ((threadIdx.x & 31) == 0) {
+    unsigned t;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(counter) : "memory");
+    last = (t == nb - 1) ? 1u : 0u;
+    if (last) *counter = 0u;
+  }
+  last = __shfl_sync(FULL, last, 0);
+  __syncwarp();
+  return last != 0;
+#else
   __threadfence();
   unsigned last = 0;
   if ((threadIdx.x & 31) == 0) {
@@ -116,6 +135,7 @@ __device__ bool warp0_elect_last(unsigned *counter, unsigned nb) {
   last = __shfl_sync(FULL, last, 0);
   if (last) __threadfence();
   return last != 0;
+#endif
 }
 
 // P-index (0..3) of local amplitude index v for the pair at local bits (TP0, TP1)
