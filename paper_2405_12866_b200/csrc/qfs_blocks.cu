@@ -25,6 +25,14 @@
 namespace qfs {
 namespace {
 
+// per-start ticket with acquire-release semantics at GPU scope (the last-CTA
+// election without separate fences, as warp0_elect_last in qfs_kernels.cu)
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned *counter) {
+  unsigned t;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(counter) : "memory");
+  return t;
+}
+
 constexpr int BLK_THREADS = 128;
 
 __device__ __forceinline__ double warp_sum_d(double v) {
@@ -404,16 +412,17 @@ __global__ void __launch_bounds__(BLK_THREADS) blk_env_kernel(const BlkEnvParams
     for (int w = 0; w < NW; ++w) { t.x += red[w][e].x; t.y += red[w][e].y; }
     cta_part[e] = t;
   }
-  __threadfence();
+  // the CTA barrier orders every thread's partial store before thread 0's
+  // release (cumulative); the last CTA's acquire orders the partial loads of
+  // all its threads through the next barrier
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned t = atomicAdd(P.counters + j, 1u);
+    const unsigned t = atom_add_acq_rel(P.counters + j);
     last_cta = t == gridDim.x - 1 ? 1u : 0u;
     if (last_cta) P.counters[j] = 0u;
   }
   __syncthreads();
   if (!last_cta) return;
-  __threadfence();
   const double2 *pp = reinterpret_cast<const double2 *>(P.partials) + (long long)j * gridDim.x * DD;
   for (int e = threadIdx.x; e < DD; e += blockDim.x) {
     double2 t = make_double2(0.0, 0.0);
@@ -500,12 +509,10 @@ __global__ void __launch_bounds__(BLK_THREADS) blk_dist_kernel(const BlkDistPara
 #pragma unroll
     for (int w = 0; w < NW; ++w) t += red[w];
     P.partials[(long long)j * gridDim.x + blockIdx.x] = t;
-    __threadfence();
-    const unsigned tk = atomicAdd(P.counters + j, 1u);
+    const unsigned tk = atom_add_acq_rel(P.counters + j);
     last_cta = tk == gridDim.x - 1 ? 1u : 0u;
     if (last_cta) {
       P.counters[j] = 0u;
-      __threadfence();
       double tot = 0.0;
       for (unsigned c = 0; c < gridDim.x; ++c) tot += __ldcg(P.partials + (long long)j * gridDim.x + c);
       P.out[j] = tot;
