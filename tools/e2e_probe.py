@@ -1,5 +1,5 @@
 import sys, time, os
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_2405_12866_b200 import inputs as I, qfs
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c4"
