@@ -730,3 +730,42 @@ def test_large_n_streamed_with_validation(qfs, n, k, m, v):
     g2, r2, _ = oracle.instantiate(n, pairs, x, y, xv, yv, init, prm)
     assert abs(r1[0]["c_val"] - r2[0]["c_val"]) <= COST_TOL * r2[0]["c_val"] + 1e-15
     assert abs(r1[0]["c_train"] - r2[0]["c_train"]) <= COST_TOL * r2[0]["c_train"] + 1e-15
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_empty_and_degenerate_calls_leave_context_usable(qfs, path):
+    """Empty inputs (no sample rows, no starts, no sweeps, m = 0, max_iter = 0)
+    are refused with QFS_ERR_ARG / QFS_ERR_CAPACITY before any device work,
+    a zero-sweep trace only reports gate validity, and
+    the sample set uploaded before them is still the one the next call uses:
+    its traces equal the oracle's (P:112 sweep; include/qfs.h error codes)."""
+    from paper_2405_12866_b200.qfs import QfsError
+    p = I.make_problem("c1")
+    ctx = _ctx(qfs, p.n, p.pairs, path)
+    ctx.set_samples(p.x, p.y)
+    empty = np.zeros((0, 1 << p.n), np.complex128)
+    with pytest.raises(QfsError) as ei:
+        ctx.set_samples(empty, empty)              # m_pool = 0
+    assert ei.value.status == 1
+    with pytest.raises(QfsError) as ei:
+        ctx.trace_sweeps(p.init[:0], p.m_init, 2)  # S = 0 starts
+    assert ei.value.status == 1
+    with pytest.raises(QfsError) as ei:
+        ctx.trace_sweeps(p.init, 0, 2)             # m = 0 rows
+    assert ei.value.status == 2
+    with pytest.raises(QfsError) as ei:
+        ctx.trace_sweeps(p.init, p.x.shape[0] + 1, 2)  # m beyond the pool
+    assert ei.value.status == 2
+    with pytest.raises(QfsError) as ei:
+        ctx.instantiate(p.init, dict(p.params, max_iter=0))
+    assert ei.value.status == 1
+    with pytest.raises(QfsError) as ei:
+        ctx.instantiate(p.init, dict(p.params, m_init=0))
+    assert ei.value.status == 2
+    z = ctx.trace_sweeps(p.init, p.m_init, 0)      # zero sweeps: nothing written
+    assert z["cost"].shape == (0, p.init.shape[0])
+    m = p.m_init
+    gt = ctx.trace_sweeps(p.init, m, 3)
+    ot = oracle.trace_sweeps(p.n, p.pairs, p.init, p.x, p.y, m, 3)
+    _compare_traces(gt, ot, f"after refused calls ({path})")
+    ctx.close()
