@@ -352,7 +352,10 @@ __global__ void __launch_bounds__(BLK_THREADS) blk_env_kernel(const BlkEnvParams
   const BlkLocal L = blk_local<A>(bg);
   // PARTS lanes share an item, each owning XR rows of E (64 complex
   // accumulators would take 256 registers for d = 8)
-  constexpr int PARTS = A == 3 ? 4 : 1, XR = D / PARTS;
+#ifndef QFS_BLK_ENV_PARTS
+#define QFS_BLK_ENV_PARTS 4
+#endif
+  constexpr int PARTS = A == 3 ? QFS_BLK_ENV_PARTS : 1, XR = D / PARTS;
   const int part = threadIdx.x % PARTS;
   double2 acc[XR * D];
 #pragma unroll
@@ -547,7 +550,7 @@ __global__ void blk_gate_check_kernel(const double2 *g, const BlkGate *bg, int K
 }
 
 int blk_grid(long long items, int n_slots) {
-  long long nb = std::max(1, 148 * 4 / std::max(1, n_slots));
+  long long nb = std::max(1, kBlkMaxCtas / std::max(1, n_slots));
   nb = std::min(nb, (items + BLK_THREADS - 1) / BLK_THREADS);
   return (int)std::max(1LL, std::min<long long>(nb, kBlkMaxCtas));
 }

@@ -263,7 +263,10 @@ int bwdt_units_per_cta_min();     // fewest stages a bulk-copy backward CTA is g
 struct BlkGate {
   int a, q[3], off, kind;
 };
-constexpr int kBlkMaxCtas = 148 * 4;  // CTAs per start of any block launch
+#ifndef QFS_BLK_CTAS_PER_SM
+#define QFS_BLK_CTAS_PER_SM 4
+#endif
+constexpr int kBlkMaxCtas = 148 * QFS_BLK_CTAS_PER_SM;  // CTAs per start of any block launch
 struct BlkApplyParams {
   int n, k, dagger, rows_fixed;  // rows_fixed > 0: that many rows per start (validation)
   const Slot *slots;
