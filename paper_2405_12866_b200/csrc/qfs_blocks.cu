@@ -355,6 +355,9 @@ __global__ void __launch_bounds__(BLK_THREADS) blk_env_kernel(const BlkEnvParams
 #ifndef QFS_BLK_ENV_PARTS
 #define QFS_BLK_ENV_PARTS 4
 #endif
+#ifndef QFS_BLK_ENV_PF
+#define QFS_BLK_ENV_PF 1  // items loaded ahead of the one accumulating
+#endif
   constexpr int PARTS = A == 3 ? QFS_BLK_ENV_PARTS : 1, XR = D / PARTS;
   const int part = threadIdx.x % PARTS;
   double2 acc[XR * D];
@@ -378,13 +381,25 @@ __global__ void __launch_bounds__(BLK_THREADS) blk_env_kernel(const BlkEnvParams
   const unsigned step = blockDim.x / PARTS;
   double2 fn[XR], cn[D];  // next item's amplitudes, loaded while this one accumulates
   if (beg + threadIdx.x / PARTS < end) load(beg + threadIdx.x / PARTS, fn, cn);
+#if QFS_BLK_ENV_PF == 2
+  double2 fn2[XR], cn2[D];  // the item after it
+  if (beg + threadIdx.x / PARTS + step < end) load(beg + threadIdx.x / PARTS + step, fn2, cn2);
+#endif
   for (unsigned w = beg + threadIdx.x / PARTS; w < end; w += step) {
     double2 f[XR], c[D];
 #pragma unroll
     for (int x = 0; x < XR; ++x) f[x] = fn[x];
 #pragma unroll
     for (int l = 0; l < D; ++l) c[l] = cn[l];
+#if QFS_BLK_ENV_PF == 2
+#pragma unroll
+    for (int x = 0; x < XR; ++x) fn[x] = fn2[x];
+#pragma unroll
+    for (int l = 0; l < D; ++l) cn[l] = cn2[l];
+    if (w + 2 * step < end) load(w + 2 * step, fn2, cn2);
+#else
     if (w + step < end) load(w + step, fn, cn);
+#endif
 #pragma unroll
     for (int x = 0; x < XR; ++x)
 #pragma unroll
